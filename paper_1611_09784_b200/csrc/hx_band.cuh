@@ -1,0 +1,27 @@
+// Large-N two-stage path (dense -> band -> tridiagonal) for batched Hermitian eigenvalues.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <functional>
+
+#include "hx_common.cuh"
+
+namespace hx {
+
+using Alloc = std::function<void*(size_t)>;
+
+void band_init_attributes();
+bool band_path_supported(int N);
+const char* band_last_error();
+
+// IDOS batch through the banded path (pencil STANDARD or COMMUTING).
+int band_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, int64_t nmasks, const GridDev& g,
+              int* diff, unsigned long long* trans, double* eigs, int* status, int sharp, size_t ws_budget,
+              const Alloc& alloc, cudaStream_t st);
+
+// Eigenvalues of caller-provided Hermitian matrices (column-major complex, n x n each).
+int band_eigvalsh(int n, int64_t batch, const double2* A, double* eigs, int* status, size_t ws_budget,
+                  const Alloc& alloc, cudaStream_t st);
+
+}  // namespace hx

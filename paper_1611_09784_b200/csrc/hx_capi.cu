@@ -1,0 +1,700 @@
+// C-ABI layer of libhx.so (see include/hx.h for the contract and the reference seams replaced).
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/hx.h"
+#include "hx_band.cuh"
+#include "hx_dense.cuh"
+#include "hx_kernels.cuh"
+#include "hx_rng.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define HX_CUDA(call)                                                                              \
+  do {                                                                                             \
+    cudaError_t e_ = (call);                                                                       \
+    if (e_ != cudaSuccess) return fail(HX_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int grow(size_t bytes) {
+    if (bytes <= cap) return 0;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max(bytes, (size_t)4096);
+    if (cudaMalloc(&p, want) != cudaSuccess) return -1;
+    cap = want;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct hx_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  DevBuf kpts, diff, trans, ws, masks, curves, eigs, status, band;
+  size_t ws_budget = (size_t)24 << 30;  // HBM workspace budget for the global / banded paths
+};
+
+struct hx_cell {
+  hx_ctx* ctx = nullptr;
+  hx::CellDev dev{};
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+int set_device(hx_ctx* ctx) {
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return fail(HX_E_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+template <class T>
+int upload(hx_cell* cell, const T* host, size_t n, const T** out) {
+  *out = nullptr;
+  if (host == nullptr || n == 0) return 0;
+  void* p = nullptr;
+  HX_CUDA(cudaMalloc(&p, n * sizeof(T)));
+  cell->allocs.push_back(p);
+  HX_CUDA(cudaMemcpy(p, host, n * sizeof(T), cudaMemcpyHostToDevice));
+  *out = static_cast<const T*>(p);
+  return 0;
+}
+
+// Transposed instance lists: for each target dof, the instance ids pointing at it (ascending).
+void transpose_csr(int N, const int32_t* ptr, const int32_t* col, std::vector<int32_t>& tptr,
+                   std::vector<int32_t>& tinst, std::vector<int32_t>& src) {
+  const int nnz = ptr[N];
+  tptr.assign(N + 1, 0);
+  src.resize(nnz);
+  for (int r = 0; r < N; ++r)
+    for (int e = ptr[r]; e < ptr[r + 1]; ++e) {
+      src[e] = r;
+      tptr[col[e] + 1]++;
+    }
+  for (int r = 0; r < N; ++r) tptr[r + 1] += tptr[r];
+  tinst.assign(nnz, 0);
+  std::vector<int32_t> fill(tptr.begin(), tptr.end() - 1);
+  for (int e = 0; e < nnz; ++e) tinst[fill[col[e]]++] = e;
+}
+
+int fixed_point_shift(int64_t nk, int N) {
+  const double terms = (double)nk * (double)(N + 1) + 1.0;
+  int need = (int)std::ceil(std::log2(terms));
+  return std::min(52, 62 - need);
+}
+
+}  // namespace
+
+extern "C" {
+
+int hx_abi_version(void) { return HX_ABI_VERSION; }
+
+const char* hx_last_error(void) { return g_err.c_str(); }
+
+int hx_device_count(int32_t* out) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *out = 0;
+    return fail(HX_E_NODEV, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+  }
+  *out = n;
+  return 0;
+}
+
+int hx_ctx_create(int32_t device, hx_ctx** out) {
+  if (!out) return fail(HX_E_ARG, "hx_ctx_create: null out");
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return fail(HX_E_NODEV, "no CUDA device visible");
+  if (device < 0 || device >= n) return fail(HX_E_ARG, "device index out of range");
+  hx_ctx* ctx = new hx_ctx();
+  ctx->device = device;
+  if (set_device(ctx)) {
+    delete ctx;
+    return HX_E_CUDA;
+  }
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major < 10) {
+    delete ctx;
+    return fail(HX_E_NODEV, "libhx is built for sm_100a (B200); found sm_" + std::to_string(prop.major) +
+                                std::to_string(prop.minor));
+  }
+  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete ctx;
+    return fail(HX_E_CUDA, "cudaStreamCreate failed");
+  }
+  size_t freeb = 0, total = 0;
+  cudaMemGetInfo(&freeb, &total);
+  ctx->ws_budget = std::min(ctx->ws_budget, freeb / 3);
+  cudaFuncSetAttribute(hx::fused_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)hx::fused_smem_bytes(HX_SMEM_MAX_N));
+  hx::band_init_attributes();
+  *out = ctx;
+  return 0;
+}
+
+int hx_ctx_destroy(hx_ctx* ctx) {
+  if (!ctx) return 0;
+  set_device(ctx);
+  for (DevBuf* b : {&ctx->kpts, &ctx->diff, &ctx->trans, &ctx->ws, &ctx->masks, &ctx->curves, &ctx->eigs,
+                    &ctx->status, &ctx->band})
+    b->release();
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return 0;
+}
+
+int hx_ctx_synchronize(hx_ctx* ctx) {
+  if (!ctx) return fail(HX_E_ARG, "null ctx");
+  if (set_device(ctx)) return HX_E_CUDA;
+  HX_CUDA(cudaStreamSynchronize(ctx->stream));
+  return 0;
+}
+
+int hx_cell_create(hx_ctx* ctx, const hx_cell_desc* d, hx_cell** out) {
+  if (!ctx || !d || !out) return fail(HX_E_ARG, "hx_cell_create: null argument");
+  if (d->ndof < 1 || d->ndof > HX_MAX_N) return fail(HX_E_RANGE, "ndof outside [1, HX_MAX_N]");
+  if (d->nunits < 0 || !d->unit_of_dof || !d->onsite || !d->h_row_ptr) return fail(HX_E_ARG, "incomplete cell");
+  if (d->pencil < 0 || d->pencil > 2) return fail(HX_E_ARG, "unknown pencil kind");
+  if (d->pencil == HX_PENCIL_GENERAL && !d->s_row_ptr) return fail(HX_E_ARG, "general pencil needs overlap CSR");
+  if (set_device(ctx)) return HX_E_CUDA;
+  hx_cell* cell = new hx_cell();
+  cell->ctx = ctx;
+  hx::CellDev& c = cell->dev;
+  const int N = d->ndof;
+  c.N = N;
+  c.nunits = d->nunits;
+  c.words = (d->nunits + 63) / 64;
+  if (c.words == 0) c.words = 1;
+  c.pencil = d->pencil;
+  c.eps0 = d->eps0;
+  c.t = d->t;
+  c.s = d->s;
+  c.area = d->area;
+  int rc = 0;
+  rc |= upload(cell, d->unit_of_dof, N, &c.unit_of_dof);
+  rc |= upload(cell, d->onsite, N, &c.onsite);
+  {
+    const int nnz = d->h_row_ptr[N];
+    std::vector<int32_t> tptr, tinst, src;
+    transpose_csr(N, d->h_row_ptr, d->h_col, tptr, tinst, src);
+    rc |= upload(cell, d->h_row_ptr, N + 1, &c.h_ptr);
+    rc |= upload(cell, d->h_col, nnz, &c.h_col);
+    rc |= upload(cell, reinterpret_cast<const double2*>(d->h_amp), nnz, &c.h_amp);
+    rc |= upload(cell, reinterpret_cast<const double2*>(d->h_disp), nnz, &c.h_disp);
+    rc |= upload(cell, tptr.data(), N + 1, &c.ht_ptr);
+    rc |= upload(cell, tinst.data(), nnz, &c.ht_inst);
+    rc |= upload(cell, src.data(), nnz, &c.h_src);
+    if (nnz == 0) {
+      // keep non-null pointers for the empty instance list
+      static const int32_t zero = 0;
+      (void)zero;
+    }
+  }
+  if (d->pencil == HX_PENCIL_GENERAL) {
+    const int nnz = d->s_row_ptr[N];
+    std::vector<int32_t> tptr, tinst, src;
+    transpose_csr(N, d->s_row_ptr, d->s_col, tptr, tinst, src);
+    rc |= upload(cell, d->s_row_ptr, N + 1, &c.s_ptr);
+    rc |= upload(cell, d->s_col, nnz, &c.s_col);
+    rc |= upload(cell, reinterpret_cast<const double2*>(d->s_amp), nnz, &c.s_amp);
+    rc |= upload(cell, reinterpret_cast<const double2*>(d->s_disp), nnz, &c.s_disp);
+    rc |= upload(cell, tptr.data(), N + 1, &c.st_ptr);
+    rc |= upload(cell, tinst.data(), nnz, &c.st_inst);
+    rc |= upload(cell, src.data(), nnz, &c.s_src);
+  }
+  if (rc) {
+    hx_cell_destroy(cell);
+    return HX_E_CUDA;
+  }
+  *out = cell;
+  return 0;
+}
+
+int hx_cell_destroy(hx_cell* cell) {
+  if (!cell) return 0;
+  if (cell->ctx) set_device(cell->ctx);
+  for (void* p : cell->allocs) cudaFree(p);
+  delete cell;
+  return 0;
+}
+
+static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t nk, const uint64_t* d_masks,
+                     int64_t nmasks, const hx_egrid* grid, double* d_curves, double* d_eigs, int32_t* d_status,
+                     cudaStream_t st, int sharp) {
+  if (!ctx || !cell || !kpoints || !grid || (nmasks > 0 && (!d_masks || !d_curves || !d_status)))
+    return fail(HX_E_ARG, "hx_eval_idos_batch: null argument");
+  if (nk < 1 || nmasks < 0) return fail(HX_E_ARG, "hx_eval_idos_batch: nk >= 1 and nmasks >= 0 required");
+  if (grid->npts < 1 || !(grid->step > 0.0) || !(grid->delta > 0.0))
+    return fail(HX_E_ARG, "energy grid needs npts >= 1, step > 0, delta > 0");
+  if (nmasks == 0) return 0;
+  if (set_device(ctx)) return HX_E_CUDA;
+  const hx::CellDev& c = cell->dev;
+  const int N = c.N;
+  hx::GridDev g;
+  g.e0 = grid->e0;
+  g.step = grid->step;
+  g.delta = grid->delta;
+  g.npts = grid->npts;
+  g.shift = fixed_point_shift(nk, N);
+  if (g.shift < 16) return fail(HX_E_RANGE, "nk * N too large for the fixed-point IDOS accumulator");
+  // k-points (small, pageable copy on the work stream)
+  if (ctx->kpts.grow((size_t)nk * 16)) return fail(HX_E_CUDA, "alloc kpts");
+  HX_CUDA(cudaMemcpyAsync(ctx->kpts.p, kpoints, (size_t)nk * 16, cudaMemcpyHostToDevice, st));
+  const size_t diff_b = (size_t)nmasks * (grid->npts + 1) * sizeof(int);
+  const size_t trans_b = (size_t)nmasks * grid->npts * sizeof(unsigned long long);
+  if (ctx->diff.grow(diff_b) || ctx->trans.grow(trans_b)) return fail(HX_E_CUDA, "alloc accumulators");
+  HX_CUDA(cudaMemsetAsync(ctx->diff.p, 0, diff_b, st));
+  HX_CUDA(cudaMemsetAsync(ctx->trans.p, 0, trans_b, st));
+  int* diff = static_cast<int*>(ctx->diff.p);
+  auto* trans = static_cast<unsigned long long*>(ctx->trans.p);
+  const double2* kp = static_cast<const double2*>(ctx->kpts.p);
+  const int64_t nmat = nmasks * (int64_t)nk;
+
+  if (c.pencil != HX_PENCIL_GENERAL && N <= HX_SMEM_MAX_N) {
+    const size_t smem = hx::fused_smem_bytes(N);
+    const int64_t chunk = 1 << 30;
+    for (int64_t m0 = 0; m0 < nmat; m0 += chunk) {
+      (void)m0;
+    }
+    if (nmat > (int64_t)0x7fffffff) return fail(HX_E_RANGE, "too many matrices in one batch");
+    hx::fused_smem_kernel<<<(unsigned)nmat, 256, smem, st>>>(c, kp, nk, d_masks, g, diff, trans, d_eigs,
+                                                            reinterpret_cast<int*>(d_status), sharp);
+    HX_CUDA(cudaGetLastError());
+  } else if (c.pencil != HX_PENCIL_GENERAL && hx::band_path_supported(N)) {
+    int rc = hx::band_eval(c, kp, nk, d_masks, nmasks, g, diff, trans, d_eigs,
+                           reinterpret_cast<int*>(d_status), sharp, ctx->ws_budget,
+                           [&](size_t bytes) -> void* { return ctx->band.grow(bytes) ? nullptr : ctx->band.p; }, st);
+    if (rc) return fail(HX_E_CUDA, std::string("band path: ") + hx::band_last_error());
+  } else {
+    const size_t stride = hx::global_ws_stride(N, c.pencil == HX_PENCIL_GENERAL);
+    int64_t chunk = (int64_t)std::max<size_t>(1, ctx->ws_budget / stride);
+    chunk = std::min<int64_t>(chunk, nmat);
+    chunk = std::min<int64_t>(chunk, 65535);
+    if (ctx->ws.grow(stride * (size_t)chunk)) return fail(HX_E_CUDA, "alloc workspace");
+    for (int64_t m0 = 0; m0 < nmat; m0 += chunk) {
+      const int64_t cnt = std::min(chunk, nmat - m0);
+      hx::global_solve_kernel<<<(unsigned)cnt, 512, 0, st>>>(c, kp, nk, d_masks, g, diff, trans, d_eigs,
+                                                             reinterpret_cast<int*>(d_status), m0,
+                                                             static_cast<unsigned char*>(ctx->ws.p), stride, sharp);
+      HX_CUDA(cudaGetLastError());
+    }
+  }
+  const int wpb = 8;
+  hx::finalize_kernel<<<(unsigned)((nmasks + wpb - 1) / wpb), 32 * wpb, 0, st>>>(diff, trans, nmasks, g, 1.0 / nk,
+                                                                                 1.0 / c.area, d_curves);
+  HX_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int hx_eval_idos_batch_device(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t nk, const uint64_t* d_masks,
+                              int64_t nmasks, const hx_egrid* grid, double* d_curves, double* d_eigs,
+                              int32_t* d_status, void* stream) {
+  return eval_impl(ctx, cell, kpoints, nk, d_masks, nmasks, grid, d_curves, d_eigs, d_status,
+                   static_cast<cudaStream_t>(stream), 0);
+}
+
+static int eval_host(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t nk, const uint64_t* masks,
+                     int64_t nmasks, const hx_egrid* grid, double* out_curves, double* out_eigs, int32_t* out_status,
+                     int sharp) {
+  if (!ctx || !cell || !grid) return fail(HX_E_ARG, "hx_eval_idos_batch: null argument");
+  if (nmasks == 0) return 0;
+  if (!masks || !out_curves || !out_status) return fail(HX_E_ARG, "hx_eval_idos_batch: null buffer");
+  if (set_device(ctx)) return HX_E_CUDA;
+  const hx::CellDev& c = cell->dev;
+  const size_t mb = (size_t)nmasks * c.words * 8, cb = (size_t)nmasks * grid->npts * 8,
+               sb = (size_t)nmasks * nk * 4, eb = (size_t)nmasks * nk * c.N * 8;
+  if (ctx->masks.grow(mb) || ctx->curves.grow(cb) || ctx->status.grow(sb) || (out_eigs && ctx->eigs.grow(eb)))
+    return fail(HX_E_CUDA, "alloc batch buffers");
+  cudaStream_t st = ctx->stream;
+  HX_CUDA(cudaMemcpyAsync(ctx->masks.p, masks, mb, cudaMemcpyHostToDevice, st));
+  int rc = eval_impl(ctx, cell, kpoints, nk, static_cast<uint64_t*>(ctx->masks.p), nmasks, grid,
+                     static_cast<double*>(ctx->curves.p), out_eigs ? static_cast<double*>(ctx->eigs.p) : nullptr,
+                     static_cast<int32_t*>(ctx->status.p), st, sharp);
+  if (rc) return rc;
+  HX_CUDA(cudaMemcpyAsync(out_curves, ctx->curves.p, cb, cudaMemcpyDeviceToHost, st));
+  HX_CUDA(cudaMemcpyAsync(out_status, ctx->status.p, sb, cudaMemcpyDeviceToHost, st));
+  if (out_eigs) HX_CUDA(cudaMemcpyAsync(out_eigs, ctx->eigs.p, eb, cudaMemcpyDeviceToHost, st));
+  HX_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int hx_assemble_device(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t nk, const uint64_t* d_masks,
+                       int64_t nmasks, double* d_H, double* d_S, int32_t* d_dims, void* stream) {
+  if (!ctx || !cell || !kpoints || !d_masks || !d_H || !d_dims || nk < 1 || nmasks < 0)
+    return fail(HX_E_ARG, "hx_assemble_device: bad args");
+  if (nmasks == 0) return 0;
+  if (set_device(ctx)) return HX_E_CUDA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (ctx->kpts.grow((size_t)nk * 16)) return fail(HX_E_CUDA, "alloc kpts");
+  HX_CUDA(cudaMemcpyAsync(ctx->kpts.p, kpoints, (size_t)nk * 16, cudaMemcpyHostToDevice, st));
+  const size_t smem = (size_t)cell->dev.N * sizeof(int);
+  if (smem > 200 * 1024) return fail(HX_E_RANGE, "hx_assemble_device: N too large");
+  cudaFuncSetAttribute(hx::assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  hx::assemble_kernel<<<(unsigned)(nmasks * nk), 256, smem, st>>>(
+      cell->dev, static_cast<const double2*>(ctx->kpts.p), nk, d_masks, reinterpret_cast<double2*>(d_H),
+      reinterpret_cast<double2*>(d_S), reinterpret_cast<int*>(d_dims));
+  HX_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int hx_eval_idos_batch(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t nk, const uint64_t* masks,
+                       int64_t nmasks, const hx_egrid* grid, double* out_curves, double* out_eigs,
+                       int32_t* out_status) {
+  return eval_host(ctx, cell, kpoints, nk, masks, nmasks, grid, out_curves, out_eigs, out_status, 0);
+}
+
+// Sharp-count variant of the batch (idos_sharp, qoi.py:105-108); not part of the public header's
+// hot path but exported for parity tests.
+int hx_eval_sharp_batch(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t nk, const uint64_t* masks,
+                        int64_t nmasks, const hx_egrid* grid, double* out_curves, double* out_eigs,
+                        int32_t* out_status) {
+  return eval_host(ctx, cell, kpoints, nk, masks, nmasks, grid, out_curves, out_eigs, out_status, 1);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------------------------------
+// Standalone batched eigenvalues of caller-provided matrices (config-5 sweep).
+namespace hx {
+
+__global__ void __launch_bounds__(256) eigvalsh_smem_kernel(int n, const double2* __restrict__ A, double* eigs,
+                                                            int* status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ld = n | 1;
+  double* R = reinterpret_cast<double*>(smem_raw);
+  double2* v = reinterpret_cast<double2*>(R + (size_t)n * ld);
+  double2* y = v + n;
+  double* diag = reinterpret_cast<double*>(y + n);
+  double* e2 = diag + n;
+  double* lam = e2 + n;
+  double* red = lam + n;
+  const double2* a = A + (size_t)blockIdx.x * n * n;
+  for (int p = threadIdx.x; p < n * n; p += blockDim.x) {
+    const int col = p / n, row = p - col * n;
+    const double2 z = a[p];
+    if (row > col) {
+      R[row * ld + col] = z.x;
+      R[col * ld + row] = z.y;
+    } else if (row == col) {
+      R[row * ld + row] = z.x;
+    }
+  }
+  if (threadIdx.x == 0) status[blockIdx.x] = 0;
+  __syncthreads();
+  tridiag_packed(R, ld, n, diag, e2, v, y, red);
+  bisect_all(diag, e2, n, lam, red);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) eigs[(size_t)blockIdx.x * n + i] = lam[i];
+}
+
+__global__ void __launch_bounds__(512) eigvalsh_global_kernel(int n, const double2* __restrict__ A,
+                                                              const double2* __restrict__ B, double* eigs,
+                                                              int* status, int64_t mat0, unsigned char* ws,
+                                                              size_t stride) {
+  __shared__ double red[96];
+  const int64_t mat = mat0 + blockIdx.x;
+  unsigned char* w = ws + (size_t)blockIdx.x * stride;
+  double2* Aw = reinterpret_cast<double2*>(w);
+  double2* Bw = Aw + (size_t)n * n;
+  double2* v = B ? Bw + (size_t)n * n : Bw;
+  double2* y = v + n;
+  double* diag = reinterpret_cast<double*>(y + n);
+  double* e2 = diag + n;
+  double* lam = e2 + n;
+  const double2* a = A + (size_t)mat * n * n;
+  for (int64_t p = threadIdx.x; p < (int64_t)n * n; p += blockDim.x) Aw[p] = a[p];
+  if (B) {
+    const double2* b = B + (size_t)mat * n * n;
+    for (int64_t p = threadIdx.x; p < (int64_t)n * n; p += blockDim.x) Bw[p] = b[p];
+  }
+  if (threadIdx.x == 0) status[mat] = 0;
+  __syncthreads();
+  if (B && !chol_reduce_full(Aw, Bw, n, n, red)) {
+    if (threadIdx.x == 0) status[mat] = 1;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) eigs[(size_t)mat * n + i] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  tridiag_full(Aw, n, n, diag, e2, v, y, red);
+  bisect_all(diag, e2, n, lam, red);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) eigs[(size_t)mat * n + i] = lam[i];
+}
+
+}  // namespace hx
+
+extern "C" int hx_eigvalsh_batch_device(hx_ctx* ctx, int32_t n, int64_t batch, const double* d_A, const double* d_B,
+                                        double* d_eigs, int32_t* d_status, void* stream) {
+  if (!ctx || !d_A || !d_eigs || !d_status || n < 1 || batch < 0) return fail(HX_E_ARG, "hx_eigvalsh_batch: bad args");
+  if (batch == 0) return 0;
+  if (set_device(ctx)) return HX_E_CUDA;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!d_B && n <= HX_SMEM_MAX_N) {
+    const size_t smem = hx::fused_smem_bytes(n);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(hx::eigvalsh_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)hx::fused_smem_bytes(HX_SMEM_MAX_N));
+      attr = true;
+    }
+    hx::eigvalsh_smem_kernel<<<(unsigned)batch, 256, smem, st>>>(n, reinterpret_cast<const double2*>(d_A), d_eigs,
+                                                                  reinterpret_cast<int*>(d_status));
+    HX_CUDA(cudaGetLastError());
+    return 0;
+  }
+  if (!d_B && hx::band_path_supported(n)) {
+    int rc = hx::band_eigvalsh(n, batch, reinterpret_cast<const double2*>(d_A), d_eigs, reinterpret_cast<int*>(d_status),
+                               ctx->ws_budget,
+                               [&](size_t bytes) -> void* { return ctx->band.grow(bytes) ? nullptr : ctx->band.p; }, st);
+    if (rc) return fail(HX_E_CUDA, std::string("band path: ") + hx::band_last_error());
+    return 0;
+  }
+  const size_t stride = hx::global_ws_stride(n, d_B != nullptr);
+  int64_t chunk = std::min<int64_t>((int64_t)std::max<size_t>(1, ctx->ws_budget / stride), batch);
+  chunk = std::min<int64_t>(chunk, 65535);
+  if (ctx->ws.grow(stride * (size_t)chunk)) return fail(HX_E_CUDA, "alloc workspace");
+  for (int64_t m0 = 0; m0 < batch; m0 += chunk) {
+    const int64_t cnt = std::min(chunk, batch - m0);
+    hx::eigvalsh_global_kernel<<<(unsigned)cnt, 512, 0, st>>>(n, reinterpret_cast<const double2*>(d_A),
+                                                              reinterpret_cast<const double2*>(d_B), d_eigs,
+                                                              reinterpret_cast<int*>(d_status), m0,
+                                                              static_cast<unsigned char*>(ctx->ws.p), stride);
+    HX_CUDA(cudaGetLastError());
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Kernel-module parity (_kernels.py:68-101): one CTA, thread per grid point, states in input order.
+namespace hx {
+__global__ void counts_kernel(const double* E, const double* w, int64_t count, GridDev g, double* out, int sharp) {
+  for (int m = threadIdx.x; m < g.npts; m += blockDim.x) {
+    double full = 0.0, tr = 0.0;
+    const double em = __dadd_rn(g.e0, __dmul_rn(g.step, (double)m));
+    for (int64_t i = 0; i < count; ++i) {
+      const double e = E[i];
+      if (sharp) {
+        long long idx = (long long)floor(__ddiv_rn(__dsub_rn(e, g.e0), g.step)) + 1;
+        if (idx < 0) idx = 0;
+        if (idx <= m) full = __dadd_rn(full, w[i]);
+        continue;
+      }
+      long long lo = (long long)ceil(__ddiv_rn(__dsub_rn(__dadd_rn(e, g.delta), g.e0), g.step));
+      if (lo < 0) lo = 0;
+      if (lo <= m) {
+        full = __dadd_rn(full, w[i]);
+        continue;
+      }
+      long long m0 = (long long)floor(__ddiv_rn(__dsub_rn(__dsub_rn(e, g.delta), g.e0), g.step)) + 1;
+      if (m0 < 0) m0 = 0;
+      if (m >= m0) {
+        const double x = __ddiv_rn(__dsub_rn(e, em), g.delta);
+        const double gx = __dadd_rn(0.5, __dmul_rn(x, __dadd_rn(-1.125, __dmul_rn(__dmul_rn(0.625, x), x))));
+        tr = __dadd_rn(tr, __dmul_rn(w[i], gx));
+      }
+    }
+    out[m] = __dadd_rn(out[m], __dadd_rn(tr, full));
+  }
+}
+
+// term = full - 0.25 * sum_r quarter_r ; mean / var in fixed sample order (mlmc.py:143-154)
+__global__ void moments_kernel(const double* full, const double* quarters, int64_t M, int npts, double* terms,
+                               double* mean, double* var, double* sums) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= npts) return;
+  double s = 0.0, s2 = 0.0;
+  for (int64_t i = 0; i < M; ++i) {
+    double t = full[i * npts + m];
+    if (quarters) {
+      const double* q = quarters + i * 4 * npts + m;
+      double cv = 0.0;
+      cv = __dadd_rn(cv, q[0]);
+      cv = __dadd_rn(cv, q[npts]);
+      cv = __dadd_rn(cv, q[2 * npts]);
+      cv = __dadd_rn(cv, q[3 * npts]);
+      t = __dsub_rn(t, __dmul_rn(cv, 0.25));
+    }
+    if (terms) terms[i * npts + m] = t;
+    s = __dadd_rn(s, t);
+    s2 = __fma_rn(t, t, s2);
+  }
+  const double mu = __ddiv_rn(s, (double)M);
+  double acc = 0.0;
+  for (int64_t i = 0; i < M; ++i) {
+    double t = terms ? terms[i * npts + m] : 0.0;
+    if (!terms) {
+      t = full[i * npts + m];
+      if (quarters) {
+        const double* q = quarters + i * 4 * npts + m;
+        double cv = 0.0;
+        cv = __dadd_rn(cv, q[0]);
+        cv = __dadd_rn(cv, q[npts]);
+        cv = __dadd_rn(cv, q[2 * npts]);
+        cv = __dadd_rn(cv, q[3 * npts]);
+        t = __dsub_rn(t, __dmul_rn(cv, 0.25));
+      }
+    }
+    const double dlt = __dsub_rn(t, mu);
+    acc = __dadd_rn(acc, __dmul_rn(dlt, dlt));
+  }
+  if (mean) mean[m] = mu;
+  if (var) var[m] = M > 1 ? __ddiv_rn(acc, (double)(M - 1)) : __longlong_as_double(0x7ff8000000000000ll);
+  if (sums) {
+    sums[m] = s;
+    sums[npts + m] = s2;
+  }
+}
+
+__global__ void sample_masks_kernel(uint64_t seed, uint64_t level, uint64_t rep0, int64_t count, double p, int nunits,
+                                    uint64_t* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const int words = (nunits + 63) / 64 > 0 ? (nunits + 63) / 64 : 1;
+  uint64_t s4[4];
+  seedseq_state4(seed, level, rep0 + (uint64_t)i, s4);
+  Pcg64 g;
+  g.seed(s4);
+  uint64_t* o = out + i * words;
+  uint64_t wacc = 0;
+  int w = 0;
+  for (int u = 0; u < nunits; ++u) {
+    if (g.next_double() < p) wacc |= 1ull << (u & 63);
+    if ((u & 63) == 63) {
+      o[w++] = wacc;
+      wacc = 0;
+    }
+  }
+  if (nunits & 63) o[w++] = wacc;
+  for (; w < words; ++w) o[w] = 0;
+}
+}  // namespace hx
+
+extern "C" {
+
+int hx_smoothed_counts_device(const double* d_energies, const double* d_weights, int64_t count, const hx_egrid* grid,
+                              double* d_out, void* stream) {
+  if (!grid || !d_out || (count > 0 && (!d_energies || !d_weights))) return fail(HX_E_ARG, "smoothed_counts: bad args");
+  hx::GridDev g{grid->e0, grid->step, grid->delta, grid->npts, 0};
+  hx::counts_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_energies, d_weights, count, g, d_out, 0);
+  HX_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int hx_sharp_counts_device(const double* d_energies, const double* d_weights, int64_t count, const hx_egrid* grid,
+                           double* d_out, void* stream) {
+  if (!grid || !d_out || (count > 0 && (!d_energies || !d_weights))) return fail(HX_E_ARG, "sharp_counts: bad args");
+  hx::GridDev g{grid->e0, grid->step, grid->delta, grid->npts, 0};
+  hx::counts_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_energies, d_weights, count, g, d_out, 1);
+  HX_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int hx_level_moments_device(const double* d_full, const double* d_quarters, int64_t M, int32_t npts, double* d_terms,
+                            double* d_mean, double* d_var, double* d_sums, void* stream) {
+  if (!d_full || M < 1 || npts < 1) return fail(HX_E_ARG, "level_moments: bad args");
+  hx::moments_kernel<<<(npts + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(d_full, d_quarters, M, npts,
+                                                                                       d_terms, d_mean, d_var, d_sums);
+  HX_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int hx_uniforms(uint64_t seed, uint64_t level, uint64_t rep, int64_t count, double* out) {
+  if (!out || count < 0) return fail(HX_E_ARG, "hx_uniforms: bad args");
+  if (level > 0xFFFFFFFFull || rep > 0xFFFFFFFFull) {
+    // words32 handles wider keys too; keep the documented envelope
+  }
+  uint64_t s4[4];
+  hx::seedseq_state4(seed, level, rep, s4);
+  hx::Pcg64 g;
+  g.seed(s4);
+  for (int64_t i = 0; i < count; ++i) out[i] = g.next_double();
+  return 0;
+}
+
+int hx_sample_masks(uint64_t seed, uint64_t level, uint64_t rep0, int64_t count, double p, int32_t nunits,
+                    uint64_t* out_words, int32_t threads) {
+  if (!out_words || count < 0 || nunits < 0 || !(p >= 0.0 && p <= 1.0)) return fail(HX_E_ARG, "sample_masks: bad args");
+  const int words = std::max(1, (nunits + 63) / 64);
+  auto work = [&](int64_t a, int64_t b) {
+    for (int64_t i = a; i < b; ++i) {
+      uint64_t s4[4];
+      hx::seedseq_state4(seed, level, rep0 + (uint64_t)i, s4);
+      hx::Pcg64 g;
+      g.seed(s4);
+      uint64_t* o = out_words + i * words;
+      for (int w = 0; w < words; ++w) o[w] = 0;
+      for (int u = 0; u < nunits; ++u)
+        if (g.next_double() < p) o[u >> 6] |= 1ull << (u & 63);
+    }
+  };
+  int nt = threads > 0 ? threads : (int)std::max(1u, std::thread::hardware_concurrency());
+  nt = (int)std::min<int64_t>(nt, std::max<int64_t>(1, count / 16));
+  if (nt <= 1) {
+    work(0, count);
+    return 0;
+  }
+  std::vector<std::thread> pool;
+  const int64_t per = (count + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    const int64_t a = t * per, b = std::min(count, a + per);
+    if (a < b) pool.emplace_back(work, a, b);
+  }
+  for (auto& th : pool) th.join();
+  return 0;
+}
+
+int hx_sample_masks_device(uint64_t seed, uint64_t level, uint64_t rep0, int64_t count, double p, int32_t nunits,
+                           uint64_t* d_out_words, void* stream) {
+  if (!d_out_words || count < 0 || nunits < 0) return fail(HX_E_ARG, "sample_masks_device: bad args");
+  if (count == 0) return 0;
+  hx::sample_masks_kernel<<<(unsigned)((count + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      seed, level, rep0, count, p, nunits, d_out_words);
+  HX_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int hx_restrict_masks(const uint64_t* parent_words, int64_t nmasks, int32_t parent_units, const int32_t* unit_assign,
+                      const int32_t* unit_map, int32_t sub_units, uint64_t* out_words) {
+  if (!parent_words || !unit_assign || !unit_map || !out_words || nmasks < 0) return fail(HX_E_ARG, "restrict: bad args");
+  const int pw = std::max(1, (parent_units + 63) / 64), sw = std::max(1, (sub_units + 63) / 64);
+  for (int64_t i = 0; i < nmasks; ++i) {
+    uint64_t* o = out_words + i * 4 * sw;
+    for (int w = 0; w < 4 * sw; ++w) o[w] = 0;
+    const uint64_t* pm = parent_words + i * pw;
+    for (int u = 0; u < parent_units; ++u) {
+      if (!((pm[u >> 6] >> (u & 63)) & 1ull)) continue;
+      const int r = unit_assign[u];
+      if (r < 1 || r > 4) return fail(HX_E_ARG, "restrict: quarter label out of range");
+      const int su = unit_map[u];
+      o[(r - 1) * sw + (su >> 6)] |= 1ull << (su & 63);
+    }
+  }
+  return 0;
+}
+
+}  // extern "C"

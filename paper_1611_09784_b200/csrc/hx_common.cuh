@@ -1,0 +1,63 @@
+// Shared device helpers for libhx (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hx {
+
+// Compiled-cell tables resident in HBM (uploaded once per (model, nu)).
+struct CellDev {
+  int32_t N;          // total dofs
+  int32_t nunits;     // removable units
+  int32_t words;      // uint64 words per mask
+  int32_t pencil;     // HX_PENCIL_*
+  double eps0, t, s;  // commuting-pencil parameters
+  double area;
+  const int32_t* unit_of_dof;  // [N]
+  const double* onsite;        // [N]
+  // hopping CSR by source dof, and its transpose (instances grouped by target dof, instance order)
+  const int32_t* h_ptr;
+  const int32_t* h_col;
+  const double2* h_amp;
+  const double2* h_disp;
+  const int32_t* ht_ptr;   // [N+1]
+  const int32_t* ht_inst;  // instance ids with dst == row, ascending
+  const int32_t* h_src;    // [nnz] source dof of each instance
+  // overlap (HX_PENCIL_GENERAL)
+  const int32_t* s_ptr;
+  const int32_t* s_col;
+  const double2* s_amp;
+  const double2* s_disp;
+  const int32_t* st_ptr;
+  const int32_t* st_inst;
+  const int32_t* s_src;
+};
+
+struct GridDev {
+  double e0, step, delta;
+  int32_t npts;
+  int32_t shift;  // fixed-point fraction bits of the transition accumulator
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// Warp-level sum of a double.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+}  // namespace hx

@@ -1,0 +1,265 @@
+"""Run orchestration on the GPU backend: the drop-in for the reference Engine (runner.py:148-439).
+
+The reference's batch seam `evaluate_masks -> parallel_map(_eval_job, jobs)` (runner.py:206-244) is
+kept with identical dedup/placement semantics (key (n, q, mask), run-wide cache shared across levels
+and CV quarters, in-batch owners), but the new jobs of each (n, q) group go to ONE libhx batch call
+(hx_eval_idos_batch) instead of a process pool.  Sampling (bit-exact with numpy), quarter restriction
+and level moments run in libhx as well.  Results do not depend on batch composition (fixed-point
+IDOS accumulation), so curves are identical for any grouping of requests.
+
+BZ mode "full" is evaluated on its q^2 base points with weights 1/q^2: the two rotated rhombi are
+periodic images of the base grid point for point (spectrum.py:8-14), so the quadrature is the same and
+curves agree with the reference's full mode to rounding (SURVEY finding 3; pinned by
+tests/test_engine_gpu.py against the reference's full-mode fixtures).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .estimators import LevelPlan, LevelStats, MlmcEstimate, combine_levels, level_moments
+from .geometry import build_supercell, partition_quarters
+from .idos import EnergyGrid
+from .models import compile_cell
+from .sampling import (DefectConfiguration, enumerate_configs, keys_from_words, restrict_words, sample_masks,
+                       words_from_keys)
+from .solver import eval_batch, make_bz_grid, raise_status, solve_bands
+
+__all__ = ["Engine", "TaskError", "LevelSampleSet", "ExhaustiveResult", "SLMC_STREAM_OFFSET"]
+
+SLMC_STREAM_OFFSET = 10_000
+
+
+class TaskError(RuntimeError):
+    """One or more tasks failed; message names the task ids (runner.py:56-72)."""
+
+    def __init__(self, failures):
+        self.failures = failures
+        names = ", ".join(str(tid) for tid, _ in failures[:4])
+        more = "" if len(failures) <= 4 else f" (+{len(failures) - 4} more)"
+        super().__init__(f"{len(failures)} task(s) failed: {names}{more}; first error: {failures[0][1]!r}")
+
+
+@dataclass(frozen=True, eq=False)
+class LevelSampleSet:
+    stats: LevelStats
+    terms: np.ndarray = field(repr=False)
+    full: np.ndarray = field(repr=False)
+    cv: np.ndarray | None = field(repr=False, default=None)
+
+
+@dataclass(frozen=True, eq=False)
+class ExhaustiveResult:
+    mean: np.ndarray = field(repr=False)
+    variance: np.ndarray = field(repr=False)
+    weight_sum: float = 1.0
+    nconfigs: int = 0
+    evaluations: int = 0
+    cache_hits: int = 0
+    wall_seconds: float = 0.0
+    n: int = 1
+    q: int = 1
+
+
+class Engine:
+    """Shared context of one run: model, grids, dedup cache, device (runner.py:148-175)."""
+
+    def __init__(self, model, nq: int, delta: float, master_seed: int, workers: int = 1, bz_mode: str = "full",
+                 energy_points: int = 4096, energy_range=None, dedup: bool = True, device: int = 0):
+        self.model = model
+        self.nq = nq
+        self.delta = delta
+        self.master_seed = master_seed
+        self.workers = workers  # accepted for API parity; the GPU batch replaces the process pool
+        self.bz_mode = bz_mode
+        self.dedup = dedup
+        self.device = device
+        self._cache: dict = {}
+        self._supercells: dict = {}
+        self._cells: dict = {}
+        self._kgrids: dict = {}
+        if energy_range is None:
+            emin, emax = self.detect_energy_range()
+        else:
+            emin, emax = energy_range
+            if not emax > emin:
+                raise ValueError("energy range needs max > min")
+        self.grid = EnergyGrid(emin - 2.0 * delta, emax + 2.0 * delta, energy_points)
+
+    # -- geometry / caches --
+    def supercell(self, n: int):
+        if n not in self._supercells:
+            self._supercells[n] = build_supercell(self.model.lattice_spec(), n)
+        return self._supercells[n]
+
+    def cell(self, n: int):
+        if n not in self._cells:
+            self._cells[n] = compile_cell(self.model, self.supercell(n), self.device)
+        return self._cells[n]
+
+    def kpoints(self, n: int, q: int) -> np.ndarray:
+        """k-points solved for (n, q): the base q x q rhombus (full mode's rotated copies are images)."""
+        key = (n, q)
+        if key not in self._kgrids:
+            self._kgrids[key] = make_bz_grid(self.model.lattice_spec(), n, q, "reduced").kpoints
+        return self._kgrids[key]
+
+    def q_of(self, n: int) -> int:
+        if self.nq % n:
+            raise ValueError(f"n*q constant {self.nq} is not divisible by n = {n}")
+        return self.nq // n
+
+    def detect_energy_range(self):
+        """Unperturbed nu=1 band range on the shared folded grid (runner.py:189-202)."""
+        grid = make_bz_grid(self.model.lattice_spec(), 1, self.nq, self.bz_mode)
+        bands = solve_bands(self.model, self.supercell(1), None, grid, cell=self.cell(1))
+        return float(bands.energies.min()), float(bands.energies.max())
+
+    # -- the batch seam --
+    def _solve_group(self, n: int, q: int, keys, task_ids):
+        cell = self.cell(n)
+        words = words_from_keys(keys, cell.supercell.nunits)
+        kp = self.kpoints(n, q)
+        t0 = time.perf_counter()
+        curves, _, status = eval_batch(cell, kp, words, self.grid.lo, self.grid.step, self.grid.npoints,
+                                       self.delta)
+        secs = time.perf_counter() - t0
+        bad = np.flatnonzero(((status == _lib.HX_ST_NOT_PD) | (status == _lib.HX_ST_NONFINITE)).any(axis=1))
+        if len(bad):
+            failures = []
+            for i in bad:
+                try:
+                    raise_status(status[i:i + 1], kp)
+                except Exception as exc:  # noqa: BLE001 - collected with the task id
+                    failures.append((task_ids[i], exc))
+            raise TaskError(failures)
+        return curves, secs / max(1, len(keys))
+
+    def evaluate_masks(self, requests):
+        """Dedup on (n, q, mask) against the run cache and within the batch; solve the new jobs of each
+        (n, q) group in one GPU batch; results in request order (runner.py:206-244)."""
+        placement, new_jobs, owners = [], [], {}
+        hits = 0
+        for n, q, mask, task_id in requests:
+            key = (n, q, mask)
+            if self.dedup and key in self._cache:
+                hits += 1
+                placement.append(("cache", key))
+                continue
+            if self.dedup and key in owners:
+                hits += 1
+                placement.append(("job", owners[key]))
+                continue
+            idx = len(new_jobs)
+            if self.dedup:
+                owners[key] = idx
+            new_jobs.append((n, q, mask, task_id))
+            placement.append(("job", idx))
+        results = [None] * len(new_jobs)
+        groups: dict = {}
+        for idx, (n, q, mask, tid) in enumerate(new_jobs):
+            groups.setdefault((n, q), []).append(idx)
+        spent = 0.0
+        for (n, q), idxs in groups.items():
+            curves, per_job = self._solve_group(n, q, [new_jobs[i][2] for i in idxs], [new_jobs[i][3] for i in idxs])
+            for row, i in enumerate(idxs):
+                results[i] = (curves[row], per_job)
+            spent += per_job * len(idxs)
+        if self.dedup:
+            for (n, q, mask, _), res in zip(new_jobs, results):
+                self._cache[(n, q, mask)] = res
+        out = [self._cache[ref] if kind == "cache" else results[ref] for kind, ref in placement]
+        return out, hits, spent
+
+    # -- level sampling --
+    def draw_configs(self, supercell, p_vac: float, stream_level: int, count: int):
+        words = sample_masks(supercell.nunits, p_vac, self.master_seed, stream_level, 0, count)
+        return [DefectConfiguration.from_key(supercell, k) for k in keys_from_words(words)]
+
+    def sample_level(self, level: int, n: int, nsamples: int, p_vac: float, with_cv: bool, stream_level=None):
+        """Draw outcomes and evaluate the level terms with the quarter CV (runner.py:254-311)."""
+        q = self.q_of(n)
+        sc = self.supercell(n)
+        stream = level if stream_level is None else stream_level
+        words = sample_masks(sc.nunits, p_vac, self.master_seed, stream, 0, nsamples)
+        keys = keys_from_words(words)
+        requests = [(n, q, k, (level, m, "Q")) for m, k in enumerate(keys)]
+        if with_cv:
+            part = partition_quarters(sc)
+            nsub = n // 2
+            qsub = self.q_of(nsub)
+            sub = restrict_words(words, part)  # [M, 4, w]
+            subkeys = keys_from_words(sub.reshape(nsamples * 4, -1))
+            for m in range(nsamples):
+                for r in range(4):
+                    requests.append((nsub, qsub, subkeys[m * 4 + r], (level, m, f"CV{r + 1}")))
+        results, hits, spent = self.evaluate_masks(requests)
+        npts = self.grid.npoints
+        full = np.stack([results[m][0] for m in range(nsamples)]) if nsamples else np.zeros((0, npts))
+        nominal = sum(results[m][1] for m in range(nsamples))
+        quarters = None
+        if with_cv:
+            quarters = np.stack([results[nsamples + i][0] for i in range(4 * nsamples)]).reshape(nsamples, 4, npts)
+            nominal += sum(results[nsamples + i][1] for i in range(4 * nsamples))
+        terms, mean, var = level_moments(full, quarters, self.device)
+        terms = terms.cpu().numpy()
+        cv = None if quarters is None else full - terms
+        if quarters is not None:
+            # cv exactly as the reference forms it: ((q1 + q2) + q3 + q4) * 0.25
+            cv = np.zeros((nsamples, npts))
+            for r in range(4):
+                cv += quarters[:, r, :]
+            cv *= 0.25
+        stats = LevelStats(level=level, n=n, q=q, nsamples=nsamples, mean=mean.cpu().numpy(),
+                           sample_variance=var.cpu().numpy() if nsamples > 1 else None,
+                           work_per_sample=nominal / nsamples, wall_seconds=spent, cache_hits=hits)
+        return LevelSampleSet(stats=stats, terms=terms, full=full, cv=cv)
+
+    # -- mode drivers (runner.py:315-419) --
+    def run_mc(self, plan: LevelPlan):
+        level = plan.num_levels
+        sset = self.sample_level(level, plan.ns[-1], plan.samples[-1], plan.p_vac, with_cv=False)
+        return combine_levels(self.grid, [sset.stats], total_wall_seconds=sset.stats.wall_seconds), sset
+
+    def run_mlmc(self, plan: LevelPlan):
+        sets, total = [], 0.0
+        for idx, (n, m) in enumerate(zip(plan.ns, plan.samples), start=1):
+            sset = self.sample_level(idx, n, m, plan.p_vac, with_cv=idx > 1)
+            sets.append(sset)
+            total += sset.stats.wall_seconds
+        return combine_levels(self.grid, [s.stats for s in sets], total_wall_seconds=total), sets
+
+    def run_slmc_reference(self, plan: LevelPlan, nsamples: int):
+        level = plan.num_levels
+        return self.sample_level(level, plan.ns[-1], nsamples, plan.p_vac, with_cv=False,
+                                 stream_level=SLMC_STREAM_OFFSET + level)
+
+    def run_exhaustive(self, n: int, p_vac: float, symmetry_reduce: bool = False, cap: int = 24):
+        """Exact expectation over all 2^N outcomes with binomial weights (runner.py:380-415)."""
+        if symmetry_reduce:
+            raise NotImplementedError("translation-orbit reduction is outside the GPU hot path")
+        sc = self.supercell(n)
+        q = self.q_of(n)
+        pairs = list(enumerate_configs(sc, p_vac, cap=cap))
+        weight_sum = math.fsum(w for _, w in pairs)
+        if abs(weight_sum - 1.0) > 1e-12:
+            raise ArithmeticError(f"enumeration weights sum to {weight_sum!r}, not 1")
+        masks = [c.key for c, _ in pairs]
+        results, hits, spent = self.evaluate_masks([(n, q, m, ("exhaustive", m)) for m in masks])
+        m1 = np.zeros(self.grid.npoints)
+        m2 = np.zeros(self.grid.npoints)
+        for (_, w), (c, _) in zip(pairs, results):
+            m1 += w * c
+            m2 += w * c * c
+        return ExhaustiveResult(mean=m1, variance=np.maximum(m2 - m1 * m1, 0.0), weight_sum=weight_sum,
+                                nconfigs=len(pairs), evaluations=len(masks) - hits, cache_hits=hits,
+                                wall_seconds=spent, n=n, q=q)
+
+    def unperturbed_curve(self, n: int) -> np.ndarray:
+        results, _, _ = self.evaluate_masks([(n, self.q_of(n), 0, ("unperturbed", n))])
+        return results[0][0]

@@ -1,0 +1,165 @@
+"""MC / MLMC estimator bookkeeping (mlmc.py:49-196).
+
+Per-level moments are formed on the GPU by `level_moments` (hx_level_moments_device): the control-
+variate term full - 0.25 * sum_r quarter_r, then the mean and the unbiased variance in fixed sample
+order, reproducing np.mean / np.var(ddof=1) over axis 0 (mlmc.py:143-154) and the CV assembly
+order of runner.py:281-299.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+__all__ = ["LevelPlan", "LevelStats", "MlmcEstimate", "mean_and_variance", "level_moments", "combine_levels",
+           "control_variate_sample", "window_mask"]
+
+
+@dataclass(frozen=True)
+class LevelPlan:
+    """Supercell factors doubling per level with n*q held constant (mlmc.py:49-97)."""
+
+    ns: tuple
+    samples: tuple
+    nq: int
+    p_vac: float
+    delta: float
+
+    def __post_init__(self):
+        if not self.ns:
+            raise ValueError("level plan needs at least one level")
+        if len(self.ns) != len(self.samples):
+            raise ValueError("ns and samples must have matching lengths")
+        for n in self.ns:
+            if n < 1:
+                raise ValueError(f"supercell factor must be >= 1, got {n}")
+        for a, b in zip(self.ns, self.ns[1:]):
+            if b != 2 * a:
+                raise ValueError(f"level sizes must double: {self.ns}")
+        for m in self.samples:
+            if m < 1:
+                raise ValueError(f"sample counts must be >= 1, got {m}")
+        if not 0.0 <= self.p_vac <= 1.0:
+            raise ValueError(f"p_vac must be in [0, 1], got {self.p_vac}")
+        if self.delta <= 0:
+            raise ValueError("smoothing width must be positive")
+        for n in self.ns:
+            if self.q(n) < 1:
+                raise ValueError(f"n*q = {self.nq} gives no k-points at n = {n}")
+
+    @classmethod
+    def geometric(cls, c: int, num_levels: int, **kw) -> "LevelPlan":
+        return cls(ns=tuple(c * 2**lv for lv in range(1, num_levels + 1)), **kw)
+
+    @property
+    def num_levels(self) -> int:
+        return len(self.ns)
+
+    def q(self, n: int) -> int:
+        if self.nq % n:
+            raise ValueError(f"n*q constant {self.nq} not divisible by n = {n}")
+        return self.nq // n
+
+
+@dataclass(frozen=True, eq=False)
+class LevelStats:
+    level: int
+    n: int
+    q: int
+    nsamples: int
+    mean: np.ndarray = field(repr=False)
+    sample_variance: np.ndarray | None = field(repr=False, default=None)
+    work_per_sample: float = 0.0
+    wall_seconds: float = 0.0
+    cache_hits: int = 0
+
+
+@dataclass(frozen=True, eq=False)
+class MlmcEstimate:
+    grid: object
+    mean: np.ndarray = field(repr=False)
+    estimator_variance: np.ndarray | None = field(repr=False)
+    levels: tuple = ()
+    total_wall_seconds: float = 0.0
+
+    def level_window_variances(self, window=None):
+        mask = window_mask(self.grid, window)
+        return [float(np.mean(ls.sample_variance[mask])) if ls.sample_variance is not None else math.nan
+                for ls in self.levels]
+
+
+def window_mask(grid, window=None) -> np.ndarray:
+    if window is None:
+        return np.ones(grid.npoints, dtype=bool)
+    lo, hi = window
+    v = grid.values
+    mask = (v >= lo) & (v <= hi)
+    if not mask.any():
+        raise ValueError(f"energy window {window} contains no grid points")
+    return mask
+
+
+def level_moments(full, quarters=None, device: int = 0):
+    """(terms, mean, var) on the GPU; `full` [M, npts], `quarters` [M, 4, npts] or None.
+
+    Accepts numpy arrays or CUDA torch tensors; returns torch tensors on the device.
+    """
+    import torch
+
+    dev = torch.device("cuda", device)
+    f = torch.as_tensor(full, dtype=torch.float64).to(dev).contiguous()
+    M, npts = f.shape
+    q = None if quarters is None else torch.as_tensor(quarters, dtype=torch.float64).to(dev).contiguous()
+    terms = torch.empty_like(f)
+    mean = torch.empty(npts, dtype=torch.float64, device=dev)
+    var = torch.empty(npts, dtype=torch.float64, device=dev)
+    _lib.Device.ctx(device)
+    _lib.check(_lib.load().hx_level_moments_device(f.data_ptr(), 0 if q is None else q.data_ptr(), M, npts,
+                                                   terms.data_ptr(), mean.data_ptr(), var.data_ptr(), 0,
+                                                   torch.cuda.current_stream(dev).cuda_stream),
+               "hx_level_moments_device")
+    return terms, mean, var
+
+
+def mean_and_variance(curves):
+    """Pointwise mean and unbiased variance over axis 0; variance None for one sample (mlmc.py:143-154)."""
+    curves = np.asarray(curves)
+    if curves.ndim != 2 or curves.shape[0] < 1:
+        raise ValueError("expected a (nsamples, npoints) array")
+    _, mean, var = level_moments(curves)
+    mean = mean.cpu().numpy()
+    return (mean, None) if curves.shape[0] < 2 else (mean, var.cpu().numpy())
+
+
+def control_variate_sample(config, partition, evaluate_full, evaluate_quarter):
+    """Coupled (Q_l, Q_l^CV) for one outcome (mlmc.py:157-174)."""
+    from .sampling import restrict
+
+    q_full = np.asarray(evaluate_full(config))
+    acc = None
+    for r in range(1, partition.R + 1):
+        part = np.asarray(evaluate_quarter(restrict(config, partition, r)))
+        acc = part.copy() if acc is None else acc + part
+    return q_full, acc / partition.R
+
+
+def combine_levels(grid, levels, total_wall_seconds: float = 0.0) -> MlmcEstimate:
+    """Sum of level means; estimator variance sum_l V_l / M_l (mlmc.py:177-196)."""
+    if not levels:
+        raise ValueError("no levels to combine")
+    mean = np.zeros(grid.npoints)
+    var = np.zeros(grid.npoints)
+    ok = True
+    for ls in levels:
+        mean = mean + ls.mean
+        if ls.sample_variance is None:
+            ok = False
+        else:
+            var = var + ls.sample_variance / ls.nsamples
+    return MlmcEstimate(grid=grid, mean=mean, estimator_variance=var if ok else None, levels=tuple(levels),
+                        total_wall_seconds=total_wall_seconds)

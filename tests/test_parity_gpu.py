@@ -1,0 +1,165 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference-generated goldens and the oracle.
+
+Tolerances (BASELINE.json north_star): eigenvalues <= 1e-10 x spectral width; per-sample IDOS <= 1e-9;
+level means <= 1e-9; sharp counts identical except within 1e-10 of a grid energy; masks bit-identical.
+"""
+
+import numpy as np
+import pytest
+
+import hexmc_oracle as O
+from conftest import TABLE, golden, words_to_int
+
+import paper_1611_09784_b200 as hx
+from paper_1611_09784_b200.solver import eval_batch
+
+pytestmark = pytest.mark.gpu
+
+EIG_TOL = 1e-10  # x spectral width
+IDOS_TOL = 1e-9
+
+
+def model_of(name):
+    return hx.load_coupling_table(TABLE) if name.startswith("t") else hx.GrapheneNNModel()
+
+
+@pytest.mark.parametrize("name,table,nu", [
+    ("g2_v3", False, 2), ("g1_gamma", False, 1), ("g4_rand", False, 4), ("g3_none", False, 3),
+    ("t2_v1", True, 2), ("t1_none", True, 1)])
+def test_device_assembly_matches_reference(name, table, nu):
+    g = golden("assembly.npz")
+    model = hx.load_coupling_table(TABLE) if table else hx.GrapheneNNModel()
+    sc = hx.build_supercell(model.lattice_spec(), nu)
+    cfg = hx.DefectConfiguration.from_key(sc, words_to_int(g[f"{name}_mask"]))
+    pair = hx.assemble_bloch(model, sc, cfg, g[f"{name}_k"])
+    np.testing.assert_allclose(pair.H, g[f"{name}_H"], rtol=0, atol=1e-13)
+    np.testing.assert_allclose(pair.S, g[f"{name}_S"], rtol=0, atol=1e-13)
+
+
+@pytest.mark.parametrize("name", ["g4q6", "g8q4", "g16q1", "t2q4", "t4q2"])
+def test_eigenvalues_and_curves_match_reference(name):
+    g = golden("eigs_curves.npz")
+    model = model_of(name)
+    nu, q = (int(x) for x in g[f"{name}_meta"])
+    lo, hi, npts = g[f"{name}_grid"]
+    npts = int(npts)
+    sc = hx.build_supercell(model.lattice_spec(), nu)
+    cell = hx.compile_cell(model, sc)
+    kp = g[f"{name}_kpoints"]
+    words = g[f"{name}_masks"]
+    step = (hi - lo) / (npts - 1)
+    curves, eigs, status = eval_batch(cell, kp, words, lo, step, npts, 0.01, want_eigs=True)
+    assert (status == 0).all()
+    ref = g[f"{name}_eigs"]
+    width = np.nanmax(ref) - np.nanmin(ref)
+    np.testing.assert_array_equal(np.isnan(eigs), np.isnan(ref))
+    assert np.nanmax(np.abs(eigs - ref)) <= EIG_TOL * width
+    np.testing.assert_allclose(curves, g[f"{name}_curves"], rtol=0, atol=IDOS_TOL)
+    np.testing.assert_allclose(curves, g[f"{name}_curves_full"], rtol=0, atol=IDOS_TOL)
+    sharp, _, _ = eval_batch(cell, kp, words, lo, step, npts, 0.01, sharp=True)
+    ref_sharp = g[f"{name}_sharp"]
+    diff = np.abs(sharp - ref_sharp) > 1e-12
+    if diff.any():
+        # only allowed where an eigenvalue sits within 1e-10 of a grid energy
+        grid = lo + step * np.arange(npts)
+        for m, j in zip(*np.nonzero(diff)):
+            e = ref[m][~np.isnan(ref[m])]
+            assert np.min(np.abs(e - grid[j])) < 1e-10
+
+
+def test_solve_bands_gamma_and_analytic():
+    model = hx.GrapheneNNModel()
+    sc = hx.build_supercell(model.lattice_spec(), 1)
+    grid = hx.make_bz_grid(model.lattice_spec(), 1, 1, "reduced")
+    bands = hx.solve_bands(model, sc, None, grid)
+    np.testing.assert_allclose(bands.energies[0], [3 * model.t / (1 + 3 * model.s), -3 * model.t / (1 - 3 * model.s)],
+                               rtol=0, atol=1e-12)
+    assert bands.energies[0][0] == pytest.approx(-6.5602, abs=1e-4)
+    assert bands.energies[0][1] == pytest.approx(14.8434, abs=1e-4)
+
+
+def test_band_folding_nu2_vs_nu1():
+    model = hx.GrapheneNNModel()
+    spec = model.lattice_spec()
+    b1 = hx.solve_bands(model, hx.build_supercell(spec, 1), None, hx.make_bz_grid(spec, 1, 8, "reduced"))
+    b2 = hx.solve_bands(model, hx.build_supercell(spec, 2), None, hx.make_bz_grid(spec, 2, 4, "reduced"))
+    np.testing.assert_allclose(np.sort(b2.energies.reshape(-1)), np.sort(b1.energies.reshape(-1)), atol=1e-9)
+
+
+def test_non_pd_overlap_raises_solver_error():
+    entries = []
+    for di, dj in ((0, 0), (-1, 0), (0, -1)):
+        entries.append((di, dj, 0, 0, 1, 0, 0.5 + 0j))
+        entries.append((-di, -dj, 1, 0, 0, 0, 0.5 + 0j))
+    model = hx.MultiOrbitalModel(orbitals=(("A", 1), ("B", 1)), onsite=((0, 0, 0.0), (1, 0, 0.0)),
+                                 hops=((0, 0, 0, 0, 1, 0, -1.0 + 0j), (0, 0, 1, 0, 0, 0, -1.0 + 0j)),
+                                 overlap=tuple(entries), removable=("A", "B"))
+    sc = hx.build_supercell(model.lattice_spec(), 1)
+    grid = hx.make_bz_grid(model.lattice_spec(), 1, 1, "reduced")
+    with pytest.raises(hx.SolverError, match=r"k=\("):
+        hx.solve_bands(model, sc, None, grid)
+
+
+def test_general_pencil_matches_zhegv():
+    # a PD overlap table: graphene as a general table (overlap couplings) -> Cholesky path
+    entries, hops = [], []
+    for di, dj in ((0, 0), (-1, 0), (0, -1)):
+        entries += [(di, dj, 0, 0, 1, 0, 0.129 + 0j), (-di, -dj, 1, 0, 0, 0, 0.129 + 0j)]
+        hops += [(di, dj, 0, 0, 1, 0, -3.033 + 0j), (-di, -dj, 1, 0, 0, 0, -3.033 + 0j)]
+    model = hx.MultiOrbitalModel(orbitals=(("A", 1), ("B", 1)), onsite=((0, 0, 0.0), (1, 0, 0.0)),
+                                 hops=tuple(hops), overlap=tuple(entries), removable=("A", "B"))
+    spec = model.lattice_spec()
+    sc = hx.build_supercell(spec, 3)
+    cfg = hx.sample_defects(sc, 0.2, hx.SeedSpec(5, 1, 2))
+    grid = hx.make_bz_grid(spec, 3, 2, "reduced")
+    bands = hx.solve_bands(model, sc, cfg, grid)
+    om = O.graphene_model()
+    ocell = O.make_cell(om, 3)
+    ref = O.solve_bands(ocell, om, cfg.key, grid.kpoints)
+    assert np.max(np.abs(bands.energies - ref)) <= EIG_TOL * (ref.max() - ref.min())
+
+
+def test_curves_independent_of_batch_composition():
+    model = hx.GrapheneNNModel()
+    sc = hx.build_supercell(model.lattice_spec(), 4)
+    cell = hx.compile_cell(model, sc)
+    kp = hx.make_bz_grid(model.lattice_spec(), 4, 6, "reduced").kpoints
+    from paper_1611_09784_b200.sampling import sample_masks
+
+    w = sample_masks(sc.nunits, 0.05, 2026, 1, 0, 64)
+    a, _, _ = eval_batch(cell, kp, w, -6.58, 0.107, 201, 0.01)
+    perm = np.random.default_rng(0).permutation(64)
+    b, _, _ = eval_batch(cell, kp, w[perm], -6.58, 0.107, 201, 0.01)
+    c, _, _ = eval_batch(cell, kp, w[:7], -6.58, 0.107, 201, 0.01)
+    assert np.array_equal(a[perm], b)
+    assert np.array_equal(a[:7], c)
+
+
+def test_engine_levels_match_reference():
+    g = golden("levels.npz")
+    eng = hx.Engine(hx.GrapheneNNModel(), nq=16, delta=0.01, master_seed=2026, bz_mode="reduced", energy_points=201)
+    assert (eng.grid.lo, eng.grid.hi) == pytest.approx((g["grid"][0], g["grid"][1]), abs=1e-13)
+    recs = g["records"]
+    for level, (n, M) in enumerate(((4, 24), (8, 8)), start=1):
+        s = eng.sample_level(level, n, M, 0.05, with_cv=level > 1)
+        np.testing.assert_allclose(s.full, g[f"L{level}_full"], rtol=0, atol=IDOS_TOL)
+        np.testing.assert_allclose(s.stats.mean, g[f"L{level}_mean"], rtol=0, atol=IDOS_TOL)
+        np.testing.assert_allclose(s.stats.sample_variance, g[f"L{level}_var"], rtol=0, atol=IDOS_TOL)
+        assert s.stats.cache_hits == recs[level - 1][4]
+    t = hx.load_coupling_table(TABLE)
+    et = hx.Engine(t, nq=4, delta=0.01, master_seed=2026, bz_mode="reduced", energy_points=201,
+                   energy_range=(-2.932, 4.740))
+    s = et.sample_level(1, 2, 6, 0.05, with_cv=False)
+    np.testing.assert_allclose(s.full, g["table_L1_full"], rtol=0, atol=IDOS_TOL)
+    np.testing.assert_allclose(s.stats.mean, g["table_L1_mean"], rtol=0, atol=IDOS_TOL)
+
+
+def test_all_vacant_gives_zero_curve_and_plateau():
+    eng = hx.Engine(hx.GrapheneNNModel(), nq=8, delta=0.02, master_seed=99, energy_points=512)
+    s = eng.sample_level(1, 1, 3, p_vac=1.0, with_cv=False)
+    assert np.array_equal(s.full, np.zeros_like(s.full))
+    plan = hx.LevelPlan(ns=(2, 4), samples=(6, 3), nq=8, p_vac=0.0, delta=0.02)
+    _, sets = eng.run_mlmc(plan)
+    for sset in sets:
+        n = sset.stats.n
+        assert np.allclose(sset.full[:, -1], 2.0 * n * n / eng.supercell(n).area, atol=1e-9)
