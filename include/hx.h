@@ -78,6 +78,8 @@ typedef struct hx_egrid {
 
 /* ---- context / lifetime ---------------------------------------------------------------------- */
 int hx_abi_version(void);
+/* Cumulative number of libhx kernel launches in this process (instrumentation for bench.py). */
+int hx_kernel_launches(uint64_t* out);
 const char* hx_last_error(void);
 int hx_device_count(int32_t* out);
 int hx_ctx_create(int32_t device, hx_ctx** out);
@@ -152,6 +154,11 @@ int hx_uniforms(uint64_t seed, uint64_t level, uint64_t rep, int64_t count, doub
 int hx_restrict_masks(const uint64_t* parent_words, int64_t nmasks, int32_t parent_units,
                       const int32_t* unit_assign, const int32_t* unit_map, int32_t sub_units,
                       uint64_t* out_words);
+
+/* Device variant of hx_restrict_masks (device pointers; quarter labels/unit map uploaded by caller). */
+int hx_restrict_masks_device(const uint64_t* d_parent_words, int64_t nmasks, int32_t parent_units,
+                             const int32_t* d_unit_assign, const int32_t* d_unit_map, int32_t sub_units,
+                             uint64_t* d_out_words, void* stream);
 
 #ifdef __cplusplus
 }

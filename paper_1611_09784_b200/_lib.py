@@ -26,7 +26,8 @@ EXPORTED = (
     "hx_ctx_synchronize", "hx_cell_create", "hx_cell_destroy", "hx_eval_idos_batch",
     "hx_eval_idos_batch_device", "hx_eigvalsh_batch_device", "hx_smoothed_counts_device",
     "hx_sharp_counts_device", "hx_level_moments_device", "hx_sample_masks", "hx_sample_masks_device",
-    "hx_uniforms", "hx_restrict_masks", "hx_assemble_device",
+    "hx_uniforms", "hx_restrict_masks", "hx_assemble_device", "hx_restrict_masks_device",
+    "hx_kernel_launches",
 )
 
 
@@ -65,6 +66,7 @@ def load():
         vp, i32, i64, u64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double
         sig = {
             "hx_abi_version": (C.c_int, []),
+            "hx_kernel_launches": (C.c_int, [C.POINTER(u64)]),
             "hx_last_error": (C.c_char_p, []),
             "hx_device_count": (C.c_int, [C.POINTER(i32)]),
             "hx_ctx_create": (C.c_int, [i32, C.POINTER(vp)]),
@@ -84,6 +86,7 @@ def load():
             "hx_uniforms": (C.c_int, [u64, u64, u64, i64, vp]),
             "hx_restrict_masks": (C.c_int, [vp, i64, i32, vp, vp, i32, vp]),
             "hx_assemble_device": (C.c_int, [vp, vp, vp, i32, vp, i64, vp, vp, vp, vp]),
+            "hx_restrict_masks_device": (C.c_int, [vp, i64, i32, vp, vp, i32, vp, vp]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -129,6 +132,12 @@ def restrict_masks(parent_words: np.ndarray, parent_units: int, assign: np.ndarr
     check(load().hx_restrict_masks(ptr(parent_words), n, parent_units, ptr(a), ptr(m), sub_units, ptr(out)),
           "hx_restrict_masks")
     return out
+
+
+def kernel_launches() -> int:
+    n = C.c_uint64(0)
+    check(load().hx_kernel_launches(C.byref(n)), "hx_kernel_launches")
+    return int(n.value)
 
 
 class Device:

@@ -1,25 +1,793 @@
-// Large-N two-stage path: placeholder until the banded reduction lands.
+// Large-N path: batched two-stage Hermitian tridiagonalisation on sm_100a.
+//
+// Stage 1 (dense -> band of width BW=32), per panel step k0 for every matrix of the batch:
+//   panel_qr_kernel    Householder QR of the m x BW panel below the band (m = N - k0 - BW):
+//                      V (explicit, unit lower trapezoidal), T (zlarft forward/columnwise), R into A.
+//   hemm_kernel        X = A22 V                    (DMMA f64 tensor cores, complex as 4 real MMAs)
+//   w_kernel           W = X T - 1/2 V (T^H V^H X T)
+//   her2k_kernel       A22 -= W V^H + V W^H          (DMMA; lower tiles computed, upper mirrored)
+// so that A22 <- Q^H A22 Q with Q = I - V T V^H (the blocked two-sided update of zhetrd/zhe2hb).
+// Stage 2 (band -> tridiagonal): bulge_chase_kernel, Householder bulge chasing on the lower band.
+// Then Sturm bisection + the reference IDOS functional (hx_dense.cuh) per matrix.
+//
+// Vacancies: kept dofs are compacted to the leading d x d block and the tail is exactly zero, so
+// every reflector acting on it is the identity; bisection runs on the leading d x d tridiagonal.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
 #include <string>
 
 #include "hx_band.cuh"
+#include "hx_dense.cuh"
+#include "hx_dmma.cuh"
+#include "hx_kernels.cuh"
 
 namespace hx {
 
-static std::string g_band_err;
+constexpr int BW = 32;  // band width of stage 1
 
-void band_init_attributes() {}
-bool band_path_supported(int) { return false; }
+static std::string g_band_err;
 const char* band_last_error() { return g_band_err.c_str(); }
 
-int band_eval(const CellDev&, const double2*, int, const uint64_t*, int64_t, const GridDev&, int*, unsigned long long*,
-              double*, int*, int, size_t, const Alloc&, cudaStream_t) {
-  g_band_err = "banded path not available";
-  return -1;
+#define BAND_CUDA(call)                                             \
+  do {                                                              \
+    cudaError_t e_ = (call);                                        \
+    if (e_ != cudaSuccess) {                                        \
+      g_band_err = std::string(#call) + ": " + cudaGetErrorString(e_); \
+      return -1;                                                    \
+    }                                                               \
+  } while (0)
+
+struct BandWs {
+  // per-matrix layout inside one workspace slab (offsets in double2 units)
+  size_t a_off, v_off, x_off, t_off, dg_off;  // dg: diag + e2 (2N doubles = N double2)
+  size_t stride;                             // per matrix, double2 units
+  static BandWs make(int N) {
+    BandWs w;
+    w.a_off = 0;
+    w.v_off = (size_t)N * N;
+    w.x_off = w.v_off + (size_t)N * BW;
+    w.t_off = w.x_off + (size_t)N * BW;
+    w.dg_off = w.t_off + (size_t)BW * BW;
+    w.stride = w.dg_off + (size_t)N + 16;
+    w.stride = (w.stride + 15) & ~(size_t)15;
+    return w;
+  }
+};
+
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+
+// ------------------------------------------------------------------------------------------------
+// Panel QR: one CTA per matrix.
+__global__ void __launch_bounds__(256) panel_qr_kernel(double2* ws, BandWs L, int N, int k0) {
+  __shared__ double red[96];
+  __shared__ double2 sred[8][BW];
+  __shared__ double2 s[BW];
+  __shared__ double2 Ts[BW][BW + 1];
+  double2* base = ws + (size_t)blockIdx.x * L.stride;
+  const int lda = N;
+  const int m = N - k0 - BW;
+  double2* P = base + L.a_off + (size_t)k0 * lda + k0 + BW;  // P[i + c*lda], i < m, c < BW
+  double2* V = base + L.v_off;                                 // V[i + c*N]
+  double2* T = base + L.t_off;
+  const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = bd >> 5;
+  for (int p = tid; p < BW * (BW + 1); p += bd) (&Ts[0][0])[p] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int j = 0; j < BW; ++j) {
+    if (j >= m) {
+      for (int i = tid; i < m; i += bd) V[i + (size_t)j * N] = make_double2(0.0, 0.0);
+      __syncthreads();
+      continue;
+    }
+    double part = 0.0;
+    for (int i = j + tid; i < m; i += bd) {
+      const double2 x = P[i + (size_t)j * lda];
+      part += x.x * x.x + x.y * x.y;
+    }
+    const double sig2 = block_sum(part, red);
+    const double2 alpha = P[j + (size_t)j * lda];
+    const Reflector h = make_reflector(alpha, sig2);
+    const double tau = h.tau;
+    // explicit V column j; R diagonal beta into the panel, zeros below it
+    for (int i = tid; i < m; i += bd) {
+      double2 vi;
+      if (i < j) vi = make_double2(0.0, 0.0);
+      else if (i == j) vi = make_double2(1.0, 0.0);
+      else vi = tau == 0.0 ? make_double2(0.0, 0.0) : cmul(P[i + (size_t)j * lda], h.scale);
+      V[i + (size_t)j * N] = vi;
+    }
+    // dots s_c = v^H col_c, col_c = P[:,c] (c > j) or V[:,c] (c < j); rows i >= j (own rows, no sync needed)
+    double2 acc[BW];
+#pragma unroll
+    for (int c = 0; c < BW; ++c) acc[c] = make_double2(0.0, 0.0);
+    if (tau != 0.0) {
+      for (int i = tid; i < m; i += bd) {
+        if (i < j) continue;
+        const double2 vi = V[i + (size_t)j * N];
+#pragma unroll
+        for (int c = 0; c < BW; ++c) {
+          if (c == j) continue;
+          const double2 x = c > j ? P[i + (size_t)c * lda] : V[i + (size_t)c * N];
+          acc[c].x += vi.x * x.x + vi.y * x.y;
+          acc[c].y += vi.x * x.y - vi.y * x.x;
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < BW; ++c) {
+      acc[c].x = warp_sum(acc[c].x);
+      acc[c].y = warp_sum(acc[c].y);
+    }
+    __syncthreads();
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < BW; ++c) sred[warp][c] = acc[c];
+    }
+    __syncthreads();
+    if (tid < BW) {
+      double2 t = make_double2(0.0, 0.0);
+      for (int w = 0; w < nw; ++w) {
+        t.x += sred[w][tid].x;
+        t.y += sred[w][tid].y;
+      }
+      s[tid] = t;
+    }
+    if (tid == 0) {
+      if (tau != 0.0) {
+        const double sg = sqrt(sig2);
+        const double aa = hypot(alpha.x, alpha.y);
+        const double2 ph = aa > 0.0 ? make_double2(alpha.x / aa, alpha.y / aa) : make_double2(1.0, 0.0);
+        P[j + (size_t)j * lda] = make_double2(-ph.x * sg, -ph.y * sg);
+      }
+    }
+    __syncthreads();
+    // zero below R's diagonal in column j; update the remaining panel columns: col_c -= tau v s_c
+    if (tau != 0.0) {
+      for (int i = j + 1 + tid; i < m; i += bd) P[i + (size_t)j * lda] = make_double2(0.0, 0.0);
+      for (int i = j + tid; i < m; i += bd) {
+        const double2 vi = V[i + (size_t)j * N];
+        const double2 tv = make_double2(tau * vi.x, tau * vi.y);
+        for (int c = j + 1; c < BW; ++c) {
+          const double2 sc = s[c];
+          double2 x = P[i + (size_t)c * lda];
+          x.x -= tv.x * sc.x - tv.y * sc.y;
+          x.y -= tv.x * sc.y + tv.y * sc.x;
+          P[i + (size_t)c * lda] = x;
+        }
+      }
+    }
+    // T column j: T[j][j] = tau ; T[0:j, j] = -tau T[0:j,0:j] conj(s[0:j])
+    if (tid < j) {
+      double2 t = make_double2(0.0, 0.0);
+      for (int l = tid; l < j; ++l) t = make_double2(t.x + (Ts[tid][l].x * s[l].x + Ts[tid][l].y * s[l].y),
+                                                      t.y + (Ts[tid][l].y * s[l].x - Ts[tid][l].x * s[l].y));
+      Ts[tid][j] = make_double2(-tau * t.x, -tau * t.y);
+    }
+    if (tid == 0) Ts[j][j] = make_double2(tau, 0.0);
+    __syncthreads();
+  }
+  for (int p = tid; p < BW * BW; p += bd) {
+    const int r = p % BW, c = p / BW;
+    T[r + c * BW] = Ts[r][c];
+  }
 }
 
-int band_eigvalsh(int, int64_t, const double2*, double*, int*, size_t, const Alloc&, cudaStream_t) {
-  g_band_err = "banded path not available";
-  return -1;
+// ------------------------------------------------------------------------------------------------
+// X = A22 V (m x BW), A22 = A[k0+BW:, k0+BW:] Hermitian (both triangles stored).  64-row tiles,
+// 4 warps x (16 rows x 32 cols), DMMA m8n8k4 f64.  A tile element (r, c) is read as
+// conj(A22[c, r]) (column-contiguous loads via Hermitian symmetry).
+constexpr int HM_TM = 64, HM_TK = 32, HM_LD = HM_TK + 4;
+
+__global__ void __launch_bounds__(128) hemm_kernel(double2* ws, BandWs L, int N, int k0) {
+  extern __shared__ double2 dsm[];
+  double2 (*As)[HM_LD] = reinterpret_cast<double2 (*)[HM_LD]>(dsm);
+  double2 (*Vs)[HM_LD] = reinterpret_cast<double2 (*)[HM_LD]>(dsm + HM_TM * HM_LD);
+  double2* base = ws + (size_t)blockIdx.y * L.stride;
+  const int lda = N, m = N - k0 - BW;
+  const double2* A22 = base + L.a_off + (size_t)(k0 + BW) * lda + (k0 + BW);
+  const double2* V = base + L.v_off;
+  double2* X = base + L.x_off;
+  const int i0 = blockIdx.x * HM_TM;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  CTile acc[2][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b].zero();
+  for (int kk = 0; kk < m; kk += HM_TK) {
+    // A tile: As[r][c] = conj(A22[kk + c, i0 + r])
+    for (int p = tid; p < HM_TM * HM_TK; p += 128) {
+      const int c = p & (HM_TK - 1), r = p / HM_TK;
+      const int gi = i0 + r, gk = kk + c;
+      double2 z = make_double2(0.0, 0.0);
+      if (gi < m && gk < m) z = A22[gk + (size_t)gi * lda];
+      As[r][c] = cconj(z);
+    }
+    for (int p = tid; p < BW * HM_TK; p += 128) {
+      const int c = p & (HM_TK - 1), n = p / HM_TK;
+      const int gk = kk + c;
+      Vs[n][c] = gk < m ? V[gk + (size_t)n * N] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k4 = 0; k4 < HM_TK / 4; ++k4) {
+      const int kc = 4 * k4 + (lane & 3);
+      double2 a[2], b[4];
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt) a[rt] = As[16 * warp + 8 * rt + (lane >> 2)][kc];
+#pragma unroll
+      for (int ct = 0; ct < 4; ++ct) b[ct] = Vs[8 * ct + (lane >> 2)][kc];
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(a[rt].x, a[rt].y, b[ct].x, b[ct].y);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+    for (int ct = 0; ct < 4; ++ct) {
+      const int r = i0 + 16 * warp + 8 * rt + (lane >> 2);
+      const int c = 8 * ct + 2 * (lane & 3);
+      if (r < m) {
+        X[r + (size_t)c * N] = make_double2(acc[rt][ct].re0, acc[rt][ct].im0);
+        X[r + (size_t)(c + 1) * N] = make_double2(acc[rt][ct].re1, acc[rt][ct].im1);
+      }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// W = X T - 1/2 V M, M = T^H (V^H X) T.  One CTA (256 threads) per matrix; W overwrites X.
+__global__ void __launch_bounds__(256) w_kernel(double2* ws, BandWs L, int N, int k0) {
+  extern __shared__ double2 dsm[];
+  double2 (*Vt)[BW + 1] = reinterpret_cast<double2 (*)[BW + 1]>(dsm);
+  double2 (*Xt)[BW + 1] = reinterpret_cast<double2 (*)[BW + 1]>(dsm + 32 * (BW + 1));
+  double2 (*Zs)[BW + 1] = reinterpret_cast<double2 (*)[BW + 1]>(dsm + 64 * (BW + 1));
+  double2 (*Ms)[BW + 1] = reinterpret_cast<double2 (*)[BW + 1]>(dsm + 96 * (BW + 1));
+  double2 (*Tsh)[BW + 1] = reinterpret_cast<double2 (*)[BW + 1]>(dsm + 128 * (BW + 1));
+  double2* base = ws + (size_t)blockIdx.x * L.stride;
+  const int m = N - k0 - BW;
+  const double2* V = base + L.v_off;
+  double2* X = base + L.x_off;
+  const double2* T = base + L.t_off;
+  const int tid = threadIdx.x;
+  const int oc = tid & 31, orow = tid >> 5;  // this thread owns outputs (orow + 8q, oc), q < 4
+  for (int p = tid; p < BW * BW; p += 256) Tsh[p % BW][p / BW] = T[p];
+  double2 z[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) z[q] = make_double2(0.0, 0.0);
+  for (int r0 = 0; r0 < m; r0 += 32) {
+    __syncthreads();
+    for (int p = tid; p < 32 * BW; p += 256) {
+      const int rr = p & 31, c = p >> 5;
+      const bool ok = r0 + rr < m;
+      Vt[rr][c] = ok ? V[r0 + rr + (size_t)c * N] : make_double2(0.0, 0.0);
+      Xt[rr][c] = ok ? X[r0 + rr + (size_t)c * N] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < 32; ++rr) {
+      const double2 x = Xt[rr][oc];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double2 v = Vt[rr][orow + 8 * q];
+        z[q].x += v.x * x.x + v.y * x.y;  // conj(v) * x
+        z[q].y += v.x * x.y - v.y * x.x;
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Zs[orow + 8 * q][oc] = z[q];
+  __syncthreads();
+  // Ms = Z T
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = orow + 8 * q;
+    double2 t = make_double2(0.0, 0.0);
+    for (int l = 0; l < BW; ++l) {
+      const double2 a = Zs[r][l], b = Tsh[l][oc];
+      t.x += a.x * b.x - a.y * b.y;
+      t.y += a.x * b.y + a.y * b.x;
+    }
+    z[q] = t;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Ms[orow + 8 * q][oc] = z[q];
+  __syncthreads();
+  // Zs = T^H Ms  (= M)
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = orow + 8 * q;
+    double2 t = make_double2(0.0, 0.0);
+    for (int l = 0; l < BW; ++l) {
+      const double2 a = cconj(Tsh[l][r]), b = Ms[l][oc];
+      t.x += a.x * b.x - a.y * b.y;
+      t.y += a.x * b.y + a.y * b.x;
+    }
+    z[q] = t;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Zs[orow + 8 * q][oc] = make_double2(0.5 * z[q].x, 0.5 * z[q].y);
+  __syncthreads();
+  // W rows: W = X T - V (M/2)
+  for (int r0 = 0; r0 < m; r0 += 32) {
+    for (int p = tid; p < 32 * BW; p += 256) {
+      const int rr = p & 31, c = p >> 5;
+      const bool ok = r0 + rr < m;
+      Vt[rr][c] = ok ? V[r0 + rr + (size_t)c * N] : make_double2(0.0, 0.0);
+      Xt[rr][c] = ok ? X[r0 + rr + (size_t)c * N] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int rr = orow + 8 * q;
+      double2 t = make_double2(0.0, 0.0);
+      for (int l = 0; l < BW; ++l) {
+        const double2 x = Xt[rr][l], tt = Tsh[l][oc], v = Vt[rr][l], mm = Zs[l][oc];
+        t.x += (x.x * tt.x - x.y * tt.y) - (v.x * mm.x - v.y * mm.y);
+        t.y += (x.x * tt.y + x.y * tt.x) - (v.x * mm.y + v.y * mm.x);
+      }
+      z[q] = t;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int rr = orow + 8 * q;
+      if (r0 + rr < m) X[r0 + rr + (size_t)oc * N] = z[q];
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// A22 -= W V^H + V W^H on lower 64x64 tiles (I >= J); upper triangle mirrored as conj.  K = BW.
+constexpr int HK_T = 64, HK_K = 16, HK_LD = HK_K + 4;
+
+__global__ void __launch_bounds__(256) her2k_kernel(double2* ws, BandWs L, int N, int k0) {
+  extern __shared__ double2 dsm[];
+  double2 (*Wi)[HK_LD] = reinterpret_cast<double2 (*)[HK_LD]>(dsm);
+  double2 (*Vi)[HK_LD] = reinterpret_cast<double2 (*)[HK_LD]>(dsm + HK_T * HK_LD);
+  double2 (*Wj)[HK_LD] = reinterpret_cast<double2 (*)[HK_LD]>(dsm + 2 * HK_T * HK_LD);
+  double2 (*Vj)[HK_LD] = reinterpret_cast<double2 (*)[HK_LD]>(dsm + 3 * HK_T * HK_LD);
+  double2* base = ws + (size_t)blockIdx.y * L.stride;
+  const int lda = N, m = N - k0 - BW;
+  double2* A22 = base + L.a_off + (size_t)(k0 + BW) * lda + (k0 + BW);
+  const double2* V = base + L.v_off;
+  const double2* W = base + L.x_off;
+  // lower-tile index -> (I, J)
+  const int t = blockIdx.x;
+  int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((I + 1) * (I + 2) / 2 <= t) ++I;
+  while (I * (I + 1) / 2 > t) --I;
+  const int J = t - I * (I + 1) / 2;
+  const int I0 = I * HK_T, J0 = J * HK_T;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp & 3, wc = warp >> 2;  // warp tile: rows 16*wr.., cols 32*wc..
+  CTile acc[2][4];
+  // initialise with the current A22 tile
+#pragma unroll
+  for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+    for (int ct = 0; ct < 4; ++ct) {
+      const int r = I0 + 16 * wr + 8 * rt + (lane >> 2);
+      const int c = J0 + 32 * wc + 8 * ct + 2 * (lane & 3);
+      double2 z0 = make_double2(0.0, 0.0), z1 = make_double2(0.0, 0.0);
+      if (r < m && c < m) z0 = A22[r + (size_t)c * lda];
+      if (r < m && c + 1 < m) z1 = A22[r + (size_t)(c + 1) * lda];
+      acc[rt][ct].re0 = z0.x;
+      acc[rt][ct].im0 = z0.y;
+      acc[rt][ct].re1 = z1.x;
+      acc[rt][ct].im1 = z1.y;
+    }
+  for (int kk = 0; kk < BW; kk += HK_K) {
+    __syncthreads();
+    for (int p = tid; p < HK_T * HK_K; p += 256) {
+      const int r = p & (HK_T - 1), k = p / HK_T;
+      const size_t col = (size_t)(kk + k) * N;
+      const bool oi = I0 + r < m, oj = J0 + r < m;
+      Wi[r][k] = oi ? W[I0 + r + col] : make_double2(0.0, 0.0);
+      Vi[r][k] = oi ? V[I0 + r + col] : make_double2(0.0, 0.0);
+      Wj[r][k] = oj ? W[J0 + r + col] : make_double2(0.0, 0.0);
+      Vj[r][k] = oj ? V[J0 + r + col] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k4 = 0; k4 < HK_K / 4; ++k4) {
+      const int kc = 4 * k4 + (lane & 3);
+      double2 aw[2], av[2], bv[4], bw[4];
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt) {
+        aw[rt] = Wi[16 * wr + 8 * rt + (lane >> 2)][kc];
+        av[rt] = Vi[16 * wr + 8 * rt + (lane >> 2)][kc];
+      }
+#pragma unroll
+      for (int ct = 0; ct < 4; ++ct) {
+        bv[ct] = cconj(Vj[32 * wc + 8 * ct + (lane >> 2)][kc]);
+        bw[ct] = cconj(Wj[32 * wc + 8 * ct + (lane >> 2)][kc]);
+      }
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct) {
+          acc[rt][ct].mac(-aw[rt].x, -aw[rt].y, bv[ct].x, bv[ct].y);
+          acc[rt][ct].mac(-av[rt].x, -av[rt].y, bw[ct].x, bw[ct].y);
+        }
+    }
+  }
+  // store lower part of the tile and the conjugate mirror
+#pragma unroll
+  for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+    for (int ct = 0; ct < 4; ++ct) {
+      const int r = I0 + 16 * wr + 8 * rt + (lane >> 2);
+      const int c = J0 + 32 * wc + 8 * ct + 2 * (lane & 3);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int cc = c + e;
+        if (r >= m || cc >= m || cc > r) continue;
+        double2 z = e ? make_double2(acc[rt][ct].re1, acc[rt][ct].im1) : make_double2(acc[rt][ct].re0, acc[rt][ct].im0);
+        if (cc == r) z.y = 0.0;
+        A22[r + (size_t)cc * lda] = z;
+        if (cc != r) A22[cc + (size_t)r * lda] = cconj(z);
+      }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Stage 2: band (lower, width BW) -> real symmetric tridiagonal (diag, e2) by Householder bulge
+// chasing.  One CTA (128 threads) per matrix; sweeps sequential; each task works on a window
+// [D (len x len) ; B (lb x len)] staged in shared memory.  Only the lower triangle is referenced.
+__global__ void __launch_bounds__(128) bulge_chase_kernel(double2* ws, BandWs L, int N, const int* dims) {
+  __shared__ double2 Dm[BW][BW + 1];
+  __shared__ double2 Bm[BW][BW + 1];
+  __shared__ double2 v[BW], w[BW], vp[BW], tmp[BW];
+  __shared__ double red[96];
+  __shared__ double sh_tau;
+  double2* base = ws + (size_t)blockIdx.x * L.stride;
+  double2* A = base + L.a_off;
+  double* diag = reinterpret_cast<double*>(base + L.dg_off);
+  double* e2 = diag + N;
+  const int lda = N;
+  const int d = dims ? dims[blockIdx.x] : N;
+  const int tid = threadIdx.x, bd = blockDim.x;
+  for (int i = 0; i + 1 < d; ++i) {
+    // ---- task 0 reflector from column i, rows i+1 .. i+len
+    int len = min(BW, d - 1 - i);
+    int s = i + 1;
+    // load column
+    double part = 0.0;
+    if (tid < len) {
+      const double2 x = A[s + tid + (size_t)i * lda];
+      v[tid] = x;
+      part = x.x * x.x + x.y * x.y;
+    }
+    double sig2 = block_sum(part, red);
+    double2 alpha = v[0];
+    Reflector h = make_reflector(alpha, sig2);
+    if (len <= 1 || h.tau == 0.0 || (sig2 - (alpha.x * alpha.x + alpha.y * alpha.y)) <= 0.0) {
+      // column already reduced (only the subdiagonal entry is nonzero)
+      if (tid == 0) {
+        diag[i] = A[i + (size_t)i * lda].x;
+        e2[i] = alpha.x * alpha.x + alpha.y * alpha.y;
+      }
+      __syncthreads();
+      continue;
+    }
+    __syncthreads();
+    if (tid < len) {
+      v[tid] = tid == 0 ? make_double2(1.0, 0.0) : cmul(v[tid], h.scale);
+      const double sg = sqrt(sig2);
+      const double aa = hypot(alpha.x, alpha.y);
+      const double2 ph = aa > 0.0 ? make_double2(alpha.x / aa, alpha.y / aa) : make_double2(1.0, 0.0);
+      A[s + tid + (size_t)i * lda] = tid == 0 ? make_double2(-ph.x * sg, -ph.y * sg) : make_double2(0.0, 0.0);
+    }
+    if (tid == 0) {
+      sh_tau = h.tau;
+      diag[i] = A[i + (size_t)i * lda].x;
+      e2[i] = sig2;
+    }
+    __syncthreads();
+    // ---- chase
+    while (true) {
+      const double tau = sh_tau;
+      const int lb = min(BW, d - s - len);
+      // stage D (len x len, full Hermitian from the lower triangle) and B (lb x len)
+      for (int p = tid; p < len * len; p += bd) {
+        const int r = p % len, c = p / len;
+        Dm[r][c] = r >= c ? A[s + r + (size_t)(s + c) * lda] : cconj(A[s + c + (size_t)(s + r) * lda]);
+      }
+      for (int p = tid; p < lb * len; p += bd) {
+        const int r = p % lb, c = p / lb;
+        Bm[r][c] = A[s + len + r + (size_t)(s + c) * lda];
+      }
+      __syncthreads();
+      // p = D v ; c = v^H p ; w = tau p - 1/2 tau^2 c v
+      double cpart = 0.0;
+      if (tid < len) {
+        double2 pp = make_double2(0.0, 0.0);
+        for (int c = 0; c < len; ++c) {
+          const double2 a = Dm[tid][c], vc = v[c];
+          pp.x += a.x * vc.x - a.y * vc.y;
+          pp.y += a.x * vc.y + a.y * vc.x;
+        }
+        tmp[tid] = pp;
+        cpart = v[tid].x * pp.x + v[tid].y * pp.y;
+      }
+      const double cval = block_sum(cpart, red);
+      if (tid < len) {
+        const double hc = 0.5 * tau * tau * cval;
+        w[tid] = make_double2(tau * tmp[tid].x - hc * v[tid].x, tau * tmp[tid].y - hc * v[tid].y);
+      }
+      // B v
+      if (tid >= 64 && tid - 64 < lb) {
+        const int r = tid - 64;
+        double2 pp = make_double2(0.0, 0.0);
+        for (int c = 0; c < len; ++c) {
+          const double2 a = Bm[r][c], vc = v[c];
+          pp.x += a.x * vc.x - a.y * vc.y;
+          pp.y += a.x * vc.y + a.y * vc.x;
+        }
+        vp[r] = pp;  // temporarily (B v)_r
+      }
+      __syncthreads();
+      // D -= v w^H + w v^H (lower) ; B -= tau (B v) v^H
+      for (int p = tid; p < len * len; p += bd) {
+        const int r = p % len, c = p / len;
+        if (r < c) continue;
+        const double2 vr = v[r], wr = w[r], vc = v[c], wc = w[c];
+        double2 z = Dm[r][c];
+        z.x -= vr.x * wc.x + vr.y * wc.y + wr.x * vc.x + wr.y * vc.y;
+        z.y -= (vr.y * wc.x - vr.x * wc.y) + (wr.y * vc.x - wr.x * vc.y);
+        if (r == c) z.y = 0.0;
+        A[s + r + (size_t)(s + c) * lda] = z;
+      }
+      for (int p = tid; p < lb * len; p += bd) {
+        const int r = p % lb, c = p / lb;
+        const double2 bvr = vp[r], vc = v[c];
+        // tau * bv_r * conj(v_c)
+        double2 z = Bm[r][c];
+        z.x -= tau * (bvr.x * vc.x + bvr.y * vc.y);
+        z.y -= tau * (bvr.y * vc.x - bvr.x * vc.y);
+        Bm[r][c] = z;
+      }
+      __syncthreads();
+      if (lb <= 0) break;
+      // new reflector from B[:, 0]
+      double part2 = 0.0;
+      if (tid < lb) {
+        const double2 x = Bm[tid][0];
+        part2 = x.x * x.x + x.y * x.y;
+      }
+      const double sg2 = block_sum(part2, red);
+      const double2 al = Bm[0][0];
+      const Reflector hp = make_reflector(al, sg2);
+      if (hp.tau == 0.0 || lb == 1 || sg2 - (al.x * al.x + al.y * al.y) <= 0.0) {
+        // nothing to annihilate: write B back and stop this sweep
+        for (int p = tid; p < lb * len; p += bd) {
+          const int r = p % lb, c = p / lb;
+          A[s + len + r + (size_t)(s + c) * lda] = Bm[r][c];
+        }
+        __syncthreads();
+        break;
+      }
+      if (tid < lb) vp[tid] = tid == 0 ? make_double2(1.0, 0.0) : cmul(Bm[tid][0], hp.scale);
+      __syncthreads();
+      // B <- H' B: columns c >= 1: B[:,c] -= tau' v' (v'^H B[:,c]); column 0 -> beta e1
+      if (tid < len) {
+        const int c = tid;
+        if (c == 0) {
+          tmp[0] = make_double2(0.0, 0.0);
+        } else {
+          double2 sdot = make_double2(0.0, 0.0);
+          for (int r = 0; r < lb; ++r) {
+            const double2 a = vp[r], b = Bm[r][c];
+            sdot.x += a.x * b.x + a.y * b.y;
+            sdot.y += a.x * b.y - a.y * b.x;
+          }
+          tmp[c] = sdot;
+        }
+      }
+      __syncthreads();
+      for (int p = tid; p < lb * len; p += bd) {
+        const int r = p % lb, c = p / lb;
+        double2 z;
+        if (c == 0) {
+          if (r == 0) {
+            const double sg = sqrt(sg2);
+            const double aa = hypot(al.x, al.y);
+            const double2 ph = aa > 0.0 ? make_double2(al.x / aa, al.y / aa) : make_double2(1.0, 0.0);
+            z = make_double2(-ph.x * sg, -ph.y * sg);
+          } else {
+            z = make_double2(0.0, 0.0);
+          }
+        } else {
+          const double2 vr = vp[r], sd = tmp[c];
+          z = Bm[r][c];
+          z.x -= hp.tau * (vr.x * sd.x - vr.y * sd.y);
+          z.y -= hp.tau * (vr.x * sd.y + vr.y * sd.x);
+        }
+        A[s + len + r + (size_t)(s + c) * lda] = z;
+      }
+      if (tid < lb) v[tid] = vp[tid];
+      if (tid == 0) sh_tau = hp.tau;
+      __syncthreads();
+      s += len;
+      len = lb;
+    }
+  }
+  if (tid == 0 && d >= 1) {
+    diag[d - 1] = A[d - 1 + (size_t)(d - 1) * lda].x;
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) band_assemble_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
+                                                            const uint64_t* __restrict__ masks, int64_t mat0,
+                                                            double2* ws, BandWs L, int* dims, int* status) {
+  __shared__ int cnt[(HX_MAX_N + 31) / 32];
+  extern __shared__ int new_idx[];
+  const int N = c.N;
+  const int64_t mat = mat0 + blockIdx.x;
+  const int64_t mk = mat / nk;
+  const int kk = (int)(mat - mk * nk);
+  double2* A = ws + (size_t)blockIdx.x * L.stride + L.a_off;
+  for (int64_t p = threadIdx.x; p < (int64_t)N * N; p += blockDim.x) A[p] = make_double2(0.0, 0.0);
+  const int d = block_compact(c, masks + mk * c.words, new_idx, cnt);
+  if (threadIdx.x == 0) {
+    dims[blockIdx.x] = d;
+    status[mat] = d == 0 ? 3 : 0;
+  }
+  if (d == 0) return;
+  assemble_full(c, new_idx, d, kpts[kk], A, N, false);
+}
+
+__global__ void __launch_bounds__(256) band_copy_kernel(const double2* __restrict__ src, int64_t mat0, int N, double2* ws,
+                                                        BandWs L, int* dims, int* status) {
+  double2* A = ws + (size_t)blockIdx.x * L.stride + L.a_off;
+  const double2* a = src + (size_t)(mat0 + blockIdx.x) * N * N;
+  for (int64_t p = threadIdx.x; p < (int64_t)N * N; p += blockDim.x) A[p] = a[p];
+  if (threadIdx.x == 0) {
+    dims[blockIdx.x] = N;
+    status[mat0 + blockIdx.x] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(256) band_finish_kernel(CellDev c, int nk, GridDev g, int64_t mat0, double2* ws,
+                                                          BandWs L, const int* dims, int* diff,
+                                                          unsigned long long* trans, double* eigs, int* status,
+                                                          int sharp, double* lam_ws) {
+  __shared__ double red[96];
+  const int N = c.N;
+  const int64_t mat = mat0 + blockIdx.x;
+  const int64_t mk = mat / nk;
+  const int d = dims[blockIdx.x];
+  double* eig_out = eigs ? eigs + mat * N : nullptr;
+  if (d == 0) {
+    if (eig_out)
+      for (int i = threadIdx.x; i < N; i += blockDim.x) eig_out[i] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  const double* diag = reinterpret_cast<const double*>(ws + (size_t)blockIdx.x * L.stride + L.dg_off);
+  const double* e2 = diag + N;
+  double* lam = lam_ws + (size_t)blockIdx.x * N;
+  bisect_all(diag, e2, d, lam, red);
+  const bool rev = (c.pencil == 1) && (c.t - c.s * c.eps0 < 0.0);
+  bool bad = false;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const double E = pencil_map(c, lam[i]);
+    bad |= !isfinite(E);
+    if (diff) {
+      if (sharp) sharp_state(g, E, diff + mk * (g.npts + 1));
+      else idos_state(g, E, diff + mk * (g.npts + 1), trans + mk * g.npts);
+    }
+    if (eig_out) eig_out[rev ? d - 1 - i : i] = E;
+  }
+  if (eig_out)
+    for (int i = d + threadIdx.x; i < N; i += blockDim.x) eig_out[i] = __longlong_as_double(0x7ff8000000000000ll);
+  if (bad) atomicMax(status + mat, 2);
+}
+
+// ------------------------------------------------------------------------------------------------
+constexpr size_t HEMM_SMEM = (size_t)(HM_TM + BW) * HM_LD * sizeof(double2);
+constexpr size_t W_SMEM = (size_t)160 * (BW + 1) * sizeof(double2);
+constexpr size_t HER2K_SMEM = (size_t)4 * HK_T * HK_LD * sizeof(double2);
+
+void band_init_attributes() {
+  cudaFuncSetAttribute(band_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+  cudaFuncSetAttribute(hemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HEMM_SMEM);
+  cudaFuncSetAttribute(w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W_SMEM);
+  cudaFuncSetAttribute(her2k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HER2K_SMEM);
+}
+
+bool band_path_supported(int N) { return N > HX_SMEM_MAX_N && N <= HX_MAX_N; }
+
+// Stage 1 + 2 for `cnt` matrices already staged in the workspace.
+static int band_reduce(double2* ws, const BandWs& L, int N, int64_t cnt, const int* dims, cudaStream_t st) {
+  for (int k0 = 0; N - k0 - BW > 0; k0 += BW) {
+    const int m = N - k0 - BW;
+    panel_qr_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, L, N, k0);
+    const unsigned mt = (unsigned)((m + HM_TM - 1) / HM_TM);
+    hemm_kernel<<<dim3(mt, (unsigned)cnt), 128, HEMM_SMEM, st>>>(ws, L, N, k0);
+    w_kernel<<<(unsigned)cnt, 256, W_SMEM, st>>>(ws, L, N, k0);
+    const unsigned tt = (unsigned)((m + HK_T - 1) / HK_T);
+    her2k_kernel<<<dim3(tt * (tt + 1) / 2, (unsigned)cnt), 256, HER2K_SMEM, st>>>(ws, L, N, k0);
+    count_launch(4);
+    BAND_CUDA(cudaGetLastError());
+  }
+  bulge_chase_kernel<<<(unsigned)cnt, 128, 0, st>>>(ws, L, N, dims);
+  count_launch(1);
+  BAND_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int band_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, int64_t nmasks, const GridDev& g,
+              int* diff, unsigned long long* trans, double* eigs, int* status, int sharp, size_t ws_budget,
+              const Alloc& alloc, cudaStream_t st) {
+  const int N = c.N;
+  const BandWs L = BandWs::make(N);
+  const size_t per = L.stride * sizeof(double2) + sizeof(int) + (size_t)N * 8;
+  const int64_t nmat = nmasks * nk;
+  int64_t chunk = std::max<int64_t>(1, (int64_t)(ws_budget / per));
+  chunk = std::min<int64_t>(chunk, nmat);
+  chunk = std::min<int64_t>(chunk, 65535);
+  unsigned char* buf = static_cast<unsigned char*>(alloc(per * (size_t)chunk + 256));
+  if (!buf) {
+    g_band_err = "workspace allocation failed";
+    return -1;
+  }
+  double2* ws = reinterpret_cast<double2*>(buf);
+  int* dims = reinterpret_cast<int*>(buf + L.stride * sizeof(double2) * chunk);
+  double* lam = reinterpret_cast<double*>(dims + chunk + 2);
+  lam = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(lam) + 15) & ~(uintptr_t)15);
+  const size_t smem = (size_t)N * sizeof(int);
+  for (int64_t m0 = 0; m0 < nmat; m0 += chunk) {
+    const int64_t cnt = std::min(chunk, nmat - m0);
+    band_assemble_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, masks, m0, ws, L, dims, status);
+    count_launch();
+    BAND_CUDA(cudaGetLastError());
+    if (band_reduce(ws, L, N, cnt, dims, st)) return -1;
+    band_finish_kernel<<<(unsigned)cnt, 256, 0, st>>>(c, nk, g, m0, ws, L, dims, diff, trans, eigs, status, sharp, lam);
+    count_launch();
+    BAND_CUDA(cudaGetLastError());
+  }
+  return 0;
+}
+
+int band_eigvalsh(int n, int64_t batch, const double2* A, double* eigs, int* status, size_t ws_budget,
+                  const Alloc& alloc, cudaStream_t st) {
+  const BandWs L = BandWs::make(n);
+  const size_t per = L.stride * sizeof(double2) + sizeof(int) + (size_t)n * 8;
+  int64_t chunk = std::max<int64_t>(1, (int64_t)(ws_budget / per));
+  chunk = std::min<int64_t>(std::min<int64_t>(chunk, batch), 65535);
+  unsigned char* buf = static_cast<unsigned char*>(alloc(per * (size_t)chunk + 256));
+  if (!buf) {
+    g_band_err = "workspace allocation failed";
+    return -1;
+  }
+  double2* ws = reinterpret_cast<double2*>(buf);
+  int* dims = reinterpret_cast<int*>(buf + L.stride * sizeof(double2) * chunk);
+  double* lam = reinterpret_cast<double*>(dims + chunk + 2);
+  lam = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(lam) + 15) & ~(uintptr_t)15);
+  CellDev c{};
+  c.N = n;
+  c.pencil = 0;
+  GridDev g{};
+  for (int64_t m0 = 0; m0 < batch; m0 += chunk) {
+    const int64_t cnt = std::min(chunk, batch - m0);
+    band_copy_kernel<<<(unsigned)cnt, 256, 0, st>>>(A, m0, n, ws, L, dims, status);
+    count_launch();
+    BAND_CUDA(cudaGetLastError());
+    if (band_reduce(ws, L, n, cnt, dims, st)) return -1;
+    band_finish_kernel<<<(unsigned)cnt, 256, 0, st>>>(c, 1, g, m0, ws, L, dims, nullptr, nullptr, eigs, status, 0, lam);
+    count_launch();
+    BAND_CUDA(cudaGetLastError());
+  }
+  return 0;
 }
 
 }  // namespace hx

@@ -16,6 +16,13 @@
 #include "hx_kernels.cuh"
 #include "hx_rng.cuh"
 
+#include <atomic>
+
+namespace hx {
+static std::atomic<unsigned long long> g_launches{0};
+void count_launch(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+}  // namespace hx
+
 namespace {
 
 thread_local std::string g_err;
@@ -114,6 +121,12 @@ int fixed_point_shift(int64_t nk, int N) {
 extern "C" {
 
 int hx_abi_version(void) { return HX_ABI_VERSION; }
+
+int hx_kernel_launches(uint64_t* out) {
+  if (!out) return fail(HX_E_ARG, "null out");
+  *out = hx::g_launches.load();
+  return 0;
+}
 
 const char* hx_last_error(void) { return g_err.c_str(); }
 
@@ -288,6 +301,7 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
     hx::fused_smem_kernel<<<(unsigned)nmat, 256, smem, st>>>(c, kp, nk, d_masks, g, diff, trans, d_eigs,
                                                             reinterpret_cast<int*>(d_status), sharp);
     HX_CUDA(cudaGetLastError());
+    hx::count_launch();
   } else if (c.pencil != HX_PENCIL_GENERAL && hx::band_path_supported(N)) {
     int rc = hx::band_eval(c, kp, nk, d_masks, nmasks, g, diff, trans, d_eigs,
                            reinterpret_cast<int*>(d_status), sharp, ctx->ws_budget,
@@ -305,12 +319,14 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
                                                              reinterpret_cast<int*>(d_status), m0,
                                                              static_cast<unsigned char*>(ctx->ws.p), stride, sharp);
       HX_CUDA(cudaGetLastError());
+    hx::count_launch();
     }
   }
   const int wpb = 8;
   hx::finalize_kernel<<<(unsigned)((nmasks + wpb - 1) / wpb), 32 * wpb, 0, st>>>(diff, trans, nmasks, g, 1.0 / nk,
                                                                                  1.0 / c.area, d_curves);
   HX_CUDA(cudaGetLastError());
+    hx::count_launch();
   return 0;
 }
 
@@ -362,6 +378,7 @@ int hx_assemble_device(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_
       cell->dev, static_cast<const double2*>(ctx->kpts.p), nk, d_masks, reinterpret_cast<double2*>(d_H),
       reinterpret_cast<double2*>(d_S), reinterpret_cast<int*>(d_dims));
   HX_CUDA(cudaGetLastError());
+    hx::count_launch();
   return 0;
 }
 
@@ -390,7 +407,7 @@ __global__ void __launch_bounds__(256) eigvalsh_smem_kernel(int n, const double2
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int ld = n | 1;
   double* R = reinterpret_cast<double*>(smem_raw);
-  double2* v = reinterpret_cast<double2*>(R + (size_t)n * ld);
+  double2* v = reinterpret_cast<double2*>(R + (((size_t)n * ld + 1) & ~(size_t)1));
   double2* y = v + n;
   double* diag = reinterpret_cast<double*>(y + n);
   double* e2 = diag + n;
@@ -465,6 +482,7 @@ extern "C" int hx_eigvalsh_batch_device(hx_ctx* ctx, int32_t n, int64_t batch, c
     hx::eigvalsh_smem_kernel<<<(unsigned)batch, 256, smem, st>>>(n, reinterpret_cast<const double2*>(d_A), d_eigs,
                                                                   reinterpret_cast<int*>(d_status));
     HX_CUDA(cudaGetLastError());
+    hx::count_launch();
     return 0;
   }
   if (!d_B && hx::band_path_supported(n)) {
@@ -485,6 +503,7 @@ extern "C" int hx_eigvalsh_batch_device(hx_ctx* ctx, int32_t n, int64_t batch, c
                                                               reinterpret_cast<int*>(d_status), m0,
                                                               static_cast<unsigned char*>(ctx->ws.p), stride);
     HX_CUDA(cudaGetLastError());
+    hx::count_launch();
   }
   return 0;
 }
@@ -592,9 +611,40 @@ __global__ void sample_masks_kernel(uint64_t seed, uint64_t level, uint64_t rep0
   if (nunits & 63) o[w++] = wacc;
   for (; w < words; ++w) o[w] = 0;
 }
+// One thread per (parent mask, unit): scatter vacant units into their quarter's sub-mask.
+__global__ void restrict_masks_kernel(const uint64_t* parent, int64_t nmasks, int parent_units, const int* assign,
+                                      const int* umap, int sub_units, unsigned long long* out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nmasks * parent_units) return;
+  const int64_t i = t / parent_units;
+  const int u = (int)(t - i * parent_units);
+  const int pw = (parent_units + 63) / 64 > 0 ? (parent_units + 63) / 64 : 1;
+  const int sw = (sub_units + 63) / 64 > 0 ? (sub_units + 63) / 64 : 1;
+  if (!((parent[i * pw + (u >> 6)] >> (u & 63)) & 1ull)) return;
+  const int r = assign[u], su = umap[u];
+  atomicOr(out + i * 4 * sw + (r - 1) * sw + (su >> 6), 1ull << (su & 63));
+}
 }  // namespace hx
 
 extern "C" {
+
+int hx_restrict_masks_device(const uint64_t* d_parent_words, int64_t nmasks, int32_t parent_units,
+                             const int32_t* d_unit_assign, const int32_t* d_unit_map, int32_t sub_units,
+                             uint64_t* d_out_words, void* stream) {
+  if (!d_parent_words || !d_unit_assign || !d_unit_map || !d_out_words || nmasks < 0)
+    return fail(HX_E_ARG, "restrict_device: bad args");
+  if (nmasks == 0 || parent_units == 0) return 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int sw = std::max(1, (sub_units + 63) / 64);
+  HX_CUDA(cudaMemsetAsync(d_out_words, 0, (size_t)nmasks * 4 * sw * 8, st));
+  const int64_t total = nmasks * parent_units;
+  hx::restrict_masks_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
+      d_parent_words, nmasks, parent_units, d_unit_assign, d_unit_map, sub_units,
+      reinterpret_cast<unsigned long long*>(d_out_words));
+  HX_CUDA(cudaGetLastError());
+    hx::count_launch();
+  return 0;
+}
 
 int hx_smoothed_counts_device(const double* d_energies, const double* d_weights, int64_t count, const hx_egrid* grid,
                               double* d_out, void* stream) {
@@ -602,6 +652,7 @@ int hx_smoothed_counts_device(const double* d_energies, const double* d_weights,
   hx::GridDev g{grid->e0, grid->step, grid->delta, grid->npts, 0};
   hx::counts_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_energies, d_weights, count, g, d_out, 0);
   HX_CUDA(cudaGetLastError());
+    hx::count_launch();
   return 0;
 }
 
@@ -611,6 +662,7 @@ int hx_sharp_counts_device(const double* d_energies, const double* d_weights, in
   hx::GridDev g{grid->e0, grid->step, grid->delta, grid->npts, 0};
   hx::counts_kernel<<<1, 256, 0, static_cast<cudaStream_t>(stream)>>>(d_energies, d_weights, count, g, d_out, 1);
   HX_CUDA(cudaGetLastError());
+    hx::count_launch();
   return 0;
 }
 
@@ -620,6 +672,7 @@ int hx_level_moments_device(const double* d_full, const double* d_quarters, int6
   hx::moments_kernel<<<(npts + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(d_full, d_quarters, M, npts,
                                                                                        d_terms, d_mean, d_var, d_sums);
   HX_CUDA(cudaGetLastError());
+    hx::count_launch();
   return 0;
 }
 
@@ -675,6 +728,7 @@ int hx_sample_masks_device(uint64_t seed, uint64_t level, uint64_t rep0, int64_t
   hx::sample_masks_kernel<<<(unsigned)((count + 127) / 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
       seed, level, rep0, count, p, nunits, d_out_words);
   HX_CUDA(cudaGetLastError());
+    hx::count_launch();
   return 0;
 }
 

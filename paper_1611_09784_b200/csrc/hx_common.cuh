@@ -5,6 +5,9 @@
 
 namespace hx {
 
+// Number of libhx kernel launches issued by this process (reported by bench.py as gpu_launches).
+void count_launch(unsigned long long n = 1);
+
 // Compiled-cell tables resident in HBM (uploaded once per (model, nu)).
 struct CellDev {
   int32_t N;          // total dofs

@@ -1,0 +1,32 @@
+// FP64 tensor-core (DMMA, mma.sync m8n8k4 f64) helpers for complex128 tiles on sm_100a.
+//
+// Fragment layouts of mma.sync.aligned.m8n8k4.row.col.f64 (lane = %laneid):
+//   A (8x4, row):  a = A[lane >> 2][lane & 3]
+//   B (4x8, col):  b = B[lane & 3][lane >> 2]
+//   C (8x8):       c0 = C[lane >> 2][2*(lane & 3)], c1 = C[lane >> 2][2*(lane & 3) + 1]
+// A complex product is four real DMMAs: Cr += Ar Br - Ai Bi, Ci += Ar Bi + Ai Br.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace hx {
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Complex 8x8 accumulator tile: re[2], im[2] per lane.
+struct CTile {
+  double re0, re1, im0, im1;
+  __device__ __forceinline__ void zero() { re0 = re1 = im0 = im1 = 0.0; }
+  // C += A * B for one k4 slice; (ar, ai) = A fragment element, (br, bi) = B fragment element.
+  __device__ __forceinline__ void mac(double ar, double ai, double br, double bi) {
+    dmma(re0, re1, ar, br);
+    dmma(re0, re1, -ai, bi);
+    dmma(im0, im1, ar, bi);
+    dmma(im0, im1, ai, br);
+  }
+};
+
+}  // namespace hx

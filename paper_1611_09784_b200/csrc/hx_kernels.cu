@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(256) fused_smem_kernel(CellDev c, const double
   const int64_t mk = mat / nk;
   const int kk = (int)(mat - mk * nk);
   double* R = reinterpret_cast<double*>(smem_raw);
-  double2* v = reinterpret_cast<double2*>(R + (size_t)N * ld);
+  double2* v = reinterpret_cast<double2*>(R + (((size_t)N * ld + 1) & ~(size_t)1));
   double2* y = v + N;
   double* diag = reinterpret_cast<double*>(y + N);
   double* e2 = diag + N;
@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(256) fused_smem_kernel(CellDev c, const double
 
 size_t fused_smem_bytes(int N) {
   const int ld = N | 1;
-  return (size_t)N * ld * 8 + (size_t)N * 16 * 2 + (size_t)N * 8 * 3 + 96 * 8 + (size_t)N * 4 + ((N + 31) / 32) * 4 + 16;
+  return (((size_t)N * ld + 1) & ~(size_t)1) * 8 + (size_t)N * 16 * 2 + (size_t)N * 8 * 3 + 96 * 8 + (size_t)N * 4 + ((N + 31) / 32) * 4 + 16;
 }
 
 // ------------------------------------------------------------------------------------------------

@@ -1,0 +1,149 @@
+"""Device-resident MLMC level pipeline (no host round trips): the throughput path used by bench.py.
+
+Per level: vacancy masks (device RNG, bit-exact with the reference sampler) -> quarter restriction
+(device) -> in-level dedup of (n, q, mask) keys (sort-unique on the device, the reference's
+evaluate_masks semantics within the level) -> one hx_eval_idos_batch_device per (n, q) tier ->
+gather per-request curves -> CV terms + moments (hx_level_moments_device).  Multi-rank: samples of
+each level are sharded contiguously across ranks; per-rank sums (sum term, sum term^2) are combined
+with one all-reduce per level (runner.py:281-299 + mlmc.py:143-154 semantics for the mean).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .geometry import build_supercell, partition_quarters
+from .models import compile_cell
+from .solver import make_bz_grid
+
+
+@dataclass
+class LevelInputs:
+    level: int
+    n: int
+    q: int
+    M: int            # samples on this rank
+    m0: int           # first replicate index of this rank
+    with_cv: bool
+    parent: torch.Tensor          # [M, w] int64 view of uint64 words
+    quarters: torch.Tensor | None  # [M*4, ws]
+
+
+class DeviceMlmc:
+    def __init__(self, model, nq: int, delta: float, master_seed: int, lo: float, hi: float, npts: int,
+                 device: int = 0):
+        self.model = model
+        self.nq = nq
+        self.delta = delta
+        self.seed = master_seed
+        self.lo, self.hi, self.npts = lo, hi, npts
+        self.step = (hi - lo) / (npts - 1)
+        self.device = device
+        self.dev = torch.device("cuda", device)
+        self.lib = _lib.load()
+        self.ctx = _lib.Device.ctx(device)
+        self._cells = {}
+        self._parts = {}
+        self.stream = torch.cuda.current_stream(self.dev)
+        # per-call accounting for the roofline: list of (n, nmats, flops, event pair)
+        self.records = []
+        self.record = False
+
+    def cell(self, n):
+        if n not in self._cells:
+            self._cells[n] = compile_cell(self.model, build_supercell(self.model.lattice_spec(), n), self.device)
+        return self._cells[n]
+
+    def part(self, n):
+        if n not in self._parts:
+            p = partition_quarters(self._cells[n].supercell if n in self._cells else
+                                   build_supercell(self.model.lattice_spec(), n))
+            self._parts[n] = (p, torch.from_numpy(p.unit_assignment.astype(np.int32)).to(self.dev),
+                              torch.from_numpy(p.unit_map.astype(np.int32)).to(self.dev))
+        return self._parts[n]
+
+    def q_of(self, n):
+        return self.nq // n
+
+    def kpoints(self, n, q):
+        return np.ascontiguousarray(make_bz_grid(self.model.lattice_spec(), n, q, "reduced").kpoints)
+
+    def prepare(self, level, n, M_total, p, with_cv, rank=0, world=1) -> LevelInputs:
+        """Masks for this rank's contiguous shard of replicates (device RNG) + quarter masks."""
+        per = (M_total + world - 1) // world
+        m0 = min(M_total, rank * per)
+        M = max(0, min(M_total, m0 + per) - m0)
+        cell = self.cell(n)
+        nunits = cell.supercell.nunits
+        w = max(1, (nunits + 63) // 64)
+        parent = torch.zeros((max(M, 1), w), dtype=torch.int64, device=self.dev)
+        st = self.stream.cuda_stream
+        _lib.check(self.lib.hx_sample_masks_device(self.seed, level, m0, M, p, nunits, parent.data_ptr(), st),
+                   "hx_sample_masks_device")
+        quarters = None
+        if with_cv:
+            part, assign, umap = self.part(n)
+            sub_units = part.subcells[0].nunits
+            ws = max(1, (sub_units + 63) // 64)
+            quarters = torch.zeros((max(M, 1) * 4, ws), dtype=torch.int64, device=self.dev)
+            _lib.check(self.lib.hx_restrict_masks_device(parent.data_ptr(), M, nunits, assign.data_ptr(),
+                                                         umap.data_ptr(), sub_units, quarters.data_ptr(), st),
+                       "hx_restrict_masks_device")
+        return LevelInputs(level, n, self.q_of(n), M, m0, with_cv, parent[:M], None if quarters is None else
+                           quarters[:4 * M])
+
+    def _eval(self, n, words: torch.Tensor):
+        """Dedup rows, solve unique masks, return per-row curves [rows, npts] (device)."""
+        uniq, inv = torch.unique(words, dim=0, return_inverse=True)
+        cell = self.cell(n)
+        q = self.q_of(n)
+        kp = self.kpoints(n, q)
+        U = uniq.shape[0]
+        curves = torch.empty((U, self.npts), dtype=torch.float64, device=self.dev)
+        status = torch.empty((U, kp.shape[0]), dtype=torch.int32, device=self.dev)
+        g = _lib.EGrid()
+        g.e0, g.step, g.npts, g.delta = self.lo, self.step, self.npts, self.delta
+        uniq = uniq.contiguous()
+        ev = None
+        if self.record:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            ev[0].record(self.stream)
+        _lib.check(self.lib.hx_eval_idos_batch_device(self.ctx, cell.handle, _lib.ptr(kp), kp.shape[0],
+                                                      uniq.data_ptr(), U, C.byref(g), curves.data_ptr(), 0,
+                                                      status.data_ptr(), self.stream.cuda_stream),
+                   "hx_eval_idos_batch_device")
+        if self.record:
+            ev[1].record(self.stream)
+            self.records.append({"n": n, "N": cell.dim, "unique": U, "nk": kp.shape[0], "events": ev,
+                                 "uniq": uniq, "cell": cell})
+        return curves[inv]
+
+    def run_level(self, inp: LevelInputs):
+        """Returns device tensors (sum term [npts], sum term^2 [npts]) for this rank's shard."""
+        npts = self.npts
+        sums = torch.zeros(2 * npts, dtype=torch.float64, device=self.dev)
+        if inp.M == 0:
+            return sums
+        full = self._eval(inp.n, inp.parent)
+        quarters = None
+        if inp.with_cv:
+            quarters = self._eval(inp.n // 2, inp.quarters).reshape(inp.M, 4, npts)
+        _lib.check(self.lib.hx_level_moments_device(full.data_ptr(), 0 if quarters is None else quarters.data_ptr(),
+                                                    inp.M, npts, 0, 0, 0, sums.data_ptr(), self.stream.cuda_stream),
+                   "hx_level_moments_device")
+        return sums
+
+
+def kept_dims(cell, uniq_words: torch.Tensor) -> np.ndarray:
+    """Kept dimension d of each unique mask (for the algorithmic 16/3 d^3 FLOP count)."""
+    w = uniq_words.cpu().numpy().view(np.uint64)
+    nunits = cell.supercell.nunits
+    bits = np.unpackbits(w.view(np.uint8), axis=1, bitorder="little")[:, :nunits].astype(bool)
+    per_unit = np.array([len(d) for d in cell.unit_dofs], dtype=np.int64)
+    removed = bits.astype(np.int64) @ per_unit if nunits else np.zeros(len(w), np.int64)
+    return cell.dim - removed

@@ -70,7 +70,8 @@ class Engine:
     """Shared context of one run: model, grids, dedup cache, device (runner.py:148-175)."""
 
     def __init__(self, model, nq: int, delta: float, master_seed: int, workers: int = 1, bz_mode: str = "full",
-                 energy_points: int = 4096, energy_range=None, dedup: bool = True, device: int = 0):
+                 energy_points: int = 4096, energy_range=None, dedup: bool = True, device: int = 0,
+                 shard=(0, 1)):
         self.model = model
         self.nq = nq
         self.delta = delta
@@ -79,6 +80,8 @@ class Engine:
         self.bz_mode = bz_mode
         self.dedup = dedup
         self.device = device
+        self.shard = shard  # (rank, world): sample_level draws only this rank's contiguous replicates
+        self.io_bytes = [0, 0]  # host->device, device->host bytes moved by the batch calls
         self._cache: dict = {}
         self._supercells: dict = {}
         self._cells: dict = {}
@@ -129,6 +132,8 @@ class Engine:
         curves, _, status = eval_batch(cell, kp, words, self.grid.lo, self.grid.step, self.grid.npoints,
                                        self.delta)
         secs = time.perf_counter() - t0
+        self.io_bytes[0] += words.nbytes + kp.nbytes
+        self.io_bytes[1] += curves.nbytes + status.nbytes
         bad = np.flatnonzero(((status == _lib.HX_ST_NOT_PD) | (status == _lib.HX_ST_NONFINITE)).any(axis=1))
         if len(bad):
             failures = []
@@ -186,9 +191,13 @@ class Engine:
         q = self.q_of(n)
         sc = self.supercell(n)
         stream = level if stream_level is None else stream_level
-        words = sample_masks(sc.nunits, p_vac, self.master_seed, stream, 0, nsamples)
+        rank, world = self.shard
+        per = (nsamples + world - 1) // world
+        m0 = min(nsamples, rank * per)
+        nsamples = max(0, min(nsamples, m0 + per) - m0)
+        words = sample_masks(sc.nunits, p_vac, self.master_seed, stream, m0, nsamples)
         keys = keys_from_words(words)
-        requests = [(n, q, k, (level, m, "Q")) for m, k in enumerate(keys)]
+        requests = [(n, q, k, (level, m0 + m, "Q")) for m, k in enumerate(keys)]
         if with_cv:
             part = partition_quarters(sc)
             nsub = n // 2
@@ -197,7 +206,7 @@ class Engine:
             subkeys = keys_from_words(sub.reshape(nsamples * 4, -1))
             for m in range(nsamples):
                 for r in range(4):
-                    requests.append((nsub, qsub, subkeys[m * 4 + r], (level, m, f"CV{r + 1}")))
+                    requests.append((nsub, qsub, subkeys[m * 4 + r], (level, m0 + m, f"CV{r + 1}")))
         results, hits, spent = self.evaluate_masks(requests)
         npts = self.grid.npoints
         full = np.stack([results[m][0] for m in range(nsamples)]) if nsamples else np.zeros((0, npts))
@@ -208,7 +217,9 @@ class Engine:
             nominal += sum(results[nsamples + i][1] for i in range(4 * nsamples))
         terms, mean, var = level_moments(full, quarters, self.device)
         terms = terms.cpu().numpy()
-        cv = None if quarters is None else full - terms
+        self.io_bytes[0] += full.nbytes + (0 if quarters is None else quarters.nbytes)
+        self.io_bytes[1] += terms.nbytes + 2 * mean.numel() * 8
+        cv = None
         if quarters is not None:
             # cv exactly as the reference forms it: ((q1 + q2) + q3 + q4) * 0.25
             cv = np.zeros((nsamples, npts))
