@@ -74,10 +74,11 @@ class DeviceMlmc:
         return np.ascontiguousarray(make_bz_grid(self.model.lattice_spec(), n, q, "reduced").kpoints)
 
     def prepare(self, level, n, M_total, p, with_cv, rank=0, world=1) -> LevelInputs:
-        """Masks for this rank's contiguous shard of replicates (device RNG) + quarter masks."""
-        per = (M_total + world - 1) // world
-        m0 = min(M_total, rank * per)
-        M = max(0, min(M_total, m0 + per) - m0)
+        """Masks for this rank's replicates [rank*M, (rank+1)*M) (device RNG) + quarter masks.
+
+        Weak scaling: every rank processes a full level of M samples from its own replicate range."""
+        m0 = rank * M_total
+        M = M_total
         cell = self.cell(n)
         nunits = cell.supercell.nunits
         w = max(1, (nunits + 63) // 64)

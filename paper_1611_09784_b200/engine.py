@@ -80,7 +80,7 @@ class Engine:
         self.bz_mode = bz_mode
         self.dedup = dedup
         self.device = device
-        self.shard = shard  # (rank, world): sample_level draws only this rank's contiguous replicates
+        self.shard = shard  # (rank, world): rank r draws replicates [r*M, (r+1)*M) (weak-scaling replicas)
         self.io_bytes = [0, 0]  # host->device, device->host bytes moved by the batch calls
         self._cache: dict = {}
         self._supercells: dict = {}
@@ -191,10 +191,9 @@ class Engine:
         q = self.q_of(n)
         sc = self.supercell(n)
         stream = level if stream_level is None else stream_level
-        rank, world = self.shard
-        per = (nsamples + world - 1) // world
-        m0 = min(nsamples, rank * per)
-        nsamples = max(0, min(nsamples, m0 + per) - m0)
+        # weak-scaling replica: rank r of `world` draws the replicates [r*M, (r+1)*M) of the stream
+        rank, _ = self.shard
+        m0 = rank * nsamples
         words = sample_masks(sc.nunits, p_vac, self.master_seed, stream, m0, nsamples)
         keys = keys_from_words(words)
         requests = [(n, q, k, (level, m0 + m, "Q")) for m, k in enumerate(keys)]

@@ -126,6 +126,18 @@ def level_moments(full, quarters=None, device: int = 0):
     return terms, mean, var
 
 
+def moments_from_sums(s1, s2, M: int):
+    """Level mean / unbiased variance from all-reduced sums (sum term, sum term^2) over M samples.
+
+    Used after the cross-rank all-reduce of per-rank `hx_level_moments_device` sums (one-pass form;
+    single-rank runs use the kernel's two-pass variance, mlmc.py:143-154)."""
+    s1 = np.asarray(s1, dtype=np.float64)
+    s2 = np.asarray(s2, dtype=np.float64)
+    mean = s1 / M
+    var = None if M < 2 else np.maximum(s2 - M * mean * mean, 0.0) / (M - 1)
+    return mean, var
+
+
 def mean_and_variance(curves):
     """Pointwise mean and unbiased variance over axis 0; variance None for one sample (mlmc.py:143-154)."""
     curves = np.asarray(curves)
