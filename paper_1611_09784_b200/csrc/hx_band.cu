@@ -7,7 +7,7 @@
 //   w_kernel           W = X T - 1/2 V (T^H V^H X T)
 //   her2k_kernel       A22 -= W V^H + V W^H          (DMMA; lower tiles computed, upper mirrored)
 // so that A22 <- Q^H A22 Q with Q = I - V T V^H (the blocked two-sided update of zhetrd/zhe2hb).
-// Stage 2 (band -> tridiagonal): bulge_chase_kernel, Householder bulge chasing on the lower band.
+// Stage 2 (band -> tridiagonal): bulge_chase_pipe_kernel (hx_chase.cuh), pipelined Householder bulge chasing.
 // Then Sturm bisection + the reference IDOS functional (hx_dense.cuh) per matrix.
 //
 // Vacancies: kept dofs are compacted to the leading d x d block and the tail is exactly zero, so
@@ -22,6 +22,7 @@
 #include "hx_dense.cuh"
 #include "hx_dmma.cuh"
 #include "hx_kernels.cuh"
+#include "hx_chase.cuh"
 
 namespace hx {
 
@@ -439,193 +440,6 @@ __global__ void __launch_bounds__(256) her2k_kernel(double2* ws, BandWs L, int N
 }
 
 // ------------------------------------------------------------------------------------------------
-// Stage 2: band (lower, width BW) -> real symmetric tridiagonal (diag, e2) by Householder bulge
-// chasing.  One CTA (128 threads) per matrix; sweeps sequential; each task works on a window
-// [D (len x len) ; B (lb x len)] staged in shared memory.  Only the lower triangle is referenced.
-__global__ void __launch_bounds__(128) bulge_chase_kernel(double2* ws, BandWs L, int N, const int* dims) {
-  __shared__ double2 Dm[BW][BW + 1];
-  __shared__ double2 Bm[BW][BW + 1];
-  __shared__ double2 v[BW], w[BW], vp[BW], tmp[BW];
-  __shared__ double red[96];
-  __shared__ double sh_tau;
-  double2* base = ws + (size_t)blockIdx.x * L.stride;
-  double2* A = base + L.a_off;
-  double* diag = reinterpret_cast<double*>(base + L.dg_off);
-  double* e2 = diag + N;
-  const int lda = N;
-  const int d = dims ? dims[blockIdx.x] : N;
-  const int tid = threadIdx.x, bd = blockDim.x;
-  for (int i = 0; i + 1 < d; ++i) {
-    // ---- task 0 reflector from column i, rows i+1 .. i+len
-    int len = min(BW, d - 1 - i);
-    int s = i + 1;
-    // load column
-    double part = 0.0;
-    if (tid < len) {
-      const double2 x = A[s + tid + (size_t)i * lda];
-      v[tid] = x;
-      part = x.x * x.x + x.y * x.y;
-    }
-    double sig2 = block_sum(part, red);
-    double2 alpha = v[0];
-    Reflector h = make_reflector(alpha, sig2);
-    if (len <= 1 || h.tau == 0.0 || (sig2 - (alpha.x * alpha.x + alpha.y * alpha.y)) <= 0.0) {
-      // column already reduced (only the subdiagonal entry is nonzero)
-      if (tid == 0) {
-        diag[i] = A[i + (size_t)i * lda].x;
-        e2[i] = alpha.x * alpha.x + alpha.y * alpha.y;
-      }
-      __syncthreads();
-      continue;
-    }
-    __syncthreads();
-    if (tid < len) {
-      v[tid] = tid == 0 ? make_double2(1.0, 0.0) : cmul(v[tid], h.scale);
-      const double sg = sqrt(sig2);
-      const double aa = hypot(alpha.x, alpha.y);
-      const double2 ph = aa > 0.0 ? make_double2(alpha.x / aa, alpha.y / aa) : make_double2(1.0, 0.0);
-      A[s + tid + (size_t)i * lda] = tid == 0 ? make_double2(-ph.x * sg, -ph.y * sg) : make_double2(0.0, 0.0);
-    }
-    if (tid == 0) {
-      sh_tau = h.tau;
-      diag[i] = A[i + (size_t)i * lda].x;
-      e2[i] = sig2;
-    }
-    __syncthreads();
-    // ---- chase
-    while (true) {
-      const double tau = sh_tau;
-      const int lb = min(BW, d - s - len);
-      // stage D (len x len, full Hermitian from the lower triangle) and B (lb x len)
-      for (int p = tid; p < len * len; p += bd) {
-        const int r = p % len, c = p / len;
-        Dm[r][c] = r >= c ? A[s + r + (size_t)(s + c) * lda] : cconj(A[s + c + (size_t)(s + r) * lda]);
-      }
-      for (int p = tid; p < lb * len; p += bd) {
-        const int r = p % lb, c = p / lb;
-        Bm[r][c] = A[s + len + r + (size_t)(s + c) * lda];
-      }
-      __syncthreads();
-      // p = D v ; c = v^H p ; w = tau p - 1/2 tau^2 c v
-      double cpart = 0.0;
-      if (tid < len) {
-        double2 pp = make_double2(0.0, 0.0);
-        for (int c = 0; c < len; ++c) {
-          const double2 a = Dm[tid][c], vc = v[c];
-          pp.x += a.x * vc.x - a.y * vc.y;
-          pp.y += a.x * vc.y + a.y * vc.x;
-        }
-        tmp[tid] = pp;
-        cpart = v[tid].x * pp.x + v[tid].y * pp.y;
-      }
-      const double cval = block_sum(cpart, red);
-      if (tid < len) {
-        const double hc = 0.5 * tau * tau * cval;
-        w[tid] = make_double2(tau * tmp[tid].x - hc * v[tid].x, tau * tmp[tid].y - hc * v[tid].y);
-      }
-      // B v
-      if (tid >= 64 && tid - 64 < lb) {
-        const int r = tid - 64;
-        double2 pp = make_double2(0.0, 0.0);
-        for (int c = 0; c < len; ++c) {
-          const double2 a = Bm[r][c], vc = v[c];
-          pp.x += a.x * vc.x - a.y * vc.y;
-          pp.y += a.x * vc.y + a.y * vc.x;
-        }
-        vp[r] = pp;  // temporarily (B v)_r
-      }
-      __syncthreads();
-      // D -= v w^H + w v^H (lower) ; B -= tau (B v) v^H
-      for (int p = tid; p < len * len; p += bd) {
-        const int r = p % len, c = p / len;
-        if (r < c) continue;
-        const double2 vr = v[r], wr = w[r], vc = v[c], wc = w[c];
-        double2 z = Dm[r][c];
-        z.x -= vr.x * wc.x + vr.y * wc.y + wr.x * vc.x + wr.y * vc.y;
-        z.y -= (vr.y * wc.x - vr.x * wc.y) + (wr.y * vc.x - wr.x * vc.y);
-        if (r == c) z.y = 0.0;
-        A[s + r + (size_t)(s + c) * lda] = z;
-      }
-      for (int p = tid; p < lb * len; p += bd) {
-        const int r = p % lb, c = p / lb;
-        const double2 bvr = vp[r], vc = v[c];
-        // tau * bv_r * conj(v_c)
-        double2 z = Bm[r][c];
-        z.x -= tau * (bvr.x * vc.x + bvr.y * vc.y);
-        z.y -= tau * (bvr.y * vc.x - bvr.x * vc.y);
-        Bm[r][c] = z;
-      }
-      __syncthreads();
-      if (lb <= 0) break;
-      // new reflector from B[:, 0]
-      double part2 = 0.0;
-      if (tid < lb) {
-        const double2 x = Bm[tid][0];
-        part2 = x.x * x.x + x.y * x.y;
-      }
-      const double sg2 = block_sum(part2, red);
-      const double2 al = Bm[0][0];
-      const Reflector hp = make_reflector(al, sg2);
-      if (hp.tau == 0.0 || lb == 1 || sg2 - (al.x * al.x + al.y * al.y) <= 0.0) {
-        // nothing to annihilate: write B back and stop this sweep
-        for (int p = tid; p < lb * len; p += bd) {
-          const int r = p % lb, c = p / lb;
-          A[s + len + r + (size_t)(s + c) * lda] = Bm[r][c];
-        }
-        __syncthreads();
-        break;
-      }
-      if (tid < lb) vp[tid] = tid == 0 ? make_double2(1.0, 0.0) : cmul(Bm[tid][0], hp.scale);
-      __syncthreads();
-      // B <- H' B: columns c >= 1: B[:,c] -= tau' v' (v'^H B[:,c]); column 0 -> beta e1
-      if (tid < len) {
-        const int c = tid;
-        if (c == 0) {
-          tmp[0] = make_double2(0.0, 0.0);
-        } else {
-          double2 sdot = make_double2(0.0, 0.0);
-          for (int r = 0; r < lb; ++r) {
-            const double2 a = vp[r], b = Bm[r][c];
-            sdot.x += a.x * b.x + a.y * b.y;
-            sdot.y += a.x * b.y - a.y * b.x;
-          }
-          tmp[c] = sdot;
-        }
-      }
-      __syncthreads();
-      for (int p = tid; p < lb * len; p += bd) {
-        const int r = p % lb, c = p / lb;
-        double2 z;
-        if (c == 0) {
-          if (r == 0) {
-            const double sg = sqrt(sg2);
-            const double aa = hypot(al.x, al.y);
-            const double2 ph = aa > 0.0 ? make_double2(al.x / aa, al.y / aa) : make_double2(1.0, 0.0);
-            z = make_double2(-ph.x * sg, -ph.y * sg);
-          } else {
-            z = make_double2(0.0, 0.0);
-          }
-        } else {
-          const double2 vr = vp[r], sd = tmp[c];
-          z = Bm[r][c];
-          z.x -= hp.tau * (vr.x * sd.x - vr.y * sd.y);
-          z.y -= hp.tau * (vr.x * sd.y + vr.y * sd.x);
-        }
-        A[s + len + r + (size_t)(s + c) * lda] = z;
-      }
-      if (tid < lb) v[tid] = vp[tid];
-      if (tid == 0) sh_tau = hp.tau;
-      __syncthreads();
-      s += len;
-      len = lb;
-    }
-  }
-  if (tid == 0 && d >= 1) {
-    diag[d - 1] = A[d - 1 + (size_t)(d - 1) * lda].x;
-  }
-}
-
-// ------------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) band_assemble_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
                                                             const uint64_t* __restrict__ masks, int64_t mat0,
                                                             double2* ws, BandWs L, int* dims, int* status) {
@@ -657,41 +471,6 @@ __global__ void __launch_bounds__(256) band_copy_kernel(const double2* __restric
   }
 }
 
-__global__ void __launch_bounds__(256) band_finish_kernel(CellDev c, int nk, GridDev g, int64_t mat0, double2* ws,
-                                                          BandWs L, const int* dims, int* diff,
-                                                          unsigned long long* trans, double* eigs, int* status,
-                                                          int sharp, double* lam_ws) {
-  __shared__ double red[96];
-  const int N = c.N;
-  const int64_t mat = mat0 + blockIdx.x;
-  const int64_t mk = mat / nk;
-  const int d = dims[blockIdx.x];
-  double* eig_out = eigs ? eigs + mat * N : nullptr;
-  if (d == 0) {
-    if (eig_out)
-      for (int i = threadIdx.x; i < N; i += blockDim.x) eig_out[i] = __longlong_as_double(0x7ff8000000000000ll);
-    return;
-  }
-  const double* diag = reinterpret_cast<const double*>(ws + (size_t)blockIdx.x * L.stride + L.dg_off);
-  const double* e2 = diag + N;
-  double* lam = lam_ws + (size_t)blockIdx.x * N;
-  bisect_all(diag, e2, d, lam, red);
-  const bool rev = (c.pencil == 1) && (c.t - c.s * c.eps0 < 0.0);
-  bool bad = false;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const double E = pencil_map(c, lam[i]);
-    bad |= !isfinite(E);
-    if (diff) {
-      if (sharp) sharp_state(g, E, diff + mk * (g.npts + 1));
-      else idos_state(g, E, diff + mk * (g.npts + 1), trans + mk * g.npts);
-    }
-    if (eig_out) eig_out[rev ? d - 1 - i : i] = E;
-  }
-  if (eig_out)
-    for (int i = d + threadIdx.x; i < N; i += blockDim.x) eig_out[i] = __longlong_as_double(0x7ff8000000000000ll);
-  if (bad) atomicMax(status + mat, 2);
-}
-
 // ------------------------------------------------------------------------------------------------
 constexpr size_t HEMM_SMEM = (size_t)(HM_TM + BW) * HM_LD * sizeof(double2);
 constexpr size_t W_SMEM = (size_t)160 * (BW + 1) * sizeof(double2);
@@ -702,6 +481,14 @@ void band_init_attributes() {
   cudaFuncSetAttribute(hemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HEMM_SMEM);
   cudaFuncSetAttribute(w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W_SMEM);
   cudaFuncSetAttribute(her2k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HER2K_SMEM);
+  cudaFuncSetAttribute(bulge_chase_pipe_kernel<1, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)chase_smem_bytes<1, BW>());
+  cudaFuncSetAttribute(bulge_chase_pipe_kernel<2, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)chase_smem_bytes<2, BW>());
+  cudaFuncSetAttribute(bulge_chase_pipe_kernel<4, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)chase_smem_bytes<4, BW>());
+  cudaFuncSetAttribute(bulge_chase_pipe_kernel<11, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)chase_smem_bytes<11, BW>());
 }
 
 bool band_path_supported(int N) { return N > HX_SMEM_MAX_N && N <= HX_MAX_N; }
@@ -719,7 +506,21 @@ static int band_reduce(double2* ws, const BandWs& L, int N, int64_t cnt, const i
     count_launch(4);
     BAND_CUDA(cudaGetLastError());
   }
-  bulge_chase_kernel<<<(unsigned)cnt, 128, 0, st>>>(ws, L, N, dims);
+  // warps per matrix: enough sweeps in flight to fill ~11 warps per SM across the batch
+  const int64_t want = (148 * 11 + cnt - 1) / cnt;
+  if (want >= 6) {
+    bulge_chase_pipe_kernel<11, BW><<<(unsigned)cnt, 11 * 32, chase_smem_bytes<11, BW>(), st>>>(
+        ws, L.stride, L.a_off, L.dg_off, N, dims);
+  } else if (want >= 3) {
+    bulge_chase_pipe_kernel<4, BW><<<(unsigned)cnt, 4 * 32, chase_smem_bytes<4, BW>(), st>>>(
+        ws, L.stride, L.a_off, L.dg_off, N, dims);
+  } else if (want >= 2) {
+    bulge_chase_pipe_kernel<2, BW><<<(unsigned)cnt, 2 * 32, chase_smem_bytes<2, BW>(), st>>>(
+        ws, L.stride, L.a_off, L.dg_off, N, dims);
+  } else {
+    bulge_chase_pipe_kernel<1, BW><<<(unsigned)cnt, 32, chase_smem_bytes<1, BW>(), st>>>(
+        ws, L.stride, L.a_off, L.dg_off, N, dims);
+  }
   count_launch(1);
   BAND_CUDA(cudaGetLastError());
   return 0;
@@ -727,7 +528,7 @@ static int band_reduce(double2* ws, const BandWs& L, int N, int64_t cnt, const i
 
 int band_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, int64_t nmasks, const GridDev& g,
               int* diff, unsigned long long* trans, double* eigs, int* status, int sharp, size_t ws_budget,
-              const Alloc& alloc, cudaStream_t st) {
+              const Alloc& alloc, cudaStream_t st, RefineItem* refine, unsigned long long* refine_count) {
   const int N = c.N;
   const BandWs L = BandWs::make(N);
   const size_t per = L.stride * sizeof(double2) + sizeof(int) + (size_t)N * 8;
@@ -742,8 +543,6 @@ int band_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks
   }
   double2* ws = reinterpret_cast<double2*>(buf);
   int* dims = reinterpret_cast<int*>(buf + L.stride * sizeof(double2) * chunk);
-  double* lam = reinterpret_cast<double*>(dims + chunk + 2);
-  lam = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(lam) + 15) & ~(uintptr_t)15);
   const size_t smem = (size_t)N * sizeof(int);
   for (int64_t m0 = 0; m0 < nmat; m0 += chunk) {
     const int64_t cnt = std::min(chunk, nmat - m0);
@@ -751,8 +550,8 @@ int band_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks
     count_launch();
     BAND_CUDA(cudaGetLastError());
     if (band_reduce(ws, L, N, cnt, dims, st)) return -1;
-    band_finish_kernel<<<(unsigned)cnt, 256, 0, st>>>(c, nk, g, m0, ws, L, dims, diff, trans, eigs, status, sharp, lam);
-    count_launch();
+    launch_eig_idos(c, nk, g, m0, cnt, reinterpret_cast<const double*>(ws + L.dg_off), L.stride * 2, dims, diff,
+                    trans, eigs, status, sharp, st, refine, refine_count);
     BAND_CUDA(cudaGetLastError());
   }
   return 0;
@@ -771,8 +570,6 @@ int band_eigvalsh(int n, int64_t batch, const double2* A, double* eigs, int* sta
   }
   double2* ws = reinterpret_cast<double2*>(buf);
   int* dims = reinterpret_cast<int*>(buf + L.stride * sizeof(double2) * chunk);
-  double* lam = reinterpret_cast<double*>(dims + chunk + 2);
-  lam = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(lam) + 15) & ~(uintptr_t)15);
   CellDev c{};
   c.N = n;
   c.pencil = 0;
@@ -783,8 +580,8 @@ int band_eigvalsh(int n, int64_t batch, const double2* A, double* eigs, int* sta
     count_launch();
     BAND_CUDA(cudaGetLastError());
     if (band_reduce(ws, L, n, cnt, dims, st)) return -1;
-    band_finish_kernel<<<(unsigned)cnt, 256, 0, st>>>(c, 1, g, m0, ws, L, dims, nullptr, nullptr, eigs, status, 0, lam);
-    count_launch();
+    launch_eig_idos(c, 1, g, m0, cnt, reinterpret_cast<const double*>(ws + L.dg_off), L.stride * 2, dims, nullptr,
+                    nullptr, eigs, status, 0, st);
     BAND_CUDA(cudaGetLastError());
   }
   return 0;

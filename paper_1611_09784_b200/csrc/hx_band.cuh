@@ -6,6 +6,7 @@
 #include <functional>
 
 #include "hx_common.cuh"
+#include "hx_kernels.cuh"
 
 namespace hx {
 
@@ -18,7 +19,7 @@ const char* band_last_error();
 // IDOS batch through the banded path (pencil STANDARD or COMMUTING).
 int band_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, int64_t nmasks, const GridDev& g,
               int* diff, unsigned long long* trans, double* eigs, int* status, int sharp, size_t ws_budget,
-              const Alloc& alloc, cudaStream_t st);
+              const Alloc& alloc, cudaStream_t st, RefineItem* refine, unsigned long long* refine_count);
 
 // Eigenvalues of caller-provided Hermitian matrices (column-major complex, n x n each).
 int band_eigvalsh(int n, int64_t batch, const double2* A, double* eigs, int* status, size_t ws_budget,

@@ -63,7 +63,7 @@ struct DevBuf {
 struct hx_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  DevBuf kpts, diff, trans, ws, masks, curves, eigs, status, band;
+  DevBuf kpts, diff, trans, ws, masks, curves, eigs, status, band, tri, refine;
   size_t ws_budget = (size_t)24 << 30;  // HBM workspace budget for the global / banded paths
 };
 
@@ -166,8 +166,10 @@ int hx_ctx_create(int32_t device, hx_ctx** out) {
   size_t freeb = 0, total = 0;
   cudaMemGetInfo(&freeb, &total);
   ctx->ws_budget = std::min(ctx->ws_budget, freeb / 3);
-  cudaFuncSetAttribute(hx::fused_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)hx::fused_smem_bytes(HX_SMEM_MAX_N));
+  cudaFuncSetAttribute(hx::small_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)hx::small_tridiag_smem(HX_SMEM_MAX_N));
+  cudaFuncSetAttribute(hx::eigvalsh_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)hx::small_tridiag_smem(HX_SMEM_MAX_N));
   hx::band_init_attributes();
   *out = ctx;
   return 0;
@@ -177,7 +179,7 @@ int hx_ctx_destroy(hx_ctx* ctx) {
   if (!ctx) return 0;
   set_device(ctx);
   for (DevBuf* b : {&ctx->kpts, &ctx->diff, &ctx->trans, &ctx->ws, &ctx->masks, &ctx->curves, &ctx->eigs,
-                    &ctx->status, &ctx->band})
+                    &ctx->status, &ctx->band, &ctx->tri, &ctx->refine})
     b->release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -291,21 +293,44 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
   const double2* kp = static_cast<const double2*>(ctx->kpts.p);
   const int64_t nmat = nmasks * (int64_t)nk;
 
+  int* status = reinterpret_cast<int*>(d_status);
+  // refinement list of the two-pass eigenvalue stage (count word first, then the items)
+  hx::RefineItem* refine = nullptr;
+  unsigned long long* refine_count = nullptr;
+  auto make_refine = [&](int64_t items) -> int {
+    if (d_eigs) return 0;  // eigenvalue output requested: single full-precision pass
+    if (ctx->refine.grow(256 + (size_t)items * sizeof(hx::RefineItem))) return -1;
+    refine_count = static_cast<unsigned long long*>(ctx->refine.p);
+    refine = reinterpret_cast<hx::RefineItem*>(static_cast<unsigned char*>(ctx->refine.p) + 256);
+    return 0;
+  };
   if (c.pencil != HX_PENCIL_GENERAL && N <= HX_SMEM_MAX_N) {
-    const size_t smem = hx::fused_smem_bytes(N);
-    const int64_t chunk = 1 << 30;
+    // shared-memory tier: tridiagonalise every (mask, k) matrix, then one thread per eigenvalue
+    const size_t smem = hx::small_tridiag_smem(N);
+    int64_t chunk = std::min<int64_t>(nmat, std::max<int64_t>(1, (int64_t)((size_t)1 << 30) / (16 * N + 4)));
+    chunk = std::max<int64_t>(nk, chunk - chunk % nk);  // whole masks per chunk
+    if (ctx->tri.grow((size_t)chunk * (2 * N * 8 + 4) + 256)) return fail(HX_E_CUDA, "alloc tridiagonal buffers");
+    double* tri = static_cast<double*>(ctx->tri.p);
+    int* dims = reinterpret_cast<int*>(tri + (size_t)chunk * 2 * N);
+    if (make_refine(chunk * N)) return fail(HX_E_CUDA, "alloc refinement list");
     for (int64_t m0 = 0; m0 < nmat; m0 += chunk) {
-      (void)m0;
+      const int64_t cnt = std::min(chunk, nmat - m0);
+      // masks/kpts offsets: the kernel indexes matrices from blockIdx.x; shift the mask base by whole masks
+      if (m0 % nk) return fail(HX_E_ARG, "internal: chunk not aligned to k-point groups");
+      hx::small_tridiag_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, d_masks + (m0 / nk) * c.words, tri, dims,
+                                                                status + m0);
+      HX_CUDA(cudaGetLastError());
+      hx::count_launch();
+      hx::launch_eig_idos(c, nk, g, m0, cnt, tri, (size_t)2 * N, dims, diff, trans, d_eigs, status, sharp, st, refine,
+                          refine_count);
+      HX_CUDA(cudaGetLastError());
     }
-    if (nmat > (int64_t)0x7fffffff) return fail(HX_E_RANGE, "too many matrices in one batch");
-    hx::fused_smem_kernel<<<(unsigned)nmat, 256, smem, st>>>(c, kp, nk, d_masks, g, diff, trans, d_eigs,
-                                                            reinterpret_cast<int*>(d_status), sharp);
-    HX_CUDA(cudaGetLastError());
-    hx::count_launch();
   } else if (c.pencil != HX_PENCIL_GENERAL && hx::band_path_supported(N)) {
+    if (make_refine(nmat * N)) return fail(HX_E_CUDA, "alloc refinement list");
     int rc = hx::band_eval(c, kp, nk, d_masks, nmasks, g, diff, trans, d_eigs,
                            reinterpret_cast<int*>(d_status), sharp, ctx->ws_budget,
-                           [&](size_t bytes) -> void* { return ctx->band.grow(bytes) ? nullptr : ctx->band.p; }, st);
+                           [&](size_t bytes) -> void* { return ctx->band.grow(bytes) ? nullptr : ctx->band.p; }, st,
+                           refine, refine_count);
     if (rc) return fail(HX_E_CUDA, std::string("band path: ") + hx::band_last_error());
   } else {
     const size_t stride = hx::global_ws_stride(N, c.pencil == HX_PENCIL_GENERAL);
@@ -313,13 +338,20 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
     chunk = std::min<int64_t>(chunk, nmat);
     chunk = std::min<int64_t>(chunk, 65535);
     if (ctx->ws.grow(stride * (size_t)chunk)) return fail(HX_E_CUDA, "alloc workspace");
+    if (ctx->tri.grow((size_t)chunk * (2 * N * 8 + 4) + 256)) return fail(HX_E_CUDA, "alloc tridiagonal buffers");
+    double* tri = static_cast<double*>(ctx->tri.p);
+    int* dims = reinterpret_cast<int*>(tri + (size_t)chunk * 2 * N);
+    if (make_refine(chunk * N)) return fail(HX_E_CUDA, "alloc refinement list");
     for (int64_t m0 = 0; m0 < nmat; m0 += chunk) {
       const int64_t cnt = std::min(chunk, nmat - m0);
-      hx::global_solve_kernel<<<(unsigned)cnt, 512, 0, st>>>(c, kp, nk, d_masks, g, diff, trans, d_eigs,
-                                                             reinterpret_cast<int*>(d_status), m0,
-                                                             static_cast<unsigned char*>(ctx->ws.p), stride, sharp);
+      hx::global_tridiag_kernel<<<(unsigned)cnt, 512, 0, st>>>(c, kp, nk, d_masks, m0,
+                                                               static_cast<unsigned char*>(ctx->ws.p), stride, tri,
+                                                               dims, status);
       HX_CUDA(cudaGetLastError());
-    hx::count_launch();
+      hx::count_launch();
+      hx::launch_eig_idos(c, nk, g, m0, cnt, tri, (size_t)2 * N, dims, diff, trans, d_eigs, status, sharp, st, refine,
+                          refine_count);
+      HX_CUDA(cudaGetLastError());
     }
   }
   const int wpb = 8;
@@ -396,117 +428,53 @@ int hx_eval_sharp_batch(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32
   return eval_host(ctx, cell, kpoints, nk, masks, nmasks, grid, out_curves, out_eigs, out_status, 1);
 }
 
-}  // extern "C"
-
-// ------------------------------------------------------------------------------------------------
 // Standalone batched eigenvalues of caller-provided matrices (config-5 sweep).
-namespace hx {
-
-__global__ void __launch_bounds__(256) eigvalsh_smem_kernel(int n, const double2* __restrict__ A, double* eigs,
-                                                            int* status) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int ld = n | 1;
-  double* R = reinterpret_cast<double*>(smem_raw);
-  double2* v = reinterpret_cast<double2*>(R + (((size_t)n * ld + 1) & ~(size_t)1));
-  double2* y = v + n;
-  double* diag = reinterpret_cast<double*>(y + n);
-  double* e2 = diag + n;
-  double* lam = e2 + n;
-  double* red = lam + n;
-  const double2* a = A + (size_t)blockIdx.x * n * n;
-  for (int p = threadIdx.x; p < n * n; p += blockDim.x) {
-    const int col = p / n, row = p - col * n;
-    const double2 z = a[p];
-    if (row > col) {
-      R[row * ld + col] = z.x;
-      R[col * ld + row] = z.y;
-    } else if (row == col) {
-      R[row * ld + row] = z.x;
-    }
-  }
-  if (threadIdx.x == 0) status[blockIdx.x] = 0;
-  __syncthreads();
-  tridiag_packed(R, ld, n, diag, e2, v, y, red);
-  bisect_all(diag, e2, n, lam, red);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) eigs[(size_t)blockIdx.x * n + i] = lam[i];
-}
-
-__global__ void __launch_bounds__(512) eigvalsh_global_kernel(int n, const double2* __restrict__ A,
-                                                              const double2* __restrict__ B, double* eigs,
-                                                              int* status, int64_t mat0, unsigned char* ws,
-                                                              size_t stride) {
-  __shared__ double red[96];
-  const int64_t mat = mat0 + blockIdx.x;
-  unsigned char* w = ws + (size_t)blockIdx.x * stride;
-  double2* Aw = reinterpret_cast<double2*>(w);
-  double2* Bw = Aw + (size_t)n * n;
-  double2* v = B ? Bw + (size_t)n * n : Bw;
-  double2* y = v + n;
-  double* diag = reinterpret_cast<double*>(y + n);
-  double* e2 = diag + n;
-  double* lam = e2 + n;
-  const double2* a = A + (size_t)mat * n * n;
-  for (int64_t p = threadIdx.x; p < (int64_t)n * n; p += blockDim.x) Aw[p] = a[p];
-  if (B) {
-    const double2* b = B + (size_t)mat * n * n;
-    for (int64_t p = threadIdx.x; p < (int64_t)n * n; p += blockDim.x) Bw[p] = b[p];
-  }
-  if (threadIdx.x == 0) status[mat] = 0;
-  __syncthreads();
-  if (B && !chol_reduce_full(Aw, Bw, n, n, red)) {
-    if (threadIdx.x == 0) status[mat] = 1;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) eigs[(size_t)mat * n + i] = __longlong_as_double(0x7ff8000000000000ll);
-    return;
-  }
-  tridiag_full(Aw, n, n, diag, e2, v, y, red);
-  bisect_all(diag, e2, n, lam, red);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) eigs[(size_t)mat * n + i] = lam[i];
-}
-
-}  // namespace hx
-
-extern "C" int hx_eigvalsh_batch_device(hx_ctx* ctx, int32_t n, int64_t batch, const double* d_A, const double* d_B,
-                                        double* d_eigs, int32_t* d_status, void* stream) {
+int hx_eigvalsh_batch_device(hx_ctx* ctx, int32_t n, int64_t batch, const double* d_A, const double* d_B,
+                             double* d_eigs, int32_t* d_status, void* stream) {
   if (!ctx || !d_A || !d_eigs || !d_status || n < 1 || batch < 0) return fail(HX_E_ARG, "hx_eigvalsh_batch: bad args");
   if (batch == 0) return 0;
+  if (n > HX_MAX_N) return fail(HX_E_RANGE, "hx_eigvalsh_batch: n too large");
   if (set_device(ctx)) return HX_E_CUDA;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (!d_B && n <= HX_SMEM_MAX_N) {
-    const size_t smem = hx::fused_smem_bytes(n);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(hx::eigvalsh_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)hx::fused_smem_bytes(HX_SMEM_MAX_N));
-      attr = true;
-    }
-    hx::eigvalsh_smem_kernel<<<(unsigned)batch, 256, smem, st>>>(n, reinterpret_cast<const double2*>(d_A), d_eigs,
-                                                                  reinterpret_cast<int*>(d_status));
-    HX_CUDA(cudaGetLastError());
-    hx::count_launch();
-    return 0;
-  }
+  int* status = reinterpret_cast<int*>(d_status);
+  hx::CellDev c{};
+  c.N = n;
+  hx::GridDev g{};
   if (!d_B && hx::band_path_supported(n)) {
-    int rc = hx::band_eigvalsh(n, batch, reinterpret_cast<const double2*>(d_A), d_eigs, reinterpret_cast<int*>(d_status),
-                               ctx->ws_budget,
+    int rc = hx::band_eigvalsh(n, batch, reinterpret_cast<const double2*>(d_A), d_eigs, status, ctx->ws_budget,
                                [&](size_t bytes) -> void* { return ctx->band.grow(bytes) ? nullptr : ctx->band.p; }, st);
     if (rc) return fail(HX_E_CUDA, std::string("band path: ") + hx::band_last_error());
     return 0;
   }
-  const size_t stride = hx::global_ws_stride(n, d_B != nullptr);
-  int64_t chunk = std::min<int64_t>((int64_t)std::max<size_t>(1, ctx->ws_budget / stride), batch);
-  chunk = std::min<int64_t>(chunk, 65535);
-  if (ctx->ws.grow(stride * (size_t)chunk)) return fail(HX_E_CUDA, "alloc workspace");
+  const bool small = !d_B && n <= HX_SMEM_MAX_N;
+  const size_t stride = small ? 0 : hx::global_ws_stride(n, d_B != nullptr);
+  int64_t chunk = small ? std::min<int64_t>(batch, 1 << 20)
+                        : std::min<int64_t>((int64_t)std::max<size_t>(1, ctx->ws_budget / stride), batch);
+  chunk = std::min<int64_t>(chunk, small ? (1 << 20) : 65535);
+  if (!small && ctx->ws.grow(stride * (size_t)chunk)) return fail(HX_E_CUDA, "alloc workspace");
+  if (ctx->tri.grow((size_t)chunk * (2 * n * 8 + 4) + 256)) return fail(HX_E_CUDA, "alloc tridiagonal buffers");
+  double* tri = static_cast<double*>(ctx->tri.p);
+  int* dims = reinterpret_cast<int*>(tri + (size_t)chunk * 2 * n);
   for (int64_t m0 = 0; m0 < batch; m0 += chunk) {
     const int64_t cnt = std::min(chunk, batch - m0);
-    hx::eigvalsh_global_kernel<<<(unsigned)cnt, 512, 0, st>>>(n, reinterpret_cast<const double2*>(d_A),
-                                                              reinterpret_cast<const double2*>(d_B), d_eigs,
-                                                              reinterpret_cast<int*>(d_status), m0,
-                                                              static_cast<unsigned char*>(ctx->ws.p), stride);
+    if (small) {
+      hx::eigvalsh_small_kernel<<<(unsigned)cnt, 256, hx::small_tridiag_smem(n), st>>>(
+          n, reinterpret_cast<const double2*>(d_A) + (size_t)m0 * n * n, tri, dims, status + m0);
+    } else {
+      hx::eigvalsh_global_kernel<<<(unsigned)cnt, 512, 0, st>>>(n, reinterpret_cast<const double2*>(d_A),
+                                                                reinterpret_cast<const double2*>(d_B), m0,
+                                                                static_cast<unsigned char*>(ctx->ws.p), stride, tri,
+                                                                dims, status);
+    }
     HX_CUDA(cudaGetLastError());
     hx::count_launch();
+    hx::launch_eig_idos(c, 1, g, m0, cnt, tri, (size_t)2 * n, dims, nullptr, nullptr, d_eigs, status, 0, st);
+    HX_CUDA(cudaGetLastError());
   }
   return 0;
 }
+
+}  // extern "C"
 
 // ------------------------------------------------------------------------------------------------
 // Kernel-module parity (_kernels.py:68-101): one CTA, thread per grid point, states in input order.

@@ -1,9 +1,11 @@
 // Per-matrix kernels of the hexmc hot path on sm_100a.
 //
-//  * fused_smem_kernel: one CTA per (mask, k) Bloch matrix, everything in shared memory
-//    (N <= HX_SMEM_MAX_N): compaction -> assembly -> tridiagonalisation -> bisection -> IDOS.
-//  * global_solve_kernel: same pipeline with the matrix in an HBM workspace slice (any N; also the
+//  * small_tridiag_kernel: one CTA per (mask, k) Bloch matrix, everything in shared memory
+//    (N <= HX_SMEM_MAX_N): compaction -> assembly -> Householder tridiagonalisation -> (diag, e2).
+//  * global_tridiag_kernel: same with the matrix in an HBM workspace slice (fallback tier, and the
 //    general (H, S) pencil via Cholesky).  The large-N two-stage path lives in hx_band.cu.
+//  * eig_idos_kernel: one THREAD per eigenvalue of every matrix in the batch (Sturm bisection),
+//    pencil map, the reference IDOS functional (fixed-point accumulation) and the eigenvalue output.
 //  * finalize_kernel: prefix-sum of the integer full-weight counts + fixed-point transition sums
 //    -> per-mask IDOS curves (qoi.py:96-102: values = counts / area, weights 1/nk).
 #include <cuda_runtime.h>
@@ -14,29 +16,12 @@
 
 namespace hx {
 
-__device__ __forceinline__ void emit_eigs_and_idos(const CellDev& c, const GridDev& g, const double* lam, int d,
-                                                   int* diff_row, unsigned long long* trans_row, double* eig_out,
-                                                   int N, int* st, bool sharp) {
-  // pencil map; the commuting map is monotone (decreasing when t - s*eps0 < 0)
-  const bool rev = (c.pencil == 1) && (c.t - c.s * c.eps0 < 0.0);
-  bool bad = false;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const double E = pencil_map(c, lam[i]);
-    bad |= !isfinite(E);
-    if (sharp) sharp_state(g, E, diff_row);
-    else idos_state(g, E, diff_row, trans_row);
-    if (eig_out) eig_out[rev ? d - 1 - i : i] = E;
-  }
-  if (eig_out)
-    for (int i = d + threadIdx.x; i < N; i += blockDim.x) eig_out[i] = __longlong_as_double(0x7ff8000000000000ll);
-  if (bad) atomicMax(st, 2);
-}
+static __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) fused_smem_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
-                                                         const uint64_t* __restrict__ masks, GridDev g, int* diff,
-                                                         unsigned long long* trans, double* eigs, int* status,
-                                                         int sharp) {
+__global__ void __launch_bounds__(256) small_tridiag_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
+                                                            const uint64_t* __restrict__ masks, double* tri,
+                                                            int* dims, int* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int N = c.N;
   const int ld = N | 1;  // odd row stride: conflict-free column walks
@@ -46,40 +31,33 @@ __global__ void __launch_bounds__(256) fused_smem_kernel(CellDev c, const double
   double* R = reinterpret_cast<double*>(smem_raw);
   double2* v = reinterpret_cast<double2*>(R + (((size_t)N * ld + 1) & ~(size_t)1));
   double2* y = v + N;
-  double* diag = reinterpret_cast<double*>(y + N);
+  double* red = reinterpret_cast<double*>(y + N);      // 96
+  int* new_idx = reinterpret_cast<int*>(red + 96);     // N
+  int* cnt = new_idx + N;                              // ceil(N/32)
+  double* diag = tri + mat * 2 * N;
   double* e2 = diag + N;
-  double* lam = e2 + N;
-  double* red = lam + N;                                   // 96
-  int* new_idx = reinterpret_cast<int*>(red + 96);         // N
-  int* cnt = new_idx + N;                                  // ceil(N/32)
 
-  int* st = status + mat;
-  if (threadIdx.x == 0) *st = 0;
   const int d = block_compact(c, masks + mk * c.words, new_idx, cnt);
-  if (d == 0) {
-    if (threadIdx.x == 0) *st = 3;
-    if (eigs)
-      for (int i = threadIdx.x; i < N; i += blockDim.x) eigs[mat * N + i] = __longlong_as_double(0x7ff8000000000000ll);
-    return;
+  if (threadIdx.x == 0) {
+    dims[mat] = d;
+    status[mat] = d == 0 ? 3 : 0;
   }
+  if (d == 0) return;
   assemble_packed(c, new_idx, d, kpts[kk], R, ld);
   tridiag_packed(R, ld, d, diag, e2, v, y, red);
-  bisect_all(diag, e2, d, lam, red);
-  emit_eigs_and_idos(c, g, lam, d, diff + mk * (g.npts + 1), trans + mk * g.npts, eigs ? eigs + mat * N : nullptr, N,
-                     st, sharp != 0);
 }
 
-size_t fused_smem_bytes(int N) {
+size_t small_tridiag_smem(int N) {
   const int ld = N | 1;
-  return (((size_t)N * ld + 1) & ~(size_t)1) * 8 + (size_t)N * 16 * 2 + (size_t)N * 8 * 3 + 96 * 8 + (size_t)N * 4 + ((N + 31) / 32) * 4 + 16;
+  return (((size_t)N * ld + 1) & ~(size_t)1) * 8 + (size_t)N * 16 * 2 + 96 * 8 + (size_t)N * 4 +
+         ((N + 31) / 32) * 4 + 16;
 }
 
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(512) global_solve_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
-                                                           const uint64_t* __restrict__ masks, GridDev g, int* diff,
-                                                           unsigned long long* trans, double* eigs, int* status,
-                                                           int64_t mat0, unsigned char* ws, size_t ws_stride,
-                                                           int sharp) {
+__global__ void __launch_bounds__(512) global_tridiag_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
+                                                             const uint64_t* __restrict__ masks, int64_t mat0,
+                                                             unsigned char* ws, size_t ws_stride, double* tri,
+                                                             int* dims, int* status) {
   __shared__ double red[96];
   __shared__ int cnt[(HX_MAX_N + 31) / 32];
   const int N = c.N;
@@ -92,37 +70,172 @@ __global__ void __launch_bounds__(512) global_solve_kernel(CellDev c, const doub
   const bool general = c.pencil == 2;
   double2* v = general ? B + (size_t)N * N : B;
   double2* y = v + N;
-  double* diag = reinterpret_cast<double*>(y + N);
+  int* new_idx = reinterpret_cast<int*>(y + N);
+  double* diag = tri + (int64_t)blockIdx.x * 2 * N;
   double* e2 = diag + N;
-  double* lam = e2 + N;
-  int* new_idx = reinterpret_cast<int*>(lam + N);
 
-  int* st = status + mat;
-  if (threadIdx.x == 0) *st = 0;
   const int d = block_compact(c, masks + mk * c.words, new_idx, cnt);
-  if (d == 0) {
-    if (threadIdx.x == 0) *st = 3;
-    if (eigs)
-      for (int i = threadIdx.x; i < N; i += blockDim.x) eigs[mat * N + i] = __longlong_as_double(0x7ff8000000000000ll);
-    return;
+  if (threadIdx.x == 0) {
+    dims[blockIdx.x] = d;
+    status[mat] = d == 0 ? 3 : 0;
   }
+  if (d == 0) return;
   const double2 k = kpts[kk];
   assemble_full(c, new_idx, d, k, A, N, false);
   if (general) {
     assemble_full(c, new_idx, d, k, B, N, true);
     if (!chol_reduce_full(A, B, N, d, red)) {
-      if (threadIdx.x == 0) *st = 1;
-      if (eigs)
-        for (int i = threadIdx.x; i < N; i += blockDim.x) eigs[mat * N + i] = __longlong_as_double(0x7ff8000000000000ll);
+      if (threadIdx.x == 0) {
+        status[mat] = 1;
+        dims[blockIdx.x] = 0;
+      }
       return;
     }
   }
   tridiag_full(A, N, d, diag, e2, v, y, red);
-  bisect_all(diag, e2, d, lam, red);
-  emit_eigs_and_idos(c, g, lam, d, diff + mk * (g.npts + 1), trans + mk * g.npts, eigs ? eigs + mat * N : nullptr, N,
-                     st, sharp != 0);
 }
 
+size_t global_ws_stride(int N, bool general) {
+  size_t b = (size_t)N * N * 16 * (general ? 2 : 1) + (size_t)N * 16 * 2 + (size_t)N * 4;
+  return (b + 255) & ~(size_t)255;
+}
+
+// ------------------------------------------------------------------------------------------------
+// One thread per (matrix, eigenvalue index).  tri: per matrix `tri_stride` doubles, diag at 0 and e2
+// at +N (N = c.N).  Matrices with dims == 0 (all vacant / failed) contribute nothing.
+__global__ void __launch_bounds__(128) eig_idos_kernel(CellDev c, int nk, GridDev g, int64_t mat0, int64_t nmat,
+                                                       const double* __restrict__ tri, size_t tri_stride,
+                                                       const int* __restrict__ dims, int* diff,
+                                                       unsigned long long* trans, double* eigs, int* status,
+                                                       int sharp, RefineItem* refine,
+                                                       unsigned long long* refine_count) {
+  const int N = c.N;
+  const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t lm = slot / N;
+  if (lm >= nmat) return;
+  const int idx = (int)(slot - lm * N);
+  const int64_t mat = mat0 + lm;
+  const int d = dims[lm];
+  double* eig_out = eigs ? eigs + mat * N : nullptr;
+  if (idx >= d) {
+    if (eig_out) eig_out[idx] = qnan();
+    return;
+  }
+  const double* diag = tri + lm * tri_stride;
+  const double* e2 = diag + N;
+  // Gershgorin interval and pivmin (dstebz conventions)
+  double gl = 1e308, gu = -1e308, em = 0.0, el = 0.0;
+  for (int i = 0; i < d; ++i) {
+    const double er2 = i + 1 < d ? e2[i] : 0.0;
+    const double er = sqrt(er2);
+    gl = fmin(gl, diag[i] - el - er);
+    gu = fmax(gu, diag[i] + el + er);
+    em = fmax(em, er2);
+    el = er;
+  }
+  const double pivmin = DBL_MIN * fmax(1.0, em);
+  const double tnorm = fmax(fabs(gl), fabs(gu));
+  gl = gl - 2.1 * tnorm * DBL_EPSILON * d - 4.2 * pivmin;
+  gu = gu + 2.1 * tnorm * DBL_EPSILON * d + 4.2 * pivmin;
+  double lo = gl, hi = gu;
+  // Without an eigenvalue output, an eigenvalue whose bracket maps entirely into one gap between the
+  // transition windows contributes a full weight at a determined grid index: stop bisecting there
+  // (the index arithmetic of _kernels.py:68-101 is constant over the widened bracket, so the result
+  // equals the reference's for any eigenvalue in it).
+  const bool early = eigs == nullptr && refine != nullptr;
+  bool settled = false;
+  long long settled_lo = 0;
+  for (int it = 0; it < 200; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    const double tol = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin;
+    if (hi - lo <= tol || mid <= lo || mid >= hi) break;
+    if (early && it >= 4) {
+      const double ea = pencil_map(c, lo), eb = pencil_map(c, hi);
+      double Ea = fmin(ea, eb), Eb = fmax(ea, eb);
+      const double eta = 16.0 * DBL_EPSILON * fmax(1.0, fmax(fabs(Ea), fabs(Eb)));
+      Ea -= eta;
+      Eb += eta;
+      if (sharp) {
+        const long long ia = (long long)floor((Ea - g.e0) / g.step), ib = (long long)floor((Eb - g.e0) / g.step);
+        if (ia == ib) {
+          settled = true;
+          settled_lo = ia + 1;
+          break;
+        }
+      } else {
+        const long long la = (long long)ceil((Ea + g.delta - g.e0) / g.step);
+        const long long lb = (long long)ceil((Eb + g.delta - g.e0) / g.step);
+        const long long ma = (long long)floor((Ea - g.delta - g.e0) / g.step) + 1;
+        const long long mb = (long long)floor((Eb - g.delta - g.e0) / g.step) + 1;
+        if (la == lb && ma == mb && ma >= la) {
+          settled = true;
+          settled_lo = la;
+          break;
+        }
+      }
+      if (it >= 14) {
+        // phase 1 done: hand the bracket to the dense refinement pass (keeps warps free of divergence)
+        const unsigned long long pos = atomicAdd(refine_count, 1ull);
+        refine[pos] = RefineItem{mat, lm, idx, lo, hi, pivmin};
+        return;
+      }
+    }
+    if (sturm_count(diag, e2, d, mid, pivmin) > idx) hi = mid;
+    else lo = mid;
+  }
+  if (settled) {
+    if (diff) {
+      const int64_t mk = mat / nk;
+      const long long l0 = settled_lo < 0 ? 0 : settled_lo;
+      if (l0 < g.npts) atomicAdd(diff + mk * (g.npts + 1) + l0, 1);
+    }
+    return;
+  }
+  const double lam = 0.5 * (lo + hi);
+  const double E = pencil_map(c, lam);
+  if (!isfinite(E)) atomicMax(status + mat, 2);
+  if (diff) {
+    const int64_t mk = mat / nk;
+    if (sharp) sharp_state(g, E, diff + mk * (g.npts + 1));
+    else idos_state(g, E, diff + mk * (g.npts + 1), trans + mk * g.npts);
+  }
+  if (eig_out) {
+    const bool rev = (c.pencil == 1) && (c.t - c.s * c.eps0 < 0.0);
+    eig_out[rev ? d - 1 - idx : idx] = E;
+  }
+}
+
+// Phase 2: full-precision bisection of the eigenvalues left unsettled by eig_idos_kernel, densely
+// packed (every lane of a warp has real work), then the IDOS contribution.
+__global__ void __launch_bounds__(128) eig_refine_kernel(CellDev c, int nk, GridDev g, const double* __restrict__ tri,
+                                                         size_t tri_stride, const int* __restrict__ dims, int* diff,
+                                                         unsigned long long* trans, int* status, int sharp,
+                                                         const RefineItem* __restrict__ items,
+                                                         const unsigned long long* __restrict__ count) {
+  const unsigned long long n = *count;
+  for (unsigned long long q = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
+       q += (unsigned long long)gridDim.x * blockDim.x) {
+    const RefineItem it = items[q];
+    const double* diag = tri + it.lm * tri_stride;
+    const double* e2 = diag + c.N;
+    const int d = dims[it.lm];
+    double lo = it.lo, hi = it.hi;
+    for (int k = 0; k < 200; ++k) {
+      const double mid = 0.5 * (lo + hi);
+      const double tol = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + it.pivmin;
+      if (hi - lo <= tol || mid <= lo || mid >= hi) break;
+      if (sturm_count(diag, e2, d, mid, it.pivmin) > it.idx) hi = mid;
+      else lo = mid;
+    }
+    const double E = pencil_map(c, 0.5 * (lo + hi));
+    if (!isfinite(E)) atomicMax(status + it.mat, 2);
+    const int64_t mk = it.mat / nk;
+    if (sharp) sharp_state(g, E, diff + mk * (g.npts + 1));
+    else idos_state(g, E, diff + mk * (g.npts + 1), trans + mk * g.npts);
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
 // Dense H(k), S(k) per (mask, k) into caller buffers (column-major N x N complex, leading d x d
 // block valid, rest zero): assemble_bloch (tbmodel.py:277-293) on the device.
 __global__ void __launch_bounds__(256) assemble_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
@@ -162,9 +275,67 @@ __global__ void __launch_bounds__(256) assemble_kernel(CellDev c, const double2*
   }
 }
 
-size_t global_ws_stride(int N, bool general) {
-  size_t b = (size_t)N * N * 16 * (general ? 2 : 1) + (size_t)N * 16 * 2 + (size_t)N * 8 * 3 + (size_t)N * 4;
-  return (b + 255) & ~(size_t)255;
+// ------------------------------------------------------------------------------------------------
+// Standalone matrices (hx_eigvalsh_batch_device): lower triangle of A -> packed smem -> (diag, e2).
+__global__ void __launch_bounds__(256) eigvalsh_small_kernel(int n, const double2* __restrict__ A, double* tri,
+                                                             int* dims, int* status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int ld = n | 1;
+  double* R = reinterpret_cast<double*>(smem_raw);
+  double2* v = reinterpret_cast<double2*>(R + (((size_t)n * ld + 1) & ~(size_t)1));
+  double2* y = v + n;
+  double* red = reinterpret_cast<double*>(y + n);
+  const double2* a = A + (size_t)blockIdx.x * n * n;
+  for (int p = threadIdx.x; p < n * n; p += blockDim.x) {
+    const int col = p / n, row = p - col * n;
+    const double2 z = a[p];
+    if (row > col) {
+      R[row * ld + col] = z.x;
+      R[col * ld + row] = z.y;
+    } else if (row == col) {
+      R[row * ld + row] = z.x;
+    }
+  }
+  if (threadIdx.x == 0) {
+    status[blockIdx.x] = 0;
+    dims[blockIdx.x] = n;
+  }
+  __syncthreads();
+  double* diag = tri + (size_t)blockIdx.x * 2 * n;
+  tridiag_packed(R, ld, n, diag, diag + n, v, y, red);
+}
+
+__global__ void __launch_bounds__(512) eigvalsh_global_kernel(int n, const double2* __restrict__ A,
+                                                              const double2* __restrict__ B, int64_t mat0,
+                                                              unsigned char* ws, size_t stride, double* tri,
+                                                              int* dims, int* status) {
+  __shared__ double red[96];
+  const int64_t mat = mat0 + blockIdx.x;
+  unsigned char* w = ws + (size_t)blockIdx.x * stride;
+  double2* Aw = reinterpret_cast<double2*>(w);
+  double2* Bw = Aw + (size_t)n * n;
+  double2* v = B ? Bw + (size_t)n * n : Bw;
+  double2* y = v + n;
+  const double2* a = A + (size_t)mat * n * n;
+  for (int64_t p = threadIdx.x; p < (int64_t)n * n; p += blockDim.x) Aw[p] = a[p];
+  if (B) {
+    const double2* b = B + (size_t)mat * n * n;
+    for (int64_t p = threadIdx.x; p < (int64_t)n * n; p += blockDim.x) Bw[p] = b[p];
+  }
+  if (threadIdx.x == 0) {
+    status[mat] = 0;
+    dims[blockIdx.x] = n;
+  }
+  __syncthreads();
+  if (B && !chol_reduce_full(Aw, Bw, n, n, red)) {
+    if (threadIdx.x == 0) {
+      status[mat] = 1;
+      dims[blockIdx.x] = 0;
+    }
+    return;
+  }
+  double* diag = tri + (size_t)blockIdx.x * 2 * n;
+  tridiag_full(Aw, n, n, diag, diag + n, v, y, red);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -181,7 +352,6 @@ __global__ void finalize_kernel(const int* diff, const unsigned long long* trans
   for (int base = 0; base < g.npts; base += 32) {
     const int m = base + lane;
     long long x = m < g.npts ? dr[m] : 0;
-    // inclusive warp scan
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const long long t = __shfl_up_sync(0xffffffffu, x, o);

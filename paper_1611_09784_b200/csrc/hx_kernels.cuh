@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "hx_common.cuh"
 
 #define HX_SMEM_MAX_N 160   // largest N held entirely in shared memory (real-packed Hermitian)
@@ -10,19 +12,61 @@
 
 namespace hx {
 
-__global__ void fused_smem_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, GridDev g, int* diff,
-                                  unsigned long long* trans, double* eigs, int* status, int sharp);
-size_t fused_smem_bytes(int N);
+// an eigenvalue bracket handed from the bisection pass to the dense refinement pass
+struct RefineItem {
+  int64_t mat;   // global matrix index (mask * nk + k)
+  int64_t lm;    // chunk-local matrix index (tri / dims row)
+  int64_t idx;   // eigenvalue index
+  double lo, hi, pivmin;
+};
 
-__global__ void global_solve_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, GridDev g, int* diff,
-                                    unsigned long long* trans, double* eigs, int* status, int64_t mat0,
-                                    unsigned char* ws, size_t ws_stride, int sharp);
+// tridiagonalisation tiers: write (diag[N], e2[N]) per matrix into `tri` (2N doubles per matrix)
+__global__ void small_tridiag_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, double* tri,
+                                     int* dims, int* status);
+size_t small_tridiag_smem(int N);
+
+__global__ void global_tridiag_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, int64_t mat0,
+                                      unsigned char* ws, size_t ws_stride, double* tri, int* dims, int* status);
 size_t global_ws_stride(int N, bool general);
+
+// eigenvalues (bisection, thread per eigenvalue) + pencil map + IDOS accumulation + eigenvalue output
+__global__ void eig_idos_kernel(CellDev c, int nk, GridDev g, int64_t mat0, int64_t nmat, const double* tri,
+                                size_t tri_stride, const int* dims, int* diff, unsigned long long* trans, double* eigs,
+                                int* status, int sharp, RefineItem* refine, unsigned long long* refine_count);
+__global__ void eig_refine_kernel(CellDev c, int nk, GridDev g, const double* tri, size_t tri_stride, const int* dims,
+                                  int* diff, unsigned long long* trans, int* status, int sharp,
+                                  const RefineItem* items, const unsigned long long* count);
 
 __global__ void assemble_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, double2* H, double2* S,
                                 int* dims);
 
+__global__ void eigvalsh_small_kernel(int n, const double2* A, double* tri, int* dims, int* status);
+__global__ void eigvalsh_global_kernel(int n, const double2* A, const double2* B, int64_t mat0, unsigned char* ws,
+                                       size_t stride, double* tri, int* dims, int* status);
+
 __global__ void finalize_kernel(const int* diff, const unsigned long long* trans, int64_t nmasks, GridDev g,
                                 double inv_nk, double inv_area, double* curves);
+
+// Eigenvalue stage over `nmat` matrices starting at global index mat0.  With a refinement buffer
+// (capacity >= nmat * N items) and no eigenvalue output, eigenvalues that settle into a gap between
+// transition windows stop early and the rest are finished by a densely packed second pass.
+inline void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, int64_t nmat, const double* tri,
+                            size_t tri_stride, const int* dims, int* diff, unsigned long long* trans, double* eigs,
+                            int* status, int sharp, cudaStream_t st, RefineItem* refine = nullptr,
+                            unsigned long long* refine_count = nullptr) {
+  const int64_t slots = nmat * (int64_t)c.N;
+  const bool two_pass = refine && refine_count && diff && !eigs;
+  if (two_pass) cudaMemsetAsync(refine_count, 0, sizeof(unsigned long long), st);
+  eig_idos_kernel<<<(unsigned)((slots + 127) / 128), 128, 0, st>>>(c, nk, g, mat0, nmat, tri, tri_stride, dims, diff,
+                                                                   trans, eigs, status, sharp,
+                                                                   two_pass ? refine : nullptr, refine_count);
+  count_launch();
+  if (two_pass) {
+    const int64_t blocks = std::min<int64_t>((slots + 127) / 128, 148 * 16);
+    eig_refine_kernel<<<(unsigned)blocks, 128, 0, st>>>(c, nk, g, tri, tri_stride, dims, diff, trans, status, sharp,
+                                                        refine, refine_count);
+    count_launch();
+  }
+}
 
 }  // namespace hx
