@@ -23,6 +23,7 @@
 #include "hx_dmma.cuh"
 #include "hx_kernels.cuh"
 #include "hx_chase.cuh"
+#include "hx_panel.cuh"
 
 namespace hx {
 
@@ -476,7 +477,15 @@ constexpr size_t HEMM_SMEM = (size_t)(HM_TM + BW) * HM_LD * sizeof(double2);
 constexpr size_t W_SMEM = (size_t)160 * (BW + 1) * sizeof(double2);
 constexpr size_t HER2K_SMEM = (size_t)4 * HK_T * HK_LD * sizeof(double2);
 
+constexpr size_t PANEL_SMEM_MAX = 200 * 1024;
+
 void band_init_attributes() {
+  cudaFuncSetAttribute(panel_qr_cluster_kernel<2, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)PANEL_SMEM_MAX);
+  cudaFuncSetAttribute(panel_qr_cluster_kernel<4, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)PANEL_SMEM_MAX);
+  cudaFuncSetAttribute(panel_qr_cluster_kernel<8, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)PANEL_SMEM_MAX);
   cudaFuncSetAttribute(band_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   cudaFuncSetAttribute(hemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HEMM_SMEM);
   cudaFuncSetAttribute(w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W_SMEM);
@@ -497,7 +506,31 @@ bool band_path_supported(int N) { return N > HX_SMEM_MAX_N && N <= HX_MAX_N; }
 static int band_reduce(double2* ws, const BandWs& L, int N, int64_t cnt, const int* dims, cudaStream_t st) {
   for (int k0 = 0; N - k0 - BW > 0; k0 += BW) {
     const int m = N - k0 - BW;
-    panel_qr_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, L, N, k0);
+    // cluster panel QR: smallest cluster whose shared memory holds the panel slices
+    // (large batches keep every SM busy with one single-CTA panel per matrix instead)
+    int CL = 0, R = 0;
+    for (int cl : {2, 4, 8}) {
+      if (cnt >= 512) break;
+      const int r = (m + cl - 1) / cl;
+      if (panel_cluster_smem<BW>(r) <= PANEL_SMEM_MAX) {
+        CL = cl;
+        R = r;
+        break;
+      }
+    }
+    const size_t psm = panel_cluster_smem<BW>(R);
+    if (CL == 2) {
+      panel_qr_cluster_kernel<2, BW><<<dim3(2, (unsigned)cnt), 256, psm, st>>>(ws, L.stride, L.a_off, L.v_off,
+                                                                              L.t_off, N, k0, R);
+    } else if (CL == 4) {
+      panel_qr_cluster_kernel<4, BW><<<dim3(4, (unsigned)cnt), 256, psm, st>>>(ws, L.stride, L.a_off, L.v_off,
+                                                                              L.t_off, N, k0, R);
+    } else if (CL == 8) {
+      panel_qr_cluster_kernel<8, BW><<<dim3(8, (unsigned)cnt), 256, psm, st>>>(ws, L.stride, L.a_off, L.v_off,
+                                                                              L.t_off, N, k0, R);
+    } else {
+      panel_qr_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, L, N, k0);  // very tall panels: L2-resident fallback
+    }
     const unsigned mt = (unsigned)((m + HM_TM - 1) / HM_TM);
     hemm_kernel<<<dim3(mt, (unsigned)cnt), 128, HEMM_SMEM, st>>>(ws, L, N, k0);
     w_kernel<<<(unsigned)cnt, 256, W_SMEM, st>>>(ws, L, N, k0);

@@ -317,7 +317,7 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
       const int64_t cnt = std::min(chunk, nmat - m0);
       // masks/kpts offsets: the kernel indexes matrices from blockIdx.x; shift the mask base by whole masks
       if (m0 % nk) return fail(HX_E_ARG, "internal: chunk not aligned to k-point groups");
-      hx::small_tridiag_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, d_masks + (m0 / nk) * c.words, tri, dims,
+      hx::small_tridiag_kernel<<<(unsigned)cnt, N > 64 ? 512 : 256, smem, st>>>(c, kp, nk, d_masks + (m0 / nk) * c.words, tri, dims,
                                                                 status + m0);
       HX_CUDA(cudaGetLastError());
       hx::count_launch();
@@ -458,7 +458,7 @@ int hx_eigvalsh_batch_device(hx_ctx* ctx, int32_t n, int64_t batch, const double
   for (int64_t m0 = 0; m0 < batch; m0 += chunk) {
     const int64_t cnt = std::min(chunk, batch - m0);
     if (small) {
-      hx::eigvalsh_small_kernel<<<(unsigned)cnt, 256, hx::small_tridiag_smem(n), st>>>(
+      hx::eigvalsh_small_kernel<<<(unsigned)cnt, n > 64 ? 512 : 256, hx::small_tridiag_smem(n), st>>>(
           n, reinterpret_cast<const double2*>(d_A) + (size_t)m0 * n * n, tri, dims, status + m0);
     } else {
       hx::eigvalsh_global_kernel<<<(unsigned)cnt, 512, 0, st>>>(n, reinterpret_cast<const double2*>(d_A),

@@ -8,6 +8,8 @@
 
 #include "hx_common.cuh"
 
+#define HX_TRI_MAXN 160  // largest dimension handled by tridiag_packed (shared-memory tier)
+
 namespace hx {
 
 // ---------------------------------------------------------------------------------------------
@@ -189,89 +191,144 @@ __device__ __forceinline__ Reflector make_reflector(double2 alpha, double sigma2
   return h;
 }
 
-// Tridiagonalise the d x d Hermitian matrix held in real-packed storage R (smem), unblocked.
-// Outputs diag[d] and e2[d-1] (squared off-diagonals).  v, y are complex scratch [d] in smem;
-// red: 33 doubles.
+// Tridiagonalise the d x d Hermitian matrix held in real-packed storage R (smem), unblocked, with
+// three CTA barriers per column: the next column's norm is accumulated while the trailing update is
+// applied, the Hermitian matrix-vector product uses P threads per row (shuffle-combined), and the
+// rank-2 update forms w = tau*y - hc*v on the fly.  Outputs diag[d] and e2[d-1] (squared
+// off-diagonals).  v, y: complex scratch [d] in smem; red: 128 doubles (double-buffered partials).
 static __device__ void tridiag_packed(double* R, int ld, int d, double* diag, double* e2, double2* v, double2* y,
-                               double* red) {
-  const int tid = threadIdx.x, bd = blockDim.x;
+                                      double* red) {
+  const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = bd >> 5;
+  double part = 0.0;
+  for (int i = 1 + tid; i < d; i += bd) {
+    const double xr = R[i * ld], xi = R[i];
+    part += xr * xr + xi * xi;
+  }
+  int par = 0;
   for (int j = 0; j + 2 < d; ++j) {
     const int b = j + 1, m = d - b;
-    // (1) column j below the diagonal: x_i = A_{b+i, j} = (R[(b+i)*ld + j], R[j*ld + b+i])
-    double part = 0.0;
-    for (int i = tid; i < m; i += bd) {
-      const double xr = R[(b + i) * ld + j], xi = R[j * ld + b + i];
-      part += xr * xr + xi * xi;
-    }
-    const double sig2 = block_sum(part, red);
+    double* rb = red + par * 64;
+    // ---- B1: column norm (partials accumulated by the previous update sweep)
+    part = warp_sum(part);
+    if (lane == 0) rb[warp] = part;
+    __syncthreads();
+    double sig2 = 0.0;
+    for (int w = 0; w < nw; ++w) sig2 += rb[w];
     const double2 alpha = make_double2(R[b * ld + j], R[j * ld + b]);
     const Reflector h = make_reflector(alpha, sig2);
     if (tid == 0) {
       diag[j] = R[j * ld + j];
       e2[j] = h.e2;
     }
+    par ^= 1;
     if (h.tau == 0.0) {
-      __syncthreads();
+      // column already reduced: next norm from the unchanged trailing matrix
+      part = 0.0;
+      for (int i = 1 + tid; i < m; i += bd) {
+        const double xr = R[(b + i) * ld + b], xi = R[b * ld + b + i];
+        part += xr * xr + xi * xi;
+      }
       continue;
     }
-    // (2) v (v0 = 1)
+    // ---- B2: v (v0 = 1)
     for (int i = tid; i < m; i += bd) {
       const double2 x = make_double2(R[(b + i) * ld + j], R[j * ld + b + i]);
       v[i] = i == 0 ? make_double2(1.0, 0.0) : cmul(x, h.scale);
     }
     __syncthreads();
-    // (3) y = A22 v ; partial c = v^H y
+    // ---- B3: y = A22 v (P threads per row), c = v^H y
+    int P = 1;
+    while (P < 8 && 2 * P * m <= bd) P *= 2;
+    const int rows_per_pass = bd / P;
     double cpart = 0.0;
-    for (int i = tid; i < m; i += bd) {
-      const int gi = b + i;
+    for (int row0 = 0; row0 < m; row0 += rows_per_pass) {
+      const int i = row0 + tid / P, kp = tid % P;
       double yr0 = 0.0, yi0 = 0.0, yr1 = 0.0, yi1 = 0.0;
-      int kk = 0;
-      for (; kk + 1 < m; kk += 2) {
+      if (i < m) {
+        const int gi = b + i;
+        int k = kp;
+        for (; k + P < m; k += 2 * P) {
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int k2 = kk + u, gk = b + k2;
+          for (int u = 0; u < 2; ++u) {
+            const int kk = k + u * P, gk = b + kk;
+            const double p = R[gi * ld + gk], q = R[gk * ld + gi];
+            const double re = kk < i ? p : (kk > i ? q : p);
+            const double im = kk < i ? q : (kk > i ? -p : 0.0);
+            const double2 vk = v[kk];
+            if (u == 0) {
+              yr0 = fma(re, vk.x, fma(-im, vk.y, yr0));
+              yi0 = fma(re, vk.y, fma(im, vk.x, yi0));
+            } else {
+              yr1 = fma(re, vk.x, fma(-im, vk.y, yr1));
+              yi1 = fma(re, vk.y, fma(im, vk.x, yi1));
+            }
+          }
+        }
+        if (k < m) {
+          const int gk = b + k;
           const double p = R[gi * ld + gk], q = R[gk * ld + gi];
-          double re, im;
-          if (k2 < i) { re = p; im = q; } else if (k2 > i) { re = q; im = -p; } else { re = p; im = 0.0; }
-          const double2 vk = v[k2];
-          if (u == 0) { yr0 += re * vk.x - im * vk.y; yi0 += re * vk.y + im * vk.x; }
-          else { yr1 += re * vk.x - im * vk.y; yi1 += re * vk.y + im * vk.x; }
+          const double re = k < i ? p : (k > i ? q : p);
+          const double im = k < i ? q : (k > i ? -p : 0.0);
+          const double2 vk = v[k];
+          yr0 = fma(re, vk.x, fma(-im, vk.y, yr0));
+          yi0 = fma(re, vk.y, fma(im, vk.x, yi0));
         }
       }
-      for (; kk < m; ++kk) {
-        const int gk = b + kk;
-        const double p = R[gi * ld + gk], q = R[gk * ld + gi];
-        double re, im;
-        if (kk < i) { re = p; im = q; } else if (kk > i) { re = q; im = -p; } else { re = p; im = 0.0; }
-        const double2 vk = v[kk];
-        yr0 += re * vk.x - im * vk.y;
-        yi0 += re * vk.y + im * vk.x;
+      double yr = yr0 + yr1, yim = yi0 + yi1;
+      for (int o = 1; o < P; o <<= 1) {
+        yr += __shfl_xor_sync(0xffffffffu, yr, o);
+        yim += __shfl_xor_sync(0xffffffffu, yim, o);
       }
-      const double2 yi = make_double2(yr0 + yr1, yi0 + yi1);
-      y[i] = yi;
-      const double2 vi = v[i];
-      cpart += vi.x * yi.x + vi.y * yi.y;  // Re(conj(v_i) y_i)
+      if (kp == 0 && i < m) {
+        y[i] = make_double2(yr, yim);
+        const double2 vi = v[i];
+        cpart += vi.x * yr + vi.y * yim;
+      }
     }
-    const double cval = block_sum(cpart, red);
-    // (4) w = tau y - 0.5 tau^2 c v  (stored over y)
+    cpart = warp_sum(cpart);
+    if (lane == 0) rb[32 + warp] = cpart;
+    __syncthreads();
+    double cval = 0.0;
+    for (int w = 0; w < nw; ++w) cval += rb[32 + w];
     const double hc = 0.5 * h.tau * h.tau * cval;
-    for (int i = tid; i < m; i += bd) {
-      const double2 yi = y[i], vi = v[i];
-      y[i] = make_double2(h.tau * yi.x - hc * vi.x, h.tau * yi.y - hc * vi.y);
+    const double tau = h.tau;
+    // ---- update A22 -= v w^H + w v^H (w = tau y - hc v), accumulating the next column's norm
+    // Position (i, k) of the packed array holds Re A_ik (i >= k) or Im A_ki (i < k); with
+    // a = v_i conj(w_k) + w_i conj(v_k) the update is R -= Re(a) (i >= k) or R += Im(a) (i < k), i.e.
+    // R -= vi.x*X1 + vi.y*X2 + wi.x*X3 + wi.y*X4 with X = (wk.x, wk.y, vk.x, vk.y) or
+    // (wk.y, -wk.x, vk.y, -vk.x).  Each lane keeps its columns' (v_k, w_k) in registers.
+    part = 0.0;
+    constexpr int KC = (HX_TRI_MAXN + 31) / 32;
+    double2 vks[KC], wks[KC];
+#pragma unroll
+    for (int t = 0; t < KC; ++t) {
+      const int k = lane + 32 * t;
+      const double2 vk = k < m ? v[k] : make_double2(0.0, 0.0);
+      const double2 yk = k < m ? y[k] : make_double2(0.0, 0.0);
+      vks[t] = vk;
+      wks[t] = make_double2(tau * yk.x - hc * vk.x, tau * yk.y - hc * vk.y);
     }
-    __syncthreads();
-    // (5) A22 -= v w^H + w v^H over the trailing square of R positions
-    for (int p = tid; p < m * m; p += bd) {
-      const int i = p / m, k = p - i * m;
-      const double2 vi = v[i], wi = y[i], vk = v[k], wk = y[k];
-      double delta;
-      if (i > k) delta = vi.x * wk.x + vi.y * wk.y + wi.x * vk.x + wi.y * vk.y;
-      else if (i < k) delta = (vk.y * wi.x - vk.x * wi.y) + (wk.y * vi.x - wk.x * vi.y);
-      else delta = 2.0 * (vi.x * wi.x + vi.y * wi.y);
-      R[(b + i) * ld + b + k] -= delta;
+    for (int i = warp; i < m; i += nw) {
+      const double2 vi = v[i], yi = y[i];
+      const double2 wi = make_double2(tau * yi.x - hc * vi.x, tau * yi.y - hc * vi.y);
+      double* row = R + (b + i) * ld + b;
+#pragma unroll
+      for (int t = 0; t < KC; ++t) {
+        const int k = lane + 32 * t;
+        if (k < m) {
+          const bool low = i >= k;
+          const double2 vk = vks[t], wk = wks[t];
+          const double x1 = low ? wk.x : wk.y, x2 = low ? wk.y : -wk.x;
+          const double x3 = low ? vk.x : vk.y, x4 = low ? vk.y : -vk.x;
+          const double delta = fma(vi.x, x1, fma(vi.y, x2, fma(wi.x, x3, wi.y * x4)));
+          const double val = row[k] - delta;
+          row[k] = val;
+          if ((k == 0 && i >= 1) || (i == 0 && k >= 1)) part = fma(val, val, part);
+        }
+      }
     }
-    __syncthreads();
   }
+  __syncthreads();
   if (tid == 0) {
     if (d >= 2) {
       const double xr = R[(d - 1) * ld + d - 2], xi = R[(d - 2) * ld + d - 1];

@@ -19,7 +19,7 @@ namespace hx {
 static __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) small_tridiag_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
+__global__ void __launch_bounds__(512) small_tridiag_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
                                                             const uint64_t* __restrict__ masks, double* tri,
                                                             int* dims, int* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -31,8 +31,8 @@ __global__ void __launch_bounds__(256) small_tridiag_kernel(CellDev c, const dou
   double* R = reinterpret_cast<double*>(smem_raw);
   double2* v = reinterpret_cast<double2*>(R + (((size_t)N * ld + 1) & ~(size_t)1));
   double2* y = v + N;
-  double* red = reinterpret_cast<double*>(y + N);      // 96
-  int* new_idx = reinterpret_cast<int*>(red + 96);     // N
+  double* red = reinterpret_cast<double*>(y + N);      // 128
+  int* new_idx = reinterpret_cast<int*>(red + 128);     // N
   int* cnt = new_idx + N;                              // ceil(N/32)
   double* diag = tri + mat * 2 * N;
   double* e2 = diag + N;
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) small_tridiag_kernel(CellDev c, const dou
 
 size_t small_tridiag_smem(int N) {
   const int ld = N | 1;
-  return (((size_t)N * ld + 1) & ~(size_t)1) * 8 + (size_t)N * 16 * 2 + 96 * 8 + (size_t)N * 4 +
+  return (((size_t)N * ld + 1) & ~(size_t)1) * 8 + (size_t)N * 16 * 2 + 128 * 8 + (size_t)N * 4 +
          ((N + 31) / 32) * 4 + 16;
 }
 
@@ -277,7 +277,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(CellDev c, const double2*
 
 // ------------------------------------------------------------------------------------------------
 // Standalone matrices (hx_eigvalsh_batch_device): lower triangle of A -> packed smem -> (diag, e2).
-__global__ void __launch_bounds__(256) eigvalsh_small_kernel(int n, const double2* __restrict__ A, double* tri,
+__global__ void __launch_bounds__(512) eigvalsh_small_kernel(int n, const double2* __restrict__ A, double* tri,
                                                              int* dims, int* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int ld = n | 1;
