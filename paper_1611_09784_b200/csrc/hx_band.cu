@@ -4,7 +4,7 @@
 //   panel_qr_kernel    Householder QR of the m x BW panel below the band (m = N - k0 - BW):
 //                      V (explicit, unit lower trapezoidal), T (zlarft forward/columnwise), R into A.
 //   hemm_kernel        X = A22 V                    (DMMA f64 tensor cores, complex as 4 real MMAs)
-//   w_kernel           W = X T - 1/2 V (T^H V^H X T)
+//   w_z/w_m/w_rows     W = X T - 1/2 V (T^H V^H X T)     (row-parallel)
 //   her2k_kernel       A22 -= W V^H + V W^H          (DMMA; lower tiles computed, upper mirrored)
 // so that A22 <- Q^H A22 Q with Q = I - V T V^H (the blocked two-sided update of zhetrd/zhe2hb).
 // Stage 2 (band -> tridiagonal): bulge_chase_pipe_kernel (hx_chase.cuh), pipelined Householder bulge chasing.
@@ -43,7 +43,7 @@ const char* band_last_error() { return g_band_err.c_str(); }
 
 struct BandWs {
   // per-matrix layout inside one workspace slab (offsets in double2 units)
-  size_t a_off, v_off, x_off, t_off, dg_off;  // dg: diag + e2 (2N doubles = N double2)
+  size_t a_off, v_off, x_off, t_off, z_off, m_off, dg_off;  // dg: diag + e2 (2N doubles = N double2)
   size_t stride;                             // per matrix, double2 units
   static BandWs make(int N) {
     BandWs w;
@@ -51,7 +51,9 @@ struct BandWs {
     w.v_off = (size_t)N * N;
     w.x_off = w.v_off + (size_t)N * BW;
     w.t_off = w.x_off + (size_t)N * BW;
-    w.dg_off = w.t_off + (size_t)BW * BW;
+    w.z_off = w.t_off + (size_t)BW * BW;
+    w.m_off = w.z_off + (size_t)16 * BW * BW;
+    w.dg_off = w.m_off + (size_t)BW * BW;
     w.stride = w.dg_off + (size_t)N + 16;
     w.stride = (w.stride + 15) & ~(size_t)15;
     return w;
@@ -241,30 +243,30 @@ __global__ void __launch_bounds__(128) hemm_kernel(double2* ws, BandWs L, int N,
 }
 
 // ------------------------------------------------------------------------------------------------
-// W = X T - 1/2 V M, M = T^H (V^H X) T.  One CTA (256 threads) per matrix; W overwrites X.
-__global__ void __launch_bounds__(256) w_kernel(double2* ws, BandWs L, int N, int k0) {
-  extern __shared__ double2 dsm[];
-  double2 (*Vt)[BW + 1] = reinterpret_cast<double2 (*)[BW + 1]>(dsm);
-  double2 (*Xt)[BW + 1] = reinterpret_cast<double2 (*)[BW + 1]>(dsm + 32 * (BW + 1));
-  double2 (*Zs)[BW + 1] = reinterpret_cast<double2 (*)[BW + 1]>(dsm + 64 * (BW + 1));
-  double2 (*Ms)[BW + 1] = reinterpret_cast<double2 (*)[BW + 1]>(dsm + 96 * (BW + 1));
-  double2 (*Tsh)[BW + 1] = reinterpret_cast<double2 (*)[BW + 1]>(dsm + 128 * (BW + 1));
-  double2* base = ws + (size_t)blockIdx.x * L.stride;
+// W = X T - 1/2 V M, M = T^H (V^H X) T, in three row-parallel steps (W overwrites X):
+//   w_z_kernel    partial Z_s = V[rows_s]^H X[rows_s] for nsplit row ranges of every matrix
+//   w_m_kernel    Z = sum_s Z_s (fixed order), M/2 = T^H Z T / 2          (one small CTA per matrix)
+//   w_rows_kernel W[rows] = X[rows] T - V[rows] (M/2)                      (32-row tiles)
+constexpr int W_SPLIT_MAX = 16;
+
+__global__ void __launch_bounds__(256) w_z_kernel(double2* ws, BandWs L, int N, int k0, int nsplit) {
+  __shared__ double2 Vt[32][BW + 1];
+  __shared__ double2 Xt[32][BW + 1];
+  double2* base = ws + (size_t)blockIdx.y * L.stride;
   const int m = N - k0 - BW;
   const double2* V = base + L.v_off;
-  double2* X = base + L.x_off;
-  const double2* T = base + L.t_off;
-  const int tid = threadIdx.x;
-  const int oc = tid & 31, orow = tid >> 5;  // this thread owns outputs (orow + 8q, oc), q < 4
-  for (int p = tid; p < BW * BW; p += 256) Tsh[p % BW][p / BW] = T[p];
+  const double2* X = base + L.x_off;
+  const int per = ((m + nsplit - 1) / nsplit + 31) & ~31;
+  const int ra = blockIdx.x * per, rb = min(m, ra + per);
+  const int tid = threadIdx.x, oc = tid & 31, orow = tid >> 5;
   double2 z[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) z[q] = make_double2(0.0, 0.0);
-  for (int r0 = 0; r0 < m; r0 += 32) {
+  for (int r0 = ra; r0 < rb; r0 += 32) {
     __syncthreads();
     for (int p = tid; p < 32 * BW; p += 256) {
       const int rr = p & 31, c = p >> 5;
-      const bool ok = r0 + rr < m;
+      const bool ok = r0 + rr < rb;
       Vt[rr][c] = ok ? V[r0 + rr + (size_t)c * N] : make_double2(0.0, 0.0);
       Xt[rr][c] = ok ? X[r0 + rr + (size_t)c * N] : make_double2(0.0, 0.0);
     }
@@ -280,13 +282,34 @@ __global__ void __launch_bounds__(256) w_kernel(double2* ws, BandWs L, int N, in
       }
     }
   }
-  __syncthreads();
+  double2* zp = base + L.z_off + (size_t)blockIdx.x * BW * BW;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) Zs[orow + 8 * q][oc] = z[q];
-  __syncthreads();
-  // Ms = Z T
+  for (int q = 0; q < 4; ++q) zp[(orow + 8 * q) * BW + oc] = z[q];
+}
+
+__global__ void __launch_bounds__(256) w_m_kernel(double2* ws, BandWs L, int nsplit) {
+  __shared__ double2 Zs[BW][BW];
+  __shared__ double2 Ms[BW][BW];
+  __shared__ double2 Tsh[BW][BW];
+  double2* base = ws + (size_t)blockIdx.x * L.stride;
+  const double2* T = base + L.t_off;
+  const double2* zp = base + L.z_off;
+  const int tid = threadIdx.x, oc = tid & 31, orow = tid >> 5;
+  for (int p = tid; p < BW * BW; p += 256) Tsh[p % BW][p / BW] = T[p];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
+    const int r = orow + 8 * q;
+    double2 t = make_double2(0.0, 0.0);
+    for (int s = 0; s < nsplit; ++s) {
+      const double2 u = zp[(size_t)s * BW * BW + r * BW + oc];
+      t = make_double2(t.x + u.x, t.y + u.y);
+    }
+    Zs[r][oc] = t;
+  }
+  __syncthreads();
+  double2 z[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // Ms = Z T
     const int r = orow + 8 * q;
     double2 t = make_double2(0.0, 0.0);
     for (int l = 0; l < BW; ++l) {
@@ -296,13 +319,12 @@ __global__ void __launch_bounds__(256) w_kernel(double2* ws, BandWs L, int N, in
     }
     z[q] = t;
   }
-  __syncthreads();
 #pragma unroll
   for (int q = 0; q < 4; ++q) Ms[orow + 8 * q][oc] = z[q];
   __syncthreads();
-  // Zs = T^H Ms  (= M)
+  double2* mh = base + L.m_off;
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < 4; ++q) {  // M/2 = T^H Ms / 2
     const int r = orow + 8 * q;
     double2 t = make_double2(0.0, 0.0);
     for (int l = 0; l < BW; ++l) {
@@ -310,39 +332,53 @@ __global__ void __launch_bounds__(256) w_kernel(double2* ws, BandWs L, int N, in
       t.x += a.x * b.x - a.y * b.y;
       t.y += a.x * b.y + a.y * b.x;
     }
-    z[q] = t;
+    mh[r * BW + oc] = make_double2(0.5 * t.x, 0.5 * t.y);
+  }
+}
+
+__global__ void __launch_bounds__(256) w_rows_kernel(double2* ws, BandWs L, int N, int k0) {
+  extern __shared__ double2 wsm[];
+  double2 (*Tsh)[BW] = reinterpret_cast<double2 (*)[BW]>(wsm);
+  double2 (*Mh)[BW] = reinterpret_cast<double2 (*)[BW]>(wsm + BW * BW);
+  double2 (*Xt)[BW + 1] = reinterpret_cast<double2 (*)[BW + 1]>(wsm + 2 * BW * BW);
+  double2 (*Vt)[BW + 1] = reinterpret_cast<double2 (*)[BW + 1]>(wsm + 2 * BW * BW + 32 * (BW + 1));
+  double2* base = ws + (size_t)blockIdx.y * L.stride;
+  const int m = N - k0 - BW;
+  const double2* V = base + L.v_off;
+  double2* X = base + L.x_off;
+  const double2* T = base + L.t_off;
+  const double2* mh = base + L.m_off;
+  const int tid = threadIdx.x, oc = tid & 31, orow = tid >> 5;
+  const int r0 = blockIdx.x * 32;
+  for (int p = tid; p < BW * BW; p += 256) {
+    Tsh[p % BW][p / BW] = T[p];
+    Mh[p / BW][p % BW] = mh[p];
+  }
+  for (int p = tid; p < 32 * BW; p += 256) {
+    const int rr = p & 31, c = p >> 5;
+    const bool ok = r0 + rr < m;
+    Vt[rr][c] = ok ? V[r0 + rr + (size_t)c * N] : make_double2(0.0, 0.0);
+    Xt[rr][c] = ok ? X[r0 + rr + (size_t)c * N] : make_double2(0.0, 0.0);
   }
   __syncthreads();
+  double2 z[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) Zs[orow + 8 * q][oc] = make_double2(0.5 * z[q].x, 0.5 * z[q].y);
-  __syncthreads();
-  // W rows: W = X T - V (M/2)
-  for (int r0 = 0; r0 < m; r0 += 32) {
-    for (int p = tid; p < 32 * BW; p += 256) {
-      const int rr = p & 31, c = p >> 5;
-      const bool ok = r0 + rr < m;
-      Vt[rr][c] = ok ? V[r0 + rr + (size_t)c * N] : make_double2(0.0, 0.0);
-      Xt[rr][c] = ok ? X[r0 + rr + (size_t)c * N] : make_double2(0.0, 0.0);
+  for (int q = 0; q < 4; ++q) {
+    const int rr = orow + 8 * q;
+    double2 t = make_double2(0.0, 0.0);
+#pragma unroll 8
+    for (int l = 0; l < BW; ++l) {
+      const double2 x = Xt[rr][l], v = Vt[rr][l];
+      const double2 tt = Tsh[l][oc], mm = Mh[l][oc];
+      t.x += (x.x * tt.x - x.y * tt.y) - (v.x * mm.x - v.y * mm.y);
+      t.y += (x.x * tt.y + x.y * tt.x) - (v.x * mm.y + v.y * mm.x);
     }
-    __syncthreads();
+    z[q] = t;
+  }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int rr = orow + 8 * q;
-      double2 t = make_double2(0.0, 0.0);
-      for (int l = 0; l < BW; ++l) {
-        const double2 x = Xt[rr][l], tt = Tsh[l][oc], v = Vt[rr][l], mm = Zs[l][oc];
-        t.x += (x.x * tt.x - x.y * tt.y) - (v.x * mm.x - v.y * mm.y);
-        t.y += (x.x * tt.y + x.y * tt.x) - (v.x * mm.y + v.y * mm.x);
-      }
-      z[q] = t;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int rr = orow + 8 * q;
-      if (r0 + rr < m) X[r0 + rr + (size_t)oc * N] = z[q];
-    }
-    __syncthreads();
+  for (int q = 0; q < 4; ++q) {
+    const int rr = orow + 8 * q;
+    if (r0 + rr < m) X[r0 + rr + (size_t)oc * N] = z[q];
   }
 }
 
@@ -474,12 +510,13 @@ __global__ void __launch_bounds__(256) band_copy_kernel(const double2* __restric
 
 // ------------------------------------------------------------------------------------------------
 constexpr size_t HEMM_SMEM = (size_t)(HM_TM + BW) * HM_LD * sizeof(double2);
-constexpr size_t W_SMEM = (size_t)160 * (BW + 1) * sizeof(double2);
 constexpr size_t HER2K_SMEM = (size_t)4 * HK_T * HK_LD * sizeof(double2);
 
 constexpr size_t PANEL_SMEM_MAX = 200 * 1024;
+constexpr size_t W_ROWS_SMEM = (size_t)(2 * BW * BW + 64 * (BW + 1)) * sizeof(double2);
 
 void band_init_attributes() {
+  cudaFuncSetAttribute(w_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W_ROWS_SMEM);
   cudaFuncSetAttribute(panel_qr_cluster_kernel<2, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)PANEL_SMEM_MAX);
   cudaFuncSetAttribute(panel_qr_cluster_kernel<4, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -488,7 +525,6 @@ void band_init_attributes() {
                        (int)PANEL_SMEM_MAX);
   cudaFuncSetAttribute(band_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   cudaFuncSetAttribute(hemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HEMM_SMEM);
-  cudaFuncSetAttribute(w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W_SMEM);
   cudaFuncSetAttribute(her2k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HER2K_SMEM);
   cudaFuncSetAttribute(bulge_chase_pipe_kernel<1, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)chase_smem_bytes<1, BW>());
@@ -533,7 +569,11 @@ static int band_reduce(double2* ws, const BandWs& L, int N, int64_t cnt, const i
     }
     const unsigned mt = (unsigned)((m + HM_TM - 1) / HM_TM);
     hemm_kernel<<<dim3(mt, (unsigned)cnt), 128, HEMM_SMEM, st>>>(ws, L, N, k0);
-    w_kernel<<<(unsigned)cnt, 256, W_SMEM, st>>>(ws, L, N, k0);
+    const int nsplit = std::min(W_SPLIT_MAX, std::max(1, (m + 127) / 128));
+    w_z_kernel<<<dim3((unsigned)nsplit, (unsigned)cnt), 256, 0, st>>>(ws, L, N, k0, nsplit);
+    w_m_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, L, nsplit);
+    w_rows_kernel<<<dim3((unsigned)((m + 31) / 32), (unsigned)cnt), 256, W_ROWS_SMEM, st>>>(ws, L, N, k0);
+    count_launch(2);
     const unsigned tt = (unsigned)((m + HK_T - 1) / HK_T);
     her2k_kernel<<<dim3(tt * (tt + 1) / 2, (unsigned)cnt), 256, HER2K_SMEM, st>>>(ws, L, N, k0);
     count_launch(4);
