@@ -66,6 +66,10 @@ typedef struct hx_cell_desc {
   int32_t pencil;          /* HX_PENCIL_* */
   double eps0, t, s;       /* HX_PENCIL_COMMUTING parameters; h_amp then holds T's amplitudes */
   double area;             /* supercell area in per-unit-area units (lattice.py:131-133) */
+  /* optional [ndof] sublattice (basis index) of each dof.  With HX_PENCIL_COMMUTING and hops that all
+   * join sublattice 0 to 1 (graphene), T = [[0, C], [C^H, 0]] and the library may use the exact
+   * bipartite identity eig(T) = +-sigma(C) (+ zeros).  NULL disables it. */
+  const int32_t* sublattice;
 } hx_cell_desc;
 
 /* Energy grid + smoothing (qoi.py:42-67, 77-82): eps_m = e0 + step*m, m < npts. */

@@ -2,6 +2,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -65,6 +66,7 @@ struct hx_ctx {
   cudaStream_t stream = nullptr;
   DevBuf kpts, diff, trans, ws, masks, curves, eigs, status, band, tri, refine;
   size_t ws_budget = (size_t)24 << 30;  // HBM workspace budget for the global / banded paths
+  bool use_bipartite = true;            // graphene: singular values of the A-B block (HX_NO_BIPARTITE=1 disables)
 };
 
 struct hx_cell {
@@ -165,6 +167,11 @@ int hx_ctx_create(int32_t device, hx_ctx** out) {
   }
   size_t freeb = 0, total = 0;
   cudaMemGetInfo(&freeb, &total);
+  {
+    const char* nb = getenv("HX_NO_BIPARTITE");
+    ctx->use_bipartite = !(nb && nb[0] && nb[0] != '0');
+  }
+  cudaFuncSetAttribute(hx::small_bidiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   ctx->ws_budget = std::min(ctx->ws_budget, freeb / 3);
   cudaFuncSetAttribute(hx::small_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)hx::small_tridiag_smem(HX_SMEM_MAX_N));
@@ -215,6 +222,23 @@ int hx_cell_create(hx_ctx* ctx, const hx_cell_desc* d, hx_cell** out) {
   c.area = d->area;
   int rc = 0;
   rc |= upload(cell, d->unit_of_dof, N, &c.unit_of_dof);
+  c.bipartite = 0;
+  c.nsub = 0;
+  if (d->sublattice && d->pencil == HX_PENCIL_COMMUTING) {
+    bool ok = true;
+    int n0 = 0, n1 = 0;
+    for (int r = 0; r < N; ++r) {
+      const int sr = d->sublattice[r];
+      if (sr != 0 && sr != 1) ok = false;
+      (sr == 0 ? n0 : n1) += 1;
+      for (int e = d->h_row_ptr[r]; e < d->h_row_ptr[r + 1]; ++e) ok &= d->sublattice[d->h_col[e]] != sr;
+    }
+    if (ok) {
+      c.bipartite = 1;
+      c.nsub = std::max(n0, n1);
+      rc |= upload(cell, d->sublattice, N, &c.sub);
+    }
+  }
   rc |= upload(cell, d->onsite, N, &c.onsite);
   {
     const int nnz = d->h_row_ptr[N];
@@ -317,8 +341,14 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
       const int64_t cnt = std::min(chunk, nmat - m0);
       // masks/kpts offsets: the kernel indexes matrices from blockIdx.x; shift the mask base by whole masks
       if (m0 % nk) return fail(HX_E_ARG, "internal: chunk not aligned to k-point groups");
-      hx::small_tridiag_kernel<<<(unsigned)cnt, N > 64 ? 512 : 256, smem, st>>>(c, kp, nk, d_masks + (m0 / nk) * c.words, tri, dims,
-                                                                status + m0);
+      const uint64_t* mk0 = d_masks + (m0 / nk) * c.words;
+      if (c.bipartite && ctx->use_bipartite && hx::small_bidiag_smem(N, c.nsub) <= 200 * 1024) {
+        hx::small_bidiag_kernel<<<(unsigned)cnt, N > 64 ? 256 : 128, hx::small_bidiag_smem(N, c.nsub), st>>>(
+            c, kp, nk, mk0, tri, dims, status + m0);
+      } else {
+        hx::small_tridiag_kernel<<<(unsigned)cnt, N > 64 ? 512 : 256, smem, st>>>(c, kp, nk, mk0, tri, dims,
+                                                                                 status + m0);
+      }
       HX_CUDA(cudaGetLastError());
       hx::count_launch();
       hx::launch_eig_idos(c, nk, g, m0, cnt, tri, (size_t)2 * N, dims, diff, trans, d_eigs, status, sharp, st, refine,

@@ -34,6 +34,10 @@ struct CellDev {
   const int32_t* st_ptr;
   const int32_t* st_inst;
   const int32_t* s_src;
+  // bipartite commuting pencil (graphene): every hop joins sublattice 0 and 1 -> T = [[0, C], [C^H, 0]]
+  int32_t bipartite;
+  int32_t nsub;        // max dofs on one sublattice
+  const int32_t* sub;  // [N] sublattice of each dof
 };
 
 struct GridDev {

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "hx_bidiag.cuh"
 #include "hx_dense.cuh"
 #include "hx_kernels.cuh"
 
@@ -45,6 +46,42 @@ __global__ void __launch_bounds__(512) small_tridiag_kernel(CellDev c, const dou
   if (d == 0) return;
   assemble_packed(c, new_idx, d, kpts[kk], R, ld);
   tridiag_packed(R, ld, d, diag, e2, v, y, red);
+}
+
+// Bipartite (graphene) variant: bidiagonalise the nA x nB block C instead of tridiagonalising T.
+__global__ void __launch_bounds__(256) small_bidiag_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
+                                                           const uint64_t* __restrict__ masks, double* tri, int* dims,
+                                                           int* status) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int N = c.N, S = c.nsub;
+  const int lm = S + 1;
+  const int64_t mat = blockIdx.x;
+  const int64_t mk = mat / nk;
+  const int kk = (int)(mat - mk * nk);
+  double2* M = reinterpret_cast<double2*>(smem_raw);
+  double2* u = M + (size_t)lm * S;
+  double2* s = u + S + 1;
+  double* red = reinterpret_cast<double*>(s + S + 1);  // 128
+  int* idx_a = reinterpret_cast<int*>(red + 128);      // N
+  int* idx_b = idx_a + N;                              // N
+  int* cnt = idx_b + N;                                // 2 ceil(N/32)
+  double* diag = tri + mat * 2 * N;
+  double* e2 = diag + N;
+  const int2 nn = block_compact_bipartite(c, masks + mk * c.words, idx_a, idx_b, cnt);
+  const int d = nn.x + nn.y;
+  if (threadIdx.x == 0) {
+    dims[mat] = d;
+    status[mat] = d == 0 ? 3 : 0;
+  }
+  if (d == 0) return;
+  const bool transpose = nn.x < nn.y;
+  const int rows = transpose ? nn.y : nn.x, cols = transpose ? nn.x : nn.y;
+  assemble_bipartite(c, idx_a, idx_b, kpts[kk], M, lm, rows, cols, transpose);
+  bidiag_tgk(M, lm, rows, cols, diag, e2, u, s, red);
+}
+
+size_t small_bidiag_smem(int N, int S) {
+  return ((size_t)(S + 1) * S + 2 * (S + 1)) * 16 + 128 * 8 + (size_t)N * 8 + 2 * ((N + 31) / 32) * 4 + 16;
 }
 
 size_t small_tridiag_smem(int N) {

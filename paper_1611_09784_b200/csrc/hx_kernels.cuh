@@ -24,6 +24,9 @@ struct RefineItem {
 __global__ void small_tridiag_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, double* tri,
                                      int* dims, int* status);
 size_t small_tridiag_smem(int N);
+__global__ void small_bidiag_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, double* tri,
+                                    int* dims, int* status);
+size_t small_bidiag_smem(int N, int S);
 
 __global__ void global_tridiag_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, int64_t mat0,
                                       unsigned char* ws, size_t ws_stride, double* tri, int* dims, int* status);

@@ -228,6 +228,9 @@ class CompiledCell:
             desc.pencil = self.pencil
             desc.eps0, desc.t, desc.s = self.pencil_params
             desc.area = float(self.supercell.area)
+            sub = np.ascontiguousarray(self.supercell.basis_index[self.dof_site], dtype=np.int32)
+            keep.append(sub)
+            desc.sublattice = _lib.ptr(sub)
             h = C.c_void_p()
             _lib.check(lib.hx_cell_create(ctx, C.byref(desc), C.byref(h)), "hx_cell_create")
             self._handle = h
