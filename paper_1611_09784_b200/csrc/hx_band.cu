@@ -538,35 +538,29 @@ void band_init_attributes() {
 
 bool band_path_supported(int N) { return N > HX_SMEM_MAX_N && N <= HX_MAX_N; }
 
+// Smallest cluster (2, 4, 8 CTAs) whose shared memory holds the panel; false if none fits.
+bool launch_cluster_panel(double2* ws, const PanelArgs& a, int64_t cnt, cudaStream_t st) {
+  for (int cl : {2, 4, 8}) {
+    const int r = (a.m + cl - 1) / cl;
+    const size_t psm = panel_cluster_smem<BW>(r);
+    if (psm > PANEL_SMEM_MAX) continue;
+    if (cl == 2) panel_qr_cluster_kernel<2, BW><<<dim3(2, (unsigned)cnt), 256, psm, st>>>(ws, a, r);
+    else if (cl == 4) panel_qr_cluster_kernel<4, BW><<<dim3(4, (unsigned)cnt), 256, psm, st>>>(ws, a, r);
+    else panel_qr_cluster_kernel<8, BW><<<dim3(8, (unsigned)cnt), 256, psm, st>>>(ws, a, r);
+    return true;
+  }
+  return false;
+}
+
 // Stage 1 + 2 for `cnt` matrices already staged in the workspace.
 static int band_reduce(double2* ws, const BandWs& L, int N, int64_t cnt, const int* dims, cudaStream_t st) {
   for (int k0 = 0; N - k0 - BW > 0; k0 += BW) {
     const int m = N - k0 - BW;
-    // cluster panel QR: smallest cluster whose shared memory holds the panel slices
-    // (large batches keep every SM busy with one single-CTA panel per matrix instead)
-    int CL = 0, R = 0;
-    for (int cl : {2, 4, 8}) {
-      if (cnt >= 512) break;
-      const int r = (m + cl - 1) / cl;
-      if (panel_cluster_smem<BW>(r) <= PANEL_SMEM_MAX) {
-        CL = cl;
-        R = r;
-        break;
-      }
-    }
-    const size_t psm = panel_cluster_smem<BW>(R);
-    if (CL == 2) {
-      panel_qr_cluster_kernel<2, BW><<<dim3(2, (unsigned)cnt), 256, psm, st>>>(ws, L.stride, L.a_off, L.v_off,
-                                                                              L.t_off, N, k0, R);
-    } else if (CL == 4) {
-      panel_qr_cluster_kernel<4, BW><<<dim3(4, (unsigned)cnt), 256, psm, st>>>(ws, L.stride, L.a_off, L.v_off,
-                                                                              L.t_off, N, k0, R);
-    } else if (CL == 8) {
-      panel_qr_cluster_kernel<8, BW><<<dim3(8, (unsigned)cnt), 256, psm, st>>>(ws, L.stride, L.a_off, L.v_off,
-                                                                              L.t_off, N, k0, R);
-    } else {
-      panel_qr_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, L, N, k0);  // very tall panels: L2-resident fallback
-    }
+    // cluster panel QR for small batches (large batches keep every SM busy with one single-CTA panel
+    // per matrix instead); very tall panels use the L2-resident single-CTA kernel
+    PanelArgs pa{L.stride, L.a_off, N, k0 + BW, k0, m, 0, L.v_off, N, L.t_off};
+    if (cnt >= 512 || !launch_cluster_panel(ws, pa, cnt, st))
+      panel_qr_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, L, N, k0);
     const unsigned mt = (unsigned)((m + HM_TM - 1) / HM_TM);
     hemm_kernel<<<dim3(mt, (unsigned)cnt), 128, HEMM_SMEM, st>>>(ws, L, N, k0);
     const int nsplit = std::min(W_SPLIT_MAX, std::max(1, (m + 127) / 128));

@@ -25,4 +25,12 @@ int band_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks
 int band_eigvalsh(int n, int64_t batch, const double2* A, double* eigs, int* status, size_t ws_budget,
                   const Alloc& alloc, cudaStream_t st);
 
+// Bipartite (graphene) banded tier: singular values of the A-B block (hx_bdband.cu).
+void bd_init_attributes();
+bool bd_path_supported(const CellDev& c);
+const char* bd_last_error();
+int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, int64_t nmasks, const GridDev& g,
+            int* diff, unsigned long long* trans, double* eigs, int* status, int sharp, size_t ws_budget,
+            const Alloc& alloc, cudaStream_t st, RefineItem* refine, unsigned long long* refine_count);
+
 }  // namespace hx

@@ -1,0 +1,361 @@
+// Bipartite (graphene) banded tier: singular values of the nA x nB block C of T = [[0, C], [C^H, 0]].
+//
+// eig(T) = +-sigma(C) plus |nA - nB| zeros (exact), and for the commuting pencil eps = (eps0 + t l)/(1 + s l).
+// C is assembled into an S x S slab (S = max sublattice size, zero padded: the padding stays exactly
+// zero under every reflector) and reduced in two stages:
+//   stage 1 (dense -> upper band, width BW), per step k0:
+//     column panel QR  C[k0:, k0:k0+BW] = Q1 R          (cluster/DSMEM panel kernel, mode 0)
+//     X1 = C_tr^H V1 ; X1 <- X1 T1 ; C_tr -= V1 X1^H      (left update Q1^H C_tr, DMMA)
+//     row panel LQ     C[k0:k0+BW, k0+BW:] = R^H Q2^H  (QR of the conj-transposed block, mode 1)
+//     Z = C_tr2 V2 ; Z <- Z T2 ; C_tr2 -= Z V2^H          (right update C_tr2 Q2, DMMA)
+//   stage 2 (upper band -> bidiagonal) by bulge chasing (bd_chase_kernel below, one warp per sweep).
+// The Golub-Kahan tridiagonal (zero diagonal, off-diagonals alpha_0, gamma_0, alpha_1, ...) truncated to
+// d = nA + nB entries has exactly the eigenvalues of T; it goes through the shared bisection + IDOS kernel.
+// Flops: ~4/3 S'^3 ... i.e. 4x fewer than tridiagonalising T, on a 4x smaller slab.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <string>
+
+#include "hx_band.cuh"
+#include "hx_bidiag.cuh"
+#include "hx_dense.cuh"
+#include "hx_dmma.cuh"
+#include "hx_kernels.cuh"
+#include "hx_panel.cuh"
+#include "hx_bdchase.cuh"
+
+namespace hx {
+
+constexpr int BB = 32;  // band width
+
+static std::string g_bd_err;
+const char* bd_last_error() { return g_bd_err.c_str(); }
+
+#define BD_CUDA(call)                                                 \
+  do {                                                                \
+    cudaError_t e_ = (call);                                          \
+    if (e_ != cudaSuccess) {                                          \
+      g_bd_err = std::string(#call) + ": " + cudaGetErrorString(e_); \
+      return -1;                                                      \
+    }                                                                 \
+  } while (0)
+
+struct BdWs {
+  size_t c_off, v1_off, v2_off, x_off, t1_off, t2_off, tgk_off;  // double2 units
+  size_t stride;
+  int S;
+  static BdWs make(int S) {
+    BdWs w;
+    w.S = S;
+    w.c_off = 0;
+    w.v1_off = (size_t)S * S;
+    w.v2_off = w.v1_off + (size_t)S * BB;
+    w.x_off = w.v2_off + (size_t)S * BB;
+    w.t1_off = w.x_off + (size_t)S * BB;
+    w.t2_off = w.t1_off + (size_t)BB * BB;
+    w.tgk_off = w.t2_off + (size_t)BB * BB;  // diag[2S] + e2[2S] doubles = 2S double2
+    w.stride = (w.tgk_off + (size_t)2 * S + 16 + 15) & ~(size_t)15;
+    return w;
+  }
+};
+
+__device__ __forceinline__ double2 conj2(double2 a) { return make_double2(a.x, -a.y); }
+
+// ------------------------------------------------------------------------------------------------
+// C = A-B block of the phase matrix per (mask, k), zero padded to S x S; dims = nA + nB.
+__global__ void __launch_bounds__(256) bd_assemble_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
+                                                          const uint64_t* __restrict__ masks, int64_t mat0,
+                                                          double2* ws, BdWs L, int* dims, int* status) {
+  extern __shared__ int bsm[];
+  int* idx_a = bsm;
+  int* idx_b = idx_a + c.N;
+  int* cnt = idx_b + c.N;
+  const int64_t mat = mat0 + blockIdx.x;
+  const int64_t mk = mat / nk;
+  const int kk = (int)(mat - mk * nk);
+  double2* C = ws + (size_t)blockIdx.x * L.stride + L.c_off;
+  const int2 nn = block_compact_bipartite(c, masks + mk * c.words, idx_a, idx_b, cnt);
+  const int d = nn.x + nn.y;
+  if (threadIdx.x == 0) {
+    dims[blockIdx.x] = d;
+    status[mat] = d == 0 ? 3 : 0;
+  }
+  assemble_bipartite(c, idx_a, idx_b, kpts[kk], C, L.S, L.S, L.S, false);
+}
+
+// ------------------------------------------------------------------------------------------------
+// X[rows x BB] = op(A) V, op(A)[i][k] = M[ar0+i][ac0+k] (MODE 0) or conj(M[ar0+k][ac0+i]) (MODE 1),
+// V [K x BB] (ld S).  64-row tiles, 4 warps x (16 x 32), DMMA m8n8k4 f64.
+constexpr int XV_TM = 64, XV_TK = 16, XV_LD = XV_TK + 4;
+
+template <int MODE>
+__global__ void __launch_bounds__(128) xv_kernel(double2* ws, BdWs L, int ar0, int ac0, int rows, int K,
+                                                 size_t v_off, size_t x_off) {
+  __shared__ double2 As[XV_TM][XV_LD];
+  __shared__ double2 Vs[BB][XV_LD];
+  double2* base = ws + (size_t)blockIdx.y * L.stride;
+  const int ld = L.S;
+  const double2* M = base + L.c_off;
+  const double2* V = base + v_off;
+  double2* X = base + x_off;
+  const int i0 = blockIdx.x * XV_TM;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  CTile acc[2][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b].zero();
+  for (int kk = 0; kk < K; kk += XV_TK) {
+    if (MODE == 1) {
+      for (int p = tid; p < XV_TM * XV_TK; p += 128) {
+        const int cc = p & (XV_TK - 1), r = p / XV_TK;
+        const int gi = i0 + r, gk = kk + cc;
+        double2 z = make_double2(0.0, 0.0);
+        if (gi < rows && gk < K) z = M[(size_t)(ac0 + gi) * ld + ar0 + gk];
+        As[r][cc] = conj2(z);
+      }
+    } else {
+      for (int p = tid; p < XV_TM * XV_TK; p += 128) {
+        const int r = p & (XV_TM - 1), cc = p / XV_TM;
+        const int gi = i0 + r, gk = kk + cc;
+        double2 z = make_double2(0.0, 0.0);
+        if (gi < rows && gk < K) z = M[(size_t)(ac0 + gk) * ld + ar0 + gi];
+        As[r][cc] = z;
+      }
+    }
+    for (int p = tid; p < BB * XV_TK; p += 128) {
+      const int cc = p & (XV_TK - 1), n = p / XV_TK;
+      const int gk = kk + cc;
+      Vs[n][cc] = gk < K ? V[gk + (size_t)n * ld] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k4 = 0; k4 < XV_TK / 4; ++k4) {
+      const int kc = 4 * k4 + (lane & 3);
+      double2 a[2], b[4];
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt) a[rt] = As[16 * warp + 8 * rt + (lane >> 2)][kc];
+#pragma unroll
+      for (int ct = 0; ct < 4; ++ct) b[ct] = Vs[8 * ct + (lane >> 2)][kc];
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(a[rt].x, a[rt].y, b[ct].x, b[ct].y);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+    for (int ct = 0; ct < 4; ++ct) {
+      const int r = i0 + 16 * warp + 8 * rt + (lane >> 2);
+      const int cc = 8 * ct + 2 * (lane & 3);
+      if (r < rows) {
+        X[r + (size_t)cc * ld] = make_double2(acc[rt][ct].re0, acc[rt][ct].im0);
+        X[r + (size_t)(cc + 1) * ld] = make_double2(acc[rt][ct].re1, acc[rt][ct].im1);
+      }
+    }
+}
+
+// X <- X T (rows x BB, ld S), 32-row tiles.
+__global__ void __launch_bounds__(256) xt_kernel(double2* ws, BdWs L, int rows, size_t x_off, size_t t_off) {
+  __shared__ double2 Tsh[BB][BB];
+  __shared__ double2 Xt[32][BB + 1];
+  double2* base = ws + (size_t)blockIdx.y * L.stride;
+  double2* X = base + x_off;
+  const double2* T = base + t_off;
+  const int ld = L.S;
+  const int tid = threadIdx.x, oc = tid & 31, orow = tid >> 5;
+  const int r0 = blockIdx.x * 32;
+  for (int p = tid; p < BB * BB; p += 256) Tsh[p % BB][p / BB] = T[p];
+  for (int p = tid; p < 32 * BB; p += 256) {
+    const int rr = p & 31, cc = p >> 5;
+    Xt[rr][cc] = r0 + rr < rows ? X[r0 + rr + (size_t)cc * ld] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int rr = orow + 8 * q;
+    double2 t = make_double2(0.0, 0.0);
+#pragma unroll 8
+    for (int l = 0; l < BB; ++l) {
+      const double2 x = Xt[rr][l], tt = Tsh[l][oc];
+      t.x += x.x * tt.x - x.y * tt.y;
+      t.y += x.x * tt.y + x.y * tt.x;
+    }
+    if (r0 + rr < rows) X[r0 + rr + (size_t)oc * ld] = t;
+  }
+}
+
+// M[mr0:mr0+m, mc0:mc0+n] -= U W^H, U [m x BB] and W [n x BB] (ld S); 64 x 64 tiles, DMMA.
+constexpr int RU_T = 64, RU_K = 16, RU_LD = RU_K + 4;
+
+__global__ void __launch_bounds__(256) rank_update_kernel(double2* ws, BdWs L, int mr0, int mc0, int m, int n,
+                                                          size_t u_off, size_t w_off) {
+  __shared__ double2 Us[RU_T][RU_LD];
+  __shared__ double2 Ws[RU_T][RU_LD];
+  double2* base = ws + (size_t)blockIdx.z * L.stride;
+  const int ld = L.S;
+  double2* M = base + L.c_off + (size_t)mc0 * ld + mr0;
+  const double2* U = base + u_off;
+  const double2* W = base + w_off;
+  const int I0 = blockIdx.x * RU_T, J0 = blockIdx.y * RU_T;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp & 3, wc = warp >> 2;
+  CTile acc[2][4];
+#pragma unroll
+  for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+    for (int ct = 0; ct < 4; ++ct) {
+      const int r = I0 + 16 * wr + 8 * rt + (lane >> 2);
+      const int cc = J0 + 32 * wc + 8 * ct + 2 * (lane & 3);
+      double2 z0 = make_double2(0.0, 0.0), z1 = make_double2(0.0, 0.0);
+      if (r < m && cc < n) z0 = M[r + (size_t)cc * ld];
+      if (r < m && cc + 1 < n) z1 = M[r + (size_t)(cc + 1) * ld];
+      acc[rt][ct].re0 = z0.x;
+      acc[rt][ct].im0 = z0.y;
+      acc[rt][ct].re1 = z1.x;
+      acc[rt][ct].im1 = z1.y;
+    }
+  for (int kk = 0; kk < BB; kk += RU_K) {
+    __syncthreads();
+    for (int p = tid; p < RU_T * RU_K; p += 256) {
+      const int r = p & (RU_T - 1), k = p / RU_T;
+      const size_t col = (size_t)(kk + k) * ld;
+      Us[r][k] = I0 + r < m ? U[I0 + r + col] : make_double2(0.0, 0.0);
+      Ws[r][k] = J0 + r < n ? W[J0 + r + col] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k4 = 0; k4 < RU_K / 4; ++k4) {
+      const int kc = 4 * k4 + (lane & 3);
+      double2 au[2], bw[4];
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt) au[rt] = Us[16 * wr + 8 * rt + (lane >> 2)][kc];
+#pragma unroll
+      for (int ct = 0; ct < 4; ++ct) bw[ct] = conj2(Ws[32 * wc + 8 * ct + (lane >> 2)][kc]);
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(-au[rt].x, -au[rt].y, bw[ct].x, bw[ct].y);
+    }
+  }
+#pragma unroll
+  for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+    for (int ct = 0; ct < 4; ++ct) {
+      const int r = I0 + 16 * wr + 8 * rt + (lane >> 2);
+      const int cc = J0 + 32 * wc + 8 * ct + 2 * (lane & 3);
+      if (r < m && cc < n) M[r + (size_t)cc * ld] = make_double2(acc[rt][ct].re0, acc[rt][ct].im0);
+      if (r < m && cc + 1 < n) M[r + (size_t)(cc + 1) * ld] = make_double2(acc[rt][ct].re1, acc[rt][ct].im1);
+    }
+}
+
+
+// ------------------------------------------------------------------------------------------------
+bool launch_cluster_panel(double2* ws, const PanelArgs& a, int64_t cnt, cudaStream_t st);
+
+static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, cudaStream_t st) {
+  const int S = L.S;
+  for (int k0 = 0; k0 < S; k0 += BB) {
+    const int m1 = S - k0, n2 = S - k0 - BB;
+    // ---- left: column panel QR, C_tr = C[k0:, k0+BB:] <- Q1^H C_tr
+    PanelArgs p1{L.stride, L.c_off, S, k0, k0, m1, 0, L.v1_off, S, L.t1_off};
+    if (!launch_cluster_panel(ws, p1, cnt, st)) {
+      g_bd_err = "panel does not fit the cluster shared memory";
+      return -1;
+    }
+    count_launch();
+    if (n2 <= 0) break;
+    xv_kernel<1><<<dim3((unsigned)((n2 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, 0, st>>>(ws, L, k0, k0 + BB, n2, m1,
+                                                                                           L.v1_off, L.x_off);
+    xt_kernel<<<dim3((unsigned)((n2 + 31) / 32), (unsigned)cnt), 256, 0, st>>>(ws, L, n2, L.x_off, L.t1_off);
+    rank_update_kernel<<<dim3((unsigned)((m1 + RU_T - 1) / RU_T), (unsigned)((n2 + RU_T - 1) / RU_T), (unsigned)cnt),
+                         256, 0, st>>>(ws, L, k0, k0 + BB, m1, n2, L.v1_off, L.x_off);
+    count_launch(3);
+    // ---- right: row panel LQ, C_tr2 = C[k0+BB:, k0+BB:] <- C_tr2 Q2
+    PanelArgs p2{L.stride, L.c_off, S, k0, k0 + BB, n2, 1, L.v2_off, S, L.t2_off};
+    if (!launch_cluster_panel(ws, p2, cnt, st)) {
+      g_bd_err = "panel does not fit the cluster shared memory";
+      return -1;
+    }
+    count_launch();
+    const int m3 = S - k0 - BB;
+    if (m3 > 0) {
+      xv_kernel<0><<<dim3((unsigned)((m3 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, 0, st>>>(
+          ws, L, k0 + BB, k0 + BB, m3, n2, L.v2_off, L.x_off);
+      xt_kernel<<<dim3((unsigned)((m3 + 31) / 32), (unsigned)cnt), 256, 0, st>>>(ws, L, m3, L.x_off, L.t2_off);
+      rank_update_kernel<<<dim3((unsigned)((m3 + RU_T - 1) / RU_T), (unsigned)((n2 + RU_T - 1) / RU_T),
+                                (unsigned)cnt),
+                           256, 0, st>>>(ws, L, k0 + BB, k0 + BB, m3, n2, L.x_off, L.v2_off);
+      count_launch(3);
+    }
+    BD_CUDA(cudaGetLastError());
+  }
+  // ---- stage 2
+  const int64_t want = (148 * 11 + cnt - 1) / cnt;
+  if (want >= 6) {
+    bd_chase_kernel<6, BB><<<(unsigned)cnt, 6 * 32, bd_chase_smem<6, BB>(), st>>>(ws, L.stride, L.c_off, L.tgk_off, S,
+                                                                                  dims);
+  } else if (want >= 2) {
+    bd_chase_kernel<2, BB><<<(unsigned)cnt, 2 * 32, bd_chase_smem<2, BB>(), st>>>(ws, L.stride, L.c_off, L.tgk_off, S,
+                                                                                  dims);
+  } else {
+    bd_chase_kernel<1, BB><<<(unsigned)cnt, 32, bd_chase_smem<1, BB>(), st>>>(ws, L.stride, L.c_off, L.tgk_off, S,
+                                                                              dims);
+  }
+  count_launch();
+  BD_CUDA(cudaGetLastError());
+  return 0;
+}
+
+void bd_init_attributes() {
+  cudaFuncSetAttribute(bd_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+  cudaFuncSetAttribute(bd_chase_kernel<1, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)bd_chase_smem<1, BB>());
+  cudaFuncSetAttribute(bd_chase_kernel<2, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)bd_chase_smem<2, BB>());
+  cudaFuncSetAttribute(bd_chase_kernel<6, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)bd_chase_smem<6, BB>());
+}
+
+int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, int64_t nmasks, const GridDev& g,
+            int* diff, unsigned long long* trans, double* eigs, int* status, int sharp, size_t ws_budget,
+            const Alloc& alloc, cudaStream_t st, RefineItem* refine, unsigned long long* refine_count) {
+  const int S = c.nsub;
+  const BdWs L = BdWs::make(S);
+  const size_t per = L.stride * sizeof(double2) + sizeof(int);
+  const int64_t nmat = nmasks * nk;
+  int64_t chunk = std::max<int64_t>(1, (int64_t)(ws_budget / per));
+  chunk = std::min<int64_t>(std::min<int64_t>(chunk, nmat), 65535);
+  unsigned char* buf = static_cast<unsigned char*>(alloc(per * (size_t)chunk + 256));
+  if (!buf) {
+    g_bd_err = "workspace allocation failed";
+    return -1;
+  }
+  double2* ws = reinterpret_cast<double2*>(buf);
+  int* dims = reinterpret_cast<int*>(buf + L.stride * sizeof(double2) * chunk);
+  const size_t smem = (size_t)c.N * 8 + 2 * ((c.N + 31) / 32) * 4 + 64;
+  // TGK tridiagonal of dimension up to 2S: eigenvalue kernel over cells of width 2S
+  CellDev ce = c;
+  ce.N = 2 * S;
+  for (int64_t m0 = 0; m0 < nmat; m0 += chunk) {
+    const int64_t cnt = std::min(chunk, nmat - m0);
+    bd_assemble_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, masks, m0, ws, L, dims, status);
+    count_launch();
+    BD_CUDA(cudaGetLastError());
+    if (bd_reduce(ws, L, cnt, dims, st)) return -1;
+    launch_eig_idos(ce, nk, g, m0, cnt, reinterpret_cast<const double*>(ws + L.tgk_off), L.stride * 2, dims, diff,
+                    trans, eigs, status, sharp, st, refine, refine_count);
+    BD_CUDA(cudaGetLastError());
+  }
+  return 0;
+}
+
+bool bd_path_supported(const CellDev& c) {
+  return c.bipartite && c.nsub >= 48 && 2 * c.nsub == c.N && c.N <= HX_MAX_N;
+}
+
+}  // namespace hx

@@ -178,6 +178,7 @@ int hx_ctx_create(int32_t device, hx_ctx** out) {
   cudaFuncSetAttribute(hx::eigvalsh_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)hx::small_tridiag_smem(HX_SMEM_MAX_N));
   hx::band_init_attributes();
+  hx::bd_init_attributes();
   *out = ctx;
   return 0;
 }
@@ -355,6 +356,12 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
                           refine_count);
       HX_CUDA(cudaGetLastError());
     }
+  } else if (c.bipartite && ctx->use_bipartite && hx::bd_path_supported(c) && N > HX_SMEM_MAX_N) {
+    if (make_refine(nmat * N)) return fail(HX_E_CUDA, "alloc refinement list");
+    int rc = hx::bd_eval(c, kp, nk, d_masks, nmasks, g, diff, trans, d_eigs, status, sharp, ctx->ws_budget,
+                         [&](size_t bytes) -> void* { return ctx->band.grow(bytes) ? nullptr : ctx->band.p; }, st,
+                         refine, refine_count);
+    if (rc) return fail(HX_E_CUDA, std::string("bipartite band path: ") + hx::bd_last_error());
   } else if (c.pencil != HX_PENCIL_GENERAL && hx::band_path_supported(N)) {
     if (make_refine(nmat * N)) return fail(HX_E_CUDA, "alloc refinement list");
     int rc = hx::band_eval(c, kp, nk, d_masks, nmasks, g, diff, trans, d_eigs,

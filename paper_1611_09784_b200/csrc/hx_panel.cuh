@@ -1,8 +1,14 @@
-// Panel QR of stage 1 on a thread-block CLUSTER: the m x BW panel below the band is split by rows over
-// the CL CTAs of a cluster and held in their shared memory for the whole factorisation; the two
-// reductions per column (column norm, dot products with the remaining columns) are combined across
-// the cluster through distributed shared memory (fixed rank order -> deterministic).  Replaces up to
-// 3 passes over an L2-resident panel per column with shared-memory sweeps + 2 cluster barriers.
+// Panel QR of stage 1 on a thread-block CLUSTER: an m x BW panel is split by rows over the CL CTAs of
+// a cluster and held in their shared memory for the whole factorisation; the two reductions per column
+// (column norm, dot products with the remaining columns) are combined across the cluster through
+// distributed shared memory (fixed rank order -> deterministic).  Replaces up to 3 passes over an
+// L2-resident panel per column with shared-memory sweeps + 2 cluster barriers.
+//
+// The panel is addressed through PanelArgs so the same kernel serves
+//   mode 0  P[i][j] = M[r0 + i][c0 + j]           (column panel; R written back, zeros below)
+//   mode 1  P[i][j] = conj(M[r0 + j][c0 + i])     (row panel of the bidiagonal reduction: LQ of the row
+//                                                  block; R^H written back, zeros right of it)
+// with M column-major (leading dimension ld) inside each matrix slab of the batch.
 #pragma once
 #include <cooperative_groups.h>
 
@@ -12,6 +18,22 @@ namespace hx {
 
 namespace cgx = cooperative_groups;
 
+struct PanelArgs {
+  size_t stride;  // per-matrix slab (double2 units)
+  size_t m_off;   // matrix offset inside the slab
+  int ld;         // leading dimension of the matrix
+  int r0, c0;     // panel origin (see mode)
+  int m;          // panel rows
+  int mode;       // 0: column panel, 1: conj-transposed row panel
+  size_t v_off;   // explicit V (m x BW, leading dimension ldv)
+  int ldv;
+  size_t t_off;   // T (BW x BW, column-major)
+};
+
+__device__ __forceinline__ double2* panel_elem(double2* M, const PanelArgs& a, int i, int j) {
+  return a.mode == 0 ? M + (size_t)(a.c0 + j) * a.ld + a.r0 + i : M + (size_t)(a.c0 + i) * a.ld + a.r0 + j;
+}
+
 template <int BWc>
 struct PanelSlot {
   double2 norm_alpha[2];  // (sigma^2 partial, 0), alpha (owner of row j only)
@@ -19,7 +41,7 @@ struct PanelSlot {
 };
 
 // Recursive-halving reduce-scatter of 32 complex per-lane values: afterwards lane l holds the warp sum
-// of index l.
+// of index l (in a[0]).
 __device__ __forceinline__ void warp_reduce_scatter32(double2 (&a)[32]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
@@ -36,11 +58,10 @@ __device__ __forceinline__ void warp_reduce_scatter32(double2 (&a)[32]) {
   }
 }
 
-// grid = (CL, batch), cluster = (CL, 1, 1), 256 threads; dynamic smem = R*(BW+1)*16 + slots.
+// grid = (CL, batch), cluster = (CL, 1, 1), 256 threads; dynamic smem = panel_cluster_smem(R).
 template <int CL, int BWc>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
-    panel_qr_cluster_kernel(double2* ws, size_t stride, size_t a_off, size_t v_off, size_t t_off, int N, int k0,
-                            int R) {
+    panel_qr_cluster_kernel(double2* ws, PanelArgs a, int R) {
   extern __shared__ __align__(16) unsigned char psm[];
   cgx::cluster_group cluster = cgx::this_cluster();
   const int rank = (int)cluster.block_rank();
@@ -53,17 +74,26 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
   __shared__ double2 Ts[BWc][BWc + 1];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double2* base = ws + (size_t)blockIdx.y * stride;
-  const int lda = N;
-  const int m = N - k0 - BWc;
-  double2* P = base + a_off + (size_t)k0 * lda + k0 + BWc;
-  double2* V = base + v_off;
+  double2* base = ws + (size_t)blockIdx.y * a.stride;
+  double2* M = base + a.m_off;
+  double2* V = base + a.v_off;
+  const int m = a.m;
   const int r0 = rank * R;
   const int rows = max(0, min(R, m - r0));
+  const bool conj_in = a.mode == 1;
 
   for (int p = tid; p < BWc * (BWc + 1); p += 256) (&Ts[0][0])[p] = make_double2(0.0, 0.0);
-  for (int c = 0; c < BWc; ++c)
-    for (int i = tid; i < rows; i += 256) Ps[c * ldp + i] = P[r0 + i + (size_t)c * lda];
+  if (!conj_in) {
+    for (int c = 0; c < BWc; ++c)
+      for (int i = tid; i < rows; i += 256) Ps[c * ldp + i] = *panel_elem(M, a, r0 + i, c);
+  } else {
+    // row panel: consecutive threads walk j (contiguous in memory for a fixed panel row i)
+    for (int p = tid; p < rows * BWc; p += 256) {
+      const int i = p / BWc, c = p % BWc;
+      const double2 z = *panel_elem(M, a, r0 + i, c);
+      Ps[c * ldp + i] = make_double2(z.x, -z.y);
+    }
+  }
   __syncthreads();
 
   for (int j = 0; j < BWc; ++j) {
@@ -117,7 +147,6 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
       }
     }
     warp_reduce_scatter32(acc);
-    // lane c holds this warp's partial for column c: acc[0] after the reduce-scatter
     if (lane < BWc) wdots[warp][lane] = acc[0];
     __syncthreads();
     if (tid < BWc) {
@@ -166,21 +195,29 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
     if (tid == 0) Ts[j][j] = make_double2(tau, 0.0);
     __syncthreads();
   }
-  // ---- write back: R (upper part) into A, zeros below; explicit V; T from rank 0
-  for (int c = 0; c < BWc; ++c)
-    for (int i = tid; i < rows; i += 256) {
-      const int gi = r0 + i;
-      const double2 x = Ps[c * ldp + i];
-      P[gi + (size_t)c * lda] = gi <= c ? x : make_double2(0.0, 0.0);
-      double2 vv;
-      if (c >= m) vv = make_double2(0.0, 0.0);
-      else if (gi < c) vv = make_double2(0.0, 0.0);
-      else if (gi == c) vv = make_double2(1.0, 0.0);
-      else vv = x;
-      V[gi + (size_t)c * N] = vv;
+  // ---- write back: R (upper part) into the matrix, zeros below; explicit V; T from rank 0
+  for (int p = tid; p < rows * BWc; p += 256) {
+    int i, c;
+    if (!conj_in) {
+      c = p / rows;
+      i = p - c * rows;
+    } else {
+      i = p / BWc;
+      c = p % BWc;
     }
+    const int gi = r0 + i;
+    const double2 x = Ps[c * ldp + i];
+    const double2 rv = gi <= c ? x : make_double2(0.0, 0.0);
+    *panel_elem(M, a, gi, c) = conj_in ? make_double2(rv.x, -rv.y) : rv;
+    double2 vv;
+    if (c >= m) vv = make_double2(0.0, 0.0);
+    else if (gi < c) vv = make_double2(0.0, 0.0);
+    else if (gi == c) vv = make_double2(1.0, 0.0);
+    else vv = x;
+    V[gi + (size_t)c * a.ldv] = vv;
+  }
   if (rank == 0) {
-    double2* T = base + t_off;
+    double2* T = base + a.t_off;
     for (int p = tid; p < BWc * BWc; p += 256) T[(p % BWc) + (p / BWc) * BWc] = Ts[p % BWc][p / BWc];
   }
   cluster.sync();  // keep every CTA's shared memory alive until remote reads are done

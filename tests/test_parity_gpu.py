@@ -163,3 +163,28 @@ def test_all_vacant_gives_zero_curve_and_plateau():
     for sset in sets:
         n = sset.stats.n
         assert np.allclose(sset.full[:, -1], 2.0 * n * n / eng.supercell(n).area, atol=1e-9)
+
+
+@pytest.mark.parametrize("nu,q,p", [(10, 2, 0.2), (11, 1, 0.3), (12, 1, 0.05), (16, 2, 0.1)])
+def test_bipartite_banded_tier_matches_oracle(nu, q, p):
+    """graphene N = 2nu^2 > 160 goes through the bipartite banded tier (nA != nB after vacancies)."""
+    model = hx.GrapheneNNModel()
+    spec = model.lattice_spec()
+    sc = hx.build_supercell(spec, nu)
+    cell = hx.compile_cell(model, sc)
+    kp = hx.make_bz_grid(spec, nu, q, "reduced").kpoints
+    from paper_1611_09784_b200.sampling import sample_masks
+
+    words = sample_masks(sc.nunits, p, 77, 3, 0, 3)
+    lo, hi, npts = -6.580201874549387, 14.863393148450246, 201
+    curves, eigs, status = eval_batch(cell, kp, words, lo, (hi - lo) / (npts - 1), npts, 0.01, want_eigs=True)
+    assert (status == 0).all()
+    om = O.graphene_model()
+    ocell = O.make_cell(om, nu)
+    for m in range(len(words)):
+        ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
+        d = ref.shape[1]
+        assert np.all(np.isnan(eigs[m, :, d:]))
+        assert np.max(np.abs(eigs[m, :, :d] - ref)) <= EIG_TOL * (ref.max() - ref.min())
+        rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), lo, hi, npts, 0.01, ocell.area)
+        np.testing.assert_allclose(curves[m], rc, rtol=0, atol=IDOS_TOL)
