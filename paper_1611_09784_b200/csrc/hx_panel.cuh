@@ -60,7 +60,7 @@ __device__ __forceinline__ void warp_reduce_scatter32(double2 (&a)[32]) {
 
 // grid = (CL, batch), cluster = (CL, 1, 1), 256 threads; dynamic smem = panel_cluster_smem(R).
 template <int CL, int BWc>
-__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256)
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(256, 2)
     panel_qr_cluster_kernel(double2* ws, PanelArgs a, int R) {
   extern __shared__ __align__(16) unsigned char psm[];
   cgx::cluster_group cluster = cgx::this_cluster();
