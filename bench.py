@@ -384,7 +384,7 @@ def run_e2e(hx, model, levels, nq, p, erange, lo, hi, args, rank, world, dev):
 
 def cpu_baseline(kind, levels, nq, p, erange):
     cores = len(os.sched_getaffinity(0))
-    frac = 1.0 / 32.0
+    frac = 1.0 / 8.0
     try:
         reference_engine_run(kind, levels[:1], nq, p, erange, 16 / levels[0][1], cores)  # warm-up
         per = reference_engine_run(kind, levels, nq, p, erange, frac, cores)
@@ -394,7 +394,7 @@ def cpu_baseline(kind, levels, nq, p, erange):
     tot_s = sum(x["seconds"] for x in per)
     tot_m = sum(x["M"] for x in per)
     return {"value": tot_m / tot_s, "unit": "samples/s", "cores": cores, "kind": kindname,
-            "sample": f"every level with M_l/32 samples through the reference Engine (workers={cores}, reduced BZ)",
+            "sample": f"every level with M_l/8 samples through the reference Engine (workers={cores}, reduced BZ)",
             "levels": per}
 
 
