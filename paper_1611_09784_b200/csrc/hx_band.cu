@@ -523,6 +523,9 @@ void band_init_attributes() {
                        (int)PANEL_SMEM_MAX);
   cudaFuncSetAttribute(panel_qr_cluster_kernel<8, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)PANEL_SMEM_MAX);
+  cudaFuncSetAttribute(panel_qr_cluster_kernel<16, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)PANEL_SMEM_MAX);
+  cudaFuncSetAttribute(panel_qr_cluster_kernel<16, BW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(band_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   cudaFuncSetAttribute(hemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HEMM_SMEM);
   cudaFuncSetAttribute(her2k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HER2K_SMEM);
@@ -540,13 +543,14 @@ bool band_path_supported(int N) { return N > HX_SMEM_MAX_N && N <= HX_MAX_N; }
 
 // Smallest cluster (2, 4, 8 CTAs) whose shared memory holds the panel; false if none fits.
 bool launch_cluster_panel(double2* ws, const PanelArgs& a, int64_t cnt, cudaStream_t st) {
-  for (int cl : {2, 4, 8}) {
+  for (int cl : {2, 4, 8, 16}) {
     const int r = (a.m + cl - 1) / cl;
     const size_t psm = panel_cluster_smem<BW>(r);
     if (psm > PANEL_SMEM_MAX) continue;
     if (cl == 2) panel_qr_cluster_kernel<2, BW><<<dim3(2, (unsigned)cnt), 256, psm, st>>>(ws, a, r);
     else if (cl == 4) panel_qr_cluster_kernel<4, BW><<<dim3(4, (unsigned)cnt), 256, psm, st>>>(ws, a, r);
-    else panel_qr_cluster_kernel<8, BW><<<dim3(8, (unsigned)cnt), 256, psm, st>>>(ws, a, r);
+    else if (cl == 8) panel_qr_cluster_kernel<8, BW><<<dim3(8, (unsigned)cnt), 256, psm, st>>>(ws, a, r);
+    else panel_qr_cluster_kernel<16, BW><<<dim3(16, (unsigned)cnt), 256, psm, st>>>(ws, a, r);  // non-portable
     return true;
   }
   return false;

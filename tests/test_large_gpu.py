@@ -1,0 +1,55 @@
+"""Config-4 scale (nu = 64, N = 8192) through the bipartite banded tier, checked with size-independent
+properties: band folding of the unperturbed supercell at Gamma (analytic two-band dispersion on the
+64 x 64 folded fundamental grid, tests/test_spectrum.py:94-110 style) and the IDOS plateau
+(= surviving orbitals / area, tests/test_qoi.py:83-92 style) for a defected sample."""
+
+import numpy as np
+import pytest
+
+import paper_1611_09784_b200 as hx
+from paper_1611_09784_b200.sampling import sample_masks
+from paper_1611_09784_b200.solver import eval_batch
+
+pytestmark = pytest.mark.gpu
+
+LO, HI, NPTS = -6.580201874549387, 14.863393148450246, 201
+
+
+def analytic_bands(model, kpts):
+    spec = model.lattice_spec()
+    a1, a2 = np.asarray(spec.a1), np.asarray(spec.a2)
+    w = np.abs(1.0 + np.exp(-1j * kpts @ a1) + np.exp(-1j * kpts @ a2))
+    lo = (model.eps_2p + model.t * w) / (1.0 + model.s * w)
+    hi = (model.eps_2p - model.t * w) / (1.0 - model.s * w)
+    return np.sort(np.concatenate([lo, hi]))
+
+
+@pytest.mark.parametrize("nu", [24, 64])
+def test_unperturbed_gamma_folds_fundamental_bands(nu):
+    model = hx.GrapheneNNModel()
+    spec = model.lattice_spec()
+    sc = hx.build_supercell(spec, nu)
+    cell = hx.compile_cell(model, sc)
+    words = np.zeros((1, max(1, (sc.nunits + 63) // 64)), dtype=np.uint64)
+    _, eigs, status = eval_batch(cell, np.zeros((1, 2)), words, LO, (HI - LO) / (NPTS - 1), NPTS, 0.01,
+                                 want_eigs=True)
+    assert (status == 0).all()
+    b1, b2 = spec.reciprocal_vectors()
+    ii, jj = np.meshgrid(np.arange(nu), np.arange(nu), indexing="ij")
+    kf = (ii.reshape(-1, 1) * b1 + jj.reshape(-1, 1) * b2) / nu
+    ref = analytic_bands(model, kf)
+    assert np.max(np.abs(eigs[0, 0] - ref)) <= 1e-10 * (ref.max() - ref.min())
+
+
+def test_nu64_defected_sample_plateau_and_monotone():
+    model = hx.GrapheneNNModel()
+    sc = hx.build_supercell(model.lattice_spec(), 64)
+    cell = hx.compile_cell(model, sc)
+    words = sample_masks(sc.nunits, 0.02, 2026, 1, 0, 1)
+    vac = sum(bin(int(w)).count("1") for w in words[0])
+    kp = hx.make_bz_grid(model.lattice_spec(), 64, 2, "reduced").kpoints  # Gamma + 3 points (config 4)
+    curves, _, status = eval_batch(cell, kp, words, LO, (HI - LO) / (NPTS - 1), NPTS, 0.01)
+    assert (status == 0).all()
+    d = sc.nunits - vac
+    assert curves[0, -1] == pytest.approx(d / sc.area, abs=1e-12)
+    assert np.all(np.diff(curves[0]) >= -1e-12)
