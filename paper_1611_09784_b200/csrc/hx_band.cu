@@ -512,20 +512,11 @@ __global__ void __launch_bounds__(256) band_copy_kernel(const double2* __restric
 constexpr size_t HEMM_SMEM = (size_t)(HM_TM + BW) * HM_LD * sizeof(double2);
 constexpr size_t HER2K_SMEM = (size_t)4 * HK_T * HK_LD * sizeof(double2);
 
-constexpr size_t PANEL_SMEM_MAX = 200 * 1024;
 constexpr size_t W_ROWS_SMEM = (size_t)(2 * BW * BW + 64 * (BW + 1)) * sizeof(double2);
 
 void band_init_attributes() {
   cudaFuncSetAttribute(w_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W_ROWS_SMEM);
-  cudaFuncSetAttribute(panel_qr_cluster_kernel<2, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)PANEL_SMEM_MAX);
-  cudaFuncSetAttribute(panel_qr_cluster_kernel<4, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)PANEL_SMEM_MAX);
-  cudaFuncSetAttribute(panel_qr_cluster_kernel<8, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)PANEL_SMEM_MAX);
-  cudaFuncSetAttribute(panel_qr_cluster_kernel<16, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)PANEL_SMEM_MAX);
-  cudaFuncSetAttribute(panel_qr_cluster_kernel<16, BW>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(panel_qr_reg_kernel<16, 8, 32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(band_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
   cudaFuncSetAttribute(hemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HEMM_SMEM);
   cudaFuncSetAttribute(her2k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HER2K_SMEM);
@@ -541,29 +532,36 @@ void band_init_attributes() {
 
 bool band_path_supported(int N) { return N > HX_SMEM_MAX_N && N <= HX_MAX_N; }
 
-// Smallest cluster (2, 4, 8 CTAs) whose shared memory holds the panel; false if none fits.
+template <int CL, int GR, int RPT>
+static void launch_panel(double2* ws, const PanelArgs& a, int64_t cnt, cudaStream_t st) {
+  const int r = (a.m + CL - 1) / CL;
+  panel_qr_reg_kernel<CL, GR, RPT><<<dim3((unsigned)CL, (unsigned)cnt), 32 * GR, 0, st>>>(ws, a, r);
+}
+
+// Panel QR with the panel in registers (hx_panel.cuh): the smallest configuration whose CTA (or
+// cluster of 2..16 CTAs of 256 rows) holds all m rows; false if the panel is taller than 4096 rows.
+// (Clusters of 128-row CTAs measured 1.5-2x slower than 256-row CTAs: two cluster barriers per column.)
 bool launch_cluster_panel(double2* ws, const PanelArgs& a, int64_t cnt, cudaStream_t st) {
-  for (int cl : {2, 4, 8, 16}) {
-    const int r = (a.m + cl - 1) / cl;
-    const size_t psm = panel_cluster_smem<BW>(r);
-    if (psm > PANEL_SMEM_MAX) continue;
-    if (cl == 2) panel_qr_cluster_kernel<2, BW><<<dim3(2, (unsigned)cnt), 256, psm, st>>>(ws, a, r);
-    else if (cl == 4) panel_qr_cluster_kernel<4, BW><<<dim3(4, (unsigned)cnt), 256, psm, st>>>(ws, a, r);
-    else if (cl == 8) panel_qr_cluster_kernel<8, BW><<<dim3(8, (unsigned)cnt), 256, psm, st>>>(ws, a, r);
-    else panel_qr_cluster_kernel<16, BW><<<dim3(16, (unsigned)cnt), 256, psm, st>>>(ws, a, r);  // non-portable
-    return true;
-  }
-  return false;
+  const int m = a.m;
+  if (m <= 32) launch_panel<1, 8, 4>(ws, a, cnt, st);
+  else if (m <= 64) launch_panel<1, 8, 8>(ws, a, cnt, st);
+  else if (m <= 128) launch_panel<1, 16, 8>(ws, a, cnt, st);
+  else if (m <= 256) launch_panel<1, 16, 16>(ws, a, cnt, st);
+  else if (m <= 512) launch_panel<2, 16, 16>(ws, a, cnt, st);
+  else if (m <= 1024) launch_panel<4, 16, 16>(ws, a, cnt, st);
+  else if (m <= 2048) launch_panel<8, 16, 16>(ws, a, cnt, st);
+  else if (m <= 4096) launch_panel<16, 8, 32>(ws, a, cnt, st);
+  else return false;
+  return true;
 }
 
 // Stage 1 + 2 for `cnt` matrices already staged in the workspace.
 static int band_reduce(double2* ws, const BandWs& L, int N, int64_t cnt, const int* dims, cudaStream_t st) {
   for (int k0 = 0; N - k0 - BW > 0; k0 += BW) {
     const int m = N - k0 - BW;
-    // cluster panel QR for small batches (large batches keep every SM busy with one single-CTA panel
-    // per matrix instead); very tall panels use the L2-resident single-CTA kernel
+    // register-resident panel QR; panels taller than 4096 rows use the L2-resident single-CTA kernel
     PanelArgs pa{L.stride, L.a_off, N, k0 + BW, k0, m, 0, L.v_off, N, L.t_off};
-    if (cnt >= 512 || !launch_cluster_panel(ws, pa, cnt, st))
+    if (!launch_cluster_panel(ws, pa, cnt, st))
       panel_qr_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, L, N, k0);
     const unsigned mt = (unsigned)((m + HM_TM - 1) / HM_TM);
     hemm_kernel<<<dim3(mt, (unsigned)cnt), 128, HEMM_SMEM, st>>>(ws, L, N, k0);
