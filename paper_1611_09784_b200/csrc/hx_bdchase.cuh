@@ -1,16 +1,22 @@
 // Stage 2 of the bipartite banded tier: upper band (width BWc) -> upper bidiagonal by bulge chasing,
 // emitting the Golub-Kahan tridiagonal (zero diagonal, e2 = |alpha_0|^2, |gamma_0|^2, |alpha_1|^2, ...).
 //
-// Sweep i annihilates row i right of the superdiagonal and chases the bulge; task t (block start
-// s = i + 1 + t*BWc, width len, next width lb):
-//   right reflector G (from row s-BWc, built by task t-1; for t = 0 from row i) on columns [s, s+len):
-//       applied to the rows above the block that intersect those columns ("top rows") and to the block
-//       X = C[s:s+len, s:s+len];
-//   left reflector H from X[:, 0] (gives alpha_s), applied to rows [s, s+len) over X and the block to its
-//       right Y = C[s:s+len, s+len:s+len+lb];
-//   next right reflector from Y[0, :] (row s, gives gamma_s), carried to task t+1.
-// Sweep i may run task t once sweep i-1 has completed task t+2 (regions are disjoint beyond that), so
-// one warp owns the sweeps i = w (mod NW) and waits on a per-warp progress counter (no CTA barriers).
+// Sweep i annihilates row i right of the superdiagonal and chases the bulge; task t works on the block
+// rows [s, s+len), s = i + 1 + t*BWc, over X = C[s:s+len, s:s+len] and Y = C[s:s+len, s+len:s+len+lb]:
+//   X' = H X G       G = I - tau_g u u^H  (right reflector carried in from the previous task; for t = 0
+//                                          built here from row i, which becomes (conj beta, 0, ...))
+//                    H = I - tau_h v v^H  (left reflector from column 0 of X G, gives alpha_s)
+//   Y' = H Y G'      G' from row 0 of H Y (gives gamma_s), carried to task t+1
+// Both are applied as one fused rank-2 row update per tile: with y = X u, p = v^H X, w = v^H (tau_g y),
+//   X'[r][c] = X[r][c] - tau_g y_r conj(u_c) - v_r * tau_h (p_c - w conj(u_c)),
+// and with q = v^H Y, f = Y u' - tau_h v (q . u'),
+//   Y'[r][c] = Y[r][c] - v_r * tau_h q_c - tau_g' f_r conj(u'_c),
+// so each tile is read twice from shared memory (one row pass, one column pass), updated in registers
+// (lane = row) and stored straight to HBM.  Applying G' to Y here (instead of to the "top rows" at the
+// start of task t+1) removes every dependent global load from the chase except row i at t = 0.
+// Task t of sweep i touches rows [s, s+32) x columns [s, s+64) only, so it may run once sweep i-1 has
+// completed its tasks 0..t+1; one warp owns the sweeps i = w (mod NW) and waits on a per-warp progress
+// counter in shared memory (no CTA barriers).
 #pragma once
 #include "hx_dense.cuh"
 
@@ -18,10 +24,11 @@ namespace hx {
 
 template <int BWc>
 struct BdChaseSmem {
-  double2 X[BWc][BWc + 1];
+  double2 X[BWc][BWc + 1];  // tiles, zero-padded to BWc x BWc
   double2 Y[BWc][BWc + 1];
-  double2 ug[BWc];  // current right reflector vector (ug[0] = 1)
-  double2 vh[BWc];  // current left reflector vector (vh[0] = 1)
+  double2 ug[BWc];  // current right reflector vector (ug[0] = 1, zero-padded)
+  double2 vh[BWc];  // left reflector vector (vh[0] = 1, zero-padded)
+  double2 cb[BWc];  // per-column update coefficients
 };
 
 __device__ __forceinline__ void bd_cp_async16(void* smem, const void* gmem) {
@@ -30,9 +37,45 @@ __device__ __forceinline__ void bd_cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void bd_cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+__device__ __forceinline__ double2 cmul_cj(double2 a, double2 b) {  // conj(a) * b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ double2 warp_csum(double2 v) { return make_double2(warp_sum(v.x), warp_sum(v.y)); }
+
+// Householder reflector for x with x_0 = alpha, |x|^2 = sig2 (same convention as make_reflector):
+// H = I - tau v v^H, v_0 = 1, v_i = x_i * scale, H x = beta e_0, beta = -phase(alpha) sqrt(sig2).
+// Division-free (rsqrt + one reciprocal) to keep the chase's critical path and code size short.
+struct QuickReflector {
+  double tau;
+  double2 scale, beta;
+};
+__device__ __forceinline__ QuickReflector quick_reflector(double2 alpha, double sig2) {
+  QuickReflector h;
+  if (!(sig2 > 0.0)) {
+    h.tau = 0.0;
+    h.scale = make_double2(0.0, 0.0);
+    h.beta = make_double2(0.0, 0.0);
+    return h;
+  }
+  const double rs = rsqrt(sig2), sigma = sig2 * rs;
+  const double a2 = alpha.x * alpha.x + alpha.y * alpha.y;
+  double2 ph = make_double2(1.0, 0.0);
+  double aa = 0.0;
+  if (a2 > 0.0) {
+    const double ra = rsqrt(a2);
+    aa = a2 * ra;
+    ph = make_double2(alpha.x * ra, alpha.y * ra);
+  }
+  const double mag = aa + sigma, rm = __drcp_rn(mag);
+  h.tau = mag * rs;
+  h.scale = make_double2(ph.x * rm, -ph.y * rm);
+  h.beta = make_double2(-ph.x * sigma, -ph.y * sigma);
+  return h;
+}
+
 template <int NW, int BWc>
-__global__ void __launch_bounds__(NW * 32) bd_chase_kernel(double2* ws, size_t stride, size_t c_off, size_t tgk_off,
-                                                            int S, const int* dims) {
+__global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_t stride, size_t c_off,
+                                                               size_t tgk_off, int S, const int* dims) {
   extern __shared__ __align__(16) unsigned char bd_smem[];
   BdChaseSmem<BWc>* all = reinterpret_cast<BdChaseSmem<BWc>*>(bd_smem);
   volatile int* prog = reinterpret_cast<volatile int*>(all + NW);
@@ -43,6 +86,7 @@ __global__ void __launch_bounds__(NW * 32) bd_chase_kernel(double2* ws, size_t s
   double* diag = reinterpret_cast<double*>(base + tgk_off);
   double* e2 = diag + 2 * S;
   const int ld = S;
+  const double2 zero = make_double2(0.0, 0.0);
   for (int q = threadIdx.x; q < 2 * S; q += blockDim.x) {
     diag[q] = 0.0;
     e2[q] = 0.0;
@@ -62,176 +106,155 @@ __global__ void __launch_bounds__(NW * 32) bd_chase_kernel(double2* ws, size_t s
     double taug = 0.0;
     for (int t = 0; t < tasks; ++t) {
       if (i > 0) {
-        const int need = (i - 1) * 65536 + min(t + 3, prev_tasks);
+        const int need = (i - 1) * 65536 + min(t + 2, prev_tasks);
         if (lane == 0)
-          while (prog[pw] < need) {
-          }
+          while (prog[pw] < need) __nanosleep(20);
         __syncwarp();
         __threadfence_block();
       }
       const int s = i + 1 + t * BWc;
       const int len = min(BWc, S - s);
       const int lb = max(0, min(BWc, S - s - len));
-      // ---- X and Y tiles (asynchronous; Y is not needed until the left reflector)
-      for (int cc = 0; cc < len; ++cc)
-        if (lane < len) bd_cp_async16(&W.X[lane][cc], C + (size_t)(s + cc) * ld + s + lane);
-      for (int cc = 0; cc < lb; ++cc)
-        if (lane < len) bd_cp_async16(&W.Y[lane][cc], C + (size_t)(s + len + cc) * ld + s + lane);
+      // ---- X and Y tiles (asynchronous, zero-padded); blk = &C[s + lane][s], columns ld apart
+      double2* const blk = C + ((size_t)s * ld + s + lane);
+      {
+        const double2* src = blk;
+#pragma unroll 4
+        for (int cc = 0; cc < BWc; ++cc, src += ld) {
+          if (lane < len && cc < len) bd_cp_async16(&W.X[lane][cc], src);
+          else W.X[lane][cc] = zero;
+        }
+#pragma unroll 4
+        for (int cc = 0; cc < BWc; ++cc, src += ld) {
+          if (lane < len && cc < lb) bd_cp_async16(&W.Y[lane][cc], src);
+          else W.Y[lane][cc] = zero;
+        }
+      }
       if (t == 0) {
-        // right reflector from row i, columns [s, s+len): row i -> (gamma_i, 0, ...)
-        double2 x = make_double2(0.0, 0.0);
+        // right reflector from row i, columns [s, s+len): row i -> (conj beta, 0, ...) = (gamma_i, 0, ...)
+        double2 x = zero;
         if (lane < len) {
           const double2 z = C[(size_t)(s + lane) * ld + i];
           x = make_double2(z.x, -z.y);
         }
         const double sig2 = warp_sum(x.x * x.x + x.y * x.y);
         const double2 al = make_double2(__shfl_sync(0xffffffffu, x.x, 0), __shfl_sync(0xffffffffu, x.y, 0));
-        const Reflector h = make_reflector(al, sig2);
+        const QuickReflector h = quick_reflector(al, sig2);
         taug = h.tau;
-        if (lane < len) {
-          W.ug[lane] = lane == 0 ? make_double2(1.0, 0.0) : cmul(x, h.scale);
-          if (taug != 0.0) {
-            double2 o = make_double2(0.0, 0.0);
-            if (lane == 0) {
-              const double sg = sqrt(sig2), aa = hypot(al.x, al.y);
-              const double2 ph = aa > 0.0 ? make_double2(al.x / aa, al.y / aa) : make_double2(1.0, 0.0);
-              o = make_double2(-ph.x * sg, ph.y * sg);  // conj(beta)
-            }
-            C[(size_t)(s + lane) * ld + i] = o;
-          }
-        }
+        W.ug[lane] = lane == 0 ? make_double2(1.0, 0.0) : (lane < len ? cmul(x, h.scale) : zero);
+        if (lane < len && taug != 0.0)
+          C[(size_t)(s + lane) * ld + i] = lane == 0 ? make_double2(h.beta.x, -h.beta.y) : zero;
         if (lane == 0) e2[2 * i + 1] = sig2;
-        __syncwarp();
-      } else if (taug != 0.0) {
-        // top rows [s-BWc+1, s): apply G from the right (lane = row), straight from/to global memory
-        const int ntop = BWc - 1;
-        if (lane < ntop) {
-          const int r = s - BWc + 1 + lane;
-          double2 row[BWc];
-          double2 w = make_double2(0.0, 0.0);
-#pragma unroll
-          for (int cc = 0; cc < BWc; ++cc) {
-            row[cc] = cc < len ? C[(size_t)(s + cc) * ld + r] : make_double2(0.0, 0.0);
-            if (cc < len) {
-              const double2 u = W.ug[cc];
-              w.x += row[cc].x * u.x - row[cc].y * u.y;
-              w.y += row[cc].x * u.y + row[cc].y * u.x;
-            }
-          }
-          w = make_double2(taug * w.x, taug * w.y);
-#pragma unroll
-          for (int cc = 0; cc < BWc; ++cc) {
-            if (cc < len) {
-              const double2 u = W.ug[cc];
-              double2 z = row[cc];
-              z.x -= w.x * u.x + w.y * u.y;
-              z.y -= w.y * u.x - w.x * u.y;
-              C[(size_t)(s + cc) * ld + r] = z;
-            }
-          }
-        }
       }
       bd_cp_async_wait_all();
       __syncwarp();
-      // ---- G on X (lane = row)
-      if (taug != 0.0 && lane < len) {
-        double2 w = make_double2(0.0, 0.0);
-        for (int cc = 0; cc < len; ++cc) {
-          const double2 a = W.X[lane][cc], u = W.ug[cc];
-          w.x += a.x * u.x - a.y * u.y;
-          w.y += a.x * u.y + a.y * u.x;
+      // ---- X row pass: ty = tau_g (X u)_r, column 0 of X G, left reflector H
+      double2 ty;
+      {
+        double2 a0 = zero, a1 = zero;
+#pragma unroll 4
+        for (int c = 0; c < BWc; c += 2) {
+          const double2 x0 = W.X[lane][c], u0 = W.ug[c], x1 = W.X[lane][c + 1], u1 = W.ug[c + 1];
+          a0.x = fma(x0.x, u0.x, fma(-x0.y, u0.y, a0.x));
+          a0.y = fma(x0.x, u0.y, fma(x0.y, u0.x, a0.y));
+          a1.x = fma(x1.x, u1.x, fma(-x1.y, u1.y, a1.x));
+          a1.y = fma(x1.x, u1.y, fma(x1.y, u1.x, a1.y));
         }
-        w = make_double2(taug * w.x, taug * w.y);
-        for (int cc = 0; cc < len; ++cc) {
-          const double2 u = W.ug[cc];
-          double2 z = W.X[lane][cc];
-          z.x -= w.x * u.x + w.y * u.y;
-          z.y -= w.y * u.x - w.x * u.y;
-          W.X[lane][cc] = z;
-        }
+        ty = make_double2(taug * (a0.x + a1.x), taug * (a0.y + a1.y));
       }
-      __syncwarp();
-      // ---- H from X[:, 0] (alpha_s)
-      const double2 xh = lane < len ? W.X[lane][0] : make_double2(0.0, 0.0);
-      const double sh2 = warp_sum(xh.x * xh.x + xh.y * xh.y);
-      const double2 ah = make_double2(__shfl_sync(0xffffffffu, xh.x, 0), __shfl_sync(0xffffffffu, xh.y, 0));
-      const Reflector hh = make_reflector(ah, sh2);
+      const double2 x00 = W.X[lane][0];
+      const double2 x0 = make_double2(x00.x - ty.x, x00.y - ty.y);
+      const double sh2 = warp_sum(x0.x * x0.x + x0.y * x0.y);
+      const double2 ah = make_double2(__shfl_sync(0xffffffffu, x0.x, 0), __shfl_sync(0xffffffffu, x0.y, 0));
+      const QuickReflector hh = quick_reflector(ah, sh2);
+      const double tauh = hh.tau;
       if (t == 0 && lane == 0) e2[2 * s] = sh2;
-      if (lane < len) W.vh[lane] = lane == 0 ? make_double2(1.0, 0.0) : cmul(xh, hh.scale);
+      const double2 v = lane == 0 ? make_double2(1.0, 0.0) : cmul(x0, hh.scale);  // zero on padded rows
+      W.vh[lane] = v;
+      const double2 w = warp_csum(cmul_cj(v, ty));  // v^H (tau_g y)
       __syncwarp();
-      if (hh.tau != 0.0) {
-        if (lane < len) {
-          double2 b0 = make_double2(0.0, 0.0);
-          if (lane == 0) {
-            const double sg = sqrt(sh2), aa = hypot(ah.x, ah.y);
-            const double2 ph = aa > 0.0 ? make_double2(ah.x / aa, ah.y / aa) : make_double2(1.0, 0.0);
-            b0 = make_double2(-ph.x * sg, -ph.y * sg);
-          }
-          W.X[lane][0] = b0;
+      // ---- X column pass: p = v^H X, b_c = tau_h (p_c - w conj(u_c))
+      {
+        double2 a0 = zero, a1 = zero;
+#pragma unroll 4
+        for (int r = 0; r < BWc; r += 2) {
+          const double2 v0 = W.vh[r], x0c = W.X[r][lane], v1 = W.vh[r + 1], x1c = W.X[r + 1][lane];
+          a0.x = fma(v0.x, x0c.x, fma(v0.y, x0c.y, a0.x));
+          a0.y = fma(v0.x, x0c.y, fma(-v0.y, x0c.x, a0.y));
+          a1.x = fma(v1.x, x1c.x, fma(v1.y, x1c.y, a1.x));
+          a1.y = fma(v1.x, x1c.y, fma(-v1.y, x1c.x, a1.y));
         }
-        // left application (lane = column): X columns 1..len-1, then Y columns 0..lb-1
-        if (lane >= 1 && lane < len) {
-          double2 z = make_double2(0.0, 0.0);
-          for (int r = 0; r < len; ++r) {
-            const double2 v = W.vh[r], a = W.X[r][lane];
-            z.x += v.x * a.x + v.y * a.y;
-            z.y += v.x * a.y - v.y * a.x;
-          }
-          z = make_double2(hh.tau * z.x, hh.tau * z.y);
-          for (int r = 0; r < len; ++r) {
-            const double2 v = W.vh[r];
-            double2 a = W.X[r][lane];
-            a.x -= v.x * z.x - v.y * z.y;
-            a.y -= v.x * z.y + v.y * z.x;
-            W.X[r][lane] = a;
-          }
-        }
-        if (lane < lb) {
-          double2 z = make_double2(0.0, 0.0);
-          for (int r = 0; r < len; ++r) {
-            const double2 v = W.vh[r], a = W.Y[r][lane];
-            z.x += v.x * a.x + v.y * a.y;
-            z.y += v.x * a.y - v.y * a.x;
-          }
-          z = make_double2(hh.tau * z.x, hh.tau * z.y);
-          for (int r = 0; r < len; ++r) {
-            const double2 v = W.vh[r];
-            double2 a = W.Y[r][lane];
-            a.x -= v.x * z.x - v.y * z.y;
-            a.y -= v.x * z.y + v.y * z.x;
-            W.Y[r][lane] = a;
-          }
-        }
+        const double2 u = W.ug[lane];
+        const double2 wu = make_double2(w.x * u.x + w.y * u.y, w.y * u.x - w.x * u.y);  // w conj(u)
+        W.cb[lane] = make_double2(tauh * (a0.x + a1.x - wu.x), tauh * (a0.y + a1.y - wu.y));
       }
       __syncwarp();
-      // ---- next right reflector from Y[0, :] (row s)
+      // ---- X: fused rank-2 row update, straight to HBM: X' = X - ty conj(u) - v b
+      if (lane < len) {
+        double2* dst = blk;
+#pragma unroll 4
+        for (int c = 0; c < BWc; ++c, dst += ld) {
+          const double2 u = W.ug[c], b = W.cb[c];
+          double2 z = W.X[lane][c];
+          z.x -= (ty.x * u.x + ty.y * u.y) + (v.x * b.x - v.y * b.y);
+          z.y -= (ty.y * u.x - ty.x * u.y) + (v.x * b.y + v.y * b.x);
+          if (c == 0 && tauh != 0.0) z = lane == 0 ? hh.beta : zero;
+          if (c < len) *dst = z;
+        }
+      }
       double next_tau = 0.0;
       if (lb > 0) {
-        double2 x = make_double2(0.0, 0.0);
-        if (lane < lb) x = make_double2(W.Y[0][lane].x, -W.Y[0][lane].y);
-        const double sg2 = warp_sum(x.x * x.x + x.y * x.y);
-        const double2 al = make_double2(__shfl_sync(0xffffffffu, x.x, 0), __shfl_sync(0xffffffffu, x.y, 0));
-        const Reflector hg = make_reflector(al, sg2);
+        // ---- Y column pass: q = v^H Y, row 0 of H Y -> next right reflector G'
+        double2 q;
+        {
+          double2 a0 = zero, a1 = zero;
+#pragma unroll 4
+          for (int r = 0; r < BWc; r += 2) {
+            const double2 v0 = W.vh[r], y0c = W.Y[r][lane], v1 = W.vh[r + 1], y1c = W.Y[r + 1][lane];
+            a0.x = fma(v0.x, y0c.x, fma(v0.y, y0c.y, a0.x));
+            a0.y = fma(v0.x, y0c.y, fma(-v0.y, y0c.x, a0.y));
+            a1.x = fma(v1.x, y1c.x, fma(v1.y, y1c.y, a1.x));
+            a1.y = fma(v1.x, y1c.y, fma(-v1.y, y1c.x, a1.y));
+          }
+          q = make_double2(a0.x + a1.x, a0.y + a1.y);
+        }
+        const double2 y0 = W.Y[0][lane];
+        const double2 xg = make_double2(y0.x - tauh * q.x, -(y0.y - tauh * q.y));  // conj(row 0 of H Y)
+        const double sg2 = warp_sum(xg.x * xg.x + xg.y * xg.y);
+        const double2 al = make_double2(__shfl_sync(0xffffffffu, xg.x, 0), __shfl_sync(0xffffffffu, xg.y, 0));
+        const QuickReflector hg = quick_reflector(al, sg2);
         next_tau = hg.tau;
+        const double2 u2 = lane == 0 ? make_double2(1.0, 0.0) : cmul(xg, hg.scale);  // zero on padded columns
+        const double2 qu = warp_csum(cmul(q, u2));                                    // (v^H Y) u'
+        __syncwarp();  // everyone is done with ug (X update) and cb
+        W.ug[lane] = u2;
+        W.cb[lane] = make_double2(tauh * q.x, tauh * q.y);  // d_c
         __syncwarp();
-        if (lane < lb) {
-          W.ug[lane] = lane == 0 ? make_double2(1.0, 0.0) : cmul(x, hg.scale);
-          if (next_tau != 0.0) {
-            double2 o = make_double2(0.0, 0.0);
-            if (lane == 0) {
-              const double sg = sqrt(sg2), aa = hypot(al.x, al.y);
-              const double2 ph = aa > 0.0 ? make_double2(al.x / aa, al.y / aa) : make_double2(1.0, 0.0);
-              o = make_double2(-ph.x * sg, ph.y * sg);
-            }
-            W.Y[0][lane] = o;
+        // ---- Y row pass: f = tau_g' (Y u' - tau_h v (q . u')), Y' = Y - v d - f conj(u'), to HBM
+        if (lane < len) {
+          double2 a0 = zero, a1 = zero;
+#pragma unroll 4
+          for (int c = 0; c < BWc; c += 2) {
+            const double2 y0c = W.Y[lane][c], u0 = W.ug[c], y1c = W.Y[lane][c + 1], u1 = W.ug[c + 1];
+            a0.x = fma(y0c.x, u0.x, fma(-y0c.y, u0.y, a0.x));
+            a0.y = fma(y0c.x, u0.y, fma(y0c.y, u0.x, a0.y));
+            a1.x = fma(y1c.x, u1.x, fma(-y1c.y, u1.y, a1.x));
+            a1.y = fma(y1c.x, u1.y, fma(y1c.y, u1.x, a1.y));
+          }
+          const double2 vq = cmul(v, qu);
+          const double2 f = make_double2(next_tau * (a0.x + a1.x - tauh * vq.x), next_tau * (a0.y + a1.y - tauh * vq.y));
+          const bool row0 = lane == 0 && next_tau != 0.0;
+          double2* dst = blk + (size_t)len * ld;
+#pragma unroll 4
+          for (int c = 0; c < BWc; ++c, dst += ld) {
+            const double2 u = W.ug[c], d = W.cb[c];
+            double2 z = W.Y[lane][c];
+            z.x -= (v.x * d.x - v.y * d.y) + (f.x * u.x + f.y * u.y);
+            z.y -= (v.x * d.y + v.y * d.x) + (f.y * u.x - f.x * u.y);
+            if (row0) z = c == 0 ? make_double2(hg.beta.x, -hg.beta.y) : zero;  // (conj beta', 0, ...)
+            if (c < lb) *dst = z;
           }
         }
-      }
-      __syncwarp();
-      // ---- write X and Y back (lane = row, coalesced per column)
-      if (lane < len) {
-        for (int cc = 0; cc < len; ++cc) C[(size_t)(s + cc) * ld + s + lane] = W.X[lane][cc];
-        for (int cc = 0; cc < lb; ++cc) C[(size_t)(s + len + cc) * ld + s + lane] = W.Y[lane][cc];
       }
       taug = next_tau;
       __threadfence_block();
