@@ -348,7 +348,7 @@ int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, 
     BD_CUDA(cudaGetLastError());
     if (bd_reduce(ws, L, cnt, dims, st)) return -1;
     launch_eig_idos(ce, nk, g, m0, cnt, reinterpret_cast<const double*>(ws + L.tgk_off), L.stride * 2, dims, diff,
-                    trans, eigs, status, sharp, st, refine, refine_count);
+                    trans, eigs, status, sharp, st, refine, refine_count, true);
     BD_CUDA(cudaGetLastError());
   }
   return 0;

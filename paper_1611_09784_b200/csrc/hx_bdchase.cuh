@@ -42,37 +42,6 @@ __device__ __forceinline__ double2 cmul_cj(double2 a, double2 b) {  // conj(a) *
 }
 __device__ __forceinline__ double2 warp_csum(double2 v) { return make_double2(warp_sum(v.x), warp_sum(v.y)); }
 
-// Householder reflector for x with x_0 = alpha, |x|^2 = sig2 (same convention as make_reflector):
-// H = I - tau v v^H, v_0 = 1, v_i = x_i * scale, H x = beta e_0, beta = -phase(alpha) sqrt(sig2).
-// Division-free (rsqrt + one reciprocal) to keep the chase's critical path and code size short.
-struct QuickReflector {
-  double tau;
-  double2 scale, beta;
-};
-__device__ __forceinline__ QuickReflector quick_reflector(double2 alpha, double sig2) {
-  QuickReflector h;
-  if (!(sig2 > 0.0)) {
-    h.tau = 0.0;
-    h.scale = make_double2(0.0, 0.0);
-    h.beta = make_double2(0.0, 0.0);
-    return h;
-  }
-  const double rs = rsqrt(sig2), sigma = sig2 * rs;
-  const double a2 = alpha.x * alpha.x + alpha.y * alpha.y;
-  double2 ph = make_double2(1.0, 0.0);
-  double aa = 0.0;
-  if (a2 > 0.0) {
-    const double ra = rsqrt(a2);
-    aa = a2 * ra;
-    ph = make_double2(alpha.x * ra, alpha.y * ra);
-  }
-  const double mag = aa + sigma, rm = __drcp_rn(mag);
-  h.tau = mag * rs;
-  h.scale = make_double2(ph.x * rm, -ph.y * rm);
-  h.beta = make_double2(-ph.x * sigma, -ph.y * sigma);
-  return h;
-}
-
 template <int NW, int BWc>
 __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_t stride, size_t c_off,
                                                                size_t tgk_off, int S, const int* dims) {

@@ -99,12 +99,18 @@ static __device__ void assemble_bipartite(const CellDev& c, const int* idx_a, co
 // then zeros (d = rows + cols).  u, s: complex scratch of max(rows, cols); red: 128 doubles.
 static __device__ void bidiag_tgk(double2* M, int lm, int rows, int cols, double* diag, double* e2, double2* u,
                                   double2* s, double* red) {
+  (void)s;
   const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = bd >> 5;
   const int d = rows + cols;
   for (int i = tid; i < d; i += bd) {
     diag[i] = 0.0;
     e2[i] = 0.0;
   }
+  // Thread layouts (no integer division, conflict-free: 8 consecutive lanes walk 8 consecutive rows):
+  //   left  (column) pass: row group g = lane & 7, column (tid >> 3) + k * bd/8; sums over g by xor 1,2,4
+  //   right (row) pass:    row (lane & 7) + 8 * warp + k * 8 nw, column group q = lane >> 3 (4 groups);
+  //                        sums over q by xor 8,16
+  const int g = lane & 7, q = lane >> 3;
   for (int j = 0; j < cols; ++j) {
     // ---------------- left reflector: column j, rows j..rows-1
     {
@@ -115,33 +121,35 @@ static __device__ void bidiag_tgk(double2* M, int lm, int rows, int cols, double
       }
       const double sig2 = block_sum(part, red);
       const double2 alpha = M[j + (size_t)j * lm];
-      const Reflector h = make_reflector(alpha, sig2);
+      const QuickReflector h = quick_reflector(alpha, sig2);
       if (tid == 0) e2[2 * j] = sig2;
       if (h.tau != 0.0) {
         for (int i = j + tid; i < rows; i += bd) u[i] = i == j ? make_double2(1.0, 0.0) : cmul(M[i + (size_t)j * lm], h.scale);
         __syncthreads();
-        // s_c = v^H M[:, c] for c > j (warp per column, lanes over rows)
-        for (int cc = j + 1 + warp; cc < cols; cc += nw) {
+        // M[:, c] -= v (tau v^H M[:, c]) for c > j: 8 lanes per column, the column sum stays in the group
+        for (int c0 = j + 1; c0 < cols; c0 += bd >> 3) {
+          const int cc = c0 + (tid >> 3);
           double2 acc = make_double2(0.0, 0.0);
-          for (int i = j + lane; i < rows; i += 32) {
-            const double2 a = u[i], b = M[i + (size_t)cc * lm];
-            acc.x += a.x * b.x + a.y * b.y;
-            acc.y += a.x * b.y - a.y * b.x;
+          if (cc < cols)
+            for (int i = j + g; i < rows; i += 8) {
+              const double2 a = u[i], b = M[i + (size_t)cc * lm];
+              acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));
+              acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
+            }
+#pragma unroll
+          for (int o = 1; o < 8; o <<= 1) {
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
           }
-          acc.x = warp_sum(acc.x);
-          acc.y = warp_sum(acc.y);
-          if (lane == 0) s[cc] = make_double2(h.tau * acc.x, h.tau * acc.y);
-        }
-        __syncthreads();
-        // M[:, c] -= v s_c
-        const int w = cols - j - 1, hgt = rows - j;
-        for (int p = tid; p < w * hgt; p += bd) {
-          const int cc = j + 1 + p / hgt, i = j + p % hgt;
-          const double2 a = u[i], b = s[cc];
-          double2 x = M[i + (size_t)cc * lm];
-          x.x -= a.x * b.x - a.y * b.y;
-          x.y -= a.x * b.y + a.y * b.x;
-          M[i + (size_t)cc * lm] = x;
+          const double2 sc = make_double2(h.tau * acc.x, h.tau * acc.y);
+          if (cc < cols)
+            for (int i = j + g; i < rows; i += 8) {
+              const double2 a = u[i];
+              double2 x = M[i + (size_t)cc * lm];
+              x.x = fma(-a.x, sc.x, fma(a.y, sc.y, x.x));
+              x.y = fma(-a.x, sc.y, fma(-a.y, sc.x, x.y));
+              M[i + (size_t)cc * lm] = x;
+            }
         }
         __syncthreads();
       }
@@ -156,7 +164,7 @@ static __device__ void bidiag_tgk(double2* M, int lm, int rows, int cols, double
       }
       const double sig2 = block_sum(part, red);
       const double2 a0 = M[j + (size_t)(j + 1) * lm];
-      const Reflector h = make_reflector(make_double2(a0.x, -a0.y), sig2);
+      const QuickReflector h = quick_reflector(make_double2(a0.x, -a0.y), sig2);
       if (tid == 0) e2[2 * j + 1] = sig2;
       if (h.tau != 0.0) {
         // u_c from conj(row j): u_{j+1} = 1
@@ -165,26 +173,30 @@ static __device__ void bidiag_tgk(double2* M, int lm, int rows, int cols, double
           u[cc] = cc == j + 1 ? make_double2(1.0, 0.0) : cmul(make_double2(x.x, -x.y), h.scale);
         }
         __syncthreads();
-        // w_r = tau * sum_c M[r][c] u_c for rows r > j (thread per row)
-        for (int r = j + 1 + tid; r < rows; r += bd) {
+        // M[r, :] -= (tau M[r, :] u) u^H for rows r > j: 4 lanes per row (column groups)
+        for (int r0 = j + 1; r0 < rows; r0 += 8 * nw) {
+          const int r = r0 + g + 8 * warp;
           double2 acc = make_double2(0.0, 0.0);
-          for (int cc = j + 1; cc < cols; ++cc) {
-            const double2 a = M[r + (size_t)cc * lm], b = u[cc];
-            acc.x += a.x * b.x - a.y * b.y;
-            acc.y += a.x * b.y + a.y * b.x;
-          }
-          s[r] = make_double2(h.tau * acc.x, h.tau * acc.y);
-        }
-        __syncthreads();
-        // M[r][c] -= w_r conj(u_c)
-        const int w = cols - j - 1, hgt = rows - j - 1;
-        for (int p = tid; p < w * hgt; p += bd) {
-          const int cc = j + 1 + p / hgt, r = j + 1 + p % hgt;
-          const double2 a = s[r], b = u[cc];
-          double2 x = M[r + (size_t)cc * lm];
-          x.x -= a.x * b.x + a.y * b.y;
-          x.y -= a.y * b.x - a.x * b.y;
-          M[r + (size_t)cc * lm] = x;
+          if (r < rows)
+            for (int cc = j + 1 + q; cc < cols; cc += 4) {
+              const double2 a = M[r + (size_t)cc * lm], b = u[cc];
+              acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+              acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+            }
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 8);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 8);
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+          const double2 w = make_double2(h.tau * acc.x, h.tau * acc.y);
+          if (r < rows)
+            for (int cc = j + 1 + q; cc < cols; cc += 4) {
+              const double2 b = u[cc];
+              double2 x = M[r + (size_t)cc * lm];
+              // x -= w conj(b)
+              x.x = fma(-w.x, b.x, fma(-w.y, b.y, x.x));
+              x.y = fma(-w.y, b.x, fma(w.x, b.y, x.y));
+              M[r + (size_t)cc * lm] = x;
+            }
         }
         __syncthreads();
       }

@@ -343,7 +343,8 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
       // masks/kpts offsets: the kernel indexes matrices from blockIdx.x; shift the mask base by whole masks
       if (m0 % nk) return fail(HX_E_ARG, "internal: chunk not aligned to k-point groups");
       const uint64_t* mk0 = d_masks + (m0 / nk) * c.words;
-      if (c.bipartite && ctx->use_bipartite && hx::small_bidiag_smem(N, c.nsub) <= 200 * 1024) {
+      const bool tgk = c.bipartite && ctx->use_bipartite && hx::small_bidiag_smem(N, c.nsub) <= 200 * 1024;
+      if (tgk) {
         hx::small_bidiag_kernel<<<(unsigned)cnt, N > 64 ? 256 : 128, hx::small_bidiag_smem(N, c.nsub), st>>>(
             c, kp, nk, mk0, tri, dims, status + m0);
       } else {
@@ -353,7 +354,7 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
       HX_CUDA(cudaGetLastError());
       hx::count_launch();
       hx::launch_eig_idos(c, nk, g, m0, cnt, tri, (size_t)2 * N, dims, diff, trans, d_eigs, status, sharp, st, refine,
-                          refine_count);
+                          refine_count, tgk);
       HX_CUDA(cudaGetLastError());
     }
   } else if (c.bipartite && ctx->use_bipartite && hx::bd_path_supported(c) && N > HX_SMEM_MAX_N) {

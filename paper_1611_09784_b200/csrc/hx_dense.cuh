@@ -191,6 +191,37 @@ __device__ __forceinline__ Reflector make_reflector(double2 alpha, double sigma2
   return h;
 }
 
+// Householder reflector for x with x_0 = alpha, |x|^2 = sig2 (same convention as make_reflector):
+// H = I - tau v v^H, v_0 = 1, v_i = x_i * scale, H x = beta e_0, beta = -phase(alpha) sqrt(sig2).
+// Division-free (rsqrt + one reciprocal) to keep the chase's critical path and code size short.
+struct QuickReflector {
+  double tau;
+  double2 scale, beta;
+};
+__device__ __forceinline__ QuickReflector quick_reflector(double2 alpha, double sig2) {
+  QuickReflector h;
+  if (!(sig2 > 0.0)) {
+    h.tau = 0.0;
+    h.scale = make_double2(0.0, 0.0);
+    h.beta = make_double2(0.0, 0.0);
+    return h;
+  }
+  const double rs = rsqrt(sig2), sigma = sig2 * rs;
+  const double a2 = alpha.x * alpha.x + alpha.y * alpha.y;
+  double2 ph = make_double2(1.0, 0.0);
+  double aa = 0.0;
+  if (a2 > 0.0) {
+    const double ra = rsqrt(a2);
+    aa = a2 * ra;
+    ph = make_double2(alpha.x * ra, alpha.y * ra);
+  }
+  const double mag = aa + sigma, rm = __drcp_rn(mag);
+  h.tau = mag * rs;
+  h.scale = make_double2(ph.x * rm, -ph.y * rm);
+  h.beta = make_double2(-ph.x * sigma, -ph.y * sigma);
+  return h;
+}
+
 // Tridiagonalise the d x d Hermitian matrix held in real-packed storage R (smem), unblocked, with
 // three CTA barriers per column: the next column's norm is accumulated while the trailing update is
 // applied, the Hermitian matrix-vector product uses P threads per row (shuffle-combined), and the
@@ -420,6 +451,31 @@ __device__ __forceinline__ int sturm_count(const double* diag, const double* e2,
   int cnt = q < 0.0;
   for (int i = 1; i < d; ++i) {
     q = (diag[i] - x) - e2[i - 1] / q;
+    if (fabs(q) <= pivmin) q = -pivmin;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+// 1/q to full double precision without the division routine: MUFU reciprocal seed + two Newton steps.
+// |q| >= pivmin = DBL_MIN * max(1, max e2) keeps q normal and e2/q finite (dstebz's pivmin argument).
+__device__ __forceinline__ double sturm_rcp(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  r = fma(r, fma(-q, r, 1.0), r);
+  r = fma(r, fma(-q, r, 1.0), r);
+  return r;
+}
+
+// Sturm count (number of eigenvalues < x) with the reciprocal above; ZD: zero diagonal (TGK matrix).
+template <bool ZD>
+__device__ __forceinline__ int sturm_count_fast(const double* __restrict__ diag, const double* __restrict__ e2, int d,
+                                                double x, double pivmin) {
+  double q = (ZD ? 0.0 : diag[0]) - x;
+  if (fabs(q) <= pivmin) q = -pivmin;
+  int cnt = q < 0.0;
+  for (int i = 1; i < d; ++i) {
+    q = fma(-e2[i - 1], sturm_rcp(q), (ZD ? 0.0 : diag[i]) - x);
     if (fabs(q) <= pivmin) q = -pivmin;
     cnt += q < 0.0;
   }

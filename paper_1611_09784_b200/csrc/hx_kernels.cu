@@ -9,6 +9,7 @@
 //  * finalize_kernel: prefix-sum of the integer full-weight counts + fixed-point transition sums
 //    -> per-mask IDOS curves (qoi.py:96-102: values = counts / area, weights 1/nk).
 #include <cuda_runtime.h>
+#include <limits.h>
 #include <stdint.h>
 
 #include "hx_bidiag.cuh"
@@ -138,8 +139,49 @@ size_t global_ws_stride(int N, bool general) {
 }
 
 // ------------------------------------------------------------------------------------------------
-// One thread per (matrix, eigenvalue index).  tri: per matrix `tri_stride` doubles, diag at 0 and e2
-// at +N (N = c.N).  Matrices with dims == 0 (all vacant / failed) contribute nothing.
+// Early exit of the bisection (no eigenvalue output): an eigenvalue whose bracket [lo, hi] maps entirely
+// into one gap between the transition windows contributes a full weight at a determined grid index
+// (the index arithmetic of _kernels.py:68-101 is constant over the widened bracket, so the result
+// equals the reference's for any eigenvalue in it).  Returns the index or LLONG_MIN if not settled.
+static __device__ __forceinline__ long long settle_index(const CellDev& c, const GridDev& g, int sharp, double lo,
+                                                         double hi) {
+  const double ea = pencil_map(c, lo), eb = pencil_map(c, hi);
+  double Ea = fmin(ea, eb), Eb = fmax(ea, eb);
+  const double eta = 16.0 * DBL_EPSILON * fmax(1.0, fmax(fabs(Ea), fabs(Eb)));
+  Ea -= eta;
+  Eb += eta;
+  if (sharp) {
+    const long long ia = (long long)floor((Ea - g.e0) / g.step), ib = (long long)floor((Eb - g.e0) / g.step);
+    return ia == ib ? ia + 1 : LLONG_MIN;
+  }
+  const long long la = (long long)ceil((Ea + g.delta - g.e0) / g.step);
+  const long long lb = (long long)ceil((Eb + g.delta - g.e0) / g.step);
+  const long long ma = (long long)floor((Ea - g.delta - g.e0) / g.step) + 1;
+  const long long mb = (long long)floor((Eb - g.delta - g.e0) / g.step) + 1;
+  return (la == lb && ma == mb && ma >= la) ? la : LLONG_MIN;
+}
+
+static __device__ __forceinline__ void add_settled(const GridDev& g, int* diff, int64_t mk, long long l) {
+  const long long l0 = l < 0 ? 0 : l;
+  if (l0 < g.npts) atomicAdd(diff + mk * (g.npts + 1) + l0, 1);
+}
+
+// IDOS contribution (and status) of one eigenvalue lam of T
+static __device__ __forceinline__ void add_eigenvalue(const CellDev& c, const GridDev& g, int sharp, int* diff,
+                                                      unsigned long long* trans, int* status, int64_t mat, int nk,
+                                                      double lam) {
+  const double E = pencil_map(c, lam);
+  if (!isfinite(E)) atomicMax(status + mat, 2);
+  const int64_t mk = mat / nk;
+  if (sharp) sharp_state(g, E, diff + mk * (g.npts + 1));
+  else idos_state(g, E, diff + mk * (g.npts + 1), trans + mk * g.npts);
+}
+
+// One thread per (matrix, eigenvalue index) - for TGK tridiagonals one thread per +-pair: it bisects
+// lambda_{d-1-j} >= 0 and also accounts for -lambda_{d-1-j} = lambda_j.  tri: per matrix `tri_stride`
+// doubles, diag at 0 and e2 at +N (N = c.N).  Matrices with dims == 0 (all vacant / failed) contribute
+// nothing.
+template <bool TGK>
 __global__ void __launch_bounds__(128) eig_idos_kernel(CellDev c, int nk, GridDev g, int64_t mat0, int64_t nmat,
                                                        const double* __restrict__ tri, size_t tri_stride,
                                                        const int* __restrict__ dims, int* diff,
@@ -147,16 +189,37 @@ __global__ void __launch_bounds__(128) eig_idos_kernel(CellDev c, int nk, GridDe
                                                        int sharp, RefineItem* refine,
                                                        unsigned long long* refine_count) {
   const int N = c.N;
+  const int per = TGK ? (N + 1) / 2 : N;
   const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t lm = slot / N;
+  const int64_t lm = slot / per;
   if (lm >= nmat) return;
-  const int idx = (int)(slot - lm * N);
+  const int j = (int)(slot - lm * per);
   const int64_t mat = mat0 + lm;
   const int d = dims[lm];
   double* eig_out = eigs ? eigs + mat * N : nullptr;
-  if (idx >= d) {
-    if (eig_out) eig_out[idx] = qnan();
-    return;
+  const bool rev = (c.pencil == 1) && (c.t - c.s * c.eps0 < 0.0);
+  auto put = [&](int k, double E) {
+    if (eig_out) eig_out[rev ? d - 1 - k : k] = E;
+  };
+  if (eig_out) {  // padding beyond d
+    if (j >= d) eig_out[j] = qnan();
+    if (TGK && N - 1 - j >= d && N - 1 - j != j) eig_out[N - 1 - j] = qnan();
+  }
+  // index bisected by this thread and whether its mirror is also ours
+  int idx;
+  bool mirror = false;
+  if (TGK) {
+    if (2 * j + 1 > d) return;  // j >= ceil(d/2)
+    idx = d - 1 - j;
+    if (idx == j) {  // odd d: the middle eigenvalue of a symmetric spectrum is exactly 0
+      if (diff) add_eigenvalue(c, g, sharp, diff, trans, status, mat, nk, 0.0);
+      put(j, pencil_map(c, 0.0));
+      return;
+    }
+    mirror = true;
+  } else {
+    if (j >= d) return;
+    idx = j;
   }
   const double* diag = tri + lm * tri_stride;
   const double* e2 = diag + N;
@@ -165,8 +228,9 @@ __global__ void __launch_bounds__(128) eig_idos_kernel(CellDev c, int nk, GridDe
   for (int i = 0; i < d; ++i) {
     const double er2 = i + 1 < d ? e2[i] : 0.0;
     const double er = sqrt(er2);
-    gl = fmin(gl, diag[i] - el - er);
-    gu = fmax(gu, diag[i] + el + er);
+    const double di = TGK ? 0.0 : diag[i];
+    gl = fmin(gl, di - el - er);
+    gu = fmax(gu, di + el + er);
     em = fmax(em, er2);
     el = er;
   }
@@ -175,75 +239,54 @@ __global__ void __launch_bounds__(128) eig_idos_kernel(CellDev c, int nk, GridDe
   gl = gl - 2.1 * tnorm * DBL_EPSILON * d - 4.2 * pivmin;
   gu = gu + 2.1 * tnorm * DBL_EPSILON * d + 4.2 * pivmin;
   double lo = gl, hi = gu;
-  // Without an eigenvalue output, an eigenvalue whose bracket maps entirely into one gap between the
-  // transition windows contributes a full weight at a determined grid index: stop bisecting there
-  // (the index arithmetic of _kernels.py:68-101 is constant over the widened bracket, so the result
-  // equals the reference's for any eigenvalue in it).
   const bool early = eigs == nullptr && refine != nullptr;
-  bool settled = false;
-  long long settled_lo = 0;
+  // settle state: bit 0 = lambda settled, bit 1 = mirror settled (or not needed)
+  int done = mirror ? 0 : 2;
+  const int64_t mk = mat / nk;
   for (int it = 0; it < 200; ++it) {
     const double mid = 0.5 * (lo + hi);
     const double tol = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin;
     if (hi - lo <= tol || mid <= lo || mid >= hi) break;
     if (early && it >= 4) {
-      const double ea = pencil_map(c, lo), eb = pencil_map(c, hi);
-      double Ea = fmin(ea, eb), Eb = fmax(ea, eb);
-      const double eta = 16.0 * DBL_EPSILON * fmax(1.0, fmax(fabs(Ea), fabs(Eb)));
-      Ea -= eta;
-      Eb += eta;
-      if (sharp) {
-        const long long ia = (long long)floor((Ea - g.e0) / g.step), ib = (long long)floor((Eb - g.e0) / g.step);
-        if (ia == ib) {
-          settled = true;
-          settled_lo = ia + 1;
-          break;
-        }
-      } else {
-        const long long la = (long long)ceil((Ea + g.delta - g.e0) / g.step);
-        const long long lb = (long long)ceil((Eb + g.delta - g.e0) / g.step);
-        const long long ma = (long long)floor((Ea - g.delta - g.e0) / g.step) + 1;
-        const long long mb = (long long)floor((Eb - g.delta - g.e0) / g.step) + 1;
-        if (la == lb && ma == mb && ma >= la) {
-          settled = true;
-          settled_lo = la;
-          break;
+      if (!(done & 1)) {
+        const long long l = settle_index(c, g, sharp, lo, hi);
+        if (l != LLONG_MIN) {
+          add_settled(g, diff, mk, l);
+          done |= 1;
         }
       }
+      if (!(done & 2)) {
+        const long long l = settle_index(c, g, sharp, -hi, -lo);
+        if (l != LLONG_MIN) {
+          add_settled(g, diff, mk, l);
+          done |= 2;
+        }
+      }
+      if (done == 3) return;
       if (it >= 14) {
         // phase 1 done: hand the bracket to the dense refinement pass (keeps warps free of divergence)
         const unsigned long long pos = atomicAdd(refine_count, 1ull);
-        refine[pos] = RefineItem{mat, lm, idx, lo, hi, pivmin};
+        refine[pos] = RefineItem{mat, lm, idx, (~done) & 3, lo, hi, pivmin};
         return;
       }
     }
-    if (sturm_count(diag, e2, d, mid, pivmin) > idx) hi = mid;
+    if (sturm_count_fast<TGK>(diag, e2, d, mid, pivmin) > idx) hi = mid;
     else lo = mid;
   }
-  if (settled) {
-    if (diff) {
-      const int64_t mk = mat / nk;
-      const long long l0 = settled_lo < 0 ? 0 : settled_lo;
-      if (l0 < g.npts) atomicAdd(diff + mk * (g.npts + 1) + l0, 1);
-    }
-    return;
-  }
   const double lam = 0.5 * (lo + hi);
-  const double E = pencil_map(c, lam);
-  if (!isfinite(E)) atomicMax(status + mat, 2);
   if (diff) {
-    const int64_t mk = mat / nk;
-    if (sharp) sharp_state(g, E, diff + mk * (g.npts + 1));
-    else idos_state(g, E, diff + mk * (g.npts + 1), trans + mk * g.npts);
+    if (!(done & 1)) add_eigenvalue(c, g, sharp, diff, trans, status, mat, nk, lam);
+    if (!(done & 2)) add_eigenvalue(c, g, sharp, diff, trans, status, mat, nk, -lam);
+  } else {
+    if (!isfinite(pencil_map(c, lam)) || (mirror && !isfinite(pencil_map(c, -lam)))) atomicMax(status + mat, 2);
   }
-  if (eig_out) {
-    const bool rev = (c.pencil == 1) && (c.t - c.s * c.eps0 < 0.0);
-    eig_out[rev ? d - 1 - idx : idx] = E;
-  }
+  put(idx, pencil_map(c, lam));
+  if (mirror) put(d - 1 - idx, pencil_map(c, -lam));
 }
 
 // Phase 2: full-precision bisection of the eigenvalues left unsettled by eig_idos_kernel, densely
-// packed (every lane of a warp has real work), then the IDOS contribution.
+// packed (every lane of a warp has real work), then the IDOS contribution (+ the TGK mirror).
+template <bool TGK>
 __global__ void __launch_bounds__(128) eig_refine_kernel(CellDev c, int nk, GridDev g, const double* __restrict__ tri,
                                                          size_t tri_stride, const int* __restrict__ dims, int* diff,
                                                          unsigned long long* trans, int* status, int sharp,
@@ -261,14 +304,41 @@ __global__ void __launch_bounds__(128) eig_refine_kernel(CellDev c, int nk, Grid
       const double mid = 0.5 * (lo + hi);
       const double tol = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + it.pivmin;
       if (hi - lo <= tol || mid <= lo || mid >= hi) break;
-      if (sturm_count(diag, e2, d, mid, it.pivmin) > it.idx) hi = mid;
+      if (sturm_count_fast<TGK>(diag, e2, d, mid, it.pivmin) > it.idx) hi = mid;
       else lo = mid;
     }
-    const double E = pencil_map(c, 0.5 * (lo + hi));
-    if (!isfinite(E)) atomicMax(status + it.mat, 2);
-    const int64_t mk = it.mat / nk;
-    if (sharp) sharp_state(g, E, diff + mk * (g.npts + 1));
-    else idos_state(g, E, diff + mk * (g.npts + 1), trans + mk * g.npts);
+    const double lam = 0.5 * (lo + hi);
+    if (it.flags & 1) add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, lam);
+    if (it.flags & 2) add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, -lam);
+  }
+}
+
+void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, int64_t nmat, const double* tri,
+                     size_t tri_stride, const int* dims, int* diff, unsigned long long* trans, double* eigs,
+                     int* status, int sharp, cudaStream_t st, RefineItem* refine, unsigned long long* refine_count,
+                     bool tgk) {
+  const int64_t per = tgk ? (c.N + 1) / 2 : c.N;
+  const int64_t slots = nmat * per;
+  const bool two_pass = refine && refine_count && diff && !eigs;
+  if (two_pass) cudaMemsetAsync(refine_count, 0, sizeof(unsigned long long), st);
+  const unsigned blocks = (unsigned)((slots + 127) / 128);
+  RefineItem* rf = two_pass ? refine : nullptr;
+  if (tgk)
+    eig_idos_kernel<true><<<blocks, 128, 0, st>>>(c, nk, g, mat0, nmat, tri, tri_stride, dims, diff, trans, eigs,
+                                                  status, sharp, rf, refine_count);
+  else
+    eig_idos_kernel<false><<<blocks, 128, 0, st>>>(c, nk, g, mat0, nmat, tri, tri_stride, dims, diff, trans, eigs,
+                                                   status, sharp, rf, refine_count);
+  count_launch();
+  if (two_pass) {
+    const int64_t rblocks = std::min<int64_t>((slots + 127) / 128, 148 * 16);
+    if (tgk)
+      eig_refine_kernel<true><<<(unsigned)rblocks, 128, 0, st>>>(c, nk, g, tri, tri_stride, dims, diff, trans, status,
+                                                                 sharp, refine, refine_count);
+    else
+      eig_refine_kernel<false><<<(unsigned)rblocks, 128, 0, st>>>(c, nk, g, tri, tri_stride, dims, diff, trans,
+                                                                  status, sharp, refine, refine_count);
+    count_launch();
   }
 }
 

@@ -14,9 +14,10 @@ namespace hx {
 
 // an eigenvalue bracket handed from the bisection pass to the dense refinement pass
 struct RefineItem {
-  int64_t mat;   // global matrix index (mask * nk + k)
-  int64_t lm;    // chunk-local matrix index (tri / dims row)
-  int64_t idx;   // eigenvalue index
+  int64_t mat;  // global matrix index (mask * nk + k)
+  int64_t lm;   // chunk-local matrix index (tri / dims row)
+  int idx;      // eigenvalue index
+  int flags;    // bit 0: contribute lambda; bit 1: contribute -lambda (TGK mirror)
   double lo, hi, pivmin;
 };
 
@@ -33,13 +34,6 @@ __global__ void global_tridiag_kernel(CellDev c, const double2* kpts, int nk, co
 size_t global_ws_stride(int N, bool general);
 
 // eigenvalues (bisection, thread per eigenvalue) + pencil map + IDOS accumulation + eigenvalue output
-__global__ void eig_idos_kernel(CellDev c, int nk, GridDev g, int64_t mat0, int64_t nmat, const double* tri,
-                                size_t tri_stride, const int* dims, int* diff, unsigned long long* trans, double* eigs,
-                                int* status, int sharp, RefineItem* refine, unsigned long long* refine_count);
-__global__ void eig_refine_kernel(CellDev c, int nk, GridDev g, const double* tri, size_t tri_stride, const int* dims,
-                                  int* diff, unsigned long long* trans, int* status, int sharp,
-                                  const RefineItem* items, const unsigned long long* count);
-
 __global__ void assemble_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, double2* H, double2* S,
                                 int* dims);
 
@@ -52,24 +46,11 @@ __global__ void finalize_kernel(const int* diff, const unsigned long long* trans
 
 // Eigenvalue stage over `nmat` matrices starting at global index mat0.  With a refinement buffer
 // (capacity >= nmat * N items) and no eigenvalue output, eigenvalues that settle into a gap between
-// transition windows stop early and the rest are finished by a densely packed second pass.
-inline void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, int64_t nmat, const double* tri,
-                            size_t tri_stride, const int* dims, int* diff, unsigned long long* trans, double* eigs,
-                            int* status, int sharp, cudaStream_t st, RefineItem* refine = nullptr,
-                            unsigned long long* refine_count = nullptr) {
-  const int64_t slots = nmat * (int64_t)c.N;
-  const bool two_pass = refine && refine_count && diff && !eigs;
-  if (two_pass) cudaMemsetAsync(refine_count, 0, sizeof(unsigned long long), st);
-  eig_idos_kernel<<<(unsigned)((slots + 127) / 128), 128, 0, st>>>(c, nk, g, mat0, nmat, tri, tri_stride, dims, diff,
-                                                                   trans, eigs, status, sharp,
-                                                                   two_pass ? refine : nullptr, refine_count);
-  count_launch();
-  if (two_pass) {
-    const int64_t blocks = std::min<int64_t>((slots + 127) / 128, 148 * 16);
-    eig_refine_kernel<<<(unsigned)blocks, 128, 0, st>>>(c, nk, g, tri, tri_stride, dims, diff, trans, status, sharp,
-                                                        refine, refine_count);
-    count_launch();
-  }
-}
+// transition windows stop early and the rest are finished by a densely packed second pass.  tgk: the
+// tridiagonals are Golub-Kahan (zero diagonal, spectrum symmetric about 0): one thread per +-pair.
+void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, int64_t nmat, const double* tri,
+                     size_t tri_stride, const int* dims, int* diff, unsigned long long* trans, double* eigs,
+                     int* status, int sharp, cudaStream_t st, RefineItem* refine = nullptr,
+                     unsigned long long* refine_count = nullptr, bool tgk = false);
 
 }  // namespace hx
