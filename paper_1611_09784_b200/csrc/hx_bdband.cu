@@ -86,15 +86,33 @@ __global__ void __launch_bounds__(256) bd_assemble_kernel(CellDev c, const doubl
 }
 
 // ------------------------------------------------------------------------------------------------
+// Asynchronous 16-byte global -> shared copy; src_bytes = 0 zero-fills the destination.
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // X[rows x BB] = op(A) V, op(A)[i][k] = M[ar0+i][ac0+k] (MODE 0) or conj(M[ar0+k][ac0+i]) (MODE 1),
-// V [K x BB] (ld S).  64-row tiles, 4 warps x (16 x 32), DMMA m8n8k4 f64.
-constexpr int XV_TM = 64, XV_TK = 16, XV_LD = XV_TK + 4;
+// V [K x BB] (ld S).  64-row tiles, 4 warps x (16 x 32), DMMA m8n8k4 f64, K in chunks of 16 through a
+// 3-stage cp.async pipeline.  Shared layouts keep the fragment loads conflict-free:
+//   MODE 0: As[k][i] (i contiguous, the matrix's column direction), ld 66 (= 2 mod 8 in 16 B units)
+//   MODE 1: As[i][k] (k contiguous), ld 20 (= 4 mod 8); the conjugate is applied at fragment load.
+constexpr int XV_TM = 64, XV_TK = 16, XV_ST = 3;
+constexpr int XV_LD0 = XV_TM + 2, XV_LD1 = XV_TK + 4, XV_LDV = XV_TK + 4;
+constexpr int XV_A_ELEMS = XV_TK * XV_LD0 > XV_TM * XV_LD1 ? XV_TK * XV_LD0 : XV_TM * XV_LD1;
+constexpr size_t XV_SMEM = (size_t)XV_ST * (XV_A_ELEMS + BB * XV_LDV) * sizeof(double2);
 
 template <int MODE>
 __global__ void __launch_bounds__(128) xv_kernel(double2* ws, BdWs L, int ar0, int ac0, int rows, int K,
                                                  size_t v_off, size_t x_off) {
-  __shared__ double2 As[XV_TM][XV_LD];
-  __shared__ double2 Vs[BB][XV_LD];
+  extern __shared__ __align__(16) double2 xv_sm[];
+  double2* As = xv_sm;                         // [XV_ST][XV_A_ELEMS]
+  double2* Vs = xv_sm + XV_ST * XV_A_ELEMS;    // [XV_ST][BB][XV_LDV]
   double2* base = ws + (size_t)blockIdx.y * L.stride;
   const int ld = L.S;
   const double2* M = base + L.c_off;
@@ -102,50 +120,78 @@ __global__ void __launch_bounds__(128) xv_kernel(double2* ws, BdWs L, int ar0, i
   double2* X = base + x_off;
   const int i0 = blockIdx.x * XV_TM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nchunks = (K + XV_TK - 1) / XV_TK;
+  auto load_chunk = [&](int ch, int stg) {
+    const int kk = ch * XV_TK;
+    double2* A = As + stg * XV_A_ELEMS;
+    if (MODE == 1) {
+      // element (i, k) at M[(ac0+i)*ld + ar0 + k]: 16 consecutive k per row i
+#pragma unroll
+      for (int q = 0; q < XV_TM * XV_TK / 128; ++q) {
+        const int p = tid + 128 * q, kc = p & (XV_TK - 1), r = p >> 4;
+        const int gi = i0 + r, gk = kk + kc;
+        const bool ok = gi < rows && gk < K;
+        cp_async16_zfill(A + r * XV_LD1 + kc, M + (ok ? (size_t)(ac0 + gi) * ld + ar0 + gk : 0), ok);
+      }
+    } else {
+      // element (i, k) at M[(ac0+k)*ld + ar0 + i]: 64 consecutive i per column k
+#pragma unroll
+      for (int q = 0; q < XV_TM * XV_TK / 128; ++q) {
+        const int p = tid + 128 * q, r = p & (XV_TM - 1), kc = p >> 6;
+        const int gi = i0 + r, gk = kk + kc;
+        const bool ok = gi < rows && gk < K;
+        cp_async16_zfill(A + kc * XV_LD0 + r, M + (ok ? (size_t)(ac0 + gk) * ld + ar0 + gi : 0), ok);
+      }
+    }
+    double2* Vt = Vs + stg * BB * XV_LDV;
+#pragma unroll
+    for (int q = 0; q < BB * XV_TK / 128; ++q) {
+      const int p = tid + 128 * q, kc = p & (XV_TK - 1), n = p >> 4;
+      const int gk = kk + kc;
+      const bool ok = gk < K;
+      cp_async16_zfill(Vt + n * XV_LDV + kc, V + (ok ? gk + (size_t)n * ld : 0), ok);
+    }
+  };
   CTile acc[2][4];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b].zero();
-  for (int kk = 0; kk < K; kk += XV_TK) {
-    if (MODE == 1) {
-      for (int p = tid; p < XV_TM * XV_TK; p += 128) {
-        const int cc = p & (XV_TK - 1), r = p / XV_TK;
-        const int gi = i0 + r, gk = kk + cc;
-        double2 z = make_double2(0.0, 0.0);
-        if (gi < rows && gk < K) z = M[(size_t)(ac0 + gi) * ld + ar0 + gk];
-        As[r][cc] = conj2(z);
-      }
-    } else {
-      for (int p = tid; p < XV_TM * XV_TK; p += 128) {
-        const int r = p & (XV_TM - 1), cc = p / XV_TM;
-        const int gi = i0 + r, gk = kk + cc;
-        double2 z = make_double2(0.0, 0.0);
-        if (gi < rows && gk < K) z = M[(size_t)(ac0 + gk) * ld + ar0 + gi];
-        As[r][cc] = z;
-      }
-    }
-    for (int p = tid; p < BB * XV_TK; p += 128) {
-      const int cc = p & (XV_TK - 1), n = p / XV_TK;
-      const int gk = kk + cc;
-      Vs[n][cc] = gk < K ? V[gk + (size_t)n * ld] : make_double2(0.0, 0.0);
-    }
+#pragma unroll
+  for (int stg = 0; stg < XV_ST - 1; ++stg) {
+    if (stg < nchunks) load_chunk(stg, stg);
+    cp_async_commit();
+  }
+  for (int ch = 0; ch < nchunks; ++ch) {
+    cp_async_wait<XV_ST - 2>();
     __syncthreads();
+    {  // prefetch chunk ch + ST - 1 into the stage freed at iteration ch - 1
+      const int nx = ch + XV_ST - 1;
+      if (nx < nchunks) load_chunk(nx, nx % XV_ST);
+      cp_async_commit();
+    }
+    const int stg = ch % XV_ST;
+    const double2* A = As + stg * XV_A_ELEMS;
+    const double2* Vt = Vs + stg * BB * XV_LDV;
 #pragma unroll
     for (int k4 = 0; k4 < XV_TK / 4; ++k4) {
       const int kc = 4 * k4 + (lane & 3);
       double2 a[2], b[4];
 #pragma unroll
-      for (int rt = 0; rt < 2; ++rt) a[rt] = As[16 * warp + 8 * rt + (lane >> 2)][kc];
+      for (int rt = 0; rt < 2; ++rt) {
+        const int r = 16 * warp + 8 * rt + (lane >> 2);
+        a[rt] = MODE == 1 ? A[r * XV_LD1 + kc] : A[kc * XV_LD0 + r];
+        if (MODE == 1) a[rt].y = -a[rt].y;
+      }
 #pragma unroll
-      for (int ct = 0; ct < 4; ++ct) b[ct] = Vs[8 * ct + (lane >> 2)][kc];
+      for (int ct = 0; ct < 4; ++ct) b[ct] = Vt[(8 * ct + (lane >> 2)) * XV_LDV + kc];
 #pragma unroll
       for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
         for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(a[rt].x, a[rt].y, b[ct].x, b[ct].y);
     }
-    __syncthreads();
   }
+  cp_async_wait<0>();
 #pragma unroll
   for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
@@ -189,13 +235,17 @@ __global__ void __launch_bounds__(256) xt_kernel(double2* ws, BdWs L, int rows, 
   }
 }
 
-// M[mr0:mr0+m, mc0:mc0+n] -= U W^H, U [m x BB] and W [n x BB] (ld S); 64 x 64 tiles, DMMA.
-constexpr int RU_T = 64, RU_K = 16, RU_LD = RU_K + 4;
+// M[mr0:mr0+m, mc0:mc0+n] -= U W^H, U [m x BB] and W [n x BB] (ld S); 64 x 64 tiles, DMMA.  The whole
+// K = BB depth of U and W is staged once with cp.async (ld 36 = 4 mod 8: conflict-free fragments) while
+// the C tile is read straight into the accumulators; 2 CTAs per SM.
+constexpr int RU_T = 64, RU_LD = BB + 4;
+constexpr size_t RU_SMEM = (size_t)2 * RU_T * RU_LD * sizeof(double2);
 
-__global__ void __launch_bounds__(256) rank_update_kernel(double2* ws, BdWs L, int mr0, int mc0, int m, int n,
-                                                          size_t u_off, size_t w_off) {
-  __shared__ double2 Us[RU_T][RU_LD];
-  __shared__ double2 Ws[RU_T][RU_LD];
+__global__ void __launch_bounds__(256, 2) rank_update_kernel(double2* ws, BdWs L, int mr0, int mc0, int m, int n,
+                                                             size_t u_off, size_t w_off) {
+  extern __shared__ __align__(16) double2 ru_sm[];
+  double2* Us = ru_sm;                // [RU_T][RU_LD]
+  double2* Ws = ru_sm + RU_T * RU_LD;  // [RU_T][RU_LD]
   double2* base = ws + (size_t)blockIdx.z * L.stride;
   const int ld = L.S;
   double2* M = base + L.c_off + (size_t)mc0 * ld + mr0;
@@ -204,6 +254,15 @@ __global__ void __launch_bounds__(256) rank_update_kernel(double2* ws, BdWs L, i
   const int I0 = blockIdx.x * RU_T, J0 = blockIdx.y * RU_T;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wr = warp & 3, wc = warp >> 2;
+#pragma unroll
+  for (int q = 0; q < RU_T * BB / 256; ++q) {
+    const int p = tid + 256 * q, r = p & (RU_T - 1), k = p >> 6;
+    const size_t col = (size_t)k * ld;
+    const bool oku = I0 + r < m, okw = J0 + r < n;
+    cp_async16_zfill(Us + r * RU_LD + k, U + (oku ? I0 + r + col : 0), oku);
+    cp_async16_zfill(Ws + r * RU_LD + k, W + (okw ? J0 + r + col : 0), okw);
+  }
+  cp_async_commit();
   CTile acc[2][4];
 #pragma unroll
   for (int rt = 0; rt < 2; ++rt)
@@ -219,28 +278,20 @@ __global__ void __launch_bounds__(256) rank_update_kernel(double2* ws, BdWs L, i
       acc[rt][ct].re1 = z1.x;
       acc[rt][ct].im1 = z1.y;
     }
-  for (int kk = 0; kk < BB; kk += RU_K) {
-    __syncthreads();
-    for (int p = tid; p < RU_T * RU_K; p += 256) {
-      const int r = p & (RU_T - 1), k = p / RU_T;
-      const size_t col = (size_t)(kk + k) * ld;
-      Us[r][k] = I0 + r < m ? U[I0 + r + col] : make_double2(0.0, 0.0);
-      Ws[r][k] = J0 + r < n ? W[J0 + r + col] : make_double2(0.0, 0.0);
-    }
-    __syncthreads();
+  cp_async_wait<0>();
+  __syncthreads();
 #pragma unroll
-    for (int k4 = 0; k4 < RU_K / 4; ++k4) {
-      const int kc = 4 * k4 + (lane & 3);
-      double2 au[2], bw[4];
+  for (int k4 = 0; k4 < BB / 4; ++k4) {
+    const int kc = 4 * k4 + (lane & 3);
+    double2 au[2], bw[4];
 #pragma unroll
-      for (int rt = 0; rt < 2; ++rt) au[rt] = Us[16 * wr + 8 * rt + (lane >> 2)][kc];
+    for (int rt = 0; rt < 2; ++rt) au[rt] = Us[(16 * wr + 8 * rt + (lane >> 2)) * RU_LD + kc];
 #pragma unroll
-      for (int ct = 0; ct < 4; ++ct) bw[ct] = conj2(Ws[32 * wc + 8 * ct + (lane >> 2)][kc]);
+    for (int ct = 0; ct < 4; ++ct) bw[ct] = conj2(Ws[(32 * wc + 8 * ct + (lane >> 2)) * RU_LD + kc]);
 #pragma unroll
-      for (int rt = 0; rt < 2; ++rt)
+    for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
-        for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(-au[rt].x, -au[rt].y, bw[ct].x, bw[ct].y);
-    }
+      for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(-au[rt].x, -au[rt].y, bw[ct].x, bw[ct].y);
   }
 #pragma unroll
   for (int rt = 0; rt < 2; ++rt)
@@ -269,11 +320,11 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     }
     count_launch();
     if (n2 <= 0) break;
-    xv_kernel<1><<<dim3((unsigned)((n2 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, 0, st>>>(ws, L, k0, k0 + BB, n2, m1,
+    xv_kernel<1><<<dim3((unsigned)((n2 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM, st>>>(ws, L, k0, k0 + BB, n2, m1,
                                                                                            L.v1_off, L.x_off);
     xt_kernel<<<dim3((unsigned)((n2 + 31) / 32), (unsigned)cnt), 256, 0, st>>>(ws, L, n2, L.x_off, L.t1_off);
     rank_update_kernel<<<dim3((unsigned)((m1 + RU_T - 1) / RU_T), (unsigned)((n2 + RU_T - 1) / RU_T), (unsigned)cnt),
-                         256, 0, st>>>(ws, L, k0, k0 + BB, m1, n2, L.v1_off, L.x_off);
+                         256, RU_SMEM, st>>>(ws, L, k0, k0 + BB, m1, n2, L.v1_off, L.x_off);
     count_launch(3);
     // ---- right: row panel LQ, C_tr2 = C[k0+BB:, k0+BB:] <- C_tr2 Q2
     PanelArgs p2{L.stride, L.c_off, S, k0, k0 + BB, n2, 1, L.v2_off, S, L.t2_off};
@@ -284,12 +335,12 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     count_launch();
     const int m3 = S - k0 - BB;
     if (m3 > 0) {
-      xv_kernel<0><<<dim3((unsigned)((m3 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, 0, st>>>(
+      xv_kernel<0><<<dim3((unsigned)((m3 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM, st>>>(
           ws, L, k0 + BB, k0 + BB, m3, n2, L.v2_off, L.x_off);
       xt_kernel<<<dim3((unsigned)((m3 + 31) / 32), (unsigned)cnt), 256, 0, st>>>(ws, L, m3, L.x_off, L.t2_off);
       rank_update_kernel<<<dim3((unsigned)((m3 + RU_T - 1) / RU_T), (unsigned)((n2 + RU_T - 1) / RU_T),
                                 (unsigned)cnt),
-                           256, 0, st>>>(ws, L, k0 + BB, k0 + BB, m3, n2, L.x_off, L.v2_off);
+                           256, RU_SMEM, st>>>(ws, L, k0 + BB, k0 + BB, m3, n2, L.x_off, L.v2_off);
       count_launch(3);
     }
     BD_CUDA(cudaGetLastError());
@@ -312,6 +363,9 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
 }
 
 void bd_init_attributes() {
+  cudaFuncSetAttribute(xv_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XV_SMEM);
+  cudaFuncSetAttribute(xv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XV_SMEM);
+  cudaFuncSetAttribute(rank_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RU_SMEM);
   cudaFuncSetAttribute(bd_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
   cudaFuncSetAttribute(bd_chase_kernel<1, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)bd_chase_smem<1, BB>());
