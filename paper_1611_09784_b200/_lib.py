@@ -155,6 +155,13 @@ class Device:
         return cls._ctxs[device]
 
     @classmethod
+    def new_ctx(cls, device: int = 0):
+        """An additional, independent context (own buffers) for concurrent work on other streams."""
+        h = C.c_void_p()
+        check(load().hx_ctx_create(device, C.byref(h)), "hx_ctx_create")
+        return h
+
+    @classmethod
     def count(cls) -> int:
         n = C.c_int32(0)
         load().hx_device_count(C.byref(n))

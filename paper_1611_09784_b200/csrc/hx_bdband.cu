@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "hx_band.cuh"
@@ -345,18 +346,26 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     }
     BD_CUDA(cudaGetLastError());
   }
-  // ---- stage 2
+  // ---- stage 2: enough sweeps in flight to fill the SMs.  Large batches (throughput-bound) use the
+  // single-tile variant (12 warps per SM); small ones the dual-tile one (lower latency per task).
+  static const int chase_mode = [] {
+    const char* e = getenv("HX_CHASE_MODE");
+    return e ? atoi(e) : 0;
+  }();
   const int64_t want = (148 * 11 + cnt - 1) / cnt;
+  const size_t a1 = L.stride, a2 = L.c_off, a3 = L.tgk_off;
+#define BD_CHASE(NW, DUAL) \
+  bd_chase_kernel<NW, BB, DUAL><<<(unsigned)cnt, NW * 32, bd_chase_smem<NW, BB, DUAL>(), st>>>(ws, a1, a2, a3, S, dims)
   if (want >= 6) {
-    bd_chase_kernel<6, BB><<<(unsigned)cnt, 6 * 32, bd_chase_smem<6, BB>(), st>>>(ws, L.stride, L.c_off, L.tgk_off, S,
-                                                                                  dims);
+    if (chase_mode == 1) BD_CHASE(11, false);
+    else BD_CHASE(6, true);
   } else if (want >= 2) {
-    bd_chase_kernel<2, BB><<<(unsigned)cnt, 2 * 32, bd_chase_smem<2, BB>(), st>>>(ws, L.stride, L.c_off, L.tgk_off, S,
-                                                                                  dims);
+    if (chase_mode == 2) BD_CHASE(2, true);
+    else BD_CHASE(2, false);
   } else {
-    bd_chase_kernel<1, BB><<<(unsigned)cnt, 32, bd_chase_smem<1, BB>(), st>>>(ws, L.stride, L.c_off, L.tgk_off, S,
-                                                                              dims);
+    BD_CHASE(1, false);
   }
+#undef BD_CHASE
   count_launch();
   BD_CUDA(cudaGetLastError());
   return 0;
@@ -367,12 +376,15 @@ void bd_init_attributes() {
   cudaFuncSetAttribute(xv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XV_SMEM);
   cudaFuncSetAttribute(rank_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RU_SMEM);
   cudaFuncSetAttribute(bd_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
-  cudaFuncSetAttribute(bd_chase_kernel<1, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)bd_chase_smem<1, BB>());
-  cudaFuncSetAttribute(bd_chase_kernel<2, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)bd_chase_smem<2, BB>());
-  cudaFuncSetAttribute(bd_chase_kernel<6, BB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)bd_chase_smem<6, BB>());
+#define BD_CHASE_ATTR(NW, DUAL)                                                                        \
+  cudaFuncSetAttribute(bd_chase_kernel<NW, BB, DUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                       (int)bd_chase_smem<NW, BB, DUAL>())
+  BD_CHASE_ATTR(1, false);
+  BD_CHASE_ATTR(2, false);
+  BD_CHASE_ATTR(2, true);
+  BD_CHASE_ATTR(6, true);
+  BD_CHASE_ATTR(11, false);
+#undef BD_CHASE_ATTR
 }
 
 int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, int64_t nmasks, const GridDev& g,

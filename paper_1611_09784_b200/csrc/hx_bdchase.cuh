@@ -22,10 +22,12 @@
 
 namespace hx {
 
-template <int BWc>
+// DUAL: X and Y tiles staged together (lowest latency per task); otherwise one tile buffer, Y loaded
+// after the X update (half the shared memory per warp -> twice the warps per SM).
+template <int BWc, bool DUAL>
 struct BdChaseSmem {
   double2 X[BWc][BWc + 1];  // tiles, zero-padded to BWc x BWc
-  double2 Y[BWc][BWc + 1];
+  double2 Y[DUAL ? BWc : 1][BWc + 1];
   double2 ug[BWc];  // current right reflector vector (ug[0] = 1, zero-padded)
   double2 vh[BWc];  // left reflector vector (vh[0] = 1, zero-padded)
   double2 cb[BWc];  // per-column update coefficients
@@ -42,14 +44,15 @@ __device__ __forceinline__ double2 cmul_cj(double2 a, double2 b) {  // conj(a) *
 }
 __device__ __forceinline__ double2 warp_csum(double2 v) { return make_double2(warp_sum(v.x), warp_sum(v.y)); }
 
-template <int NW, int BWc>
+template <int NW, int BWc, bool DUAL>
 __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_t stride, size_t c_off,
                                                                size_t tgk_off, int S, const int* dims) {
   extern __shared__ __align__(16) unsigned char bd_smem[];
-  BdChaseSmem<BWc>* all = reinterpret_cast<BdChaseSmem<BWc>*>(bd_smem);
+  BdChaseSmem<BWc, DUAL>* all = reinterpret_cast<BdChaseSmem<BWc, DUAL>*>(bd_smem);
   volatile int* prog = reinterpret_cast<volatile int*>(all + NW);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  BdChaseSmem<BWc>& W = all[warp];
+  BdChaseSmem<BWc, DUAL>& W = all[warp];
+  auto Yt = [&]() -> double2(*)[BWc + 1] { return DUAL ? W.Y : W.X; };
   double2* base = ws + (size_t)blockIdx.x * stride;
   double2* C = base + c_off;
   double* diag = reinterpret_cast<double*>(base + tgk_off);
@@ -93,10 +96,12 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
           if (lane < len && cc < len) bd_cp_async16(&W.X[lane][cc], src);
           else W.X[lane][cc] = zero;
         }
+        if (DUAL) {
 #pragma unroll 4
-        for (int cc = 0; cc < BWc; ++cc, src += ld) {
-          if (lane < len && cc < lb) bd_cp_async16(&W.Y[lane][cc], src);
-          else W.Y[lane][cc] = zero;
+          for (int cc = 0; cc < BWc; ++cc, src += ld) {
+            if (lane < len && cc < lb) bd_cp_async16(&W.Y[lane][cc], src);
+            else W.Y[lane][cc] = zero;
+          }
         }
       }
       if (t == 0) {
@@ -173,13 +178,25 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
       }
       double next_tau = 0.0;
       if (lb > 0) {
+        if (!DUAL) {  // Y into the (now free) tile buffer
+          __syncwarp();
+          const double2* src = blk + (size_t)len * ld;
+#pragma unroll 4
+          for (int cc = 0; cc < BWc; ++cc, src += ld) {
+            if (lane < len && cc < lb) bd_cp_async16(&W.X[lane][cc], src);
+            else W.X[lane][cc] = zero;
+          }
+          bd_cp_async_wait_all();
+          __syncwarp();
+        }
+        double2(*Y)[BWc + 1] = Yt();
         // ---- Y column pass: q = v^H Y, row 0 of H Y -> next right reflector G'
         double2 q;
         {
           double2 a0 = zero, a1 = zero;
 #pragma unroll 4
           for (int r = 0; r < BWc; r += 2) {
-            const double2 v0 = W.vh[r], y0c = W.Y[r][lane], v1 = W.vh[r + 1], y1c = W.Y[r + 1][lane];
+            const double2 v0 = W.vh[r], y0c = Y[r][lane], v1 = W.vh[r + 1], y1c = Y[r + 1][lane];
             a0.x = fma(v0.x, y0c.x, fma(v0.y, y0c.y, a0.x));
             a0.y = fma(v0.x, y0c.y, fma(-v0.y, y0c.x, a0.y));
             a1.x = fma(v1.x, y1c.x, fma(v1.y, y1c.y, a1.x));
@@ -187,7 +204,7 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
           }
           q = make_double2(a0.x + a1.x, a0.y + a1.y);
         }
-        const double2 y0 = W.Y[0][lane];
+        const double2 y0 = Y[0][lane];
         const double2 xg = make_double2(y0.x - tauh * q.x, -(y0.y - tauh * q.y));  // conj(row 0 of H Y)
         const double sg2 = warp_sum(xg.x * xg.x + xg.y * xg.y);
         const double2 al = make_double2(__shfl_sync(0xffffffffu, xg.x, 0), __shfl_sync(0xffffffffu, xg.y, 0));
@@ -204,7 +221,7 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
           double2 a0 = zero, a1 = zero;
 #pragma unroll 4
           for (int c = 0; c < BWc; c += 2) {
-            const double2 y0c = W.Y[lane][c], u0 = W.ug[c], y1c = W.Y[lane][c + 1], u1 = W.ug[c + 1];
+            const double2 y0c = Y[lane][c], u0 = W.ug[c], y1c = Y[lane][c + 1], u1 = W.ug[c + 1];
             a0.x = fma(y0c.x, u0.x, fma(-y0c.y, u0.y, a0.x));
             a0.y = fma(y0c.x, u0.y, fma(y0c.y, u0.x, a0.y));
             a1.x = fma(y1c.x, u1.x, fma(-y1c.y, u1.y, a1.x));
@@ -217,7 +234,7 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
 #pragma unroll 4
           for (int c = 0; c < BWc; ++c, dst += ld) {
             const double2 u = W.ug[c], d = W.cb[c];
-            double2 z = W.Y[lane][c];
+            double2 z = Y[lane][c];
             z.x -= (v.x * d.x - v.y * d.y) + (f.x * u.x + f.y * u.y);
             z.y -= (v.x * d.y + v.y * d.x) + (f.y * u.x - f.x * u.y);
             if (row0) z = c == 0 ? make_double2(hg.beta.x, -hg.beta.y) : zero;  // (conj beta', 0, ...)
@@ -233,9 +250,9 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
   }
 }
 
-template <int NW, int BWc>
+template <int NW, int BWc, bool DUAL>
 constexpr size_t bd_chase_smem() {
-  return NW * sizeof(BdChaseSmem<BWc>) + 64;
+  return NW * sizeof(BdChaseSmem<BWc, DUAL>) + 64;
 }
 
 }  // namespace hx

@@ -53,6 +53,16 @@ class DeviceMlmc:
         # per-call accounting for the roofline: list of (n, nmats, flops, event pair)
         self.records = []
         self.record = False
+        self._lanes = []  # (ctx, stream) pairs for run_levels
+
+    def _lane(self, i):
+        # lane 0 carries the largest tier (the critical path of a level set) on a high-priority stream, so
+        # its latency-bound kernels (e.g. the bulge chase on a few large matrices) are not starved of SMs
+        # by the throughput-bound tiers running beside it
+        while len(self._lanes) <= i:
+            prio = -1 if not self._lanes else 0
+            self._lanes.append((_lib.Device.new_ctx(self.device), torch.cuda.Stream(self.dev, priority=prio)))
+        return self._lanes[i]
 
     def cell(self, n):
         if n not in self._cells:
@@ -101,6 +111,12 @@ class DeviceMlmc:
     def _eval(self, n, words: torch.Tensor):
         """Dedup rows, solve unique masks, return per-row curves [rows, npts] (device)."""
         uniq, inv = torch.unique(words, dim=0, return_inverse=True)
+        return self._solve(n, uniq.contiguous(), self.ctx, self.stream)[0][inv]
+
+    def _solve(self, n, uniq: torch.Tensor, ctx, stream):
+        """Curves [U, npts] of the unique masks `uniq`, enqueued on `stream` with context `ctx`.  The
+        outputs (curves, status) are allocated on the caller's current stream, which must wait on `stream`
+        before using or releasing them."""
         cell = self.cell(n)
         q = self.q_of(n)
         kp = self.kpoints(n, q)
@@ -109,20 +125,19 @@ class DeviceMlmc:
         status = torch.empty((U, kp.shape[0]), dtype=torch.int32, device=self.dev)
         g = _lib.EGrid()
         g.e0, g.step, g.npts, g.delta = self.lo, self.step, self.npts, self.delta
-        uniq = uniq.contiguous()
         ev = None
         if self.record:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-            ev[0].record(self.stream)
-        _lib.check(self.lib.hx_eval_idos_batch_device(self.ctx, cell.handle, _lib.ptr(kp), kp.shape[0],
+            ev[0].record(stream)
+        _lib.check(self.lib.hx_eval_idos_batch_device(ctx, cell.handle, _lib.ptr(kp), kp.shape[0],
                                                       uniq.data_ptr(), U, C.byref(g), curves.data_ptr(), 0,
-                                                      status.data_ptr(), self.stream.cuda_stream),
+                                                      status.data_ptr(), stream.cuda_stream),
                    "hx_eval_idos_batch_device")
         if self.record:
-            ev[1].record(self.stream)
+            ev[1].record(stream)
             self.records.append({"n": n, "N": cell.dim, "unique": U, "nk": kp.shape[0], "events": ev,
                                  "uniq": uniq, "cell": cell})
-        return curves[inv]
+        return curves, status
 
     def run_level(self, inp: LevelInputs):
         """Returns device tensors (sum term [npts], sum term^2 [npts]) for this rank's shard."""
@@ -138,6 +153,61 @@ class DeviceMlmc:
                                                     inp.M, npts, 0, 0, 0, sums.data_ptr(), self.stream.cuda_stream),
                    "hx_level_moments_device")
         return sums
+
+
+    def run_levels(self, inputs):
+        """All levels at once: every (level, fine / coarse) solve on its own stream and context, so the
+        latency-bound tails of one tier (e.g. the nu = 32 bulge chase on 64 matrices) overlap with the
+        others.  Same results as run_level per input (each solve is deterministic); returns the list of
+        per-level sums on the current stream."""
+        main = self.stream
+        jobs = []  # (input index, n, uniq, inv)
+        for i, inp in enumerate(inputs):
+            if inp.M == 0:
+                continue
+            u, inv = torch.unique(inp.parent, dim=0, return_inverse=True)
+            jobs.append((i, inp.n, u.contiguous(), inv))
+            if inp.with_cv:
+                u, inv = torch.unique(inp.quarters, dim=0, return_inverse=True)
+                jobs.append((i, inp.n // 2, u.contiguous(), inv))
+        start = torch.cuda.Event()
+        start.record(main)
+        outs = [None] * len(jobs)
+        # largest tier first (lane 0 = high priority)
+        order = sorted(range(len(jobs)), key=lambda j: -self.cell(jobs[j][1]).dim)
+        for lane, j in enumerate(order):
+            i, n, uniq, inv = jobs[j]
+            ctx, stream = self._lane(lane)
+            stream.wait_event(start)
+            curves, status = self._solve(n, uniq, ctx, stream)
+            done = torch.cuda.Event()
+            done.record(stream)
+            outs[j] = (curves, done, status)
+        res = []
+        k = 0
+        for inp in inputs:
+            sums = torch.zeros(2 * self.npts, dtype=torch.float64, device=self.dev)
+            if inp.M == 0:
+                res.append(sums)
+                continue
+            curves, done, _ = outs[k]
+            main.wait_event(done)
+            full = curves[jobs[k][3]]
+            k += 1
+            quarters = None
+            if inp.with_cv:
+                curves, done, _ = outs[k]
+                main.wait_event(done)
+                quarters = curves[jobs[k][3]].reshape(inp.M, 4, self.npts)
+                k += 1
+            _lib.check(self.lib.hx_level_moments_device(full.data_ptr(),
+                                                        0 if quarters is None else quarters.data_ptr(), inp.M,
+                                                        self.npts, 0, 0, 0, sums.data_ptr(), main.cuda_stream),
+                       "hx_level_moments_device")
+            res.append(sums)
+        for _, done, _ in outs:  # every lane joins the main stream before its outputs can be released
+            main.wait_event(done)
+        return res
 
 
 def kept_dims(cell, uniq_words: torch.Tensor) -> np.ndarray:

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--levels", default="", help="comma list of level indices (1-based) to run; default all")
     ap.add_argument("--passes", type=int, default=1)
     ap.add_argument("--warm", type=int, default=0)
+    ap.add_argument("--concurrent", action="store_true", help="all levels at once (run_levels, as bench.py)")
     args = ap.parse_args()
     kind, levels, nq, p, erange, _ = bench.CONFIGS[args.config]
     lo, hi = bench.grid_range(kind, erange)
@@ -34,6 +35,16 @@ def main():
         for inp in inputs:
             run.run_level(inp)
     torch.cuda.synchronize()
+    if args.concurrent:
+        for _ in range(args.warm):
+            run.run_levels(inputs)
+        for _ in range(args.passes):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            run.run_levels(inputs)
+            torch.cuda.synchronize()
+            print(f"all levels concurrently: {1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
+        return
     for _ in range(args.passes):
         for inp in inputs:
             t0 = time.perf_counter()
