@@ -87,6 +87,10 @@ int hx_kernel_launches(uint64_t* out);
 const char* hx_last_error(void);
 int hx_device_count(int32_t* out);
 int hx_ctx_create(int32_t device, hx_ctx** out);
+/* Same with the context's work stream at CUDA stream priority `priority` (lower = higher priority;
+ * clamped to the device range).  Several contexts evaluate independent (n, q) groups concurrently:
+ * the host mirror puts the largest tier of a batch on a high-priority context. */
+int hx_ctx_create_priority(int32_t device, int32_t priority, hx_ctx** out);
 int hx_ctx_destroy(hx_ctx* ctx);
 int hx_ctx_synchronize(hx_ctx* ctx);
 

@@ -22,7 +22,8 @@ HX_ST_OK, HX_ST_NOT_PD, HX_ST_NONFINITE, HX_ST_EMPTY = 0, 1, 2, 3
 
 # every symbol declared in include/hx.h (checked by tests/test_boundary.py)
 EXPORTED = (
-    "hx_abi_version", "hx_last_error", "hx_device_count", "hx_ctx_create", "hx_ctx_destroy",
+    "hx_abi_version", "hx_last_error", "hx_device_count", "hx_ctx_create", "hx_ctx_create_priority",
+    "hx_ctx_destroy",
     "hx_ctx_synchronize", "hx_cell_create", "hx_cell_destroy", "hx_eval_idos_batch",
     "hx_eval_idos_batch_device", "hx_eigvalsh_batch_device", "hx_smoothed_counts_device",
     "hx_sharp_counts_device", "hx_level_moments_device", "hx_sample_masks", "hx_sample_masks_device",
@@ -70,6 +71,7 @@ def load():
             "hx_last_error": (C.c_char_p, []),
             "hx_device_count": (C.c_int, [C.POINTER(i32)]),
             "hx_ctx_create": (C.c_int, [i32, C.POINTER(vp)]),
+            "hx_ctx_create_priority": (C.c_int, [i32, i32, C.POINTER(vp)]),
             "hx_ctx_destroy": (C.c_int, [vp]),
             "hx_ctx_synchronize": (C.c_int, [vp]),
             "hx_cell_create": (C.c_int, [vp, C.POINTER(CellDesc), C.POINTER(vp)]),
@@ -154,12 +156,23 @@ class Device:
             cls._ctxs[device] = h
         return cls._ctxs[device]
 
+    _pools: dict = {}
+
     @classmethod
-    def new_ctx(cls, device: int = 0):
-        """An additional, independent context (own buffers) for concurrent work on other streams."""
+    def new_ctx(cls, device: int = 0, priority: int = 0):
+        """An additional, independent context (own buffers and work stream) for concurrent work."""
         h = C.c_void_p()
-        check(load().hx_ctx_create(device, C.byref(h)), "hx_ctx_create")
+        check(load().hx_ctx_create_priority(device, priority, C.byref(h)), "hx_ctx_create_priority")
         return h
+
+    @classmethod
+    def lane(cls, device: int, i: int):
+        """Context i of the per-device pool used to evaluate independent groups concurrently (lane 0 on a
+        high-priority stream)."""
+        pool = cls._pools.setdefault(device, [])
+        while len(pool) <= i:
+            pool.append(cls.new_ctx(device, -1 if not pool else 0))
+        return pool[i]
 
     @classmethod
     def count(cls) -> int:

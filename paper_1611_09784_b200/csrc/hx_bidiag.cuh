@@ -205,4 +205,106 @@ static __device__ void bidiag_tgk(double2* M, int lm, int rows, int cols, double
   __syncthreads();
 }
 
+// Leading dimension of the bidiagonalisation workspace: >= S + 1 and = 1 (mod 8) in 16-byte units, so
+// that lanes walking different columns at the same row hit distinct banks.
+__host__ __device__ constexpr int bidiag_ld(int S) { return (S + 7) / 8 * 8 + 1; }
+
+// Same reduction with ONE WARP per matrix (no CTA barriers, only __syncwarp): lanes own columns in the
+// left (column) pass and rows in the right (row) pass, two accumulators per lane for latency hiding.
+// Used for S <= 64 where a 256-thread CTA spends most of its time in per-step barriers and reductions.
+static __device__ void bidiag_tgk_warp(double2* M, int lm, int rows, int cols, double* diag, double* e2,
+                                       double2* u) {
+  const int lane = threadIdx.x & 31;
+  const int d = rows + cols;
+  for (int i = lane; i < d; i += 32) {
+    diag[i] = 0.0;
+    e2[i] = 0.0;
+  }
+  for (int j = 0; j < cols; ++j) {
+    // ---------------- left reflector: column j, rows j..rows-1
+    {
+      const double2* colj = M + (size_t)j * lm;
+      double part = 0.0;
+      for (int i = j + lane; i < rows; i += 32) part = fma(colj[i].x, colj[i].x, fma(colj[i].y, colj[i].y, part));
+      const double sig2 = warp_sum(part);
+      const QuickReflector h = quick_reflector(colj[j], sig2);
+      if (lane == 0) e2[2 * j] = sig2;
+      for (int i = j + lane; i < rows; i += 32) u[i] = i == j ? make_double2(1.0, 0.0) : cmul(colj[i], h.scale);
+      __syncwarp();
+      if (h.tau != 0.0)
+        for (int cc = j + 1 + lane; cc < cols; cc += 32) {
+          double2* col = M + (size_t)cc * lm;
+          double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+          int i = j;
+          for (; i + 1 < rows; i += 2) {
+            const double2 v0 = u[i], x0 = col[i], v1 = u[i + 1], x1 = col[i + 1];
+            a0.x = fma(v0.x, x0.x, fma(v0.y, x0.y, a0.x));
+            a0.y = fma(v0.x, x0.y, fma(-v0.y, x0.x, a0.y));
+            a1.x = fma(v1.x, x1.x, fma(v1.y, x1.y, a1.x));
+            a1.y = fma(v1.x, x1.y, fma(-v1.y, x1.x, a1.y));
+          }
+          if (i < rows) {
+            const double2 v0 = u[i], x0 = col[i];
+            a0.x = fma(v0.x, x0.x, fma(v0.y, x0.y, a0.x));
+            a0.y = fma(v0.x, x0.y, fma(-v0.y, x0.x, a0.y));
+          }
+          const double2 sc = make_double2(h.tau * (a0.x + a1.x), h.tau * (a0.y + a1.y));
+          for (i = j; i < rows; ++i) {
+            const double2 v = u[i];
+            double2 x = col[i];
+            x.x = fma(-v.x, sc.x, fma(v.y, sc.y, x.x));
+            x.y = fma(-v.x, sc.y, fma(-v.y, sc.x, x.y));
+            col[i] = x;
+          }
+        }
+      __syncwarp();
+    }
+    if (j + 1 >= cols) break;
+    // ---------------- right reflector: row j, columns j+1..cols-1 (on the conjugated row)
+    {
+      double part = 0.0;
+      for (int cc = j + 1 + lane; cc < cols; cc += 32) {
+        const double2 x = M[j + (size_t)cc * lm];
+        part = fma(x.x, x.x, fma(x.y, x.y, part));
+      }
+      const double sig2 = warp_sum(part);
+      const double2 a0 = M[j + (size_t)(j + 1) * lm];
+      const QuickReflector h = quick_reflector(make_double2(a0.x, -a0.y), sig2);
+      if (lane == 0) e2[2 * j + 1] = sig2;
+      for (int cc = j + 1 + lane; cc < cols; cc += 32) {
+        const double2 x = M[j + (size_t)cc * lm];
+        u[cc] = cc == j + 1 ? make_double2(1.0, 0.0) : cmul(make_double2(x.x, -x.y), h.scale);
+      }
+      __syncwarp();
+      if (h.tau != 0.0)
+        for (int r = j + 1 + lane; r < rows; r += 32) {
+          double2 a0r = make_double2(0.0, 0.0), a1r = a0r;
+          int cc = j + 1;
+          for (; cc + 1 < cols; cc += 2) {
+            const double2 x0 = M[r + (size_t)cc * lm], b0 = u[cc], x1 = M[r + (size_t)(cc + 1) * lm], b1 = u[cc + 1];
+            a0r.x = fma(x0.x, b0.x, fma(-x0.y, b0.y, a0r.x));
+            a0r.y = fma(x0.x, b0.y, fma(x0.y, b0.x, a0r.y));
+            a1r.x = fma(x1.x, b1.x, fma(-x1.y, b1.y, a1r.x));
+            a1r.y = fma(x1.x, b1.y, fma(x1.y, b1.x, a1r.y));
+          }
+          if (cc < cols) {
+            const double2 x0 = M[r + (size_t)cc * lm], b0 = u[cc];
+            a0r.x = fma(x0.x, b0.x, fma(-x0.y, b0.y, a0r.x));
+            a0r.y = fma(x0.x, b0.y, fma(x0.y, b0.x, a0r.y));
+          }
+          const double2 w = make_double2(h.tau * (a0r.x + a1r.x), h.tau * (a0r.y + a1r.y));
+          for (cc = j + 1; cc < cols; ++cc) {
+            const double2 b = u[cc];
+            double2 x = M[r + (size_t)cc * lm];
+            x.x = fma(-w.x, b.x, fma(-w.y, b.y, x.x));
+            x.y = fma(-w.y, b.x, fma(w.x, b.y, x.y));
+            M[r + (size_t)cc * lm] = x;
+          }
+        }
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+}
+
 }  // namespace hx

@@ -66,6 +66,9 @@ struct hx_ctx {
   cudaStream_t stream = nullptr;
   DevBuf kpts, diff, trans, ws, masks, curves, eigs, status, band, tri, refine;
   size_t ws_budget = (size_t)24 << 30;  // HBM workspace budget for the global / banded paths
+  int bd_min_n = HX_SMEM_MAX_N;          // bipartite cells with N above this take the banded SVD tier
+  int bidiag_warp_max_s = 32;            // shared-memory bidiagonalisation: one warp per matrix up to this S
+  int bidiag_threads = 256;              // ... and a CTA of this size above it
   bool use_bipartite = true;            // graphene: singular values of the A-B block (HX_NO_BIPARTITE=1 disables)
 };
 
@@ -143,7 +146,9 @@ int hx_device_count(int32_t* out) {
   return 0;
 }
 
-int hx_ctx_create(int32_t device, hx_ctx** out) {
+int hx_ctx_create(int32_t device, hx_ctx** out) { return hx_ctx_create_priority(device, 0, out); }
+
+int hx_ctx_create_priority(int32_t device, int32_t priority, hx_ctx** out) {
   if (!out) return fail(HX_E_ARG, "hx_ctx_create: null out");
   int n = 0;
   if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) return fail(HX_E_NODEV, "no CUDA device visible");
@@ -161,7 +166,10 @@ int hx_ctx_create(int32_t device, hx_ctx** out) {
     return fail(HX_E_NODEV, "libhx is built for sm_100a (B200); found sm_" + std::to_string(prop.major) +
                                 std::to_string(prop.minor));
   }
-  if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+  int lo_prio = 0, hi_prio = 0;
+  cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+  const int prio = std::max(hi_prio, std::min(lo_prio, (int)priority));
+  if (cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, prio) != cudaSuccess) {
     delete ctx;
     return fail(HX_E_CUDA, "cudaStreamCreate failed");
   }
@@ -170,6 +178,12 @@ int hx_ctx_create(int32_t device, hx_ctx** out) {
   {
     const char* nb = getenv("HX_NO_BIPARTITE");
     ctx->use_bipartite = !(nb && nb[0] && nb[0] != '0');
+    const char* bm = getenv("HX_BD_MIN_N");
+    if (bm && bm[0]) ctx->bd_min_n = atoi(bm);
+    const char* bw = getenv("HX_BIDIAG_WARP_MAX_S");
+    if (bw && bw[0]) ctx->bidiag_warp_max_s = atoi(bw);
+    const char* bt = getenv("HX_BIDIAG_THREADS");
+    if (bt && bt[0]) ctx->bidiag_threads = atoi(bt);
   }
   cudaFuncSetAttribute(hx::small_bidiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   ctx->ws_budget = std::min(ctx->ws_budget, freeb / 3);
@@ -329,7 +343,8 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
     refine = reinterpret_cast<hx::RefineItem*>(static_cast<unsigned char*>(ctx->refine.p) + 256);
     return 0;
   };
-  if (c.pencil != HX_PENCIL_GENERAL && N <= HX_SMEM_MAX_N) {
+  const bool use_bd = c.bipartite && ctx->use_bipartite && hx::bd_path_supported(c) && N > ctx->bd_min_n;
+  if (c.pencil != HX_PENCIL_GENERAL && N <= HX_SMEM_MAX_N && !use_bd) {
     // shared-memory tier: tridiagonalise every (mask, k) matrix, then one thread per eigenvalue
     const size_t smem = hx::small_tridiag_smem(N);
     int64_t chunk = std::min<int64_t>(nmat, std::max<int64_t>(1, (int64_t)((size_t)1 << 30) / (16 * N + 4)));
@@ -345,7 +360,10 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
       const uint64_t* mk0 = d_masks + (m0 / nk) * c.words;
       const bool tgk = c.bipartite && ctx->use_bipartite && hx::small_bidiag_smem(N, c.nsub) <= 200 * 1024;
       if (tgk) {
-        hx::small_bidiag_kernel<<<(unsigned)cnt, N > 64 ? 256 : 128, hx::small_bidiag_smem(N, c.nsub), st>>>(
+        // one warp per matrix up to S = 32 (latency of the serial reflector chain is hidden by many
+        // matrices per SM), a CTA beyond
+        hx::small_bidiag_kernel<<<(unsigned)cnt, c.nsub <= ctx->bidiag_warp_max_s ? 32 : ctx->bidiag_threads,
+                                  hx::small_bidiag_smem(N, c.nsub), st>>>(
             c, kp, nk, mk0, tri, dims, status + m0);
       } else {
         hx::small_tridiag_kernel<<<(unsigned)cnt, N > 64 ? 512 : 256, smem, st>>>(c, kp, nk, mk0, tri, dims,
@@ -357,7 +375,7 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
                           refine_count, tgk);
       HX_CUDA(cudaGetLastError());
     }
-  } else if (c.bipartite && ctx->use_bipartite && hx::bd_path_supported(c) && N > HX_SMEM_MAX_N) {
+  } else if (use_bd) {
     if (make_refine(nmat * N)) return fail(HX_E_CUDA, "alloc refinement list");
     int rc = hx::bd_eval(c, kp, nk, d_masks, nmasks, g, diff, trans, d_eigs, status, sharp, ctx->ws_budget,
                          [&](size_t bytes) -> void* { return ctx->band.grow(bytes) ? nullptr : ctx->band.p; }, st,

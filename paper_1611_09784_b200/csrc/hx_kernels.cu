@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(256) small_bidiag_kernel(CellDev c, const doub
                                                            int* status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int N = c.N, S = c.nsub;
-  const int lm = S + 1;
+  const int lm = bidiag_ld(S);
   const int64_t mat = blockIdx.x;
   const int64_t mk = mat / nk;
   const int kk = (int)(mat - mk * nk);
@@ -78,11 +78,12 @@ __global__ void __launch_bounds__(256) small_bidiag_kernel(CellDev c, const doub
   const bool transpose = nn.x < nn.y;
   const int rows = transpose ? nn.y : nn.x, cols = transpose ? nn.x : nn.y;
   assemble_bipartite(c, idx_a, idx_b, kpts[kk], M, lm, rows, cols, transpose);
-  bidiag_tgk(M, lm, rows, cols, diag, e2, u, s, red);
+  if (blockDim.x == 32) bidiag_tgk_warp(M, lm, rows, cols, diag, e2, u);
+  else bidiag_tgk(M, lm, rows, cols, diag, e2, u, s, red);
 }
 
 size_t small_bidiag_smem(int N, int S) {
-  return ((size_t)(S + 1) * S + 2 * (S + 1)) * 16 + 128 * 8 + (size_t)N * 8 + 2 * ((N + 31) / 32) * 4 + 16;
+  return ((size_t)bidiag_ld(S) * S + 2 * (S + 1)) * 16 + 128 * 8 + (size_t)N * 8 + 2 * ((N + 31) / 32) * 4 + 16;
 }
 
 size_t small_tridiag_smem(int N) {

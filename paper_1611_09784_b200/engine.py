@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import math
 import time
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -124,13 +125,13 @@ class Engine:
         return float(bands.energies.min()), float(bands.energies.max())
 
     # -- the batch seam --
-    def _solve_group(self, n: int, q: int, keys, task_ids):
+    def _solve_group(self, n: int, q: int, keys, task_ids, ctx=None):
         cell = self.cell(n)
         words = words_from_keys(keys, cell.supercell.nunits)
         kp = self.kpoints(n, q)
         t0 = time.perf_counter()
         curves, _, status = eval_batch(cell, kp, words, self.grid.lo, self.grid.step, self.grid.npoints,
-                                       self.delta)
+                                       self.delta, ctx=ctx)
         secs = time.perf_counter() - t0
         self.io_bytes[0] += words.nbytes + kp.nbytes
         self.io_bytes[1] += curves.nbytes + status.nbytes
@@ -144,6 +145,22 @@ class Engine:
                     failures.append((task_ids[i], exc))
             raise TaskError(failures)
         return curves, secs / max(1, len(keys))
+
+    def _solve_groups(self, groups, new_jobs):
+        """Solve every (n, q) group; several groups run concurrently, each from its own thread on its own
+        hx context (the largest tier on the high-priority one), as the reference's parallel_map runs its
+        jobs side by side (runner.py:75-93)."""
+        for n, _ in groups:
+            self.cell(n)  # compile cells up front (not thread-safe)
+        args = {g: ([new_jobs[i][2] for i in idxs], [new_jobs[i][3] for i in idxs]) for g, idxs in groups.items()}
+        if len(groups) == 1:
+            g = next(iter(groups))
+            return {g: self._solve_group(g[0], g[1], *args[g])}
+        order = sorted(groups, key=lambda g: -self.cell(g[0]).dim)
+        with ThreadPoolExecutor(max_workers=len(order)) as ex:
+            futs = {g: ex.submit(self._solve_group, g[0], g[1], *args[g], _lib.Device.lane(self.device, lane))
+                    for lane, g in enumerate(order)}
+            return {g: f.result() for g, f in futs.items()}
 
     def evaluate_masks(self, requests):
         """Dedup on (n, q, mask) against the run cache and within the batch; solve the new jobs of each
@@ -170,8 +187,9 @@ class Engine:
         for idx, (n, q, mask, tid) in enumerate(new_jobs):
             groups.setdefault((n, q), []).append(idx)
         spent = 0.0
+        solved = self._solve_groups(groups, new_jobs)
         for (n, q), idxs in groups.items():
-            curves, per_job = self._solve_group(n, q, [new_jobs[i][2] for i in idxs], [new_jobs[i][3] for i in idxs])
+            curves, per_job = solved[(n, q)]
             for row, i in enumerate(idxs):
                 results[i] = (curves[row], per_job)
             spent += per_job * len(idxs)

@@ -90,10 +90,13 @@ def raise_status(status: np.ndarray, kpoints: np.ndarray, what: str = "eigensolv
 
 
 def eval_batch(cell: CompiledCell, kpoints: np.ndarray, words: np.ndarray, lo: float, step: float, npts: int,
-               delta: float, want_eigs: bool = False, sharp: bool = False):
-    """Host-buffer call of hx_eval_idos_batch for one (n, q) group: curves [M, npts] (+ eigs, status)."""
+               delta: float, want_eigs: bool = False, sharp: bool = False, ctx=None):
+    """Host-buffer call of hx_eval_idos_batch for one (n, q) group: curves [M, npts] (+ eigs, status).
+    ctx: the hx context to use (default: the device's primary context); the call blocks until done and
+    releases the GIL, so groups on different contexts run concurrently from different threads."""
     lib = _lib.load()
-    ctx = _lib.Device.ctx(cell.device)
+    if ctx is None:
+        ctx = _lib.Device.ctx(cell.device)
     words = np.ascontiguousarray(words, dtype=np.uint64)
     M = words.shape[0]
     kp = np.ascontiguousarray(kpoints, dtype=np.float64).reshape(-1, 2)
