@@ -5,9 +5,9 @@
 // zero under every reflector) and reduced in two stages:
 //   stage 1 (dense -> upper band, width BW), per step k0:
 //     column panel QR  C[k0:, k0:k0+BW] = Q1 R          (cluster/DSMEM panel kernel, mode 0)
-//     X1 = C_tr^H V1 ; X1 <- X1 T1 ; C_tr -= V1 X1^H      (left update Q1^H C_tr, DMMA)
+//     X1 = (C_tr^H V1) T1 ; C_tr -= V1 X1^H              (left update Q1^H C_tr, DMMA; T in the epilogue)
 //     row panel LQ     C[k0:k0+BW, k0+BW:] = R^H Q2^H  (QR of the conj-transposed block, mode 1)
-//     Z = C_tr2 V2 ; Z <- Z T2 ; C_tr2 -= Z V2^H          (right update C_tr2 Q2, DMMA)
+//     Z = (C_tr2 V2) T2 ; C_tr2 -= Z V2^H                 (right update C_tr2 Q2, DMMA)
 //   stage 2 (upper band -> bidiagonal) by bulge chasing (bd_chase_kernel below, one warp per sweep).
 // The Golub-Kahan tridiagonal (zero diagonal, off-diagonals alpha_0, gamma_0, alpha_1, ...) truncated to
 // d = nA + nB entries has exactly the eigenvalues of T; it goes through the shared bisection + IDOS kernel.
@@ -107,10 +107,11 @@ constexpr int XV_TM = 64, XV_TK = 16, XV_ST = 3;
 constexpr int XV_LD0 = XV_TM + 2, XV_LD1 = XV_TK + 4, XV_LDV = XV_TK + 4;
 constexpr int XV_A_ELEMS = XV_TK * XV_LD0 > XV_TM * XV_LD1 ? XV_TK * XV_LD0 : XV_TM * XV_LD1;
 constexpr size_t XV_SMEM = (size_t)XV_ST * (XV_A_ELEMS + BB * XV_LDV) * sizeof(double2);
+static_assert((size_t)(XV_TM + BB) * (BB + 4) * sizeof(double2) <= XV_SMEM, "xv epilogue tile does not fit");
 
 template <int MODE>
 __global__ void __launch_bounds__(128) xv_kernel(double2* ws, BdWs L, int ar0, int ac0, int rows, int K,
-                                                 size_t v_off, size_t x_off) {
+                                                 size_t v_off, size_t x_off, size_t t_off) {
   extern __shared__ __align__(16) double2 xv_sm[];
   double2* As = xv_sm;                         // [XV_ST][XV_A_ELEMS]
   double2* Vs = xv_sm + XV_ST * XV_A_ELEMS;    // [XV_ST][BB][XV_LDV]
@@ -192,7 +193,39 @@ __global__ void __launch_bounds__(128) xv_kernel(double2* ws, BdWs L, int ar0, i
         for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(a[rt].x, a[rt].y, b[ct].x, b[ct].y);
     }
   }
+  // ---- epilogue: X <- (op(A) V) T with T (BB x BB, column-major) - the block reflector's T factor,
+  //      applied on the tile in shared memory (DMMA), saving a pass over X
   cp_async_wait<0>();
+  __syncthreads();
+  constexpr int XL = BB + 4;  // 4 (mod 8): conflict-free fragments
+  double2* Xs = xv_sm;        // [XV_TM][XL]   (reuses the pipeline stages)
+  double2* Ts = xv_sm + XV_TM * XL;  // [BB (n)][XL (k)] = T[k][n]
+  const double2* T = base + t_off;
+  for (int p = tid; p < BB * BB; p += 128) Ts[(p / BB) * XL + (p % BB)] = T[p];
+#pragma unroll
+  for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+    for (int ct = 0; ct < 4; ++ct) {
+      const int r = 16 * warp + 8 * rt + (lane >> 2);
+      const int cc = 8 * ct + 2 * (lane & 3);
+      Xs[r * XL + cc] = make_double2(acc[rt][ct].re0, acc[rt][ct].im0);
+      Xs[r * XL + cc + 1] = make_double2(acc[rt][ct].re1, acc[rt][ct].im1);
+      acc[rt][ct].zero();
+    }
+  __syncthreads();
+#pragma unroll
+  for (int k4 = 0; k4 < BB / 4; ++k4) {
+    const int kc = 4 * k4 + (lane & 3);
+    double2 a[2], b[4];
+#pragma unroll
+    for (int rt = 0; rt < 2; ++rt) a[rt] = Xs[(16 * warp + 8 * rt + (lane >> 2)) * XL + kc];
+#pragma unroll
+    for (int ct = 0; ct < 4; ++ct) b[ct] = Ts[(8 * ct + (lane >> 2)) * XL + kc];
+#pragma unroll
+    for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+      for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(a[rt].x, a[rt].y, b[ct].x, b[ct].y);
+  }
 #pragma unroll
   for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
@@ -204,36 +237,6 @@ __global__ void __launch_bounds__(128) xv_kernel(double2* ws, BdWs L, int ar0, i
         X[r + (size_t)(cc + 1) * ld] = make_double2(acc[rt][ct].re1, acc[rt][ct].im1);
       }
     }
-}
-
-// X <- X T (rows x BB, ld S), 32-row tiles.
-__global__ void __launch_bounds__(256) xt_kernel(double2* ws, BdWs L, int rows, size_t x_off, size_t t_off) {
-  __shared__ double2 Tsh[BB][BB];
-  __shared__ double2 Xt[32][BB + 1];
-  double2* base = ws + (size_t)blockIdx.y * L.stride;
-  double2* X = base + x_off;
-  const double2* T = base + t_off;
-  const int ld = L.S;
-  const int tid = threadIdx.x, oc = tid & 31, orow = tid >> 5;
-  const int r0 = blockIdx.x * 32;
-  for (int p = tid; p < BB * BB; p += 256) Tsh[p % BB][p / BB] = T[p];
-  for (int p = tid; p < 32 * BB; p += 256) {
-    const int rr = p & 31, cc = p >> 5;
-    Xt[rr][cc] = r0 + rr < rows ? X[r0 + rr + (size_t)cc * ld] : make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int rr = orow + 8 * q;
-    double2 t = make_double2(0.0, 0.0);
-#pragma unroll 8
-    for (int l = 0; l < BB; ++l) {
-      const double2 x = Xt[rr][l], tt = Tsh[l][oc];
-      t.x += x.x * tt.x - x.y * tt.y;
-      t.y += x.x * tt.y + x.y * tt.x;
-    }
-    if (r0 + rr < rows) X[r0 + rr + (size_t)oc * ld] = t;
-  }
 }
 
 // M[mr0:mr0+m, mc0:mc0+n] -= U W^H, U [m x BB] and W [n x BB] (ld S); 64 x 64 tiles, DMMA.  The whole
@@ -321,12 +324,11 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     }
     count_launch();
     if (n2 <= 0) break;
-    xv_kernel<1><<<dim3((unsigned)((n2 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM, st>>>(ws, L, k0, k0 + BB, n2, m1,
-                                                                                           L.v1_off, L.x_off);
-    xt_kernel<<<dim3((unsigned)((n2 + 31) / 32), (unsigned)cnt), 256, 0, st>>>(ws, L, n2, L.x_off, L.t1_off);
+    xv_kernel<1><<<dim3((unsigned)((n2 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM, st>>>(
+        ws, L, k0, k0 + BB, n2, m1, L.v1_off, L.x_off, L.t1_off);
     rank_update_kernel<<<dim3((unsigned)((m1 + RU_T - 1) / RU_T), (unsigned)((n2 + RU_T - 1) / RU_T), (unsigned)cnt),
                          256, RU_SMEM, st>>>(ws, L, k0, k0 + BB, m1, n2, L.v1_off, L.x_off);
-    count_launch(3);
+    count_launch(2);
     // ---- right: row panel LQ, C_tr2 = C[k0+BB:, k0+BB:] <- C_tr2 Q2
     PanelArgs p2{L.stride, L.c_off, S, k0, k0 + BB, n2, 1, L.v2_off, S, L.t2_off};
     if (!launch_cluster_panel(ws, p2, cnt, st)) {
@@ -337,12 +339,11 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     const int m3 = S - k0 - BB;
     if (m3 > 0) {
       xv_kernel<0><<<dim3((unsigned)((m3 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM, st>>>(
-          ws, L, k0 + BB, k0 + BB, m3, n2, L.v2_off, L.x_off);
-      xt_kernel<<<dim3((unsigned)((m3 + 31) / 32), (unsigned)cnt), 256, 0, st>>>(ws, L, m3, L.x_off, L.t2_off);
+          ws, L, k0 + BB, k0 + BB, m3, n2, L.v2_off, L.x_off, L.t2_off);
       rank_update_kernel<<<dim3((unsigned)((m3 + RU_T - 1) / RU_T), (unsigned)((n2 + RU_T - 1) / RU_T),
                                 (unsigned)cnt),
                            256, RU_SMEM, st>>>(ws, L, k0 + BB, k0 + BB, m3, n2, L.x_off, L.v2_off);
-      count_launch(3);
+      count_launch(2);
     }
     BD_CUDA(cudaGetLastError());
   }
@@ -354,16 +355,30 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
   }();
   const int64_t want = (148 * 11 + cnt - 1) / cnt;
   const size_t a1 = L.stride, a2 = L.c_off, a3 = L.tgk_off;
-#define BD_CHASE(NW, DUAL) \
-  bd_chase_kernel<NW, BB, DUAL><<<(unsigned)cnt, NW * 32, bd_chase_smem<NW, BB, DUAL>(), st>>>(ws, a1, a2, a3, S, dims)
+#define BD_CHASE(NW, DUAL, CL)                                                                          \
+  {                                                                                                     \
+    cudaLaunchConfig_t cfg = {};                                                                        \
+    cudaLaunchAttribute attr[1];                                                                        \
+    cfg.gridDim = dim3((unsigned)(cnt * CL));                                                           \
+    cfg.blockDim = dim3(NW * 32);                                                                       \
+    cfg.dynamicSmemBytes = bd_chase_smem<NW, BB, DUAL>();                                               \
+    cfg.stream = st;                                                                                    \
+    attr[0].id = cudaLaunchAttributeClusterDimension;                                                   \
+    attr[0].val.clusterDim.x = CL;                                                                      \
+    attr[0].val.clusterDim.y = 1;                                                                       \
+    attr[0].val.clusterDim.z = 1;                                                                       \
+    cfg.attrs = attr;                                                                                   \
+    cfg.numAttrs = 1;                                                                                   \
+    BD_CUDA(cudaLaunchKernelEx(&cfg, bd_chase_kernel<NW, BB, DUAL, CL>, ws, a1, a2, a3, S, dims)); \
+  }
   if (want >= 6) {
-    if (chase_mode == 1) BD_CHASE(11, false);
-    else BD_CHASE(6, true);
+    if (chase_mode == 1) BD_CHASE(11, false, 1)
+    else if (chase_mode == 2) BD_CHASE(6, true, 1)
+    else BD_CHASE(8, false, 2)
   } else if (want >= 2) {
-    if (chase_mode == 2) BD_CHASE(2, true);
-    else BD_CHASE(2, false);
+    BD_CHASE(2, false, 1)
   } else {
-    BD_CHASE(1, false);
+    BD_CHASE(1, false, 1)
   }
 #undef BD_CHASE
   count_launch();
@@ -376,14 +391,14 @@ void bd_init_attributes() {
   cudaFuncSetAttribute(xv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XV_SMEM);
   cudaFuncSetAttribute(rank_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RU_SMEM);
   cudaFuncSetAttribute(bd_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
-#define BD_CHASE_ATTR(NW, DUAL)                                                                        \
-  cudaFuncSetAttribute(bd_chase_kernel<NW, BB, DUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+#define BD_CHASE_ATTR(NW, DUAL, CL)                                                                        \
+  cudaFuncSetAttribute(bd_chase_kernel<NW, BB, DUAL, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                        (int)bd_chase_smem<NW, BB, DUAL>())
-  BD_CHASE_ATTR(1, false);
-  BD_CHASE_ATTR(2, false);
-  BD_CHASE_ATTR(2, true);
-  BD_CHASE_ATTR(6, true);
-  BD_CHASE_ATTR(11, false);
+  BD_CHASE_ATTR(1, false, 1);
+  BD_CHASE_ATTR(2, false, 1);
+  BD_CHASE_ATTR(6, true, 1);
+  BD_CHASE_ATTR(11, false, 1);
+  BD_CHASE_ATTR(8, false, 2);
 #undef BD_CHASE_ATTR
 }
 
@@ -419,6 +434,18 @@ int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, 
   }
   return 0;
 }
+
+#ifdef HX_CHASE_PROFILE
+extern "C" int hx_debug_chase_prof(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, hx_chase_prof, sizeof(unsigned long long) * 16);
+  if (reset) {
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(hx_chase_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 bool bd_path_supported(const CellDev& c) {
   return c.bipartite && c.nsub >= 48 && 2 * c.nsub == c.N && c.N <= HX_MAX_N;

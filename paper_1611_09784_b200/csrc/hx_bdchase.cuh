@@ -18,6 +18,8 @@
 // completed its tasks 0..t+1; one warp owns the sweeps i = w (mod NW) and waits on a per-warp progress
 // counter in shared memory (no CTA barriers).
 #pragma once
+#include <cooperative_groups.h>
+
 #include "hx_dense.cuh"
 
 namespace hx {
@@ -33,9 +35,13 @@ struct BdChaseSmem {
   double2 cb[BWc];  // per-column update coefficients
 };
 
+// L1-cached copies when every sweep of a matrix runs on one SM; L2 (.cg) when the sweeps of a matrix are
+// spread over a cluster (another SM's stores are not visible through this SM's L1).
+template <bool L2ONLY>
 __device__ __forceinline__ void bd_cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+  if (L2ONLY) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void bd_cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -44,7 +50,27 @@ __device__ __forceinline__ double2 cmul_cj(double2 a, double2 b) {  // conj(a) *
 }
 __device__ __forceinline__ double2 warp_csum(double2 v) { return make_double2(warp_sum(v.x), warp_sum(v.y)); }
 
-template <int NW, int BWc, bool DUAL>
+#ifdef HX_CHASE_PROFILE
+// Debug builds only: per-phase clock64() totals of the warps of block 0 (phase k in slot k).
+__device__ unsigned long long hx_chase_prof[16];
+#define HX_PROF_MARK(k)                                                      \
+  do {                                                                       \
+    if (blockIdx.x == 0 && lane == 0) {                                      \
+      const long long now_ = clock64();                                      \
+      atomicAdd(&hx_chase_prof[k], (unsigned long long)(now_ - prof_t0_));   \
+      prof_t0_ = now_;                                                       \
+    }                                                                        \
+  } while (0)
+#else
+#define HX_PROF_MARK(k) \
+  do {                  \
+  } while (0)
+#endif
+
+// CL > 1: the sweeps of one matrix are dealt round-robin to the warps of a CL-CTA cluster (CL x NW sweeps
+// in flight, CL SMs per matrix); progress counters are read across the cluster through DSMEM and the
+// tiles go through L2.
+template <int NW, int BWc, bool DUAL, int CL>
 __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_t stride, size_t c_off,
                                                                size_t tgk_off, int S, const int* dims) {
   extern __shared__ __align__(16) unsigned char bd_smem[];
@@ -53,53 +79,73 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   BdChaseSmem<BWc, DUAL>& W = all[warp];
   auto Yt = [&]() -> double2(*)[BWc + 1] { return DUAL ? W.Y : W.X; };
-  double2* base = ws + (size_t)blockIdx.x * stride;
+  constexpr bool L2ONLY = CL > 1;
+  const int rank = CL > 1 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
+  const int64_t mat = blockIdx.x / CL;
+  constexpr int TW = CL * NW;  // sweeps in flight per matrix
+  const int gw = rank * NW + warp;
+  double2* base = ws + (size_t)mat * stride;
   double2* C = base + c_off;
   double* diag = reinterpret_cast<double*>(base + tgk_off);
   double* e2 = diag + 2 * S;
   const int ld = S;
   const double2 zero = make_double2(0.0, 0.0);
-  for (int q = threadIdx.x; q < 2 * S; q += blockDim.x) {
-    diag[q] = 0.0;
-    e2[q] = 0.0;
+  if (rank == 0) {
+    for (int q = threadIdx.x; q < 2 * S; q += blockDim.x) {
+      diag[q] = 0.0;
+      e2[q] = 0.0;
+    }
   }
   if (lane == 0) prog[warp] = -1;
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if (CL > 1) cooperative_groups::this_cluster().sync();
+  else __syncthreads();
+  if (rank == 0 && threadIdx.x == 0) {
     const double2 a0 = C[0];
     e2[0] = a0.x * a0.x + a0.y * a0.y;  // alpha_0: final after stage 1
   }
-  if (dims && dims[blockIdx.x] == 0) return;
-  const int nsweeps = S - 1;
-  for (int i = warp; i < nsweeps; i += NW) {
+  const bool skip = dims && dims[mat] == 0;  // uniform over the cluster
+  const int nsweeps = skip ? 0 : S - 1;
+  for (int i = gw; i < nsweeps; i += TW) {
     const int tasks = (S - 1 - i + BWc - 1) / BWc;
     const int prev_tasks = i > 0 ? (S - i + BWc - 1) / BWc : 0;
-    const int pw = (i - 1 + NW) % NW;
+    volatile int* pflag;  // progress counter of the warp that owns sweep i - 1
+    {
+      const int gp = (i - 1 + TW) % TW;
+      if (CL > 1)
+        pflag = cooperative_groups::this_cluster().map_shared_rank(const_cast<int*>(prog), gp / NW) + gp % NW;
+      else pflag = prog + gp;
+    }
     double taug = 0.0;
+#ifdef HX_CHASE_PROFILE
+    long long prof_t0_ = clock64();
+#endif
     for (int t = 0; t < tasks; ++t) {
+      HX_PROF_MARK(0);
       if (i > 0) {
         const int need = (i - 1) * 65536 + min(t + 2, prev_tasks);
         if (lane == 0)
-          while (prog[pw] < need) __nanosleep(20);
+          while (*pflag < need) __nanosleep(20);
         __syncwarp();
-        __threadfence_block();
+        if (CL > 1) __threadfence();
+        else __threadfence_block();
       }
       const int s = i + 1 + t * BWc;
       const int len = min(BWc, S - s);
       const int lb = max(0, min(BWc, S - s - len));
+      HX_PROF_MARK(1);  // wait for the previous sweep
       // ---- X and Y tiles (asynchronous, zero-padded); blk = &C[s + lane][s], columns ld apart
       double2* const blk = C + ((size_t)s * ld + s + lane);
       {
         const double2* src = blk;
 #pragma unroll 4
         for (int cc = 0; cc < BWc; ++cc, src += ld) {
-          if (lane < len && cc < len) bd_cp_async16(&W.X[lane][cc], src);
+          if (lane < len && cc < len) bd_cp_async16<L2ONLY>(&W.X[lane][cc], src);
           else W.X[lane][cc] = zero;
         }
         if (DUAL) {
 #pragma unroll 4
           for (int cc = 0; cc < BWc; ++cc, src += ld) {
-            if (lane < len && cc < lb) bd_cp_async16(&W.Y[lane][cc], src);
+            if (lane < len && cc < lb) bd_cp_async16<L2ONLY>(&W.Y[lane][cc], src);
             else W.Y[lane][cc] = zero;
           }
         }
@@ -108,7 +154,8 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
         // right reflector from row i, columns [s, s+len): row i -> (conj beta, 0, ...) = (gamma_i, 0, ...)
         double2 x = zero;
         if (lane < len) {
-          const double2 z = C[(size_t)(s + lane) * ld + i];
+          const double2* zp = C + (size_t)(s + lane) * ld + i;
+          const double2 z = L2ONLY ? __ldcg(zp) : *zp;
           x = make_double2(z.x, -z.y);
         }
         const double sig2 = warp_sum(x.x * x.x + x.y * x.y);
@@ -147,6 +194,7 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
       W.vh[lane] = v;
       const double2 w = warp_csum(cmul_cj(v, ty));  // v^H (tau_g y)
       __syncwarp();
+      HX_PROF_MARK(4);  // X row pass + H
       // ---- X column pass: p = v^H X, b_c = tau_h (p_c - w conj(u_c))
       {
         double2 a0 = zero, a1 = zero;
@@ -163,6 +211,7 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
         W.cb[lane] = make_double2(tauh * (a0.x + a1.x - wu.x), tauh * (a0.y + a1.y - wu.y));
       }
       __syncwarp();
+      HX_PROF_MARK(5);  // X column pass
       // ---- X: fused rank-2 row update, straight to HBM: X' = X - ty conj(u) - v b
       if (lane < len) {
         double2* dst = blk;
@@ -176,6 +225,7 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
           if (c < len) *dst = z;
         }
       }
+      HX_PROF_MARK(6);  // X update + stores
       double next_tau = 0.0;
       if (lb > 0) {
         if (!DUAL) {  // Y into the (now free) tile buffer
@@ -183,12 +233,13 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
           const double2* src = blk + (size_t)len * ld;
 #pragma unroll 4
           for (int cc = 0; cc < BWc; ++cc, src += ld) {
-            if (lane < len && cc < lb) bd_cp_async16(&W.X[lane][cc], src);
+            if (lane < len && cc < lb) bd_cp_async16<L2ONLY>(&W.X[lane][cc], src);
             else W.X[lane][cc] = zero;
           }
           bd_cp_async_wait_all();
           __syncwarp();
         }
+        HX_PROF_MARK(7);  // Y tile (single-tile variant)
         double2(*Y)[BWc + 1] = Yt();
         // ---- Y column pass: q = v^H Y, row 0 of H Y -> next right reflector G'
         double2 q;
@@ -216,6 +267,7 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
         W.ug[lane] = u2;
         W.cb[lane] = make_double2(tauh * q.x, tauh * q.y);  // d_c
         __syncwarp();
+        HX_PROF_MARK(8);  // Y column pass + G'
         // ---- Y row pass: f = tau_g' (Y u' - tau_h v (q . u')), Y' = Y - v d - f conj(u'), to HBM
         if (lane < len) {
           double2 a0 = zero, a1 = zero;
@@ -242,12 +294,16 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
           }
         }
       }
+      HX_PROF_MARK(9);  // Y row pass + update + stores
       taug = next_tau;
-      __threadfence_block();
+      if (CL > 1) __threadfence();
+      else __threadfence_block();
       __syncwarp();
       if (lane == 0) prog[warp] = i * 65536 + t + 1;
+      HX_PROF_MARK(10);  // fence + publish
     }
   }
+  if (CL > 1) cooperative_groups::this_cluster().sync();  // remote pollers may still read our counters
 }
 
 template <int NW, int BWc, bool DUAL>

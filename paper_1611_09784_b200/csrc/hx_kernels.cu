@@ -294,8 +294,56 @@ __global__ void __launch_bounds__(128) eig_refine_kernel(CellDev c, int nk, Grid
                                                          const RefineItem* __restrict__ items,
                                                          const unsigned long long* __restrict__ count) {
   const unsigned long long n = *count;
+  const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+  // G lanes per item: G-point multisection (log2(G+1) bits per Sturm round).  Few items (large matrices)
+  // are latency-bound and get up to 8 lanes each; many items are throughput-bound and keep one thread.
+  int G = 1;
+  while (G < 8 && n * (unsigned long long)(2 * G) * 2 <= nthreads) G *= 2;
+  if (G > 1) {
+    const int lane = threadIdx.x & 31, sub = lane % G, base = lane - sub;
+    const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << base;
+    const unsigned long long ngroups = nthreads / G;
+    const double inv = 1.0 / (double)(G + 1);
+    // loop bound uniform over the warp: every lane runs the same number of rounds (shuffles/ballots)
+    const unsigned long long g0 = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+    const unsigned long long wfirst = ((unsigned long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31u)) / G;
+    for (unsigned long long qw = wfirst; qw < n; qw += ngroups) {
+      const unsigned long long q = qw + (g0 - wfirst);
+      const bool valid = q < n;
+      RefineItem it = items[valid ? q : qw];
+      const double* diag = tri + it.lm * tri_stride;
+      const double* e2 = diag + c.N;
+      const int d = dims[it.lm];
+      double lo = it.lo, hi = it.hi;
+      bool done = false;
+      for (int k = 0; k < 200; ++k) {
+        const double tol = 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + it.pivmin;
+        const double mid = 0.5 * (lo + hi);
+        done = done || hi - lo <= tol || mid <= lo || mid >= hi;
+        if (__all_sync(0xffffffffu, done)) break;
+        // points x_m = lo + (m + 1) (hi - lo) / (G + 1); the first with count > idx brackets lambda
+        const double x = fma((double)(sub + 1) * inv, hi - lo, lo);
+        bool above = true;
+        if (!done) above = (x > lo && x < hi) ? sturm_count_fast<TGK>(diag, e2, d, x, it.pivmin) > it.idx : x >= hi;
+        const unsigned b = (__ballot_sync(0xffffffffu, above) & gmask) >> base;
+        const int m = b ? __ffs(b) - 1 : G;  // lambda in (x_{m-1}, x_m]
+        const double nlo = __shfl_sync(0xffffffffu, x, base + (m == 0 ? 0 : m - 1));
+        const double nhi = __shfl_sync(0xffffffffu, x, base + (m == G ? G - 1 : m));
+        if (!done) {
+          lo = m == 0 ? lo : nlo;
+          hi = m == G ? hi : nhi;
+        }
+      }
+      if (valid && sub == 0) {
+        const double lam = 0.5 * (lo + hi);
+        if (it.flags & 1) add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, lam);
+        if (it.flags & 2) add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, -lam);
+      }
+    }
+    return;
+  }
   for (unsigned long long q = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
-       q += (unsigned long long)gridDim.x * blockDim.x) {
+       q += nthreads) {
     const RefineItem it = items[q];
     const double* diag = tri + it.lm * tri_stride;
     const double* e2 = diag + c.N;
@@ -332,7 +380,8 @@ void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, i
                                                    status, sharp, rf, refine_count);
   count_launch();
   if (two_pass) {
-    const int64_t rblocks = std::min<int64_t>((slots + 127) / 128, 148 * 16);
+    // at least 148 x 16 blocks: when few items are left (large matrices) each gets a whole warp
+    const int64_t rblocks = 148 * 16;
     if (tgk)
       eig_refine_kernel<true><<<(unsigned)rblocks, 128, 0, st>>>(c, nk, g, tri, tri_stride, dims, diff, trans, status,
                                                                  sharp, refine, refine_count);
