@@ -526,8 +526,8 @@ void band_init_attributes() {
                        (int)chase_smem_bytes<2, BW>());
   cudaFuncSetAttribute(bulge_chase_pipe_kernel<4, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)chase_smem_bytes<4, BW>());
-  cudaFuncSetAttribute(bulge_chase_pipe_kernel<11, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)chase_smem_bytes<11, BW>());
+  cudaFuncSetAttribute(bulge_chase_pipe_kernel<6, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)chase_smem_bytes<6, BW>());
 }
 
 bool band_path_supported(int N) { return N > HX_SMEM_MAX_N && N <= HX_MAX_N; }
@@ -578,7 +578,7 @@ static int band_reduce(double2* ws, const BandWs& L, int N, int64_t cnt, const i
   // warps per matrix: enough sweeps in flight to fill ~11 warps per SM across the batch
   const int64_t want = (148 * 11 + cnt - 1) / cnt;
   if (want >= 6) {
-    bulge_chase_pipe_kernel<11, BW><<<(unsigned)cnt, 11 * 32, chase_smem_bytes<11, BW>(), st>>>(
+    bulge_chase_pipe_kernel<6, BW><<<(unsigned)cnt, 6 * 32, chase_smem_bytes<6, BW>(), st>>>(
         ws, L.stride, L.a_off, L.dg_off, N, dims);
   } else if (want >= 3) {
     bulge_chase_pipe_kernel<4, BW><<<(unsigned)cnt, 4 * 32, chase_smem_bytes<4, BW>(), st>>>(

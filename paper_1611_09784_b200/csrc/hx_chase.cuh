@@ -1,52 +1,49 @@
-// Stage 2 of the banded path: band (lower, width BW) -> real symmetric tridiagonal by Householder
-// bulge chasing, pipelined over sweeps.
+// Stage 2 of the Hermitian banded path: band (lower, width BW) -> real symmetric tridiagonal by
+// Householder bulge chasing, pipelined over sweeps.
 //
 // Sweep i annihilates column i below the subdiagonal and chases the bulge down the band in tasks
-// t = 0, 1, ...; task t works on D_t = A[s:s+len, s:s+len] (s = i+1+t*BW) and the block below it
-// B_t = A[s+len : s+len+lb, s:s+len]:
-//     D <- H D H,  B <- B H,  H' = reflector(B[:,0]),  B <- H' B,  pass H' to task t+1.
-// Task t of sweep i touches columns [s-1, s+BW); task t of sweep i+1 only columns left of task t+2
-// of sweep i, so sweep i+1 may run task t as soon as sweep i has completed task t+1.  One warp owns
-// the sweeps i = w (mod NW) of its CTA's matrix and waits on a per-warp progress counter in shared
-// memory (no CTA-wide barriers).  Inside a warp lane r owns row r of D in registers (full Hermitian
-// row), B lives in the warp's shared-memory tile (copied in with cp.async), vectors are broadcast
-// from shared memory.
+// t = 0, 1, ...; task t works on the diagonal block D = A[s:s+len, s:s+len] (s = i+1+t*BW) and the
+// block below it B = A[s+len : s+len+lb, s:s+len]:
+//     D <- H D H                   (two-sided: p = D v, w = tau p - tau^2/2 (v^H p) v, D -= v w^H + w v^H)
+//     B <- H' B H                  (H' from column 0 of B H; fused into one rank-2 row update:
+//                                   with q = tau B v, pB = v'^H B, wq = v'^H q, z = tau' (pB - wq conj(v)),
+//                                   B'' = B - q v^H - v' z^T, column 0 -> (beta', 0, ...))
+//     H' is carried to task t+1.
+// Task t of sweep i touches rows/columns [s, s+2 BW); sweep i+1 may run task t once sweep i has completed
+// task t+1.  One warp owns the sweeps i = w (mod NW) of its CTA's matrix and waits on a per-warp
+// progress counter in shared memory (no CTA-wide barriers).  Tiles are zero padded to BW x BW so every
+// loop is a fixed, compact 32-iteration loop (the fully predicated unrolled form was instruction-cache
+// bound), lane = row for row passes and updates (stores coalesced per column), lane = column for the
+// column pass.
 #pragma once
 #include "hx_dense.cuh"
 
 namespace hx {
 
-// 16-byte global -> shared asynchronous copy (LDGSTS): all of a tile's loads are in flight at once.
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// warp sum of conj(a) * b
+__device__ __forceinline__ double2 warp_csum_hx(double2 a, double2 b) {
+  return make_double2(warp_sum(a.x * b.x + a.y * b.y), warp_sum(a.x * b.y - a.y * b.x));
+}
+
 template <int BWc>
 struct ChaseWarpSmem {
-  double2 B[BWc][BWc + 1];
-  double2 v[BWc], w[BWc], vp[BWc], z[BWc];
+  double2 D[BWc][BWc + 1];  // full Hermitian diagonal block (zero padded)
+  double2 B[BWc][BWc + 1];  // block below (zero padded)
+  double2 v[BWc];           // current reflector (v[0] = 1, zero padded)
+  double2 w[BWc];           // two-sided update vector
+  double2 vp[BWc];          // next reflector
+  double2 z[BWc];           // column coefficients of the B update
 };
 
-__device__ __forceinline__ double2 cfma_acc(double2 acc, double2 a, double2 b) {  // acc + a*b
-  acc.x = fma(a.x, b.x, acc.x);
-  acc.x = fma(-a.y, b.y, acc.x);
-  acc.y = fma(a.x, b.y, acc.y);
-  acc.y = fma(a.y, b.x, acc.y);
-  return acc;
-}
-__device__ __forceinline__ double2 cfma_conj_acc(double2 acc, double2 a, double2 b) {  // acc + conj(a)*b
-  acc.x = fma(a.x, b.x, acc.x);
-  acc.x = fma(a.y, b.y, acc.x);
-  acc.y = fma(a.x, b.y, acc.y);
-  acc.y = fma(-a.y, b.x, acc.y);
-  return acc;
-}
-
 template <int NW, int BWc>
-__global__ void __launch_bounds__(NW * 32) bulge_chase_pipe_kernel(double2* ws, size_t stride, size_t a_off,
-                                                                    size_t dg_off, int N, const int* dims) {
+__global__ void __launch_bounds__(NW * 32, 1) bulge_chase_pipe_kernel(double2* ws, size_t stride, size_t a_off,
+                                                                       size_t dg_off, int N, const int* dims) {
   extern __shared__ __align__(16) unsigned char chase_smem[];
   ChaseWarpSmem<BWc>* all = reinterpret_cast<ChaseWarpSmem<BWc>*>(chase_smem);
   volatile int* prog = reinterpret_cast<volatile int*>(all + NW);  // per warp: sweep*65536 + tasks done
@@ -58,6 +55,7 @@ __global__ void __launch_bounds__(NW * 32) bulge_chase_pipe_kernel(double2* ws, 
   double* e2 = diag + N;
   const int lda = N;
   const int d = dims ? dims[blockIdx.x] : N;
+  const double2 zero = make_double2(0.0, 0.0);
   if (lane == 0) prog[warp] = -1;
   __syncthreads();
   if (d <= 0) return;
@@ -72,164 +70,143 @@ __global__ void __launch_bounds__(NW * 32) bulge_chase_pipe_kernel(double2* ws, 
       if (i > 0) {
         const int need = (i - 1) * 65536 + min(t + 2, prev_tasks);
         if (lane == 0)
-          while (prog[pw] < need) {
-          }
+          while (prog[pw] < need) __nanosleep(20);
         __syncwarp();
         __threadfence_block();
       }
       const int s = i + 1 + t * BWc;
       const int len = min(BWc, d - s);
       const int lb = max(0, min(BWc, d - s - len));
+      // ---- D (lower triangle) and B tiles, asynchronously; colp = &A[s + lane][s], columns lda apart
+      double2* const colp = A + ((size_t)s * lda + s + lane);
+      {
+        const double2* src = colp;
+#pragma unroll 4
+        for (int c = 0; c < BWc; ++c, src += lda) {
+          if (c < len && lane >= c && lane < len) cp_async16(&S.D[lane][c], src);
+          else S.D[lane][c] = zero;
+        }
+        src = colp + len;
+#pragma unroll 4
+        for (int c = 0; c < BWc; ++c, src += lda) {
+          if (c < len && lane < lb) cp_async16(&S.B[lane][c], src);
+          else S.B[lane][c] = zero;
+        }
+      }
       if (t == 0) {
         // reflector from column i, rows s .. s+len-1
-        double2 x = make_double2(0.0, 0.0);
+        double2 x = zero;
         if (lane < len) x = A[s + lane + (size_t)i * lda];
         const double sig2 = warp_sum(x.x * x.x + x.y * x.y);
         const double2 alpha = make_double2(__shfl_sync(0xffffffffu, x.x, 0), __shfl_sync(0xffffffffu, x.y, 0));
-        const Reflector h = make_reflector(alpha, sig2);
+        const QuickReflector h = quick_reflector(alpha, sig2);
         tau = h.tau;
-        if (lane < len) {
-          S.v[lane] = lane == 0 ? make_double2(1.0, 0.0) : cmul(x, h.scale);
-          if (tau != 0.0) {
-            double2 outv = make_double2(0.0, 0.0);
-            if (lane == 0) {
-              const double sg = sqrt(sig2), aa = hypot(alpha.x, alpha.y);
-              const double2 ph = aa > 0.0 ? make_double2(alpha.x / aa, alpha.y / aa) : make_double2(1.0, 0.0);
-              outv = make_double2(-ph.x * sg, -ph.y * sg);
-            }
-            A[s + lane + (size_t)i * lda] = outv;
-          }
-        }
+        S.v[lane] = lane == 0 ? make_double2(1.0, 0.0) : (lane < len ? cmul(x, h.scale) : zero);
+        if (lane < len && tau != 0.0) A[s + lane + (size_t)i * lda] = lane == 0 ? h.beta : zero;
         if (lane == 0) {
           diag[i] = A[i + (size_t)i * lda].x;
           e2[i] = sig2;
         }
-        __syncwarp();
       }
-      // ---- stage D (lower triangle) through the B tile, build full rows in registers
-#pragma unroll
-      for (int c = 0; c < BWc; ++c)
-        if (c < len && lane >= c && lane < len) cp_async16(&S.B[lane][c], A + s + lane + (size_t)(s + c) * lda);
       cp_async_wait_all();
       __syncwarp();
-      double2 dr[BWc];
-#pragma unroll
-      for (int c = 0; c < BWc; ++c) {
-        double2 z = make_double2(0.0, 0.0);
-        if (lane < len && c < len) {
-          if (c <= lane) {
-            z = S.B[lane][c];
-          } else {
-            const double2 u = S.B[c][lane];
-            z = make_double2(u.x, -u.y);
-          }
+      // mirror the strictly upper part of D from its lower triangle
+#pragma unroll 4
+      for (int c = 0; c < BWc; ++c)
+        if (c > lane) {
+          const double2 u = S.D[c][lane];
+          S.D[lane][c] = make_double2(u.x, -u.y);
         }
-        dr[c] = z;
-      }
       __syncwarp();
-      // ---- B tile (completes while p = D v is computed from registers)
-#pragma unroll
-      for (int c = 0; c < BWc; ++c)
-        if (c < len && lane < lb) cp_async16(&S.B[lane][c], A + s + len + lane + (size_t)(s + c) * lda);
-      // ---- p = D v (4 independent partial sums); cval = v^H p ; w = tau p - 1/2 tau^2 cval v
-      double2 pp[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
-                       make_double2(0.0, 0.0)};
-#pragma unroll
-      for (int c = 0; c < BWc; ++c)
-        if (c < len) pp[c & 3] = cfma_acc(pp[c & 3], dr[c], S.v[c]);
-      const double2 p = make_double2((pp[0].x + pp[1].x) + (pp[2].x + pp[3].x), (pp[0].y + pp[1].y) + (pp[2].y + pp[3].y));
-      const double2 vr = lane < len ? S.v[lane] : make_double2(0.0, 0.0);
-      const double cval = warp_sum(lane < len ? vr.x * p.x + vr.y * p.y : 0.0);
+      // ---- D: p = D v (lane = row), cval = v^H p, w = tau p - tau^2/2 cval v
+      double2 p;
+      {
+        double2 a0 = zero, a1 = zero;
+#pragma unroll 4
+        for (int c = 0; c < BWc; c += 2) {
+          const double2 x0 = S.D[lane][c], v0 = S.v[c], x1 = S.D[lane][c + 1], v1 = S.v[c + 1];
+          a0.x = fma(x0.x, v0.x, fma(-x0.y, v0.y, a0.x));
+          a0.y = fma(x0.x, v0.y, fma(x0.y, v0.x, a0.y));
+          a1.x = fma(x1.x, v1.x, fma(-x1.y, v1.y, a1.x));
+          a1.y = fma(x1.x, v1.y, fma(x1.y, v1.x, a1.y));
+        }
+        p = make_double2(a0.x + a1.x, a0.y + a1.y);
+      }
+      const double2 vr = S.v[lane];
+      const double cval = warp_sum(vr.x * p.x + vr.y * p.y);
       const double hc = 0.5 * tau * tau * cval;
       const double2 wr = make_double2(tau * p.x - hc * vr.x, tau * p.y - hc * vr.y);
-      if (lane < len) S.w[lane] = wr;
+      S.w[lane] = wr;
       __syncwarp();
-      // ---- D -= v w^H + w v^H ; write the lower triangle back
-#pragma unroll
-      for (int c = 0; c < BWc; ++c) {
-        if (c < len) {
+      // ---- D -= v w^H + w v^H ; lower triangle straight to HBM (coalesced per column)
+      if (lane < len) {
+        double2* dst = colp;
+#pragma unroll 4
+        for (int c = 0; c < BWc; ++c, dst += lda) {
           const double2 vc = S.v[c], wc = S.w[c];
-          dr[c].x -= vr.x * wc.x + vr.y * wc.y + wr.x * vc.x + wr.y * vc.y;
-          dr[c].y -= (vr.y * wc.x - vr.x * wc.y) + (wr.y * vc.x - wr.x * vc.y);
-          if (lane < len && c <= lane) {
-            double2 z = dr[c];
-            if (c == lane) z.y = 0.0;
-            A[s + lane + (size_t)(s + c) * lda] = z;
-          }
+          double2 z = S.D[lane][c];
+          z.x -= (vr.x * wc.x + vr.y * wc.y) + (wr.x * vc.x + wr.y * vc.y);
+          z.y -= (vr.y * wc.x - vr.x * wc.y) + (wr.y * vc.x - wr.x * vc.y);
+          if (c == lane) z.y = 0.0;
+          if (c <= lane) *dst = z;
         }
       }
-      cp_async_wait_all();
-      __syncwarp();
       if (lb > 0) {
-        // ---- B <- B H : q = B v ; B -= tau q v^H  (lane = row)
-        double2 qq[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
-                         make_double2(0.0, 0.0)};
-        double2 brow[BWc];
-#pragma unroll
-        for (int c = 0; c < BWc; ++c) {
-          brow[c] = (c < len && lane < lb) ? S.B[lane][c] : make_double2(0.0, 0.0);
-          if (c < len) qq[c & 3] = cfma_acc(qq[c & 3], brow[c], S.v[c]);
-        }
-        const double2 q = make_double2(tau * ((qq[0].x + qq[1].x) + (qq[2].x + qq[3].x)),
-                                       tau * ((qq[0].y + qq[1].y) + (qq[2].y + qq[3].y)));
-#pragma unroll
-        for (int c = 0; c < BWc; ++c) {
-          if (c < len) {
-            const double2 vc = S.v[c];
-            brow[c].x -= q.x * vc.x + q.y * vc.y;
-            brow[c].y -= q.y * vc.x - q.x * vc.y;
+        // ---- B: q = tau B v (lane = row); x0 = column 0 of B - q v^H; H'
+        double2 q;
+        {
+          double2 a0 = zero, a1 = zero;
+#pragma unroll 4
+          for (int c = 0; c < BWc; c += 2) {
+            const double2 x0 = S.B[lane][c], v0 = S.v[c], x1 = S.B[lane][c + 1], v1 = S.v[c + 1];
+            a0.x = fma(x0.x, v0.x, fma(-x0.y, v0.y, a0.x));
+            a0.y = fma(x0.x, v0.y, fma(x0.y, v0.x, a0.y));
+            a1.x = fma(x1.x, v1.x, fma(-x1.y, v1.y, a1.x));
+            a1.y = fma(x1.x, v1.y, fma(x1.y, v1.x, a1.y));
           }
+          q = make_double2(tau * (a0.x + a1.x), tau * (a0.y + a1.y));
         }
-        // ---- H' from B[:, 0] (lane r holds B[r][0] in brow[0])
-        const double2 x = lane < lb ? brow[0] : make_double2(0.0, 0.0);
-        const double sg2 = warp_sum(x.x * x.x + x.y * x.y);
-        const double2 al = make_double2(__shfl_sync(0xffffffffu, x.x, 0), __shfl_sync(0xffffffffu, x.y, 0));
-        const Reflector hp = make_reflector(al, sg2);
-        const double2 vpr = lane == 0 ? make_double2(1.0, 0.0) : cmul(x, hp.scale);
-        if (lane < lb) {
-          S.vp[lane] = vpr;
-#pragma unroll
-          for (int c = 0; c < BWc; ++c)
-            if (c < len) S.B[lane][c] = brow[c];
+        const double2 b00 = S.B[lane][0];
+        const double2 x0 = make_double2(b00.x - q.x, b00.y - q.y);  // (B - q v^H)[r][0], v_0 = 1
+        const double sg2 = warp_sum(x0.x * x0.x + x0.y * x0.y);
+        const double2 al = make_double2(__shfl_sync(0xffffffffu, x0.x, 0), __shfl_sync(0xffffffffu, x0.y, 0));
+        const QuickReflector hp = quick_reflector(al, sg2);
+        const double2 vpr = lane == 0 ? make_double2(1.0, 0.0) : cmul(x0, hp.scale);  // zero on padded rows
+        S.vp[lane] = vpr;
+        const double2 wq = warp_csum_hx(vpr, q);  // v'^H q
+        __syncwarp();
+        // ---- column pass (lane = column): z_c = tau' (v'^H B[:, c] - wq conj(v_c))
+        {
+          double2 a0 = zero, a1 = zero;
+#pragma unroll 4
+          for (int r = 0; r < BWc; r += 2) {
+            const double2 p0 = S.vp[r], b0 = S.B[r][lane], p1 = S.vp[r + 1], b1 = S.B[r + 1][lane];
+            a0.x = fma(p0.x, b0.x, fma(p0.y, b0.y, a0.x));
+            a0.y = fma(p0.x, b0.y, fma(-p0.y, b0.x, a0.y));
+            a1.x = fma(p1.x, b1.x, fma(p1.y, b1.y, a1.x));
+            a1.y = fma(p1.x, b1.y, fma(-p1.y, b1.x, a1.y));
+          }
+          const double2 vc = S.v[lane];
+          const double2 wv = make_double2(wq.x * vc.x + wq.y * vc.y, wq.y * vc.x - wq.x * vc.y);  // wq conj(v_c)
+          S.z[lane] = make_double2(hp.tau * (a0.x + a1.x - wv.x), hp.tau * (a0.y + a1.y - wv.y));
         }
         __syncwarp();
-        // ---- z_c = v'^H B[:, c] (lane = column)
-        if (lane < len && lane > 0) {
-          double2 zz[4] = {make_double2(0.0, 0.0), make_double2(0.0, 0.0), make_double2(0.0, 0.0),
-                           make_double2(0.0, 0.0)};
-#pragma unroll
-          for (int r = 0; r < BWc; ++r)
-            if (r < lb) zz[r & 3] = cfma_conj_acc(zz[r & 3], S.vp[r], S.B[r][lane]);
-          S.z[lane] = make_double2(hp.tau * ((zz[0].x + zz[1].x) + (zz[2].x + zz[3].x)),
-                                   hp.tau * ((zz[0].y + zz[1].y) + (zz[2].y + zz[3].y)));
-        }
-        __syncwarp();
-        // ---- B <- H' B (lane = row), column 0 -> beta' e1 ; write B back (coalesced per column)
+        // ---- B'' = B - q v^H - v' z^T (lane = row), column 0 -> (beta', 0, ...); straight to HBM
         if (lane < lb) {
-#pragma unroll
-          for (int c = 1; c < BWc; ++c) {
-            if (c < len && hp.tau != 0.0) {
-              const double2 zc = S.z[c];
-              brow[c].x -= vpr.x * zc.x - vpr.y * zc.y;
-              brow[c].y -= vpr.x * zc.y + vpr.y * zc.x;
-            }
+          double2* dst = colp + len;
+#pragma unroll 4
+          for (int c = 0; c < BWc; ++c, dst += lda) {
+            const double2 vc = S.v[c], zc = S.z[c];
+            double2 y = S.B[lane][c];
+            y.x -= (q.x * vc.x + q.y * vc.y) + (vpr.x * zc.x - vpr.y * zc.y);
+            y.y -= (q.y * vc.x - q.x * vc.y) + (vpr.x * zc.y + vpr.y * zc.x);
+            if (c == 0 && hp.tau != 0.0) y = lane == 0 ? hp.beta : zero;
+            if (c < len) *dst = y;
           }
-          if (hp.tau != 0.0) {
-            double2 b0 = make_double2(0.0, 0.0);
-            if (lane == 0) {
-              const double sg = sqrt(sg2), aa = hypot(al.x, al.y);
-              const double2 ph = aa > 0.0 ? make_double2(al.x / aa, al.y / aa) : make_double2(1.0, 0.0);
-              b0 = make_double2(-ph.x * sg, -ph.y * sg);
-            }
-            brow[0] = b0;
-          }
-#pragma unroll
-          for (int c = 0; c < BWc; ++c)
-            if (c < len) A[s + len + lane + (size_t)(s + c) * lda] = brow[c];
         }
         __syncwarp();
         // carry H' to the next task of this sweep
-        if (lane < lb) S.v[lane] = vpr;
+        S.v[lane] = vpr;
         tau = hp.tau;
       }
       // ---- publish progress (release the global writes of this task to the other warps)
