@@ -3,9 +3,9 @@
 // Stage 1 (dense -> band of width BW=32), per panel step k0 for every matrix of the batch:
 //   panel_qr_kernel    Householder QR of the m x BW panel below the band (m = N - k0 - BW):
 //                      V (explicit, unit lower trapezoidal), T (zlarft forward/columnwise), R into A.
-//   hemm_kernel        X = A22 V                    (DMMA f64 tensor cores, complex as 4 real MMAs)
-//   w_z/w_m/w_rows     W = X T - 1/2 V (T^H V^H X T)     (row-parallel)
-//   her2k_kernel       A22 -= W V^H + V W^H          (DMMA; lower tiles computed, upper mirrored)
+//   xv_kernel<1>       Y = A22 V T                  (hx_gemm.cuh: DMMA f64 tensor cores, cp.async pipeline)
+//   w_z/w_m/w_rows     W = Y - 1/2 V (T^H V^H Y)         (row-parallel)
+//   her2k_kernel       A22 -= W V^H + V W^H          (hx_gemm.cuh; lower tiles computed, upper mirrored)
 // so that A22 <- Q^H A22 Q with Q = I - V T V^H (the blocked two-sided update of zhetrd/zhe2hb).
 // Stage 2 (band -> tridiagonal): bulge_chase_pipe_kernel (hx_chase.cuh), pipelined Householder bulge chasing.
 // Then Sturm bisection + the reference IDOS functional (hx_dense.cuh) per matrix.
@@ -21,6 +21,7 @@
 #include "hx_band.cuh"
 #include "hx_dense.cuh"
 #include "hx_dmma.cuh"
+#include "hx_gemm.cuh"
 #include "hx_kernels.cuh"
 #include "hx_chase.cuh"
 #include "hx_panel.cuh"
@@ -178,75 +179,11 @@ __global__ void __launch_bounds__(256) panel_qr_kernel(double2* ws, BandWs L, in
 }
 
 // ------------------------------------------------------------------------------------------------
-// X = A22 V (m x BW), A22 = A[k0+BW:, k0+BW:] Hermitian (both triangles stored).  64-row tiles,
-// 4 warps x (16 rows x 32 cols), DMMA m8n8k4 f64.  A tile element (r, c) is read as
-// conj(A22[c, r]) (column-contiguous loads via Hermitian symmetry).
-constexpr int HM_TM = 64, HM_TK = 32, HM_LD = HM_TK + 4;
-
-__global__ void __launch_bounds__(128) hemm_kernel(double2* ws, BandWs L, int N, int k0) {
-  extern __shared__ double2 dsm[];
-  double2 (*As)[HM_LD] = reinterpret_cast<double2 (*)[HM_LD]>(dsm);
-  double2 (*Vs)[HM_LD] = reinterpret_cast<double2 (*)[HM_LD]>(dsm + HM_TM * HM_LD);
-  double2* base = ws + (size_t)blockIdx.y * L.stride;
-  const int lda = N, m = N - k0 - BW;
-  const double2* A22 = base + L.a_off + (size_t)(k0 + BW) * lda + (k0 + BW);
-  const double2* V = base + L.v_off;
-  double2* X = base + L.x_off;
-  const int i0 = blockIdx.x * HM_TM;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  CTile acc[2][4];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b].zero();
-  for (int kk = 0; kk < m; kk += HM_TK) {
-    // A tile: As[r][c] = conj(A22[kk + c, i0 + r])
-    for (int p = tid; p < HM_TM * HM_TK; p += 128) {
-      const int c = p & (HM_TK - 1), r = p / HM_TK;
-      const int gi = i0 + r, gk = kk + c;
-      double2 z = make_double2(0.0, 0.0);
-      if (gi < m && gk < m) z = A22[gk + (size_t)gi * lda];
-      As[r][c] = cconj(z);
-    }
-    for (int p = tid; p < BW * HM_TK; p += 128) {
-      const int c = p & (HM_TK - 1), n = p / HM_TK;
-      const int gk = kk + c;
-      Vs[n][c] = gk < m ? V[gk + (size_t)n * N] : make_double2(0.0, 0.0);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k4 = 0; k4 < HM_TK / 4; ++k4) {
-      const int kc = 4 * k4 + (lane & 3);
-      double2 a[2], b[4];
-#pragma unroll
-      for (int rt = 0; rt < 2; ++rt) a[rt] = As[16 * warp + 8 * rt + (lane >> 2)][kc];
-#pragma unroll
-      for (int ct = 0; ct < 4; ++ct) b[ct] = Vs[8 * ct + (lane >> 2)][kc];
-#pragma unroll
-      for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-        for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(a[rt].x, a[rt].y, b[ct].x, b[ct].y);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-    for (int ct = 0; ct < 4; ++ct) {
-      const int r = i0 + 16 * warp + 8 * rt + (lane >> 2);
-      const int c = 8 * ct + 2 * (lane & 3);
-      if (r < m) {
-        X[r + (size_t)c * N] = make_double2(acc[rt][ct].re0, acc[rt][ct].im0);
-        X[r + (size_t)(c + 1) * N] = make_double2(acc[rt][ct].re1, acc[rt][ct].im1);
-      }
-    }
-}
-
-// ------------------------------------------------------------------------------------------------
-// W = X T - 1/2 V M, M = T^H (V^H X) T, in three row-parallel steps (W overwrites X):
-//   w_z_kernel    partial Z_s = V[rows_s]^H X[rows_s] for nsplit row ranges of every matrix
-//   w_m_kernel    Z = sum_s Z_s (fixed order), M/2 = T^H Z T / 2          (one small CTA per matrix)
-//   w_rows_kernel W[rows] = X[rows] T - V[rows] (M/2)                      (32-row tiles)
+// With Y = X T = A22 V T (xv_kernel's epilogue): W = Y - 1/2 V M, M = T^H (V^H Y), in three row-parallel
+// steps (W overwrites Y):
+//   w_z_kernel    partial Z_s = V[rows_s]^H Y[rows_s] for nsplit row ranges of every matrix
+//   w_m_kernel    Z = sum_s Z_s (fixed order), M/2 = T^H Z / 2             (one small CTA per matrix)
+//   w_rows_kernel W[rows] = Y[rows] - V[rows] (M/2)                        (32-row tiles)
 constexpr int W_SPLIT_MAX = 16;
 
 __global__ void __launch_bounds__(256) w_z_kernel(double2* ws, BandWs L, int N, int k0, int nsplit) {
@@ -289,7 +226,6 @@ __global__ void __launch_bounds__(256) w_z_kernel(double2* ws, BandWs L, int N, 
 
 __global__ void __launch_bounds__(256) w_m_kernel(double2* ws, BandWs L, int nsplit) {
   __shared__ double2 Zs[BW][BW];
-  __shared__ double2 Ms[BW][BW];
   __shared__ double2 Tsh[BW][BW];
   double2* base = ws + (size_t)blockIdx.x * L.stride;
   const double2* T = base + L.t_off;
@@ -307,28 +243,13 @@ __global__ void __launch_bounds__(256) w_m_kernel(double2* ws, BandWs L, int nsp
     Zs[r][oc] = t;
   }
   __syncthreads();
-  double2 z[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {  // Ms = Z T
-    const int r = orow + 8 * q;
-    double2 t = make_double2(0.0, 0.0);
-    for (int l = 0; l < BW; ++l) {
-      const double2 a = Zs[r][l], b = Tsh[l][oc];
-      t.x += a.x * b.x - a.y * b.y;
-      t.y += a.x * b.y + a.y * b.x;
-    }
-    z[q] = t;
-  }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) Ms[orow + 8 * q][oc] = z[q];
-  __syncthreads();
   double2* mh = base + L.m_off;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {  // M/2 = T^H Ms / 2
     const int r = orow + 8 * q;
     double2 t = make_double2(0.0, 0.0);
     for (int l = 0; l < BW; ++l) {
-      const double2 a = cconj(Tsh[l][r]), b = Ms[l][oc];
+      const double2 a = cconj(Tsh[l][r]), b = Zs[l][oc];
       t.x += a.x * b.x - a.y * b.y;
       t.y += a.x * b.y + a.y * b.x;
     }
@@ -365,13 +286,12 @@ __global__ void __launch_bounds__(256) w_rows_kernel(double2* ws, BandWs L, int 
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int rr = orow + 8 * q;
-    double2 t = make_double2(0.0, 0.0);
+    double2 t = Xt[rr][oc];
 #pragma unroll 8
     for (int l = 0; l < BW; ++l) {
-      const double2 x = Xt[rr][l], v = Vt[rr][l];
-      const double2 tt = Tsh[l][oc], mm = Mh[l][oc];
-      t.x += (x.x * tt.x - x.y * tt.y) - (v.x * mm.x - v.y * mm.y);
-      t.y += (x.x * tt.y + x.y * tt.x) - (v.x * mm.y + v.y * mm.x);
+      const double2 v = Vt[rr][l], mm = Mh[l][oc];
+      t.x -= v.x * mm.x - v.y * mm.y;
+      t.y -= v.x * mm.y + v.y * mm.x;
     }
     z[q] = t;
   }
@@ -380,100 +300,6 @@ __global__ void __launch_bounds__(256) w_rows_kernel(double2* ws, BandWs L, int 
     const int rr = orow + 8 * q;
     if (r0 + rr < m) X[r0 + rr + (size_t)oc * N] = z[q];
   }
-}
-
-// ------------------------------------------------------------------------------------------------
-// A22 -= W V^H + V W^H on lower 64x64 tiles (I >= J); upper triangle mirrored as conj.  K = BW.
-constexpr int HK_T = 64, HK_K = 16, HK_LD = HK_K + 4;
-
-__global__ void __launch_bounds__(256) her2k_kernel(double2* ws, BandWs L, int N, int k0) {
-  extern __shared__ double2 dsm[];
-  double2 (*Wi)[HK_LD] = reinterpret_cast<double2 (*)[HK_LD]>(dsm);
-  double2 (*Vi)[HK_LD] = reinterpret_cast<double2 (*)[HK_LD]>(dsm + HK_T * HK_LD);
-  double2 (*Wj)[HK_LD] = reinterpret_cast<double2 (*)[HK_LD]>(dsm + 2 * HK_T * HK_LD);
-  double2 (*Vj)[HK_LD] = reinterpret_cast<double2 (*)[HK_LD]>(dsm + 3 * HK_T * HK_LD);
-  double2* base = ws + (size_t)blockIdx.y * L.stride;
-  const int lda = N, m = N - k0 - BW;
-  double2* A22 = base + L.a_off + (size_t)(k0 + BW) * lda + (k0 + BW);
-  const double2* V = base + L.v_off;
-  const double2* W = base + L.x_off;
-  // lower-tile index -> (I, J)
-  const int t = blockIdx.x;
-  int I = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-  while ((I + 1) * (I + 2) / 2 <= t) ++I;
-  while (I * (I + 1) / 2 > t) --I;
-  const int J = t - I * (I + 1) / 2;
-  const int I0 = I * HK_T, J0 = J * HK_T;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wr = warp & 3, wc = warp >> 2;  // warp tile: rows 16*wr.., cols 32*wc..
-  CTile acc[2][4];
-  // initialise with the current A22 tile
-#pragma unroll
-  for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-    for (int ct = 0; ct < 4; ++ct) {
-      const int r = I0 + 16 * wr + 8 * rt + (lane >> 2);
-      const int c = J0 + 32 * wc + 8 * ct + 2 * (lane & 3);
-      double2 z0 = make_double2(0.0, 0.0), z1 = make_double2(0.0, 0.0);
-      if (r < m && c < m) z0 = A22[r + (size_t)c * lda];
-      if (r < m && c + 1 < m) z1 = A22[r + (size_t)(c + 1) * lda];
-      acc[rt][ct].re0 = z0.x;
-      acc[rt][ct].im0 = z0.y;
-      acc[rt][ct].re1 = z1.x;
-      acc[rt][ct].im1 = z1.y;
-    }
-  for (int kk = 0; kk < BW; kk += HK_K) {
-    __syncthreads();
-    for (int p = tid; p < HK_T * HK_K; p += 256) {
-      const int r = p & (HK_T - 1), k = p / HK_T;
-      const size_t col = (size_t)(kk + k) * N;
-      const bool oi = I0 + r < m, oj = J0 + r < m;
-      Wi[r][k] = oi ? W[I0 + r + col] : make_double2(0.0, 0.0);
-      Vi[r][k] = oi ? V[I0 + r + col] : make_double2(0.0, 0.0);
-      Wj[r][k] = oj ? W[J0 + r + col] : make_double2(0.0, 0.0);
-      Vj[r][k] = oj ? V[J0 + r + col] : make_double2(0.0, 0.0);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k4 = 0; k4 < HK_K / 4; ++k4) {
-      const int kc = 4 * k4 + (lane & 3);
-      double2 aw[2], av[2], bv[4], bw[4];
-#pragma unroll
-      for (int rt = 0; rt < 2; ++rt) {
-        aw[rt] = Wi[16 * wr + 8 * rt + (lane >> 2)][kc];
-        av[rt] = Vi[16 * wr + 8 * rt + (lane >> 2)][kc];
-      }
-#pragma unroll
-      for (int ct = 0; ct < 4; ++ct) {
-        bv[ct] = cconj(Vj[32 * wc + 8 * ct + (lane >> 2)][kc]);
-        bw[ct] = cconj(Wj[32 * wc + 8 * ct + (lane >> 2)][kc]);
-      }
-#pragma unroll
-      for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-        for (int ct = 0; ct < 4; ++ct) {
-          acc[rt][ct].mac(-aw[rt].x, -aw[rt].y, bv[ct].x, bv[ct].y);
-          acc[rt][ct].mac(-av[rt].x, -av[rt].y, bw[ct].x, bw[ct].y);
-        }
-    }
-  }
-  // store lower part of the tile and the conjugate mirror
-#pragma unroll
-  for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-    for (int ct = 0; ct < 4; ++ct) {
-      const int r = I0 + 16 * wr + 8 * rt + (lane >> 2);
-      const int c = J0 + 32 * wc + 8 * ct + 2 * (lane & 3);
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int cc = c + e;
-        if (r >= m || cc >= m || cc > r) continue;
-        double2 z = e ? make_double2(acc[rt][ct].re1, acc[rt][ct].im1) : make_double2(acc[rt][ct].re0, acc[rt][ct].im0);
-        if (cc == r) z.y = 0.0;
-        A22[r + (size_t)cc * lda] = z;
-        if (cc != r) A22[cc + (size_t)r * lda] = cconj(z);
-      }
-    }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -509,8 +335,6 @@ __global__ void __launch_bounds__(256) band_copy_kernel(const double2* __restric
 }
 
 // ------------------------------------------------------------------------------------------------
-constexpr size_t HEMM_SMEM = (size_t)(HM_TM + BW) * HM_LD * sizeof(double2);
-constexpr size_t HER2K_SMEM = (size_t)4 * HK_T * HK_LD * sizeof(double2);
 
 constexpr size_t W_ROWS_SMEM = (size_t)(2 * BW * BW + 64 * (BW + 1)) * sizeof(double2);
 
@@ -518,16 +342,18 @@ void band_init_attributes() {
   cudaFuncSetAttribute(w_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W_ROWS_SMEM);
   cudaFuncSetAttribute(panel_qr_reg_kernel<16, 8, 32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(band_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  cudaFuncSetAttribute(hemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HEMM_SMEM);
-  cudaFuncSetAttribute(her2k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HER2K_SMEM);
-  cudaFuncSetAttribute(bulge_chase_pipe_kernel<1, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)chase_smem_bytes<1, BW>());
-  cudaFuncSetAttribute(bulge_chase_pipe_kernel<2, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)chase_smem_bytes<2, BW>());
-  cudaFuncSetAttribute(bulge_chase_pipe_kernel<4, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)chase_smem_bytes<4, BW>());
-  cudaFuncSetAttribute(bulge_chase_pipe_kernel<6, BW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)chase_smem_bytes<6, BW>());
+  cudaFuncSetAttribute(her2k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HK_SMEM);
+  cudaFuncSetAttribute(xv_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XV_SMEM);
+  cudaFuncSetAttribute(xv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XV_SMEM);
+#define HCHASE_ATTR(NW)                                                                           \
+  cudaFuncSetAttribute(bulge_chase_pipe_kernel<NW, BW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                       (int)chase_smem_bytes<NW, BW, false>())
+  HCHASE_ATTR(1);
+  HCHASE_ATTR(2);
+  HCHASE_ATTR(3);
+  HCHASE_ATTR(6);
+  HCHASE_ATTR(11);
+#undef HCHASE_ATTR
 }
 
 bool band_path_supported(int N) { return N > HX_SMEM_MAX_N && N <= HX_MAX_N; }
@@ -563,33 +389,32 @@ static int band_reduce(double2* ws, const BandWs& L, int N, int64_t cnt, const i
     PanelArgs pa{L.stride, L.a_off, N, k0 + BW, k0, m, 0, L.v_off, N, L.t_off};
     if (!launch_cluster_panel(ws, pa, cnt, st))
       panel_qr_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, L, N, k0);
-    const unsigned mt = (unsigned)((m + HM_TM - 1) / HM_TM);
-    hemm_kernel<<<dim3(mt, (unsigned)cnt), 128, HEMM_SMEM, st>>>(ws, L, N, k0);
+    const SlabGeom G{L.stride, N, L.a_off};
+    // Y = A22 V T; op(A)[i][k] = conj(A[k0+BW+k][k0+BW+i]) = A22[i][k] (Hermitian, column-contiguous reads)
+    xv_kernel<1><<<dim3((unsigned)((m + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM, st>>>(
+        ws, G, k0 + BW, k0 + BW, m, m, L.v_off, L.x_off, L.t_off);
     const int nsplit = std::min(W_SPLIT_MAX, std::max(1, (m + 127) / 128));
     w_z_kernel<<<dim3((unsigned)nsplit, (unsigned)cnt), 256, 0, st>>>(ws, L, N, k0, nsplit);
     w_m_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, L, nsplit);
     w_rows_kernel<<<dim3((unsigned)((m + 31) / 32), (unsigned)cnt), 256, W_ROWS_SMEM, st>>>(ws, L, N, k0);
     count_launch(2);
-    const unsigned tt = (unsigned)((m + HK_T - 1) / HK_T);
-    her2k_kernel<<<dim3(tt * (tt + 1) / 2, (unsigned)cnt), 256, HER2K_SMEM, st>>>(ws, L, N, k0);
+    const unsigned tt = (unsigned)((m + RU_T - 1) / RU_T);
+    her2k_kernel<<<dim3(tt * (tt + 1) / 2, (unsigned)cnt), 256, HK_SMEM, st>>>(ws, G, k0 + BW, m, L.x_off, L.v_off);
     count_launch(4);
     BAND_CUDA(cudaGetLastError());
   }
-  // warps per matrix: enough sweeps in flight to fill ~11 warps per SM across the batch
-  const int64_t want = (148 * 11 + cnt - 1) / cnt;
-  if (want >= 6) {
-    bulge_chase_pipe_kernel<6, BW><<<(unsigned)cnt, 6 * 32, chase_smem_bytes<6, BW>(), st>>>(
-        ws, L.stride, L.a_off, L.dg_off, N, dims);
-  } else if (want >= 3) {
-    bulge_chase_pipe_kernel<4, BW><<<(unsigned)cnt, 4 * 32, chase_smem_bytes<4, BW>(), st>>>(
-        ws, L.stride, L.a_off, L.dg_off, N, dims);
-  } else if (want >= 2) {
-    bulge_chase_pipe_kernel<2, BW><<<(unsigned)cnt, 2 * 32, chase_smem_bytes<2, BW>(), st>>>(
-        ws, L.stride, L.a_off, L.dg_off, N, dims);
-  } else {
-    bulge_chase_pipe_kernel<1, BW><<<(unsigned)cnt, 32, chase_smem_bytes<1, BW>(), st>>>(
-        ws, L.stride, L.a_off, L.dg_off, N, dims);
-  }
+  // warps per matrix: enough sweeps in flight to fill ~12 warps per SM across the batch (single-tile
+  // variant: 19 KB of shared memory per warp)
+  const int64_t want = (148 * 12 + cnt - 1) / cnt;
+#define HCHASE(NW)                                                                                \
+  bulge_chase_pipe_kernel<NW, BW, false><<<(unsigned)cnt, NW * 32, chase_smem_bytes<NW, BW, false>(), st>>>( \
+      ws, L.stride, L.a_off, L.dg_off, N, dims)
+  if (want >= 11) HCHASE(11);
+  else if (want >= 6) HCHASE(6);
+  else if (want >= 3) HCHASE(3);
+  else if (want >= 2) HCHASE(2);
+  else HCHASE(1);
+#undef HCHASE
   count_launch(1);
   BAND_CUDA(cudaGetLastError());
   return 0;

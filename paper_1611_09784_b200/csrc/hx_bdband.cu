@@ -23,6 +23,7 @@
 #include "hx_bidiag.cuh"
 #include "hx_dense.cuh"
 #include "hx_dmma.cuh"
+#include "hx_gemm.cuh"
 #include "hx_kernels.cuh"
 #include "hx_panel.cuh"
 #include "hx_bdchase.cuh"
@@ -62,7 +63,6 @@ struct BdWs {
   }
 };
 
-__device__ __forceinline__ double2 conj2(double2 a) { return make_double2(a.x, -a.y); }
 
 // ------------------------------------------------------------------------------------------------
 // C = A-B block of the phase matrix per (mask, k), zero padded to S x S; dims = nA + nB.
@@ -87,233 +87,11 @@ __global__ void __launch_bounds__(256) bd_assemble_kernel(CellDev c, const doubl
 }
 
 // ------------------------------------------------------------------------------------------------
-// Asynchronous 16-byte global -> shared copy; src_bytes = 0 zero-fills the destination.
-__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// X[rows x BB] = op(A) V, op(A)[i][k] = M[ar0+i][ac0+k] (MODE 0) or conj(M[ar0+k][ac0+i]) (MODE 1),
-// V [K x BB] (ld S).  64-row tiles, 4 warps x (16 x 32), DMMA m8n8k4 f64, K in chunks of 16 through a
-// 3-stage cp.async pipeline.  Shared layouts keep the fragment loads conflict-free:
-//   MODE 0: As[k][i] (i contiguous, the matrix's column direction), ld 66 (= 2 mod 8 in 16 B units)
-//   MODE 1: As[i][k] (k contiguous), ld 20 (= 4 mod 8); the conjugate is applied at fragment load.
-constexpr int XV_TM = 64, XV_TK = 16, XV_ST = 3;
-constexpr int XV_LD0 = XV_TM + 2, XV_LD1 = XV_TK + 4, XV_LDV = XV_TK + 4;
-constexpr int XV_A_ELEMS = XV_TK * XV_LD0 > XV_TM * XV_LD1 ? XV_TK * XV_LD0 : XV_TM * XV_LD1;
-constexpr size_t XV_SMEM = (size_t)XV_ST * (XV_A_ELEMS + BB * XV_LDV) * sizeof(double2);
-static_assert((size_t)(XV_TM + BB) * (BB + 4) * sizeof(double2) <= XV_SMEM, "xv epilogue tile does not fit");
-
-template <int MODE>
-__global__ void __launch_bounds__(128) xv_kernel(double2* ws, BdWs L, int ar0, int ac0, int rows, int K,
-                                                 size_t v_off, size_t x_off, size_t t_off) {
-  extern __shared__ __align__(16) double2 xv_sm[];
-  double2* As = xv_sm;                         // [XV_ST][XV_A_ELEMS]
-  double2* Vs = xv_sm + XV_ST * XV_A_ELEMS;    // [XV_ST][BB][XV_LDV]
-  double2* base = ws + (size_t)blockIdx.y * L.stride;
-  const int ld = L.S;
-  const double2* M = base + L.c_off;
-  const double2* V = base + v_off;
-  double2* X = base + x_off;
-  const int i0 = blockIdx.x * XV_TM;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nchunks = (K + XV_TK - 1) / XV_TK;
-  auto load_chunk = [&](int ch, int stg) {
-    const int kk = ch * XV_TK;
-    double2* A = As + stg * XV_A_ELEMS;
-    if (MODE == 1) {
-      // element (i, k) at M[(ac0+i)*ld + ar0 + k]: 16 consecutive k per row i
-#pragma unroll
-      for (int q = 0; q < XV_TM * XV_TK / 128; ++q) {
-        const int p = tid + 128 * q, kc = p & (XV_TK - 1), r = p >> 4;
-        const int gi = i0 + r, gk = kk + kc;
-        const bool ok = gi < rows && gk < K;
-        cp_async16_zfill(A + r * XV_LD1 + kc, M + (ok ? (size_t)(ac0 + gi) * ld + ar0 + gk : 0), ok);
-      }
-    } else {
-      // element (i, k) at M[(ac0+k)*ld + ar0 + i]: 64 consecutive i per column k
-#pragma unroll
-      for (int q = 0; q < XV_TM * XV_TK / 128; ++q) {
-        const int p = tid + 128 * q, r = p & (XV_TM - 1), kc = p >> 6;
-        const int gi = i0 + r, gk = kk + kc;
-        const bool ok = gi < rows && gk < K;
-        cp_async16_zfill(A + kc * XV_LD0 + r, M + (ok ? (size_t)(ac0 + gk) * ld + ar0 + gi : 0), ok);
-      }
-    }
-    double2* Vt = Vs + stg * BB * XV_LDV;
-#pragma unroll
-    for (int q = 0; q < BB * XV_TK / 128; ++q) {
-      const int p = tid + 128 * q, kc = p & (XV_TK - 1), n = p >> 4;
-      const int gk = kk + kc;
-      const bool ok = gk < K;
-      cp_async16_zfill(Vt + n * XV_LDV + kc, V + (ok ? gk + (size_t)n * ld : 0), ok);
-    }
-  };
-  CTile acc[2][4];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b].zero();
-#pragma unroll
-  for (int stg = 0; stg < XV_ST - 1; ++stg) {
-    if (stg < nchunks) load_chunk(stg, stg);
-    cp_async_commit();
-  }
-  for (int ch = 0; ch < nchunks; ++ch) {
-    cp_async_wait<XV_ST - 2>();
-    __syncthreads();
-    {  // prefetch chunk ch + ST - 1 into the stage freed at iteration ch - 1
-      const int nx = ch + XV_ST - 1;
-      if (nx < nchunks) load_chunk(nx, nx % XV_ST);
-      cp_async_commit();
-    }
-    const int stg = ch % XV_ST;
-    const double2* A = As + stg * XV_A_ELEMS;
-    const double2* Vt = Vs + stg * BB * XV_LDV;
-#pragma unroll
-    for (int k4 = 0; k4 < XV_TK / 4; ++k4) {
-      const int kc = 4 * k4 + (lane & 3);
-      double2 a[2], b[4];
-#pragma unroll
-      for (int rt = 0; rt < 2; ++rt) {
-        const int r = 16 * warp + 8 * rt + (lane >> 2);
-        a[rt] = MODE == 1 ? A[r * XV_LD1 + kc] : A[kc * XV_LD0 + r];
-        if (MODE == 1) a[rt].y = -a[rt].y;
-      }
-#pragma unroll
-      for (int ct = 0; ct < 4; ++ct) b[ct] = Vt[(8 * ct + (lane >> 2)) * XV_LDV + kc];
-#pragma unroll
-      for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-        for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(a[rt].x, a[rt].y, b[ct].x, b[ct].y);
-    }
-  }
-  // ---- epilogue: X <- (op(A) V) T with T (BB x BB, column-major) - the block reflector's T factor,
-  //      applied on the tile in shared memory (DMMA), saving a pass over X
-  cp_async_wait<0>();
-  __syncthreads();
-  constexpr int XL = BB + 4;  // 4 (mod 8): conflict-free fragments
-  double2* Xs = xv_sm;        // [XV_TM][XL]   (reuses the pipeline stages)
-  double2* Ts = xv_sm + XV_TM * XL;  // [BB (n)][XL (k)] = T[k][n]
-  const double2* T = base + t_off;
-  for (int p = tid; p < BB * BB; p += 128) Ts[(p / BB) * XL + (p % BB)] = T[p];
-#pragma unroll
-  for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-    for (int ct = 0; ct < 4; ++ct) {
-      const int r = 16 * warp + 8 * rt + (lane >> 2);
-      const int cc = 8 * ct + 2 * (lane & 3);
-      Xs[r * XL + cc] = make_double2(acc[rt][ct].re0, acc[rt][ct].im0);
-      Xs[r * XL + cc + 1] = make_double2(acc[rt][ct].re1, acc[rt][ct].im1);
-      acc[rt][ct].zero();
-    }
-  __syncthreads();
-#pragma unroll
-  for (int k4 = 0; k4 < BB / 4; ++k4) {
-    const int kc = 4 * k4 + (lane & 3);
-    double2 a[2], b[4];
-#pragma unroll
-    for (int rt = 0; rt < 2; ++rt) a[rt] = Xs[(16 * warp + 8 * rt + (lane >> 2)) * XL + kc];
-#pragma unroll
-    for (int ct = 0; ct < 4; ++ct) b[ct] = Ts[(8 * ct + (lane >> 2)) * XL + kc];
-#pragma unroll
-    for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-      for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(a[rt].x, a[rt].y, b[ct].x, b[ct].y);
-  }
-#pragma unroll
-  for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-    for (int ct = 0; ct < 4; ++ct) {
-      const int r = i0 + 16 * warp + 8 * rt + (lane >> 2);
-      const int cc = 8 * ct + 2 * (lane & 3);
-      if (r < rows) {
-        X[r + (size_t)cc * ld] = make_double2(acc[rt][ct].re0, acc[rt][ct].im0);
-        X[r + (size_t)(cc + 1) * ld] = make_double2(acc[rt][ct].re1, acc[rt][ct].im1);
-      }
-    }
-}
-
-// M[mr0:mr0+m, mc0:mc0+n] -= U W^H, U [m x BB] and W [n x BB] (ld S); 64 x 64 tiles, DMMA.  The whole
-// K = BB depth of U and W is staged once with cp.async (ld 36 = 4 mod 8: conflict-free fragments) while
-// the C tile is read straight into the accumulators; 2 CTAs per SM.
-constexpr int RU_T = 64, RU_LD = BB + 4;
-constexpr size_t RU_SMEM = (size_t)2 * RU_T * RU_LD * sizeof(double2);
-
-__global__ void __launch_bounds__(256, 2) rank_update_kernel(double2* ws, BdWs L, int mr0, int mc0, int m, int n,
-                                                             size_t u_off, size_t w_off) {
-  extern __shared__ __align__(16) double2 ru_sm[];
-  double2* Us = ru_sm;                // [RU_T][RU_LD]
-  double2* Ws = ru_sm + RU_T * RU_LD;  // [RU_T][RU_LD]
-  double2* base = ws + (size_t)blockIdx.z * L.stride;
-  const int ld = L.S;
-  double2* M = base + L.c_off + (size_t)mc0 * ld + mr0;
-  const double2* U = base + u_off;
-  const double2* W = base + w_off;
-  const int I0 = blockIdx.x * RU_T, J0 = blockIdx.y * RU_T;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wr = warp & 3, wc = warp >> 2;
-#pragma unroll
-  for (int q = 0; q < RU_T * BB / 256; ++q) {
-    const int p = tid + 256 * q, r = p & (RU_T - 1), k = p >> 6;
-    const size_t col = (size_t)k * ld;
-    const bool oku = I0 + r < m, okw = J0 + r < n;
-    cp_async16_zfill(Us + r * RU_LD + k, U + (oku ? I0 + r + col : 0), oku);
-    cp_async16_zfill(Ws + r * RU_LD + k, W + (okw ? J0 + r + col : 0), okw);
-  }
-  cp_async_commit();
-  CTile acc[2][4];
-#pragma unroll
-  for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-    for (int ct = 0; ct < 4; ++ct) {
-      const int r = I0 + 16 * wr + 8 * rt + (lane >> 2);
-      const int cc = J0 + 32 * wc + 8 * ct + 2 * (lane & 3);
-      double2 z0 = make_double2(0.0, 0.0), z1 = make_double2(0.0, 0.0);
-      if (r < m && cc < n) z0 = M[r + (size_t)cc * ld];
-      if (r < m && cc + 1 < n) z1 = M[r + (size_t)(cc + 1) * ld];
-      acc[rt][ct].re0 = z0.x;
-      acc[rt][ct].im0 = z0.y;
-      acc[rt][ct].re1 = z1.x;
-      acc[rt][ct].im1 = z1.y;
-    }
-  cp_async_wait<0>();
-  __syncthreads();
-#pragma unroll
-  for (int k4 = 0; k4 < BB / 4; ++k4) {
-    const int kc = 4 * k4 + (lane & 3);
-    double2 au[2], bw[4];
-#pragma unroll
-    for (int rt = 0; rt < 2; ++rt) au[rt] = Us[(16 * wr + 8 * rt + (lane >> 2)) * RU_LD + kc];
-#pragma unroll
-    for (int ct = 0; ct < 4; ++ct) bw[ct] = conj2(Ws[(32 * wc + 8 * ct + (lane >> 2)) * RU_LD + kc]);
-#pragma unroll
-    for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-      for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(-au[rt].x, -au[rt].y, bw[ct].x, bw[ct].y);
-  }
-#pragma unroll
-  for (int rt = 0; rt < 2; ++rt)
-#pragma unroll
-    for (int ct = 0; ct < 4; ++ct) {
-      const int r = I0 + 16 * wr + 8 * rt + (lane >> 2);
-      const int cc = J0 + 32 * wc + 8 * ct + 2 * (lane & 3);
-      if (r < m && cc < n) M[r + (size_t)cc * ld] = make_double2(acc[rt][ct].re0, acc[rt][ct].im0);
-      if (r < m && cc + 1 < n) M[r + (size_t)(cc + 1) * ld] = make_double2(acc[rt][ct].re1, acc[rt][ct].im1);
-    }
-}
-
-
-// ------------------------------------------------------------------------------------------------
 bool launch_cluster_panel(double2* ws, const PanelArgs& a, int64_t cnt, cudaStream_t st);
 
 static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, cudaStream_t st) {
   const int S = L.S;
+  const SlabGeom G{L.stride, S, L.c_off};
   for (int k0 = 0; k0 < S; k0 += BB) {
     const int m1 = S - k0, n2 = S - k0 - BB;
     // ---- left: column panel QR, C_tr = C[k0:, k0+BB:] <- Q1^H C_tr
@@ -325,9 +103,9 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     count_launch();
     if (n2 <= 0) break;
     xv_kernel<1><<<dim3((unsigned)((n2 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM, st>>>(
-        ws, L, k0, k0 + BB, n2, m1, L.v1_off, L.x_off, L.t1_off);
+        ws, G, k0, k0 + BB, n2, m1, L.v1_off, L.x_off, L.t1_off);
     rank_update_kernel<<<dim3((unsigned)((m1 + RU_T - 1) / RU_T), (unsigned)((n2 + RU_T - 1) / RU_T), (unsigned)cnt),
-                         256, RU_SMEM, st>>>(ws, L, k0, k0 + BB, m1, n2, L.v1_off, L.x_off);
+                         256, RU_SMEM, st>>>(ws, G, k0, k0 + BB, m1, n2, L.v1_off, L.x_off);
     count_launch(2);
     // ---- right: row panel LQ, C_tr2 = C[k0+BB:, k0+BB:] <- C_tr2 Q2
     PanelArgs p2{L.stride, L.c_off, S, k0, k0 + BB, n2, 1, L.v2_off, S, L.t2_off};
@@ -339,10 +117,10 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     const int m3 = S - k0 - BB;
     if (m3 > 0) {
       xv_kernel<0><<<dim3((unsigned)((m3 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM, st>>>(
-          ws, L, k0 + BB, k0 + BB, m3, n2, L.v2_off, L.x_off, L.t2_off);
+          ws, G, k0 + BB, k0 + BB, m3, n2, L.v2_off, L.x_off, L.t2_off);
       rank_update_kernel<<<dim3((unsigned)((m3 + RU_T - 1) / RU_T), (unsigned)((n2 + RU_T - 1) / RU_T),
                                 (unsigned)cnt),
-                           256, RU_SMEM, st>>>(ws, L, k0 + BB, k0 + BB, m3, n2, L.x_off, L.v2_off);
+                           256, RU_SMEM, st>>>(ws, G, k0 + BB, k0 + BB, m3, n2, L.x_off, L.v2_off);
       count_launch(2);
     }
     BD_CUDA(cudaGetLastError());

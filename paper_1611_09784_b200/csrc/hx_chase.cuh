@@ -31,24 +31,27 @@ __device__ __forceinline__ double2 warp_csum_hx(double2 a, double2 b) {
   return make_double2(warp_sum(a.x * b.x + a.y * b.y), warp_sum(a.x * b.y - a.y * b.x));
 }
 
-template <int BWc>
+// DUAL: D and B tiles staged together; otherwise one tile buffer (B loaded after the D update): half the
+// shared memory per warp, twice the warps (sweeps in flight) per SM.
+template <int BWc, bool DUAL>
 struct ChaseWarpSmem {
-  double2 D[BWc][BWc + 1];  // full Hermitian diagonal block (zero padded)
-  double2 B[BWc][BWc + 1];  // block below (zero padded)
+  double2 D[BWc][BWc + 1];              // full Hermitian diagonal block (zero padded)
+  double2 B[DUAL ? BWc : 1][BWc + 1];   // block below (zero padded)
   double2 v[BWc];           // current reflector (v[0] = 1, zero padded)
   double2 w[BWc];           // two-sided update vector
   double2 vp[BWc];          // next reflector
   double2 z[BWc];           // column coefficients of the B update
 };
 
-template <int NW, int BWc>
+template <int NW, int BWc, bool DUAL>
 __global__ void __launch_bounds__(NW * 32, 1) bulge_chase_pipe_kernel(double2* ws, size_t stride, size_t a_off,
                                                                        size_t dg_off, int N, const int* dims) {
   extern __shared__ __align__(16) unsigned char chase_smem[];
-  ChaseWarpSmem<BWc>* all = reinterpret_cast<ChaseWarpSmem<BWc>*>(chase_smem);
+  ChaseWarpSmem<BWc, DUAL>* all = reinterpret_cast<ChaseWarpSmem<BWc, DUAL>*>(chase_smem);
   volatile int* prog = reinterpret_cast<volatile int*>(all + NW);  // per warp: sweep*65536 + tasks done
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  ChaseWarpSmem<BWc>& S = all[warp];
+  ChaseWarpSmem<BWc, DUAL>& S = all[warp];
+  double2(*Bt)[BWc + 1] = DUAL ? S.B : S.D;
   double2* base = ws + (size_t)blockIdx.x * stride;
   double2* A = base + a_off;
   double* diag = reinterpret_cast<double*>(base + dg_off);
@@ -86,11 +89,13 @@ __global__ void __launch_bounds__(NW * 32, 1) bulge_chase_pipe_kernel(double2* w
           if (c < len && lane >= c && lane < len) cp_async16(&S.D[lane][c], src);
           else S.D[lane][c] = zero;
         }
-        src = colp + len;
+        if (DUAL) {
+          src = colp + len;
 #pragma unroll 4
-        for (int c = 0; c < BWc; ++c, src += lda) {
-          if (c < len && lane < lb) cp_async16(&S.B[lane][c], src);
-          else S.B[lane][c] = zero;
+          for (int c = 0; c < BWc; ++c, src += lda) {
+            if (c < len && lane < lb) cp_async16(&S.B[lane][c], src);
+            else S.B[lane][c] = zero;
+          }
         }
       }
       if (t == 0) {
@@ -152,13 +157,24 @@ __global__ void __launch_bounds__(NW * 32, 1) bulge_chase_pipe_kernel(double2* w
         }
       }
       if (lb > 0) {
+        if (!DUAL) {  // B into the (now free) tile buffer
+          __syncwarp();
+          const double2* src = colp + len;
+#pragma unroll 4
+          for (int c = 0; c < BWc; ++c, src += lda) {
+            if (c < len && lane < lb) cp_async16(&S.D[lane][c], src);
+            else S.D[lane][c] = zero;
+          }
+          cp_async_wait_all();
+          __syncwarp();
+        }
         // ---- B: q = tau B v (lane = row); x0 = column 0 of B - q v^H; H'
         double2 q;
         {
           double2 a0 = zero, a1 = zero;
 #pragma unroll 4
           for (int c = 0; c < BWc; c += 2) {
-            const double2 x0 = S.B[lane][c], v0 = S.v[c], x1 = S.B[lane][c + 1], v1 = S.v[c + 1];
+            const double2 x0 = Bt[lane][c], v0 = S.v[c], x1 = Bt[lane][c + 1], v1 = S.v[c + 1];
             a0.x = fma(x0.x, v0.x, fma(-x0.y, v0.y, a0.x));
             a0.y = fma(x0.x, v0.y, fma(x0.y, v0.x, a0.y));
             a1.x = fma(x1.x, v1.x, fma(-x1.y, v1.y, a1.x));
@@ -166,7 +182,7 @@ __global__ void __launch_bounds__(NW * 32, 1) bulge_chase_pipe_kernel(double2* w
           }
           q = make_double2(tau * (a0.x + a1.x), tau * (a0.y + a1.y));
         }
-        const double2 b00 = S.B[lane][0];
+        const double2 b00 = Bt[lane][0];
         const double2 x0 = make_double2(b00.x - q.x, b00.y - q.y);  // (B - q v^H)[r][0], v_0 = 1
         const double sg2 = warp_sum(x0.x * x0.x + x0.y * x0.y);
         const double2 al = make_double2(__shfl_sync(0xffffffffu, x0.x, 0), __shfl_sync(0xffffffffu, x0.y, 0));
@@ -180,7 +196,7 @@ __global__ void __launch_bounds__(NW * 32, 1) bulge_chase_pipe_kernel(double2* w
           double2 a0 = zero, a1 = zero;
 #pragma unroll 4
           for (int r = 0; r < BWc; r += 2) {
-            const double2 p0 = S.vp[r], b0 = S.B[r][lane], p1 = S.vp[r + 1], b1 = S.B[r + 1][lane];
+            const double2 p0 = S.vp[r], b0 = Bt[r][lane], p1 = S.vp[r + 1], b1 = Bt[r + 1][lane];
             a0.x = fma(p0.x, b0.x, fma(p0.y, b0.y, a0.x));
             a0.y = fma(p0.x, b0.y, fma(-p0.y, b0.x, a0.y));
             a1.x = fma(p1.x, b1.x, fma(p1.y, b1.y, a1.x));
@@ -197,7 +213,7 @@ __global__ void __launch_bounds__(NW * 32, 1) bulge_chase_pipe_kernel(double2* w
 #pragma unroll 4
           for (int c = 0; c < BWc; ++c, dst += lda) {
             const double2 vc = S.v[c], zc = S.z[c];
-            double2 y = S.B[lane][c];
+            double2 y = Bt[lane][c];
             y.x -= (q.x * vc.x + q.y * vc.y) + (vpr.x * zc.x - vpr.y * zc.y);
             y.y -= (q.y * vc.x - q.x * vc.y) + (vpr.x * zc.y + vpr.y * zc.x);
             if (c == 0 && hp.tau != 0.0) y = lane == 0 ? hp.beta : zero;
@@ -219,9 +235,9 @@ __global__ void __launch_bounds__(NW * 32, 1) bulge_chase_pipe_kernel(double2* w
   if (threadIdx.x == 0) diag[d - 1] = A[d - 1 + (size_t)(d - 1) * lda].x;
 }
 
-template <int NW, int BWc>
+template <int NW, int BWc, bool DUAL>
 constexpr size_t chase_smem_bytes() {
-  return NW * sizeof(ChaseWarpSmem<BWc>) + 64;
+  return NW * sizeof(ChaseWarpSmem<BWc, DUAL>) + 64;
 }
 
 }  // namespace hx
