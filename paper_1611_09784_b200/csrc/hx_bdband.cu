@@ -89,6 +89,22 @@ __global__ void __launch_bounds__(256) bd_assemble_kernel(CellDev c, const doubl
 // ------------------------------------------------------------------------------------------------
 bool launch_cluster_panel(double2* ws, const PanelArgs& a, int64_t cnt, cudaStream_t st);
 
+// M[mr0.., mc0..] -= U W^H (m x n, K = 32): 64 x 64 tiles at 2 CTAs/SM (HX_RU_TN=32: 64 x 32 at 4/SM, same speed)
+static void launch_rank_update(double2* ws, const SlabGeom& G, int mr0, int mc0, int m, int n, size_t u_off,
+                               size_t w_off, int64_t cnt, cudaStream_t st) {
+  static const int tn = [] {
+    const char* e = getenv("HX_RU_TN");
+    return e && atoi(e) == 32 ? 32 : 64;
+  }();
+  const unsigned gx = (unsigned)((m + RU_T - 1) / RU_T);
+  if (tn == 64)
+    rank_update_kernel<64><<<dim3(gx, (unsigned)((n + 63) / 64), (unsigned)cnt), 256, ru_smem<64>(), st>>>(
+        ws, G, mr0, mc0, m, n, u_off, w_off);
+  else
+    rank_update_kernel<32><<<dim3(gx, (unsigned)((n + 31) / 32), (unsigned)cnt), 128, ru_smem<32>(), st>>>(
+        ws, G, mr0, mc0, m, n, u_off, w_off);
+}
+
 static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, cudaStream_t st) {
   const int S = L.S;
   const SlabGeom G{L.stride, S, L.c_off};
@@ -104,8 +120,7 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     if (n2 <= 0) break;
     xv_kernel<1><<<dim3((unsigned)((n2 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM, st>>>(
         ws, G, k0, k0 + BB, n2, m1, L.v1_off, L.x_off, L.t1_off);
-    rank_update_kernel<<<dim3((unsigned)((m1 + RU_T - 1) / RU_T), (unsigned)((n2 + RU_T - 1) / RU_T), (unsigned)cnt),
-                         256, RU_SMEM, st>>>(ws, G, k0, k0 + BB, m1, n2, L.v1_off, L.x_off);
+    launch_rank_update(ws, G, k0, k0 + BB, m1, n2, L.v1_off, L.x_off, cnt, st);
     count_launch(2);
     // ---- right: row panel LQ, C_tr2 = C[k0+BB:, k0+BB:] <- C_tr2 Q2
     PanelArgs p2{L.stride, L.c_off, S, k0, k0 + BB, n2, 1, L.v2_off, S, L.t2_off};
@@ -118,9 +133,7 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     if (m3 > 0) {
       xv_kernel<0><<<dim3((unsigned)((m3 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM, st>>>(
           ws, G, k0 + BB, k0 + BB, m3, n2, L.v2_off, L.x_off, L.t2_off);
-      rank_update_kernel<<<dim3((unsigned)((m3 + RU_T - 1) / RU_T), (unsigned)((n2 + RU_T - 1) / RU_T),
-                                (unsigned)cnt),
-                           256, RU_SMEM, st>>>(ws, G, k0 + BB, k0 + BB, m3, n2, L.x_off, L.v2_off);
+      launch_rank_update(ws, G, k0 + BB, k0 + BB, m3, n2, L.x_off, L.v2_off, cnt, st);
       count_launch(2);
     }
     BD_CUDA(cudaGetLastError());
@@ -167,7 +180,8 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
 void bd_init_attributes() {
   cudaFuncSetAttribute(xv_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XV_SMEM);
   cudaFuncSetAttribute(xv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XV_SMEM);
-  cudaFuncSetAttribute(rank_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RU_SMEM);
+  cudaFuncSetAttribute(rank_update_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ru_smem<64>());
+  cudaFuncSetAttribute(rank_update_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ru_smem<32>());
   cudaFuncSetAttribute(bd_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
 #define BD_CHASE_ATTR(NW, DUAL, CL)                                                                        \
   cudaFuncSetAttribute(bd_chase_kernel<NW, BB, DUAL, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, \

@@ -182,26 +182,34 @@ __global__ void __launch_bounds__(128) xv_kernel(double2* ws, SlabGeom g, int ar
 constexpr int RU_T = 64, RU_LD = GBW + 4;
 constexpr size_t RU_SMEM = (size_t)2 * RU_T * RU_LD * sizeof(double2);
 
-static __global__ void __launch_bounds__(256, 2) rank_update_kernel(double2* ws, SlabGeom g, int mr0, int mc0, int m, int n,
-                                                             size_t u_off, size_t w_off) {
+// TN = 64: 8 warps (4 x 2) per 64 x 64 tile, 2 CTAs/SM; TN = 32: 4 warps per 64 x 32 tile, 4 CTAs/SM.
+template <int TN>
+__global__ void __launch_bounds__(2 * TN * 2, TN == 64 ? 2 : 4) rank_update_kernel(double2* ws, SlabGeom g, int mr0,
+                                                                                  int mc0, int m, int n, size_t u_off,
+                                                                                  size_t w_off) {
+  constexpr int NT = 4 * TN;  // threads: 4 row warps x TN/32 column warps
   extern __shared__ __align__(16) double2 ru_sm[];
   double2* Us = ru_sm;                // [RU_T][RU_LD]
-  double2* Ws = ru_sm + RU_T * RU_LD;  // [RU_T][RU_LD]
+  double2* Ws = ru_sm + RU_T * RU_LD;  // [TN][RU_LD]
   double2* base = ws + (size_t)blockIdx.z * g.stride;
   const int ld = g.ld;
   double2* M = base + g.m_off + (size_t)mc0 * ld + mr0;
   const double2* U = base + u_off;
   const double2* W = base + w_off;
-  const int I0 = blockIdx.x * RU_T, J0 = blockIdx.y * RU_T;
+  const int I0 = blockIdx.x * RU_T, J0 = blockIdx.y * TN;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wr = warp & 3, wc = warp >> 2;
 #pragma unroll
-  for (int q = 0; q < RU_T * GBW / 256; ++q) {
-    const int p = tid + 256 * q, r = p & (RU_T - 1), k = p >> 6;
-    const size_t col = (size_t)k * ld;
-    const bool oku = I0 + r < m, okw = J0 + r < n;
-    cp_async16_zfill(Us + r * RU_LD + k, U + (oku ? I0 + r + col : 0), oku);
-    cp_async16_zfill(Ws + r * RU_LD + k, W + (okw ? J0 + r + col : 0), okw);
+  for (int q = 0; q < RU_T * GBW / NT; ++q) {
+    const int p = tid + NT * q, r = p & (RU_T - 1), k = p >> 6;
+    const bool oku = I0 + r < m;
+    cp_async16_zfill(Us + r * RU_LD + k, U + (oku ? I0 + r + (size_t)k * ld : 0), oku);
+  }
+#pragma unroll
+  for (int q = 0; q < TN * GBW / NT; ++q) {
+    const int p = tid + NT * q, r = p % TN, k = p / TN;
+    const bool okw = J0 + r < n;
+    cp_async16_zfill(Ws + r * RU_LD + k, W + (okw ? J0 + r + (size_t)k * ld : 0), okw);
   }
   cp_async_commit();
   CTile acc[2][4];
@@ -243,6 +251,10 @@ static __global__ void __launch_bounds__(256, 2) rank_update_kernel(double2* ws,
       if (r < m && cc < n) M[r + (size_t)cc * ld] = make_double2(acc[rt][ct].re0, acc[rt][ct].im0);
       if (r < m && cc + 1 < n) M[r + (size_t)(cc + 1) * ld] = make_double2(acc[rt][ct].re1, acc[rt][ct].im1);
     }
+}
+template <int TN>
+constexpr size_t ru_smem() {
+  return (size_t)(RU_T + TN) * RU_LD * sizeof(double2);
 }
 
 
