@@ -125,9 +125,9 @@ class Engine:
         return float(bands.energies.min()), float(bands.energies.max())
 
     # -- the batch seam --
-    def _solve_group(self, n: int, q: int, keys, task_ids, ctx=None):
+    def _solve_group(self, n: int, q: int, words, task_ids, ctx=None):
+        """One GPU batch for the (n, q) group: words uint64 [R, w] (task_ids: R ids for error reports)."""
         cell = self.cell(n)
-        words = words_from_keys(keys, cell.supercell.nunits)
         kp = self.kpoints(n, q)
         t0 = time.perf_counter()
         curves, _, status = eval_batch(cell, kp, words, self.grid.lo, self.grid.step, self.grid.npoints,
@@ -144,59 +144,96 @@ class Engine:
                 except Exception as exc:  # noqa: BLE001 - collected with the task id
                     failures.append((task_ids[i], exc))
             raise TaskError(failures)
-        return curves, secs / max(1, len(keys))
+        return curves, secs / max(1, len(words))
 
-    def _solve_groups(self, groups, new_jobs):
-        """Solve every (n, q) group; several groups run concurrently, each from its own thread on its own
-        hx context (the largest tier on the high-priority one), as the reference's parallel_map runs its
-        jobs side by side (runner.py:75-93)."""
-        for n, _ in groups:
+    def _solve_groups(self, jobs):
+        """Solve every (n, q) group {(n, q): (words, task_ids)}; several groups run concurrently, each
+        from its own thread on its own hx context (the largest tier on the high-priority one), as the
+        reference's parallel_map runs its jobs side by side (runner.py:75-93)."""
+        for n, _ in jobs:
             self.cell(n)  # compile cells up front (not thread-safe)
-        args = {g: ([new_jobs[i][2] for i in idxs], [new_jobs[i][3] for i in idxs]) for g, idxs in groups.items()}
-        if len(groups) == 1:
-            g = next(iter(groups))
-            return {g: self._solve_group(g[0], g[1], *args[g])}
-        order = sorted(groups, key=lambda g: -self.cell(g[0]).dim)
+        if len(jobs) == 1:
+            g = next(iter(jobs))
+            return {g: self._solve_group(g[0], g[1], *jobs[g])}
+        order = sorted(jobs, key=lambda g: -self.cell(g[0]).dim)
         with ThreadPoolExecutor(max_workers=len(order)) as ex:
-            futs = {g: ex.submit(self._solve_group, g[0], g[1], *args[g], _lib.Device.lane(self.device, lane))
+            futs = {g: ex.submit(self._solve_group, g[0], g[1], *jobs[g], _lib.Device.lane(self.device, lane))
                     for lane, g in enumerate(order)}
             return {g: f.result() for g, f in futs.items()}
 
+    def _evaluate_words(self, groups, task_ids):
+        """Vectorised batch seam.  groups: list of (n, q, words uint64 [R, w]) in request order;
+        task_ids(i_group, rows) -> ids of those rows (only built for error reports).  Dedup on
+        (n, q, mask) against the run cache and within the batch (np.unique over the rows instead of a
+        per-request dict), one GPU batch per group for the new masks.  Returns per group (curves [R, npts],
+        per_job [R]) in row order, the hit count and the nominal work spent (runner.py:206-244)."""
+        npts = self.grid.npoints
+        plans, jobs = [], {}
+        hits = 0
+        for gi, (n, q, words) in enumerate(groups):
+            words = np.ascontiguousarray(words, dtype=np.uint64)
+            R = words.shape[0]
+            if self.dedup and R:
+                uniq, inv = np.unique(words, axis=0, return_inverse=True)
+                inv = inv.reshape(-1)
+                keys = [(n, q, row.tobytes()) for row in uniq]
+                cached = np.fromiter((k in self._cache for k in keys), dtype=bool, count=len(keys))
+                hits += (R - len(uniq)) + int(cached.sum())
+            else:
+                uniq, inv, keys = words, np.arange(R), None
+                cached = np.zeros(R, dtype=bool)
+            new = np.flatnonzero(~cached)
+            if len(new):
+                if (n, q) in jobs:  # two groups with the same (n, q): solve them as one batch
+                    w0, ids0 = jobs[(n, q)]
+                    jobs[(n, q)] = (np.concatenate([w0, uniq[new]]), ids0 + task_ids(gi, new, inv))
+                else:
+                    jobs[(n, q)] = (uniq[new], task_ids(gi, new, inv))
+            plans.append((n, q, uniq, inv, keys, cached, new))
+        solved = self._solve_groups(jobs) if jobs else {}
+        used = {g: 0 for g in jobs}
+        out, spent = [], 0.0
+        for n, q, uniq, inv, keys, cached, new in plans:
+            cu = np.empty((len(uniq), npts))
+            pj = np.empty(len(uniq))
+            if len(new):
+                curves, per_job = solved[(n, q)]
+                k0 = used[(n, q)]
+                used[(n, q)] = k0 + len(new)
+                cu[new] = curves[k0:k0 + len(new)]
+                pj[new] = per_job
+                spent += per_job * len(new)
+                if self.dedup:
+                    for i in new:
+                        self._cache[keys[i]] = (cu[i], per_job)
+            for i in np.flatnonzero(cached):
+                cu[i], pj[i] = self._cache[keys[i]]
+            out.append((cu[inv], pj[inv]))
+        return out, hits, spent
+
     def evaluate_masks(self, requests):
         """Dedup on (n, q, mask) against the run cache and within the batch; solve the new jobs of each
-        (n, q) group in one GPU batch; results in request order (runner.py:206-244)."""
-        placement, new_jobs, owners = [], [], {}
-        hits = 0
-        for n, q, mask, task_id in requests:
-            key = (n, q, mask)
-            if self.dedup and key in self._cache:
-                hits += 1
-                placement.append(("cache", key))
-                continue
-            if self.dedup and key in owners:
-                hits += 1
-                placement.append(("job", owners[key]))
-                continue
-            idx = len(new_jobs)
-            if self.dedup:
-                owners[key] = idx
-            new_jobs.append((n, q, mask, task_id))
-            placement.append(("job", idx))
-        results = [None] * len(new_jobs)
-        groups: dict = {}
-        for idx, (n, q, mask, tid) in enumerate(new_jobs):
-            groups.setdefault((n, q), []).append(idx)
-        spent = 0.0
-        solved = self._solve_groups(groups, new_jobs)
-        for (n, q), idxs in groups.items():
-            curves, per_job = solved[(n, q)]
-            for row, i in enumerate(idxs):
-                results[i] = (curves[row], per_job)
-            spent += per_job * len(idxs)
-        if self.dedup:
-            for (n, q, mask, _), res in zip(new_jobs, results):
-                self._cache[(n, q, mask)] = res
-        out = [self._cache[ref] if kind == "cache" else results[ref] for kind, ref in placement]
+        (n, q) group in one GPU batch; results [(curve, per_job)] in request order (runner.py:206-244)."""
+        order: dict = {}
+        for idx, (n, q, mask, tid) in enumerate(requests):
+            order.setdefault((n, q), []).append(idx)
+        groups, rows_of = [], []
+        for (n, q), idxs in order.items():
+            nunits = self.supercell(n).nunits
+            groups.append((n, q, words_from_keys([requests[i][2] for i in idxs], nunits)))
+            rows_of.append(idxs)
+
+        def ids(gi, new, inv):
+            first = {}
+            for r, u in enumerate(inv):
+                first.setdefault(int(u), r)
+            return [requests[rows_of[gi][first[int(u)]]][3] for u in new]
+
+        res, hits, spent = self._evaluate_words(groups, ids)
+        out = [None] * len(requests)
+        for (cu, pj), idxs in zip(res, rows_of):
+            for r, i in enumerate(idxs):
+                out[i] = (cu[r], float(pj[r]))
         return out, hits, spent
 
     # -- level sampling --
@@ -213,25 +250,31 @@ class Engine:
         rank, _ = self.shard
         m0 = rank * nsamples
         words = sample_masks(sc.nunits, p_vac, self.master_seed, stream, m0, nsamples)
-        keys = keys_from_words(words)
-        requests = [(n, q, k, (level, m0 + m, "Q")) for m, k in enumerate(keys)]
+        groups = [(n, q, words)]
         if with_cv:
             part = partition_quarters(sc)
             nsub = n // 2
-            qsub = self.q_of(nsub)
             sub = restrict_words(words, part)  # [M, 4, w]
-            subkeys = keys_from_words(sub.reshape(nsamples * 4, -1))
-            for m in range(nsamples):
-                for r in range(4):
-                    requests.append((nsub, qsub, subkeys[m * 4 + r], (level, m0 + m, f"CV{r + 1}")))
-        results, hits, spent = self.evaluate_masks(requests)
+            groups.append((nsub, self.q_of(nsub), sub.reshape(nsamples * 4, -1)))
+
+        def ids(gi, new, inv):  # task ids (level, replicate, "Q" / "CVr") of the first row of each new mask
+            first = np.full(inv.max() + 1 if len(inv) else 0, -1)
+            for r in range(len(inv) - 1, -1, -1):
+                first[inv[r]] = r
+            rows = first[new]
+            if gi == 0:
+                return [(level, m0 + int(r), "Q") for r in rows]
+            return [(level, m0 + int(r) // 4, f"CV{int(r) % 4 + 1}") for r in rows]
+
+        res, hits, spent = self._evaluate_words(groups, ids)
         npts = self.grid.npoints
-        full = np.stack([results[m][0] for m in range(nsamples)]) if nsamples else np.zeros((0, npts))
-        nominal = sum(results[m][1] for m in range(nsamples))
+        full, pj = res[0]
+        nominal = float(pj.sum())
         quarters = None
         if with_cv:
-            quarters = np.stack([results[nsamples + i][0] for i in range(4 * nsamples)]).reshape(nsamples, 4, npts)
-            nominal += sum(results[nsamples + i][1] for i in range(4 * nsamples))
+            qc, qpj = res[1]
+            quarters = qc.reshape(nsamples, 4, npts)
+            nominal += float(qpj.sum())
         terms, mean, var = level_moments(full, quarters, self.device)
         terms = terms.cpu().numpy()
         self.io_bytes[0] += full.nbytes + (0 if quarters is None else quarters.nbytes)
