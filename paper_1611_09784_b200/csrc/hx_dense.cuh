@@ -173,10 +173,17 @@ struct Reflector {
   double e2;      // |beta|^2 = sigma^2: squared off-diagonal of the tridiagonal
 };
 
+// Columns whose squared norm is below HX_REFLECTOR_TINY are treated as exactly zero (identity reflector):
+// their entries (< 1e-100 for O(1) matrices) are noise left by earlier reflections, and below ~1e-154 the
+// squares underflow into the denormal range, where the norm loses its precision and a reflector built
+// from it is no longer unitary (tau inconsistent with |v|^2) - measured: 6e-8 loss of unitarity in a
+// row panel of a vacancy-rich graphene cell.
+#define HX_REFLECTOR_TINY 1e-200
+
 __device__ __forceinline__ Reflector make_reflector(double2 alpha, double sigma2) {
   Reflector h;
   h.e2 = sigma2;
-  if (sigma2 == 0.0) {
+  if (!(sigma2 >= HX_REFLECTOR_TINY)) {
     h.tau = 0.0;
     h.scale = make_double2(0.0, 0.0);
     return h;
@@ -200,14 +207,24 @@ struct QuickReflector {
 };
 __device__ __forceinline__ QuickReflector quick_reflector(double2 alpha, double sig2) {
   QuickReflector h;
-  if (!(sig2 > 0.0)) {
+  if (!(sig2 >= HX_REFLECTOR_TINY)) {
     h.tau = 0.0;
     h.scale = make_double2(0.0, 0.0);
     h.beta = make_double2(0.0, 0.0);
     return h;
   }
-  const double rs = rsqrt(sig2), sigma = sig2 * rs;
   const double a2 = alpha.x * alpha.x + alpha.y * alpha.y;
+  if (a2 < 1e-280 && (alpha.x != 0.0 || alpha.y != 0.0)) {
+    // (near-)underflow: squares lose their precision / the phase of alpha; divide the careful way
+    const double sigma = sqrt(sig2), aa = hypot(alpha.x, alpha.y);
+    const double2 ph = aa > 0.0 ? make_double2(alpha.x / aa, alpha.y / aa) : make_double2(1.0, 0.0);
+    const double mag = aa + sigma;
+    h.tau = mag / sigma;
+    h.scale = make_double2(ph.x / mag, -ph.y / mag);
+    h.beta = make_double2(-ph.x * sigma, -ph.y * sigma);
+    return h;
+  }
+  const double rs = rsqrt(sig2), sigma = sig2 * rs;
   double2 ph = make_double2(1.0, 0.0);
   double aa = 0.0;
   if (a2 > 0.0) {

@@ -166,10 +166,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(32 * GR, GR == 8 &&
     }
     // ---- owners of column j: reflector, publish v, keep (beta, V) in registers
     if (c == j) {
-      const Reflector h = make_reflector(alpha, sig2);
-      const double sg = sqrt(sig2), aa = hypot(alpha.x, alpha.y);
-      const double2 ph = aa > 0.0 ? make_double2(alpha.x / aa, alpha.y / aa) : make_double2(1.0, 0.0);
-      const double2 beta = make_double2(-ph.x * sg, -ph.y * sg);
+      const QuickReflector h = quick_reflector(alpha, sig2);
+      const double2 beta = h.beta;
 #pragma unroll
       for (int r = 0; r < RPT; ++r) {
         const int li = g + GR * r;

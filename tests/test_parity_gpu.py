@@ -165,9 +165,12 @@ def test_all_vacant_gives_zero_curve_and_plateau():
         assert np.allclose(sset.full[:, -1], 2.0 * n * n / eng.supercell(n).area, atol=1e-9)
 
 
-@pytest.mark.parametrize("nu,q,p", [(10, 2, 0.2), (11, 1, 0.3), (12, 1, 0.05), (16, 2, 0.1)])
+@pytest.mark.parametrize("nu,q,p", [(10, 2, 0.2), (11, 1, 0.3), (12, 1, 0.05), (16, 2, 0.1), (12, 1, 0.5),
+                                    (13, 1, 0.4), (14, 1, 0.45), (17, 1, 0.35)])
 def test_bipartite_banded_tier_matches_oracle(nu, q, p):
-    """graphene N = 2nu^2 > 160 goes through the bipartite banded tier (nA != nB after vacancies)."""
+    """graphene N = 2nu^2 > 160 goes through the bipartite banded tier (nA != nB after vacancies).  High
+    vacancy rates leave exactly-zero rows/columns whose reflections produce ever smaller noise columns
+    (down to the denormal range): the reflectors must stay unitary (HX_REFLECTOR_TINY)."""
     model = hx.GrapheneNNModel()
     spec = model.lattice_spec()
     sc = hx.build_supercell(spec, nu)
@@ -185,6 +188,32 @@ def test_bipartite_banded_tier_matches_oracle(nu, q, p):
         ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
         d = ref.shape[1]
         assert np.all(np.isnan(eigs[m, :, d:]))
+        assert np.max(np.abs(eigs[m, :, :d] - ref)) <= EIG_TOL * (ref.max() - ref.min())
+        rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), lo, hi, npts, 0.01, ocell.area)
+        np.testing.assert_allclose(curves[m], rc, rtol=0, atol=IDOS_TOL)
+
+
+@pytest.mark.parametrize("kind,nu,q,p", [("table", 4, 2, 0.4), ("table", 5, 1, 0.5), ("graphene", 8, 2, 0.5),
+                                         ("graphene", 4, 3, 0.6), ("graphene", 6, 2, 0.45)])
+def test_high_vacancy_tiers_match_oracle(kind, nu, q, p):
+    """Every tier at high vacancy rates (exact zero rows/columns -> noise-only reflector columns): the
+    Hermitian banded tier (table nu >= 4), the shared-memory bidiagonalisation (CTA: S = 64, warp: S <= 32)."""
+    model = hx.load_coupling_table(TABLE) if kind == "table" else hx.GrapheneNNModel()
+    om = O.parse_table(str(TABLE)) if kind == "table" else O.graphene_model()
+    spec = model.lattice_spec()
+    sc = hx.build_supercell(spec, nu)
+    cell = hx.compile_cell(model, sc)
+    kp = hx.make_bz_grid(spec, nu, q, "reduced").kpoints
+    from paper_1611_09784_b200.sampling import sample_masks
+
+    words = sample_masks(sc.nunits, p, 91, 2, 0, 3)
+    lo, hi, npts = (-2.952, 4.760, 201) if kind == "table" else (-6.580201874549387, 14.863393148450246, 201)
+    curves, eigs, status = eval_batch(cell, kp, words, lo, (hi - lo) / (npts - 1), npts, 0.01, want_eigs=True)
+    assert (status == 0).all()
+    ocell = O.make_cell(om, nu)
+    for m in range(len(words)):
+        ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
+        d = ref.shape[1]
         assert np.max(np.abs(eigs[m, :, :d] - ref)) <= EIG_TOL * (ref.max() - ref.min())
         rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), lo, hi, npts, 0.01, ocell.area)
         np.testing.assert_allclose(curves[m], rc, rtol=0, atol=IDOS_TOL)
