@@ -123,8 +123,10 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
       HX_PROF_MARK(0);
       if (i > 0) {
         const int need = (i - 1) * 65536 + min(t + 2, prev_tasks);
+        // latency-bound launches (clusters / many sweeps per matrix) poll tightly, throughput-bound ones
+        // back off so that waiting warps do not steal issue slots from working ones
         if (lane == 0)
-          while (*pflag < need) __nanosleep(20);
+          while (*pflag < need) __nanosleep(CL > 1 || NW >= 6 ? 20 : 200);
         __syncwarp();
         if (CL > 1) __threadfence();
         else __threadfence_block();
@@ -135,7 +137,15 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
       HX_PROF_MARK(1);  // wait for the previous sweep
       // ---- X and Y tiles (asynchronous, zero-padded); blk = &C[s + lane][s], columns ld apart
       double2* const blk = C + ((size_t)s * ld + s + lane);
-      {
+      if (len == BWc && (!DUAL || lb == BWc)) {  // full tiles: no padding predicates
+        const double2* src = blk;
+#pragma unroll 8
+        for (int cc = 0; cc < BWc; ++cc, src += ld) bd_cp_async16<L2ONLY>(&W.X[lane][cc], src);
+        if (DUAL) {
+#pragma unroll 8
+          for (int cc = 0; cc < BWc; ++cc, src += ld) bd_cp_async16<L2ONLY>(&W.Y[lane][cc], src);
+        }
+      } else {
         const double2* src = blk;
 #pragma unroll 4
         for (int cc = 0; cc < BWc; ++cc, src += ld) {
@@ -231,10 +241,15 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
         if (!DUAL) {  // Y into the (now free) tile buffer
           __syncwarp();
           const double2* src = blk + (size_t)len * ld;
+          if (len == BWc && lb == BWc) {
+#pragma unroll 8
+            for (int cc = 0; cc < BWc; ++cc, src += ld) bd_cp_async16<L2ONLY>(&W.X[lane][cc], src);
+          } else {
 #pragma unroll 4
-          for (int cc = 0; cc < BWc; ++cc, src += ld) {
-            if (lane < len && cc < lb) bd_cp_async16<L2ONLY>(&W.X[lane][cc], src);
-            else W.X[lane][cc] = zero;
+            for (int cc = 0; cc < BWc; ++cc, src += ld) {
+              if (lane < len && cc < lb) bd_cp_async16<L2ONLY>(&W.X[lane][cc], src);
+              else W.X[lane][cc] = zero;
+            }
           }
           bd_cp_async_wait_all();
           __syncwarp();
