@@ -232,29 +232,32 @@ static __device__ void bidiag_tgk_warp(double2* M, int lm, int rows, int cols, d
       for (int i = j + lane; i < rows; i += 32) u[i] = i == j ? make_double2(1.0, 0.0) : cmul(colj[i], h.scale);
       __syncwarp();
       if (h.tau != 0.0)
-        for (int cc = j + 1 + lane; cc < cols; cc += 32) {
-          double2* col = M + (size_t)cc * lm;
+        // two columns per lane (c0, c0 + 32): the u loads are shared and the two dot chains interleave
+        for (int c0 = j + 1 + lane; c0 < cols; c0 += 64) {
+          const bool has1 = c0 + 32 < cols;
+          double2* col0 = M + (size_t)c0 * lm;
+          double2* col1 = M + (size_t)(has1 ? c0 + 32 : c0) * lm;
           double2 a0 = make_double2(0.0, 0.0), a1 = a0;
-          int i = j;
-          for (; i + 1 < rows; i += 2) {
-            const double2 v0 = u[i], x0 = col[i], v1 = u[i + 1], x1 = col[i + 1];
-            a0.x = fma(v0.x, x0.x, fma(v0.y, x0.y, a0.x));
-            a0.y = fma(v0.x, x0.y, fma(-v0.y, x0.x, a0.y));
-            a1.x = fma(v1.x, x1.x, fma(v1.y, x1.y, a1.x));
-            a1.y = fma(v1.x, x1.y, fma(-v1.y, x1.x, a1.y));
+#pragma unroll 2
+          for (int i = j; i < rows; ++i) {
+            const double2 v = u[i], x0 = col0[i], x1 = col1[i];
+            a0.x = fma(v.x, x0.x, fma(v.y, x0.y, a0.x));
+            a0.y = fma(v.x, x0.y, fma(-v.y, x0.x, a0.y));
+            a1.x = fma(v.x, x1.x, fma(v.y, x1.y, a1.x));
+            a1.y = fma(v.x, x1.y, fma(-v.y, x1.x, a1.y));
           }
-          if (i < rows) {
-            const double2 v0 = u[i], x0 = col[i];
-            a0.x = fma(v0.x, x0.x, fma(v0.y, x0.y, a0.x));
-            a0.y = fma(v0.x, x0.y, fma(-v0.y, x0.x, a0.y));
-          }
-          const double2 sc = make_double2(h.tau * (a0.x + a1.x), h.tau * (a0.y + a1.y));
-          for (i = j; i < rows; ++i) {
+          const double2 s0 = make_double2(h.tau * a0.x, h.tau * a0.y);
+          const double2 s1 = make_double2(has1 ? h.tau * a1.x : 0.0, has1 ? h.tau * a1.y : 0.0);
+#pragma unroll 2
+          for (int i = j; i < rows; ++i) {
             const double2 v = u[i];
-            double2 x = col[i];
-            x.x = fma(-v.x, sc.x, fma(v.y, sc.y, x.x));
-            x.y = fma(-v.x, sc.y, fma(-v.y, sc.x, x.y));
-            col[i] = x;
+            double2 x0 = col0[i], x1 = col1[i];
+            x0.x = fma(-v.x, s0.x, fma(v.y, s0.y, x0.x));
+            x0.y = fma(-v.x, s0.y, fma(-v.y, s0.x, x0.y));
+            x1.x = fma(-v.x, s1.x, fma(v.y, s1.y, x1.x));
+            x1.y = fma(-v.x, s1.y, fma(-v.y, s1.x, x1.y));
+            col0[i] = x0;
+            if (has1) col1[i] = x1;
           }
         }
       __syncwarp();
@@ -277,28 +280,31 @@ static __device__ void bidiag_tgk_warp(double2* M, int lm, int rows, int cols, d
       }
       __syncwarp();
       if (h.tau != 0.0)
-        for (int r = j + 1 + lane; r < rows; r += 32) {
-          double2 a0r = make_double2(0.0, 0.0), a1r = a0r;
-          int cc = j + 1;
-          for (; cc + 1 < cols; cc += 2) {
-            const double2 x0 = M[r + (size_t)cc * lm], b0 = u[cc], x1 = M[r + (size_t)(cc + 1) * lm], b1 = u[cc + 1];
-            a0r.x = fma(x0.x, b0.x, fma(-x0.y, b0.y, a0r.x));
-            a0r.y = fma(x0.x, b0.y, fma(x0.y, b0.x, a0r.y));
-            a1r.x = fma(x1.x, b1.x, fma(-x1.y, b1.y, a1r.x));
-            a1r.y = fma(x1.x, b1.y, fma(x1.y, b1.x, a1r.y));
+        // two rows per lane (r0, r0 + 32), shared u loads, interleaved chains
+        for (int r0 = j + 1 + lane; r0 < rows; r0 += 64) {
+          const bool has1 = r0 + 32 < rows;
+          const int r1 = has1 ? r0 + 32 : r0;
+          double2 a0 = make_double2(0.0, 0.0), a1 = a0;
+#pragma unroll 2
+          for (int cc = j + 1; cc < cols; ++cc) {
+            const double2 b = u[cc], x0 = M[r0 + (size_t)cc * lm], x1 = M[r1 + (size_t)cc * lm];
+            a0.x = fma(x0.x, b.x, fma(-x0.y, b.y, a0.x));
+            a0.y = fma(x0.x, b.y, fma(x0.y, b.x, a0.y));
+            a1.x = fma(x1.x, b.x, fma(-x1.y, b.y, a1.x));
+            a1.y = fma(x1.x, b.y, fma(x1.y, b.x, a1.y));
           }
-          if (cc < cols) {
-            const double2 x0 = M[r + (size_t)cc * lm], b0 = u[cc];
-            a0r.x = fma(x0.x, b0.x, fma(-x0.y, b0.y, a0r.x));
-            a0r.y = fma(x0.x, b0.y, fma(x0.y, b0.x, a0r.y));
-          }
-          const double2 w = make_double2(h.tau * (a0r.x + a1r.x), h.tau * (a0r.y + a1r.y));
-          for (cc = j + 1; cc < cols; ++cc) {
+          const double2 w0 = make_double2(h.tau * a0.x, h.tau * a0.y);
+          const double2 w1 = make_double2(has1 ? h.tau * a1.x : 0.0, has1 ? h.tau * a1.y : 0.0);
+#pragma unroll 2
+          for (int cc = j + 1; cc < cols; ++cc) {
             const double2 b = u[cc];
-            double2 x = M[r + (size_t)cc * lm];
-            x.x = fma(-w.x, b.x, fma(-w.y, b.y, x.x));
-            x.y = fma(-w.y, b.x, fma(w.x, b.y, x.y));
-            M[r + (size_t)cc * lm] = x;
+            double2 x0 = M[r0 + (size_t)cc * lm], x1 = M[r1 + (size_t)cc * lm];
+            x0.x = fma(-w0.x, b.x, fma(-w0.y, b.y, x0.x));
+            x0.y = fma(-w0.y, b.x, fma(w0.x, b.y, x0.y));
+            x1.x = fma(-w1.x, b.x, fma(-w1.y, b.y, x1.x));
+            x1.y = fma(-w1.y, b.x, fma(w1.x, b.y, x1.y));
+            M[r0 + (size_t)cc * lm] = x0;
+            if (has1) M[r1 + (size_t)cc * lm] = x1;
           }
         }
       __syncwarp();
