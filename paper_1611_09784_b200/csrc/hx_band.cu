@@ -339,15 +339,14 @@ __global__ void __launch_bounds__(256) band_copy_kernel(const double2* __restric
 constexpr size_t W_ROWS_SMEM = (size_t)(2 * BW * BW + 64 * (BW + 1)) * sizeof(double2);
 
 void band_init_attributes() {
-  cudaFuncSetAttribute(w_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W_ROWS_SMEM);
+  set_smem_attr(w_rows_kernel, (int)W_ROWS_SMEM);
   cudaFuncSetAttribute(panel_qr_reg_kernel<16, 8, 32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  cudaFuncSetAttribute(band_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-  cudaFuncSetAttribute(her2k_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HK_SMEM);
-  cudaFuncSetAttribute(xv_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XV_SMEM);
-  cudaFuncSetAttribute(xv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XV_SMEM);
+  set_smem_attr(band_assemble_kernel, 64 * 1024);
+  set_smem_attr(her2k_kernel, (int)HK_SMEM);
+  set_smem_attr(xv_kernel<0>, (int)XV_SMEM);
+  set_smem_attr(xv_kernel<1>, (int)XV_SMEM);
 #define HCHASE_ATTR(NW)                                                                           \
-  cudaFuncSetAttribute(bulge_chase_pipe_kernel<NW, BW, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                       (int)chase_smem_bytes<NW, BW, false>())
+  set_smem_attr(bulge_chase_pipe_kernel<NW, BW, false>, chase_smem_bytes<NW, BW, false>())
   HCHASE_ATTR(1);
   HCHASE_ATTR(2);
   HCHASE_ATTR(3);

@@ -45,7 +45,7 @@ const char* bd_last_error() { return g_bd_err.c_str(); }
   } while (0)
 
 struct BdWs {
-  size_t c_off, v1_off, v2_off, x_off, t1_off, t2_off, tgk_off;  // double2 units
+  size_t c_off, v1_off, v2_off, x_off, z_off, t1_off, t2_off, tgk_off;  // double2 units
   size_t stride;
   int S;
   static BdWs make(int S) {
@@ -55,7 +55,8 @@ struct BdWs {
     w.v1_off = (size_t)S * S;
     w.v2_off = w.v1_off + (size_t)S * BB;
     w.x_off = w.v2_off + (size_t)S * BB;
-    w.t1_off = w.x_off + (size_t)S * BB;
+    w.z_off = w.x_off + (size_t)S * BB;
+    w.t1_off = w.z_off + (size_t)S * BB;
     w.t2_off = w.t1_off + (size_t)BB * BB;
     w.tgk_off = w.t2_off + (size_t)BB * BB;  // diag[2S] + e2[2S] doubles = 2S double2
     w.stride = (w.tgk_off + (size_t)2 * S + 16 + 15) & ~(size_t)15;
@@ -105,9 +106,29 @@ static void launch_rank_update(double2* ws, const SlabGeom& G, int mr0, int mc0,
         ws, G, mr0, mc0, m, n, u_off, w_off);
 }
 
+// Stage 1.  Default: per step  L-panel -> X1 = (C_tr^H V1) T1 -> C_tr -= V1 X1^H -> R-panel ->
+// Z = (C_tr2 V2) T2 -> C_tr2 -= Z V2^H.  Optional (HX_FUSED_UPDATE=1) the trailing updates are fused into the
+// next product (one pass over the trailing matrix per side instead of two):
+//   L-panel(k0) -> V1, T1
+//   X1 = (C[k0:, k0+32:]^H V1) T1        (xv<1>; from step 2 on it first applies the pending right
+//                                         update of the previous step to the chunks it streams)
+//   C[k0:k0+32, k0+32:] -= V1[:32] X1^H   (the 32 rows the row panel needs)
+//   R-panel(k0) -> V2, T2
+//   Z = (C[k0+32:, k0+32:] V2) T2         (xv<0>, applying the pending left update V1[32:] X1^H on the fly)
+//   C[k0+32:, k0+32:k0+64] -= Z V2[:32]^H (the 32 columns the next column panel needs)
+// and C[k0+32:, k0+64:] -= Z V2[32:]^H stays pending for the next step's xv<1>.
 static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, cudaStream_t st) {
   const int S = L.S;
   const SlabGeom G{L.stride, S, L.c_off};
+  // HX_FUSED_UPDATE=1: fold the trailing rank updates into the next product (one pass over the trailing
+  // matrix per side).  Correct, but measured ~10% slower than separate rank updates on sm_100a (the fused
+  // kernel needs ~210 registers: 2 CTAs/SM instead of 3, and the DMMA pipe idles during the update), so
+  // it is off by default.
+  static const bool fused = [] {
+    const char* e = getenv("HX_FUSED_UPDATE");
+    return e && e[0] == '1';
+  }();
+  bool pend = false;  // right update of the previous step pending on columns >= k0 + 32
   for (int k0 = 0; k0 < S; k0 += BB) {
     const int m1 = S - k0, n2 = S - k0 - BB;
     // ---- left: column panel QR, C_tr = C[k0:, k0+BB:] <- Q1^H C_tr
@@ -118,11 +139,15 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     }
     count_launch();
     if (n2 <= 0) break;
-    xv_kernel<1><<<dim3((unsigned)((n2 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM, st>>>(
-        ws, G, k0, k0 + BB, n2, m1, L.v1_off, L.x_off, L.t1_off);
-    launch_rank_update(ws, G, k0, k0 + BB, m1, n2, L.v1_off, L.x_off, cnt, st);
+    const dim3 gx1((unsigned)((n2 + XV_TM - 1) / XV_TM), (unsigned)cnt);
+    if (!pend)
+      xv_kernel<1><<<gx1, 128, XV_SMEM, st>>>(ws, G, k0, k0 + BB, n2, m1, L.v1_off, L.x_off, L.t1_off);
+    else  // pending: C[r][c] -= Z[r - k0] conj(V2[32 + c - (k0 + 32)])
+      xv_kernel<1, true><<<gx1, 128, XV_SMEM_UPD, st>>>(ws, G, k0, k0 + BB, n2, m1, L.v1_off, L.x_off, L.t1_off,
+                                                         L.v2_off + BB, L.z_off);
+    launch_rank_update(ws, G, k0, k0 + BB, fused ? std::min(BB, m1) : m1, n2, L.v1_off, L.x_off, cnt, st);
     count_launch(2);
-    // ---- right: row panel LQ, C_tr2 = C[k0+BB:, k0+BB:] <- C_tr2 Q2
+    // ---- right: row panel LQ of the (updated) rows k0..k0+BB, C_tr2 = C[k0+BB:, k0+BB:] <- C_tr2 Q2
     PanelArgs p2{L.stride, L.c_off, S, k0, k0 + BB, n2, 1, L.v2_off, S, L.t2_off};
     if (!launch_cluster_panel(ws, p2, cnt, st)) {
       g_bd_err = "panel does not fit the cluster shared memory";
@@ -130,11 +155,19 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     }
     count_launch();
     const int m3 = S - k0 - BB;
-    if (m3 > 0) {
+    pend = false;
+    if (m3 > 0 && !fused) {
       xv_kernel<0><<<dim3((unsigned)((m3 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM, st>>>(
-          ws, G, k0 + BB, k0 + BB, m3, n2, L.v2_off, L.x_off, L.t2_off);
-      launch_rank_update(ws, G, k0 + BB, k0 + BB, m3, n2, L.x_off, L.v2_off, cnt, st);
+          ws, G, k0 + BB, k0 + BB, m3, n2, L.v2_off, L.z_off, L.t2_off);
+      launch_rank_update(ws, G, k0 + BB, k0 + BB, m3, n2, L.z_off, L.v2_off, cnt, st);
       count_launch(2);
+    } else if (m3 > 0) {
+      // Z = (C_tr2 V2) T2 with the pending left update C[r][c] -= V1[32 + r - (k0+32)] conj(X1[c - (k0+32)])
+      xv_kernel<0, true><<<dim3((unsigned)((m3 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM_UPD, st>>>(
+          ws, G, k0 + BB, k0 + BB, m3, n2, L.v2_off, L.z_off, L.t2_off, L.v1_off + BB, L.x_off);
+      launch_rank_update(ws, G, k0 + BB, k0 + BB, m3, std::min(BB, n2), L.z_off, L.v2_off, cnt, st);
+      count_launch(2);
+      pend = n2 > BB;
     }
     BD_CUDA(cudaGetLastError());
   }
@@ -178,14 +211,15 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
 }
 
 void bd_init_attributes() {
-  cudaFuncSetAttribute(xv_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XV_SMEM);
-  cudaFuncSetAttribute(xv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XV_SMEM);
-  cudaFuncSetAttribute(rank_update_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ru_smem<64>());
-  cudaFuncSetAttribute(rank_update_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ru_smem<32>());
-  cudaFuncSetAttribute(bd_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+  set_smem_attr(xv_kernel<0>, (int)XV_SMEM);
+  set_smem_attr(xv_kernel<1>, (int)XV_SMEM);
+  set_smem_attr(xv_kernel<0, true>, XV_SMEM_UPD);
+  set_smem_attr(xv_kernel<1, true>, XV_SMEM_UPD);
+  set_smem_attr(rank_update_kernel<64>, (int)ru_smem<64>());
+  set_smem_attr(rank_update_kernel<32>, (int)ru_smem<32>());
+  set_smem_attr(bd_assemble_kernel, 140 * 1024);
 #define BD_CHASE_ATTR(NW, DUAL, CL)                                                                        \
-  cudaFuncSetAttribute(bd_chase_kernel<NW, BB, DUAL, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                       (int)bd_chase_smem<NW, BB, DUAL>())
+  set_smem_attr(bd_chase_kernel<NW, BB, DUAL, CL>, bd_chase_smem<NW, BB, DUAL>())
   BD_CHASE_ATTR(1, false, 1);
   BD_CHASE_ATTR(2, false, 1);
   BD_CHASE_ATTR(6, true, 1);

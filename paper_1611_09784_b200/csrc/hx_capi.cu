@@ -185,12 +185,10 @@ int hx_ctx_create_priority(int32_t device, int32_t priority, hx_ctx** out) {
     const char* bt = getenv("HX_BIDIAG_THREADS");
     if (bt && bt[0]) ctx->bidiag_threads = atoi(bt);
   }
-  cudaFuncSetAttribute(hx::small_bidiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  hx::set_smem_attr(hx::small_bidiag_kernel, 200 * 1024);
   ctx->ws_budget = std::min(ctx->ws_budget, freeb / 3);
-  cudaFuncSetAttribute(hx::small_tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)hx::small_tridiag_smem(HX_SMEM_MAX_N));
-  cudaFuncSetAttribute(hx::eigvalsh_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)hx::small_tridiag_smem(HX_SMEM_MAX_N));
+  hx::set_smem_attr(hx::small_tridiag_kernel, (int)hx::small_tridiag_smem(HX_SMEM_MAX_N));
+  hx::set_smem_attr(hx::eigvalsh_small_kernel, (int)hx::small_tridiag_smem(HX_SMEM_MAX_N));
   hx::band_init_attributes();
   hx::bd_init_attributes();
   *out = ctx;
@@ -461,7 +459,7 @@ int hx_assemble_device(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_
   HX_CUDA(cudaMemcpyAsync(ctx->kpts.p, kpoints, (size_t)nk * 16, cudaMemcpyHostToDevice, st));
   const size_t smem = (size_t)cell->dev.N * sizeof(int);
   if (smem > 200 * 1024) return fail(HX_E_RANGE, "hx_assemble_device: N too large");
-  cudaFuncSetAttribute(hx::assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  hx::set_smem_attr(hx::assemble_kernel, 200 * 1024);
   hx::assemble_kernel<<<(unsigned)(nmasks * nk), 256, smem, st>>>(
       cell->dev, static_cast<const double2*>(ctx->kpts.p), nk, d_masks, reinterpret_cast<double2*>(d_H),
       reinterpret_cast<double2*>(d_S), reinterpret_cast<int*>(d_dims));

@@ -67,4 +67,12 @@ __device__ __forceinline__ double warp_min(double v) {
   return v;
 }
 
+// Dynamic shared memory limit of a kernel.  (Forcing the maximum shared-memory carveout as well was
+// measured slower: the bulge chase and the rank update lose more to the smaller L1 than they gain from
+// extra resident CTAs.)
+template <typename K>
+inline void set_smem_attr(K* kernel, size_t bytes) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 }  // namespace hx

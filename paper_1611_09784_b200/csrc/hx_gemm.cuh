@@ -44,17 +44,27 @@ constexpr int XV_TM = 64, XV_TK = 16, XV_ST = 3;
 constexpr int XV_LD0 = XV_TM + 2, XV_LD1 = XV_TK + 4, XV_LDV = XV_TK + 4;
 constexpr int XV_A_ELEMS = XV_TK * XV_LD0 > XV_TM * XV_LD1 ? XV_TK * XV_LD0 : XV_TM * XV_LD1;
 constexpr size_t XV_SMEM = (size_t)XV_ST * (XV_A_ELEMS + GBW * XV_LDV) * sizeof(double2);
+constexpr int XV_LDS = GBW + 4;  // S chunk rows (k) x 32 (l), 4 (mod 8)
+constexpr size_t XV_SMEM_UPD = XV_SMEM + (size_t)XV_ST * XV_TK * XV_LDS * sizeof(double2);
 static_assert((size_t)(XV_TM + GBW) * (GBW + 4) * sizeof(double2) <= XV_SMEM, "xv epilogue tile does not fit");
 
-template <int MODE>
+// UPD: before a chunk of op(A) enters the product it receives the pending rank-32 update of the other
+// side, op(A) -= R S^H (R: the CTA's 64 rows, resident in registers; S: the chunk's 16 rows, staged with
+// the chunk), and the updated chunk is written back to M - one pass over the trailing matrix instead of
+// a separate rank update (read + write) followed by this product (read).  In matrix terms:
+//   MODE 0: M[ar0+i][ac0+k] -= R[i] conj(S[k]);   MODE 1: M[ar0+k][ac0+i] -= S[k] conj(R[i]).
+// R[i][l] = base[r_off + i0 + i + l*ld], S[k][l] = base[s_off + k + l*ld].
+template <int MODE, bool UPD = false>
 __global__ void __launch_bounds__(128) xv_kernel(double2* ws, SlabGeom g, int ar0, int ac0, int rows, int K,
-                                                 size_t v_off, size_t x_off, size_t t_off) {
+                                                 size_t v_off, size_t x_off, size_t t_off, size_t r_off = 0,
+                                                 size_t s_off = 0) {
   extern __shared__ __align__(16) double2 xv_sm[];
   double2* As = xv_sm;                         // [XV_ST][XV_A_ELEMS]
   double2* Vs = xv_sm + XV_ST * XV_A_ELEMS;    // [XV_ST][GBW][XV_LDV]
+  double2* Ss = Vs + XV_ST * GBW * XV_LDV;     // UPD: [XV_ST][XV_TK][XV_LDS]
   double2* base = ws + (size_t)blockIdx.y * g.stride;
   const int ld = g.ld;
-  const double2* M = base + g.m_off;
+  double2* M = base + g.m_off;
   const double2* V = base + v_off;
   double2* X = base + x_off;
   const int i0 = blockIdx.x * XV_TM;
@@ -90,7 +100,30 @@ __global__ void __launch_bounds__(128) xv_kernel(double2* ws, SlabGeom g, int ar
       const bool ok = gk < K;
       cp_async16_zfill(Vt + n * XV_LDV + kc, V + (ok ? gk + (size_t)n * ld : 0), ok);
     }
+    if (UPD) {
+      double2* St = Ss + stg * XV_TK * XV_LDS;
+      const double2* Sg = base + s_off;
+#pragma unroll
+      for (int q = 0; q < GBW * XV_TK / 128; ++q) {
+        const int p = tid + 128 * q, kc = p & (XV_TK - 1), l = p >> 4;
+        const int gk = kk + kc;
+        const bool ok = gk < K;
+        cp_async16_zfill(St + kc * XV_LDS + l, Sg + (ok ? gk + (size_t)l * ld : 0), ok);
+      }
+    }
   };
+  // UPD: this warp's 16 rows of R as DMMA A fragments (row 16 warp + 8 rt + lane/4, column 4 k4 + lane%4)
+  double2 rf[2][GBW / 4];
+  if (UPD) {
+    const double2* Rg = base + r_off;
+#pragma unroll
+    for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+      for (int k4 = 0; k4 < GBW / 4; ++k4) {
+        const int r = i0 + 16 * warp + 8 * rt + (lane >> 2);
+        rf[rt][k4] = r < rows ? Rg[r + (size_t)(4 * k4 + (lane & 3)) * ld] : make_double2(0.0, 0.0);
+      }
+  }
   CTile acc[2][4];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -110,8 +143,65 @@ __global__ void __launch_bounds__(128) xv_kernel(double2* ws, SlabGeom g, int ar
       cp_async_commit();
     }
     const int stg = ch % XV_ST;
-    const double2* A = As + stg * XV_A_ELEMS;
+    double2* A = As + stg * XV_A_ELEMS;
     const double2* Vt = Vs + stg * GBW * XV_LDV;
+    if (UPD) {
+      // op(A)[rows of this warp][16 columns of the chunk] -= R S^H (K = 32), in place + back to M
+      const double2* St = Ss + stg * XV_TK * XV_LDS;
+      const int kk = ch * XV_TK;
+      CTile u[2][2];
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+        for (int ct = 0; ct < 2; ++ct) {
+          const int r = 16 * warp + 8 * rt + (lane >> 2), c = 8 * ct + 2 * (lane & 3);
+          const double2 z0 = MODE == 1 ? A[r * XV_LD1 + c] : A[c * XV_LD0 + r];
+          const double2 z1 = MODE == 1 ? A[r * XV_LD1 + c + 1] : A[(c + 1) * XV_LD0 + r];
+          // op(A) holds conj(M) in MODE 1: update the conjugates (A - R S^H)
+          u[rt][ct].re0 = z0.x;
+          u[rt][ct].im0 = MODE == 1 ? -z0.y : z0.y;
+          u[rt][ct].re1 = z1.x;
+          u[rt][ct].im1 = MODE == 1 ? -z1.y : z1.y;
+        }
+#pragma unroll
+      for (int k4 = 0; k4 < GBW / 4; ++k4) {
+        const int lc = 4 * k4 + (lane & 3);
+        double2 b[2];
+#pragma unroll
+        for (int ct = 0; ct < 2; ++ct) b[ct] = gconj(St[(8 * ct + (lane >> 2)) * XV_LDS + lc]);
+#pragma unroll
+        for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+          for (int ct = 0; ct < 2; ++ct) u[rt][ct].mac(-rf[rt][k4].x, -rf[rt][k4].y, b[ct].x, b[ct].y);
+      }
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+        for (int ct = 0; ct < 2; ++ct) {
+          const int r = 16 * warp + 8 * rt + (lane >> 2), c = 8 * ct + 2 * (lane & 3);
+          const double2 n0 = make_double2(u[rt][ct].re0, MODE == 1 ? -u[rt][ct].im0 : u[rt][ct].im0);
+          const double2 n1 = make_double2(u[rt][ct].re1, MODE == 1 ? -u[rt][ct].im1 : u[rt][ct].im1);
+          if (MODE == 1) {
+            A[r * XV_LD1 + c] = n0;
+            A[r * XV_LD1 + c + 1] = n1;
+          } else {
+            A[c * XV_LD0 + r] = n0;
+            A[(c + 1) * XV_LD0 + r] = n1;
+          }
+          const int gi = i0 + r, gk = kk + c;
+          if (gi < rows) {
+            if (MODE == 1) {  // M[ar0 + k][ac0 + i] = conj(op(A)) = n (the tile holds raw M values)
+              double2* mp = M + (size_t)(ac0 + gi) * ld + ar0 + gk;
+              if (gk < K) mp[0] = n0;
+              if (gk + 1 < K) mp[1] = n1;
+            } else {
+              if (gk < K) M[(size_t)(ac0 + gk) * ld + ar0 + gi] = n0;
+              if (gk + 1 < K) M[(size_t)(ac0 + gk + 1) * ld + ar0 + gi] = n1;
+            }
+          }
+        }
+      __syncwarp();  // the product below reads only this warp's rows of the chunk
+    }
 #pragma unroll
     for (int k4 = 0; k4 < XV_TK / 4; ++k4) {
       const int kc = 4 * k4 + (lane & 3);
