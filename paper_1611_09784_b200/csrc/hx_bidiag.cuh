@@ -110,85 +110,101 @@ static __device__ void bidiag_tgk(double2* M, int lm, int rows, int cols, double
   //   left  (column) pass: row group g = lane & 7, column (tid >> 3) + k * bd/8; sums over g by xor 1,2,4
   //   right (row) pass:    row (lane & 7) + 8 * warp + k * 8 nw, column group q = lane >> 3 (4 groups);
   //                        sums over q by xor 8,16
+  // Two barriers per reflector: the squared norm the NEXT reflector needs (row j after the left update,
+  // column j+1 after the right update) is accumulated by the threads that write those entries and
+  // combined from per-warp partials (red[0..31]: column norm, red[32..63]: row norm).
   const int g = lane & 7, q = lane >> 3;
+  double* lred = red;
+  double* rred = red + 32;
+  {
+    double part = 0.0;
+    for (int i = tid; i < rows; i += bd) {
+      const double2 x = M[i];
+      part = fma(x.x, x.x, fma(x.y, x.y, part));
+    }
+    part = warp_sum(part);
+    if (lane == 0) lred[warp] = part;
+    __syncthreads();
+  }
   for (int j = 0; j < cols; ++j) {
     // ---------------- left reflector: column j, rows j..rows-1
     {
-      double part = 0.0;
-      for (int i = j + tid; i < rows; i += bd) {
-        const double2 x = M[i + (size_t)j * lm];
-        part += x.x * x.x + x.y * x.y;
-      }
-      const double sig2 = block_sum(part, red);
-      const double2 alpha = M[j + (size_t)j * lm];
-      const QuickReflector h = quick_reflector(alpha, sig2);
+      double sig2 = 0.0;
+      for (int w = 0; w < nw; ++w) sig2 += lred[w];
+      const double2* colj = M + (size_t)j * lm;
+      const QuickReflector h = quick_reflector(colj[j], sig2);
       if (tid == 0) e2[2 * j] = sig2;
-      if (h.tau != 0.0) {
-        for (int i = j + tid; i < rows; i += bd) u[i] = i == j ? make_double2(1.0, 0.0) : cmul(M[i + (size_t)j * lm], h.scale);
-        __syncthreads();
-        // M[:, c] -= v (tau v^H M[:, c]) for c > j: 8 lanes per column, the column sum stays in the group
-        for (int c0 = j + 1; c0 < cols; c0 += bd >> 3) {
-          const int cc = c0 + (tid >> 3);
-          double2 acc = make_double2(0.0, 0.0);
-          if (cc < cols)
-            for (int i = j + g; i < rows; i += 8) {
-              const double2 a = u[i], b = M[i + (size_t)cc * lm];
-              acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));
-              acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
-            }
-#pragma unroll
-          for (int o = 1; o < 8; o <<= 1) {
-            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      for (int i = j + tid; i < rows; i += bd) u[i] = i == j ? make_double2(1.0, 0.0) : cmul(colj[i], h.scale);
+      __syncthreads();
+      // M[:, c] -= v (tau v^H M[:, c]) for c > j: 8 lanes per column, the column sum stays in the group
+      double rpart = 0.0;  // |M[j][c]|^2 after the update (row norm for the right reflector)
+      for (int c0 = j + 1; c0 < cols; c0 += bd >> 3) {
+        const int cc = c0 + (tid >> 3);
+        double2 acc = make_double2(0.0, 0.0);
+        if (cc < cols && h.tau != 0.0)
+          for (int i = j + g; i < rows; i += 8) {
+            const double2 a = u[i], b = M[i + (size_t)cc * lm];
+            acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));
+            acc.y = fma(a.x, b.y, fma(-a.y, b.x, acc.y));
           }
-          const double2 sc = make_double2(h.tau * acc.x, h.tau * acc.y);
-          if (cc < cols)
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        }
+        const double2 sc = make_double2(h.tau * acc.x, h.tau * acc.y);
+        if (cc < cols) {
+          if (h.tau != 0.0)
             for (int i = j + g; i < rows; i += 8) {
               const double2 a = u[i];
               double2 x = M[i + (size_t)cc * lm];
               x.x = fma(-a.x, sc.x, fma(a.y, sc.y, x.x));
               x.y = fma(-a.x, sc.y, fma(-a.y, sc.x, x.y));
               M[i + (size_t)cc * lm] = x;
+              if (i == j) rpart = fma(x.x, x.x, fma(x.y, x.y, rpart));
             }
+          else if (g == 0) {
+            const double2 x = M[j + (size_t)cc * lm];
+            rpart = fma(x.x, x.x, fma(x.y, x.y, rpart));
+          }
         }
-        __syncthreads();
       }
+      rpart = warp_sum(rpart);
+      if (lane == 0) rred[warp] = rpart;
+      __syncthreads();
     }
     if (j + 1 >= cols) break;
     // ---------------- right reflector: row j, columns j+1..cols-1 (on the conjugated row)
     {
-      double part = 0.0;
-      for (int cc = j + 1 + tid; cc < cols; cc += bd) {
-        const double2 x = M[j + (size_t)cc * lm];
-        part += x.x * x.x + x.y * x.y;
-      }
-      const double sig2 = block_sum(part, red);
+      double sig2 = 0.0;
+      for (int w = 0; w < nw; ++w) sig2 += rred[w];
       const double2 a0 = M[j + (size_t)(j + 1) * lm];
       const QuickReflector h = quick_reflector(make_double2(a0.x, -a0.y), sig2);
       if (tid == 0) e2[2 * j + 1] = sig2;
-      if (h.tau != 0.0) {
-        // u_c from conj(row j): u_{j+1} = 1
-        for (int cc = j + 1 + tid; cc < cols; cc += bd) {
-          const double2 x = M[j + (size_t)cc * lm];
-          u[cc] = cc == j + 1 ? make_double2(1.0, 0.0) : cmul(make_double2(x.x, -x.y), h.scale);
-        }
-        __syncthreads();
-        // M[r, :] -= (tau M[r, :] u) u^H for rows r > j: 4 lanes per row (column groups)
-        for (int r0 = j + 1; r0 < rows; r0 += 8 * nw) {
-          const int r = r0 + g + 8 * warp;
-          double2 acc = make_double2(0.0, 0.0);
-          if (r < rows)
-            for (int cc = j + 1 + q; cc < cols; cc += 4) {
-              const double2 a = M[r + (size_t)cc * lm], b = u[cc];
-              acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
-              acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
-            }
-          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 8);
-          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 8);
-          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
-          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
-          const double2 w = make_double2(h.tau * acc.x, h.tau * acc.y);
-          if (r < rows)
+      // u_c from conj(row j): u_{j+1} = 1
+      for (int cc = j + 1 + tid; cc < cols; cc += bd) {
+        const double2 x = M[j + (size_t)cc * lm];
+        u[cc] = cc == j + 1 ? make_double2(1.0, 0.0) : cmul(make_double2(x.x, -x.y), h.scale);
+      }
+      __syncthreads();
+      // M[r, :] -= (tau M[r, :] u) u^H for rows r > j: 4 lanes per row (column groups)
+      double lpart = 0.0;  // |M[r][j+1]|^2, r > j, after the update (column norm for the next left)
+      for (int r0 = j + 1; r0 < rows; r0 += 8 * nw) {
+        const int r = r0 + g + 8 * warp;
+        double2 acc = make_double2(0.0, 0.0);
+        if (r < rows && h.tau != 0.0)
+          for (int cc = j + 1 + q; cc < cols; cc += 4) {
+            const double2 a = M[r + (size_t)cc * lm], b = u[cc];
+            acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+            acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+          }
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 8);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 8);
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+        const double2 w = make_double2(h.tau * acc.x, h.tau * acc.y);
+        if (r < rows) {
+          if (h.tau != 0.0)
             for (int cc = j + 1 + q; cc < cols; cc += 4) {
               const double2 b = u[cc];
               double2 x = M[r + (size_t)cc * lm];
@@ -196,10 +212,17 @@ static __device__ void bidiag_tgk(double2* M, int lm, int rows, int cols, double
               x.x = fma(-w.x, b.x, fma(-w.y, b.y, x.x));
               x.y = fma(-w.y, b.x, fma(w.x, b.y, x.y));
               M[r + (size_t)cc * lm] = x;
+              if (cc == j + 1) lpart = fma(x.x, x.x, fma(x.y, x.y, lpart));
             }
+          else if (q == 0) {
+            const double2 x = M[r + (size_t)(j + 1) * lm];
+            lpart = fma(x.x, x.x, fma(x.y, x.y, lpart));
+          }
         }
-        __syncthreads();
       }
+      lpart = warp_sum(lpart);
+      if (lane == 0) lred[warp] = lpart;
+      __syncthreads();
     }
   }
   __syncthreads();
