@@ -316,6 +316,7 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
   g.delta = grid->delta;
   g.npts = grid->npts;
   g.shift = fixed_point_shift(nk, N);
+  g.inv_step = 1.0 / g.step;
   if (g.shift < 16) return fail(HX_E_RANGE, "nk * N too large for the fixed-point IDOS accumulator");
   // k-points (small, pageable copy on the work stream)
   if (ctx->kpts.grow((size_t)nk * 16)) return fail(HX_E_CUDA, "alloc kpts");

@@ -43,7 +43,8 @@ struct CellDev {
 struct GridDev {
   double e0, step, delta;
   int32_t npts;
-  int32_t shift;  // fixed-point fraction bits of the transition accumulator
+  int32_t shift;     // fixed-point fraction bits of the transition accumulator
+  double inv_step;   // 1 / step: only for the (eta-widened) early-settle test, never for contributions
 };
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {

@@ -151,14 +151,17 @@ static __device__ __forceinline__ long long settle_index(const CellDev& c, const
   const double eta = 16.0 * DBL_EPSILON * fmax(1.0, fmax(fabs(Ea), fabs(Eb)));
   Ea -= eta;
   Eb += eta;
+  // multiplying by 1/step instead of dividing moves a quotient by <= 2 ulp; the 16-ulp widening above
+  // (>= 10 ulp of the quotient) keeps the decision identical to the reference's division
+  const double is = g.inv_step;
   if (sharp) {
-    const long long ia = (long long)floor((Ea - g.e0) / g.step), ib = (long long)floor((Eb - g.e0) / g.step);
+    const long long ia = (long long)floor((Ea - g.e0) * is), ib = (long long)floor((Eb - g.e0) * is);
     return ia == ib ? ia + 1 : LLONG_MIN;
   }
-  const long long la = (long long)ceil((Ea + g.delta - g.e0) / g.step);
-  const long long lb = (long long)ceil((Eb + g.delta - g.e0) / g.step);
-  const long long ma = (long long)floor((Ea - g.delta - g.e0) / g.step) + 1;
-  const long long mb = (long long)floor((Eb - g.delta - g.e0) / g.step) + 1;
+  const long long la = (long long)ceil((Ea + g.delta - g.e0) * is);
+  const long long lb = (long long)ceil((Eb + g.delta - g.e0) * is);
+  const long long ma = (long long)floor((Ea - g.delta - g.e0) * is) + 1;
+  const long long mb = (long long)floor((Eb - g.delta - g.e0) * is) + 1;
   return (la == lb && ma == mb && ma >= la) ? la : LLONG_MIN;
 }
 
