@@ -171,8 +171,7 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     }
     BD_CUDA(cudaGetLastError());
   }
-  // ---- stage 2: enough sweeps in flight to fill the SMs.  Large batches (throughput-bound) use the
-  // single-tile variant (12 warps per SM); small ones the dual-tile one (lower latency per task).
+  // ---- stage 2: enough sweeps in flight to fill the SMs (single-tile variant: 19 KB per warp).
   static const int chase_mode = [] {
     const char* e = getenv("HX_CHASE_MODE");
     return e ? atoi(e) : 0;
@@ -196,9 +195,11 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     BD_CUDA(cudaLaunchKernelEx(&cfg, bd_chase_kernel<NW, BB, DUAL, CL>, ws, a1, a2, a3, S, dims)); \
   }
   if (want >= 6) {
-    if (chase_mode == 1) BD_CHASE(11, false, 1)
-    else if (chase_mode == 2) BD_CHASE(6, true, 1)
-    else BD_CHASE(8, false, 2)
+    // one CTA (11 sweeps in flight) per matrix: in the concurrent tier schedule the 2-CTA cluster variant
+    // (16 sweeps, 3-6 % lower latency alone) costs more than it gains by occupying twice the SMs
+    if (chase_mode == 2) BD_CHASE(8, false, 2)
+    else if (chase_mode == 3) BD_CHASE(6, true, 1)
+    else BD_CHASE(11, false, 1)
   } else if (want >= 2) {
     BD_CHASE(2, false, 1)
   } else {
