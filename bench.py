@@ -530,9 +530,10 @@ def run_e2e(hx, model, levels, nq, p, erange, lo, hi, args, rank, world, dev):
     def one(count_bytes):
         eng = hx.Engine(model, nq=nq, delta=DELTA, master_seed=SEED, bz_mode="reduced", energy_points=NPTS,
                         energy_range=(lo + 2 * DELTA, hi - 2 * DELTA), device=dev.index, shard=(rank, world))
+        plan = hx.LevelPlan(ns=tuple(nu for nu, _ in plan_levels), samples=tuple(M for _, M in plan_levels), nq=nq,
+                            p_vac=p, delta=DELTA)
         t0 = time.perf_counter()
-        for lvl, (nu, M) in enumerate(plan_levels, start=1):
-            eng.sample_level(lvl, nu, M, p, with_cv=lvl > 1)
+        eng.run_mlmc(plan)
         torch.cuda.synchronize(dev)
         dt = time.perf_counter() - t0
         return dt, eng.io_bytes
@@ -552,7 +553,7 @@ def run_e2e(hx, model, levels, nq, p, erange, lo, hi, args, rank, world, dev):
         dt = float(t.item())
     total = world * sum(M for _, M in levels)
     return {"value": total / dt, "unit": "samples/s", "h2d_bytes_per_step": int(io[0]), "d2h_bytes_per_step": int(io[1]),
-            "api": "paper_1611_09784_b200.Engine.sample_level per level (host RNG + dedup, hx_eval_idos_batch)"}
+            "api": "paper_1611_09784_b200.Engine.run_mlmc (host RNG + dedup per level, every (n, q) tier of every level through hx_eval_idos_batch concurrently)"}
 
 
 def cpu_baseline(kind, levels, nq, p, erange):

@@ -162,54 +162,84 @@ class Engine:
             return {g: f.result() for g, f in futs.items()}
 
     def _evaluate_words(self, groups, task_ids):
-        """Vectorised batch seam.  groups: list of (n, q, words uint64 [R, w]) in request order;
-        task_ids(i_group, rows) -> ids of those rows (only built for error reports).  Dedup on
-        (n, q, mask) against the run cache and within the batch (np.unique over the rows instead of a
-        per-request dict), one GPU batch per group for the new masks.  Returns per group (curves [R, npts],
-        per_job [R]) in row order, the hit count and the nominal work spent (runner.py:206-244)."""
+        """One batch of the seam (see _evaluate_batches)."""
+        return self._evaluate_batches([(groups, task_ids)])[0]
+
+    def _evaluate_batches(self, batches):
+        """Vectorised batch seam for several consecutive batches.  batches: list of (groups, task_ids),
+        groups = [(n, q, words uint64 [R, w]), ...] in request order, task_ids(i_group, new, inv) -> ids of
+        the new masks (error reports only).  Every batch is deduplicated on (n, q, mask) against the run
+        cache, against itself (np.unique over the rows instead of a per-request dict) and against the new
+        masks of the EARLIER batches - the hit accounting of calling the batches one after another
+        (runner.py:206-244) - but the new masks of all batches are solved together, one GPU batch per
+        (n, q), groups concurrently.  Returns per batch ([(curves [R, npts], per_job [R]) per group],
+        hits, spent)."""
         npts = self.grid.npoints
-        plans, jobs = [], {}
-        hits = 0
-        for gi, (n, q, words) in enumerate(groups):
-            words = np.ascontiguousarray(words, dtype=np.uint64)
-            R = words.shape[0]
-            if self.dedup and R:
-                uniq, inv = np.unique(words, axis=0, return_inverse=True)
-                inv = inv.reshape(-1)
-                keys = [(n, q, row.tobytes()) for row in uniq]
-                cached = np.fromiter((k in self._cache for k in keys), dtype=bool, count=len(keys))
-                hits += (R - len(uniq)) + int(cached.sum())
-            else:
-                uniq, inv, keys = words, np.arange(R), None
-                cached = np.zeros(R, dtype=bool)
-            new = np.flatnonzero(~cached)
-            if len(new):
-                if (n, q) in jobs:  # two groups with the same (n, q): solve them as one batch
-                    w0, ids0 = jobs[(n, q)]
-                    jobs[(n, q)] = (np.concatenate([w0, uniq[new]]), ids0 + task_ids(gi, new, inv))
+        pending = {}  # key -> (group key (n, q), row in that group's job)
+        jobs = {}     # (n, q) -> [list of word arrays, list of task ids, row count]
+        plans = []
+        for bi, (groups, task_ids) in enumerate(batches):
+            bplans, hits = [], 0
+            for gi, (n, q, words) in enumerate(groups):
+                words = np.ascontiguousarray(words, dtype=np.uint64)
+                R = words.shape[0]
+                if self.dedup and R:
+                    uniq, inv = np.unique(words, axis=0, return_inverse=True)
+                    inv = inv.reshape(-1)
+                    keys = [(n, q, row.tobytes()) for row in uniq]
                 else:
-                    jobs[(n, q)] = (uniq[new], task_ids(gi, new, inv))
-            plans.append((n, q, uniq, inv, keys, cached, new))
-        solved = self._solve_groups(jobs) if jobs else {}
-        used = {g: 0 for g in jobs}
-        out, spent = [], 0.0
-        for n, q, uniq, inv, keys, cached, new in plans:
-            cu = np.empty((len(uniq), npts))
-            pj = np.empty(len(uniq))
-            if len(new):
-                curves, per_job = solved[(n, q)]
-                k0 = used[(n, q)]
-                used[(n, q)] = k0 + len(new)
-                cu[new] = curves[k0:k0 + len(new)]
-                pj[new] = per_job
-                spent += per_job * len(new)
-                if self.dedup:
-                    for i in new:
-                        self._cache[keys[i]] = (cu[i], per_job)
-            for i in np.flatnonzero(cached):
-                cu[i], pj[i] = self._cache[keys[i]]
-            out.append((cu[inv], pj[inv]))
-        return out, hits, spent
+                    uniq, inv, keys = words, np.arange(R), None
+                src = []  # per unique row: ("cache", key) | ("job", (n, q), row)
+                new = []
+                for i in range(len(uniq)):
+                    k = keys[i] if keys is not None else None
+                    if k is not None and k in self._cache:
+                        src.append(("cache", k))
+                        hits += 1
+                    elif k is not None and k in pending:
+                        src.append(("job",) + pending[k])
+                        hits += 1
+                    else:
+                        job = jobs.setdefault((n, q), [[], [], 0])
+                        src.append(("job", (n, q), job[2]))
+                        if k is not None:
+                            pending[k] = ((n, q), job[2])
+                        job[2] += 1
+                        new.append(i)
+                hits += R - len(uniq)
+                if new:
+                    new = np.asarray(new)
+                    jobs[(n, q)][0].append(uniq[new])
+                    jobs[(n, q)][1].extend(task_ids(gi, new, inv))
+                bplans.append((uniq, inv, keys, src))
+            plans.append((bplans, hits))
+        solved = self._solve_groups({g: (np.concatenate(j[0]), j[1]) for g, j in jobs.items()}) if jobs else {}
+        out = []
+        for bplans, hits in plans:
+            res, spent = [], 0.0
+            for uniq, inv, keys, src in bplans:
+                cu = np.empty((len(uniq), npts))
+                pj = np.empty(len(uniq))
+                for i, sref in enumerate(src):
+                    if sref[0] == "cache":
+                        cu[i], pj[i] = self._cache[sref[1]]
+                    else:
+                        curves, per_job = solved[sref[1]]
+                        cu[i], pj[i] = curves[sref[2]], per_job
+                res.append((cu[inv], pj[inv]))
+            out.append((res, hits, spent))
+        # nominal time spent on new jobs, attributed to the batch that first requested them
+        for bi, (bplans, _) in enumerate(plans):
+            spent = 0.0
+            for uniq, inv, keys, src in bplans:
+                for i, sref in enumerate(src):
+                    if sref[0] == "job" and not (keys is not None and keys[i] in self._cache):
+                        if keys is None or pending.get(keys[i]) == (sref[1], sref[2]):
+                            spent += solved[sref[1]][1]
+                            if keys is not None:
+                                self._cache[keys[i]] = (solved[sref[1]][0][sref[2]], solved[sref[1]][1])
+            out[bi] = (out[bi][0], out[bi][1], spent)
+        return out
 
     def evaluate_masks(self, requests):
         """Dedup on (n, q, mask) against the run cache and within the batch; solve the new jobs of each
@@ -241,8 +271,8 @@ class Engine:
         words = sample_masks(supercell.nunits, p_vac, self.master_seed, stream_level, 0, count)
         return [DefectConfiguration.from_key(supercell, k) for k in keys_from_words(words)]
 
-    def sample_level(self, level: int, n: int, nsamples: int, p_vac: float, with_cv: bool, stream_level=None):
-        """Draw outcomes and evaluate the level terms with the quarter CV (runner.py:254-311)."""
+    def _level_batch(self, level: int, n: int, nsamples: int, p_vac: float, with_cv: bool, stream_level=None):
+        """Masks of one level (parents, + restricted quarters) as a batch of the seam."""
         q = self.q_of(n)
         sc = self.supercell(n)
         stream = level if stream_level is None else stream_level
@@ -266,7 +296,12 @@ class Engine:
                 return [(level, m0 + int(r), "Q") for r in rows]
             return [(level, m0 + int(r) // 4, f"CV{int(r) % 4 + 1}") for r in rows]
 
-        res, hits, spent = self._evaluate_words(groups, ids)
+        return groups, ids
+
+    def _level_finish(self, level, n, nsamples, with_cv, evaluated):
+        """Level terms + moments from the seam's results for the level's batch (runner.py:281-311)."""
+        res, hits, spent = evaluated
+        q = self.q_of(n)
         npts = self.grid.npoints
         full, pj = res[0]
         nominal = float(pj.sum())
@@ -291,6 +326,11 @@ class Engine:
                            work_per_sample=nominal / nsamples, wall_seconds=spent, cache_hits=hits)
         return LevelSampleSet(stats=stats, terms=terms, full=full, cv=cv)
 
+    def sample_level(self, level: int, n: int, nsamples: int, p_vac: float, with_cv: bool, stream_level=None):
+        """Draw outcomes and evaluate the level terms with the quarter CV (runner.py:254-311)."""
+        batch = self._level_batch(level, n, nsamples, p_vac, with_cv, stream_level)
+        return self._level_finish(level, n, nsamples, with_cv, self._evaluate_batches([batch])[0])
+
     # -- mode drivers (runner.py:315-419) --
     def run_mc(self, plan: LevelPlan):
         level = plan.num_levels
@@ -298,11 +338,14 @@ class Engine:
         return combine_levels(self.grid, [sset.stats], total_wall_seconds=sset.stats.wall_seconds), sset
 
     def run_mlmc(self, plan: LevelPlan):
-        sets, total = [], 0.0
-        for idx, (n, m) in enumerate(zip(plan.ns, plan.samples), start=1):
-            sset = self.sample_level(idx, n, m, plan.p_vac, with_cv=idx > 1)
-            sets.append(sset)
-            total += sset.stats.wall_seconds
+        """All levels of the plan (runner.py:315-340).  The levels are deduplicated in order (the same
+        cache hits as sampling them one after another) but their new masks are solved in one concurrent
+        submission - every (n, q) tier of every level in flight at once."""
+        levels = list(enumerate(zip(plan.ns, plan.samples), start=1))
+        batches = [self._level_batch(idx, n, m, plan.p_vac, idx > 1) for idx, (n, m) in levels]
+        evaluated = self._evaluate_batches(batches)
+        sets = [self._level_finish(idx, n, m, idx > 1, ev) for (idx, (n, m)), ev in zip(levels, evaluated)]
+        total = sum(s.stats.wall_seconds for s in sets)
         return combine_levels(self.grid, [s.stats for s in sets], total_wall_seconds=total), sets
 
     def run_slmc_reference(self, plan: LevelPlan, nsamples: int):

@@ -217,3 +217,19 @@ def test_high_vacancy_tiers_match_oracle(kind, nu, q, p):
         assert np.max(np.abs(eigs[m, :, :d] - ref)) <= EIG_TOL * (ref.max() - ref.min())
         rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), lo, hi, npts, 0.01, ocell.area)
         np.testing.assert_allclose(curves[m], rc, rtol=0, atol=IDOS_TOL)
+
+
+def test_run_mlmc_batched_equals_level_by_level():
+    """run_mlmc submits every level at once; means, variances and cache hits must equal sampling the levels
+    one after another (cross-level hits: level l's quarters at nu/2 meet level l-1's parents)."""
+    kw = dict(nq=16, delta=0.01, master_seed=2026, bz_mode="reduced", energy_points=201)
+    plan = hx.LevelPlan(ns=(2, 4, 8), samples=(64, 16, 4), nq=16, p_vac=0.1, delta=0.01)
+    a = hx.Engine(hx.GrapheneNNModel(), **kw)
+    _, sets = a.run_mlmc(plan)
+    b = hx.Engine(hx.GrapheneNNModel(), **kw)
+    for idx, (n, m) in enumerate(zip(plan.ns, plan.samples), start=1):
+        s = b.sample_level(idx, n, m, plan.p_vac, with_cv=idx > 1)
+        t = sets[idx - 1]
+        assert np.array_equal(s.full, t.full)
+        assert np.array_equal(s.stats.mean, t.stats.mean)
+        assert s.stats.cache_hits == t.stats.cache_hits
