@@ -171,7 +171,7 @@ class Device:
         high-priority stream)."""
         pool = cls._pools.setdefault(device, [])
         while len(pool) <= i:
-            pool.append(cls.new_ctx(device, -1 if not pool else 0))
+            pool.append(cls.new_ctx(device, -100 if not pool else 0))  # -100: clamped to the greatest priority
         return pool[i]
 
     @classmethod

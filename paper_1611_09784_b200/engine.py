@@ -146,21 +146,6 @@ class Engine:
             raise TaskError(failures)
         return curves, secs / max(1, len(words))
 
-    def _solve_groups(self, jobs):
-        """Solve every (n, q) group {(n, q): (words, task_ids)}; several groups run concurrently, each
-        from its own thread on its own hx context (the largest tier on the high-priority one), as the
-        reference's parallel_map runs its jobs side by side (runner.py:75-93)."""
-        for n, _ in jobs:
-            self.cell(n)  # compile cells up front (not thread-safe)
-        if len(jobs) == 1:
-            g = next(iter(jobs))
-            return {g: self._solve_group(g[0], g[1], *jobs[g])}
-        order = sorted(jobs, key=lambda g: -self.cell(g[0]).dim)
-        with ThreadPoolExecutor(max_workers=len(order)) as ex:
-            futs = {g: ex.submit(self._solve_group, g[0], g[1], *jobs[g], _lib.Device.lane(self.device, lane))
-                    for lane, g in enumerate(order)}
-            return {g: f.result() for g, f in futs.items()}
-
     def _evaluate_words(self, groups, task_ids):
         """One batch of the seam (see _evaluate_batches)."""
         return self._evaluate_batches([(groups, task_ids)])[0]
@@ -171,74 +156,82 @@ class Engine:
         the new masks (error reports only).  Every batch is deduplicated on (n, q, mask) against the run
         cache, against itself (np.unique over the rows instead of a per-request dict) and against the new
         masks of the EARLIER batches - the hit accounting of calling the batches one after another
-        (runner.py:206-244) - but the new masks of all batches are solved together, one GPU batch per
-        (n, q), groups concurrently.  Returns per batch ([(curves [R, npts], per_job [R]) per group],
-        hits, spent)."""
+        (runner.py:206-244).  Keys of different (n, q) never meet, so the planning runs one (n, q) tier at
+        a time, most expensive tier first, and each tier's GPU batch is submitted (its own thread and hx
+        context, the first on the high-priority one) as soon as it is planned: the host work of the
+        smaller tiers overlaps the device work of the big one.  Returns per batch ([(curves [R, npts],
+        per_job [R]) per group], hits, spent)."""
         npts = self.grid.npoints
-        pending = {}  # key -> (group key (n, q), row in that group's job)
-        jobs = {}     # (n, q) -> [list of word arrays, list of task ids, row count]
-        plans = []
-        for bi, (groups, task_ids) in enumerate(batches):
-            bplans, hits = [], 0
+        tiers: dict = {}  # (n, q) -> [(batch index, group index, words)] in batch order
+        for bi, (groups, _) in enumerate(batches):
             for gi, (n, q, words) in enumerate(groups):
-                words = np.ascontiguousarray(words, dtype=np.uint64)
-                R = words.shape[0]
-                if self.dedup and R:
-                    uniq, inv = np.unique(words, axis=0, return_inverse=True)
-                    inv = inv.reshape(-1)
-                    keys = [(n, q, row.tobytes()) for row in uniq]
-                else:
-                    uniq, inv, keys = words, np.arange(R), None
-                src = []  # per unique row: ("cache", key) | ("job", (n, q), row)
-                new = []
-                for i in range(len(uniq)):
-                    k = keys[i] if keys is not None else None
-                    if k is not None and k in self._cache:
-                        src.append(("cache", k))
-                        hits += 1
-                    elif k is not None and k in pending:
-                        src.append(("job",) + pending[k])
-                        hits += 1
+                tiers.setdefault((n, q), []).append((bi, gi, np.ascontiguousarray(words, dtype=np.uint64)))
+        for n, _ in tiers:
+            self.cell(n)  # compile cells up front (not thread-safe)
+        order = sorted(tiers, key=lambda g: -self.cell(g[0]).dim)
+        hits = [0] * len(batches)
+        spent = [0.0] * len(batches)
+        plans = {}  # (bi, gi) -> (uniq, inv, keys, src)
+        futs = {}
+        first_batch = {}  # (tier, row) -> batch that requested the new mask first
+        with ThreadPoolExecutor(max_workers=max(1, len(order))) as ex:
+            for lane, tier in enumerate(order):
+                pending = {}
+                rows, ids = [], []
+                count = 0
+                for bi, gi, words in tiers[tier]:
+                    R = words.shape[0]
+                    if self.dedup and R:
+                        uniq, inv = np.unique(words, axis=0, return_inverse=True)
+                        inv = inv.reshape(-1)
+                        keys = [(tier[0], tier[1], row.tobytes()) for row in uniq]
                     else:
-                        job = jobs.setdefault((n, q), [[], [], 0])
-                        src.append(("job", (n, q), job[2]))
-                        if k is not None:
-                            pending[k] = ((n, q), job[2])
-                        job[2] += 1
-                        new.append(i)
-                hits += R - len(uniq)
-                if new:
-                    new = np.asarray(new)
-                    jobs[(n, q)][0].append(uniq[new])
-                    jobs[(n, q)][1].extend(task_ids(gi, new, inv))
-                bplans.append((uniq, inv, keys, src))
-            plans.append((bplans, hits))
-        solved = self._solve_groups({g: (np.concatenate(j[0]), j[1]) for g, j in jobs.items()}) if jobs else {}
+                        uniq, inv, keys = words, np.arange(R), None
+                    src, new = [], []
+                    for i in range(len(uniq)):
+                        k = keys[i] if keys is not None else None
+                        if k is not None and k in self._cache:
+                            src.append(-1)
+                            hits[bi] += 1
+                        elif k is not None and k in pending:
+                            src.append(pending[k])
+                            hits[bi] += 1
+                        else:
+                            src.append(count)
+                            if k is not None:
+                                pending[k] = count
+                            first_batch[(tier, count)] = bi
+                            count += 1
+                            new.append(i)
+                    hits[bi] += R - len(uniq)
+                    if new:
+                        new = np.asarray(new)
+                        rows.append(uniq[new])
+                        ids.extend(batches[bi][1](gi, new, inv))
+                    plans[(bi, gi)] = (tier, uniq, inv, keys, src)
+                if count:
+                    ctx = _lib.Device.lane(self.device, lane) if len(order) > 1 else None
+                    futs[tier] = ex.submit(self._solve_group, tier[0], tier[1], np.concatenate(rows), ids, ctx)
+            solved = {tier: f.result() for tier, f in futs.items()}
         out = []
-        for bplans, hits in plans:
-            res, spent = [], 0.0
-            for uniq, inv, keys, src in bplans:
+        for bi, (groups, _) in enumerate(batches):
+            res = []
+            for gi in range(len(groups)):
+                tier, uniq, inv, keys, src = plans[(bi, gi)]
                 cu = np.empty((len(uniq), npts))
                 pj = np.empty(len(uniq))
-                for i, sref in enumerate(src):
-                    if sref[0] == "cache":
-                        cu[i], pj[i] = self._cache[sref[1]]
+                for i, r in enumerate(src):
+                    if r < 0:
+                        cu[i], pj[i] = self._cache[keys[i]]
                     else:
-                        curves, per_job = solved[sref[1]]
-                        cu[i], pj[i] = curves[sref[2]], per_job
-                res.append((cu[inv], pj[inv]))
-            out.append((res, hits, spent))
-        # nominal time spent on new jobs, attributed to the batch that first requested them
-        for bi, (bplans, _) in enumerate(plans):
-            spent = 0.0
-            for uniq, inv, keys, src in bplans:
-                for i, sref in enumerate(src):
-                    if sref[0] == "job" and not (keys is not None and keys[i] in self._cache):
-                        if keys is None or pending.get(keys[i]) == (sref[1], sref[2]):
-                            spent += solved[sref[1]][1]
+                        curves, per_job = solved[tier]
+                        cu[i], pj[i] = curves[r], per_job
+                        if first_batch[(tier, r)] == bi and (keys is None or keys[i] not in self._cache):
+                            spent[bi] += per_job
                             if keys is not None:
-                                self._cache[keys[i]] = (solved[sref[1]][0][sref[2]], solved[sref[1]][1])
-            out[bi] = (out[bi][0], out[bi][1], spent)
+                                self._cache[keys[i]] = (curves[r], per_job)
+                res.append((cu[inv], pj[inv]))
+            out.append((res, hits[bi], spent[bi]))
         return out
 
     def evaluate_masks(self, requests):
