@@ -57,6 +57,25 @@ DELTA = 0.01
 NPTS = 201
 
 
+# ncu DRAM bytes (read + write) of one hx_eval_idos_batch_device call of the dominant tier, the same masks
+# as the bench's tier (seeded), from a committed capture: (config, N) -> (profile, line prefix)
+TRAFFIC = {("c2", 2048): ("profiles/r01_traffic_L4_parent.txt", "total (hx kernels)")}
+
+
+def traffic_of(config, N):
+    """Bytes per launch from the committed ncu summary (None when there is no capture for this tier)."""
+    import re
+
+    path, prefix = TRAFFIC.get((config, N), (None, None))
+    if path is None or not (ROOT / path).exists():
+        return None
+    for line in (ROOT / path).read_text().splitlines():
+        if line.startswith(prefix):
+            m = re.search(r"= ([0-9.]+) GB", line)
+            return float(m.group(1)) * 1e9 if m else None
+    return None
+
+
 def env_rank():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
 
@@ -505,8 +524,10 @@ def main():
                        "l2": "flushed between timed steps (256 MB write)", "parallelism": f"replicas x{world} (rank r draws replicates [r*M, (r+1)*M) of each level stream; one all-reduce of level sums)",
                        "schedule": "all levels and both tiers of each level (parent nu, quarters nu/2) in flight at once on independent streams + contexts; largest tier on a high-priority stream",
                        "levels_note": "per-level ms from a separate sequential analysis pass (the timed step runs them concurrently)"},
-            "roofline": {"bound": "fp64", "kernel": f"batched eigensolve N={dom['N']}", "achieved": achieved,
-                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+            "roofline": {"bound": "tensor", "kernel": f"batched eigensolve N={dom['N']}", "achieved": achieved,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": traffic_of(args.config, dom["N"]),
+                         "traffic_source": TRAFFIC.get((args.config, dom["N"]), (None, None))[0],
                          "peak_source": "live cuBLAS ZGEMM 4096^3 complex128 on this GPU (best of 5)",
                          "flops_per_launch": dom["flops"] / max(1, dom["launches"]), "note": FRAC_NOTE,
                          "tiers": sorted(tiers.values(), key=lambda t: -t["ms"])},

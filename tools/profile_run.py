@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--passes", type=int, default=1)
     ap.add_argument("--warm", type=int, default=0)
     ap.add_argument("--concurrent", action="store_true", help="all levels at once (run_levels, as bench.py)")
+    ap.add_argument("--parent-only", action="store_true",
+                    help="only the parent (nu) tier of each selected level: one hx_eval_idos_batch_device call")
     args = ap.parse_args()
     kind, levels, nq, p, erange, _ = bench.CONFIGS[args.config]
     lo, hi = bench.grid_range(kind, erange)
@@ -35,6 +37,17 @@ def main():
         for inp in inputs:
             run.run_level(inp)
     torch.cuda.synchronize()
+    if args.parent_only:
+        for _ in range(args.passes):
+            for inp in inputs:
+                uniq = torch.unique(inp.parent, dim=0).contiguous()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                run._solve(inp.n, uniq, run.ctx, run.stream)
+                torch.cuda.synchronize()
+                print(f"level {inp.level} parent tier nu={inp.n} ({uniq.shape[0]} masks): "
+                      f"{1e3 * (time.perf_counter() - t0):.1f} ms", flush=True)
+        return
     if args.concurrent:
         for _ in range(args.warm):
             run.run_levels(inputs)
