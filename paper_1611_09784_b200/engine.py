@@ -35,6 +35,12 @@ __all__ = ["Engine", "TaskError", "LevelSampleSet", "ExhaustiveResult", "SLMC_ST
 
 SLMC_STREAM_OFFSET = 10_000
 
+# Compiled cells (device-resident instance tables) shared by every Engine of the process, keyed on the
+# (hashable, frozen) model, the supercell size and the device: the reference keeps the same per-process
+# cache in each worker (runner.py:98-111).  Rebuilding them per Engine costs a few ms of uploads, and
+# releasing them (cudaFree) synchronises the device.
+_CELL_CACHE: dict = {}
+
 
 class TaskError(RuntimeError):
     """One or more tasks failed; message names the task ids (runner.py:56-72)."""
@@ -103,7 +109,17 @@ class Engine:
 
     def cell(self, n: int):
         if n not in self._cells:
-            self._cells[n] = compile_cell(self.model, self.supercell(n), self.device)
+            try:
+                key = (self.model, n, self.device)
+                hash(key)
+            except TypeError:
+                key = None
+            if key is not None and key in _CELL_CACHE:
+                self._cells[n] = _CELL_CACHE[key]
+            else:
+                self._cells[n] = compile_cell(self.model, self.supercell(n), self.device)
+                if key is not None:
+                    _CELL_CACHE[key] = self._cells[n]
         return self._cells[n]
 
     def kpoints(self, n: int, q: int) -> np.ndarray:
@@ -157,9 +173,10 @@ class Engine:
         cache, against itself (np.unique over the rows instead of a per-request dict) and against the new
         masks of the EARLIER batches - the hit accounting of calling the batches one after another
         (runner.py:206-244).  Keys of different (n, q) never meet, so the planning runs one (n, q) tier at
-        a time, most expensive tier first, and each tier's GPU batch is submitted (its own thread and hx
-        context, the first on the high-priority one) as soon as it is planned: the host work of the
-        smaller tiers overlaps the device work of the big one.  Returns per batch ([(curves [R, npts],
+        a time, most expensive tier first, and the new masks each batch contributes to a tier are submitted
+        as their own GPU batch (own thread and hx context; the first tier's on the high-priority one) as
+        soon as they are planned: the host work of the smaller tiers overlaps the device work of the big
+        one, and the pieces of different levels run concurrently.  Returns per batch ([(curves [R, npts],
         per_job [R]) per group], hits, spent)."""
         npts = self.grid.npoints
         tiers: dict = {}  # (n, q) -> [(batch index, group index, words)] in batch order
@@ -171,13 +188,12 @@ class Engine:
         order = sorted(tiers, key=lambda g: -self.cell(g[0]).dim)
         hits = [0] * len(batches)
         spent = [0.0] * len(batches)
-        plans = {}  # (bi, gi) -> (uniq, inv, keys, src)
-        futs = {}
-        first_batch = {}  # (tier, row) -> batch that requested the new mask first
-        with ThreadPoolExecutor(max_workers=max(1, len(order))) as ex:
-            for lane, tier in enumerate(order):
+        plans = {}  # (bi, gi) -> (tier, uniq, inv, keys, src)
+        pieces = {}  # tier -> [(first new row, future)] in row order
+        lane = 0
+        with ThreadPoolExecutor(max_workers=max(1, sum(len(v) for v in tiers.values()))) as ex:
+            for tier in order:
                 pending = {}
-                rows, ids = [], []
                 count = 0
                 for bi, gi, words in tiers[tier]:
                     R = words.shape[0]
@@ -187,49 +203,54 @@ class Engine:
                         keys = [(tier[0], tier[1], row.tobytes()) for row in uniq]
                     else:
                         uniq, inv, keys = words, np.arange(R), None
-                    src, new = [], []
+                    src = np.empty(len(uniq), dtype=np.int64)
+                    start = count
                     for i in range(len(uniq)):
                         k = keys[i] if keys is not None else None
                         if k is not None and k in self._cache:
-                            src.append(-1)
-                            hits[bi] += 1
+                            src[i] = -1
                         elif k is not None and k in pending:
-                            src.append(pending[k])
-                            hits[bi] += 1
+                            src[i] = pending[k]
                         else:
-                            src.append(count)
+                            src[i] = count
                             if k is not None:
                                 pending[k] = count
-                            first_batch[(tier, count)] = bi
                             count += 1
-                            new.append(i)
-                    hits[bi] += R - len(uniq)
-                    if new:
-                        new = np.asarray(new)
-                        rows.append(uniq[new])
-                        ids.extend(batches[bi][1](gi, new, inv))
-                    plans[(bi, gi)] = (tier, uniq, inv, keys, src)
-                if count:
-                    ctx = _lib.Device.lane(self.device, lane) if len(order) > 1 else None
-                    futs[tier] = ex.submit(self._solve_group, tier[0], tier[1], np.concatenate(rows), ids, ctx)
-            solved = {tier: f.result() for tier, f in futs.items()}
+                    new = np.flatnonzero(src >= start)
+                    hits[bi] += R - len(new)
+                    if len(new):
+                        ids = batches[bi][1](gi, new, inv)
+                        ctx = _lib.Device.lane(self.device, lane) if len(tiers) > 1 or len(tiers[tier]) > 1 else None
+                        lane += 1
+                        pieces.setdefault(tier, []).append(
+                            (start, ex.submit(self._solve_group, tier[0], tier[1], uniq[new], ids, ctx)))
+                    plans[(bi, gi)] = (tier, uniq, inv, keys, src, start)
+            solved = {}
+            for tier, lst in pieces.items():
+                res = [f.result() for _, f in lst]
+                curves = np.concatenate([c for c, _ in res]) if len(res) > 1 else res[0][0]
+                per_job = np.concatenate([np.full(len(c), pj) for c, pj in res])
+                solved[tier] = (curves, per_job)
         out = []
         for bi, (groups, _) in enumerate(batches):
             res = []
             for gi in range(len(groups)):
-                tier, uniq, inv, keys, src = plans[(bi, gi)]
+                tier, uniq, inv, keys, src, start = plans[(bi, gi)]
                 cu = np.empty((len(uniq), npts))
                 pj = np.empty(len(uniq))
-                for i, r in enumerate(src):
-                    if r < 0:
-                        cu[i], pj[i] = self._cache[keys[i]]
-                    else:
-                        curves, per_job = solved[tier]
-                        cu[i], pj[i] = curves[r], per_job
-                        if first_batch[(tier, r)] == bi and (keys is None or keys[i] not in self._cache):
-                            spent[bi] += per_job
-                            if keys is not None:
-                                self._cache[keys[i]] = (curves[r], per_job)
+                got = src >= 0
+                if got.any():
+                    curves, per_job = solved[tier]
+                    cu[got] = curves[src[got]]
+                    pj[got] = per_job[src[got]]
+                for i in np.flatnonzero(~got):
+                    cu[i], pj[i] = self._cache[keys[i]]
+                # masks this batch solved first: their cost is this batch's, and they enter the run cache
+                own = np.flatnonzero(src >= start)
+                spent[bi] += float(pj[own].sum())
+                if keys is not None:
+                    for i in own:
+                        self._cache[keys[i]] = (cu[i], pj[i])
                 res.append((cu[inv], pj[inv]))
             out.append((res, hits[bi], spent[bi]))
         return out
