@@ -182,6 +182,8 @@ int hx_ctx_create_priority(int32_t device, int32_t priority, hx_ctx** out) {
     if (bm && bm[0]) ctx->bd_min_n = atoi(bm);
     const char* bw = getenv("HX_BIDIAG_WARP_MAX_S");
     if (bw && bw[0]) ctx->bidiag_warp_max_s = atoi(bw);
+    const char* zm = getenv("HX_ZONE_MIN_N");
+    if (zm && zm[0]) hx::g_zone_min_n = atoi(zm);
     const char* bt = getenv("HX_BIDIAG_THREADS");
     if (bt && bt[0]) ctx->bidiag_threads = atoi(bt);
   }

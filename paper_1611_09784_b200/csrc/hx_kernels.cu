@@ -10,6 +10,9 @@
 //    -> per-mask IDOS curves (qoi.py:96-102: values = counts / area, weights 1/nk).
 #include <cuda_runtime.h>
 #include <limits.h>
+#include <math.h>
+
+#include <cmath>
 #include <stdint.h>
 
 #include "hx_bidiag.cuh"
@@ -296,21 +299,14 @@ __device__ __forceinline__ double refine_tol(double lo, double hi, double pivmin
   return fmax(2.0 * DBL_EPSILON * m + pivmin, 1e-13 * fmax(1.0, m));
 }
 
-// Phase 2: bisection of the eigenvalues left unsettled by eig_idos_kernel, densely
-// packed (every lane of a warp has real work), then the IDOS contribution (+ the TGK mirror).
+// G lanes per item: G-point multisection (log2(G+1) bits per Sturm round) for the latency-bound case of
+// few items (large matrices); shared by the bisection and the zone refinement passes.
 template <bool TGK>
-__global__ void __launch_bounds__(128) eig_refine_kernel(CellDev c, int nk, GridDev g, const double* __restrict__ tri,
-                                                         size_t tri_stride, const int* __restrict__ dims, int* diff,
-                                                         unsigned long long* trans, int* status, int sharp,
-                                                         const RefineItem* __restrict__ items,
-                                                         const unsigned long long* __restrict__ count) {
-  const unsigned long long n = *count;
+__device__ void refine_multisection(const CellDev& c, int nk, const GridDev& g, const double* __restrict__ tri,
+                                    size_t tri_stride, const int* __restrict__ dims, int* diff,
+                                    unsigned long long* trans, int* status, int sharp,
+                                    const RefineItem* __restrict__ items, unsigned long long n, int G) {
   const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
-  // G lanes per item: G-point multisection (log2(G+1) bits per Sturm round).  Few items (large matrices)
-  // are latency-bound and get up to 8 lanes each; many items are throughput-bound and keep one thread.
-  int G = 1;
-  while (G < 8 && n * (unsigned long long)(2 * G) * 2 <= nthreads) G *= 2;
-  if (G > 1) {
     const int lane = threadIdx.x & 31, sub = lane % G, base = lane - sub;
     const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << base;
     const unsigned long long ngroups = nthreads / G;
@@ -351,6 +347,24 @@ __global__ void __launch_bounds__(128) eig_refine_kernel(CellDev c, int nk, Grid
         if (it.flags & 2) add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, -lam);
       }
     }
+}
+
+// Phase 2: bisection of the eigenvalues left unsettled by eig_idos_kernel, densely
+// packed (every lane of a warp has real work), then the IDOS contribution (+ the TGK mirror).
+template <bool TGK>
+__global__ void __launch_bounds__(128) eig_refine_kernel(CellDev c, int nk, GridDev g, const double* __restrict__ tri,
+                                                         size_t tri_stride, const int* __restrict__ dims, int* diff,
+                                                         unsigned long long* trans, int* status, int sharp,
+                                                         const RefineItem* __restrict__ items,
+                                                         const unsigned long long* __restrict__ count) {
+  const unsigned long long n = *count;
+  const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+  // G lanes per item: G-point multisection (log2(G+1) bits per Sturm round).  Few items (large matrices)
+  // are latency-bound and get up to 8 lanes each; many items are throughput-bound and keep one thread.
+  int G = 1;
+  while (G < 8 && n * (unsigned long long)(2 * G) * 2 <= nthreads) G *= 2;
+  if (G > 1) {
+    refine_multisection<TGK>(c, nk, g, tri, tri_stride, dims, diff, trans, status, sharp, items, n, G);
     return;
   }
   for (unsigned long long q = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; q < n;
@@ -373,6 +387,275 @@ __global__ void __launch_bounds__(128) eig_refine_kernel(CellDev c, int nk, Grid
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Zone path of the eigenvalue stage (IDOS only, no eigenvalue output).
+//
+// Every eigenvalue contributes to the curve through the reference's index arithmetic
+// (_kernels.py:68-101): a full weight from lo = ceil((E + delta - e0)/step) on, and transition terms for
+// the grid points within delta of E.  Around every grid energy e_m lies a transition zone
+// Z_m = [e_m - w - eta, e_m + w + eta] (w = delta, or 0 for the sharp counts; eta = 4e-12 max(1, |E|)
+// covers the rounding of the reference's own quotients).  An eigenvalue between Z_{m-1} and Z_m
+// contributes exactly a full weight at index m - nothing else depends on where it lies in that gap - so
+// the gap populations follow from Sturm counts at the 2 npts zone edges alone (one thread per zone, two
+// interleaved recurrences), and only the eigenvalues inside a zone (about 2(w + eta)/step of them) are
+// located, by a Newton-accelerated bracketed search from the zone's own bracket (zone_refine_kernel).
+// For a matrix of dimension d this costs 2 npts + (zone eigenvalues) x (a few) Sturm counts instead of
+// ~d/2 x (8 .. 14) bisection steps plus the refinement of the zone eigenvalues from a full-width start.
+
+// Inverse of pencil_map (E -> lambda) on the branch 1 + s lambda > 0.
+__host__ __device__ __forceinline__ double pencil_inv(int pencil, double eps0, double t, double s, double E) {
+  if (pencil != 1) return E;
+  return (E - eps0) / (t - s * E);
+}
+
+// lambda-space bracket [la, lb] of zone m.
+__device__ __forceinline__ void zone_bracket(const CellDev& c, const GridDev& g, int sharp, int m, double& la,
+                                             double& lb) {
+  const double em = __dadd_rn(g.e0, __dmul_rn(g.step, (double)m));
+  const double w = sharp ? 0.0 : g.delta;
+  double Elo = em - w, Ehi = em + w;
+  Elo -= 4e-12 * fmax(1.0, fabs(Elo));
+  Ehi += 4e-12 * fmax(1.0, fabs(Ehi));
+  const double a = pencil_inv(c.pencil, c.eps0, c.t, c.s, Elo), b = pencil_inv(c.pencil, c.eps0, c.t, c.s, Ehi);
+  la = fmin(a, b);
+  lb = fmax(a, b);
+}
+
+// One CTA per matrix.  counts[2m] / counts[2m+1]: eigenvalues below the lower / upper lambda edge of zone m
+// (dynamic shared memory, 2 npts ints).  rev: E decreases with lambda.
+template <bool ZD>
+__global__ void __launch_bounds__(256) zone_count_kernel(CellDev c, int nk, GridDev g, int sharp, int rev,
+                                                         int64_t mat0, int64_t nmat, const double* __restrict__ tri,
+                                                         size_t tri_stride, const int* __restrict__ dims, int* diff,
+                                                         RefineItem* refine, unsigned long long* refine_count) {
+  extern __shared__ int zc[];
+  __shared__ double red[3][32];
+  const int64_t lm = blockIdx.x;
+  if (lm >= nmat) return;
+  const int d = dims[lm];
+  if (d <= 0) return;
+  const int N = c.N, npts = g.npts;
+  const int64_t mat = mat0 + lm;
+  const int64_t mk = mat / nk;
+  const double* diag = tri + lm * tri_stride;
+  const double* e2 = diag + N;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  // Gershgorin interval and pivmin (dstebz conventions, as eig_idos_kernel)
+  double gl = 1e308, gu = -1e308, em = 0.0;
+  for (int i = tid; i < d; i += blockDim.x) {
+    const double el = i > 0 ? sqrt(e2[i - 1]) : 0.0;
+    const double er2 = i + 1 < d ? e2[i] : 0.0;
+    const double er = sqrt(er2);
+    const double di = ZD ? 0.0 : diag[i];
+    gl = fmin(gl, di - el - er);
+    gu = fmax(gu, di + el + er);
+    em = fmax(em, er2);
+  }
+  gl = warp_min(gl);
+  gu = warp_max(gu);
+  em = warp_max(em);
+  if (lane == 0) {
+    red[0][warp] = gl;
+    red[1][warp] = gu;
+    red[2][warp] = em;
+  }
+  __syncthreads();
+  gl = red[0][0];
+  gu = red[1][0];
+  em = red[2][0];
+  for (int w = 1; w < nw; ++w) {
+    gl = fmin(gl, red[0][w]);
+    gu = fmax(gu, red[1][w]);
+    em = fmax(em, red[2][w]);
+  }
+  const double pivmin = DBL_MIN * fmax(1.0, em);
+  const double tnorm = fmax(fabs(gl), fabs(gu));
+  gl = gl - 2.1 * tnorm * DBL_EPSILON * d - 4.2 * pivmin;
+  gu = gu + 2.1 * tnorm * DBL_EPSILON * d + 4.2 * pivmin;
+  for (int m = tid; m < npts; m += blockDim.x) {
+    double xa, xb;
+    zone_bracket(c, g, sharp, m, xa, xb);
+    // two interleaved Sturm recurrences (edges outside the Gershgorin interval are trivial)
+    const bool ra = xa > gl && xa < gu, rb = xb > gl && xb < gu;
+    int ca = xa <= gl ? 0 : d, cb = xb <= gl ? 0 : d;
+    if (ra || rb) {
+      double qa = (ZD ? 0.0 : diag[0]) - xa, qb = (ZD ? 0.0 : diag[0]) - xb;
+      if (fabs(qa) <= pivmin) qa = -pivmin;
+      if (fabs(qb) <= pivmin) qb = -pivmin;
+      int na = qa < 0.0, nb = qb < 0.0;
+      for (int i = 1; i < d; ++i) {
+        const double e = e2[i - 1], a = ZD ? 0.0 : diag[i];
+        qa = fma(-e, sturm_rcp(qa), a - xa);
+        qb = fma(-e, sturm_rcp(qb), a - xb);
+        if (fabs(qa) <= pivmin) qa = -pivmin;
+        if (fabs(qb) <= pivmin) qb = -pivmin;
+        na += qa < 0.0;
+        nb += qb < 0.0;
+      }
+      if (ra) ca = na;
+      if (rb) cb = nb;
+    }
+    zc[2 * m] = ca;
+    zc[2 * m + 1] = max(ca, cb);
+  }
+  __syncthreads();
+  int* drow = diff + mk * (npts + 1);
+  for (int m = tid; m < npts; m += blockDim.x) {
+    // gap below zone m (in E): settles at index m
+    int n;
+    if (!rev) n = zc[2 * m] - (m > 0 ? zc[2 * m - 1] : 0);
+    else n = (m > 0 ? zc[2 * m - 2] : d) - zc[2 * m + 1];
+    if (n > 0) atomicAdd(drow + m, n);
+    // eigenvalues inside zone m: refinement items from the zone's own bracket
+    const int i0 = zc[2 * m], nz = zc[2 * m + 1] - i0;
+    if (nz > 0) {
+      double xa, xb;
+      zone_bracket(c, g, sharp, m, xa, xb);
+      const unsigned long long pos = atomicAdd(refine_count, (unsigned long long)nz);
+      for (int k = 0; k < nz; ++k)
+        refine[pos + k] = RefineItem{mat, lm, i0 + k, (int)(1u | ((unsigned)k << 2) | ((unsigned)nz << 17)),
+                                     fmax(xa, gl), fmin(xb, gu), pivmin};
+    }
+  }
+}
+
+// Sturm count below x and, with it, s = d/dx log|det(T - x)| = sum_i q_i'/q_i (q_i' = -1 + e q_{i-1}'/q_{i-1}^2).
+template <bool ZD>
+__device__ __forceinline__ int sturm_count_deriv(const double* __restrict__ diag, const double* __restrict__ e2, int d,
+                                                 double x, double pivmin, double& s) {
+  double q = (ZD ? 0.0 : diag[0]) - x;
+  if (fabs(q) <= pivmin) q = -pivmin;
+  int cnt = q < 0.0;
+  double r = sturm_rcp(q), dq = -1.0;
+  double acc = -r;
+  for (int i = 1; i < d; ++i) {
+    const double e = e2[i - 1];
+    const double er = e * r;
+    q = fma(-e, r, (ZD ? 0.0 : diag[i]) - x);
+    dq = fma(er * r, dq, -1.0);
+    if (fabs(q) <= pivmin) q = -pivmin;
+    cnt += q < 0.0;
+    r = sturm_rcp(q);
+    acc = fma(dq, r, acc);
+  }
+  s = acc;
+  return cnt;
+}
+
+// Eigenvalue idx of the tridiagonal inside [lo, hi] (clo / chi: Sturm counts at lo / hi) to the
+// refinement tolerance.  Bisection until the bracket isolates the eigenvalue (chi - clo == 1), then a
+// safeguarded Newton iteration on det(T - x) (rtsafe rules: a Newton step is taken only when it stays in
+// the bracket and at least halves the previous step, else bisection); every trial point's Sturm count
+// shrinks the bracket, and a converged iterate is certified by closing the bracket around it with two
+// counts.  Exact (or sub-tolerance) multiple eigenvalues never isolate and finish by bisection.
+template <bool ZD>
+__device__ double zone_locate(const double* diag, const double* e2, int d, int idx, double lo, double hi, int clo,
+                              int chi, double pivmin) {
+  for (int it = 0; it < 200 && chi - clo > 1; ++it) {
+    if (hi - lo <= refine_tol(lo, hi, pivmin)) return 0.5 * (lo + hi);
+    const double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) return mid;
+    const int cm = sturm_count_fast<ZD>(diag, e2, d, mid, pivmin);
+    if (cm > idx) {
+      hi = mid;
+      chi = cm;
+    } else {
+      lo = mid;
+      clo = cm;
+    }
+  }
+  double x = 0.5 * (lo + hi), dxold = hi - lo, dx = dxold;
+  for (int it = 0; it < 200; ++it) {
+    double tol = refine_tol(lo, hi, pivmin);
+    if (hi - lo <= tol) break;
+    double sd;
+    const int cnt = sturm_count_deriv<ZD>(diag, e2, d, x, pivmin, sd);
+    if (cnt > idx) hi = x;
+    else lo = x;
+    tol = refine_tol(lo, hi, pivmin);
+    if (hi - lo <= tol) break;
+    const double nstep = (sd != 0.0 && isfinite(sd)) ? 1.0 / sd : 0.0;
+    if (nstep != 0.0 && fabs(nstep) <= 0.25 * tol) {
+      // converged (the step is below the tolerance, possibly below an ulp of x).  The bracket isolates
+      // the eigenvalue (one root of det(T - x) in it), so the Newton point is within d |step| of it
+      // (Laguerre's bound; in practice ~step^2): accept it.
+      const double xc = fmin(fmax(x - nstep, lo), hi);
+      if (chi - clo == 1) return xc;
+      const double a = fmax(lo, xc - 0.5 * tol), b = fmin(hi, xc + 0.5 * tol);
+      if (a > lo) {
+        if (sturm_count_fast<ZD>(diag, e2, d, a, pivmin) > idx) hi = a;
+        else lo = a;
+      }
+      if (b < hi && b > lo) {
+        if (sturm_count_fast<ZD>(diag, e2, d, b, pivmin) > idx) hi = b;
+        else lo = b;
+      }
+      x = 0.5 * (lo + hi);
+      dxold = dx = hi - lo;
+      continue;
+    }
+    const double xn = x - nstep;
+    if (nstep == 0.0 || !(xn > lo && xn < hi) || fabs(2.0 * nstep) > fabs(dxold)) {
+      dxold = dx;
+      dx = 0.5 * (hi - lo);
+      x = lo + dx;
+      if (x <= lo || x >= hi) break;
+      continue;
+    }
+    dxold = dx;
+    dx = nstep;
+    x = xn;
+  }
+  return 0.5 * (lo + hi);
+}
+
+template <bool ZD>
+__global__ void __launch_bounds__(128) zone_refine_kernel(CellDev c, int nk, GridDev g, const double* __restrict__ tri,
+                                                          size_t tri_stride, const int* __restrict__ dims, int* diff,
+                                                          unsigned long long* trans, int* status, int sharp,
+                                                          const RefineItem* __restrict__ items,
+                                                          const unsigned long long* __restrict__ count) {
+  const unsigned long long n = *count;
+  const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+  // few items (large matrices): the slowest item bounds the launch, so use G-lane multisection with its
+  // fixed round count; many items: one thread per item, Newton (about 11 Sturm counts on average)
+  int G = 1;
+  while (G < 8 && n * (unsigned long long)(2 * G) * 2 <= nthreads) G *= 2;
+  if (G >= 4) {
+    refine_multisection<ZD>(c, nk, g, tri, tri_stride, dims, diff, trans, status, sharp, items, n, G);
+    return;
+  }
+  for (unsigned long long q = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += nthreads) {
+    const RefineItem it = items[q];
+    const double* diag = tri + it.lm * tri_stride;
+    // flags: bit 0 set; bits 2..16: k = idx - (count at lo); bits 17..31: eigenvalues in the zone
+    const unsigned f = (unsigned)it.flags;
+    const int k = (int)((f >> 2) & 0x7fffu), nz = (int)(f >> 17);
+    const int clo = it.idx - k;
+    const double lam = zone_locate<ZD>(diag, diag + c.N, dims[it.lm], it.idx, it.lo, it.hi, clo, clo + nz, it.pivmin);
+    add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, lam);
+  }
+}
+
+// Host-side applicability of the zone path: non-overlapping zones and an inverse pencil map that is
+// monotone (one branch) over the whole energy grid.
+static bool zone_path_ok(const CellDev& c, const GridDev& g, int sharp, bool& rev) {
+  const double w = sharp ? 0.0 : g.delta;
+  const double hi_e = g.e0 + g.step * (g.npts - 1);
+  const double margin = 8e-12 * std::max(1.0, std::max(std::fabs(g.e0), std::fabs(hi_e)));
+  if (!(2.0 * (w + margin) < 0.95 * g.step)) return false;
+  rev = (c.pencil == 1) && (c.t - c.s * c.eps0 < 0.0);
+  if (c.pencil == 1) {
+    // lambda(E) = (E - eps0) / (t - s E) stays on one branch: t - s E keeps its sign over the grid
+    const double a = c.t - c.s * (g.e0 - w - 1.0), b = c.t - c.s * (hi_e + w + 1.0);
+    if (!(a * b > 0.0)) return false;
+    if ((c.t - c.s * c.eps0) * a <= 0.0) return false;
+  }
+  return (size_t)g.npts * 2 * sizeof(int) <= 96 * 1024;
+}
+
+int g_zone_min_n = 96;
+
 void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, int64_t nmat, const double* tri,
                      size_t tri_stride, const int* dims, int* diff, unsigned long long* trans, double* eigs,
                      int* status, int sharp, cudaStream_t st, RefineItem* refine, unsigned long long* refine_count,
@@ -381,6 +664,31 @@ void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, i
   const int64_t slots = nmat * per;
   const bool two_pass = refine && refine_count && diff && !eigs;
   if (two_pass) cudaMemsetAsync(refine_count, 0, sizeof(unsigned long long), st);
+  bool rev = false;
+  // zone path: 2 npts Sturm counts per matrix beat ~d/2 x 10 bisection steps from d ~ 96 on
+  if (two_pass && c.N >= g_zone_min_n && zone_path_ok(c, g, sharp, rev)) {
+    const size_t zsm = (size_t)g.npts * 2 * sizeof(int);
+    const int zt = g.npts >= 256 ? 256 : ((g.npts + 31) / 32) * 32;
+    if (tgk) {
+      set_smem_attr(zone_count_kernel<true>, zsm);
+      zone_count_kernel<true><<<(unsigned)nmat, zt, zsm, st>>>(c, nk, g, sharp, rev, mat0, nmat, tri, tri_stride,
+                                                              dims, diff, refine, refine_count);
+    } else {
+      set_smem_attr(zone_count_kernel<false>, zsm);
+      zone_count_kernel<false><<<(unsigned)nmat, zt, zsm, st>>>(c, nk, g, sharp, rev, mat0, nmat, tri, tri_stride,
+                                                               dims, diff, refine, refine_count);
+    }
+    count_launch();
+    const int64_t rblocks = 148 * 16;
+    if (tgk)
+      zone_refine_kernel<true><<<(unsigned)rblocks, 128, 0, st>>>(c, nk, g, tri, tri_stride, dims, diff, trans, status,
+                                                                  sharp, refine, refine_count);
+    else
+      zone_refine_kernel<false><<<(unsigned)rblocks, 128, 0, st>>>(c, nk, g, tri, tri_stride, dims, diff, trans,
+                                                                   status, sharp, refine, refine_count);
+    count_launch();
+    return;
+  }
   const unsigned blocks = (unsigned)((slots + 127) / 128);
   RefineItem* rf = two_pass ? refine : nullptr;
   if (tgk)
