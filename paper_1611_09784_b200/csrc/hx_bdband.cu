@@ -30,6 +30,9 @@
 
 namespace hx {
 
+bool g_bd_chase_pair = true;  // warp-pair bulge chase (HX_CHASE_PAIR=0: one warp per task)
+
+
 constexpr int BB = 32;  // band width
 
 static std::string g_bd_err;
@@ -194,7 +197,20 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     cfg.numAttrs = 1;                                                                                   \
     BD_CUDA(cudaLaunchKernelEx(&cfg, bd_chase_kernel<NW, BB, DUAL, CL>, ws, a1, a2, a3, S, dims)); \
   }
-  if (want >= 6) {
+#define BD_CHASE_PAIR(NT)                                                                                \
+  {                                                                                                     \
+    bd_chase_pair_kernel<NT, BB><<<(unsigned)cnt, NT * 64, bd_chase_pair_smem<NT, BB>(), st>>>(ws, a1, a2, a3, S, \
+                                                                                                 dims);  \
+    BD_CUDA(cudaGetLastError());                                                                        \
+  }
+  const bool pair = chase_mode >= 4 || (chase_mode == 0 && g_bd_chase_pair);
+  // warp-pair tasks for the throughput-bound launches (many matrices); the latency-bound one-CTA-per-matrix
+  // launch keeps one warp per task (its shared-memory pipe is the limit, measured 24.3 vs 25.1 ms)
+  if (pair && (want < 6 || chase_mode >= 4)) {
+    if (want >= 6) BD_CHASE_PAIR(10)
+    else if (want >= 2) BD_CHASE_PAIR(2)
+    else BD_CHASE_PAIR(1)
+  } else if (want >= 6) {
     // one CTA (11 sweeps in flight) per matrix: in the concurrent tier schedule the 2-CTA cluster variant
     // (16 sweeps, 3-6 % lower latency alone) costs more than it gains by occupying twice the SMs
     if (chase_mode == 2) BD_CHASE(8, false, 2)
@@ -205,6 +221,7 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
   } else {
     BD_CHASE(1, false, 1)
   }
+#undef BD_CHASE_PAIR
 #undef BD_CHASE
   count_launch();
   BD_CUDA(cudaGetLastError());
@@ -227,6 +244,11 @@ void bd_init_attributes() {
   BD_CHASE_ATTR(11, false, 1);
   BD_CHASE_ATTR(8, false, 2);
 #undef BD_CHASE_ATTR
+  set_smem_attr(bd_chase_pair_kernel<1, BB>, bd_chase_pair_smem<1, BB>());
+  set_smem_attr(bd_chase_pair_kernel<2, BB>, bd_chase_pair_smem<2, BB>());
+  set_smem_attr(bd_chase_pair_kernel<10, BB>, bd_chase_pair_smem<10, BB>());
+  const char* pe = getenv("HX_CHASE_PAIR");
+  if (pe && pe[0]) g_bd_chase_pair = atoi(pe) != 0;
 }
 
 int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, int64_t nmasks, const GridDev& g,

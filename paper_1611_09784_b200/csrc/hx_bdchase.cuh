@@ -321,6 +321,279 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
   if (CL > 1) cooperative_groups::this_cluster().sync();  // remote pollers may still read our counters
 }
 
+// ---------------------------------------------------------------------------------------------------
+// Warp-pair variant: every task is split over two warps (64 threads, a pair of one "slot"), halving the
+// serial instruction stream of a task (the chase is bound by the latency of one task times the sweep
+// stagger, and by the issue rate of the few tasks in flight).  Lane = row in the row-oriented phases
+// (each warp takes 16 of the 32 tile columns), lane = column in the column-oriented phases (each warp
+// takes 16 of the 32 tile rows); the half sums meet in shared memory behind a 64-thread named barrier.
+// Reflectors are built redundantly by both warps from the combined sums (identical values, each warp
+// keeps its own copy), so only the partial sums cross warps.  The Y tile is loaded into the X buffer
+// after the X update: each warp overwrites exactly the columns it alone reads in the row phases.
+template <int BWc>
+struct BdPairSmem {
+  double2 X[BWc][BWc + 1];  // X, then Y (zero-padded)
+  double2 ug[2][BWc];       // right reflector vector, per warp
+  double2 vh[2][BWc];       // left reflector vector, per warp
+  double2 cb[2][BWc];       // per-column update coefficients, per warp
+  double2 part[2][2][BWc];  // [buffer][half][row or column] partial sums (alternating buffers)
+};
+
+__device__ __forceinline__ void pair_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+
+template <int NT, int BWc>
+__global__ void __launch_bounds__(NT * 64, NT <= 2 ? 4 : 1) bd_chase_pair_kernel(double2* ws, size_t stride, size_t c_off,
+                                                                    size_t tgk_off, int S, const int* dims) {
+  static_assert(BWc == 32, "lane = row / column of a 32-wide tile");
+  static_assert(NT <= 15, "one named barrier per slot");
+  constexpr int HW = BWc / 2;
+  extern __shared__ __align__(16) unsigned char bd_smem[];
+  BdPairSmem<BWc>* all = reinterpret_cast<BdPairSmem<BWc>*>(bd_smem);
+  volatile int* prog = reinterpret_cast<volatile int*>(all + NT);
+  const int lane = threadIdx.x & 31, slot = threadIdx.x >> 6, h = (threadIdx.x >> 5) & 1;
+  const int bar = 1 + slot;
+  BdPairSmem<BWc>& W = all[slot];
+  double2* const ug = W.ug[h];
+  double2* const vh = W.vh[h];
+  double2* const cb = W.cb[h];
+  const int64_t mat = blockIdx.x;
+  double2* base = ws + (size_t)mat * stride;
+  double2* C = base + c_off;
+  double* diag = reinterpret_cast<double*>(base + tgk_off);
+  double* e2 = diag + 2 * S;
+  const int ld = S;
+  const double2 zero = make_double2(0.0, 0.0);
+  for (int q = threadIdx.x; q < 2 * S; q += blockDim.x) {
+    diag[q] = 0.0;
+    e2[q] = 0.0;
+  }
+  if (threadIdx.x < NT) prog[threadIdx.x] = -1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double2 a0 = C[0];
+    e2[0] = a0.x * a0.x + a0.y * a0.y;  // alpha_0: final after stage 1
+  }
+  const bool skip = dims && dims[mat] == 0;
+  const int nsweeps = skip ? 0 : S - 1;
+  const int c0 = h * HW;  // this warp's columns (row phases) / rows (column phases)
+  int pb = 0;             // alternating partial-sum buffer
+  for (int i = slot; i < nsweeps; i += NT) {
+    const int tasks = (S - 1 - i + BWc - 1) / BWc;
+    const int prev_tasks = i > 0 ? (S - i + BWc - 1) / BWc : 0;
+    volatile int* pflag = prog + (i - 1 + NT) % NT;
+    double taug = 0.0;
+    for (int t = 0; t < tasks; ++t) {
+      if (i > 0) {
+        const int need = (i - 1) * 65536 + min(t + 2, prev_tasks);
+        if (lane == 0)
+          while (*pflag < need) __nanosleep(NT >= 6 ? 20 : 100);
+        __syncwarp();
+        __threadfence_block();
+      }
+      const int s = i + 1 + t * BWc;
+      const int len = min(BWc, S - s);
+      const int lb = max(0, min(BWc, S - s - len));
+      double2* const blk = C + ((size_t)s * ld + s + lane);
+      // ---- X tile, this warp's 16 columns
+      {
+        const double2* src = blk + (size_t)c0 * ld;
+        if (len == BWc) {
+#pragma unroll
+          for (int cc = 0; cc < HW; ++cc, src += ld) bd_cp_async16<false>(&W.X[lane][c0 + cc], src);
+        } else {
+#pragma unroll 4
+          for (int cc = 0; cc < HW; ++cc, src += ld) {
+            if (lane < len && c0 + cc < len) bd_cp_async16<false>(&W.X[lane][c0 + cc], src);
+            else W.X[lane][c0 + cc] = zero;
+          }
+        }
+      }
+      if (t == 0) {
+        // right reflector from row i, columns [s, s+len) (both warps, identical values)
+        double2 x = zero;
+        if (lane < len) {
+          const double2 z = C[(size_t)(s + lane) * ld + i];
+          x = make_double2(z.x, -z.y);
+        }
+        const double sig2 = warp_sum(x.x * x.x + x.y * x.y);
+        const double2 al = make_double2(__shfl_sync(0xffffffffu, x.x, 0), __shfl_sync(0xffffffffu, x.y, 0));
+        const QuickReflector hq = quick_reflector(al, sig2);
+        taug = hq.tau;
+        ug[lane] = lane == 0 ? make_double2(1.0, 0.0) : (lane < len ? cmul(x, hq.scale) : zero);
+        if (h == 0) {
+          if (lane < len && taug != 0.0)
+            C[(size_t)(s + lane) * ld + i] = lane == 0 ? make_double2(hq.beta.x, -hq.beta.y) : zero;
+          if (lane == 0) e2[2 * i + 1] = sig2;
+        }
+      }
+      bd_cp_async_wait_all();
+      pair_bar(bar);  // B1: both column halves of X in shared memory
+      // ---- X row pass (lane = row): ty = tau_g (X u)_r over both halves
+      {
+        double2 a0 = zero, a1 = zero;
+#pragma unroll
+        for (int c = c0; c < c0 + HW; c += 2) {
+          const double2 x0 = W.X[lane][c], u0 = ug[c], x1 = W.X[lane][c + 1], u1 = ug[c + 1];
+          a0.x = fma(x0.x, u0.x, fma(-x0.y, u0.y, a0.x));
+          a0.y = fma(x0.x, u0.y, fma(x0.y, u0.x, a0.y));
+          a1.x = fma(x1.x, u1.x, fma(-x1.y, u1.y, a1.x));
+          a1.y = fma(x1.x, u1.y, fma(x1.y, u1.x, a1.y));
+        }
+        W.part[pb][h][lane] = make_double2(a0.x + a1.x, a0.y + a1.y);
+      }
+      pair_bar(bar);  // B2
+      double2 ty;
+      {
+        const double2 p0 = W.part[pb][0][lane], p1 = W.part[pb][1][lane];
+        ty = make_double2(taug * (p0.x + p1.x), taug * (p0.y + p1.y));
+      }
+      pb ^= 1;
+      const double2 x00 = W.X[lane][0];
+      const double2 x0 = make_double2(x00.x - ty.x, x00.y - ty.y);
+      const double sh2 = warp_sum(x0.x * x0.x + x0.y * x0.y);
+      const double2 ah = make_double2(__shfl_sync(0xffffffffu, x0.x, 0), __shfl_sync(0xffffffffu, x0.y, 0));
+      const QuickReflector hh = quick_reflector(ah, sh2);
+      const double tauh = hh.tau;
+      if (t == 0 && h == 0 && lane == 0) e2[2 * s] = sh2;
+      const double2 v = lane == 0 ? make_double2(1.0, 0.0) : cmul(x0, hh.scale);  // zero on padded rows
+      vh[lane] = v;
+      const double2 w = warp_csum(cmul_cj(v, ty));  // v^H (tau_g y)
+      __syncwarp();
+      // ---- X column pass (lane = column): p = v^H X over this warp's 16 rows
+      {
+        double2 a0 = zero, a1 = zero;
+#pragma unroll
+        for (int r = c0; r < c0 + HW; r += 2) {
+          const double2 v0 = vh[r], x0c = W.X[r][lane], v1 = vh[r + 1], x1c = W.X[r + 1][lane];
+          a0.x = fma(v0.x, x0c.x, fma(v0.y, x0c.y, a0.x));
+          a0.y = fma(v0.x, x0c.y, fma(-v0.y, x0c.x, a0.y));
+          a1.x = fma(v1.x, x1c.x, fma(v1.y, x1c.y, a1.x));
+          a1.y = fma(v1.x, x1c.y, fma(-v1.y, x1c.x, a1.y));
+        }
+        W.part[pb][h][lane] = make_double2(a0.x + a1.x, a0.y + a1.y);
+      }
+      pair_bar(bar);  // B3: partials written; both warps are done reading the other half of X
+      {
+        const double2 p0 = W.part[pb][0][lane], p1 = W.part[pb][1][lane];
+        const double2 u = ug[lane];
+        const double2 wu = make_double2(w.x * u.x + w.y * u.y, w.y * u.x - w.x * u.y);  // w conj(u)
+        cb[lane] = make_double2(tauh * (p0.x + p1.x - wu.x), tauh * (p0.y + p1.y - wu.y));
+      }
+      pb ^= 1;
+      __syncwarp();
+      // ---- X: fused rank-2 row update of this warp's columns, straight to HBM:
+      //      X' = X - ty conj(u) - v b   (column 0 of row 0 -> beta_h, rest of column 0 -> 0)
+      if (lane < len) {
+        double2* dst = blk + (size_t)c0 * ld;
+#pragma unroll
+        for (int c = c0; c < c0 + HW; ++c, dst += ld) {
+          const double2 u = ug[c], b = cb[c];
+          double2 z = W.X[lane][c];
+          z.x = fma(-ty.x, u.x, fma(-ty.y, u.y, fma(-v.x, b.x, fma(v.y, b.y, z.x))));
+          z.y = fma(-ty.y, u.x, fma(ty.x, u.y, fma(-v.x, b.y, fma(-v.y, b.x, z.y))));
+          if (c == 0 && tauh != 0.0) z = lane == 0 ? hh.beta : zero;
+          if (c < len) *dst = z;
+        }
+      }
+      double next_tau = 0.0;
+      if (lb > 0) {
+        // ---- Y tile into the X buffer, this warp's columns (it alone reads them from here on in row phases)
+        {
+          __syncwarp();
+          const double2* src = blk + (size_t)(len + c0) * ld;
+          if (len == BWc && lb == BWc) {
+#pragma unroll
+            for (int cc = 0; cc < HW; ++cc, src += ld) bd_cp_async16<false>(&W.X[lane][c0 + cc], src);
+          } else {
+#pragma unroll 4
+            for (int cc = 0; cc < HW; ++cc, src += ld) {
+              if (lane < len && c0 + cc < lb) bd_cp_async16<false>(&W.X[lane][c0 + cc], src);
+              else W.X[lane][c0 + cc] = zero;
+            }
+          }
+          bd_cp_async_wait_all();
+        }
+        pair_bar(bar);  // B4: both halves of Y loaded
+        // ---- Y column pass (lane = column): q = v^H Y over this warp's rows
+        {
+          double2 a0 = zero, a1 = zero;
+#pragma unroll
+          for (int r = c0; r < c0 + HW; r += 2) {
+            const double2 v0 = vh[r], y0c = W.X[r][lane], v1 = vh[r + 1], y1c = W.X[r + 1][lane];
+            a0.x = fma(v0.x, y0c.x, fma(v0.y, y0c.y, a0.x));
+            a0.y = fma(v0.x, y0c.y, fma(-v0.y, y0c.x, a0.y));
+            a1.x = fma(v1.x, y1c.x, fma(v1.y, y1c.y, a1.x));
+            a1.y = fma(v1.x, y1c.y, fma(-v1.y, y1c.x, a1.y));
+          }
+          W.part[pb][h][lane] = make_double2(a0.x + a1.x, a0.y + a1.y);
+        }
+        pair_bar(bar);  // B5
+        double2 q;
+        {
+          const double2 p0 = W.part[pb][0][lane], p1 = W.part[pb][1][lane];
+          q = make_double2(p0.x + p1.x, p0.y + p1.y);
+        }
+        pb ^= 1;
+        const double2 y0 = W.X[0][lane];
+        const double2 xg = make_double2(y0.x - tauh * q.x, -(y0.y - tauh * q.y));  // conj(row 0 of H Y)
+        const double sg2 = warp_sum(xg.x * xg.x + xg.y * xg.y);
+        const double2 al = make_double2(__shfl_sync(0xffffffffu, xg.x, 0), __shfl_sync(0xffffffffu, xg.y, 0));
+        const QuickReflector hg = quick_reflector(al, sg2);
+        next_tau = hg.tau;
+        const double2 u2 = lane == 0 ? make_double2(1.0, 0.0) : cmul(xg, hg.scale);  // zero on padded columns
+        const double2 qu = warp_csum(cmul(q, u2));                                    // (v^H Y) u'
+        ug[lane] = u2;  // this warp's copy: its X update (the last reader) is done
+        cb[lane] = make_double2(tauh * q.x, tauh * q.y);  // d_c
+        __syncwarp();
+        // ---- Y row pass (lane = row): f = tau_g' (Y u' - tau_h v (q . u')) over both halves
+        {
+          double2 a0 = zero, a1 = zero;
+#pragma unroll
+          for (int c = c0; c < c0 + HW; c += 2) {
+            const double2 y0c = W.X[lane][c], u0 = ug[c], y1c = W.X[lane][c + 1], u1 = ug[c + 1];
+            a0.x = fma(y0c.x, u0.x, fma(-y0c.y, u0.y, a0.x));
+            a0.y = fma(y0c.x, u0.y, fma(y0c.y, u0.x, a0.y));
+            a1.x = fma(y1c.x, u1.x, fma(-y1c.y, u1.y, a1.x));
+            a1.y = fma(y1c.x, u1.y, fma(y1c.y, u1.x, a1.y));
+          }
+          W.part[pb][h][lane] = make_double2(a0.x + a1.x, a0.y + a1.y);
+        }
+        pair_bar(bar);  // B6
+        double2 f;
+        {
+          const double2 p0 = W.part[pb][0][lane], p1 = W.part[pb][1][lane];
+          const double2 vq = cmul(v, qu);
+          f = make_double2(next_tau * (p0.x + p1.x - tauh * vq.x), next_tau * (p0.y + p1.y - tauh * vq.y));
+        }
+        pb ^= 1;
+        // ---- Y' = Y - v d - f conj(u') on this warp's columns, to HBM; row 0 -> (conj beta', 0, ...)
+        if (lane < len) {
+          const bool row0 = lane == 0 && next_tau != 0.0;
+          double2* dst = blk + (size_t)(len + c0) * ld;
+#pragma unroll
+          for (int c = c0; c < c0 + HW; ++c, dst += ld) {
+            const double2 u = ug[c], dd = cb[c];
+            double2 z = W.X[lane][c];
+            z.x = fma(-v.x, dd.x, fma(v.y, dd.y, fma(-f.x, u.x, fma(-f.y, u.y, z.x))));
+            z.y = fma(-v.x, dd.y, fma(-v.y, dd.x, fma(-f.y, u.x, fma(f.x, u.y, z.y))));
+            if (row0) z = c == 0 ? make_double2(hg.beta.x, -hg.beta.y) : zero;
+            if (c < lb) *dst = z;
+          }
+        }
+      }
+      taug = next_tau;
+      __threadfence_block();
+      pair_bar(bar);  // B7: both warps' stores done (and the X buffer free for the next task)
+      if (h == 0 && lane == 0) prog[slot] = i * 65536 + t + 1;
+    }
+  }
+}
+
+template <int NT, int BWc>
+constexpr size_t bd_chase_pair_smem() {
+  return NT * sizeof(BdPairSmem<BWc>) + 64;
+}
+
 template <int NW, int BWc, bool DUAL>
 constexpr size_t bd_chase_smem() {
   return NW * sizeof(BdChaseSmem<BWc, DUAL>) + 64;

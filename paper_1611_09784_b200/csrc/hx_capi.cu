@@ -189,6 +189,10 @@ int hx_ctx_create_priority(int32_t device, int32_t priority, hx_ctx** out) {
   }
   hx::set_smem_attr(hx::small_bidiag_kernel, 200 * 1024);
   ctx->ws_budget = std::min(ctx->ws_budget, freeb / 3);
+  {
+    const char* wb = getenv("HX_WS_BUDGET_MB");  // experiments: workspace chunk budget (L2-resident chunks)
+    if (wb && wb[0]) ctx->ws_budget = (size_t)atoll(wb) << 20;
+  }
   hx::set_smem_attr(hx::small_tridiag_kernel, (int)hx::small_tridiag_smem(HX_SMEM_MAX_N));
   hx::set_smem_attr(hx::eigvalsh_small_kernel, (int)hx::small_tridiag_smem(HX_SMEM_MAX_N));
   hx::band_init_attributes();

@@ -56,6 +56,11 @@ def test_eigenvalues_and_curves_match_reference(name):
     assert np.nanmax(np.abs(eigs - ref)) <= EIG_TOL * width
     np.testing.assert_allclose(curves, g[f"{name}_curves"], rtol=0, atol=IDOS_TOL)
     np.testing.assert_allclose(curves, g[f"{name}_curves_full"], rtol=0, atol=IDOS_TOL)
+    # without the eigenvalue output the IDOS takes the fast paths (zone counts + Newton for N >= 96,
+    # early-settling bisection below): same curves
+    fast, _, status = eval_batch(cell, kp, words, lo, step, npts, 0.01)
+    assert (status == 0).all()
+    np.testing.assert_allclose(fast, g[f"{name}_curves"], rtol=0, atol=IDOS_TOL)
     sharp, _, _ = eval_batch(cell, kp, words, lo, step, npts, 0.01, sharp=True)
     ref_sharp = g[f"{name}_sharp"]
     diff = np.abs(sharp - ref_sharp) > 1e-12
