@@ -571,50 +571,66 @@ __global__ void counts_kernel(const double* E, const double* w, int64_t count, G
 }
 
 // term = full - 0.25 * sum_r quarter_r ; mean / var in fixed sample order (mlmc.py:143-154)
-__global__ void moments_kernel(const double* full, const double* quarters, int64_t M, int npts, double* terms,
-                               double* mean, double* var, double* sums) {
-  const int m = blockIdx.x * blockDim.x + threadIdx.x;
-  if (m >= npts) return;
+// CV terms and level moments per grid point (runner.py:281-299, mlmc.py:143-154).  Block = 32 grid points x
+// 8 sample groups (sample i in group i % 8); the group partials are combined in a fixed order, so results
+// do not depend on scheduling.  Two passes (mean, then the centred sum of squares).
+constexpr int MOM_P = 32, MOM_G = 8;
+__device__ __forceinline__ double cv_term(const double* full, const double* quarters, int64_t i, int npts, int m) {
+  double t = full[i * npts + m];
+  if (quarters) {
+    const double* q = quarters + i * 4 * npts + m;
+    double cv = 0.0;
+    cv = __dadd_rn(cv, q[0]);
+    cv = __dadd_rn(cv, q[npts]);
+    cv = __dadd_rn(cv, q[2 * npts]);
+    cv = __dadd_rn(cv, q[3 * npts]);
+    t = __dsub_rn(t, __dmul_rn(cv, 0.25));
+  }
+  return t;
+}
+
+__global__ void __launch_bounds__(MOM_P * MOM_G) moments_kernel(const double* full, const double* quarters, int64_t M,
+                                                                int npts, double* terms, double* mean, double* var,
+                                                                double* sums) {
+  __shared__ double ps[MOM_G][MOM_P], ps2[MOM_G][MOM_P];
+  const int pl = threadIdx.x % MOM_P, grp = threadIdx.x / MOM_P;
+  const int m = blockIdx.x * MOM_P + pl;
+  const bool on = m < npts;
   double s = 0.0, s2 = 0.0;
-  for (int64_t i = 0; i < M; ++i) {
-    double t = full[i * npts + m];
-    if (quarters) {
-      const double* q = quarters + i * 4 * npts + m;
-      double cv = 0.0;
-      cv = __dadd_rn(cv, q[0]);
-      cv = __dadd_rn(cv, q[npts]);
-      cv = __dadd_rn(cv, q[2 * npts]);
-      cv = __dadd_rn(cv, q[3 * npts]);
-      t = __dsub_rn(t, __dmul_rn(cv, 0.25));
+  if (on)
+    for (int64_t i = grp; i < M; i += MOM_G) {
+      const double t = cv_term(full, quarters, i, npts, m);
+      if (terms) terms[i * npts + m] = t;
+      s = __dadd_rn(s, t);
+      s2 = __fma_rn(t, t, s2);
     }
-    if (terms) terms[i * npts + m] = t;
-    s = __dadd_rn(s, t);
-    s2 = __fma_rn(t, t, s2);
+  ps[grp][pl] = s;
+  ps2[grp][pl] = s2;
+  __syncthreads();
+  double st = 0.0, st2 = 0.0;
+  for (int q = 0; q < MOM_G; ++q) {
+    st = __dadd_rn(st, ps[q][pl]);
+    st2 = __dadd_rn(st2, ps2[q][pl]);
   }
-  const double mu = __ddiv_rn(s, (double)M);
+  const double mu = __ddiv_rn(st, (double)M);
   double acc = 0.0;
-  for (int64_t i = 0; i < M; ++i) {
-    double t = terms ? terms[i * npts + m] : 0.0;
-    if (!terms) {
-      t = full[i * npts + m];
-      if (quarters) {
-        const double* q = quarters + i * 4 * npts + m;
-        double cv = 0.0;
-        cv = __dadd_rn(cv, q[0]);
-        cv = __dadd_rn(cv, q[npts]);
-        cv = __dadd_rn(cv, q[2 * npts]);
-        cv = __dadd_rn(cv, q[3 * npts]);
-        t = __dsub_rn(t, __dmul_rn(cv, 0.25));
-      }
+  if (on)
+    for (int64_t i = grp; i < M; i += MOM_G) {
+      const double dlt = __dsub_rn(cv_term(full, quarters, i, npts, m), mu);
+      acc = __fma_rn(dlt, dlt, acc);
     }
-    const double dlt = __dsub_rn(t, mu);
-    acc = __dadd_rn(acc, __dmul_rn(dlt, dlt));
-  }
-  if (mean) mean[m] = mu;
-  if (var) var[m] = M > 1 ? __ddiv_rn(acc, (double)(M - 1)) : __longlong_as_double(0x7ff8000000000000ll);
-  if (sums) {
-    sums[m] = s;
-    sums[npts + m] = s2;
+  __syncthreads();
+  ps[grp][pl] = acc;
+  __syncthreads();
+  if (grp == 0 && on) {
+    double a = 0.0;
+    for (int q = 0; q < MOM_G; ++q) a = __dadd_rn(a, ps[q][pl]);
+    if (mean) mean[m] = mu;
+    if (var) var[m] = M > 1 ? __ddiv_rn(a, (double)(M - 1)) : __longlong_as_double(0x7ff8000000000000ll);
+    if (sums) {
+      sums[m] = st;
+      sums[npts + m] = st2;
+    }
   }
 }
 
@@ -698,7 +714,7 @@ int hx_sharp_counts_device(const double* d_energies, const double* d_weights, in
 int hx_level_moments_device(const double* d_full, const double* d_quarters, int64_t M, int32_t npts, double* d_terms,
                             double* d_mean, double* d_var, double* d_sums, void* stream) {
   if (!d_full || M < 1 || npts < 1) return fail(HX_E_ARG, "level_moments: bad args");
-  hx::moments_kernel<<<(npts + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(d_full, d_quarters, M, npts,
+  hx::moments_kernel<<<(npts + hx::MOM_P - 1) / hx::MOM_P, hx::MOM_P * hx::MOM_G, 0, static_cast<cudaStream_t>(stream)>>>(d_full, d_quarters, M, npts,
                                                                                        d_terms, d_mean, d_var, d_sums);
   HX_CUDA(cudaGetLastError());
     hx::count_launch();
