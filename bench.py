@@ -194,6 +194,40 @@ def reference_engine_run(kind, levels, nq, p, erange, frac, workers):
     return per_level
 
 
+LARGE_NU = 64  # levels at or above this size are timed by one reference eigensolve, extrapolated
+
+
+def reference_single_solve(kind, nu, q, p, cores):
+    """Bounded reference sample for the large-N configs (c4: one N = 8192 sample is ~4 x 50 s of LAPACK on
+    16 cores): ONE k-point (Gamma) of one seeded sample through the reference's solve_bands + idos
+    (spectrum.py:120-134, qoi.py:96-102) with every host core as BLAS threads; per-sample time =
+    q^2 x that (the k-points of a sample cost the same).  Returns (seconds per sample, solve seconds)."""
+    ref = ROOT / "baseline" / "_ref"
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_hexmc")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import hexmc
+    from hexmc.disorder import SeedSpec, sample_defects
+    from hexmc.lattice import build_supercell
+    from hexmc.qoi import EnergyGrid, SmoothingSpec, idos
+    from hexmc.spectrum import make_bz_grid, solve_bands
+    from threadpoolctl import threadpool_limits
+
+    model = hexmc.GrapheneNNModel() if kind == "graphene" else hexmc.load_coupling_table(TABLE)
+    sc = build_supercell(model.lattice_spec(), nu)
+    cfg = sample_defects(sc, p, SeedSpec(SEED, 1, 0))
+    grid1 = make_bz_grid(model.lattice_spec(), nu, 1, "reduced")  # Gamma only
+    with threadpool_limits(limits=cores):
+        sc2 = build_supercell(model.lattice_spec(), 2)  # warm-up (numba kernels, LAPACK threads)
+        idos(solve_bands(model, sc2, None, make_bz_grid(model.lattice_spec(), 2, 1, "reduced")),
+             EnergyGrid(LO_G, HI_G, NPTS), SmoothingSpec(DELTA), sc2.area)
+        t0 = time.perf_counter()
+        bands = solve_bands(model, sc, cfg, grid1)
+        idos(bands, EnergyGrid(LO_G, HI_G, NPTS), SmoothingSpec(DELTA), sc.area)
+        dt = time.perf_counter() - t0
+    return dt * q * q, dt
+
+
 def run_reference_arm(args):
     rank, world, _ = env_rank()
     if rank != 0:
@@ -201,6 +235,26 @@ def run_reference_arm(args):
     kind, levels, nq, p, erange, desc = CONFIGS[args.config]
     cores = len(os.sched_getaffinity(0))
     frac = args.ref_fraction
+    if max(nu for nu, _ in levels) >= LARGE_NU:
+        nu = levels[-1][0]
+        try:
+            vals = [1.0 / reference_single_solve(kind, nu, nq // nu, p, cores)[0] for _ in range(max(1, args.steps))]
+        except Exception as exc:  # noqa: BLE001
+            print(json.dumps({"impl": "reference", "unavailable": f"reference import/run failed: {exc!r}"[:300]}))
+            return 0
+        value = statistics.median(vals)
+        sample = (f"one nu={nu} Gamma-point solve_bands+idos per step ({cores} BLAS threads), x{(nq // nu) ** 2} "
+                  "k-points per sample (extrapolated)")
+        print(json.dumps({"impl": "reference", "metric": f"IDOS samples/sec ({desc})", "value": value,
+                          "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": 0,
+                          "ms_per_step": 1e3 / value, "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded reference sampler)",
+                          "config": {"workload": desc}, "cpu_baseline": {"value": value, "unit": "samples/s",
+                                                                          "cores": cores, "kind": "reference",
+                                                                          "sample": sample},
+                          "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                                  "d2h_bytes_per_step": 0}}))
+        return 0
     try:
         # warm-up: one small level (loky spawn + numba load), then timed steps
         for _ in range(max(1, args.warmup)):
@@ -580,6 +634,15 @@ def run_e2e(hx, model, levels, nq, p, erange, lo, hi, args, rank, world, dev):
 def cpu_baseline(kind, levels, nq, p, erange):
     cores = len(os.sched_getaffinity(0))
     frac = 1.0 / 8.0
+    if max(nu for nu, _ in levels) >= LARGE_NU:
+        nu = levels[-1][0]
+        try:
+            per_sample, solve_s = reference_single_solve(kind, nu, nq // nu, p, cores)
+        except Exception:  # noqa: BLE001 - reference not installed
+            return None
+        return {"value": 1.0 / per_sample, "unit": "samples/s", "cores": cores, "kind": "reference",
+                "sample": f"one nu={nu} Gamma-point solve_bands+idos of a seeded sample ({solve_s:.1f} s, {cores} BLAS "
+                          f"threads), x{(nq // nu) ** 2} k-points per sample (extrapolated)"}
     try:
         reference_engine_run(kind, levels[:1], nq, p, erange, 16 / levels[0][1], cores)  # warm-up
         per = reference_engine_run(kind, levels, nq, p, erange, frac, cores)

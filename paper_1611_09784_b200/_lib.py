@@ -166,12 +166,14 @@ class Device:
         return h
 
     @classmethod
-    def lane(cls, device: int, i: int):
-        """Context i of the per-device pool used to evaluate independent groups concurrently (lane 0 on a
-        high-priority stream)."""
-        pool = cls._pools.setdefault(device, [])
+    def lane(cls, device: int, i: int, high: bool | None = None):
+        """Context i of the per-device pool used to evaluate independent groups concurrently.  Default:
+        lane 0 on a high-priority stream, the others normal; `high` picks the pool explicitly."""
+        if high is None:
+            high = i == 0
+        pool = cls._pools.setdefault((device, bool(high)), [])
         while len(pool) <= i:
-            pool.append(cls.new_ctx(device, -100 if not pool else 0))  # -100: clamped to the greatest priority
+            pool.append(cls.new_ctx(device, -100 if high else 0))  # -100: clamped to the greatest priority
         return pool[i]
 
     @classmethod

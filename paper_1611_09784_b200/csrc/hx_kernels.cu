@@ -621,7 +621,9 @@ __global__ void __launch_bounds__(128) zone_refine_kernel(CellDev c, int nk, Gri
   // fixed round count; many items: one thread per item, Newton (about 11 Sturm counts on average)
   int G = 1;
   while (G < 8 && n * (unsigned long long)(2 * G) * 2 <= nthreads) G *= 2;
-  if (G >= 4) {
+  // very large matrices hold ~10 eigenvalues per zone, often in near-degenerate clusters that Newton
+  // cannot isolate: the fixed round count of multisection wins there already at G = 2
+  if (G >= 4 || (G >= 2 && c.N >= 4096)) {
     refine_multisection<ZD>(c, nk, g, tri, tri_stride, dims, diff, trans, status, sharp, items, n, G);
     return;
   }

@@ -16,8 +16,9 @@ tests/test_engine_gpu.py against the reference's full-mode fixtures).
 from __future__ import annotations
 
 import math
+import os
 import time
-from concurrent.futures import ThreadPoolExecutor
+from concurrent.futures import FIRST_COMPLETED, ThreadPoolExecutor, wait
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -40,6 +41,7 @@ SLMC_STREAM_OFFSET = 10_000
 # cache in each worker (runner.py:98-111).  Rebuilding them per Engine costs a few ms of uploads, and
 # releasing them (cudaFree) synchronises the device.
 _CELL_CACHE: dict = {}
+_E2E_PRIO = os.environ.get("HX_E2E_PRIO", "big")  # experiment: "big+small" also raises the small tiers
 
 
 class TaskError(RuntimeError):
@@ -166,7 +168,7 @@ class Engine:
         """One batch of the seam (see _evaluate_batches)."""
         return self._evaluate_batches([(groups, task_ids)])[0]
 
-    def _evaluate_batches(self, batches):
+    def _evaluate_batches(self, batches, on_batch=None):
         """Vectorised batch seam for several consecutive batches.  batches: list of (groups, task_ids),
         groups = [(n, q, words uint64 [R, w]), ...] in request order, task_ids(i_group, new, inv) -> ids of
         the new masks (error reports only).  Every batch is deduplicated on (n, q, mask) against the run
@@ -220,40 +222,63 @@ class Engine:
                     hits[bi] += R - len(new)
                     if len(new):
                         ids = batches[bi][1](gi, new, inv)
-                        ctx = _lib.Device.lane(self.device, lane) if len(tiers) > 1 or len(tiers[tier]) > 1 else None
+                        high = lane == 0 or (_E2E_PRIO == "big+small" and self.cell(tier[0]).dim <= 128)
+                        ctx = (_lib.Device.lane(self.device, lane, high)
+                               if len(tiers) > 1 or len(tiers[tier]) > 1 else None)
                         lane += 1
                         pieces.setdefault(tier, []).append(
-                            (start, ex.submit(self._solve_group, tier[0], tier[1], uniq[new], ids, ctx)))
+                            (start, ex.submit(self._solve_group, tier[0], tier[1], uniq[new], ids, ctx), bi))
                     plans[(bi, gi)] = (tier, uniq, inv, keys, src, start)
-            solved = {}
-            for tier, lst in pieces.items():
-                res = [f.result() for _, f in lst]
-                curves = np.concatenate([c for c, _ in res]) if len(res) > 1 else res[0][0]
-                per_job = np.concatenate([np.full(len(c), pj) for c, pj in res])
-                solved[tier] = (curves, per_job)
-        out = []
-        for bi, (groups, _) in enumerate(batches):
-            res = []
-            for gi in range(len(groups)):
-                tier, uniq, inv, keys, src, start = plans[(bi, gi)]
-                cu = np.empty((len(uniq), npts))
-                pj = np.empty(len(uniq))
-                got = src >= 0
-                if got.any():
-                    curves, per_job = solved[tier]
-                    cu[got] = curves[src[got]]
-                    pj[got] = per_job[src[got]]
-                for i in np.flatnonzero(~got):
-                    cu[i], pj[i] = self._cache[keys[i]]
-                # masks this batch solved first: their cost is this batch's, and they enter the run cache
-                own = np.flatnonzero(src >= start)
-                spent[bi] += float(pj[own].sum())
-                if keys is not None:
-                    for i in own:
-                        self._cache[keys[i]] = (cu[i], pj[i])
-                res.append((cu[inv], pj[inv]))
-            out.append((res, hits[bi], spent[bi]))
+            # batch bi can be placed once every piece of its tiers submitted by batches <= bi is done;
+            # batches are finished (placement, cache, on_batch) as soon as that holds, so their host work
+            # overlaps the device work still running for later batches
+            needs = {}
+            for bi, (groups, _) in enumerate(batches):
+                fs = []
+                for n, q, _w in groups:
+                    fs += [f for (start, f, pbi) in pieces.get((n, q), []) if pbi <= bi]
+                needs[bi] = fs
+            out = [None] * len(batches)
+            left = list(range(len(batches)))
+            while left:
+                ready = [bi for bi in left if all(f.done() for f in needs[bi])]
+                if not ready:
+                    wait([f for bi in left for f in needs[bi] if not f.done()], return_when=FIRST_COMPLETED)
+                    continue
+                for bi in ready:
+                    out[bi] = self._place_batch(bi, batches[bi][0], plans, pieces, hits, spent, npts)
+                    left.remove(bi)
+                    if on_batch is not None:
+                        on_batch(bi, out[bi])
         return out
+
+    def _place_batch(self, bi, groups, plans, pieces, hits, spent, npts):
+        """Per-request curves of batch bi from the run cache and the solved pieces (runner.py:234-243)."""
+        res = []
+        for gi in range(len(groups)):
+            tier, uniq, inv, keys, src, start = plans[(bi, gi)]
+            cu = np.empty((len(uniq), npts))
+            pj = np.empty(len(uniq))
+            got = np.flatnonzero(src >= 0)
+            if len(got):
+                lst = pieces[tier]
+                starts = np.array([st for st, _, _ in lst])
+                which = np.searchsorted(starts, src[got], side="right") - 1
+                for k in np.unique(which):
+                    curves, per_job = lst[k][1].result()
+                    sel = got[which == k]
+                    cu[sel] = curves[src[sel] - lst[k][0]]
+                    pj[sel] = per_job
+            for i in np.flatnonzero(src < 0):
+                cu[i], pj[i] = self._cache[keys[i]]
+            # masks this batch solved first: their cost is this batch's, and they enter the run cache
+            own = np.flatnonzero(src >= start)
+            spent[bi] += float(pj[own].sum())
+            if keys is not None:
+                for i in own:
+                    self._cache[keys[i]] = (cu[i], pj[i])
+            res.append((cu[inv], pj[inv]))
+        return res, hits[bi], spent[bi]
 
     def evaluate_masks(self, requests):
         """Dedup on (n, q, mask) against the run cache and within the batch; solve the new jobs of each
@@ -357,8 +382,13 @@ class Engine:
         submission - every (n, q) tier of every level in flight at once."""
         levels = list(enumerate(zip(plan.ns, plan.samples), start=1))
         batches = [self._level_batch(idx, n, m, plan.p_vac, idx > 1) for idx, (n, m) in levels]
-        evaluated = self._evaluate_batches(batches)
-        sets = [self._level_finish(idx, n, m, idx > 1, ev) for (idx, (n, m)), ev in zip(levels, evaluated)]
+        sets = [None] * len(levels)
+
+        def finish(bi, ev):  # each level's terms/moments as soon as its curves are in
+            idx, (n, m) = levels[bi]
+            sets[bi] = self._level_finish(idx, n, m, idx > 1, ev)
+
+        self._evaluate_batches(batches, on_batch=finish)
         total = sum(s.stats.wall_seconds for s in sets)
         return combine_levels(self.grid, [s.stats for s in sets], total_wall_seconds=total), sets
 

@@ -25,7 +25,7 @@ class FakeEngine(hx.Engine):
 
 @pytest.fixture
 def engine(monkeypatch):
-    monkeypatch.setattr(_lib.Device, "lane", classmethod(lambda cls, d, i: None))
+    monkeypatch.setattr(_lib.Device, "lane", classmethod(lambda cls, d, i, high=None: None))
     return FakeEngine(hx.GrapheneNNModel(), nq=16, delta=0.01, master_seed=7, bz_mode="reduced",
                       energy_points=11, energy_range=(LO + 0.02, HI - 0.02))
 
