@@ -238,3 +238,56 @@ def test_run_mlmc_batched_equals_level_by_level():
         assert np.array_equal(s.full, t.full)
         assert np.array_equal(s.stats.mean, t.stats.mean)
         assert s.stats.cache_hits == t.stats.cache_hits
+
+
+def test_exhaustive_matches_oracle_enumeration():
+    """run_exhaustive (runner.py:380-415): binomially weighted mean over all 2^N outcomes; nu = 1, p = 0.5 has
+    terminal value 1.0 (the reference's test_cli.py:109-120), and the whole curve equals the oracle's own
+    enumeration."""
+    lo, hi, npts = -6.580201874549387, 14.863393148450246, 201
+    eng = hx.Engine(hx.GrapheneNNModel(), nq=6, delta=0.01, master_seed=1, bz_mode="reduced", energy_points=npts,
+                    energy_range=(lo + 0.02, hi - 0.02))
+    res = eng.run_exhaustive(1, 0.5)
+    assert res.nconfigs == 4 and res.weight_sum == pytest.approx(1.0, abs=1e-15)
+    assert res.mean[-1] == pytest.approx(1.0, abs=1e-12)
+    om = O.graphene_model()
+    cell = O.make_cell(om, 1)
+    kp = hx.make_bz_grid(hx.GrapheneNNModel().lattice_spec(), 1, 6, "reduced").kpoints
+    w = np.full(len(kp), 1.0 / len(kp))
+    want = np.zeros(npts)
+    for mask in range(4):
+        nvac = bin(mask).count("1")
+        weight = 0.5 ** nvac * 0.5 ** (2 - nvac)
+        if nvac == 2:
+            continue  # all removed: zero curve
+        bands = O.solve_bands(cell, om, mask, kp)
+        want += weight * O.idos_from_bands(bands, w, lo, hi, npts, 0.01, cell.area)
+    np.testing.assert_allclose(res.mean, want, rtol=0, atol=IDOS_TOL)
+
+
+def test_empty_and_mixed_batches_on_the_zone_path():
+    """nmasks = 0 is a no-op; a zone-path batch (N = 128) mixing the pristine, a fully vacant and random
+    masks gives each mask the curve it gets alone (no cross-talk through the fixed-point accumulators)."""
+    model = hx.GrapheneNNModel()
+    sc = hx.build_supercell(model.lattice_spec(), 8)
+    cell = hx.compile_cell(model, sc)
+    kp = hx.make_bz_grid(model.lattice_spec(), 8, 2, "reduced").kpoints
+    lo, hi, npts = -6.580201874549387, 14.863393148450246, 201
+    step = (hi - lo) / (npts - 1)
+    curves, _, status = eval_batch(cell, kp, np.zeros((0, 2), dtype=np.uint64), lo, step, npts, 0.01)
+    assert curves.shape == (0, npts) and status.shape == (0, len(kp))
+    from paper_1611_09784_b200.sampling import sample_masks
+
+    words = np.concatenate([np.zeros((1, 2), np.uint64), np.full((1, 2), np.iinfo(np.uint64).max, np.uint64),
+                            sample_masks(sc.nunits, 0.1, 5, 1, 0, 6)])
+    both, _, status = eval_batch(cell, kp, words, lo, step, npts, 0.01)
+    assert (status[1] == 3).all() and (status[[0, 2, 3]] == 0).all()
+    assert np.array_equal(both[1], np.zeros(npts))
+    for i in (0, 3, 7):
+        alone, _, _ = eval_batch(cell, kp, words[i:i + 1], lo, step, npts, 0.01)
+        np.testing.assert_array_equal(both[i], alone[0])
+    om = O.graphene_model()
+    ocell = O.make_cell(om, 8)
+    ref = O.idos_from_bands(O.solve_bands(ocell, om, 0, kp), np.full(len(kp), 1.0 / len(kp)), lo, hi, npts, 0.01,
+                            ocell.area)
+    np.testing.assert_allclose(both[0], ref, rtol=0, atol=IDOS_TOL)
