@@ -124,6 +124,18 @@ int hx_eval_idos_batch_device(hx_ctx* ctx, hx_cell* cell, const double* kpoints,
                               const uint64_t* d_masks, int64_t nmasks, const hx_egrid* grid,
                               double* d_curves, double* d_eigs, int32_t* d_status, void* stream);
 
+/* Weighted k-point variants (IDOS only, no eigenvalue output): kmult[k] >= 1 is the multiplicity of
+ * k-point k, the IDOS weights are kmult[k] / sum(kmult) (qoi.py:96-102 with BzGrid weights).  Used with
+ * time-reversal pairs merged: for real-amplitude models H(-k) = conj(H(k)) has the spectrum of H(k),
+ * so k and -k of the reference's grid (spectrum.py:59-84) are solved once with multiplicity 2.
+ * out_status / d_status: [nmasks x nk] for the given (representative) k-points. */
+int hx_eval_idos_batch_k(hx_ctx* ctx, hx_cell* cell, const double* kpoints, const int32_t* kmult, int32_t nk,
+                         const uint64_t* masks, int64_t nmasks, const hx_egrid* grid, double* out_curves,
+                         int32_t* out_status);
+int hx_eval_idos_batch_device_k(hx_ctx* ctx, hx_cell* cell, const double* kpoints, const int32_t* kmult,
+                                int32_t nk, const uint64_t* d_masks, int64_t nmasks, const hx_egrid* grid,
+                                double* d_curves, int32_t* d_status, void* stream);
+
 /* Batched Hermitian (generalized) eigenvalues of caller-assembled matrices (config-5 sweep,
  * unit parity with spectrum._eigvals, spectrum.py:100-117).  A, B: device, column-major complex128
  * (interleaved re/im), n x n each, `batch` matrices; B == NULL -> standard problem.

@@ -25,7 +25,7 @@ EXPORTED = (
     "hx_abi_version", "hx_last_error", "hx_device_count", "hx_ctx_create", "hx_ctx_create_priority",
     "hx_ctx_destroy",
     "hx_ctx_synchronize", "hx_cell_create", "hx_cell_destroy", "hx_eval_idos_batch",
-    "hx_eval_idos_batch_device", "hx_eigvalsh_batch_device", "hx_smoothed_counts_device",
+    "hx_eval_idos_batch_device", "hx_eval_idos_batch_k", "hx_eval_idos_batch_device_k", "hx_eigvalsh_batch_device", "hx_smoothed_counts_device",
     "hx_sharp_counts_device", "hx_level_moments_device", "hx_sample_masks", "hx_sample_masks_device",
     "hx_uniforms", "hx_restrict_masks", "hx_assemble_device", "hx_restrict_masks_device",
     "hx_kernel_launches",
@@ -79,6 +79,8 @@ def load():
             "hx_eval_idos_batch": (C.c_int, [vp, vp, vp, i32, vp, i64, C.POINTER(EGrid), vp, vp, vp]),
             "hx_eval_sharp_batch": (C.c_int, [vp, vp, vp, i32, vp, i64, C.POINTER(EGrid), vp, vp, vp]),
             "hx_eval_idos_batch_device": (C.c_int, [vp, vp, vp, i32, vp, i64, C.POINTER(EGrid), vp, vp, vp, vp]),
+            "hx_eval_idos_batch_k": (C.c_int, [vp, vp, vp, vp, i32, vp, i64, C.POINTER(EGrid), vp, vp]),
+            "hx_eval_idos_batch_device_k": (C.c_int, [vp, vp, vp, vp, i32, vp, i64, C.POINTER(EGrid), vp, vp, vp]),
             "hx_eigvalsh_batch_device": (C.c_int, [vp, i32, i64, vp, vp, vp, vp, vp]),
             "hx_smoothed_counts_device": (C.c_int, [vp, vp, i64, C.POINTER(EGrid), vp, vp]),
             "hx_sharp_counts_device": (C.c_int, [vp, vp, i64, C.POINTER(EGrid), vp, vp]),

@@ -64,7 +64,7 @@ struct DevBuf {
 struct hx_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
-  DevBuf kpts, diff, trans, ws, masks, curves, eigs, status, band, tri, refine;
+  DevBuf kpts, kmult, diff, trans, ws, masks, curves, eigs, status, band, tri, refine;
   size_t ws_budget = (size_t)24 << 30;  // HBM workspace budget for the global / banded paths
   int bd_min_n = HX_SMEM_MAX_N;          // bipartite cells with N above this take the banded SVD tier
   int bidiag_warp_max_s = 32;            // shared-memory bidiagonalisation: one warp per matrix up to this S
@@ -204,7 +204,7 @@ int hx_ctx_create_priority(int32_t device, int32_t priority, hx_ctx** out) {
 int hx_ctx_destroy(hx_ctx* ctx) {
   if (!ctx) return 0;
   set_device(ctx);
-  for (DevBuf* b : {&ctx->kpts, &ctx->diff, &ctx->trans, &ctx->ws, &ctx->masks, &ctx->curves, &ctx->eigs,
+  for (DevBuf* b : {&ctx->kpts, &ctx->kmult, &ctx->diff, &ctx->trans, &ctx->ws, &ctx->masks, &ctx->curves, &ctx->eigs,
                     &ctx->status, &ctx->band, &ctx->tri, &ctx->refine})
     b->release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -304,9 +304,11 @@ int hx_cell_destroy(hx_cell* cell) {
   return 0;
 }
 
+// kmult (host, optional): multiplicity of each k-point (time-reversal pairs merged by the caller); the IDOS
+// weights become kmult[k] / sum(kmult) instead of 1 / nk.
 static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t nk, const uint64_t* d_masks,
                      int64_t nmasks, const hx_egrid* grid, double* d_curves, double* d_eigs, int32_t* d_status,
-                     cudaStream_t st, int sharp) {
+                     cudaStream_t st, int sharp, const int32_t* kmult = nullptr) {
   if (!ctx || !cell || !kpoints || !grid || (nmasks > 0 && (!d_masks || !d_curves || !d_status)))
     return fail(HX_E_ARG, "hx_eval_idos_batch: null argument");
   if (nk < 1 || nmasks < 0) return fail(HX_E_ARG, "hx_eval_idos_batch: nk >= 1 and nmasks >= 0 required");
@@ -316,17 +318,32 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
   if (set_device(ctx)) return HX_E_CUDA;
   const hx::CellDev& c = cell->dev;
   const int N = c.N;
-  hx::GridDev g;
+  int64_t nk_total = nk;
+  if (kmult) {
+    if (d_eigs) return fail(HX_E_ARG, "k-point multiplicities need the IDOS-only call (no eigenvalue output)");
+    nk_total = 0;
+    for (int k = 0; k < nk; ++k) {
+      if (kmult[k] < 1) return fail(HX_E_ARG, "k-point multiplicities must be >= 1");
+      nk_total += kmult[k];
+    }
+  }
+  hx::GridDev g{};
   g.e0 = grid->e0;
   g.step = grid->step;
   g.delta = grid->delta;
   g.npts = grid->npts;
-  g.shift = fixed_point_shift(nk, N);
+  g.shift = fixed_point_shift(nk_total, N);
   g.inv_step = 1.0 / g.step;
+  g.kmult = nullptr;
   if (g.shift < 16) return fail(HX_E_RANGE, "nk * N too large for the fixed-point IDOS accumulator");
   // k-points (small, pageable copy on the work stream)
   if (ctx->kpts.grow((size_t)nk * 16)) return fail(HX_E_CUDA, "alloc kpts");
   HX_CUDA(cudaMemcpyAsync(ctx->kpts.p, kpoints, (size_t)nk * 16, cudaMemcpyHostToDevice, st));
+  if (kmult) {
+    if (ctx->kmult.grow((size_t)nk * 4)) return fail(HX_E_CUDA, "alloc kmult");
+    HX_CUDA(cudaMemcpyAsync(ctx->kmult.p, kmult, (size_t)nk * 4, cudaMemcpyHostToDevice, st));
+    g.kmult = static_cast<const int*>(ctx->kmult.p);
+  }
   const size_t diff_b = (size_t)nmasks * (grid->npts + 1) * sizeof(int);
   const size_t trans_b = (size_t)nmasks * grid->npts * sizeof(unsigned long long);
   if (ctx->diff.grow(diff_b) || ctx->trans.grow(trans_b)) return fail(HX_E_CUDA, "alloc accumulators");
@@ -416,7 +433,8 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
     }
   }
   const int wpb = 8;
-  hx::finalize_kernel<<<(unsigned)((nmasks + wpb - 1) / wpb), 32 * wpb, 0, st>>>(diff, trans, nmasks, g, 1.0 / nk,
+  hx::finalize_kernel<<<(unsigned)((nmasks + wpb - 1) / wpb), 32 * wpb, 0, st>>>(diff, trans, nmasks, g,
+                                                                                 1.0 / (double)nk_total,
                                                                                  1.0 / c.area, d_curves);
   HX_CUDA(cudaGetLastError());
     hx::count_launch();
@@ -430,9 +448,16 @@ int hx_eval_idos_batch_device(hx_ctx* ctx, hx_cell* cell, const double* kpoints,
                    static_cast<cudaStream_t>(stream), 0);
 }
 
+int hx_eval_idos_batch_device_k(hx_ctx* ctx, hx_cell* cell, const double* kpoints, const int32_t* kmult, int32_t nk,
+                                const uint64_t* d_masks, int64_t nmasks, const hx_egrid* grid, double* d_curves,
+                                int32_t* d_status, void* stream) {
+  return eval_impl(ctx, cell, kpoints, nk, d_masks, nmasks, grid, d_curves, nullptr, d_status,
+                   static_cast<cudaStream_t>(stream), 0, kmult);
+}
+
 static int eval_host(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t nk, const uint64_t* masks,
                      int64_t nmasks, const hx_egrid* grid, double* out_curves, double* out_eigs, int32_t* out_status,
-                     int sharp) {
+                     int sharp, const int32_t* kmult = nullptr) {
   if (!ctx || !cell || !grid) return fail(HX_E_ARG, "hx_eval_idos_batch: null argument");
   if (nmasks == 0) return 0;
   if (!masks || !out_curves || !out_status) return fail(HX_E_ARG, "hx_eval_idos_batch: null buffer");
@@ -446,7 +471,7 @@ static int eval_host(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
   HX_CUDA(cudaMemcpyAsync(ctx->masks.p, masks, mb, cudaMemcpyHostToDevice, st));
   int rc = eval_impl(ctx, cell, kpoints, nk, static_cast<uint64_t*>(ctx->masks.p), nmasks, grid,
                      static_cast<double*>(ctx->curves.p), out_eigs ? static_cast<double*>(ctx->eigs.p) : nullptr,
-                     static_cast<int32_t*>(ctx->status.p), st, sharp);
+                     static_cast<int32_t*>(ctx->status.p), st, sharp, kmult);
   if (rc) return rc;
   HX_CUDA(cudaMemcpyAsync(out_curves, ctx->curves.p, cb, cudaMemcpyDeviceToHost, st));
   HX_CUDA(cudaMemcpyAsync(out_status, ctx->status.p, sb, cudaMemcpyDeviceToHost, st));
@@ -479,6 +504,12 @@ int hx_eval_idos_batch(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_
                        int64_t nmasks, const hx_egrid* grid, double* out_curves, double* out_eigs,
                        int32_t* out_status) {
   return eval_host(ctx, cell, kpoints, nk, masks, nmasks, grid, out_curves, out_eigs, out_status, 0);
+}
+
+int hx_eval_idos_batch_k(hx_ctx* ctx, hx_cell* cell, const double* kpoints, const int32_t* kmult, int32_t nk,
+                         const uint64_t* masks, int64_t nmasks, const hx_egrid* grid, double* out_curves,
+                         int32_t* out_status) {
+  return eval_host(ctx, cell, kpoints, nk, masks, nmasks, grid, out_curves, nullptr, out_status, 0, kmult);
 }
 
 // Sharp-count variant of the batch (idos_sharp, qoi.py:105-108); not part of the public header's

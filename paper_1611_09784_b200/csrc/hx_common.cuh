@@ -45,7 +45,13 @@ struct GridDev {
   int32_t npts;
   int32_t shift;     // fixed-point fraction bits of the transition accumulator
   double inv_step;   // 1 / step: only for the (eta-widened) early-settle test, never for contributions
+  const int* kmult;  // device: multiplicity of each k-point of the batch (time-reversal pairs), or nullptr
 };
+
+// Multiplicity of matrix `mat` (= mask * nk + k) in the IDOS sums.
+__device__ __forceinline__ int kmul(const GridDev& g, int64_t mat, int nk) {
+  return g.kmult ? g.kmult[mat % nk] : 1;
+}
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);

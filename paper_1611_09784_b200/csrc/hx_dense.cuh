@@ -558,11 +558,12 @@ __device__ __forceinline__ double pencil_map(const CellDev& c, double lam) {
 // diff[lo] += 1 (full weight for m >= lo) and fixed-point g(x) for the transition band,
 // with the reference's index arithmetic (_kernels.py:68-88): lo = ceil((E + delta - e0)/step),
 // m0 = floor((E - delta - e0)/step) + 1, x = (E - (e0 + step*m))/delta, g = 0.5 + x(-1.125 + 0.625x^2).
-__device__ __forceinline__ void idos_state(const GridDev& g, double E, int* diff, unsigned long long* trans) {
+__device__ __forceinline__ void idos_state(const GridDev& g, double E, int* diff, unsigned long long* trans,
+                                           int mult = 1) {
   const double ulo = __ddiv_rn(__dsub_rn(__dadd_rn(E, g.delta), g.e0), g.step);
   long long lo = (long long)ceil(ulo);
   if (lo < 0) lo = 0;
-  if (lo < g.npts) atomicAdd(diff + lo, 1);
+  if (lo < g.npts) atomicAdd(diff + lo, mult);
   const double um0 = __ddiv_rn(__dsub_rn(__dsub_rn(E, g.delta), g.e0), g.step);
   long long m0 = (long long)floor(um0) + 1;
   if (m0 < 0) m0 = 0;
@@ -573,15 +574,15 @@ __device__ __forceinline__ void idos_state(const GridDev& g, double E, int* diff
     const double x = __ddiv_rn(__dsub_rn(E, em), g.delta);
     const double gx = __dadd_rn(0.5, __dmul_rn(x, __dadd_rn(-1.125, __dmul_rn(__dmul_rn(0.625, x), x))));
     const long long fx = __double2ll_rn(gx * scale);
-    atomicAdd(trans + m, (unsigned long long)fx);
+    atomicAdd(trans + m, (unsigned long long)(fx * mult));
   }
 }
 
 // Sharp count contribution: weight at m >= floor((E - e0)/step) + 1 (_kernels.py:91-101).
-__device__ __forceinline__ void sharp_state(const GridDev& g, double E, int* diff) {
+__device__ __forceinline__ void sharp_state(const GridDev& g, double E, int* diff, int mult = 1) {
   long long idx = (long long)floor(__ddiv_rn(__dsub_rn(E, g.e0), g.step)) + 1;
   if (idx < 0) idx = 0;
-  if (idx < g.npts) atomicAdd(diff + idx, 1);
+  if (idx < g.npts) atomicAdd(diff + idx, mult);
 }
 
 // ---------------------------------------------------------------------------------------------

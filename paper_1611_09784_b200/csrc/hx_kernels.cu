@@ -168,9 +168,9 @@ static __device__ __forceinline__ long long settle_index(const CellDev& c, const
   return (la == lb && ma == mb && ma >= la) ? la : LLONG_MIN;
 }
 
-static __device__ __forceinline__ void add_settled(const GridDev& g, int* diff, int64_t mk, long long l) {
+static __device__ __forceinline__ void add_settled(const GridDev& g, int* diff, int64_t mk, long long l, int mult) {
   const long long l0 = l < 0 ? 0 : l;
-  if (l0 < g.npts) atomicAdd(diff + mk * (g.npts + 1) + l0, 1);
+  if (l0 < g.npts) atomicAdd(diff + mk * (g.npts + 1) + l0, mult);
 }
 
 // IDOS contribution (and status) of one eigenvalue lam of T
@@ -180,8 +180,9 @@ static __device__ __forceinline__ void add_eigenvalue(const CellDev& c, const Gr
   const double E = pencil_map(c, lam);
   if (!isfinite(E)) atomicMax(status + mat, 2);
   const int64_t mk = mat / nk;
-  if (sharp) sharp_state(g, E, diff + mk * (g.npts + 1));
-  else idos_state(g, E, diff + mk * (g.npts + 1), trans + mk * g.npts);
+  const int mult = kmul(g, mat, nk);
+  if (sharp) sharp_state(g, E, diff + mk * (g.npts + 1), mult);
+  else idos_state(g, E, diff + mk * (g.npts + 1), trans + mk * g.npts, mult);
 }
 
 // One thread per (matrix, eigenvalue index) - for TGK tridiagonals one thread per +-pair: it bisects
@@ -258,14 +259,14 @@ __global__ void __launch_bounds__(128) eig_idos_kernel(CellDev c, int nk, GridDe
       if (!(done & 1)) {
         const long long l = settle_index(c, g, sharp, lo, hi);
         if (l != LLONG_MIN) {
-          add_settled(g, diff, mk, l);
+          add_settled(g, diff, mk, l, kmul(g, mat, nk));
           done |= 1;
         }
       }
       if (!(done & 2)) {
         const long long l = settle_index(c, g, sharp, -hi, -lo);
         if (l != LLONG_MIN) {
-          add_settled(g, diff, mk, l);
+          add_settled(g, diff, mk, l, kmul(g, mat, nk));
           done |= 2;
         }
       }
@@ -505,7 +506,7 @@ __global__ void __launch_bounds__(256) zone_count_kernel(CellDev c, int nk, Grid
     int n;
     if (!rev) n = zc[2 * m] - (m > 0 ? zc[2 * m - 1] : 0);
     else n = (m > 0 ? zc[2 * m - 2] : d) - zc[2 * m + 1];
-    if (n > 0) atomicAdd(drow + m, n);
+    if (n > 0) atomicAdd(drow + m, n * kmul(g, mat, nk));
     // eigenvalues inside zone m: refinement items from the zone's own bracket
     const int i0 = zc[2 * m], nz = zc[2 * m + 1] - i0;
     if (nz > 0) {

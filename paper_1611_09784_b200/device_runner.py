@@ -19,7 +19,7 @@ import torch
 from . import _lib
 from .geometry import build_supercell, partition_quarters
 from .models import compile_cell
-from .solver import make_bz_grid
+from .solver import make_bz_grid, time_reversal_reduce, use_time_reversal
 
 
 @dataclass
@@ -49,6 +49,7 @@ class DeviceMlmc:
         self.ctx = _lib.Device.ctx(device)
         self._cells = {}
         self._parts = {}
+        self._kpts = {}
         self.stream = torch.cuda.current_stream(self.dev)
         # per-call accounting for the roofline: list of (n, nmats, flops, event pair)
         self.records = []
@@ -81,7 +82,16 @@ class DeviceMlmc:
         return self.nq // n
 
     def kpoints(self, n, q):
-        return np.ascontiguousarray(make_bz_grid(self.model.lattice_spec(), n, q, "reduced").kpoints)
+        """(k-points, multiplicities): the reduced grid, time-reversal pairs merged for real-amplitude
+        models (solver.time_reversal_reduce; multiplicities None otherwise)."""
+        key = (n, q)
+        if key not in self._kpts:
+            kp = np.ascontiguousarray(make_bz_grid(self.model.lattice_spec(), n, q, "reduced").kpoints)
+            if use_time_reversal() and self.cell(n).time_reversal_symmetric:
+                self._kpts[key] = time_reversal_reduce(self.model.lattice_spec(), n, kp)
+            else:
+                self._kpts[key] = (kp, None)
+        return self._kpts[key]
 
     def prepare(self, level, n, M_total, p, with_cv, rank=0, world=1) -> LevelInputs:
         """Masks for this rank's replicates [rank*M, (rank+1)*M) (device RNG) + quarter masks.
@@ -119,7 +129,7 @@ class DeviceMlmc:
         before using or releasing them."""
         cell = self.cell(n)
         q = self.q_of(n)
-        kp = self.kpoints(n, q)
+        kp, kmult = self.kpoints(n, q)
         U = uniq.shape[0]
         curves = torch.empty((U, self.npts), dtype=torch.float64, device=self.dev)
         status = torch.empty((U, kp.shape[0]), dtype=torch.int32, device=self.dev)
@@ -129,10 +139,17 @@ class DeviceMlmc:
         if self.record:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             ev[0].record(stream)
-        _lib.check(self.lib.hx_eval_idos_batch_device(ctx, cell.handle, _lib.ptr(kp), kp.shape[0],
-                                                      uniq.data_ptr(), U, C.byref(g), curves.data_ptr(), 0,
-                                                      status.data_ptr(), stream.cuda_stream),
-                   "hx_eval_idos_batch_device")
+        if kmult is None:
+            _lib.check(self.lib.hx_eval_idos_batch_device(ctx, cell.handle, _lib.ptr(kp), kp.shape[0],
+                                                          uniq.data_ptr(), U, C.byref(g), curves.data_ptr(), 0,
+                                                          status.data_ptr(), stream.cuda_stream),
+                       "hx_eval_idos_batch_device")
+        else:
+            _lib.check(self.lib.hx_eval_idos_batch_device_k(ctx, cell.handle, _lib.ptr(kp), _lib.ptr(kmult),
+                                                            kp.shape[0], uniq.data_ptr(), U, C.byref(g),
+                                                            curves.data_ptr(), status.data_ptr(),
+                                                            stream.cuda_stream),
+                       "hx_eval_idos_batch_device_k")
         if self.record:
             ev[1].record(stream)
             self.records.append({"n": n, "N": cell.dim, "unique": U, "nk": kp.shape[0], "events": ev,

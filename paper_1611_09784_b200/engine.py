@@ -30,7 +30,8 @@ from .idos import EnergyGrid
 from .models import compile_cell
 from .sampling import (DefectConfiguration, enumerate_configs, keys_from_words, restrict_words, sample_masks,
                        words_from_keys)
-from .solver import eval_batch, make_bz_grid, raise_status, solve_bands
+from .solver import (eval_batch, make_bz_grid, raise_status, solve_bands, time_reversal_reduce,
+                     use_time_reversal)
 
 __all__ = ["Engine", "TaskError", "LevelSampleSet", "ExhaustiveResult", "SLMC_STREAM_OFFSET"]
 
@@ -131,6 +132,18 @@ class Engine:
             self._kgrids[key] = make_bz_grid(self.model.lattice_spec(), n, q, "reduced").kpoints
         return self._kgrids[key]
 
+    def kpoints_tr(self, n: int, q: int):
+        """(k-points, multiplicities) of the IDOS batches: time-reversal pairs merged for real-amplitude
+        models (solver.time_reversal_reduce), otherwise the full base grid with multiplicity 1."""
+        key = ("tr", n, q)
+        if key not in self._kgrids:
+            kp = self.kpoints(n, q)
+            if use_time_reversal() and self.cell(n).time_reversal_symmetric:
+                self._kgrids[key] = time_reversal_reduce(self.model.lattice_spec(), n, kp)
+            else:
+                self._kgrids[key] = (kp, None)
+        return self._kgrids[key]
+
     def q_of(self, n: int) -> int:
         if self.nq % n:
             raise ValueError(f"n*q constant {self.nq} is not divisible by n = {n}")
@@ -146,10 +159,10 @@ class Engine:
     def _solve_group(self, n: int, q: int, words, task_ids, ctx=None):
         """One GPU batch for the (n, q) group: words uint64 [R, w] (task_ids: R ids for error reports)."""
         cell = self.cell(n)
-        kp = self.kpoints(n, q)
+        kp, kmult = self.kpoints_tr(n, q)
         t0 = time.perf_counter()
         curves, _, status = eval_batch(cell, kp, words, self.grid.lo, self.grid.step, self.grid.npoints,
-                                       self.delta, ctx=ctx)
+                                       self.delta, ctx=ctx, kmult=kmult)
         secs = time.perf_counter() - t0
         self.io_bytes[0] += words.nbytes + kp.nbytes
         self.io_bytes[1] += curves.nbytes + status.nbytes
@@ -185,8 +198,9 @@ class Engine:
         for bi, (groups, _) in enumerate(batches):
             for gi, (n, q, words) in enumerate(groups):
                 tiers.setdefault((n, q), []).append((bi, gi, np.ascontiguousarray(words, dtype=np.uint64)))
-        for n, _ in tiers:
-            self.cell(n)  # compile cells up front (not thread-safe)
+        for n, q in tiers:
+            self.cell(n)  # compile cells and k-sets up front (not thread-safe)
+            self.kpoints_tr(n, q)
         order = sorted(tiers, key=lambda g: -self.cell(g[0]).dim)
         hits = [0] * len(batches)
         spent = [0.0] * len(batches)

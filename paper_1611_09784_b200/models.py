@@ -194,6 +194,13 @@ class CompiledCell:
         self.device = device
         self._handle = None
 
+    @property
+    def time_reversal_symmetric(self) -> bool:
+        """Real hopping / overlap amplitudes and on-site terms: H(-k) = conj(H(k)), S(-k) = conj(S(k)), so k
+        and -k share a spectrum (the IDOS batches merge them, solver.time_reversal_reduce)."""
+        amps = [np.asarray(self.h[2])] + ([] if self.s is None else [np.asarray(self.s[2])])
+        return all(not np.any(np.imag(a)) for a in amps) and not np.any(np.imag(self.onsite))
+
     def _pencil_kind(self):
         m = self.model
         if isinstance(m, GrapheneNNModel) and m.t != 0.0:

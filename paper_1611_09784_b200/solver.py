@@ -9,6 +9,7 @@ the reference's message text (spectrum.py:109-117).
 from __future__ import annotations
 
 import ctypes as C
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -17,7 +18,8 @@ import numpy as np
 from . import _lib
 from .models import CompiledCell, compile_cell
 
-__all__ = ["BzGrid", "BandGrid", "SolverError", "make_bz_grid", "solve_bands", "estimate_solve_cost", "eval_batch"]
+__all__ = ["BzGrid", "BandGrid", "SolverError", "make_bz_grid", "solve_bands", "estimate_solve_cost", "eval_batch",
+           "time_reversal_reduce", "use_time_reversal"]
 
 
 class SolverError(RuntimeError):
@@ -60,6 +62,39 @@ def make_bz_grid(spec, n: int, q: int, mode: str = "full") -> BzGrid:
     return BzGrid(n=n, q=q, mode=mode, kpoints=kp, weights=np.full(len(kp), 1.0 / len(kp)))
 
 
+def use_time_reversal() -> bool:
+    """k -> -k pairing of the IDOS batches (HX_NO_TIME_REVERSAL=1 disables it)."""
+    return os.environ.get("HX_NO_TIME_REVERSAL", "0") in ("", "0")
+
+
+def time_reversal_reduce(spec, n: int, kpoints: np.ndarray):
+    """Representatives and multiplicities of `kpoints` under k -> -k modulo the supercell reciprocal
+    lattice (b1/n, b2/n).  For real-amplitude models H(-k) = conj(H(k)) (and S likewise), so both have the
+    spectrum of H(k): the IDOS sum over the reference's grid (weights 1/nk, spectrum.py:59-84) equals the
+    sum over the representatives with weights mult/nk.  On the q x q corner grid the pairs are
+    (i, j) <-> (-i mod q, -j mod q); the time-reversal-invariant points keep multiplicity 1."""
+    kp = np.asarray(kpoints, dtype=np.float64).reshape(-1, 2)
+    b1, b2 = spec.reciprocal_vectors()
+    B = np.stack([np.asarray(b1) / n, np.asarray(b2) / n], axis=1)
+    frac = np.linalg.solve(B, kp.T).T
+
+    def key(f):
+        r = np.round(np.mod(f, 1.0), 9)
+        return tuple(np.mod(r, 1.0))
+
+    index = {}  # key of a representative -> its slot
+    reps, mult = [], []
+    for i, f in enumerate(frac):
+        j = index.get(key(-f))
+        if j is not None and mult[j] == 1:  # the partner of an earlier, still unpaired point
+            mult[j] = 2
+            continue
+        index.setdefault(key(f), len(reps))
+        reps.append(i)
+        mult.append(1)
+    return np.ascontiguousarray(kp[reps]), np.asarray(mult, dtype=np.int32)
+
+
 @dataclass(frozen=True, eq=False)
 class BandGrid:
     grid: BzGrid
@@ -90,7 +125,7 @@ def raise_status(status: np.ndarray, kpoints: np.ndarray, what: str = "eigensolv
 
 
 def eval_batch(cell: CompiledCell, kpoints: np.ndarray, words: np.ndarray, lo: float, step: float, npts: int,
-               delta: float, want_eigs: bool = False, sharp: bool = False, ctx=None):
+               delta: float, want_eigs: bool = False, sharp: bool = False, ctx=None, kmult=None):
     """Host-buffer call of hx_eval_idos_batch for one (n, q) group: curves [M, npts] (+ eigs, status).
     ctx: the hx context to use (default: the device's primary context); the call blocks until done and
     releases the GIL, so groups on different contexts run concurrently from different threads."""
@@ -104,8 +139,18 @@ def eval_batch(cell: CompiledCell, kpoints: np.ndarray, words: np.ndarray, lo: f
     curves = np.zeros((M, npts))
     status = np.zeros((M, nk), dtype=np.int32)
     eigs = np.empty((M, nk, cell.dim)) if want_eigs else None
-    fn = lib.hx_eval_sharp_batch if sharp else lib.hx_eval_idos_batch
     g = _egrid(lo, step, npts, delta)
+    if kmult is not None:
+        # k-point multiplicities (time-reversal pairs): smoothed IDOS only
+        if want_eigs or sharp:
+            raise ValueError("k-point multiplicities apply to the smoothed IDOS without eigenvalue output")
+        km = np.ascontiguousarray(kmult, dtype=np.int32)
+        if km.shape != (nk,):
+            raise ValueError("one multiplicity per k-point")
+        _lib.check(lib.hx_eval_idos_batch_k(ctx, cell.handle, _lib.ptr(kp), _lib.ptr(km), nk, _lib.ptr(words), M,
+                                            C.byref(g), _lib.ptr(curves), _lib.ptr(status)), "hx_eval_idos_batch_k")
+        return curves, None, status
+    fn = lib.hx_eval_sharp_batch if sharp else lib.hx_eval_idos_batch
     _lib.check(fn(ctx, cell.handle, _lib.ptr(kp), nk, _lib.ptr(words), M, C.byref(g), _lib.ptr(curves),
                   _lib.ptr(eigs) if want_eigs else 0, _lib.ptr(status)), "hx_eval_idos_batch")
     return curves, eigs, status

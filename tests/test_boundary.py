@@ -113,3 +113,25 @@ def test_pencil_kinds():
     tc = compile_cell(t, build_supercell(t.lattice_spec(), 2))
     assert tc.pencil == _lib.HX_PENCIL_STANDARD
     assert tc.dim == 44 and tc.supercell.nunits == 4
+
+
+@pytest.mark.parametrize("n,q", [(4, 8), (8, 4), (16, 2), (32, 1), (4, 6), (3, 5)])
+def test_time_reversal_pairs_of_the_reference_grid(n, q):
+    """k -> -k classes of the reduced q x q grid (spectrum.py:59-84): multiplicities sum to q^2, the
+    invariant points are the 4 (q even) or 1 (q odd) TRIMs, and every merged point's partner is its negative
+    modulo the supercell reciprocal lattice."""
+    from paper_1611_09784_b200.models import GrapheneNNModel
+    from paper_1611_09784_b200.solver import make_bz_grid, time_reversal_reduce
+
+    spec = GrapheneNNModel().lattice_spec()
+    kp = make_bz_grid(spec, n, q, "reduced").kpoints
+    reps, mult = time_reversal_reduce(spec, n, kp)
+    assert mult.sum() == q * q
+    assert (mult == 1).sum() == (min(q, 2) ** 2 if q % 2 == 0 else 1)
+    b1, b2 = spec.reciprocal_vectors()
+    B = np.stack([np.asarray(b1) / n, np.asarray(b2) / n], axis=1)
+    frac = np.linalg.solve(B, kp.T).T
+    for r in np.linalg.solve(B, reps.T).T:
+        partners = [f for f in frac if np.allclose(np.mod(f + r + 1e-12, 1.0), 0.0, atol=1e-9)
+                    or np.allclose(np.mod(f + r + 1e-12, 1.0), 1.0, atol=1e-9)]
+        assert len(partners) == 1

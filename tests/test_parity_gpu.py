@@ -291,3 +291,40 @@ def test_empty_and_mixed_batches_on_the_zone_path():
     ref = O.idos_from_bands(O.solve_bands(ocell, om, 0, kp), np.full(len(kp), 1.0 / len(kp)), lo, hi, npts, 0.01,
                             ocell.area)
     np.testing.assert_allclose(both[0], ref, rtol=0, atol=IDOS_TOL)
+
+
+@pytest.mark.parametrize("nu,q", [(4, 8), (8, 4), (4, 6), (3, 5)])
+def test_time_reversal_pairs_give_the_same_curves(nu, q, monkeypatch):
+    """Graphene (real amplitudes): merging k and -k (multiplicity 2, hx_eval_idos_batch_k) reproduces the
+    curves of the full reference grid, and the oracle's."""
+    from paper_1611_09784_b200.sampling import sample_masks
+    from paper_1611_09784_b200.solver import time_reversal_reduce
+
+    model = hx.GrapheneNNModel()
+    sc = hx.build_supercell(model.lattice_spec(), nu)
+    cell = hx.compile_cell(model, sc)
+    assert cell.time_reversal_symmetric
+    kp = hx.make_bz_grid(model.lattice_spec(), nu, q, "reduced").kpoints
+    reps, mult = time_reversal_reduce(model.lattice_spec(), nu, kp)
+    lo, hi, npts = -6.580201874549387, 14.863393148450246, 201
+    step = (hi - lo) / (npts - 1)
+    words = sample_masks(sc.nunits, 0.1, 11, 1, 0, 12)
+    full, _, st1 = eval_batch(cell, kp, words, lo, step, npts, 0.01)
+    paired, _, st2 = eval_batch(cell, reps, words, lo, step, npts, 0.01, kmult=mult)
+    assert (st1 == 0).all() and (st2 == 0).all() and st2.shape == (12, len(reps))
+    np.testing.assert_allclose(paired, full, rtol=0, atol=1e-11)
+    om = O.graphene_model()
+    ocell = O.make_cell(om, nu)
+    key = sum(int(w) << (64 * i) for i, w in enumerate(words[3]))
+    ref = O.idos_from_bands(O.solve_bands(ocell, om, key, kp), np.full(len(kp), 1.0 / len(kp)), lo, hi, npts, 0.01,
+                            ocell.area)
+    np.testing.assert_allclose(paired[3], ref, rtol=0, atol=IDOS_TOL)
+    # the Engine uses the paired sets; switching them off gives the same level curves
+    eng = hx.Engine(model, nq=nu * q, delta=0.01, master_seed=4, bz_mode="reduced", energy_points=npts,
+                    energy_range=(lo + 0.02, hi - 0.02))
+    a = eng.sample_level(1, nu, 8, 0.1, with_cv=False).full
+    monkeypatch.setenv("HX_NO_TIME_REVERSAL", "1")
+    eng2 = hx.Engine(model, nq=nu * q, delta=0.01, master_seed=4, bz_mode="reduced", energy_points=npts,
+                     energy_range=(lo + 0.02, hi - 0.02))
+    b = eng2.sample_level(1, nu, 8, 0.1, with_cv=False).full
+    np.testing.assert_allclose(a, b, rtol=0, atol=1e-11)
