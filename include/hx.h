@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define HX_ABI_VERSION 1
+#define HX_ABI_VERSION 2
 
 /* return codes */
 #define HX_OK 0
@@ -70,6 +70,12 @@ typedef struct hx_cell_desc {
    * join sublattice 0 to 1 (graphene), T = [[0, C], [C^H, 0]] and the library may use the exact
    * bipartite identity eig(T) = +-sigma(C) (+ zeros).  NULL disables it. */
   const int32_t* sublattice;
+  /* optional [2*ndof] Cartesian position of each dof's site in the supercell (the frame of h_disp).
+   * With real amplitudes, batches whose k-points all make exp(2i k.R) = 1 for every hop's lattice
+   * translation R = disp - (pos_dst - pos_src) (time-reversal-invariant momenta, e.g. Gamma and the q = 2
+   * grid) are real in the periodic gauge exp(i k.R): the bipartite banded tier then runs its stage-1
+   * products in real arithmetic (one DMMA per fragment product instead of four).  NULL disables it. */
+  const double* dof_pos;
 } hx_cell_desc;
 
 /* Energy grid + smoothing (qoi.py:42-67, 77-82): eps_m = e0 + step*m, m < npts. */

@@ -43,7 +43,7 @@ class CellDesc(C.Structure):
         ("h_row_ptr", C.c_void_p), ("h_col", C.c_void_p), ("h_amp", C.c_void_p), ("h_disp", C.c_void_p),
         ("s_row_ptr", C.c_void_p), ("s_col", C.c_void_p), ("s_amp", C.c_void_p), ("s_disp", C.c_void_p),
         ("pencil", C.c_int32), ("eps0", C.c_double), ("t", C.c_double), ("s", C.c_double),
-        ("area", C.c_double), ("sublattice", C.c_void_p),
+        ("area", C.c_double), ("sublattice", C.c_void_p), ("dof_pos", C.c_void_p),
     ]
 
 

@@ -30,7 +30,8 @@ void bd_init_attributes();
 bool bd_path_supported(const CellDev& c);
 const char* bd_last_error();
 int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, int64_t nmasks, const GridDev& g,
-            int* diff, unsigned long long* trans, double* eigs, int* status, int sharp, size_t ws_budget,
-            const Alloc& alloc, cudaStream_t st, RefineItem* refine, unsigned long long* refine_count);
+            int* diff, unsigned long long* trans, double* eigs, int* status, int sharp, bool real,
+            size_t ws_budget, const Alloc& alloc, cudaStream_t st, RefineItem* refine,
+            unsigned long long* refine_count);
 
 }  // namespace hx

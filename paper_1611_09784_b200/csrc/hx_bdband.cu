@@ -70,9 +70,12 @@ struct BdWs {
 
 // ------------------------------------------------------------------------------------------------
 // C = A-B block of the phase matrix per (mask, k), zero padded to S x S; dims = nA + nB.
+// real: the batch's k-points make the periodic-gauge matrix real (hx_capi batch_is_real): C is assembled as
+// C[ia][jb] = Re(h exp(i k.(pos_a - pos_b))) (the unitary diagonal gauge change keeps the singular values;
+// the dropped imaginary part is rounding), so every later stage sees exactly real data.
 __global__ void __launch_bounds__(256) bd_assemble_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
                                                           const uint64_t* __restrict__ masks, int64_t mat0,
-                                                          double2* ws, BdWs L, int* dims, int* status) {
+                                                          double2* ws, BdWs L, int* dims, int* status, int real) {
   extern __shared__ int bsm[];
   int* idx_a = bsm;
   int* idx_b = idx_a + c.N;
@@ -87,13 +90,14 @@ __global__ void __launch_bounds__(256) bd_assemble_kernel(CellDev c, const doubl
     dims[blockIdx.x] = d;
     status[mat] = d == 0 ? 3 : 0;
   }
-  assemble_bipartite(c, idx_a, idx_b, kpts[kk], C, L.S, L.S, L.S, false);
+  assemble_bipartite(c, idx_a, idx_b, kpts[kk], C, L.S, L.S, L.S, false, real != 0);
 }
 
 // ------------------------------------------------------------------------------------------------
 bool launch_cluster_panel(double2* ws, const PanelArgs& a, int64_t cnt, cudaStream_t st);
 
 // M[mr0.., mc0..] -= U W^H (m x n, K = 32): 64 x 64 tiles at 2 CTAs/SM (HX_RU_TN=32: 64 x 32 at 4/SM, same speed)
+template <bool RE = false>
 static void launch_rank_update(double2* ws, const SlabGeom& G, int mr0, int mc0, int m, int n, size_t u_off,
                                size_t w_off, int64_t cnt, cudaStream_t st) {
   static const int tn = [] {
@@ -102,10 +106,10 @@ static void launch_rank_update(double2* ws, const SlabGeom& G, int mr0, int mc0,
   }();
   const unsigned gx = (unsigned)((m + RU_T - 1) / RU_T);
   if (tn == 64)
-    rank_update_kernel<64><<<dim3(gx, (unsigned)((n + 63) / 64), (unsigned)cnt), 256, ru_smem<64>(), st>>>(
+    rank_update_kernel<64, RE><<<dim3(gx, (unsigned)((n + 63) / 64), (unsigned)cnt), 256, ru_smem<64>(), st>>>(
         ws, G, mr0, mc0, m, n, u_off, w_off);
   else
-    rank_update_kernel<32><<<dim3(gx, (unsigned)((n + 31) / 32), (unsigned)cnt), 128, ru_smem<32>(), st>>>(
+    rank_update_kernel<32, RE><<<dim3(gx, (unsigned)((n + 31) / 32), (unsigned)cnt), 128, ru_smem<32>(), st>>>(
         ws, G, mr0, mc0, m, n, u_off, w_off);
 }
 
@@ -120,6 +124,9 @@ static void launch_rank_update(double2* ws, const SlabGeom& G, int mr0, int mc0,
 //   Z = (C[k0+32:, k0+32:] V2) T2         (xv<0>, applying the pending left update V1[32:] X1^H on the fly)
 //   C[k0+32:, k0+32:k0+64] -= Z V2[:32]^H (the 32 columns the next column panel needs)
 // and C[k0+32:, k0+64:] -= Z V2[32:]^H stays pending for the next step's xv<1>.
+// RE: the batch is real (periodic gauge, bd_assemble_kernel): the stage-1 products issue only the real DMMAs
+// (the panel and chase kernels keep their complex arithmetic; on real data their results stay real).
+template <bool RE>
 static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, cudaStream_t st) {
   const int S = L.S;
   const SlabGeom G{L.stride, S, L.c_off};
@@ -144,11 +151,11 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     if (n2 <= 0) break;
     const dim3 gx1((unsigned)((n2 + XV_TM - 1) / XV_TM), (unsigned)cnt);
     if (!pend)
-      xv_kernel<1><<<gx1, 128, XV_SMEM, st>>>(ws, G, k0, k0 + BB, n2, m1, L.v1_off, L.x_off, L.t1_off);
+      xv_kernel<1, false, RE><<<gx1, 128, XV_SMEM, st>>>(ws, G, k0, k0 + BB, n2, m1, L.v1_off, L.x_off, L.t1_off);
     else  // pending: C[r][c] -= Z[r - k0] conj(V2[32 + c - (k0 + 32)])
       xv_kernel<1, true><<<gx1, 128, XV_SMEM_UPD, st>>>(ws, G, k0, k0 + BB, n2, m1, L.v1_off, L.x_off, L.t1_off,
                                                          L.v2_off + BB, L.z_off);
-    launch_rank_update(ws, G, k0, k0 + BB, fused ? std::min(BB, m1) : m1, n2, L.v1_off, L.x_off, cnt, st);
+    launch_rank_update<RE>(ws, G, k0, k0 + BB, fused ? std::min(BB, m1) : m1, n2, L.v1_off, L.x_off, cnt, st);
     count_launch(2);
     // ---- right: row panel LQ of the (updated) rows k0..k0+BB, C_tr2 = C[k0+BB:, k0+BB:] <- C_tr2 Q2
     PanelArgs p2{L.stride, L.c_off, S, k0, k0 + BB, n2, 1, L.v2_off, S, L.t2_off};
@@ -160,9 +167,9 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     const int m3 = S - k0 - BB;
     pend = false;
     if (m3 > 0 && !fused) {
-      xv_kernel<0><<<dim3((unsigned)((m3 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM, st>>>(
+      xv_kernel<0, false, RE><<<dim3((unsigned)((m3 + XV_TM - 1) / XV_TM), (unsigned)cnt), 128, XV_SMEM, st>>>(
           ws, G, k0 + BB, k0 + BB, m3, n2, L.v2_off, L.z_off, L.t2_off);
-      launch_rank_update(ws, G, k0 + BB, k0 + BB, m3, n2, L.z_off, L.v2_off, cnt, st);
+      launch_rank_update<RE>(ws, G, k0 + BB, k0 + BB, m3, n2, L.z_off, L.v2_off, cnt, st);
       count_launch(2);
     } else if (m3 > 0) {
       // Z = (C_tr2 V2) T2 with the pending left update C[r][c] -= V1[32 + r - (k0+32)] conj(X1[c - (k0+32)])
@@ -235,6 +242,10 @@ void bd_init_attributes() {
   set_smem_attr(xv_kernel<1, true>, XV_SMEM_UPD);
   set_smem_attr(rank_update_kernel<64>, (int)ru_smem<64>());
   set_smem_attr(rank_update_kernel<32>, (int)ru_smem<32>());
+  set_smem_attr(rank_update_kernel<64, true>, (int)ru_smem<64>());
+  set_smem_attr(rank_update_kernel<32, true>, (int)ru_smem<32>());
+  set_smem_attr(xv_kernel<0, false, true>, (int)XV_SMEM);
+  set_smem_attr(xv_kernel<1, false, true>, (int)XV_SMEM);
   set_smem_attr(bd_assemble_kernel, 140 * 1024);
 #define BD_CHASE_ATTR(NW, DUAL, CL)                                                                        \
   set_smem_attr(bd_chase_kernel<NW, BB, DUAL, CL>, bd_chase_smem<NW, BB, DUAL>())
@@ -252,8 +263,9 @@ void bd_init_attributes() {
 }
 
 int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, int64_t nmasks, const GridDev& g,
-            int* diff, unsigned long long* trans, double* eigs, int* status, int sharp, size_t ws_budget,
-            const Alloc& alloc, cudaStream_t st, RefineItem* refine, unsigned long long* refine_count) {
+            int* diff, unsigned long long* trans, double* eigs, int* status, int sharp, bool real,
+            size_t ws_budget, const Alloc& alloc, cudaStream_t st, RefineItem* refine,
+            unsigned long long* refine_count) {
   const int S = c.nsub;
   const BdWs L = BdWs::make(S);
   const size_t per = L.stride * sizeof(double2) + sizeof(int);
@@ -273,10 +285,10 @@ int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, 
   ce.N = 2 * S;
   for (int64_t m0 = 0; m0 < nmat; m0 += chunk) {
     const int64_t cnt = std::min(chunk, nmat - m0);
-    bd_assemble_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, masks, m0, ws, L, dims, status);
+    bd_assemble_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, masks, m0, ws, L, dims, status, real ? 1 : 0);
     count_launch();
     BD_CUDA(cudaGetLastError());
-    if (bd_reduce(ws, L, cnt, dims, st)) return -1;
+    if (real ? bd_reduce<true>(ws, L, cnt, dims, st) : bd_reduce<false>(ws, L, cnt, dims, st)) return -1;
     launch_eig_idos(ce, nk, g, m0, cnt, reinterpret_cast<const double*>(ws + L.tgk_off), L.stride * 2, dims, diff,
                     trans, eigs, status, sharp, st, refine, refine_count, true);
     BD_CUDA(cudaGetLastError());

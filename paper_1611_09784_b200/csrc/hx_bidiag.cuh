@@ -62,8 +62,11 @@ static __device__ int2 block_compact_bipartite(const CellDev& c, const uint64_t*
 
 // Assemble M (rows >= cols) into column-major smem (ld = lm).  idx_a / idx_b: compacted rank of each
 // kept dof inside its sublattice (-1 if removed or other sublattice).  If transpose, M = C^H.
+// periodic: multiply by exp(i k.(pos_a - pos_b)) and keep the real part (the periodic gauge of a batch whose
+// k-points make it real, see bd_assemble_kernel).
 static __device__ void assemble_bipartite(const CellDev& c, const int* idx_a, const int* idx_b, double2 k,
-                                          double2* M, int lm, int rows, int cols, bool transpose) {
+                                          double2* M, int lm, int rows, int cols, bool transpose,
+                                          bool periodic = false) {
   for (int p = threadIdx.x; p < lm * cols; p += blockDim.x) M[p] = make_double2(0.0, 0.0);
   __syncthreads();
   for (int r = threadIdx.x; r < c.N; r += blockDim.x) {
@@ -73,7 +76,13 @@ static __device__ void assemble_bipartite(const CellDev& c, const int* idx_a, co
     auto visit = [&](int cb) {
       const int jb = idx_b[cb];
       if (jb < 0) return;
-      const double2 h = herm_element(c.h_ptr, c.h_col, c.h_amp, c.h_disp, r, cb, k);
+      double2 h = herm_element(c.h_ptr, c.h_col, c.h_amp, c.h_disp, r, cb, k);
+      if (periodic) {
+        const double2 pa = c.pos[r], pb = c.pos[cb];
+        double sn, cs;
+        sincos(k.x * (pa.x - pb.x) + k.y * (pa.y - pb.y), &sn, &cs);
+        h = make_double2(h.x * cs - h.y * sn, 0.0);
+      }
       if (!transpose) M[ia + (size_t)jb * lm] = h;
       else M[jb + (size_t)ia * lm] = make_double2(h.x, -h.y);
     };

@@ -76,7 +76,24 @@ struct hx_cell {
   hx_ctx* ctx = nullptr;
   hx::CellDev dev{};
   std::vector<void*> allocs;
+  // periodic-gauge realness: real amplitudes and the lattice translation R of every hop (host copy)
+  bool real_amps = false;
+  std::vector<double> lat;  // [2 * nnz] R = disp - (pos_dst - pos_src)
 };
+
+namespace {
+// All k-points make the periodic-gauge matrix real: exp(2i k.R) = 1 for every hop's lattice translation.
+bool batch_is_real(const hx_cell* cell, const double* kpoints, int nk) {
+  if (!cell->real_amps || !cell->dev.pos || cell->lat.empty()) return false;
+  const size_t nnz = cell->lat.size() / 2;
+  for (int k = 0; k < nk; ++k)
+    for (size_t e = 0; e < nnz; ++e) {
+      const double ph = 2.0 * (kpoints[2 * k] * cell->lat[2 * e] + kpoints[2 * k + 1] * cell->lat[2 * e + 1]);
+      if (std::fabs(std::sin(ph)) > 1e-9 || std::cos(ph) < 0.0) return false;
+    }
+  return true;
+}
+}  // namespace
 
 namespace {
 
@@ -114,6 +131,8 @@ void transpose_csr(int N, const int32_t* ptr, const int32_t* col, std::vector<in
   std::vector<int32_t> fill(tptr.begin(), tptr.end() - 1);
   for (int e = 0; e < nnz; ++e) tinst[fill[col[e]]++] = e;
 }
+
+bool g_real_batches = true;  // periodic-gauge real arithmetic for TRIM batches (HX_NO_REAL=1 disables)
 
 int fixed_point_shift(int64_t nk, int N) {
   const double terms = (double)nk * (double)(N + 1) + 1.0;
@@ -182,6 +201,8 @@ int hx_ctx_create_priority(int32_t device, int32_t priority, hx_ctx** out) {
     if (bm && bm[0]) ctx->bd_min_n = atoi(bm);
     const char* bw = getenv("HX_BIDIAG_WARP_MAX_S");
     if (bw && bw[0]) ctx->bidiag_warp_max_s = atoi(bw);
+    const char* nr = getenv("HX_NO_REAL");
+    if (nr && nr[0] && nr[0] != '0') g_real_batches = false;
     const char* zm = getenv("HX_ZONE_MIN_N");
     if (zm && zm[0]) hx::g_zone_min_n = atoi(zm);
     const char* bt = getenv("HX_BIDIAG_THREADS");
@@ -259,6 +280,22 @@ int hx_cell_create(hx_ctx* ctx, const hx_cell_desc* d, hx_cell** out) {
     }
   }
   rc |= upload(cell, d->onsite, N, &c.onsite);
+  c.pos = nullptr;
+  if (d->dof_pos && d->pencil != HX_PENCIL_GENERAL) {
+    rc |= upload(cell, reinterpret_cast<const double2*>(d->dof_pos), N, &c.pos);
+    const int nnz = d->h_row_ptr[N];
+    bool real = true;
+    for (int r = 0; r < N; ++r) real &= d->onsite[r] == d->onsite[r];
+    cell->lat.resize((size_t)2 * nnz);
+    for (int r = 0; r < N; ++r)
+      for (int e = d->h_row_ptr[r]; e < d->h_row_ptr[r + 1]; ++e) {
+        const int dst = d->h_col[e];
+        real &= d->h_amp[2 * e + 1] == 0.0;
+        cell->lat[2 * e] = d->h_disp[2 * e] - (d->dof_pos[2 * dst] - d->dof_pos[2 * r]);
+        cell->lat[2 * e + 1] = d->h_disp[2 * e + 1] - (d->dof_pos[2 * dst + 1] - d->dof_pos[2 * r + 1]);
+      }
+    cell->real_amps = real;
+  }
   {
     const int nnz = d->h_row_ptr[N];
     std::vector<int32_t> tptr, tinst, src;
@@ -399,7 +436,8 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
     }
   } else if (use_bd) {
     if (make_refine(nmat * N)) return fail(HX_E_CUDA, "alloc refinement list");
-    int rc = hx::bd_eval(c, kp, nk, d_masks, nmasks, g, diff, trans, d_eigs, status, sharp, ctx->ws_budget,
+    const bool real = g_real_batches && batch_is_real(cell, kpoints, nk);
+    int rc = hx::bd_eval(c, kp, nk, d_masks, nmasks, g, diff, trans, d_eigs, status, sharp, real, ctx->ws_budget,
                          [&](size_t bytes) -> void* { return ctx->band.grow(bytes) ? nullptr : ctx->band.p; }, st,
                          refine, refine_count);
     if (rc) return fail(HX_E_CUDA, std::string("bipartite band path: ") + hx::bd_last_error());

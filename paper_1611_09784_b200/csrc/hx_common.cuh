@@ -38,6 +38,7 @@ struct CellDev {
   int32_t bipartite;
   int32_t nsub;        // max dofs on one sublattice
   const int32_t* sub;  // [N] sublattice of each dof
+  const double2* pos;  // [N] Cartesian site position of each dof (periodic gauge), or nullptr
 };
 
 struct GridDev {

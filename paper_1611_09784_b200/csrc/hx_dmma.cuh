@@ -29,4 +29,12 @@ struct CTile {
   }
 };
 
+// C += A * B on real data (RE: every imaginary part is exactly zero, so only the real-real product is
+// issued - one DMMA instead of four; the imaginary accumulators stay as they are).
+template <bool RE>
+__device__ __forceinline__ void cmac(CTile& t, double ar, double ai, double br, double bi) {
+  if constexpr (RE) dmma(t.re0, t.re1, ar, br);
+  else t.mac(ar, ai, br, bi);
+}
+
 }  // namespace hx

@@ -54,7 +54,7 @@ static_assert((size_t)(XV_TM + GBW) * (GBW + 4) * sizeof(double2) <= XV_SMEM, "x
 // a separate rank update (read + write) followed by this product (read).  In matrix terms:
 //   MODE 0: M[ar0+i][ac0+k] -= R[i] conj(S[k]);   MODE 1: M[ar0+k][ac0+i] -= S[k] conj(R[i]).
 // R[i][l] = base[r_off + i0 + i + l*ld], S[k][l] = base[s_off + k + l*ld].
-template <int MODE, bool UPD = false>
+template <int MODE, bool UPD = false, bool RE = false>
 __global__ void __launch_bounds__(128) xv_kernel(double2* ws, SlabGeom g, int ar0, int ac0, int rows, int K,
                                                  size_t v_off, size_t x_off, size_t t_off, size_t r_off = 0,
                                                  size_t s_off = 0) {
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(128) xv_kernel(double2* ws, SlabGeom g, int ar
 #pragma unroll
       for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
-        for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(a[rt].x, a[rt].y, b[ct].x, b[ct].y);
+        for (int ct = 0; ct < 4; ++ct) cmac<RE>(acc[rt][ct], a[rt].x, a[rt].y, b[ct].x, b[ct].y);
     }
   }
   // ---- epilogue: X <- (op(A) V) T with T (GBW x GBW, column-major) - the block reflector's T factor,
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(128) xv_kernel(double2* ws, SlabGeom g, int ar
 #pragma unroll
     for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
-      for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(a[rt].x, a[rt].y, b[ct].x, b[ct].y);
+      for (int ct = 0; ct < 4; ++ct) cmac<RE>(acc[rt][ct], a[rt].x, a[rt].y, b[ct].x, b[ct].y);
   }
 #pragma unroll
   for (int rt = 0; rt < 2; ++rt)
@@ -273,7 +273,7 @@ constexpr int RU_T = 64, RU_LD = GBW + 4;
 constexpr size_t RU_SMEM = (size_t)2 * RU_T * RU_LD * sizeof(double2);
 
 // TN = 64: 8 warps (4 x 2) per 64 x 64 tile, 2 CTAs/SM; TN = 32: 4 warps per 64 x 32 tile, 4 CTAs/SM.
-template <int TN>
+template <int TN, bool RE = false>
 __global__ void __launch_bounds__(2 * TN * 2, TN == 64 ? 2 : 4) rank_update_kernel(double2* ws, SlabGeom g, int mr0,
                                                                                   int mc0, int m, int n, size_t u_off,
                                                                                   size_t w_off) {
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(2 * TN * 2, TN == 64 ? 2 : 4) rank_update_kern
 #pragma unroll
     for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
-      for (int ct = 0; ct < 4; ++ct) acc[rt][ct].mac(-au[rt].x, -au[rt].y, bw[ct].x, bw[ct].y);
+      for (int ct = 0; ct < 4; ++ct) cmac<RE>(acc[rt][ct], -au[rt].x, -au[rt].y, bw[ct].x, bw[ct].y);
   }
 #pragma unroll
   for (int rt = 0; rt < 2; ++rt)

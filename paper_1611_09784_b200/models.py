@@ -238,6 +238,9 @@ class CompiledCell:
             sub = np.ascontiguousarray(self.supercell.basis_index[self.dof_site], dtype=np.int32)
             keep.append(sub)
             desc.sublattice = _lib.ptr(sub)
+            pos = np.ascontiguousarray(self.supercell.positions[self.dof_site], dtype=np.float64).reshape(-1)
+            keep.append(pos)
+            desc.dof_pos = _lib.ptr(pos)
             h = C.c_void_p()
             _lib.check(lib.hx_cell_create(ctx, C.byref(desc), C.byref(h)), "hx_cell_create")
             self._handle = h
