@@ -31,6 +31,7 @@
 namespace hx {
 
 bool g_bd_chase_pair = true;  // warp-pair bulge chase (HX_CHASE_PAIR=0: one warp per task)
+bool g_bd_chase_real = true;  // real bulge chase for real (periodic-gauge) batches (HX_CHASE_REAL=0: complex)
 
 
 constexpr int BB = 32;  // band width
@@ -48,7 +49,7 @@ const char* bd_last_error() { return g_bd_err.c_str(); }
   } while (0)
 
 struct BdWs {
-  size_t c_off, v1_off, v2_off, x_off, z_off, t1_off, t2_off, tgk_off;  // double2 units
+  size_t c_off, v1_off, v2_off, x_off, z_off, t1_off, t2_off, band_off, tgk_off;  // double2 units
   size_t stride;
   int S;
   static BdWs make(int S) {
@@ -61,7 +62,8 @@ struct BdWs {
     w.z_off = w.x_off + (size_t)S * BB;
     w.t1_off = w.z_off + (size_t)S * BB;
     w.t2_off = w.t1_off + (size_t)BB * BB;
-    w.tgk_off = w.t2_off + (size_t)BB * BB;  // diag[2S] + e2[2S] doubles = 2S double2
+    w.band_off = w.t2_off + (size_t)BB * BB;  // real chase: compact band, S x RB_LD doubles
+    w.tgk_off = w.band_off + (size_t)S * RB_LD / 2 + 1;  // diag[2S] + e2[2S] doubles = 2S double2
     w.stride = (w.tgk_off + (size_t)2 * S + 16 + 15) & ~(size_t)15;
     return w;
   }
@@ -210,6 +212,23 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
                                                                                                  dims);  \
     BD_CUDA(cudaGetLastError());                                                                        \
   }
+#define BD_CHASE_REAL(NW)                                                                                \
+  {                                                                                                     \
+    bd_chase_real_kernel<NW, BB><<<(unsigned)cnt, NW * 32, bd_chase_real_smem<NW, BB>(), st>>>(ws, a1, L.band_off, \
+                                                                                                a3, S, dims); \
+    BD_CUDA(cudaGetLastError());                                                                        \
+  }
+  if (RE && g_bd_chase_real) {
+    bd_band_extract_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, L.stride, L.c_off, L.band_off, S);
+    count_launch();
+    // real band: a quarter of the arithmetic and half the shared memory per sweep
+    if (want >= 6) BD_CHASE_REAL(16)
+    else if (want >= 2) BD_CHASE_REAL(2)
+    else BD_CHASE_REAL(1)
+    count_launch();
+    return 0;
+  }
+#undef BD_CHASE_REAL
   const bool pair = chase_mode >= 4 || (chase_mode == 0 && g_bd_chase_pair);
   // warp-pair tasks for the throughput-bound launches (many matrices); the latency-bound one-CTA-per-matrix
   // launch keeps one warp per task (its shared-memory pipe is the limit, measured 24.3 vs 25.1 ms)
@@ -258,6 +277,16 @@ void bd_init_attributes() {
   set_smem_attr(bd_chase_pair_kernel<1, BB>, bd_chase_pair_smem<1, BB>());
   set_smem_attr(bd_chase_pair_kernel<2, BB>, bd_chase_pair_smem<2, BB>());
   set_smem_attr(bd_chase_pair_kernel<10, BB>, bd_chase_pair_smem<10, BB>());
+  set_smem_attr(bd_chase_real_kernel<1, BB>, bd_chase_real_smem<1, BB>());
+  set_smem_attr(bd_chase_real_kernel<2, BB>, bd_chase_real_smem<2, BB>());
+  set_smem_attr(bd_chase_real_kernel<16, BB>, bd_chase_real_smem<16, BB>());
+  const char* sp = getenv("HX_CHASE_SPIN_NS");
+  if (sp && sp[0]) {
+    const unsigned v = (unsigned)atoi(sp);
+    cudaMemcpyToSymbol(g_spin_ns, &v, sizeof(v));
+  }
+  const char* cr = getenv("HX_CHASE_REAL");
+  if (cr && cr[0]) g_bd_chase_real = atoi(cr) != 0;
   const char* pe = getenv("HX_CHASE_PAIR");
   if (pe && pe[0]) g_bd_chase_pair = atoi(pe) != 0;
 }

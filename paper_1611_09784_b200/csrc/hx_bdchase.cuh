@@ -322,6 +322,250 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_kernel(double2* ws, size_
 }
 
 // ---------------------------------------------------------------------------------------------------
+// Real variant for the batches whose band is real (periodic gauge at time-reversal-invariant k, see
+// bd_assemble_kernel): same sweep / task / progress-flag structure as bd_chase_kernel (one warp per
+// sweep, single tile buffer), real reflectors, real tiles (half the shared memory per warp, a quarter of
+// the arithmetic).  Only the real parts of the double2 band are read (8-byte cp.async) and written.
+// Poll interval of a waiting sweep in the real chase (ns; HX_CHASE_SPIN_NS).
+__constant__ unsigned g_spin_ns = 20;
+
+struct QuickReflectorR {
+  double tau, scale, beta;
+};
+__device__ __forceinline__ QuickReflectorR quick_reflector_r(double alpha, double sig2) {
+  QuickReflectorR h;
+  if (!(sig2 >= HX_REFLECTOR_TINY)) {
+    h.tau = h.scale = h.beta = 0.0;
+    return h;
+  }
+  const double aa = fabs(alpha), ph = alpha < 0.0 ? -1.0 : 1.0;
+  if (aa * aa < 1e-280 && alpha != 0.0) {
+    const double sigma = sqrt(sig2), mag = aa + sigma;
+    h.tau = mag / sigma;
+    h.scale = ph / mag;
+    h.beta = -ph * sigma;
+    return h;
+  }
+  const double rs = rsqrt(sig2), sigma = sig2 * rs, mag = aa + sigma;
+  h.tau = mag * rs;
+  h.scale = ph * __drcp_rn(mag);
+  h.beta = -ph * sigma;
+  return h;
+}
+
+// Compact real band of the real chase: element (r, c) with c - 63 <= r <= c + 31 (the upper band of width
+// 32 plus the bulges of the X and Y tiles) at B[c * RB_LD + r - c + RB_OFF]; stepping one column right
+// along a row is a stride of RB_LD - 1.
+constexpr int RB_LD = 96, RB_OFF = 63;
+
+template <int BWc>
+struct BdChaseSmemR {
+  double X[BWc][BWc + 1];  // X, then Y (zero-padded)
+  double ug[BWc], vh[BWc], cb[BWc];
+};
+
+__device__ __forceinline__ void bd_cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem));
+}
+
+template <int NW, int BWc>
+__global__ void __launch_bounds__(NW * 32, 1) bd_chase_real_kernel(double2* ws, size_t stride, size_t band_off,
+                                                                    size_t tgk_off, int S, const int* dims) {
+  extern __shared__ __align__(16) unsigned char bd_smem[];
+  BdChaseSmemR<BWc>* all = reinterpret_cast<BdChaseSmemR<BWc>*>(bd_smem);
+  volatile int* prog = reinterpret_cast<volatile int*>(all + NW);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  BdChaseSmemR<BWc>& W = all[warp];
+  const int64_t mat = blockIdx.x;
+  double2* base = ws + (size_t)mat * stride;
+  // compact real band (bd_band_extract_kernel): element (r, c), c - 63 <= r <= c + 31, at B[c * RB_LD + r - c + 63]
+  double* B = reinterpret_cast<double*>(base + band_off);
+  double* diag = reinterpret_cast<double*>(base + tgk_off);
+  double* e2 = diag + 2 * S;
+  for (int q = threadIdx.x; q < 2 * S; q += blockDim.x) {
+    diag[q] = 0.0;
+    e2[q] = 0.0;
+  }
+  if (lane == 0) prog[warp] = -1;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const double a0 = B[RB_OFF];
+    e2[0] = a0 * a0;  // alpha_0: final after stage 1
+  }
+  const bool skip = dims && dims[mat] == 0;
+  const int nsweeps = skip ? 0 : S - 1;
+  for (int i = warp; i < nsweeps; i += NW) {
+    const int tasks = (S - 1 - i + BWc - 1) / BWc;
+    const int prev_tasks = i > 0 ? (S - i + BWc - 1) / BWc : 0;
+    volatile int* pflag = prog + (i - 1 + NW) % NW;
+    double taug = 0.0;
+    for (int t = 0; t < tasks; ++t) {
+      if (i > 0) {
+        const int need = (i - 1) * 65536 + min(t + 2, prev_tasks);
+        if (lane == 0)
+          while (*pflag < need) __nanosleep(g_spin_ns);
+        __syncwarp();
+        __threadfence_block();
+      }
+      const int s = i + 1 + t * BWc;
+      const int len = min(BWc, S - s);
+      const int lb = max(0, min(BWc, S - s - len));
+      // ---- X tile (zero-padded): element (s + lane, s + cc) at blk[cc * (RB_LD - 1)]
+      double* const blk = B + ((size_t)s * RB_LD + lane + RB_OFF);
+      {
+        const double* src = blk;
+        if (len == BWc) {
+#pragma unroll 8
+          for (int cc = 0; cc < BWc; ++cc, src += RB_LD - 1) bd_cp_async8(&W.X[lane][cc], src);
+        } else {
+#pragma unroll 4
+          for (int cc = 0; cc < BWc; ++cc, src += RB_LD - 1) {
+            if (lane < len && cc < len) bd_cp_async8(&W.X[lane][cc], src);
+            else W.X[lane][cc] = 0.0;
+          }
+        }
+      }
+      if (t == 0) {
+        // right reflector from row i, columns [s, s+len): row i -> (beta, 0, ...)
+        double* const rowi = B + ((size_t)(s + lane) * RB_LD + i - (s + lane) + RB_OFF);  // (i, s + lane)
+        const double x = lane < len ? *rowi : 0.0;
+        const double sig2 = warp_sum(x * x);
+        const QuickReflectorR h = quick_reflector_r(__shfl_sync(0xffffffffu, x, 0), sig2);
+        taug = h.tau;
+        W.ug[lane] = lane == 0 ? 1.0 : (lane < len ? x * h.scale : 0.0);
+        if (lane < len && taug != 0.0) *rowi = lane == 0 ? h.beta : 0.0;
+        if (lane == 0) e2[2 * i + 1] = sig2;
+      }
+      bd_cp_async_wait_all();
+      __syncwarp();
+      // ---- X row pass: ty = tau_g (X u)_r; column 0 of X G -> left reflector H
+      double ty;
+      {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+        for (int c = 0; c < BWc; c += 2) {
+          a0 = fma(W.X[lane][c], W.ug[c], a0);
+          a1 = fma(W.X[lane][c + 1], W.ug[c + 1], a1);
+        }
+        ty = taug * (a0 + a1);
+      }
+      const double x0 = W.X[lane][0] - ty;
+      const double sh2 = warp_sum(x0 * x0);
+      const QuickReflectorR hh = quick_reflector_r(__shfl_sync(0xffffffffu, x0, 0), sh2);
+      const double tauh = hh.tau;
+      if (t == 0 && lane == 0) e2[2 * s] = sh2;
+      const double v = lane == 0 ? 1.0 : x0 * hh.scale;  // zero on padded rows
+      W.vh[lane] = v;
+      const double w = warp_sum(v * ty);  // v^T (tau_g y)
+      __syncwarp();
+      // ---- X column pass: p = v^T X, b_c = tau_h (p_c - w u_c)
+      {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+        for (int r = 0; r < BWc; r += 2) {
+          a0 = fma(W.vh[r], W.X[r][lane], a0);
+          a1 = fma(W.vh[r + 1], W.X[r + 1][lane], a1);
+        }
+        W.cb[lane] = tauh * (a0 + a1 - w * W.ug[lane]);
+      }
+      __syncwarp();
+      // ---- X: fused rank-2 row update, straight to HBM: X' = X - ty u^T - v b^T
+      if (lane < len) {
+        double* dst = blk;
+#pragma unroll 4
+        for (int c = 0; c < BWc; ++c, dst += RB_LD - 1) {
+          double z = fma(-v, W.cb[c], fma(-ty, W.ug[c], W.X[lane][c]));
+          if (c == 0 && tauh != 0.0) z = lane == 0 ? hh.beta : 0.0;
+          if (c < len) *dst = z;
+        }
+      }
+      double next_tau = 0.0;
+      if (lb > 0) {
+        __syncwarp();
+        {
+          const double* src = blk + (size_t)len * (RB_LD - 1);  // (s + lane, s + len + cc)
+          if (len == BWc && lb == BWc) {
+#pragma unroll 8
+            for (int cc = 0; cc < BWc; ++cc, src += RB_LD - 1) bd_cp_async8(&W.X[lane][cc], src);
+          } else {
+#pragma unroll 4
+            for (int cc = 0; cc < BWc; ++cc, src += RB_LD - 1) {
+              if (lane < len && cc < lb) bd_cp_async8(&W.X[lane][cc], src);
+              else W.X[lane][cc] = 0.0;
+            }
+          }
+          bd_cp_async_wait_all();
+          __syncwarp();
+        }
+        // ---- Y column pass: q = v^T Y; row 0 of H Y -> next right reflector G'
+        double q;
+        {
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+          for (int r = 0; r < BWc; r += 2) {
+            a0 = fma(W.vh[r], W.X[r][lane], a0);
+            a1 = fma(W.vh[r + 1], W.X[r + 1][lane], a1);
+          }
+          q = a0 + a1;
+        }
+        const double xg = W.X[0][lane] - tauh * q;  // row 0 of H Y
+        const double sg2 = warp_sum(xg * xg);
+        const QuickReflectorR hg = quick_reflector_r(__shfl_sync(0xffffffffu, xg, 0), sg2);
+        next_tau = hg.tau;
+        const double u2 = lane == 0 ? 1.0 : xg * hg.scale;  // zero on padded columns
+        const double qu = warp_sum(q * u2);                  // (v^T Y) u'
+        __syncwarp();  // everyone is done with ug (X update) and cb
+        W.ug[lane] = u2;
+        W.cb[lane] = tauh * q;  // d_c
+        __syncwarp();
+        // ---- Y row pass: f = tau_g' (Y u' - tau_h v (q . u')), Y' = Y - v d^T - f u'^T, to HBM
+        if (lane < len) {
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+          for (int c = 0; c < BWc; c += 2) {
+            a0 = fma(W.X[lane][c], W.ug[c], a0);
+            a1 = fma(W.X[lane][c + 1], W.ug[c + 1], a1);
+          }
+          const double f = next_tau * (a0 + a1 - tauh * v * qu);
+          const bool row0 = lane == 0 && next_tau != 0.0;
+          double* dst = blk + (size_t)len * (RB_LD - 1);
+#pragma unroll 4
+          for (int c = 0; c < BWc; ++c, dst += RB_LD - 1) {
+            double z = fma(-f, W.ug[c], fma(-v, W.cb[c], W.X[lane][c]));
+            if (row0) z = c == 0 ? hg.beta : 0.0;
+            if (c < lb) *dst = z;
+          }
+        }
+      }
+      taug = next_tau;
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) prog[warp] = i * 65536 + t + 1;
+    }
+  }
+}
+
+// Real parts of the upper band (and the zero window around it) of the dense S x S slab C into the compact
+// band buffer of the real chase.  One CTA per matrix.
+static __global__ void __launch_bounds__(256) bd_band_extract_kernel(double2* ws, size_t stride, size_t c_off,
+                                                                      size_t band_off, int S) {
+  double2* base = ws + (size_t)blockIdx.x * stride;
+  const double2* C = base + c_off;
+  double* B = reinterpret_cast<double*>(base + band_off);
+  const size_t n = (size_t)S * RB_LD;
+  for (size_t p = threadIdx.x; p < n; p += blockDim.x) {
+    const int c = (int)(p / RB_LD), r = c + (int)(p % RB_LD) - RB_OFF;
+    B[p] = (r >= 0 && r < S) ? C[r + (size_t)c * S].x : 0.0;
+  }
+}
+
+template <int NW, int BWc>
+constexpr size_t bd_chase_real_smem() {
+  return NW * sizeof(BdChaseSmemR<BWc>) + 64;
+}
+
+// ---------------------------------------------------------------------------------------------------
 // Warp-pair variant: every task is split over two warps (64 threads, a pair of one "slot"), halving the
 // serial instruction stream of a task (the chase is bound by the latency of one task times the sweep
 // stagger, and by the issue rate of the few tasks in flight).  Lane = row in the row-oriented phases
