@@ -26,7 +26,8 @@ def test_library_loads_and_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) <= set(_lib.EXPORTED)
-    assert lib.hx_abi_version() == 1
+    header_version = int(re.search(r"#define HX_ABI_VERSION (\d+)", (ROOT / "include" / "hx.h").read_text()).group(1))
+    assert lib.hx_abi_version() == header_version
 
 
 def test_no_device_is_reported_loudly_without_gpu():
