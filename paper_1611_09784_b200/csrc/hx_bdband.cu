@@ -27,11 +27,13 @@
 #include "hx_kernels.cuh"
 #include "hx_panel.cuh"
 #include "hx_bdchase.cuh"
+#include "hx_real.cuh"
 
 namespace hx {
 
 bool g_bd_chase_pair = true;  // warp-pair bulge chase (HX_CHASE_PAIR=0: one warp per task)
 bool g_bd_chase_real = true;  // real bulge chase for real (periodic-gauge) batches (HX_CHASE_REAL=0: complex)
+bool g_bd_real_stage1 = true;  // real storage + arithmetic in stage 1 of real batches, S % 4 == 0 (HX_REAL_STAGE1=0)
 
 
 constexpr int BB = 32;  // band width
@@ -92,7 +94,9 @@ __global__ void __launch_bounds__(256) bd_assemble_kernel(CellDev c, const doubl
     dims[blockIdx.x] = d;
     status[mat] = d == 0 ? 3 : 0;
   }
-  assemble_bipartite(c, idx_a, idx_b, kpts[kk], C, L.S, L.S, L.S, false, real != 0);
+  // real == 2: real storage (doubles, ld S) for the real stage 1 (hx_real.cuh)
+  assemble_bipartite(c, idx_a, idx_b, kpts[kk], C, L.S, L.S, L.S, false, real != 0,
+                     real == 2 ? reinterpret_cast<double*>(C) : nullptr);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -254,7 +258,117 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
   return 0;
 }
 
+// ------------------------------------------------------------------------------------------------
+// Real stage 1 (hx_real.cuh): the slab holds C as an S x S double matrix (ld S) at 2 * c_off, V1/V2/X/Z as
+// S x 32 doubles and T1/T2 as 32 x 32 doubles at twice their double2 offsets.
+static __global__ void __launch_bounds__(256) bd_band_extract_real_kernel(double* ws, size_t stride, size_t c_off,
+                                                                           size_t band_off, int S) {
+  double* base = ws + (size_t)blockIdx.x * stride;
+  const double* C = base + c_off;
+  double* B = base + band_off;
+  const size_t n = (size_t)S * RB_LD;
+  for (size_t p = threadIdx.x; p < n; p += blockDim.x) {
+    const int c = (int)(p / RB_LD), r = c + (int)(p % RB_LD) - RB_OFF;
+    B[p] = (r >= 0 && r < S) ? C[r + (size_t)c * S] : 0.0;
+  }
+}
+
+template <int CL, int GR, int RPT>
+static void launch_real_panel(double* ws, const RPanelArgs& a, int64_t cnt, cudaStream_t st) {
+  const int r = (a.m + CL - 1) / CL;
+  panel_qr_real_kernel<CL, GR, RPT><<<dim3((unsigned)CL, (unsigned)cnt), 32 * GR, 0, st>>>(ws, a, r);
+}
+
+// Smallest configuration whose CTA (or cluster of CTAs of up to 512 rows) holds the m panel rows: real
+// rows take half the registers of complex ones, so a CTA holds twice as many (half the cluster barriers).
+static bool launch_real_cluster_panel(double* ws, const RPanelArgs& a, int64_t cnt, cudaStream_t st) {
+  const int m = a.m;
+  if (m <= 32) launch_real_panel<1, 8, 4>(ws, a, cnt, st);
+  else if (m <= 64) launch_real_panel<1, 8, 8>(ws, a, cnt, st);
+  else if (m <= 128) launch_real_panel<1, 16, 8>(ws, a, cnt, st);
+  else if (m <= 256) launch_real_panel<1, 16, 16>(ws, a, cnt, st);
+  else if (m <= 512) launch_real_panel<1, 16, 32>(ws, a, cnt, st);
+  else if (m <= 1024) launch_real_panel<2, 16, 32>(ws, a, cnt, st);
+  else if (m <= 2048) launch_real_panel<4, 16, 32>(ws, a, cnt, st);
+  else if (m <= 4096) launch_real_panel<8, 16, 32>(ws, a, cnt, st);
+  else return false;
+  return true;
+}
+
+template <int RT>
+static void launch_rank_update_real(double* ws, const RSlab& G, int mr0, int mc0, int m, int n, size_t u_off,
+                                    size_t w_off, int64_t cnt, cudaStream_t st) {
+  rank_update_real_kernel<RT><<<dim3((unsigned)((m + RT - 1) / RT), (unsigned)((n + RRU_TN - 1) / RRU_TN), (unsigned)cnt),
+                                256, rru_smem<RT>(), st>>>(ws, G, mr0, mc0, m, n, u_off, w_off);
+}
+
+static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* dims, cudaStream_t st) {
+  const int S = L.S;
+  double* ws = reinterpret_cast<double*>(ws2);
+  const size_t sd = 2 * L.stride, c0 = 2 * L.c_off, v1 = 2 * L.v1_off, v2 = 2 * L.v2_off, x = 2 * L.x_off,
+               z = 2 * L.z_off, t1 = 2 * L.t1_off, t2 = 2 * L.t2_off;
+  const RSlab G{sd, S, c0};
+  static const int ru_rt = [] {
+    const char* e = getenv("HX_RRU_RT");
+    return e && atoi(e) == 128 ? 128 : 64;
+  }();
+  auto rank_update = [&](int mr0, int mc0, int m, int n, size_t u, size_t w) {
+    if (ru_rt == 128) launch_rank_update_real<128>(ws, G, mr0, mc0, m, n, u, w, cnt, st);
+    else launch_rank_update_real<64>(ws, G, mr0, mc0, m, n, u, w, cnt, st);
+  };
+  for (int k0 = 0; k0 < S; k0 += BB) {
+    const int m1 = S - k0, n2 = S - k0 - BB;
+    // ---- left: column panel QR, C_tr = C[k0:, k0+BB:] <- Q1^T C_tr
+    const RPanelArgs p1{sd, c0, S, k0, k0, m1, 0, v1, S, t1};
+    if (!launch_real_cluster_panel(ws, p1, cnt, st)) {
+      g_bd_err = "panel does not fit the cluster shared memory";
+      return -1;
+    }
+    count_launch();
+    if (n2 <= 0) break;
+    xv_real_kernel<1><<<dim3((unsigned)((n2 + RXV_TM - 1) / RXV_TM), (unsigned)cnt), 128, RXV_SMEM, st>>>(
+        ws, G, k0, k0 + BB, n2, m1, v1, x, t1);
+    rank_update(k0, k0 + BB, m1, n2, v1, x);
+    count_launch(2);
+    // ---- right: row panel LQ of rows k0..k0+BB, C_tr2 = C[k0+BB:, k0+BB:] <- C_tr2 Q2
+    const RPanelArgs p2{sd, c0, S, k0, k0 + BB, n2, 1, v2, S, t2};
+    if (!launch_real_cluster_panel(ws, p2, cnt, st)) {
+      g_bd_err = "panel does not fit the cluster shared memory";
+      return -1;
+    }
+    count_launch();
+    const int m3 = S - k0 - BB;
+    if (m3 > 0) {
+      xv_real_kernel<0><<<dim3((unsigned)((m3 + RXV_TM - 1) / RXV_TM), (unsigned)cnt), 128, RXV_SMEM, st>>>(
+          ws, G, k0 + BB, k0 + BB, m3, n2, v2, z, t2);
+      rank_update(k0 + BB, k0 + BB, m3, n2, z, v2);
+      count_launch(2);
+    }
+    BD_CUDA(cudaGetLastError());
+  }
+  bd_band_extract_real_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, sd, c0, 2 * L.band_off, S);
+  count_launch();
+  const int64_t want = (148 * 11 + cnt - 1) / cnt;
+  const size_t a1 = L.stride, a3 = L.tgk_off;
+#define BD_CHASE_REAL(NW)                                                                                       \
+  bd_chase_real_kernel<NW, BB><<<(unsigned)cnt, NW * 32, bd_chase_real_smem<NW, BB>(), st>>>(ws2, a1, L.band_off, \
+                                                                                               a3, S, dims)
+  if (want >= 6) BD_CHASE_REAL(16);
+  else if (want >= 2) BD_CHASE_REAL(2);
+  else BD_CHASE_REAL(1);
+#undef BD_CHASE_REAL
+  count_launch();
+  BD_CUDA(cudaGetLastError());
+  return 0;
+}
+
 void bd_init_attributes() {
+  set_smem_attr(xv_real_kernel<0>, (int)RXV_SMEM);
+  set_smem_attr(xv_real_kernel<1>, (int)RXV_SMEM);
+  set_smem_attr(rank_update_real_kernel<64>, (int)rru_smem<64>());
+  set_smem_attr(rank_update_real_kernel<128>, (int)rru_smem<128>());
+  const char* rs = getenv("HX_REAL_STAGE1");
+  if (rs && rs[0]) g_bd_real_stage1 = atoi(rs) != 0;
   set_smem_attr(xv_kernel<0>, (int)XV_SMEM);
   set_smem_attr(xv_kernel<1>, (int)XV_SMEM);
   set_smem_attr(xv_kernel<0, true>, XV_SMEM_UPD);
@@ -299,6 +413,7 @@ int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, 
   const BdWs L = BdWs::make(S);
   const size_t per = L.stride * sizeof(double2) + sizeof(int);
   const int64_t nmat = nmasks * nk;
+  const bool real_s1 = real && g_bd_real_stage1 && g_bd_chase_real && S % 4 == 0;
   int64_t chunk = std::max<int64_t>(1, (int64_t)(ws_budget / per));
   chunk = std::min<int64_t>(std::min<int64_t>(chunk, nmat), 65535);
   unsigned char* buf = static_cast<unsigned char*>(alloc(per * (size_t)chunk + 256));
@@ -314,10 +429,13 @@ int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, 
   ce.N = 2 * S;
   for (int64_t m0 = 0; m0 < nmat; m0 += chunk) {
     const int64_t cnt = std::min(chunk, nmat - m0);
-    bd_assemble_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, masks, m0, ws, L, dims, status, real ? 1 : 0);
+    bd_assemble_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, masks, m0, ws, L, dims, status,
+                                                         real ? (real_s1 ? 2 : 1) : 0);
     count_launch();
     BD_CUDA(cudaGetLastError());
-    if (real ? bd_reduce<true>(ws, L, cnt, dims, st) : bd_reduce<false>(ws, L, cnt, dims, st)) return -1;
+    const int rc = real_s1 ? bd_reduce_real(ws, L, cnt, dims, st)
+                           : (real ? bd_reduce<true>(ws, L, cnt, dims, st) : bd_reduce<false>(ws, L, cnt, dims, st));
+    if (rc) return -1;
     launch_eig_idos(ce, nk, g, m0, cnt, reinterpret_cast<const double*>(ws + L.tgk_off), L.stride * 2, dims, diff,
                     trans, eigs, status, sharp, st, refine, refine_count, true);
     BD_CUDA(cudaGetLastError());

@@ -66,8 +66,12 @@ static __device__ int2 block_compact_bipartite(const CellDev& c, const uint64_t*
 // k-points make it real, see bd_assemble_kernel).
 static __device__ void assemble_bipartite(const CellDev& c, const int* idx_a, const int* idx_b, double2 k,
                                           double2* M, int lm, int rows, int cols, bool transpose,
-                                          bool periodic = false) {
-  for (int p = threadIdx.x; p < lm * cols; p += blockDim.x) M[p] = make_double2(0.0, 0.0);
+                                          bool periodic = false, double* Mr = nullptr) {
+  // Mr (periodic only): write the real matrix as doubles instead (real stage 1, hx_real.cuh)
+  if (Mr)
+    for (int p = threadIdx.x; p < lm * cols; p += blockDim.x) Mr[p] = 0.0;
+  else
+    for (int p = threadIdx.x; p < lm * cols; p += blockDim.x) M[p] = make_double2(0.0, 0.0);
   __syncthreads();
   for (int r = threadIdx.x; r < c.N; r += blockDim.x) {
     const int ia = idx_a[r];
@@ -82,6 +86,10 @@ static __device__ void assemble_bipartite(const CellDev& c, const int* idx_a, co
         double sn, cs;
         sincos(k.x * (pa.x - pb.x) + k.y * (pa.y - pb.y), &sn, &cs);
         h = make_double2(h.x * cs - h.y * sn, 0.0);
+        if (Mr) {
+          Mr[ia + (size_t)jb * lm] = h.x;
+          return;
+        }
       }
       if (!transpose) M[ia + (size_t)jb * lm] = h;
       else M[jb + (size_t)ia * lm] = make_double2(h.x, -h.y);

@@ -171,11 +171,13 @@ def test_all_vacant_gives_zero_curve_and_plateau():
 
 
 @pytest.mark.parametrize("nu,q,p", [(10, 2, 0.2), (11, 1, 0.3), (12, 1, 0.05), (16, 2, 0.1), (12, 1, 0.5),
-                                    (13, 1, 0.4), (14, 1, 0.45), (17, 1, 0.35)])
+                                    (13, 1, 0.4), (14, 1, 0.45), (17, 1, 0.35), (20, 2, 0.05), (24, 1, 0.1)])
 def test_bipartite_banded_tier_matches_oracle(nu, q, p):
     """graphene N = 2nu^2 > 160 goes through the bipartite banded tier (nA != nB after vacancies).  High
     vacancy rates leave exactly-zero rows/columns whose reflections produce ever smaller noise columns
-    (down to the denormal range): the reflectors must stay unitary (HX_REFLECTOR_TINY)."""
+    (down to the denormal range): the reflectors must stay unitary (HX_REFLECTOR_TINY).  Even nu with
+    q <= 2 (S = nu^2 % 4 == 0, real batch) run the real-storage stage 1 (hx_real.cuh: one-CTA 512-row
+    panels at nu = 20, two-CTA clusters at nu = 24); odd nu the complex-storage one."""
     model = hx.GrapheneNNModel()
     spec = model.lattice_spec()
     sc = hx.build_supercell(spec, nu)
