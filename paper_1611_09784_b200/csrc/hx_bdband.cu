@@ -350,11 +350,32 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
   count_launch();
   const int64_t want = (148 * 11 + cnt - 1) / cnt;
   const size_t a1 = L.stride, a3 = L.tgk_off;
-#define BD_CHASE_REAL(NW)                                                                                       \
-  bd_chase_real_kernel<NW, BB><<<(unsigned)cnt, NW * 32, bd_chase_real_smem<NW, BB>(), st>>>(ws2, a1, L.band_off, \
-                                                                                               a3, S, dims)
-  if (want >= 6) BD_CHASE_REAL(16);
-  else if (want >= 2) BD_CHASE_REAL(2);
+  // Many-matrix launches (2 <= want < 6, e.g. the 1024 N = 512 matrices of a c2 level): 4 sweeps per matrix
+  // and at most 5 CTAs per SM (padded dynamic shared memory), which bounds the bands in flight (~740 x
+  // 196 KB) - measured 3-4 % faster per pass than 2 sweeps at full occupancy (the launch is L2-capacity
+  // bound: 17.7 GB DRAM traffic for 200 MB of bands).  HX_CHASE_RNW / HX_CHASE_CAP override (0 = off).
+  static const int rnw = [] {
+    const char* e = getenv("HX_CHASE_RNW");
+    return e ? atoi(e) : -1;
+  }();
+  static const int cap = [&] {
+    const char* e = getenv("HX_CHASE_CAP");
+    return e ? atoi(e) : 5;
+  }();
+  auto smem_of = [&](size_t need) {
+    return cap > 0 && want < 6 && want >= 2 ? std::max(need, (size_t)(220 * 1024) / cap) : need;
+  };
+#define BD_CHASE_REAL(NW)                                                                                 \
+  bd_chase_real_kernel<NW, BB><<<(unsigned)cnt, NW * 32, smem_of(bd_chase_real_smem<NW, BB>()), st>>>( \
+      ws2, a1, L.band_off, a3, S, dims)
+  if (want >= 6 && rnw > 0) BD_CHASE_REAL(16);
+  else if (rnw == 1) BD_CHASE_REAL(1);
+  else if (rnw == 2) BD_CHASE_REAL(2);
+  else if (rnw == 4) BD_CHASE_REAL(4);
+  else if (rnw == 8) BD_CHASE_REAL(8);
+  else if (rnw == 16) BD_CHASE_REAL(16);
+  else if (want >= 6) BD_CHASE_REAL(16);
+  else if (want >= 2) BD_CHASE_REAL(4);
   else BD_CHASE_REAL(1);
 #undef BD_CHASE_REAL
   count_launch();
@@ -391,9 +412,11 @@ void bd_init_attributes() {
   set_smem_attr(bd_chase_pair_kernel<1, BB>, bd_chase_pair_smem<1, BB>());
   set_smem_attr(bd_chase_pair_kernel<2, BB>, bd_chase_pair_smem<2, BB>());
   set_smem_attr(bd_chase_pair_kernel<10, BB>, bd_chase_pair_smem<10, BB>());
-  set_smem_attr(bd_chase_real_kernel<1, BB>, bd_chase_real_smem<1, BB>());
-  set_smem_attr(bd_chase_real_kernel<2, BB>, bd_chase_real_smem<2, BB>());
-  set_smem_attr(bd_chase_real_kernel<16, BB>, bd_chase_real_smem<16, BB>());
+  set_smem_attr(bd_chase_real_kernel<1, BB>, 220 * 1024);
+  set_smem_attr(bd_chase_real_kernel<2, BB>, 220 * 1024);
+  set_smem_attr(bd_chase_real_kernel<16, BB>, 220 * 1024);
+  set_smem_attr(bd_chase_real_kernel<4, BB>, 220 * 1024);
+  set_smem_attr(bd_chase_real_kernel<8, BB>, 220 * 1024);
   const char* sp = getenv("HX_CHASE_SPIN_NS");
   if (sp && sp[0]) {
     const unsigned v = (unsigned)atoi(sp);

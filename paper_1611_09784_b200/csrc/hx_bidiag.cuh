@@ -87,7 +87,8 @@ static __device__ void assemble_bipartite(const CellDev& c, const int* idx_a, co
         sincos(k.x * (pa.x - pb.x) + k.y * (pa.y - pb.y), &sn, &cs);
         h = make_double2(h.x * cs - h.y * sn, 0.0);
         if (Mr) {
-          Mr[ia + (size_t)jb * lm] = h.x;
+          if (!transpose) Mr[ia + (size_t)jb * lm] = h.x;
+          else Mr[jb + (size_t)ia * lm] = h.x;
           return;
         }
       }
@@ -343,6 +344,184 @@ static __device__ void bidiag_tgk_warp(double2* M, int lm, int rows, int cols, d
             x0.y = fma(-w0.y, b.x, fma(w0.x, b.y, x0.y));
             x1.x = fma(-w1.x, b.x, fma(-w1.y, b.y, x1.x));
             x1.y = fma(-w1.y, b.x, fma(w1.x, b.y, x1.y));
+            M[r0 + (size_t)cc * lm] = x0;
+            if (has1) M[r1 + (size_t)cc * lm] = x1;
+          }
+        }
+      __syncwarp();
+    }
+  }
+  __syncwarp();
+}
+
+// ------------------------------------------------------------------------------------------------
+// Real variants (periodic gauge at a time-reversal-invariant k: C is exactly real, hx_capi k_is_real):
+// the same schedules on doubles - a quarter of the FMAs and half the shared-memory traffic.
+// Leading dimensions: CTA variant 8 (mod 16) doubles (the half-warp's two columns x 8 rows hit distinct
+// banks), warp variant odd (lanes walking 16 columns at one row hit distinct banks).
+__host__ __device__ constexpr int bidiag_ld_real(int S) { return (S + 8) / 16 * 16 + 8; }
+__host__ __device__ constexpr int bidiag_ld_real_warp(int S) { return S | 1; }
+
+static __device__ void bidiag_tgk_real(double* M, int lm, int rows, int cols, double* diag, double* e2, double* u,
+                                       double* red) {
+  const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = bd >> 5;
+  const int d = rows + cols;
+  for (int i = tid; i < d; i += bd) {
+    diag[i] = 0.0;
+    e2[i] = 0.0;
+  }
+  const int g = lane & 7, q = lane >> 3;
+  double* lred = red;
+  double* rred = red + 32;
+  {
+    double part = 0.0;
+    for (int i = tid; i < rows; i += bd) part = fma(M[i], M[i], part);
+    part = warp_sum(part);
+    if (lane == 0) lred[warp] = part;
+    __syncthreads();
+  }
+  for (int j = 0; j < cols; ++j) {
+    {
+      double sig2 = 0.0;
+      for (int w = 0; w < nw; ++w) sig2 += lred[w];
+      const double* colj = M + (size_t)j * lm;
+      const QuickReflector h = quick_reflector(make_double2(colj[j], 0.0), sig2);
+      if (tid == 0) e2[2 * j] = sig2;
+      for (int i = j + tid; i < rows; i += bd) u[i] = i == j ? 1.0 : colj[i] * h.scale.x;
+      __syncthreads();
+      double rpart = 0.0;
+      for (int c0 = j + 1; c0 < cols; c0 += bd >> 3) {
+        const int cc = c0 + (tid >> 3);
+        double acc = 0.0;
+        if (cc < cols && h.tau != 0.0)
+          for (int i = j + g; i < rows; i += 8) acc = fma(u[i], M[i + (size_t)cc * lm], acc);
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        const double sc = h.tau * acc;
+        if (cc < cols) {
+          if (h.tau != 0.0)
+            for (int i = j + g; i < rows; i += 8) {
+              const double x = fma(-u[i], sc, M[i + (size_t)cc * lm]);
+              M[i + (size_t)cc * lm] = x;
+              if (i == j) rpart = fma(x, x, rpart);
+            }
+          else if (g == 0) {
+            const double x = M[j + (size_t)cc * lm];
+            rpart = fma(x, x, rpart);
+          }
+        }
+      }
+      rpart = warp_sum(rpart);
+      if (lane == 0) rred[warp] = rpart;
+      __syncthreads();
+    }
+    if (j + 1 >= cols) break;
+    {
+      double sig2 = 0.0;
+      for (int w = 0; w < nw; ++w) sig2 += rred[w];
+      const QuickReflector h = quick_reflector(make_double2(M[j + (size_t)(j + 1) * lm], 0.0), sig2);
+      if (tid == 0) e2[2 * j + 1] = sig2;
+      for (int cc = j + 1 + tid; cc < cols; cc += bd) u[cc] = cc == j + 1 ? 1.0 : M[j + (size_t)cc * lm] * h.scale.x;
+      __syncthreads();
+      double lpart = 0.0;
+      for (int r0 = j + 1; r0 < rows; r0 += 8 * nw) {
+        const int r = r0 + g + 8 * warp;
+        double acc = 0.0;
+        if (r < rows && h.tau != 0.0)
+          for (int cc = j + 1 + q; cc < cols; cc += 4) acc = fma(M[r + (size_t)cc * lm], u[cc], acc);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 8);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 16);
+        const double w = h.tau * acc;
+        if (r < rows) {
+          if (h.tau != 0.0)
+            for (int cc = j + 1 + q; cc < cols; cc += 4) {
+              const double x = fma(-w, u[cc], M[r + (size_t)cc * lm]);
+              M[r + (size_t)cc * lm] = x;
+              if (cc == j + 1) lpart = fma(x, x, lpart);
+            }
+          else if (q == 0) {
+            const double x = M[r + (size_t)(j + 1) * lm];
+            lpart = fma(x, x, lpart);
+          }
+        }
+      }
+      lpart = warp_sum(lpart);
+      if (lane == 0) lred[warp] = lpart;
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+}
+
+static __device__ void bidiag_tgk_warp_real(double* M, int lm, int rows, int cols, double* diag, double* e2,
+                                            double* u) {
+  const int lane = threadIdx.x & 31;
+  const int d = rows + cols;
+  for (int i = lane; i < d; i += 32) {
+    diag[i] = 0.0;
+    e2[i] = 0.0;
+  }
+  for (int j = 0; j < cols; ++j) {
+    {
+      const double* colj = M + (size_t)j * lm;
+      double part = 0.0;
+      for (int i = j + lane; i < rows; i += 32) part = fma(colj[i], colj[i], part);
+      const double sig2 = warp_sum(part);
+      const QuickReflector h = quick_reflector(make_double2(colj[j], 0.0), sig2);
+      if (lane == 0) e2[2 * j] = sig2;
+      for (int i = j + lane; i < rows; i += 32) u[i] = i == j ? 1.0 : colj[i] * h.scale.x;
+      __syncwarp();
+      if (h.tau != 0.0)
+        for (int c0 = j + 1 + lane; c0 < cols; c0 += 64) {
+          const bool has1 = c0 + 32 < cols;
+          double* col0 = M + (size_t)c0 * lm;
+          double* col1 = M + (size_t)(has1 ? c0 + 32 : c0) * lm;
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+          for (int i = j; i < rows; ++i) {
+            const double v = u[i];
+            a0 = fma(v, col0[i], a0);
+            a1 = fma(v, col1[i], a1);
+          }
+          const double s0 = h.tau * a0, s1 = has1 ? h.tau * a1 : 0.0;
+#pragma unroll 4
+          for (int i = j; i < rows; ++i) {
+            const double v = u[i];
+            const double x0 = fma(-v, s0, col0[i]), x1 = fma(-v, s1, col1[i]);
+            col0[i] = x0;
+            if (has1) col1[i] = x1;
+          }
+        }
+      __syncwarp();
+    }
+    if (j + 1 >= cols) break;
+    {
+      double part = 0.0;
+      for (int cc = j + 1 + lane; cc < cols; cc += 32) {
+        const double x = M[j + (size_t)cc * lm];
+        part = fma(x, x, part);
+      }
+      const double sig2 = warp_sum(part);
+      const QuickReflector h = quick_reflector(make_double2(M[j + (size_t)(j + 1) * lm], 0.0), sig2);
+      if (lane == 0) e2[2 * j + 1] = sig2;
+      for (int cc = j + 1 + lane; cc < cols; cc += 32) u[cc] = cc == j + 1 ? 1.0 : M[j + (size_t)cc * lm] * h.scale.x;
+      __syncwarp();
+      if (h.tau != 0.0)
+        for (int r0 = j + 1 + lane; r0 < rows; r0 += 64) {
+          const bool has1 = r0 + 32 < rows;
+          const int r1 = has1 ? r0 + 32 : r0;
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+          for (int cc = j + 1; cc < cols; ++cc) {
+            const double b = u[cc];
+            a0 = fma(M[r0 + (size_t)cc * lm], b, a0);
+            a1 = fma(M[r1 + (size_t)cc * lm], b, a1);
+          }
+          const double w0 = h.tau * a0, w1 = has1 ? h.tau * a1 : 0.0;
+#pragma unroll 4
+          for (int cc = j + 1; cc < cols; ++cc) {
+            const double b = u[cc];
+            const double x0 = fma(-w0, b, M[r0 + (size_t)cc * lm]), x1 = fma(-w1, b, M[r1 + (size_t)cc * lm]);
             M[r0 + (size_t)cc * lm] = x0;
             if (has1) M[r1 + (size_t)cc * lm] = x1;
           }

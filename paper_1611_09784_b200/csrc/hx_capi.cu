@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <string>
 #include <thread>
 #include <vector>
@@ -69,6 +70,8 @@ struct hx_ctx {
   int bd_min_n = HX_SMEM_MAX_N;          // bipartite cells with N above this take the banded SVD tier
   int bidiag_warp_max_s = 32;            // shared-memory bidiagonalisation: one warp per matrix up to this S
   int bidiag_threads = 256;              // ... and a CTA of this size above it
+  int bidiag_real_warp_max_s = 64;       // real (time-reversal-invariant) k-points: one warp per matrix up to this S
+  bool bidiag_real = true;               // real Golub-Kahan for those k-points (HX_BIDIAG_REAL=0 disables)
   bool use_bipartite = true;            // graphene: singular values of the A-B block (HX_NO_BIPARTITE=1 disables)
 };
 
@@ -91,6 +94,17 @@ bool batch_is_real(const hx_cell* cell, const double* kpoints, int nk) {
       const double ph = 2.0 * (kpoints[2 * k] * cell->lat[2 * e] + kpoints[2 * k + 1] * cell->lat[2 * e + 1]);
       if (std::fabs(std::sin(ph)) > 1e-9 || std::cos(ph) < 0.0) return false;
     }
+  return true;
+}
+
+// One k-point makes the periodic-gauge matrix real (per-k version of batch_is_real).
+bool k_is_real(const hx_cell* cell, const double* kpoints, int k) {
+  if (!cell->real_amps || !cell->dev.pos || cell->lat.empty()) return false;
+  const size_t nnz = cell->lat.size() / 2;
+  for (size_t e = 0; e < nnz; ++e) {
+    const double ph = 2.0 * (kpoints[2 * k] * cell->lat[2 * e] + kpoints[2 * k + 1] * cell->lat[2 * e + 1]);
+    if (std::fabs(std::sin(ph)) > 1e-9 || std::cos(ph) < 0.0) return false;
+  }
   return true;
 }
 }  // namespace
@@ -207,6 +221,10 @@ int hx_ctx_create_priority(int32_t device, int32_t priority, hx_ctx** out) {
     if (zm && zm[0]) hx::g_zone_min_n = atoi(zm);
     const char* bt = getenv("HX_BIDIAG_THREADS");
     if (bt && bt[0]) ctx->bidiag_threads = atoi(bt);
+    const char* br = getenv("HX_BIDIAG_REAL");
+    if (br && br[0]) ctx->bidiag_real = atoi(br) != 0;
+    const char* brw = getenv("HX_BIDIAG_REAL_WARP_MAX_S");
+    if (brw && brw[0]) ctx->bidiag_real_warp_max_s = atoi(brw);
   }
   hx::set_smem_attr(hx::small_bidiag_kernel, 200 * 1024);
   ctx->ws_budget = std::min(ctx->ws_budget, freeb / 3);
@@ -374,8 +392,21 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
   g.kmult = nullptr;
   if (g.shift < 16) return fail(HX_E_RANGE, "nk * N too large for the fixed-point IDOS accumulator");
   // k-points (small, pageable copy on the work stream)
-  if (ctx->kpts.grow((size_t)nk * 16)) return fail(HX_E_CUDA, "alloc kpts");
-  HX_CUDA(cudaMemcpyAsync(ctx->kpts.p, kpoints, (size_t)nk * 16, cudaMemcpyHostToDevice, st));
+  // followed by the k-point lists of the shared-memory bipartite tier: complex k-points, then those whose
+  // periodic-gauge block is real (time-reversal-invariant: real Golub-Kahan, one warp per matrix)
+  std::vector<int> klist_c, klist_r;
+  if (c.bipartite && ctx->use_bipartite && g_real_batches && ctx->bidiag_real)
+    for (int k = 0; k < nk; ++k) (k_is_real(cell, kpoints, k) ? klist_r : klist_c).push_back(k);
+  std::vector<unsigned char> kbuf((size_t)nk * 20);  // one pageable copy carries both
+  std::memcpy(kbuf.data(), kpoints, (size_t)nk * 16);
+  if (!klist_r.empty()) {
+    std::memcpy(kbuf.data() + (size_t)nk * 16, klist_c.data(), klist_c.size() * 4);
+    std::memcpy(kbuf.data() + (size_t)nk * 16 + klist_c.size() * 4, klist_r.data(), klist_r.size() * 4);
+  }
+  if (ctx->kpts.grow((size_t)nk * 20)) return fail(HX_E_CUDA, "alloc kpts");
+  HX_CUDA(cudaMemcpyAsync(ctx->kpts.p, kbuf.data(), (size_t)nk * 20, cudaMemcpyHostToDevice, st));
+  const int* d_klist_c = reinterpret_cast<const int*>(static_cast<const unsigned char*>(ctx->kpts.p) + (size_t)nk * 16);
+  const int* d_klist_r = d_klist_c + klist_c.size();
   if (kmult) {
     if (ctx->kmult.grow((size_t)nk * 4)) return fail(HX_E_CUDA, "alloc kmult");
     HX_CUDA(cudaMemcpyAsync(ctx->kmult.p, kmult, (size_t)nk * 4, cudaMemcpyHostToDevice, st));
@@ -421,9 +452,24 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
       if (tgk) {
         // one warp per matrix up to S = 32 (latency of the serial reflector chain is hidden by many
         // matrices per SM), a CTA beyond
-        hx::small_bidiag_kernel<<<(unsigned)cnt, c.nsub <= ctx->bidiag_warp_max_s ? 32 : ctx->bidiag_threads,
-                                  hx::small_bidiag_smem(N, c.nsub), st>>>(
-            c, kp, nk, mk0, tri, dims, status + m0);
+        const int nkc = (int)klist_c.size(), nkr = (int)klist_r.size();
+        const int64_t nm = cnt / nk;  // whole masks in this chunk
+        if (nkr == 0) {
+          hx::small_bidiag_kernel<<<(unsigned)cnt, c.nsub <= ctx->bidiag_warp_max_s ? 32 : ctx->bidiag_threads,
+                                    hx::small_bidiag_smem(N, c.nsub), st>>>(c, kp, nk, mk0, tri, dims, status + m0,
+                                                                            nullptr, nk, 0);
+        } else {
+          if (nkc > 0)
+            hx::small_bidiag_kernel<<<(unsigned)(nm * nkc), c.nsub <= ctx->bidiag_warp_max_s ? 32 : ctx->bidiag_threads,
+                                      hx::small_bidiag_smem(N, c.nsub), st>>>(c, kp, nk, mk0, tri, dims, status + m0,
+                                                                              d_klist_c, nkc, 0);
+          // real k-points: one warp per matrix up to S = 64 (two columns / rows per lane)
+          const bool rw = c.nsub <= ctx->bidiag_real_warp_max_s;
+          hx::small_bidiag_kernel<<<(unsigned)(nm * nkr), rw ? 32 : ctx->bidiag_threads,
+                                    hx::small_bidiag_smem_real(N, c.nsub, rw), st>>>(c, kp, nk, mk0, tri, dims,
+                                                                                     status + m0, d_klist_r, nkr, 1);
+          hx::count_launch();
+        }
       } else {
         hx::small_tridiag_kernel<<<(unsigned)cnt, N > 64 ? 512 : 256, smem, st>>>(c, kp, nk, mk0, tri, dims,
                                                                                  status + m0);

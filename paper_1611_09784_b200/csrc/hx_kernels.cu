@@ -53,22 +53,36 @@ __global__ void __launch_bounds__(512) small_tridiag_kernel(CellDev c, const dou
 }
 
 // Bipartite (graphene) variant: bidiagonalise the nA x nB block C instead of tridiagonalising T.
+// klist (optional): this launch covers the k-points klist[0..nks) of every mask (block = mask * nks + i),
+// written at the batch's matrix index mask * nk + klist[i].  real: those k-points make the periodic-gauge
+// block exactly real (hx_capi k_is_real) - real Golub-Kahan on doubles (bidiag_tgk(_warp)_real).
 __global__ void __launch_bounds__(256) small_bidiag_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
                                                            const uint64_t* __restrict__ masks, double* tri, int* dims,
-                                                           int* status) {
+                                                           int* status, const int* __restrict__ klist, int nks,
+                                                           int real) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int N = c.N, S = c.nsub;
-  const int lm = bidiag_ld(S);
-  const int64_t mat = blockIdx.x;
-  const int64_t mk = mat / nk;
-  const int kk = (int)(mat - mk * nk);
+  int64_t mk, mat;
+  int kk;
+  if (klist) {
+    mk = blockIdx.x / nks;
+    kk = klist[blockIdx.x - mk * nks];
+    mat = mk * nk + kk;
+  } else {
+    mat = blockIdx.x;
+    mk = mat / nk;
+    kk = (int)(mat - mk * nk);
+  }
+  const int lm = real ? (blockDim.x == 32 ? bidiag_ld_real_warp(S) : bidiag_ld_real(S)) : bidiag_ld(S);
   double2* M = reinterpret_cast<double2*>(smem_raw);
+  double* Mr = reinterpret_cast<double*>(smem_raw);
   double2* u = M + (size_t)lm * S;
   double2* s = u + S + 1;
-  double* red = reinterpret_cast<double*>(s + S + 1);  // 128
-  int* idx_a = reinterpret_cast<int*>(red + 128);      // N
-  int* idx_b = idx_a + N;                              // N
-  int* cnt = idx_b + N;                                // 2 ceil(N/32)
+  double* ur = Mr + (size_t)lm * S;
+  double* red = real ? ur + S + 1 : reinterpret_cast<double*>(s + S + 1);  // 128
+  int* idx_a = reinterpret_cast<int*>(red + 128);                           // N
+  int* idx_b = idx_a + N;                                                   // N
+  int* cnt = idx_b + N;                                                     // 2 ceil(N/32)
   double* diag = tri + mat * 2 * N;
   double* e2 = diag + N;
   const int2 nn = block_compact_bipartite(c, masks + mk * c.words, idx_a, idx_b, cnt);
@@ -80,6 +94,12 @@ __global__ void __launch_bounds__(256) small_bidiag_kernel(CellDev c, const doub
   if (d == 0) return;
   const bool transpose = nn.x < nn.y;
   const int rows = transpose ? nn.y : nn.x, cols = transpose ? nn.x : nn.y;
+  if (real) {
+    assemble_bipartite(c, idx_a, idx_b, kpts[kk], M, lm, rows, cols, transpose, true, Mr);
+    if (blockDim.x == 32) bidiag_tgk_warp_real(Mr, lm, rows, cols, diag, e2, ur);
+    else bidiag_tgk_real(Mr, lm, rows, cols, diag, e2, ur, red);
+    return;
+  }
   assemble_bipartite(c, idx_a, idx_b, kpts[kk], M, lm, rows, cols, transpose);
   if (blockDim.x == 32) bidiag_tgk_warp(M, lm, rows, cols, diag, e2, u);
   else bidiag_tgk(M, lm, rows, cols, diag, e2, u, s, red);
@@ -87,6 +107,11 @@ __global__ void __launch_bounds__(256) small_bidiag_kernel(CellDev c, const doub
 
 size_t small_bidiag_smem(int N, int S) {
   return ((size_t)bidiag_ld(S) * S + 2 * (S + 1)) * 16 + 128 * 8 + (size_t)N * 8 + 2 * ((N + 31) / 32) * 4 + 16;
+}
+
+size_t small_bidiag_smem_real(int N, int S, bool warp) {
+  const int lm = warp ? bidiag_ld_real_warp(S) : bidiag_ld_real(S);
+  return ((size_t)lm * S + (S + 1)) * 8 + 128 * 8 + (size_t)N * 8 + 2 * ((N + 31) / 32) * 4 + 16;
 }
 
 size_t small_tridiag_smem(int N) {

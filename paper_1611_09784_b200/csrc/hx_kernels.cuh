@@ -25,9 +25,12 @@ struct RefineItem {
 __global__ void small_tridiag_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, double* tri,
                                      int* dims, int* status);
 size_t small_tridiag_smem(int N);
+// klist / nks (optional): the launch covers k-points klist[0..nks) of every mask; real: those k-points make the
+// periodic-gauge block real (real Golub-Kahan)
 __global__ void small_bidiag_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, double* tri,
-                                    int* dims, int* status);
+                                    int* dims, int* status, const int* klist, int nks, int real);
 size_t small_bidiag_smem(int N, int S);
+size_t small_bidiag_smem_real(int N, int S, bool warp);
 
 __global__ void global_tridiag_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, int64_t mat0,
                                       unsigned char* ws, size_t ws_stride, double* tri, int* dims, int* status);
