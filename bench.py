@@ -48,10 +48,11 @@ CONFIGS = {
 }
 FRAC_NOTE = ("achieved/frac use the algorithmic count of SURVEY 8d (16/3 d^3 complex-Hermitian tridiagonalisation flops "
              "per (sample, k) matrix solved); the graphene tiers solve the bipartite SVD (1/4 of it) and the "
-             "time-reversal-invariant batches (q = 1, 2: the N = 512 / 2048 tiers) run in real arithmetic (1/4 again), "
-             "so frac exceeds 1. Executed FP64 per c2 pass (ncu DFMA/DMUL/DADD + DMMA counters): 642 GFLOP, 5.7 TF/s "
-             "over the serialised kernel time, profiles/r01_fp64_executed_c2.txt; the dominant tier's rank-32 "
-             "updates are DRAM-bound (3.5 TB/s), traffic below and profiles/r01_traffic_L4_parent.txt")
+             "time-reversal-invariant batches (q = 1, 2: the N = 512 / 2048 tiers, and the TRIM k-points of the others) "
+             "run in real arithmetic with real storage (1/4 again), so frac exceeds 1. Executed FP64 per c2 pass (ncu "
+             "DFMA/DMUL/DADD + DMMA counters): 527 GFLOP, 6.2 TF/s over the serialised kernel time, "
+             "profiles/r01_fp64_executed_c2.txt; the dominant tier's rank-32 updates are DRAM-bound (3.7 TB/s), "
+             "traffic below and profiles/r01_traffic_L4_parent.txt")
 # c5 batches: floor(0.5 * 180 GB / (16 n^2)) matrices, one (mask, k) matrix each
 C5_BATCH = {4: 5_490_000, 8: 343_000, 16: 21_500, 32: 1_341}
 SEED = 2026
