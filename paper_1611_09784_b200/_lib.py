@@ -168,14 +168,16 @@ class Device:
         return h
 
     @classmethod
-    def lane(cls, device: int, i: int, high: bool | None = None):
+    def lane(cls, device: int, i: int, high=None):
         """Context i of the per-device pool used to evaluate independent groups concurrently.  Default:
-        lane 0 on a high-priority stream, the others normal; `high` picks the pool explicitly."""
+        lane 0 on a high-priority stream, the others normal; `high` picks the pool explicitly: True / False
+        (greatest / default priority) or an int stream priority (clamped to the device's range)."""
         if high is None:
             high = i == 0
-        pool = cls._pools.setdefault((device, bool(high)), [])
+        prio = high if isinstance(high, int) and not isinstance(high, bool) else (-100 if high else 0)
+        pool = cls._pools.setdefault((device, prio), [])
         while len(pool) <= i:
-            pool.append(cls.new_ctx(device, -100 if high else 0))  # -100: clamped to the greatest priority
+            pool.append(cls.new_ctx(device, prio))  # -100: clamped to the greatest priority
         return pool[i]
 
     @classmethod

@@ -60,12 +60,41 @@ struct DevBuf {
   }
 };
 
+// Pinned host staging buffer: host-API copies go through it so that they are true asynchronous DMA on the
+// context's stream (pageable copies are staged by the driver and were measured to hold a small tier's
+// results back until the concurrent large tier finished).  `ev` marks the last copy that reads it.
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaEvent_t ev = nullptr;
+  int grow(size_t bytes) {
+    if (!ev && cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return -1;
+    cudaEventSynchronize(ev);  // the previous copy from / to this buffer has completed
+    if (bytes <= cap) return 0;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max(bytes, (size_t)4096);
+    if (cudaHostAlloc(&p, want, cudaHostAllocPortable) != cudaSuccess) return -1;
+    cap = want;
+    return 0;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    if (ev) cudaEventDestroy(ev);
+    p = nullptr;
+    ev = nullptr;
+    cap = 0;
+  }
+};
+
 }  // namespace
 
 struct hx_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   DevBuf kpts, kmult, diff, trans, ws, masks, curves, eigs, status, band, tri, refine;
+  HostBuf h_kpts, h_io;  // pinned staging: k-points (+ lists, multiplicities); masks in / curves + status out
   size_t ws_budget = (size_t)24 << 30;  // HBM workspace budget for the global / banded paths
   int bd_min_n = HX_SMEM_MAX_N;          // bipartite cells with N above this take the banded SVD tier
   int bidiag_warp_max_s = 32;            // shared-memory bidiagonalisation: one warp per matrix up to this S
@@ -246,6 +275,9 @@ int hx_ctx_destroy(hx_ctx* ctx) {
   for (DevBuf* b : {&ctx->kpts, &ctx->kmult, &ctx->diff, &ctx->trans, &ctx->ws, &ctx->masks, &ctx->curves, &ctx->eigs,
                     &ctx->status, &ctx->band, &ctx->tri, &ctx->refine})
     b->release();
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ctx->h_kpts.release();
+  ctx->h_io.release();
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return 0;
@@ -397,21 +429,22 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
   std::vector<int> klist_c, klist_r;
   if (c.bipartite && ctx->use_bipartite && g_real_batches && ctx->bidiag_real)
     for (int k = 0; k < nk; ++k) (k_is_real(cell, kpoints, k) ? klist_r : klist_c).push_back(k);
-  std::vector<unsigned char> kbuf((size_t)nk * 20);  // one pageable copy carries both
-  std::memcpy(kbuf.data(), kpoints, (size_t)nk * 16);
+  // one pinned staging copy carries k-points, k lists and multiplicities
+  const size_t kbytes = (size_t)nk * 24;
+  if (ctx->h_kpts.grow(kbytes)) return fail(HX_E_CUDA, "alloc pinned kpts");
+  unsigned char* kbuf = static_cast<unsigned char*>(ctx->h_kpts.p);
+  std::memcpy(kbuf, kpoints, (size_t)nk * 16);
   if (!klist_r.empty()) {
-    std::memcpy(kbuf.data() + (size_t)nk * 16, klist_c.data(), klist_c.size() * 4);
-    std::memcpy(kbuf.data() + (size_t)nk * 16 + klist_c.size() * 4, klist_r.data(), klist_r.size() * 4);
+    std::memcpy(kbuf + (size_t)nk * 16, klist_c.data(), klist_c.size() * 4);
+    std::memcpy(kbuf + (size_t)nk * 16 + klist_c.size() * 4, klist_r.data(), klist_r.size() * 4);
   }
-  if (ctx->kpts.grow((size_t)nk * 20)) return fail(HX_E_CUDA, "alloc kpts");
-  HX_CUDA(cudaMemcpyAsync(ctx->kpts.p, kbuf.data(), (size_t)nk * 20, cudaMemcpyHostToDevice, st));
+  if (kmult) std::memcpy(kbuf + (size_t)nk * 20, kmult, (size_t)nk * 4);
+  if (ctx->kpts.grow(kbytes)) return fail(HX_E_CUDA, "alloc kpts");
+  HX_CUDA(cudaMemcpyAsync(ctx->kpts.p, kbuf, kbytes, cudaMemcpyHostToDevice, st));
+  HX_CUDA(cudaEventRecord(ctx->h_kpts.ev, st));
   const int* d_klist_c = reinterpret_cast<const int*>(static_cast<const unsigned char*>(ctx->kpts.p) + (size_t)nk * 16);
   const int* d_klist_r = d_klist_c + klist_c.size();
-  if (kmult) {
-    if (ctx->kmult.grow((size_t)nk * 4)) return fail(HX_E_CUDA, "alloc kmult");
-    HX_CUDA(cudaMemcpyAsync(ctx->kmult.p, kmult, (size_t)nk * 4, cudaMemcpyHostToDevice, st));
-    g.kmult = static_cast<const int*>(ctx->kmult.p);
-  }
+  if (kmult) g.kmult = reinterpret_cast<const int*>(static_cast<const unsigned char*>(ctx->kpts.p) + (size_t)nk * 20);
   const size_t diff_b = (size_t)nmasks * (grid->npts + 1) * sizeof(int);
   const size_t trans_b = (size_t)nmasks * grid->npts * sizeof(unsigned long long);
   if (ctx->diff.grow(diff_b) || ctx->trans.grow(trans_b)) return fail(HX_E_CUDA, "alloc accumulators");
@@ -552,15 +585,27 @@ static int eval_host(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
   if (ctx->masks.grow(mb) || ctx->curves.grow(cb) || ctx->status.grow(sb) || (out_eigs && ctx->eigs.grow(eb)))
     return fail(HX_E_CUDA, "alloc batch buffers");
   cudaStream_t st = ctx->stream;
-  HX_CUDA(cudaMemcpyAsync(ctx->masks.p, masks, mb, cudaMemcpyHostToDevice, st));
+  // pinned staging (ctx->h_io): masks in, then curves | status | eigs out in the same buffer
+  const size_t out_b = cb + sb + (out_eigs ? eb : 0);
+  if (ctx->h_io.grow(std::max(mb, out_b))) return fail(HX_E_CUDA, "alloc pinned staging");
+  unsigned char* hio = static_cast<unsigned char*>(ctx->h_io.p);
+  std::memcpy(hio, masks, mb);
+  HX_CUDA(cudaMemcpyAsync(ctx->masks.p, hio, mb, cudaMemcpyHostToDevice, st));
   int rc = eval_impl(ctx, cell, kpoints, nk, static_cast<uint64_t*>(ctx->masks.p), nmasks, grid,
                      static_cast<double*>(ctx->curves.p), out_eigs ? static_cast<double*>(ctx->eigs.p) : nullptr,
                      static_cast<int32_t*>(ctx->status.p), st, sharp, kmult);
-  if (rc) return rc;
-  HX_CUDA(cudaMemcpyAsync(out_curves, ctx->curves.p, cb, cudaMemcpyDeviceToHost, st));
-  HX_CUDA(cudaMemcpyAsync(out_status, ctx->status.p, sb, cudaMemcpyDeviceToHost, st));
-  if (out_eigs) HX_CUDA(cudaMemcpyAsync(out_eigs, ctx->eigs.p, eb, cudaMemcpyDeviceToHost, st));
+  if (rc) {
+    cudaStreamSynchronize(st);
+    return rc;
+  }
+  HX_CUDA(cudaMemcpyAsync(hio, ctx->curves.p, cb, cudaMemcpyDeviceToHost, st));
+  HX_CUDA(cudaMemcpyAsync(hio + cb, ctx->status.p, sb, cudaMemcpyDeviceToHost, st));
+  if (out_eigs) HX_CUDA(cudaMemcpyAsync(hio + cb + sb, ctx->eigs.p, eb, cudaMemcpyDeviceToHost, st));
+  HX_CUDA(cudaEventRecord(ctx->h_io.ev, st));
   HX_CUDA(cudaStreamSynchronize(st));
+  std::memcpy(out_curves, hio, cb);
+  std::memcpy(out_status, hio + cb, sb);
+  if (out_eigs) std::memcpy(out_eigs, hio + cb + sb, eb);
   return 0;
 }
 

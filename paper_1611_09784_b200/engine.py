@@ -42,7 +42,13 @@ SLMC_STREAM_OFFSET = 10_000
 # cache in each worker (runner.py:98-111).  Rebuilding them per Engine costs a few ms of uploads, and
 # releasing them (cudaFree) synchronises the device.
 _CELL_CACHE: dict = {}
-_E2E_PRIO = os.environ.get("HX_E2E_PRIO", "big")  # experiment: "big+small" also raises the small tiers
+# Concurrent tier schedule of the seam: the largest tier is planned and submitted first (it is the critical
+# path), then the others smallest first; the small tiers (dim <= 128) run on the greatest stream priority so
+# that their levels finish early and the host work of placing them overlaps the device work still running,
+# the largest tier next, the rest at the default priority (e2e run_mlmc on c2: 87 -> 71 ms with pinned
+# staging).  Experiments: HX_E2E_PRIO=big|big+small, HX_E2E_ORDER=big-first.
+_E2E_PRIO = os.environ.get("HX_E2E_PRIO", "tiered")
+_E2E_ORDER = os.environ.get("HX_E2E_ORDER", "big-then-small")
 
 
 class TaskError(RuntimeError):
@@ -202,6 +208,9 @@ class Engine:
             self.cell(n)  # compile cells and k-sets up front (not thread-safe)
             self.kpoints_tr(n, q)
         order = sorted(tiers, key=lambda g: -self.cell(g[0]).dim)
+        if _E2E_ORDER == "big-then-small" and len(order) > 2:
+            # the largest tier first (critical path), then the rest smallest first
+            order = order[:1] + order[1:][::-1]
         hits = [0] * len(batches)
         spent = [0.0] * len(batches)
         plans = {}  # (bi, gi) -> (tier, uniq, inv, keys, src)
@@ -236,7 +245,13 @@ class Engine:
                     hits[bi] += R - len(new)
                     if len(new):
                         ids = batches[bi][1](gi, new, inv)
-                        high = lane == 0 or (_E2E_PRIO == "big+small" and self.cell(tier[0]).dim <= 128)
+                        small = self.cell(tier[0]).dim <= 128
+                        if _E2E_PRIO == "tiered":
+                            # small tiers first (their levels finish early and the host work of placing
+                            # them overlaps the device work left), then the largest tier, then the rest
+                            high = -100 if small else (-1 if lane == 0 else 0)
+                        else:
+                            high = lane == 0 or (_E2E_PRIO == "big+small" and small)
                         ctx = (_lib.Device.lane(self.device, lane, high)
                                if len(tiers) > 1 or len(tiers[tier]) > 1 else None)
                         lane += 1

@@ -112,18 +112,36 @@ def level_moments(full, quarters=None, device: int = 0):
     import torch
 
     dev = torch.device("cuda", device)
-    f = torch.as_tensor(full, dtype=torch.float64).to(dev).contiguous()
-    M, npts = f.shape
-    q = None if quarters is None else torch.as_tensor(quarters, dtype=torch.float64).to(dev).contiguous()
-    terms = torch.empty_like(f)
-    mean = torch.empty(npts, dtype=torch.float64, device=dev)
-    var = torch.empty(npts, dtype=torch.float64, device=dev)
-    _lib.Device.ctx(device)
-    _lib.check(_lib.load().hx_level_moments_device(f.data_ptr(), 0 if q is None else q.data_ptr(), M, npts,
-                                                   terms.data_ptr(), mean.data_ptr(), var.data_ptr(), 0,
-                                                   torch.cuda.current_stream(dev).cuda_stream),
-               "hx_level_moments_device")
+    # a high-priority stream: a level's moments are short and run while the later levels' solves still
+    # occupy the SMs - the priority puts their blocks ahead of the queued solve blocks
+    st = _moments_stream(device)
+    st.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(st):
+        f = torch.as_tensor(full, dtype=torch.float64).to(dev, non_blocking=False).contiguous()
+        M, npts = f.shape
+        q = None if quarters is None else torch.as_tensor(quarters, dtype=torch.float64).to(dev).contiguous()
+        terms = torch.empty_like(f)
+        mean = torch.empty(npts, dtype=torch.float64, device=dev)
+        var = torch.empty(npts, dtype=torch.float64, device=dev)
+        _lib.Device.ctx(device)
+        _lib.check(_lib.load().hx_level_moments_device(f.data_ptr(), 0 if q is None else q.data_ptr(), M, npts,
+                                                       terms.data_ptr(), mean.data_ptr(), var.data_ptr(), 0,
+                                                       st.cuda_stream),
+                   "hx_level_moments_device")
+    torch.cuda.current_stream(dev).wait_stream(st)
     return terms, mean, var
+
+
+_MOMENT_STREAMS: dict = {}
+
+
+def _moments_stream(device: int):
+    import torch
+
+    st = _MOMENT_STREAMS.get(device)
+    if st is None:
+        st = _MOMENT_STREAMS[device] = torch.cuda.Stream(device=device, priority=-1)
+    return st
 
 
 def moments_from_sums(s1, s2, M: int):
