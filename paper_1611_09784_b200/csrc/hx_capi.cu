@@ -585,18 +585,34 @@ static int eval_host(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
   if (ctx->masks.grow(mb) || ctx->curves.grow(cb) || ctx->status.grow(sb) || (out_eigs && ctx->eigs.grow(eb)))
     return fail(HX_E_CUDA, "alloc batch buffers");
   cudaStream_t st = ctx->stream;
-  // pinned staging (ctx->h_io): masks in, then curves | status | eigs out in the same buffer
+  // pinned staging (ctx->h_io) for batches up to 256 MB of traffic: masks in, then curves | status | eigs
+  // out in the same buffer (true async DMA: concurrent small tiers are not held back by pageable staging);
+  // larger batches are bandwidth-bound and copy straight between pageable memory and the device (staging
+  // them would add a host memcpy of the whole result)
   const size_t out_b = cb + sb + (out_eigs ? eb : 0);
-  if (ctx->h_io.grow(std::max(mb, out_b))) return fail(HX_E_CUDA, "alloc pinned staging");
-  unsigned char* hio = static_cast<unsigned char*>(ctx->h_io.p);
-  std::memcpy(hio, masks, mb);
-  HX_CUDA(cudaMemcpyAsync(ctx->masks.p, hio, mb, cudaMemcpyHostToDevice, st));
+  const bool staged = std::max(mb, out_b) <= ((size_t)256 << 20);
+  unsigned char* hio = nullptr;
+  if (staged) {
+    if (ctx->h_io.grow(std::max(mb, out_b))) return fail(HX_E_CUDA, "alloc pinned staging");
+    hio = static_cast<unsigned char*>(ctx->h_io.p);
+    std::memcpy(hio, masks, mb);
+    HX_CUDA(cudaMemcpyAsync(ctx->masks.p, hio, mb, cudaMemcpyHostToDevice, st));
+  } else {
+    HX_CUDA(cudaMemcpyAsync(ctx->masks.p, masks, mb, cudaMemcpyHostToDevice, st));
+  }
   int rc = eval_impl(ctx, cell, kpoints, nk, static_cast<uint64_t*>(ctx->masks.p), nmasks, grid,
                      static_cast<double*>(ctx->curves.p), out_eigs ? static_cast<double*>(ctx->eigs.p) : nullptr,
                      static_cast<int32_t*>(ctx->status.p), st, sharp, kmult);
   if (rc) {
     cudaStreamSynchronize(st);
     return rc;
+  }
+  if (!staged) {
+    HX_CUDA(cudaMemcpyAsync(out_curves, ctx->curves.p, cb, cudaMemcpyDeviceToHost, st));
+    HX_CUDA(cudaMemcpyAsync(out_status, ctx->status.p, sb, cudaMemcpyDeviceToHost, st));
+    if (out_eigs) HX_CUDA(cudaMemcpyAsync(out_eigs, ctx->eigs.p, eb, cudaMemcpyDeviceToHost, st));
+    HX_CUDA(cudaStreamSynchronize(st));
+    return 0;
   }
   HX_CUDA(cudaMemcpyAsync(hio, ctx->curves.p, cb, cudaMemcpyDeviceToHost, st));
   HX_CUDA(cudaMemcpyAsync(hio + cb, ctx->status.p, sb, cudaMemcpyDeviceToHost, st));
