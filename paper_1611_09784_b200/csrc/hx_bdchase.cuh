@@ -358,11 +358,16 @@ __device__ __forceinline__ QuickReflectorR quick_reflector_r(double alpha, doubl
 // along a row is a stride of RB_LD - 1.
 constexpr int RB_LD = 96, RB_OFF = 63;
 
+// Tile rows of stride BWc + 2 (even): a lane's row is 16-byte aligned, so the row passes and the
+// broadcast vectors use 128-bit shared loads (half the LDS instructions of a stride-(BWc + 1) tile; the
+// column passes stay conflict-free, the 8-byte tile fills see 2-way conflicts).
 template <int BWc>
-struct BdChaseSmemR {
-  double X[BWc][BWc + 1];  // X, then Y (zero-padded)
+struct __align__(16) BdChaseSmemR {
+  double X[BWc][BWc + 2];  // X, then Y (zero-padded)
   double ug[BWc], vh[BWc], cb[BWc];
 };
+
+__device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
 __device__ __forceinline__ void bd_cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -445,8 +450,9 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_real_kernel(double2* ws, 
         double a0 = 0.0, a1 = 0.0;
 #pragma unroll 4
         for (int c = 0; c < BWc; c += 2) {
-          a0 = fma(W.X[lane][c], W.ug[c], a0);
-          a1 = fma(W.X[lane][c + 1], W.ug[c + 1], a1);
+          const double2 x = lds2(&W.X[lane][c]), u = lds2(&W.ug[c]);
+          a0 = fma(x.x, u.x, a0);
+          a1 = fma(x.y, u.y, a1);
         }
         ty = taug * (a0 + a1);
       }
@@ -464,8 +470,9 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_real_kernel(double2* ws, 
         double a0 = 0.0, a1 = 0.0;
 #pragma unroll 4
         for (int r = 0; r < BWc; r += 2) {
-          a0 = fma(W.vh[r], W.X[r][lane], a0);
-          a1 = fma(W.vh[r + 1], W.X[r + 1][lane], a1);
+          const double2 vv = lds2(&W.vh[r]);
+          a0 = fma(vv.x, W.X[r][lane], a0);
+          a1 = fma(vv.y, W.X[r + 1][lane], a1);
         }
         W.cb[lane] = tauh * (a0 + a1 - w * W.ug[lane]);
       }
@@ -474,10 +481,13 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_real_kernel(double2* ws, 
       if (lane < len) {
         double* dst = blk;
 #pragma unroll 4
-        for (int c = 0; c < BWc; ++c, dst += RB_LD - 1) {
-          double z = fma(-v, W.cb[c], fma(-ty, W.ug[c], W.X[lane][c]));
-          if (c == 0 && tauh != 0.0) z = lane == 0 ? hh.beta : 0.0;
-          if (c < len) *dst = z;
+        for (int c = 0; c < BWc; c += 2, dst += 2 * (RB_LD - 1)) {
+          const double2 x = lds2(&W.X[lane][c]), u = lds2(&W.ug[c]), b = lds2(&W.cb[c]);
+          double z0 = fma(-v, b.x, fma(-ty, u.x, x.x));
+          const double z1 = fma(-v, b.y, fma(-ty, u.y, x.y));
+          if (c == 0 && tauh != 0.0) z0 = lane == 0 ? hh.beta : 0.0;
+          if (c < len) dst[0] = z0;
+          if (c + 1 < len) dst[RB_LD - 1] = z1;
         }
       }
       double next_tau = 0.0;
@@ -504,8 +514,9 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_real_kernel(double2* ws, 
           double a0 = 0.0, a1 = 0.0;
 #pragma unroll 4
           for (int r = 0; r < BWc; r += 2) {
-            a0 = fma(W.vh[r], W.X[r][lane], a0);
-            a1 = fma(W.vh[r + 1], W.X[r + 1][lane], a1);
+            const double2 vv = lds2(&W.vh[r]);
+            a0 = fma(vv.x, W.X[r][lane], a0);
+            a1 = fma(vv.y, W.X[r + 1][lane], a1);
           }
           q = a0 + a1;
         }
@@ -524,17 +535,23 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_real_kernel(double2* ws, 
           double a0 = 0.0, a1 = 0.0;
 #pragma unroll 4
           for (int c = 0; c < BWc; c += 2) {
-            a0 = fma(W.X[lane][c], W.ug[c], a0);
-            a1 = fma(W.X[lane][c + 1], W.ug[c + 1], a1);
+            const double2 x = lds2(&W.X[lane][c]), u = lds2(&W.ug[c]);
+            a0 = fma(x.x, u.x, a0);
+            a1 = fma(x.y, u.y, a1);
           }
           const double f = next_tau * (a0 + a1 - tauh * v * qu);
           const bool row0 = lane == 0 && next_tau != 0.0;
           double* dst = blk + (size_t)len * (RB_LD - 1);
 #pragma unroll 4
-          for (int c = 0; c < BWc; ++c, dst += RB_LD - 1) {
-            double z = fma(-f, W.ug[c], fma(-v, W.cb[c], W.X[lane][c]));
-            if (row0) z = c == 0 ? hg.beta : 0.0;
-            if (c < lb) *dst = z;
+          for (int c = 0; c < BWc; c += 2, dst += 2 * (RB_LD - 1)) {
+            const double2 x = lds2(&W.X[lane][c]), u = lds2(&W.ug[c]), b = lds2(&W.cb[c]);
+            double z0 = fma(-f, u.x, fma(-v, b.x, x.x)), z1 = fma(-f, u.y, fma(-v, b.y, x.y));
+            if (row0) {
+              z0 = c == 0 ? hg.beta : 0.0;
+              z1 = 0.0;
+            }
+            if (c < lb) dst[0] = z0;
+            if (c + 1 < lb) dst[RB_LD - 1] = z1;
           }
         }
       }
