@@ -316,6 +316,17 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
     if (ru_rt == 128) launch_rank_update_real<128>(ws, G, mr0, mc0, m, n, u, w, cnt, st);
     else launch_rank_update_real<64>(ws, G, mr0, mc0, m, n, u, w, cnt, st);
   };
+  // Fused schedule (HX_REAL_FUSED=1 forces it on, =0 off; default on for S >= 2048): the trailing rank update
+  // of each side is applied by the next product while it streams the matrix (xv_real_kernel<MODE, true>),
+  // two passes over the trailing matrix fewer per step.  The DRAM-bound updates dominate a lone large tier
+  // (c4, S = 4096); in the concurrent c2 schedule it measured even (64.4 vs 63.9 ms), so smaller S keep the
+  // separate updates.
+  static const int fused_env = [] {
+    const char* e = getenv("HX_REAL_FUSED");
+    return e && e[0] ? atoi(e) : -1;
+  }();
+  const bool fused = fused_env >= 0 ? fused_env != 0 : S >= 2048;
+  bool pend = false;  // right update of the previous step pending on columns >= k0 + 32
   for (int k0 = 0; k0 < S; k0 += BB) {
     const int m1 = S - k0, n2 = S - k0 - BB;
     // ---- left: column panel QR, C_tr = C[k0:, k0+BB:] <- Q1^T C_tr
@@ -326,9 +337,12 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
     }
     count_launch();
     if (n2 <= 0) break;
-    xv_real_kernel<1><<<dim3((unsigned)((n2 + RXV_TM - 1) / RXV_TM), (unsigned)cnt), 128, RXV_SMEM, st>>>(
-        ws, G, k0, k0 + BB, n2, m1, v1, x, t1);
-    rank_update(k0, k0 + BB, m1, n2, v1, x);
+    const dim3 gx1((unsigned)((n2 + RXV_TM - 1) / RXV_TM), (unsigned)cnt);
+    if (!pend)
+      xv_real_kernel<1><<<gx1, 128, RXV_SMEM, st>>>(ws, G, k0, k0 + BB, n2, m1, v1, x, t1);
+    else  // pending: C[r][c] -= Z[r - k0] . V2[32 + c - (k0 + 32)]
+      xv_real_kernel<1, true><<<gx1, 128, RXV_SMEM_UPD, st>>>(ws, G, k0, k0 + BB, n2, m1, v1, x, t1, v2 + BB, z);
+    rank_update(k0, k0 + BB, fused ? std::min(BB, m1) : m1, n2, v1, x);
     count_launch(2);
     // ---- right: row panel LQ of rows k0..k0+BB, C_tr2 = C[k0+BB:, k0+BB:] <- C_tr2 Q2
     const RPanelArgs p2{sd, c0, S, k0, k0 + BB, n2, 1, v2, S, t2};
@@ -338,11 +352,19 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
     }
     count_launch();
     const int m3 = S - k0 - BB;
-    if (m3 > 0) {
-      xv_real_kernel<0><<<dim3((unsigned)((m3 + RXV_TM - 1) / RXV_TM), (unsigned)cnt), 128, RXV_SMEM, st>>>(
-          ws, G, k0 + BB, k0 + BB, m3, n2, v2, z, t2);
+    pend = false;
+    const dim3 gx3((unsigned)((m3 + RXV_TM - 1) / RXV_TM), (unsigned)cnt);
+    if (m3 > 0 && !fused) {
+      xv_real_kernel<0><<<gx3, 128, RXV_SMEM, st>>>(ws, G, k0 + BB, k0 + BB, m3, n2, v2, z, t2);
       rank_update(k0 + BB, k0 + BB, m3, n2, z, v2);
       count_launch(2);
+    } else if (m3 > 0) {
+      // Z = (C_tr2 V2) T2 with the pending left update C[r][c] -= V1[32 + r - (k0+32)] . X1[c - (k0+32)]
+      xv_real_kernel<0, true><<<gx3, 128, RXV_SMEM_UPD, st>>>(ws, G, k0 + BB, k0 + BB, m3, n2, v2, z, t2,
+                                                              v1 + BB, x);
+      rank_update(k0 + BB, k0 + BB, m3, std::min(BB, n2), z, v2);
+      count_launch(2);
+      pend = n2 > BB;
     }
     BD_CUDA(cudaGetLastError());
   }
@@ -362,6 +384,14 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
     const char* e = getenv("HX_CHASE_CAP");
     return e ? atoi(e) : 5;
   }();
+  // cluster size of the few-matrix launches: HX_CHASE_RCL overrides; default 1 (one CTA per matrix)
+  static const int rcl_env = [] {
+    const char* e = getenv("HX_CHASE_RCL");
+    return e ? atoi(e) : -1;
+  }();
+  int rcl = rcl_env >= 0 ? rcl_env : (S >= 2048 ? 8 : 1);  // c4 (S = 4096, 32 matrices): 14.5 -> 17.1 samples/s
+  rcl = rcl >= 8 ? 8 : rcl >= 4 ? 4 : rcl >= 2 ? 2 : 1;
+  while (rcl > 1 && (cnt * rcl > 148 || rcl * 16 > S / BB)) rcl /= 2;  // co-resident; <= one slot per task
   auto smem_of = [&](size_t need) {
     return cap > 0 && want < 6 && want >= 2 ? std::max(need, (size_t)(220 * 1024) / cap) : need;
   };
@@ -374,7 +404,16 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
   else if (rnw == 4) BD_CHASE_REAL(4);
   else if (rnw == 8) BD_CHASE_REAL(8);
   else if (rnw == 16) BD_CHASE_REAL(16);
-  else if (want >= 6) BD_CHASE_REAL(16);
+  else if (want >= 6 && rcl > 1) {
+    // few matrices with long sweeps: CL CTAs (SMs) per matrix, CL x 16 sweeps in flight
+#define BD_CHASE_REAL_CL(CLN)                                                                                \
+  bd_chase_real_kernel<16, BB, CLN><<<(unsigned)(cnt * CLN), 16 * 32, bd_chase_real_smem<16, BB>(), st>>>( \
+      ws2, a1, L.band_off, a3, S, dims)
+    if (rcl == 2) BD_CHASE_REAL_CL(2);
+    else if (rcl == 4) BD_CHASE_REAL_CL(4);
+    else BD_CHASE_REAL_CL(8);
+#undef BD_CHASE_REAL_CL
+  } else if (want >= 6) BD_CHASE_REAL(16);
   else if (want >= 2) BD_CHASE_REAL(4);
   else BD_CHASE_REAL(1);
 #undef BD_CHASE_REAL
@@ -386,6 +425,8 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
 void bd_init_attributes() {
   set_smem_attr(xv_real_kernel<0>, (int)RXV_SMEM);
   set_smem_attr(xv_real_kernel<1>, (int)RXV_SMEM);
+  set_smem_attr(xv_real_kernel<0, true>, (int)RXV_SMEM_UPD);
+  set_smem_attr(xv_real_kernel<1, true>, (int)RXV_SMEM_UPD);
   set_smem_attr(rank_update_real_kernel<64>, (int)rru_smem<64>());
   set_smem_attr(rank_update_real_kernel<128>, (int)rru_smem<128>());
   const char* rs = getenv("HX_REAL_STAGE1");
@@ -415,6 +456,9 @@ void bd_init_attributes() {
   set_smem_attr(bd_chase_real_kernel<1, BB>, 220 * 1024);
   set_smem_attr(bd_chase_real_kernel<2, BB>, 220 * 1024);
   set_smem_attr(bd_chase_real_kernel<16, BB>, 220 * 1024);
+  set_smem_attr(bd_chase_real_kernel<16, BB, 2>, bd_chase_real_smem<16, BB>());
+  set_smem_attr(bd_chase_real_kernel<16, BB, 4>, bd_chase_real_smem<16, BB>());
+  set_smem_attr(bd_chase_real_kernel<16, BB, 8>, bd_chase_real_smem<16, BB>());
   set_smem_attr(bd_chase_real_kernel<4, BB>, 220 * 1024);
   set_smem_attr(bd_chase_real_kernel<8, BB>, 220 * 1024);
   const char* sp = getenv("HX_CHASE_SPIN_NS");

@@ -374,36 +374,54 @@ __device__ __forceinline__ void bd_cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem));
 }
 
-template <int NW, int BWc>
-__global__ void __launch_bounds__(NW * 32, 1) bd_chase_real_kernel(double2* ws, size_t stride, size_t band_off,
-                                                                    size_t tgk_off, int S, const int* dims) {
+// CL > 1: the sweeps of one matrix are dealt round-robin to the warps of a CL-CTA cluster (CL x NW sweeps
+// in flight on CL SMs, for launches with few matrices); progress counters are read across the cluster
+// through DSMEM, the band goes through L2 (ld.global.cg: another SM's stores are not visible in this SM's
+// L1) and the fences are device-scope.
+template <int NW, int BWc, int CL = 1>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NW * 32, 1)
+    bd_chase_real_kernel(double2* ws, size_t stride, size_t band_off, size_t tgk_off, int S, const int* dims) {
   extern __shared__ __align__(16) unsigned char bd_smem[];
   BdChaseSmemR<BWc>* all = reinterpret_cast<BdChaseSmemR<BWc>*>(bd_smem);
   volatile int* prog = reinterpret_cast<volatile int*>(all + NW);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   BdChaseSmemR<BWc>& W = all[warp];
-  const int64_t mat = blockIdx.x;
+  const int rank = CL > 1 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
+  const int gw = rank * NW + warp;  // global warp (sweep slot) of the cluster
+  constexpr int TW = CL * NW;
+  const int64_t mat = blockIdx.x / CL;
   double2* base = ws + (size_t)mat * stride;
   // compact real band (bd_band_extract_kernel): element (r, c), c - 63 <= r <= c + 31, at B[c * RB_LD + r - c + 63]
   double* B = reinterpret_cast<double*>(base + band_off);
   double* diag = reinterpret_cast<double*>(base + tgk_off);
   double* e2 = diag + 2 * S;
-  for (int q = threadIdx.x; q < 2 * S; q += blockDim.x) {
+  for (int q = threadIdx.x + rank * blockDim.x; q < 2 * S; q += blockDim.x * CL) {
     diag[q] = 0.0;
     e2[q] = 0.0;
   }
   if (lane == 0) prog[warp] = -1;
-  __syncthreads();
-  if (threadIdx.x == 0) {
+  if constexpr (CL > 1) {
+    __threadfence();
+    cooperative_groups::this_cluster().sync();
+  } else {
+    __syncthreads();
+  }
+  if (rank == 0 && threadIdx.x == 0) {
     const double a0 = B[RB_OFF];
     e2[0] = a0 * a0;  // alpha_0: final after stage 1
   }
   const bool skip = dims && dims[mat] == 0;
   const int nsweeps = skip ? 0 : S - 1;
-  for (int i = warp; i < nsweeps; i += NW) {
+  for (int i = gw; i < nsweeps; i += TW) {
     const int tasks = (S - 1 - i + BWc - 1) / BWc;
     const int prev_tasks = i > 0 ? (S - i + BWc - 1) / BWc : 0;
-    volatile int* pflag = prog + (i - 1 + NW) % NW;
+    volatile int* pflag;  // progress counter of the warp that owns sweep i - 1
+    {
+      const int gp = (i - 1 + TW) % TW;
+      if constexpr (CL > 1)
+        pflag = cooperative_groups::this_cluster().map_shared_rank(const_cast<int*>(prog), gp / NW) + gp % NW;
+      else pflag = prog + gp;
+    }
     double taug = 0.0;
     for (int t = 0; t < tasks; ++t) {
       if (i > 0) {
@@ -411,7 +429,8 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_real_kernel(double2* ws, 
         if (lane == 0)
           while (*pflag < need) __nanosleep(g_spin_ns);
         __syncwarp();
-        __threadfence_block();
+        if constexpr (CL > 1) __threadfence();
+        else __threadfence_block();
       }
       const int s = i + 1 + t * BWc;
       const int len = min(BWc, S - s);
@@ -420,7 +439,11 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_real_kernel(double2* ws, 
       double* const blk = B + ((size_t)s * RB_LD + lane + RB_OFF);
       {
         const double* src = blk;
-        if (len == BWc) {
+        if (CL > 1) {  // L2-coherent loads (the band is written by other SMs of the cluster)
+#pragma unroll 8
+          for (int cc = 0; cc < BWc; ++cc, src += RB_LD - 1)
+            W.X[lane][cc] = (len == BWc || (lane < len && cc < len)) ? __ldcg(src) : 0.0;
+        } else if (len == BWc) {
 #pragma unroll 8
           for (int cc = 0; cc < BWc; ++cc, src += RB_LD - 1) bd_cp_async8(&W.X[lane][cc], src);
         } else {
@@ -434,7 +457,7 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_real_kernel(double2* ws, 
       if (t == 0) {
         // right reflector from row i, columns [s, s+len): row i -> (beta, 0, ...)
         double* const rowi = B + ((size_t)(s + lane) * RB_LD + i - (s + lane) + RB_OFF);  // (i, s + lane)
-        const double x = lane < len ? *rowi : 0.0;
+        const double x = lane < len ? (CL > 1 ? __ldcg(rowi) : *rowi) : 0.0;
         const double sig2 = warp_sum(x * x);
         const QuickReflectorR h = quick_reflector_r(__shfl_sync(0xffffffffu, x, 0), sig2);
         taug = h.tau;
@@ -495,7 +518,11 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_real_kernel(double2* ws, 
         __syncwarp();
         {
           const double* src = blk + (size_t)len * (RB_LD - 1);  // (s + lane, s + len + cc)
-          if (len == BWc && lb == BWc) {
+          if (CL > 1) {
+#pragma unroll 8
+            for (int cc = 0; cc < BWc; ++cc, src += RB_LD - 1)
+              W.X[lane][cc] = ((len == BWc && lb == BWc) || (lane < len && cc < lb)) ? __ldcg(src) : 0.0;
+          } else if (len == BWc && lb == BWc) {
 #pragma unroll 8
             for (int cc = 0; cc < BWc; ++cc, src += RB_LD - 1) bd_cp_async8(&W.X[lane][cc], src);
           } else {
@@ -556,11 +583,13 @@ __global__ void __launch_bounds__(NW * 32, 1) bd_chase_real_kernel(double2* ws, 
         }
       }
       taug = next_tau;
-      __threadfence_block();
+      if constexpr (CL > 1) __threadfence();
+      else __threadfence_block();
       __syncwarp();
       if (lane == 0) prog[warp] = i * 65536 + t + 1;
     }
   }
+  if constexpr (CL > 1) cooperative_groups::this_cluster().sync();  // remote pollers may still read our counters
 }
 
 // Real parts of the upper band (and the zero window around it) of the dense S x S slab C into the compact

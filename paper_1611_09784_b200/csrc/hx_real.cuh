@@ -221,15 +221,26 @@ constexpr int RXV_A = RXV_TK * RXV_LD0 > RXV_TM * RXV_LD1 ? RXV_TK * RXV_LD0 : R
 constexpr size_t RXV_SMEM = (size_t)RXV_ST * (RXV_A + GBW * RXV_LDV) * sizeof(double);
 static_assert((size_t)(RXV_TM + GBW) * (GBW + 4) * sizeof(double) <= RXV_SMEM, "real xv epilogue tile does not fit");
 
-template <int MODE>
+// UPD (fused schedule): before a chunk of op(A) enters the product it receives the pending rank-32 update of
+// the other side, op(A)[i][k] -= sum_l R[i][l] S[k][l] (R: the CTA's 64 rows, in registers as DMMA A
+// fragments; S: the chunk's 32 rows, staged with the chunk), and the updated chunk is written back to M -
+// one pass over the trailing matrix instead of a rank update (read + write) followed by this product (read).
+//   MODE 0: M[ar0+i][ac0+k] -= R[i] . S[k];   MODE 1: M[ar0+k][ac0+i] -= S[k] . R[i]
+// R[i][l] = base[r_off + i0 + i + l*ld], S[k][l] = base[s_off + k + l*ld].
+constexpr int RXV_LDS = RXV_TK + 4;  // Ss[l][k]
+constexpr size_t RXV_SMEM_UPD = RXV_SMEM + (size_t)RXV_ST * GBW * RXV_LDS * sizeof(double);
+
+template <int MODE, bool UPD = false>
 __global__ void __launch_bounds__(128) xv_real_kernel(double* ws, RSlab g, int ar0, int ac0, int rows, int K,
-                                                      size_t v_off, size_t x_off, size_t t_off) {
+                                                      size_t v_off, size_t x_off, size_t t_off, size_t r_off = 0,
+                                                      size_t s_off = 0) {
   extern __shared__ __align__(16) double rxv_sm[];
   double* As = rxv_sm;
   double* Vs = rxv_sm + RXV_ST * RXV_A;
+  double* Ss = Vs + RXV_ST * GBW * RXV_LDV;  // UPD: [RXV_ST][GBW (l)][RXV_LDS (k)]
   double* base = ws + (size_t)blockIdx.y * g.stride;
   const int ld = g.ld;
-  const double* M = base + g.m_off;
+  double* M = base + g.m_off;
   const double* V = base + v_off;
   double* X = base + x_off;
   const int i0 = blockIdx.x * RXV_TM;
@@ -263,7 +274,30 @@ __global__ void __launch_bounds__(128) xv_real_kernel(double* ws, RSlab g, int a
       const bool ok = gk < K;
       cp_async16_zfill(Vt + n * RXV_LDV + kc, V + (ok ? gk + (size_t)n * ld : 0), ok);
     }
+    if (UPD) {
+      double* St = Ss + stg * GBW * RXV_LDS;
+      const double* Sg = base + s_off;
+#pragma unroll
+      for (int q = 0; q < GBW * RXV_TK / 256; ++q) {
+        const int p = tid + 128 * q, kc = 2 * (p & 15), l = p >> 4;
+        const int gk = kk + kc;
+        const bool ok = gk < K;
+        cp_async16_zfill(St + l * RXV_LDS + kc, Sg + (ok ? gk + (size_t)l * ld : 0), ok);
+      }
+    }
   };
+  // UPD: this warp's 16 rows of R as DMMA A fragments (row 16 warp + 8 rt + lane/4, column 4 k4 + lane%4)
+  double rf[2][GBW / 4];
+  if (UPD) {
+    const double* Rg = base + r_off;
+#pragma unroll
+    for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+      for (int k4 = 0; k4 < GBW / 4; ++k4) {
+        const int r = i0 + 16 * warp + 8 * rt + (lane >> 2);
+        rf[rt][k4] = r < rows ? -Rg[r + (size_t)(4 * k4 + (lane & 3)) * ld] : 0.0;
+      }
+  }
   double acc[2][4][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -283,8 +317,57 @@ __global__ void __launch_bounds__(128) xv_real_kernel(double* ws, RSlab g, int a
       cp_async_commit();
     }
     const int stg = ch % RXV_ST;
-    const double* A = As + stg * RXV_A;
+    double* A = As + stg * RXV_A;
     const double* Vt = Vs + stg * GBW * RXV_LDV;
+    if (UPD) {
+      // op(A)[rows of this warp][32 columns of the chunk] -= R S^T (K = 32), in place + back to M
+      const double* St = Ss + stg * GBW * RXV_LDS;
+      const int kk = ch * RXV_TK;
+      double u[2][4][2];
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct) {
+          const int r = 16 * warp + 8 * rt + (lane >> 2), c = 8 * ct + 2 * (lane & 3);
+          u[rt][ct][0] = MODE == 1 ? A[r * RXV_LD1 + c] : A[c * RXV_LD0 + r];
+          u[rt][ct][1] = MODE == 1 ? A[r * RXV_LD1 + c + 1] : A[(c + 1) * RXV_LD0 + r];
+        }
+#pragma unroll
+      for (int k4 = 0; k4 < GBW / 4; ++k4) {
+        const int lc = 4 * k4 + (lane & 3);
+        double b[4];
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct) b[ct] = St[lc * RXV_LDS + 8 * ct + (lane >> 2)];
+#pragma unroll
+        for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+          for (int ct = 0; ct < 4; ++ct) dmma(u[rt][ct][0], u[rt][ct][1], rf[rt][k4], b[ct]);
+      }
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct) {
+          const int r = 16 * warp + 8 * rt + (lane >> 2), c = 8 * ct + 2 * (lane & 3);
+          if (MODE == 1) {
+            A[r * RXV_LD1 + c] = u[rt][ct][0];
+            A[r * RXV_LD1 + c + 1] = u[rt][ct][1];
+          } else {
+            A[c * RXV_LD0 + r] = u[rt][ct][0];
+            A[(c + 1) * RXV_LD0 + r] = u[rt][ct][1];
+          }
+          const int gi = i0 + r, gk = kk + c;
+          if (gi < rows && gk < K) {  // K even, gk even: gk + 1 < K too
+            if (MODE == 1) {
+              *reinterpret_cast<double2*>(M + (size_t)(ac0 + gi) * ld + ar0 + gk) =
+                  make_double2(u[rt][ct][0], u[rt][ct][1]);
+            } else {
+              M[(size_t)(ac0 + gk) * ld + ar0 + gi] = u[rt][ct][0];
+              M[(size_t)(ac0 + gk + 1) * ld + ar0 + gi] = u[rt][ct][1];
+            }
+          }
+        }
+      __syncwarp();  // the product below reads only this warp's rows of the chunk
+    }
 #pragma unroll
     for (int k4 = 0; k4 < RXV_TK / 4; ++k4) {
       const int kc = 4 * k4 + (lane & 3);
