@@ -15,6 +15,7 @@ tests/test_engine_gpu.py against the reference's full-mode fixtures).
 
 from __future__ import annotations
 
+import functools
 import math
 import os
 import time
@@ -187,7 +188,7 @@ class Engine:
         """One batch of the seam (see _evaluate_batches)."""
         return self._evaluate_batches([(groups, task_ids)])[0]
 
-    def _evaluate_batches(self, batches, on_batch=None):
+    def _evaluate_batches(self, batches, on_batch=None, tiers_of=None):
         """Vectorised batch seam for several consecutive batches.  batches: list of (groups, task_ids),
         groups = [(n, q, words uint64 [R, w]), ...] in request order, task_ids(i_group, new, inv) -> ids of
         the new masks (error reports only).  Every batch is deduplicated on (n, q, mask) against the run
@@ -198,12 +199,38 @@ class Engine:
         as their own GPU batch (own thread and hx context; the first tier's on the high-priority one) as
         soon as they are planned: the host work of the smaller tiers overlaps the device work of the big
         one, and the pieces of different levels run concurrently.  Returns per batch ([(curves [R, npts],
-        per_job [R]) per group], hits, spent)."""
+        per_job [R]) per group], hits, spent).
+
+        A batch may also be given as a zero-argument callable returning (groups, task_ids), with `tiers_of`
+        naming the (n, q) of its groups in order: it is then drawn only when the first tier it contributes
+        to is planned, so the largest tier's masks are drawn and submitted before the other levels' masks
+        exist (the GPU starts while the host is still drawing)."""
         npts = self.grid.npoints
-        tiers: dict = {}  # (n, q) -> [(batch index, group index, words)] in batch order
-        for bi, (groups, _) in enumerate(batches):
-            for gi, (n, q, words) in enumerate(groups):
-                tiers.setdefault((n, q), []).append((bi, gi, np.ascontiguousarray(words, dtype=np.uint64)))
+        made: dict = {}
+
+        def get(bi):
+            b = batches[bi]
+            if callable(b):
+                if bi not in made:
+                    made[bi] = b()
+                return made[bi]
+            return b
+
+        if tiers_of is None:
+            tiers_of = [[(n, q) for n, q, _w in get(bi)[0]] for bi in range(len(batches))]
+        tiers: dict = {}  # (n, q) -> [batch indices contributing] in batch order
+        for bi, tl in enumerate(tiers_of):
+            for t in tl:
+                tiers.setdefault(t, []).append(bi)
+
+        def members(tier):  # [(batch index, group index, words)] of a tier, drawing its batches on demand
+            out = []
+            for bi in tiers[tier]:
+                for gi, (n, q, words) in enumerate(get(bi)[0]):
+                    if (n, q) == tier:
+                        out.append((bi, gi, np.ascontiguousarray(words, dtype=np.uint64)))
+            return out
+
         for n, q in tiers:
             self.cell(n)  # compile cells and k-sets up front (not thread-safe)
             self.kpoints_tr(n, q)
@@ -220,7 +247,7 @@ class Engine:
             for tier in order:
                 pending = {}
                 count = 0
-                for bi, gi, words in tiers[tier]:
+                for bi, gi, words in members(tier):
                     R = words.shape[0]
                     if self.dedup and R:
                         uniq, inv = np.unique(words, axis=0, return_inverse=True)
@@ -244,7 +271,7 @@ class Engine:
                     new = np.flatnonzero(src >= start)
                     hits[bi] += R - len(new)
                     if len(new):
-                        ids = batches[bi][1](gi, new, inv)
+                        ids = get(bi)[1](gi, new, inv)
                         small = self.cell(tier[0]).dim <= 128
                         if _E2E_PRIO == "tiered":
                             # small tiers first (their levels finish early and the host work of placing
@@ -262,9 +289,9 @@ class Engine:
             # batches are finished (placement, cache, on_batch) as soon as that holds, so their host work
             # overlaps the device work still running for later batches
             needs = {}
-            for bi, (groups, _) in enumerate(batches):
+            for bi, tl in enumerate(tiers_of):
                 fs = []
-                for n, q, _w in groups:
+                for n, q in tl:
                     fs += [f for (start, f, pbi) in pieces.get((n, q), []) if pbi <= bi]
                 needs[bi] = fs
             out = [None] * len(batches)
@@ -275,7 +302,7 @@ class Engine:
                     wait([f for bi in left for f in needs[bi] if not f.done()], return_when=FIRST_COMPLETED)
                     continue
                 for bi in ready:
-                    out[bi] = self._place_batch(bi, batches[bi][0], plans, pieces, hits, spent, npts)
+                    out[bi] = self._place_batch(bi, get(bi)[0], plans, pieces, hits, spent, npts)
                     left.remove(bi)
                     if on_batch is not None:
                         on_batch(bi, out[bi])
@@ -410,14 +437,16 @@ class Engine:
         cache hits as sampling them one after another) but their new masks are solved in one concurrent
         submission - every (n, q) tier of every level in flight at once."""
         levels = list(enumerate(zip(plan.ns, plan.samples), start=1))
-        batches = [self._level_batch(idx, n, m, plan.p_vac, idx > 1) for idx, (n, m) in levels]
+        # drawn lazily: the largest tier's level first, so its solve starts while the others are drawn
+        batches = [functools.partial(self._level_batch, idx, n, m, plan.p_vac, idx > 1) for idx, (n, m) in levels]
+        tiers_of = [[(n, self.q_of(n))] + ([(n // 2, self.q_of(n // 2))] if idx > 1 else []) for idx, (n, _) in levels]
         sets = [None] * len(levels)
 
         def finish(bi, ev):  # each level's terms/moments as soon as its curves are in
             idx, (n, m) = levels[bi]
             sets[bi] = self._level_finish(idx, n, m, idx > 1, ev)
 
-        self._evaluate_batches(batches, on_batch=finish)
+        self._evaluate_batches(batches, on_batch=finish, tiers_of=tiers_of)
         total = sum(s.stats.wall_seconds for s in sets)
         return combine_levels(self.grid, [s.stats for s in sets], total_wall_seconds=total), sets
 
