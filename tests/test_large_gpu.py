@@ -53,3 +53,33 @@ def test_nu64_defected_sample_plateau_and_monotone():
     d = sc.nunits - vac
     assert curves[0, -1] == pytest.approx(d / sc.area, abs=1e-12)
     assert np.all(np.diff(curves[0]) >= -1e-12)
+
+
+def test_nu46_defected_matches_oracle_on_the_large_real_path():
+    """S = 46^2 = 2116 >= 2048: the real-storage stage 1 with the fused schedule (trailing updates applied
+    by the next xv pass) and the clustered real chase (several SMs per matrix) - a defected sample at Gamma
+    against the oracle (LAPACK zhegv on the N = 4232 pencil, ~10 s on the host): eigenvalues within
+    1e-10 x width, IDOS within 1e-9."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "oracle"))
+    import hexmc_oracle as O
+
+    nu = 46
+    model = hx.GrapheneNNModel()
+    spec = model.lattice_spec()
+    sc = hx.build_supercell(spec, nu)
+    cell = hx.compile_cell(model, sc)
+    kp = hx.make_bz_grid(spec, nu, 1, "reduced").kpoints
+    words = sample_masks(sc.nunits, 0.02, 5, 2, 0, 1)
+    curves, eigs, status = eval_batch(cell, kp, words, LO, (HI - LO) / (NPTS - 1), NPTS, 0.01, want_eigs=True)
+    assert (status == 0).all()
+    om = O.graphene_model()
+    ocell = O.make_cell(om, nu)
+    key = sum(int(w) << (64 * i) for i, w in enumerate(words[0]))
+    ref = O.solve_bands(ocell, om, key, kp)
+    d = ref.shape[1]
+    assert np.max(np.abs(eigs[0, :, :d] - ref)) <= 1e-10 * (ref.max() - ref.min())
+    rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), LO, HI, NPTS, 0.01, ocell.area)
+    np.testing.assert_allclose(curves[0], rc, rtol=0, atol=1e-9)
