@@ -96,3 +96,23 @@ def _np_moments(full, quarters):
     terms = full if quarters is None else full - quarters.sum(axis=1) * 0.25
     t = torch.from_numpy(np.ascontiguousarray(terms))
     return t, t.mean(0), t.var(0) if len(terms) > 1 else t.mean(0)
+
+
+def test_unique_rows_matches_numpy_axis0_unique():
+    """The seam's row dedup (engine.unique_rows / first_rows) equals np.unique(axis=0) - same lexicographic
+    order of the unique masks, same inverse - and the first-occurrence map of the reference loop."""
+    from paper_1611_09784_b200.engine import first_rows, unique_rows
+
+    rng = np.random.default_rng(7)
+    for w in (1, 2, 4):
+        for R in (1, 3, 257, 2048):
+            words = (rng.integers(0, 5, size=(R, w)).astype(np.uint64) << np.uint64(61)) | np.uint64(3)
+            u0, i0 = np.unique(words, axis=0, return_inverse=True)
+            u1, i1 = unique_rows(words)
+            assert np.array_equal(u0, u1) and np.array_equal(i0.reshape(-1), i1)
+            first = np.full(i1.max() + 1, -1)
+            for r in range(R - 1, -1, -1):
+                first[i1[r]] = r
+            assert np.array_equal(first, first_rows(i1))
+    u, i = unique_rows(np.zeros((0, 2), dtype=np.uint64))
+    assert u.shape == (0, 2) and i.shape == (0,)
