@@ -369,6 +369,15 @@ struct __align__(16) BdChaseSmemR {
 
 __device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
+// Two warp sums in one reduction round (the shuffles of the two values pipeline).
+__device__ __forceinline__ void warp_sum2(double& a, double& b) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+}
+
 __device__ __forceinline__ void bd_cp_async8(void* smem, const void* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem));
@@ -480,13 +489,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NW * 32, 1)
         ty = taug * (a0 + a1);
       }
       const double x0 = W.X[lane][0] - ty;
-      const double sh2 = warp_sum(x0 * x0);
+      // one reduction round for |x0|^2 and sum_{r>=1} x0_r ty_r: w = v^T (tau_g y) = ty_0 + scale * that
+      double sh2 = x0 * x0, xt = lane == 0 ? 0.0 : x0 * ty;
+      warp_sum2(sh2, xt);
       const QuickReflectorR hh = quick_reflector_r(__shfl_sync(0xffffffffu, x0, 0), sh2);
       const double tauh = hh.tau;
       if (t == 0 && lane == 0) e2[2 * s] = sh2;
       const double v = lane == 0 ? 1.0 : x0 * hh.scale;  // zero on padded rows
       W.vh[lane] = v;
-      const double w = warp_sum(v * ty);  // v^T (tau_g y)
+      const double w = fma(hh.scale, xt, __shfl_sync(0xffffffffu, ty, 0));
       __syncwarp();
       // ---- X column pass: p = v^T X, b_c = tau_h (p_c - w u_c)
       {
@@ -548,11 +559,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NW * 32, 1)
           q = a0 + a1;
         }
         const double xg = W.X[0][lane] - tauh * q;  // row 0 of H Y
-        const double sg2 = warp_sum(xg * xg);
+        // one reduction round for |xg|^2 and sum_{c>=1} q_c xg_c: qu = (v^T Y) u' = q_0 + scale * that
+        double sg2 = xg * xg, qx = lane == 0 ? 0.0 : q * xg;
+        warp_sum2(sg2, qx);
         const QuickReflectorR hg = quick_reflector_r(__shfl_sync(0xffffffffu, xg, 0), sg2);
         next_tau = hg.tau;
         const double u2 = lane == 0 ? 1.0 : xg * hg.scale;  // zero on padded columns
-        const double qu = warp_sum(q * u2);                  // (v^T Y) u'
+        const double qu = fma(hg.scale, qx, __shfl_sync(0xffffffffu, q, 0));
         __syncwarp();  // everyone is done with ug (X update) and cb
         W.ug[lane] = u2;
         W.cb[lane] = tauh * q;  // d_c
