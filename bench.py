@@ -447,7 +447,7 @@ def run_c5(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)  # ~1.3 s timed region on c2: several clock samples
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="hx", choices=["hx", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
