@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define HX_ABI_VERSION 2
+#define HX_ABI_VERSION 3
 
 /* return codes */
 #define HX_OK 0
@@ -91,6 +91,14 @@ int hx_abi_version(void);
 /* Cumulative number of libhx kernel launches in this process (instrumentation for bench.py). */
 int hx_kernel_launches(uint64_t* out);
 const char* hx_last_error(void);
+/* Path-selection / tuning knobs (the HX_* names documented in DESIGN.md, e.g. HX_CHASE_RNW, HX_NO_REAL,
+ * HX_REAL_STAGE1, HX_BIDIAG_REAL).  A value set here overrides the environment variable of the same
+ * name; every batch call re-reads them, so tests force each kernel variant in-process.  No reference
+ * counterpart (the reference selects its kernels once, by HEXMC_NO_NUMBA, _kernels.py:19-29).
+ * hx_clear_option(NULL) clears every override. */
+int hx_set_option(const char* name, int64_t value);
+int hx_clear_option(const char* name);
+int hx_get_option(const char* name, int64_t dflt, int64_t* out);
 int hx_device_count(int32_t* out);
 int hx_ctx_create(int32_t device, hx_ctx** out);
 /* Same with the context's work stream at CUDA stream priority `priority` (lower = higher priority;

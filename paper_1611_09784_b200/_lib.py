@@ -28,7 +28,7 @@ EXPORTED = (
     "hx_eval_idos_batch_device", "hx_eval_idos_batch_k", "hx_eval_idos_batch_device_k", "hx_eigvalsh_batch_device", "hx_smoothed_counts_device",
     "hx_sharp_counts_device", "hx_level_moments_device", "hx_sample_masks", "hx_sample_masks_device",
     "hx_uniforms", "hx_restrict_masks", "hx_assemble_device", "hx_restrict_masks_device",
-    "hx_kernel_launches",
+    "hx_kernel_launches", "hx_set_option", "hx_clear_option", "hx_get_option",
 )
 
 
@@ -69,6 +69,9 @@ def load():
             "hx_abi_version": (C.c_int, []),
             "hx_kernel_launches": (C.c_int, [C.POINTER(u64)]),
             "hx_last_error": (C.c_char_p, []),
+            "hx_set_option": (C.c_int, [C.c_char_p, i64]),
+            "hx_clear_option": (C.c_int, [C.c_char_p]),
+            "hx_get_option": (C.c_int, [C.c_char_p, i64, C.POINTER(i64)]),
             "hx_device_count": (C.c_int, [C.POINTER(i32)]),
             "hx_ctx_create": (C.c_int, [i32, C.POINTER(vp)]),
             "hx_ctx_create_priority": (C.c_int, [i32, i32, C.POINTER(vp)]),
@@ -136,6 +139,37 @@ def restrict_masks(parent_words: np.ndarray, parent_units: int, assign: np.ndarr
     check(load().hx_restrict_masks(ptr(parent_words), n, parent_units, ptr(a), ptr(m), sub_units, ptr(out)),
           "hx_restrict_masks")
     return out
+
+
+def set_option(name: str, value: int):
+    check(load().hx_set_option(name.encode(), int(value)), f"hx_set_option({name})")
+
+
+def clear_option(name: str | None = None):
+    check(load().hx_clear_option(None if name is None else name.encode()), "hx_clear_option")
+
+
+def get_option(name: str, default: int = -1) -> int:
+    v = C.c_int64(0)
+    check(load().hx_get_option(name.encode(), int(default), C.byref(v)), "hx_get_option")
+    return int(v.value)
+
+
+class options:
+    """Context manager forcing libhx path knobs (hx_set_option), restoring them on exit:
+    `with options(HX_CHASE_RNW=4): ...`."""
+
+    def __init__(self, **kv):
+        self.kv = kv
+
+    def __enter__(self):
+        for k, v in self.kv.items():
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k in self.kv:
+            clear_option(k)
 
 
 def kernel_launches() -> int:

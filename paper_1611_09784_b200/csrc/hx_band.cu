@@ -407,10 +407,7 @@ static int band_reduce(double2* ws, const BandWs& L, int N, int64_t cnt, const i
   // at least 3 sweeps in flight per matrix: the many-matrix launches (c3 level 2: ~1900 matrices) ran one
   // warp per matrix with its sweeps fully serialised (c3 levels 2 / 3: 521 -> 446 / 1487 -> 1412 ms);
   // HX_HCHASE_MIN_NW overrides
-  static const int min_nw = [] {
-    const char* e = getenv("HX_HCHASE_MIN_NW");
-    return e ? atoi(e) : 3;
-  }();
+  const int min_nw = (int)opt("HX_HCHASE_MIN_NW", 3);
   const int64_t want = std::max<int64_t>(min_nw, (148 * 12 + cnt - 1) / cnt);
 #define HCHASE(NW)                                                                                \
   bulge_chase_pipe_kernel<NW, BW, false><<<(unsigned)cnt, NW * 32, chase_smem_bytes<NW, BW, false>(), st>>>( \

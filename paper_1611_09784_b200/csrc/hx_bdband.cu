@@ -31,9 +31,12 @@
 
 namespace hx {
 
-bool g_bd_chase_pair = true;  // warp-pair bulge chase (HX_CHASE_PAIR=0: one warp per task)
-bool g_bd_chase_real = true;  // real bulge chase for real (periodic-gauge) batches (HX_CHASE_REAL=0: complex)
-bool g_bd_real_stage1 = true;  // real storage + arithmetic in stage 1 of real batches, S % 4 == 0 (HX_REAL_STAGE1=0)
+// warp-pair bulge chase (HX_CHASE_PAIR=0: one warp per task)
+static bool bd_chase_pair() { return opt("HX_CHASE_PAIR", 1) != 0; }
+// real bulge chase for real (periodic-gauge) batches (HX_CHASE_REAL=0: complex)
+static bool bd_chase_real() { return opt("HX_CHASE_REAL", 1) != 0; }
+// real storage + arithmetic in stage 1 of real batches, S % 4 == 0 (HX_REAL_STAGE1=0)
+static bool bd_real_stage1() { return opt("HX_REAL_STAGE1", 1) != 0; }
 
 
 constexpr int BB = 32;  // band width
@@ -106,10 +109,7 @@ bool launch_cluster_panel(double2* ws, const PanelArgs& a, int64_t cnt, cudaStre
 template <bool RE = false>
 static void launch_rank_update(double2* ws, const SlabGeom& G, int mr0, int mc0, int m, int n, size_t u_off,
                                size_t w_off, int64_t cnt, cudaStream_t st) {
-  static const int tn = [] {
-    const char* e = getenv("HX_RU_TN");
-    return e && atoi(e) == 32 ? 32 : 64;
-  }();
+  const int tn = opt("HX_RU_TN", 64) == 32 ? 32 : 64;
   const unsigned gx = (unsigned)((m + RU_T - 1) / RU_T);
   if (tn == 64)
     rank_update_kernel<64, RE><<<dim3(gx, (unsigned)((n + 63) / 64), (unsigned)cnt), 256, ru_smem<64>(), st>>>(
@@ -140,10 +140,7 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
   // matrix per side).  Correct, but measured ~10% slower than separate rank updates on sm_100a (the fused
   // kernel needs ~210 registers: 2 CTAs/SM instead of 3, and the DMMA pipe idles during the update), so
   // it is off by default.
-  static const bool fused = [] {
-    const char* e = getenv("HX_FUSED_UPDATE");
-    return e && e[0] == '1';
-  }();
+  const bool fused = opt("HX_FUSED_UPDATE", 0) == 1;
   bool pend = false;  // right update of the previous step pending on columns >= k0 + 32
   for (int k0 = 0; k0 < S; k0 += BB) {
     const int m1 = S - k0, n2 = S - k0 - BB;
@@ -188,10 +185,7 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     BD_CUDA(cudaGetLastError());
   }
   // ---- stage 2: enough sweeps in flight to fill the SMs (single-tile variant: 19 KB per warp).
-  static const int chase_mode = [] {
-    const char* e = getenv("HX_CHASE_MODE");
-    return e ? atoi(e) : 0;
-  }();
+  const int chase_mode = (int)opt("HX_CHASE_MODE", 0);
   const int64_t want = (148 * 11 + cnt - 1) / cnt;
   const size_t a1 = L.stride, a2 = L.c_off, a3 = L.tgk_off;
 #define BD_CHASE(NW, DUAL, CL)                                                                          \
@@ -222,7 +216,7 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
                                                                                                 a3, S, dims); \
     BD_CUDA(cudaGetLastError());                                                                        \
   }
-  if (RE && g_bd_chase_real) {
+  if (RE && bd_chase_real()) {
     bd_band_extract_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, L.stride, L.c_off, L.band_off, S);
     count_launch();
     // real band: a quarter of the arithmetic and half the shared memory per sweep
@@ -233,7 +227,7 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
     return 0;
   }
 #undef BD_CHASE_REAL
-  const bool pair = chase_mode >= 4 || (chase_mode == 0 && g_bd_chase_pair);
+  const bool pair = chase_mode >= 4 || (chase_mode == 0 && bd_chase_pair());
   // warp-pair tasks for the throughput-bound launches (many matrices); the latency-bound one-CTA-per-matrix
   // launch keeps one warp per task (its shared-memory pipe is the limit, measured 24.3 vs 25.1 ms)
   if (pair && (want < 6 || chase_mode >= 4)) {
@@ -308,10 +302,7 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
   const size_t sd = 2 * L.stride, c0 = 2 * L.c_off, v1 = 2 * L.v1_off, v2 = 2 * L.v2_off, x = 2 * L.x_off,
                z = 2 * L.z_off, t1 = 2 * L.t1_off, t2 = 2 * L.t2_off;
   const RSlab G{sd, S, c0};
-  static const int ru_rt = [] {
-    const char* e = getenv("HX_RRU_RT");
-    return e && atoi(e) == 128 ? 128 : 64;
-  }();
+  const int ru_rt = opt("HX_RRU_RT", 64) == 128 ? 128 : 64;
   auto rank_update = [&](int mr0, int mc0, int m, int n, size_t u, size_t w) {
     if (ru_rt == 128) launch_rank_update_real<128>(ws, G, mr0, mc0, m, n, u, w, cnt, st);
     else launch_rank_update_real<64>(ws, G, mr0, mc0, m, n, u, w, cnt, st);
@@ -321,10 +312,7 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
   // two passes over the trailing matrix fewer per step.  The DRAM-bound updates dominate a lone large tier
   // (c4, S = 4096); in the concurrent c2 schedule it measured even (64.4 vs 63.9 ms), so smaller S keep the
   // separate updates.
-  static const int fused_env = [] {
-    const char* e = getenv("HX_REAL_FUSED");
-    return e && e[0] ? atoi(e) : -1;
-  }();
+  const int fused_env = (int)opt("HX_REAL_FUSED", -1);
   const bool fused = fused_env >= 0 ? fused_env != 0 : S >= 2048;
   bool pend = false;  // right update of the previous step pending on columns >= k0 + 32
   for (int k0 = 0; k0 < S; k0 += BB) {
@@ -376,19 +364,10 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
   // and at most 5 CTAs per SM (padded dynamic shared memory), which bounds the bands in flight (~740 x
   // 196 KB) - measured 3-4 % faster per pass than 2 sweeps at full occupancy (the launch is L2-capacity
   // bound: 17.7 GB DRAM traffic for 200 MB of bands).  HX_CHASE_RNW / HX_CHASE_CAP override (0 = off).
-  static const int rnw = [] {
-    const char* e = getenv("HX_CHASE_RNW");
-    return e ? atoi(e) : -1;
-  }();
-  static const int cap = [&] {
-    const char* e = getenv("HX_CHASE_CAP");
-    return e ? atoi(e) : 5;
-  }();
+  const int rnw = (int)opt("HX_CHASE_RNW", -1);
+  const int cap = (int)opt("HX_CHASE_CAP", 5);
   // cluster size of the few-matrix launches: HX_CHASE_RCL overrides; default 1 (one CTA per matrix)
-  static const int rcl_env = [] {
-    const char* e = getenv("HX_CHASE_RCL");
-    return e ? atoi(e) : -1;
-  }();
+  const int rcl_env = (int)opt("HX_CHASE_RCL", -1);
   int rcl = rcl_env >= 0 ? rcl_env : (S >= 2048 ? 8 : 1);  // c4 (S = 4096, 32 matrices): 14.5 -> 17.1 samples/s
   rcl = rcl >= 8 ? 8 : rcl >= 4 ? 4 : rcl >= 2 ? 2 : 1;
   while (rcl > 1 && (cnt * rcl > 148 || rcl * 16 > S / BB)) rcl /= 2;  // co-resident; <= one slot per task
@@ -429,8 +408,6 @@ void bd_init_attributes() {
   set_smem_attr(xv_real_kernel<1, true>, (int)RXV_SMEM_UPD);
   set_smem_attr(rank_update_real_kernel<64>, (int)rru_smem<64>());
   set_smem_attr(rank_update_real_kernel<128>, (int)rru_smem<128>());
-  const char* rs = getenv("HX_REAL_STAGE1");
-  if (rs && rs[0]) g_bd_real_stage1 = atoi(rs) != 0;
   set_smem_attr(xv_kernel<0>, (int)XV_SMEM);
   set_smem_attr(xv_kernel<1>, (int)XV_SMEM);
   set_smem_attr(xv_kernel<0, true>, XV_SMEM_UPD);
@@ -466,10 +443,6 @@ void bd_init_attributes() {
     const unsigned v = (unsigned)atoi(sp);
     cudaMemcpyToSymbol(g_spin_ns, &v, sizeof(v));
   }
-  const char* cr = getenv("HX_CHASE_REAL");
-  if (cr && cr[0]) g_bd_chase_real = atoi(cr) != 0;
-  const char* pe = getenv("HX_CHASE_PAIR");
-  if (pe && pe[0]) g_bd_chase_pair = atoi(pe) != 0;
 }
 
 int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, int64_t nmasks, const GridDev& g,
@@ -480,7 +453,7 @@ int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, 
   const BdWs L = BdWs::make(S);
   const size_t per = L.stride * sizeof(double2) + sizeof(int);
   const int64_t nmat = nmasks * nk;
-  const bool real_s1 = real && g_bd_real_stage1 && g_bd_chase_real && S % 4 == 0;
+  const bool real_s1 = real && bd_real_stage1() && bd_chase_real() && S % 4 == 0;
   int64_t chunk = std::max<int64_t>(1, (int64_t)(ws_budget / per));
   chunk = std::min<int64_t>(std::min<int64_t>(chunk, nmat), 65535);
   unsigned char* buf = static_cast<unsigned char*>(alloc(per * (size_t)chunk + 256));

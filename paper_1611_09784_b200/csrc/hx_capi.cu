@@ -9,6 +9,8 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <map>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -23,6 +25,21 @@
 namespace hx {
 static std::atomic<unsigned long long> g_launches{0};
 void count_launch(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+std::mutex g_opt_mu;
+std::map<std::string, long> g_opts;
+}  // namespace
+
+long opt(const char* name, long dflt) {
+  {
+    std::lock_guard<std::mutex> lk(g_opt_mu);
+    auto it = g_opts.find(name);
+    if (it != g_opts.end()) return it->second;
+  }
+  const char* e = getenv(name);
+  return e && e[0] ? atol(e) : dflt;
+}
 }  // namespace hx
 
 namespace {
@@ -102,7 +119,23 @@ struct hx_ctx {
   int bidiag_real_warp_max_s = 64;       // real (time-reversal-invariant) k-points: one warp per matrix up to this S
   bool bidiag_real = true;               // real Golub-Kahan for those k-points (HX_BIDIAG_REAL=0 disables)
   bool use_bipartite = true;            // graphene: singular values of the A-B block (HX_NO_BIPARTITE=1 disables)
+  size_t ws_budget_default = ws_budget;
 };
+
+namespace {
+// Path-selection knobs of a context, re-read from the option registry at every batch call (hx::opt).
+void refresh_opts(hx_ctx* ctx) {
+  ctx->use_bipartite = hx::opt("HX_NO_BIPARTITE", 0) == 0;
+  ctx->bd_min_n = (int)hx::opt("HX_BD_MIN_N", HX_SMEM_MAX_N);
+  ctx->bidiag_warp_max_s = (int)hx::opt("HX_BIDIAG_WARP_MAX_S", 32);
+  ctx->bidiag_threads = (int)hx::opt("HX_BIDIAG_THREADS", 256);
+  ctx->bidiag_real = hx::opt("HX_BIDIAG_REAL", 1) != 0;
+  ctx->bidiag_real_warp_max_s = (int)hx::opt("HX_BIDIAG_REAL_WARP_MAX_S", 64);
+  // experiments: workspace chunk budget in MB (L2-resident chunks)
+  const long wb = hx::opt("HX_WS_BUDGET_MB", 0);
+  ctx->ws_budget = wb > 0 ? (size_t)wb << 20 : ctx->ws_budget_default;
+}
+}  // namespace
 
 struct hx_cell {
   hx_ctx* ctx = nullptr;
@@ -175,7 +208,8 @@ void transpose_csr(int N, const int32_t* ptr, const int32_t* col, std::vector<in
   for (int e = 0; e < nnz; ++e) tinst[fill[col[e]]++] = e;
 }
 
-bool g_real_batches = true;  // periodic-gauge real arithmetic for TRIM batches (HX_NO_REAL=1 disables)
+// periodic-gauge real arithmetic for TRIM batches (HX_NO_REAL=1 disables)
+bool real_batches() { return hx::opt("HX_NO_REAL", 0) == 0; }
 
 int fixed_point_shift(int64_t nk, int N) {
   const double terms = (double)nk * (double)(N + 1) + 1.0;
@@ -188,6 +222,26 @@ int fixed_point_shift(int64_t nk, int N) {
 extern "C" {
 
 int hx_abi_version(void) { return HX_ABI_VERSION; }
+
+int hx_set_option(const char* name, int64_t value) {
+  if (!name || std::strncmp(name, "HX_", 3) != 0) return fail(HX_E_ARG, "option names start with HX_");
+  std::lock_guard<std::mutex> lk(hx::g_opt_mu);
+  hx::g_opts[name] = (long)value;
+  return 0;
+}
+
+int hx_clear_option(const char* name) {
+  std::lock_guard<std::mutex> lk(hx::g_opt_mu);
+  if (name) hx::g_opts.erase(name);
+  else hx::g_opts.clear();
+  return 0;
+}
+
+int hx_get_option(const char* name, int64_t dflt, int64_t* out) {
+  if (!name || !out) return fail(HX_E_ARG, "null argument");
+  *out = hx::opt(name, (long)dflt);
+  return 0;
+}
 
 int hx_kernel_launches(uint64_t* out) {
   if (!out) return fail(HX_E_ARG, "null out");
@@ -237,30 +291,10 @@ int hx_ctx_create_priority(int32_t device, int32_t priority, hx_ctx** out) {
   }
   size_t freeb = 0, total = 0;
   cudaMemGetInfo(&freeb, &total);
-  {
-    const char* nb = getenv("HX_NO_BIPARTITE");
-    ctx->use_bipartite = !(nb && nb[0] && nb[0] != '0');
-    const char* bm = getenv("HX_BD_MIN_N");
-    if (bm && bm[0]) ctx->bd_min_n = atoi(bm);
-    const char* bw = getenv("HX_BIDIAG_WARP_MAX_S");
-    if (bw && bw[0]) ctx->bidiag_warp_max_s = atoi(bw);
-    const char* nr = getenv("HX_NO_REAL");
-    if (nr && nr[0] && nr[0] != '0') g_real_batches = false;
-    const char* zm = getenv("HX_ZONE_MIN_N");
-    if (zm && zm[0]) hx::g_zone_min_n = atoi(zm);
-    const char* bt = getenv("HX_BIDIAG_THREADS");
-    if (bt && bt[0]) ctx->bidiag_threads = atoi(bt);
-    const char* br = getenv("HX_BIDIAG_REAL");
-    if (br && br[0]) ctx->bidiag_real = atoi(br) != 0;
-    const char* brw = getenv("HX_BIDIAG_REAL_WARP_MAX_S");
-    if (brw && brw[0]) ctx->bidiag_real_warp_max_s = atoi(brw);
-  }
   hx::set_smem_attr(hx::small_bidiag_kernel, 200 * 1024);
   ctx->ws_budget = std::min(ctx->ws_budget, freeb / 3);
-  {
-    const char* wb = getenv("HX_WS_BUDGET_MB");  // experiments: workspace chunk budget (L2-resident chunks)
-    if (wb && wb[0]) ctx->ws_budget = (size_t)atoll(wb) << 20;
-  }
+  ctx->ws_budget_default = ctx->ws_budget;
+  refresh_opts(ctx);
   hx::set_smem_attr(hx::small_tridiag_kernel, (int)hx::small_tridiag_smem(HX_SMEM_MAX_N));
   hx::set_smem_attr(hx::eigvalsh_small_kernel, (int)hx::small_tridiag_smem(HX_SMEM_MAX_N));
   hx::band_init_attributes();
@@ -403,6 +437,7 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
     return fail(HX_E_ARG, "energy grid needs npts >= 1, step > 0, delta > 0");
   if (nmasks == 0) return 0;
   if (set_device(ctx)) return HX_E_CUDA;
+  refresh_opts(ctx);
   const hx::CellDev& c = cell->dev;
   const int N = c.N;
   int64_t nk_total = nk;
@@ -427,7 +462,7 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
   // followed by the k-point lists of the shared-memory bipartite tier: complex k-points, then those whose
   // periodic-gauge block is real (time-reversal-invariant: real Golub-Kahan, one warp per matrix)
   std::vector<int> klist_c, klist_r;
-  if (c.bipartite && ctx->use_bipartite && g_real_batches && ctx->bidiag_real)
+  if (c.bipartite && ctx->use_bipartite && real_batches() && ctx->bidiag_real)
     for (int k = 0; k < nk; ++k) (k_is_real(cell, kpoints, k) ? klist_r : klist_c).push_back(k);
   // one pinned staging copy carries k-points, k lists and multiplicities
   const size_t kbytes = (size_t)nk * 24;
@@ -515,7 +550,7 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
     }
   } else if (use_bd) {
     if (make_refine(nmat * N)) return fail(HX_E_CUDA, "alloc refinement list");
-    const bool real = g_real_batches && batch_is_real(cell, kpoints, nk);
+    const bool real = real_batches() && batch_is_real(cell, kpoints, nk);
     int rc = hx::bd_eval(c, kp, nk, d_masks, nmasks, g, diff, trans, d_eigs, status, sharp, real, ctx->ws_budget,
                          [&](size_t bytes) -> void* { return ctx->band.grow(bytes) ? nullptr : ctx->band.p; }, st,
                          refine, refine_count);
@@ -672,6 +707,7 @@ int hx_eigvalsh_batch_device(hx_ctx* ctx, int32_t n, int64_t batch, const double
   if (batch == 0) return 0;
   if (n > HX_MAX_N) return fail(HX_E_RANGE, "hx_eigvalsh_batch: n too large");
   if (set_device(ctx)) return HX_E_CUDA;
+  refresh_opts(ctx);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int* status = reinterpret_cast<int*>(d_status);
   hx::CellDev c{};

@@ -8,6 +8,11 @@ namespace hx {
 // Number of libhx kernel launches issued by this process (reported by bench.py as gpu_launches).
 void count_launch(unsigned long long n = 1);
 
+// Tuning / path-selection knobs (HX_*): a value set through hx_set_option() wins, else the environment
+// variable of the same name, else `dflt`.  Read at every batch call, so tests can force each kernel
+// variant in-process (hx_capi.cu).
+long opt(const char* name, long dflt);
+
 // Compiled-cell tables resident in HBM (uploaded once per (model, nu)).
 struct CellDev {
   int32_t N;          // total dofs

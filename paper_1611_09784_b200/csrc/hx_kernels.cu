@@ -682,7 +682,7 @@ static bool zone_path_ok(const CellDev& c, const GridDev& g, int sharp, bool& re
   return (size_t)g.npts * 2 * sizeof(int) <= 96 * 1024;
 }
 
-int g_zone_min_n = 96;
+
 
 void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, int64_t nmat, const double* tri,
                      size_t tri_stride, const int* dims, int* diff, unsigned long long* trans, double* eigs,
@@ -694,7 +694,7 @@ void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, i
   if (two_pass) cudaMemsetAsync(refine_count, 0, sizeof(unsigned long long), st);
   bool rev = false;
   // zone path: 2 npts Sturm counts per matrix beat ~d/2 x 10 bisection steps from d ~ 96 on
-  if (two_pass && c.N >= g_zone_min_n && zone_path_ok(c, g, sharp, rev)) {
+  if (two_pass && c.N >= opt("HX_ZONE_MIN_N", 96) && zone_path_ok(c, g, sharp, rev)) {
     const size_t zsm = (size_t)g.npts * 2 * sizeof(int);
     const int zt = g.npts >= 256 ? 256 : ((g.npts + 31) / 32) * 32;
     if (tgk) {

@@ -52,7 +52,6 @@ __global__ void finalize_kernel(const int* diff, const unsigned long long* trans
 // transition windows stop early and the rest are finished by a densely packed second pass.  tgk: the
 // tridiagonals are Golub-Kahan (zero diagonal, spectrum symmetric about 0): one thread per +-pair.
 // smallest N that takes the zone path of the eigenvalue stage (HX_ZONE_MIN_N; 0 = always)
-extern int g_zone_min_n;
 
 void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, int64_t nmat, const double* tri,
                      size_t tri_stride, const int* dims, int* diff, unsigned long long* trans, double* eigs,

@@ -1,0 +1,145 @@
+"""GPU parity of every kernel variant the benchmark shapes select, against the oracle (LAPACK restatement).
+
+The banded tiers pick their kernels from the batch size and the matrix size (hx_bdband.cu: real bulge chase
+with 16 / 4 / 1 warps per matrix from ceil(1628 / matrices), padded shared memory for 2 <= want < 6,
+clusters of 2-8 SMs per matrix for S >= 1024 ... 4096; real or complex storage; real Golub-Kahan at the
+time-reversal-invariant k-points of the shared-memory tier).  Each test below either builds a batch of the
+size the bench uses for that tier, or forces the variant through the option registry (hx_set_option, the
+`_lib.options` context manager), and compares a subset of the batch with the oracle:
+eigenvalues <= 1e-10 x spectral width, IDOS <= 1e-9 (BASELINE.json north_star).  Reference:
+spectrum.py:100-134 (zhegv / zheevd per k), qoi.py:96-102 (IDOS).
+"""
+
+import numpy as np
+import pytest
+
+import hexmc_oracle as O
+from conftest import TABLE, words_to_int
+
+import paper_1611_09784_b200 as hx
+from paper_1611_09784_b200 import _lib
+from paper_1611_09784_b200.sampling import sample_masks
+from paper_1611_09784_b200.solver import eval_batch
+
+pytestmark = pytest.mark.gpu
+
+EIG_TOL = 1e-10
+IDOS_TOL = 1e-9
+LO_G, HI_G = -6.580201874549387, 14.863393148450246
+LO_T, HI_T = -2.952, 4.760
+NPTS = 201
+
+
+def _setup(kind, nu, q, kp=None):
+    model = hx.load_coupling_table(TABLE) if kind == "table" else hx.GrapheneNNModel()
+    om = O.parse_table(str(TABLE)) if kind == "table" else O.graphene_model()
+    spec = model.lattice_spec()
+    sc = hx.build_supercell(spec, nu)
+    cell = hx.compile_cell(model, sc)
+    if kp is None:
+        kp = hx.make_bz_grid(spec, nu, q, "reduced").kpoints
+    return model, om, sc, cell, np.ascontiguousarray(kp)
+
+
+def check_batch(kind, nu, q, p, nmasks, seed, check, kp=None, opts=None, eigs_too=True):
+    """Solve `nmasks` seeded masks in ONE batch (so the batch-size-dependent variant runs), compare the
+    masks `check` with the oracle.  Both the eigenvalue path and the IDOS-only fast path are checked."""
+    _, om, sc, cell, kp = _setup(kind, nu, q, kp)
+    lo, hi = (LO_T, HI_T) if kind == "table" else (LO_G, HI_G)
+    step = (hi - lo) / (NPTS - 1)
+    words = sample_masks(sc.nunits, p, seed, 3, 0, nmasks)
+    with _lib.options(**(opts or {})):
+        fast, _, st_fast = eval_batch(cell, kp, words, lo, step, NPTS, 0.01)
+        if eigs_too:
+            curves, eigs, status = eval_batch(cell, kp, words, lo, step, NPTS, 0.01, want_eigs=True)
+    assert (st_fast == 0).all()
+    if eigs_too:
+        assert (status == 0).all()
+        np.testing.assert_allclose(fast, curves, rtol=0, atol=1e-11)
+    ocell = O.make_cell(om, nu)
+    for m in check:
+        ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
+        d = ref.shape[1]
+        if eigs_too:
+            assert np.all(np.isnan(eigs[m, :, d:]))
+            err = np.max(np.abs(eigs[m, :, :d] - ref))
+            assert err <= EIG_TOL * (ref.max() - ref.min()), (m, err)
+        rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), lo, hi, NPTS, 0.01, ocell.area)
+        np.testing.assert_allclose(fast[m], rc, rtol=0, atol=IDOS_TOL)
+    return fast
+
+
+# ---- real bulge chase: every warps-per-matrix variant, forced (nu = 16, q = 2: S = 256, real batch) ----------
+@pytest.mark.parametrize("rnw", [1, 2, 4, 8, 16])
+def test_real_chase_warp_variants_forced(rnw):
+    check_batch("graphene", 16, 2, 0.05, 6, 31, (0, 5), opts={"HX_CHASE_RNW": rnw})
+
+
+# ---- the variants the c2 batch sizes select by themselves ----------------------------------------------------
+def test_real_chase_padded_nw4_at_bench_batch():
+    """c2 level 3 / level-4 quarters: 256 masks x 4 k = 1024 N = 512 matrices -> want = 2: the 4-warp chase with
+    padded shared memory (5 CTAs / SM).  8 masks spread over the batch are checked."""
+    check_batch("graphene", 16, 2, 0.05, 256, 2026, (0, 37, 101, 128, 170, 201, 240, 255), eigs_too=False)
+
+
+def test_real_chase_nw1_at_large_batch():
+    """>= 1628 matrices -> want = 1: one warp per matrix (c5 n = 512 batches)."""
+    check_batch("graphene", 16, 2, 0.05, 420, 7, (0, 211, 419), eigs_too=False)
+
+
+def test_c2_level4_parent_batch():
+    """c2 level 4: 64 nu = 32 masks at Gamma (N = 2048, S = 1024) in one batch - the 16-warp real chase."""
+    check_batch("graphene", 32, 1, 0.05, 64, 2026, (0, 33, 63), eigs_too=False)
+
+
+def test_clustered_real_chase_two_sms():
+    """HX_CHASE_RCL = 2 (2 SMs per matrix) on S = 1024 (the default picks it from S >= 2048)."""
+    check_batch("graphene", 32, 1, 0.05, 2, 5, (0, 1), opts={"HX_CHASE_RCL": 2})
+
+
+@pytest.mark.parametrize("rcl", [2, 4])
+def test_clustered_real_chase_nu46(rcl):
+    check_batch("graphene", 46, 1, 0.02, 1, 9, (0,), opts={"HX_CHASE_RCL": rcl})
+
+
+# ---- real / complex storage and arithmetic switches -----------------------------------------------------------
+@pytest.mark.parametrize("opts", [{"HX_NO_REAL": 1}, {"HX_REAL_STAGE1": 0}, {"HX_CHASE_REAL": 0},
+                                  {"HX_CHASE_PAIR": 0}, {"HX_REAL_FUSED": 1}, {"HX_FUSED_UPDATE": 1}])
+@pytest.mark.parametrize("nu,q", [(16, 2), (12, 1), (11, 1)])
+def test_real_path_switches(nu, q, opts):
+    check_batch("graphene", nu, q, 0.1, 4, 13, (0, 3), opts=opts)
+
+
+@pytest.mark.parametrize("opts", [{}, {"HX_BIDIAG_REAL": 0}, {"HX_NO_REAL": 1}, {"HX_NO_BIPARTITE": 1}])
+@pytest.mark.parametrize("nu,q", [(4, 8), (8, 4), (8, 2)])
+def test_shared_memory_tiers_switches(nu, q, opts):
+    """The shared-memory tiers of c1/c2 (N = 32, 128): complex warp / CTA Golub-Kahan, real Golub-Kahan at the
+    TRIM k-points, and the Hermitian (non-bipartite) tier with HX_NO_BIPARTITE."""
+    check_batch("graphene", nu, q, 0.05, 40, 17, (0, 19, 39), opts=opts)
+
+
+# ---- complex bipartite banded tier (non-TRIM k, N > 160) ------------------------------------------------------
+@pytest.mark.parametrize("nu,q", [(10, 3), (11, 4), (12, 3)])
+def test_complex_bipartite_banded_tier(nu, q):
+    check_batch("graphene", nu, q, 0.05, 3, 21, (0, 2))
+
+
+@pytest.mark.parametrize("nu", [16, 32])
+def test_c5_generic_k_point(nu):
+    """c5 sweep: one generic k (reduced q = 3 grid, point 4) per matrix at n = 512 and 2048."""
+    kp = hx.make_bz_grid(hx.GrapheneNNModel().lattice_spec(), nu, 3, "reduced").kpoints[4:5]
+    check_batch("graphene", nu, 1, 0.05, 4 if nu == 32 else 16, 2026, (0, 3), kp=kp)
+
+
+# ---- c3 (11-band table, Hermitian banded tier) at the bench sizes ----------------------------------------------
+def test_c3_table_nu8():
+    check_batch("table", 8, 2, 0.05, 6, 2026, (0, 5))
+
+
+def test_c3_table_nu16():
+    check_batch("table", 16, 1, 0.05, 2, 2026, (0,))
+
+
+# ---- c4 scale: a defected nu = 64 sample at Gamma against zhegv on the N = 8192 pencil -------------------------
+def test_c4_defected_nu64_gamma():
+    check_batch("graphene", 64, 1, 0.02, 1, 2026, (0,))
