@@ -46,13 +46,26 @@ CONFIGS = {
     "c5": ("graphene", [(4, 0), (8, 0), (16, 0), (32, 0)], 0, 0.05, None,
            "batched eigensolve+IDOS sweep n=32/128/512/2048 (graphene-vacancy Bloch matrices, ~50% HBM batches)"),
 }
-FRAC_NOTE = ("achieved/frac use the algorithmic count of SURVEY 8d (16/3 d^3 complex-Hermitian tridiagonalisation flops "
-             "per (sample, k) matrix solved); the graphene tiers solve the bipartite SVD (1/4 of it) and the "
-             "time-reversal-invariant batches (q = 1, 2: the N = 512 / 2048 tiers, and the TRIM k-points of the others) "
-             "run in real arithmetic with real storage (1/4 again), so frac exceeds 1. Executed FP64 per c2 pass (ncu "
-             "DFMA/DMUL/DADD + DMMA counters): 527 GFLOP, 6.2 TF/s over the serialised kernel time, "
-             "profiles/r01_fp64_executed_c2.txt; the dominant tier's rank-32 updates are DRAM-bound (3.7 TB/s), "
-             "traffic below and profiles/r01_traffic_L4_parent.txt")
+FRAC_NOTE = ("frac = EXECUTED FP64 flops / device time / FP64 peak.  Executed flops are ncu instruction counts of the "
+             "same workload and build (DFMA x2 + DMUL + DADD per thread instruction, DMMA m8n8k4 x512 per warp "
+             "instruction; tools/ncu_flops.py over a serialised pass, committed under profiles/) - the bipartite SVD, real "
+             "arithmetic at time-reversal-invariant k and k/-k pairing mean far fewer flops are executed than the "
+             "SURVEY 8(d) count 16/3 d^3 per (sample, k) matrix, which is reported separately as `algorithmic` "
+             "(a rate of the dense complex-Hermitian method, not a hardware fraction).")
+# executed-FP64 profiles (tools/profile_run.py under ncu + tools/ncu_flops.py --json): config -> path
+EXECUTED = {"c2": "profiles/r02_fp64_executed_c2.json", "c3": "profiles/r02_fp64_executed_c3.json",
+            "c4": "profiles/r02_fp64_executed_c4.json", "c1": "profiles/r02_fp64_executed_c1.json"}
+# the dominant tier alone (--levels L --parent-only): (config, N) -> path
+EXECUTED_TIER = {("c2", 2048): "profiles/r02_fp64_executed_c2_L4_parent.json"}
+
+
+def executed_gflop(path):
+    """Executed FP64 GFLOP per pass from a committed ncu summary (None when absent)."""
+    if path is None or not (ROOT / path).exists():
+        return None
+    return json.loads((ROOT / path).read_text())["executed_gflop_per_pass"]
+
+
 # c5 batches: floor(0.5 * 180 GB / (16 n^2)) matrices (SURVEY 8d), one (mask, k) matrix each
 C5_BATCH = {4: 5_490_000, 8: 343_000, 16: 21_500, 32: 1_341}
 SEED = 2026
@@ -174,6 +187,26 @@ def flush_l2(buf):
     buf.add_(1.0)
 
 
+REF_MAX_STEPS = 8
+
+
+def ref_fraction(levels, cores, floor):
+    """Sample fraction of the reference legs: the smallest level gets at least `cores` samples (every worker
+    busy on every level; c2 on 16 cores: 1/4 -> M = 1024/256/64/16), and at least `floor`."""
+    m_min = min(M for _, M in levels)
+    return min(1.0, max(floor, cores / m_min))
+
+
+def host_cpu():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return f"{line.split(':', 1)[1].strip()} x {len(os.sched_getaffinity(0))} threads"
+    except OSError:
+        pass
+    return None
+
+
 # ---------------------------------------------------------------------------------------------------
 def reference_engine_run(kind, levels, nq, p, erange, frac, workers):
     """The reference (baseline/_ref hexmc) on a bounded sample: M_l * frac samples per level."""
@@ -237,7 +270,7 @@ def run_reference_arm(args):
         return 0
     kind, levels, nq, p, erange, desc = CONFIGS[args.config]
     cores = len(os.sched_getaffinity(0))
-    frac = args.ref_fraction
+    frac = ref_fraction(levels, cores, args.ref_fraction)
     if max(nu for nu, _ in levels) >= LARGE_NU:
         nu = levels[-1][0]
         try:
@@ -263,7 +296,7 @@ def run_reference_arm(args):
         for _ in range(max(1, args.warmup)):
             reference_engine_run(kind, levels[:1], nq, p, erange, min(frac, 16 / levels[0][1]), cores)
         step_vals, step_ms, last = [], [], None
-        for _ in range(args.steps):
+        for _ in range(min(args.steps, REF_MAX_STEPS)):
             per = reference_engine_run(kind, levels, nq, p, erange, frac, cores)
             tot_s = sum(x["seconds"] for x in per)
             tot_m = sum(x["M"] for x in per)
@@ -277,10 +310,14 @@ def run_reference_arm(args):
     line = {
         "metric": "IDOS samples/sec per MLMC level (graphene MLMC, BASELINE config 2)" if args.config == "c2"
         else f"IDOS samples/sec ({desc})",
-        "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "value": value, "unit": "samples/s", "n_gpus": world, "steps": len(step_vals), "steps_requested": args.steps,
+        "warmup": args.warmup,
         "ms_per_step": statistics.median(step_ms), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded reference sampler)", "impl": "reference",
-        "config": {"workload": desc, "bz_mode": "reduced", "levels": last, "sample_fraction": frac},
+        "config": {"workload": desc, "bz_mode": "reduced", "levels": last, "sample_fraction": frac,
+                   "host_cpu": host_cpu(), "same_config": frac == 1.0,
+                   "note": f"each step = every level at M_l x {frac:g} (every level >= {cores} samples, so no worker "
+                           f"idles); at most {REF_MAX_STEPS} steps so the run stays within a few minutes"},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "reference",
                          "sample": f"each step = every level with M_l x {frac} samples, reference Engine "
                                    f"workers={cores} (1 BLAS thread each)"},
@@ -444,6 +481,19 @@ def run_c5(args):
     return 0
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` run without torchrun: re-launch this command under torch.distributed.run with N
+    ranks (one process per GPU, NCCL); rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(ROOT / "bench.py")] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -454,7 +504,12 @@ def main():
     ap.add_argument("--ref-fraction", type=float, default=1.0 / 16.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank a full level set of its own replicates (default); strong: one level set, "
+                         "its unique masks split over the ranks by sum d^3, curves all-gathered")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "reference":
         return run_reference_arm(args)
     if args.config == "c5":
@@ -476,7 +531,9 @@ def main():
     kind, levels, nq, p, erange, desc = CONFIGS[args.config]
     lo, hi = grid_range(kind, erange)
     model = make_model(kind)
-    runner = DeviceMlmc(model, nq, DELTA, SEED, lo, hi, NPTS, device=local)
+    mode = "replicas" if args.scaling == "weak" else "split"
+    runner = DeviceMlmc(model, nq, DELTA, SEED, lo, hi, NPTS, device=local,
+                        group=dist.group.WORLD if world > 1 else None, mode=mode)
 
     def barrier():
         if world > 1:
@@ -487,15 +544,13 @@ def main():
     l2 = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
 
     def step():
-        out = runner.run_levels(inputs)
-        if world > 1:
-            for s in out:
-                dist.all_reduce(s)
-        return out
+        return runner.run_levels(inputs)
 
     for _ in range(args.warmup):
-        step()
+        out = step()
     torch.cuda.synchronize(dev)
+    runner.check_status()  # every (mask, k) solve of the timed workload succeeded
+    value_means = [m.cpu().numpy() for m, _ in out]
     launches0 = _lib.kernel_launches()
     times = []
     with ClockSampler(local) as clk:
@@ -538,7 +593,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    total_samples = world * sum(M for _, M in levels)  # weak scaling: every rank runs a full level set
+    # weak: every rank runs a full level set of its own replicates; strong: one level set split over the ranks
+    total_samples = (world if mode == "replicas" else 1) * sum(M for _, M in levels)
     value = total_samples / (ms_per_step * 1e-3)
 
     # per-tier accounting for the roofline (algorithmic 16/3 d^3 per (sample, k) matrix)
@@ -554,16 +610,22 @@ def main():
         t["launches"] += 1
     dom = max(tiers.values(), key=lambda t: t["ms"])
     peak = fp64_peak_live(dev)
-    achieved = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
     level_info = []
     for (nu, M), ms in zip(levels, level_ms):
         level_info.append({"nu": nu, "q": nq // nu, "M": M, "ms": round(float(ms), 3),
                            "samples_per_s": round(M / (ms * 1e-3), 2) if ms > 0 else None})
 
     # e2e through the public Engine API (host buffers, copies inside the timed region)
-    e2e = None
+    e2e, self_check = None, None
     if not args.no_e2e:
-        e2e = run_e2e(hx, model, levels, nq, p, erange, lo, hi, args, rank, world, dev)
+        e2e, e2e_means = run_e2e(hx, model, levels, nq, p, erange, lo, hi, args, rank, world, dev)
+        # the timed device pipeline and the public Engine API must give the same level means (same masks,
+        # same curves, exact moments): bitwise, for any number of ranks
+        diffs = [float(np.max(np.abs(a - b))) for a, b in zip(value_means, e2e_means)]
+        self_check = {"level_means_max_abs_diff_vs_engine": max(diffs),
+                      "bitwise_equal": all(np.array_equal(a, b) for a, b in zip(value_means, e2e_means))}
+        if max(diffs) > 1e-9:
+            raise SystemExit(f"self-check failed: device pipeline vs Engine level means differ by {max(diffs)}")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -574,23 +636,18 @@ def main():
             "metric": "IDOS samples/sec per MLMC level (graphene MLMC, BASELINE config 2)" if args.config == "c2"
             else f"IDOS samples/sec ({desc})",
             "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded reference sampler, bit-exact masks)",
             "config": {"workload": desc, "bz_mode": "reduced (== full to <1e-10, SURVEY finding 3)",
                        "energy_points": NPTS, "delta": DELTA, "master_seed": SEED, "levels": level_info,
-                       "l2": "flushed between timed steps (256 MB write)", "parallelism": f"replicas x{world} (rank r draws replicates [r*M, (r+1)*M) of each level stream; one all-reduce of level sums)",
+                       "l2": "flushed between timed steps (256 MB write)", "parallelism": (f"replicas x{world} (rank r draws replicates [r*M, (r+1)*M) of each level stream; exact fixed-point level sums, int64 all-reduce)" if mode == "replicas" else f"split x{world} (one level set; unique masks of each tier split over the ranks by sum d^3, curves all-gathered)"),
                        "schedule": "all levels and both tiers of each level (parent nu, quarters nu/2) in flight at once on independent streams + contexts; largest tier on a high-priority stream",
                        "levels_note": "per-level ms from a separate sequential analysis pass (the timed step runs them concurrently)"},
-            "roofline": {"bound": "tensor", "kernel": f"batched eigensolve N={dom['N']}", "achieved": achieved,
-                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "traffic": traffic_of(args.config, dom["N"]),
-                         "traffic_source": TRAFFIC.get((args.config, dom["N"]), (None, None))[0],
-                         "peak_source": "live cuBLAS ZGEMM 4096^3 complex128 on this GPU (best of 5)",
-                         "flops_per_launch": dom["flops"] / max(1, dom["launches"]), "note": FRAC_NOTE,
-                         "tiers": sorted(tiers.values(), key=lambda t: -t["ms"])},
+            "roofline": roofline_block(args.config, world, mode, ms_per_step, peak, dom, tiers, apasses),
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,
+            "self_check": self_check,
             "cpu_baseline": cpu,
         }
         print(json.dumps(line))
@@ -599,22 +656,54 @@ def main():
     return 0
 
 
+def roofline_block(config, world, mode, ms_per_step, peak, dom, tiers, apasses):
+    """FP64 roofline of the timed step: executed flops (ncu counts of the same pass) / device time / peak; the
+    dominant tier (largest event time in the sequential analysis pass) likewise; the SURVEY 8(d) algorithmic
+    count reported beside it as a rate, not a fraction."""
+    per_rank_sets = 1 if mode == "replicas" else 1.0 / world  # level sets a rank runs per step
+    exe = executed_gflop(EXECUTED.get(config))
+    achieved = None if exe is None else exe * 1e9 * per_rank_sets / (ms_per_step * 1e-3) / 1e12
+    block = {"bound": "fp64", "kernel": f"batched eigensolve, every hx kernel of one {config} step (all tiers)",
+             "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+             "frac": None if achieved is None else achieved / peak,
+             "executed_gflop_per_step": None if exe is None else exe * per_rank_sets,
+             "executed_source": EXECUTED.get(config),
+             "peak_source": "live cuBLAS ZGEMM 4096^3 complex128 on this GPU (best of 5)", "note": FRAC_NOTE}
+    tier_exe = executed_gflop(EXECUTED_TIER.get((config, dom["N"])))
+    dom_ms = dom["ms"] / max(1, dom["launches"])
+    block["dominant_tier"] = {
+        "N": dom["N"], "ms_per_launch": dom_ms, "matrices_per_launch": dom["matrices"] / max(1, dom["launches"]),
+        "executed_gflop_per_launch": tier_exe, "executed_source": EXECUTED_TIER.get((config, dom["N"])),
+        "achieved_tflops": None if tier_exe is None else tier_exe / dom_ms,
+        "frac": None if tier_exe is None else tier_exe / dom_ms / peak,
+        "traffic": traffic_of(config, dom["N"]), "traffic_source": TRAFFIC.get((config, dom["N"]), (None, None))[0]}
+    block["traffic"] = block["dominant_tier"]["traffic"]
+    alg = sum(t["flops"] for t in tiers.values()) / apasses
+    block["algorithmic"] = {"count": "16/3 d^3 per (sample, k) matrix solved (SURVEY 8d)", "flops_per_step": alg,
+                            "rate_tflops": alg * per_rank_sets / (ms_per_step * 1e-3) / 1e12}
+    block["tiers"] = sorted(tiers.values(), key=lambda t: -t["ms"])
+    return block
+
+
 def run_e2e(hx, model, levels, nq, p, erange, lo, hi, args, rank, world, dev):
+    """Engine.run_mlmc (the public API) with host buffers; returns (e2e dict, level means of the last run)."""
     import torch
     import torch.distributed as dist
 
     plan_levels = levels
+    shard_mode = "replicas" if args.scaling == "weak" else "split"
 
     def one(count_bytes):
         eng = hx.Engine(model, nq=nq, delta=DELTA, master_seed=SEED, bz_mode="reduced", energy_points=NPTS,
-                        energy_range=(lo + 2 * DELTA, hi - 2 * DELTA), device=dev.index, shard=(rank, world))
+                        energy_range=(lo + 2 * DELTA, hi - 2 * DELTA), device=dev.index, shard=(rank, world),
+                        shard_mode=shard_mode)
         plan = hx.LevelPlan(ns=tuple(nu for nu, _ in plan_levels), samples=tuple(M for _, M in plan_levels), nq=nq,
                             p_vac=p, delta=DELTA)
         t0 = time.perf_counter()
-        eng.run_mlmc(plan)
+        _, sets = eng.run_mlmc(plan)
         torch.cuda.synchronize(dev)
         dt = time.perf_counter() - t0
-        return dt, eng.io_bytes
+        return dt, eng.io_bytes, [s.stats.mean for s in sets]
 
     for _ in range(1):
         one(False)
@@ -622,21 +711,21 @@ def run_e2e(hx, model, levels, nq, p, erange, lo, hi, args, rank, world, dev):
     for _ in range(max(1, min(args.steps, 3))):
         if world > 1:
             dist.barrier()
-        dt, io = one(True)
+        dt, io, means = one(True)
         dts.append(dt)
     dt = statistics.median(dts)
     if world > 1:
         t = torch.tensor([dt], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
-    total = world * sum(M for _, M in levels)
+    total = (world if shard_mode == "replicas" else 1) * sum(M for _, M in levels)
     return {"value": total / dt, "unit": "samples/s", "h2d_bytes_per_step": int(io[0]), "d2h_bytes_per_step": int(io[1]),
-            "api": "paper_1611_09784_b200.Engine.run_mlmc (host RNG + dedup per level, every (n, q) tier of every level through hx_eval_idos_batch concurrently)"}
+            "api": f"paper_1611_09784_b200.Engine.run_mlmc (shard_mode={shard_mode}; host RNG + dedup per level, every (n, q) tier of every level through hx_eval_idos_batch concurrently)"}, means
 
 
 def cpu_baseline(kind, levels, nq, p, erange):
     cores = len(os.sched_getaffinity(0))
-    frac = 1.0 / 8.0
+    frac = ref_fraction(levels, cores, 1.0 / 16.0)
     if max(nu for nu, _ in levels) >= LARGE_NU:
         nu = levels[-1][0]
         try:
@@ -655,8 +744,8 @@ def cpu_baseline(kind, levels, nq, p, erange):
     tot_s = sum(x["seconds"] for x in per)
     tot_m = sum(x["M"] for x in per)
     return {"value": tot_m / tot_s, "unit": "samples/s", "cores": cores, "kind": kindname,
-            "sample": f"every level with M_l/8 samples through the reference Engine (workers={cores}, reduced BZ)",
-            "levels": per}
+            "sample": f"every level with M_l x {frac:g} samples through the reference Engine (workers={cores}, reduced "
+                      f"BZ; every level >= {cores} samples)", "host_cpu": host_cpu(), "levels": per}
 
 
 if __name__ == "__main__":

@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define HX_ABI_VERSION 3
+#define HX_ABI_VERSION 4
 
 /* return codes */
 #define HX_OK 0
@@ -167,11 +167,31 @@ int hx_sharp_counts_device(const double* d_energies, const double* d_weights, in
 
 /* ---- MLMC level moments (runner.py:281-299 + mlmc.py:143-154), device pointers ------------- */
 /* term[m] = full[m] - 0.25 * sum_r quarter[m][r] (quarters may be NULL -> no CV);
- * mean = sum_m term / M (row order m = 0..M-1), var = sum (term-mean)^2 / (M-1) (M>1 else NaN).
- * d_terms optional [M * npts].  Also returns sums for cross-device reduction: d_sums[2*npts]
- * = (sum term, sum term^2) in fixed row order. */
+ * mean = sum_m term / M, var = sum (term-mean)^2 / (M-1) (M>1 else NaN) - the two-pass np.var form, with
+ * both sums EXACT (fixed point, see below), so they do not depend on the order or split of the samples.
+ * d_terms optional [M * npts]; d_mean / d_var optional [npts]. */
 int hx_level_moments_device(const double* d_full, const double* d_quarters, int64_t M, int32_t npts,
-                            double* d_terms, double* d_mean, double* d_var, double* d_sums, void* stream);
+                            double* d_terms, double* d_mean, double* d_var, void* stream);
+
+/* Exact fixed-point level sums for multi-device / multi-rank levels (north_star (4)).
+ * Every term is converted on its own to a fixed-point integer of HX_FX_LIMBS signed 32-bit limbs (held in
+ * int64, HX_FX_FRAC fraction bits; |term| < 2^(32*HX_FX_LIMBS - HX_FX_FRAC - 1)) and the limbs are summed
+ * as integers, so partial limbs of any split of the samples add (an int64 all-reduce, ncclInt64) to the
+ * bits of the single-device sum.  d_limbs [npts * HX_FX_LIMBS] (overwritten):
+ *   d_center == NULL : sum_m term_m          (pass 1; mean = finalize(sum, M_total))
+ *   d_center != NULL : sum_m (term_m - center)^2  (pass 2 with the global mean; var = finalize(sum, M_total-1))
+ * hx_level_moments_device computes its mean / var through the same functions, so one device and G devices
+ * agree bitwise. */
+#define HX_FX_LIMBS 6
+#define HX_FX_FRAC 112
+int hx_level_sums_fixed_device(const double* d_full, const double* d_quarters, int64_t M, int32_t npts,
+                               const double* d_center, int64_t* d_limbs, void* stream);
+/* out[m] = value(limbs[m]) / divisor (divisor <= 0 -> NaN). */
+int hx_fixed_finalize_device(const int64_t* d_limbs, int32_t npts, double divisor, double* d_out, void* stream);
+/* Host-pointer twins (same arithmetic, bitwise equal to the device ones); used by the CPU multi-rank tests. */
+int hx_level_sums_fixed(const double* full, const double* quarters, int64_t M, int32_t npts, const double* center,
+                        int64_t* limbs);
+int hx_fixed_finalize(const int64_t* limbs, int32_t npts, double divisor, double* out);
 
 /* ---- disorder sampling (disorder.py:57-94), host C, bit-exact with numpy ---------------------- */
 /* SeedSequence(seed, spawn_key=(level, rep0 + i)) -> PCG64 -> random(nunits) < p, for i < count.

@@ -29,7 +29,10 @@ EXPORTED = (
     "hx_sharp_counts_device", "hx_level_moments_device", "hx_sample_masks", "hx_sample_masks_device",
     "hx_uniforms", "hx_restrict_masks", "hx_assemble_device", "hx_restrict_masks_device",
     "hx_kernel_launches", "hx_set_option", "hx_clear_option", "hx_get_option",
+    "hx_level_sums_fixed_device", "hx_fixed_finalize_device", "hx_level_sums_fixed", "hx_fixed_finalize",
 )
+
+HX_FX_LIMBS = 6  # include/hx.h: fixed-point limbs per grid point of the exact level sums
 
 
 class HxError(RuntimeError):
@@ -87,7 +90,11 @@ def load():
             "hx_eigvalsh_batch_device": (C.c_int, [vp, i32, i64, vp, vp, vp, vp, vp]),
             "hx_smoothed_counts_device": (C.c_int, [vp, vp, i64, C.POINTER(EGrid), vp, vp]),
             "hx_sharp_counts_device": (C.c_int, [vp, vp, i64, C.POINTER(EGrid), vp, vp]),
-            "hx_level_moments_device": (C.c_int, [vp, vp, i64, i32, vp, vp, vp, vp, vp]),
+            "hx_level_moments_device": (C.c_int, [vp, vp, i64, i32, vp, vp, vp, vp]),
+            "hx_level_sums_fixed_device": (C.c_int, [vp, vp, i64, i32, vp, vp, vp]),
+            "hx_fixed_finalize_device": (C.c_int, [vp, i32, dbl, vp, vp]),
+            "hx_level_sums_fixed": (C.c_int, [vp, vp, i64, i32, vp, vp]),
+            "hx_fixed_finalize": (C.c_int, [vp, i32, dbl, vp]),
             "hx_sample_masks": (C.c_int, [u64, u64, u64, i64, dbl, i32, vp, i32]),
             "hx_sample_masks_device": (C.c_int, [u64, u64, u64, i64, dbl, i32, vp, vp]),
             "hx_uniforms": (C.c_int, [u64, u64, u64, i64, vp]),
@@ -138,6 +145,27 @@ def restrict_masks(parent_words: np.ndarray, parent_units: int, assign: np.ndarr
     m = np.ascontiguousarray(umap, dtype=np.int32)
     check(load().hx_restrict_masks(ptr(parent_words), n, parent_units, ptr(a), ptr(m), sub_units, ptr(out)),
           "hx_restrict_masks")
+    return out
+
+
+def fixed_sums(full: np.ndarray, quarters: np.ndarray | None = None, center: np.ndarray | None = None) -> np.ndarray:
+    """Exact fixed-point limbs [npts, HX_FX_LIMBS] of sum_m term_m (center None) or sum_m (term_m - center)^2,
+    term = full - 0.25 * sum_r quarters[:, r] (hx_level_sums_fixed, host twin of the device kernel)."""
+    full = np.ascontiguousarray(full, dtype=np.float64)
+    M, npts = full.shape
+    q = None if quarters is None else np.ascontiguousarray(quarters, dtype=np.float64).reshape(M, 4, npts)
+    c = None if center is None else np.ascontiguousarray(center, dtype=np.float64).reshape(npts)
+    out = np.zeros((npts, HX_FX_LIMBS), dtype=np.int64)
+    check(load().hx_level_sums_fixed(ptr(full), ptr(q) if q is not None else 0, M, npts,
+                                     ptr(c) if c is not None else 0, ptr(out)), "hx_level_sums_fixed")
+    return out
+
+
+def fixed_finalize(limbs: np.ndarray, divisor: float) -> np.ndarray:
+    """value(limbs) / divisor per grid point (NaN for divisor <= 0)."""
+    limbs = np.ascontiguousarray(limbs, dtype=np.int64).reshape(-1, HX_FX_LIMBS)
+    out = np.empty(limbs.shape[0])
+    check(load().hx_fixed_finalize(ptr(limbs), limbs.shape[0], float(divisor), ptr(out)), "hx_fixed_finalize")
     return out
 
 

@@ -19,6 +19,7 @@
 #include "hx_dense.cuh"
 #include "hx_kernels.cuh"
 #include "hx_rng.cuh"
+#include "hx_fixed.cuh"
 
 #include <atomic>
 
@@ -782,68 +783,121 @@ __global__ void counts_kernel(const double* E, const double* w, int64_t count, G
   }
 }
 
-// term = full - 0.25 * sum_r quarter_r ; mean / var in fixed sample order (mlmc.py:143-154)
 // CV terms and level moments per grid point (runner.py:281-299, mlmc.py:143-154).  Block = 32 grid points x
-// 8 sample groups (sample i in group i % 8); the group partials are combined in a fixed order, so results
-// do not depend on scheduling.  Two passes (mean, then the centred sum of squares).
+// 8 sample groups (sample i in group i % 8).  Mean and variance come from exact fixed-point sums (hx_fixed.cuh):
+// sum_i term_i, then sum_i (term_i - mean)^2 (two passes, the np.var form), each an integer sum of per-term
+// fixed-point values, so the results do not depend on scheduling, on the batch split or on the number of
+// devices the samples were spread over (hx_level_sums_fixed_device + an int64 all-reduce gives the same bits).
 constexpr int MOM_P = 32, MOM_G = 8;
-__device__ __forceinline__ double cv_term(const double* full, const double* quarters, int64_t i, int npts, int m) {
+__host__ __device__ __forceinline__ double cv_term(const double* full, const double* quarters, int64_t i, int npts,
+                                                   int m) {
   double t = full[i * npts + m];
   if (quarters) {
+    // cv = ((q1 + q2) + q3 + q4) * 0.25, term = full - cv: the reference's order (runner.py:289-297)
     const double* q = quarters + i * 4 * npts + m;
-    double cv = 0.0;
-    cv = __dadd_rn(cv, q[0]);
-    cv = __dadd_rn(cv, q[npts]);
-    cv = __dadd_rn(cv, q[2 * npts]);
-    cv = __dadd_rn(cv, q[3 * npts]);
+#ifdef __CUDA_ARCH__
+    double cv = __dadd_rn(__dadd_rn(__dadd_rn(q[0], q[npts]), q[2 * npts]), q[3 * npts]);
     t = __dsub_rn(t, __dmul_rn(cv, 0.25));
+#else
+    volatile double cv = ((q[0] + q[npts]) + q[2 * npts]) + q[3 * npts];
+    volatile double c4 = cv * 0.25;
+    t = t - c4;
+#endif
   }
   return t;
 }
 
+__host__ __device__ __forceinline__ double fx_sq_dev(double t, double mu) {
+#ifdef __CUDA_ARCH__
+  const double d = __dsub_rn(t, mu);
+  return __dmul_rn(d, d);
+#else
+  volatile double d = t - mu;
+  volatile double d2 = d * d;
+  return d2;
+#endif
+}
+
+__device__ __forceinline__ double fx_nan() { return __longlong_as_double(0x7ff8000000000000ll); }
+
+// Block-wide exact sum of the per-thread limbs of grid point `pl`: group 0's threads get the total.
+__device__ __forceinline__ void fx_block_sum(int64_t (*sh)[FX_NL][MOM_P], const int64_t* L, int grp, int pl,
+                                             int64_t* out) {
+#pragma unroll
+  for (int j = 0; j < FX_NL; ++j) sh[grp][j][pl] = L[j];
+  __syncthreads();
+  if (grp == 0) {
+#pragma unroll
+    for (int j = 0; j < FX_NL; ++j) {
+      int64_t a = 0;
+      for (int q = 0; q < MOM_G; ++q) a += sh[q][j][pl];
+      out[j] = a;
+    }
+  }
+  __syncthreads();
+}
+
+// mode 0: terms, mean, var (single device).  mode 1: limbs of sum term.  mode 2: limbs of sum (term - center)^2.
+// bad[m] is raised for non-finite terms (they are left out of the sums).
 __global__ void __launch_bounds__(MOM_P * MOM_G) moments_kernel(const double* full, const double* quarters, int64_t M,
                                                                 int npts, double* terms, double* mean, double* var,
-                                                                double* sums) {
-  __shared__ double ps[MOM_G][MOM_P], ps2[MOM_G][MOM_P];
+                                                                int64_t* limbs, const double* center, int mode,
+                                                                int* bad) {
+  __shared__ int64_t sh[MOM_G][FX_NL][MOM_P];
+  __shared__ double smu[MOM_P];
+  __shared__ int sbad[MOM_P];
   const int pl = threadIdx.x % MOM_P, grp = threadIdx.x / MOM_P;
   const int m = blockIdx.x * MOM_P + pl;
   const bool on = m < npts;
-  double s = 0.0, s2 = 0.0;
-  if (on)
+  int64_t L[FX_NL], T[FX_NL];
+#pragma unroll
+  for (int j = 0; j < FX_NL; ++j) L[j] = 0;
+  bool ok = true;
+  if (grp == 0) sbad[pl] = 0;
+  __syncthreads();
+  if (on && mode != 2)
     for (int64_t i = grp; i < M; i += MOM_G) {
       const double t = cv_term(full, quarters, i, npts, m);
       if (terms) terms[i * npts + m] = t;
-      s = __dadd_rn(s, t);
-      s2 = __fma_rn(t, t, s2);
+      ok &= fx_add(L, t);
     }
-  ps[grp][pl] = s;
-  ps2[grp][pl] = s2;
-  __syncthreads();
-  double st = 0.0, st2 = 0.0;
-  for (int q = 0; q < MOM_G; ++q) {
-    st = __dadd_rn(st, ps[q][pl]);
-    st2 = __dadd_rn(st2, ps2[q][pl]);
+  if (mode == 1) {
+    fx_block_sum(sh, L, grp, pl, T);
+    if (grp == 0 && on)
+      for (int j = 0; j < FX_NL; ++j) limbs[(int64_t)m * FX_NL + j] = T[j];
+    if (!ok && bad) atomicOr(bad, 1);
+    return;
   }
-  const double mu = __ddiv_rn(st, (double)M);
-  double acc = 0.0;
+  double mu = 0.0;
+  if (mode == 0) {
+    fx_block_sum(sh, L, grp, pl, T);
+    if (grp == 0) smu[pl] = fx_to_double(T) / (double)M;
+    __syncthreads();
+    mu = smu[pl];
+  } else if (on) {
+    mu = center[m];
+  }
+#pragma unroll
+  for (int j = 0; j < FX_NL; ++j) L[j] = 0;
   if (on)
-    for (int64_t i = grp; i < M; i += MOM_G) {
-      const double dlt = __dsub_rn(cv_term(full, quarters, i, npts, m), mu);
-      acc = __fma_rn(dlt, dlt, acc);
-    }
-  __syncthreads();
-  ps[grp][pl] = acc;
-  __syncthreads();
-  if (grp == 0 && on) {
-    double a = 0.0;
-    for (int q = 0; q < MOM_G; ++q) a = __dadd_rn(a, ps[q][pl]);
-    if (mean) mean[m] = mu;
-    if (var) var[m] = M > 1 ? __ddiv_rn(a, (double)(M - 1)) : __longlong_as_double(0x7ff8000000000000ll);
-    if (sums) {
-      sums[m] = st;
-      sums[npts + m] = st2;
-    }
+    for (int64_t i = grp; i < M; i += MOM_G) ok &= fx_add(L, fx_sq_dev(cv_term(full, quarters, i, npts, m), mu));
+  if (!ok) sbad[pl] = 1;
+  fx_block_sum(sh, L, grp, pl, T);
+  if (!ok && bad) atomicOr(bad, 1);
+  if (grp != 0 || !on) return;
+  ok = !sbad[pl];
+  if (mode == 2) {
+    for (int j = 0; j < FX_NL; ++j) limbs[(int64_t)m * FX_NL + j] = T[j];
+    return;
   }
+  if (mean) mean[m] = ok ? mu : fx_nan();
+  if (var) var[m] = (M > 1 && ok) ? fx_to_double(T) / (double)(M - 1) : fx_nan();
+}
+
+__global__ void fixed_finalize_kernel(const int64_t* limbs, int npts, double divisor, double* out) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= npts) return;
+  out[m] = divisor > 0.0 ? fx_to_double(limbs + (int64_t)m * FX_NL) / divisor : fx_nan();
 }
 
 __global__ void sample_masks_kernel(uint64_t seed, uint64_t level, uint64_t rep0, int64_t count, double p, int nunits,
@@ -924,12 +978,58 @@ int hx_sharp_counts_device(const double* d_energies, const double* d_weights, in
 }
 
 int hx_level_moments_device(const double* d_full, const double* d_quarters, int64_t M, int32_t npts, double* d_terms,
-                            double* d_mean, double* d_var, double* d_sums, void* stream) {
+                            double* d_mean, double* d_var, void* stream) {
   if (!d_full || M < 1 || npts < 1) return fail(HX_E_ARG, "level_moments: bad args");
-  hx::moments_kernel<<<(npts + hx::MOM_P - 1) / hx::MOM_P, hx::MOM_P * hx::MOM_G, 0, static_cast<cudaStream_t>(stream)>>>(d_full, d_quarters, M, npts,
-                                                                                       d_terms, d_mean, d_var, d_sums);
+  hx::moments_kernel<<<(npts + hx::MOM_P - 1) / hx::MOM_P, hx::MOM_P * hx::MOM_G, 0, static_cast<cudaStream_t>(stream)>>>(
+      d_full, d_quarters, M, npts, d_terms, d_mean, d_var, nullptr, nullptr, 0, nullptr);
   HX_CUDA(cudaGetLastError());
-    hx::count_launch();
+  hx::count_launch();
+  return 0;
+}
+
+int hx_level_sums_fixed_device(const double* d_full, const double* d_quarters, int64_t M, int32_t npts,
+                               const double* d_center, int64_t* d_limbs, void* stream) {
+  if (!d_full || M < 0 || npts < 1 || !d_limbs) return fail(HX_E_ARG, "level_sums_fixed_device: bad args");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (M == 0) {
+    HX_CUDA(cudaMemsetAsync(d_limbs, 0, (size_t)npts * HX_FX_LIMBS * 8, st));
+    return 0;
+  }
+  hx::moments_kernel<<<(npts + hx::MOM_P - 1) / hx::MOM_P, hx::MOM_P * hx::MOM_G, 0, st>>>(
+      d_full, d_quarters, M, npts, nullptr, nullptr, nullptr, d_limbs, d_center, d_center ? 2 : 1, nullptr);
+  HX_CUDA(cudaGetLastError());
+  hx::count_launch();
+  return 0;
+}
+
+int hx_fixed_finalize_device(const int64_t* d_limbs, int32_t npts, double divisor, double* d_out, void* stream) {
+  if (!d_limbs || !d_out || npts < 1) return fail(HX_E_ARG, "fixed_finalize_device: bad args");
+  hx::fixed_finalize_kernel<<<(npts + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(d_limbs, npts, divisor,
+                                                                                            d_out);
+  HX_CUDA(cudaGetLastError());
+  hx::count_launch();
+  return 0;
+}
+
+int hx_level_sums_fixed(const double* full, const double* quarters, int64_t M, int32_t npts, const double* center,
+                        int64_t* limbs) {
+  if (!full || M < 0 || npts < 1 || !limbs) return fail(HX_E_ARG, "level_sums_fixed: bad args");
+  for (int m = 0; m < npts; ++m) {
+    int64_t* L = limbs + (int64_t)m * HX_FX_LIMBS;
+    for (int j = 0; j < HX_FX_LIMBS; ++j) L[j] = 0;
+    for (int64_t i = 0; i < M; ++i) {
+      const double t = hx::cv_term(full, quarters, i, npts, m);
+      if (!hx::fx_add(L, center ? hx::fx_sq_dev(t, center[m]) : t))
+        return fail(HX_E_RANGE, "level_sums_fixed: non-finite or out-of-range term");
+    }
+  }
+  return 0;
+}
+
+int hx_fixed_finalize(const int64_t* limbs, int32_t npts, double divisor, double* out) {
+  if (!limbs || !out || npts < 0) return fail(HX_E_ARG, "fixed_finalize: bad args");
+  for (int m = 0; m < npts; ++m)
+    out[m] = divisor > 0.0 ? hx::fx_to_double(limbs + (int64_t)m * HX_FX_LIMBS) / divisor : NAN;
   return 0;
 }
 

@@ -2,7 +2,7 @@
 // vacancy sampler (disorder.py:66-68, :79).  Third-party algorithm (numpy 2.3.5, not vendored in the
 // reference): SeedSequence pool mixing (pool size 4, hashmix/mix constants), generate_state(4, uint64),
 // PCG64 "setseq" seeding (state = 0; step; state += initstate; step), XSL-RR 128/64 output after each
-// step, random() = (next64 >> 11) * 2^-53.  Pinned against numpy in tests/test_boundary.py (rng draws, masks) and tests/test_device_pass_gpu.py (device sampler).
+// step, random() = (next64 >> 11) * 2^-53.  Pinned against numpy in tests/test_boundary.py (rng draws, masks) and tests/test_device_pipeline_gpu.py (device sampler).
 #pragma once
 #include <stdint.h>
 

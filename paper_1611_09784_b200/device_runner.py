@@ -1,11 +1,19 @@
 """Device-resident MLMC level pipeline (no host round trips): the throughput path used by bench.py.
 
-Per level: vacancy masks (device RNG, bit-exact with the reference sampler) -> quarter restriction
-(device) -> in-level dedup of (n, q, mask) keys (sort-unique on the device, the reference's
-evaluate_masks semantics within the level) -> one hx_eval_idos_batch_device per (n, q) tier ->
-gather per-request curves -> CV terms + moments (hx_level_moments_device).  Multi-rank: samples of
-each level are sharded contiguously across ranks; per-rank sums (sum term, sum term^2) are combined
-with one all-reduce per level (runner.py:281-299 + mlmc.py:143-154 semantics for the mean).
+Per level: vacancy masks (device RNG, bit-exact with the reference sampler, disorder.py:57-81) -> quarter
+restriction (device, disorder.py:84-94) -> dedup of (n, q, mask) keys within the level (sort-unique on the
+device: the reference's evaluate_masks semantics within the level, runner.py:206-244) -> one
+hx_eval_idos_batch_device per (n, q) tier -> gather per-request curves -> CV terms + EXACT level moments
+(fixed-point sums, hx_level_sums_fixed_device; runner.py:281-299, mlmc.py:143-154).
+
+Multi-rank, two modes:
+  replicas (weak scaling, bench default): rank r draws the replicates [r*M, (r+1)*M) of every level stream;
+     the fixed-point limbs of the level sums are all-reduced (int64), so the level mean / variance are the
+     bits of one device running all world*M replicates.
+  split (strong scaling): every rank draws the whole level (cheap), dedups it identically, solves a
+     contiguous slice of the unique masks balanced by sum d^3 (d = kept dimension), and the slices' curves
+     are all-gathered; the moments are then the bits of the single-device run (and cache semantics are the
+     single-device ones).
 """
 
 from __future__ import annotations
@@ -19,6 +27,7 @@ import torch
 from . import _lib
 from .geometry import build_supercell, partition_quarters
 from .models import compile_cell
+from .estimators import exact_level_moments
 from .solver import make_bz_grid, time_reversal_reduce, use_time_reversal
 
 
@@ -36,8 +45,13 @@ class LevelInputs:
 
 class DeviceMlmc:
     def __init__(self, model, nq: int, delta: float, master_seed: int, lo: float, hi: float, npts: int,
-                 device: int = 0):
+                 device: int = 0, group=None, mode: str = "replicas"):
+        if mode not in ("replicas", "split"):
+            raise ValueError(f"unknown multi-rank mode {mode!r}")
         self.model = model
+        self.mode = mode
+        self.group = group  # torch.distributed process group (None: single rank)
+        self.statuses = []  # per-solve status tensors of the last run (check_status)
         self.nq = nq
         self.delta = delta
         self.seed = master_seed
@@ -96,8 +110,9 @@ class DeviceMlmc:
     def prepare(self, level, n, M_total, p, with_cv, rank=0, world=1) -> LevelInputs:
         """Masks for this rank's replicates [rank*M, (rank+1)*M) (device RNG) + quarter masks.
 
-        Weak scaling: every rank processes a full level of M samples from its own replicate range."""
-        m0 = rank * M_total
+        replicas: every rank processes a full level of M samples from its own replicate range (weak scaling).
+        split: every rank draws the whole level [0, M); the unique masks are split in run_levels."""
+        m0 = rank * M_total if self.mode == "replicas" else 0
         M = M_total
         cell = self.cell(n)
         nunits = cell.supercell.nunits
@@ -117,11 +132,6 @@ class DeviceMlmc:
                        "hx_restrict_masks_device")
         return LevelInputs(level, n, self.q_of(n), M, m0, with_cv, parent[:M], None if quarters is None else
                            quarters[:4 * M])
-
-    def _eval(self, n, words: torch.Tensor):
-        """Dedup rows, solve unique masks, return per-row curves [rows, npts] (device)."""
-        uniq, inv = torch.unique(words, dim=0, return_inverse=True)
-        return self._solve(n, uniq.contiguous(), self.ctx, self.stream)[0][inv]
 
     def _solve(self, n, uniq: torch.Tensor, ctx, stream):
         """Curves [U, npts] of the unique masks `uniq`, enqueued on `stream` with context `ctx`.  The
@@ -156,75 +166,125 @@ class DeviceMlmc:
                                  "uniq": uniq, "cell": cell})
         return curves, status
 
+    def _world(self):
+        if self.group is None:
+            return 0, 1
+        import torch.distributed as dist
+
+        return dist.get_rank(self.group), dist.get_world_size(self.group)
+
+    def _allreduce(self):
+        if self.group is None or self.mode != "replicas":
+            return None
+        import torch.distributed as dist
+
+        return lambda t: dist.all_reduce(t, group=self.group)
+
+    def _split(self, n, uniq):
+        """split mode: [start, stop) of this rank's contiguous slice of the unique masks, balanced by d^3, and
+        the cut points of every rank (all ranks compute the same cuts)."""
+        rank, world = self._world()
+        U = uniq.shape[0]
+        if world == 1 or U == 0:
+            return 0, U, [0, U]
+        d = kept_dims_device(self.cell(n), uniq).to(torch.float64)
+        c = torch.cumsum(d * d * d, 0)
+        targets = c[-1] * torch.arange(1, world, dtype=torch.float64, device=self.dev) / world
+        cuts = [0] + torch.searchsorted(c, targets).add_(1).clamp_(max=U).tolist() + [U]
+        for i in range(1, len(cuts)):
+            cuts[i] = max(cuts[i], cuts[i - 1])
+        return cuts[rank], cuts[rank + 1], cuts
+
+    def _gather(self, curves, cuts):
+        """split mode: all ranks' slices of the unique curves, in unique order."""
+        import torch.distributed as dist
+
+        rank, world = self._world()
+        if world == 1:
+            return curves
+        width = max(b - a for a, b in zip(cuts[:-1], cuts[1:]))
+        pad = torch.zeros((width, self.npts), dtype=torch.float64, device=self.dev)
+        pad[: curves.shape[0]] = curves
+        out = torch.empty((world * width, self.npts), dtype=torch.float64, device=self.dev)
+        dist.all_gather_into_tensor(out, pad, group=self.group)
+        return torch.cat([out[r * width: r * width + (cuts[r + 1] - cuts[r])] for r in range(world)])
+
     def run_level(self, inp: LevelInputs):
-        """Returns device tensors (sum term [npts], sum term^2 [npts]) for this rank's shard."""
-        npts = self.npts
-        sums = torch.zeros(2 * npts, dtype=torch.float64, device=self.dev)
-        if inp.M == 0:
-            return sums
-        full = self._eval(inp.n, inp.parent)
-        quarters = None
-        if inp.with_cv:
-            quarters = self._eval(inp.n // 2, inp.quarters).reshape(inp.M, 4, npts)
-        _lib.check(self.lib.hx_level_moments_device(full.data_ptr(), 0 if quarters is None else quarters.data_ptr(),
-                                                    inp.M, npts, 0, 0, 0, sums.data_ptr(), self.stream.cuda_stream),
-                   "hx_level_moments_device")
-        return sums
+        """(mean [npts], var [npts]) device tensors of one level, tiers one after another on the main stream."""
+        return self.run_levels([inp], concurrent=False)[0]
 
-
-    def run_levels(self, inputs):
+    def run_levels(self, inputs, concurrent: bool = True):
         """All levels at once: every (level, fine / coarse) solve on its own stream and context, so the
         latency-bound tails of one tier (e.g. the nu = 32 bulge chase on 64 matrices) overlap with the
-        others.  Same results as run_level per input (each solve is deterministic); returns the list of
-        per-level sums on the current stream."""
+        others.  Each solve is deterministic, so the results do not depend on the schedule.  Returns the
+        per-level (mean, var) on the current stream (exact fixed-point moments, combined over the ranks)."""
         main = self.stream
-        jobs = []  # (input index, n, uniq, inv)
+        jobs = []  # (input index, n, uniq slice of this rank, inv, cuts)
         for i, inp in enumerate(inputs):
             if inp.M == 0:
                 continue
-            u, inv = torch.unique(inp.parent, dim=0, return_inverse=True)
-            jobs.append((i, inp.n, u.contiguous(), inv))
-            if inp.with_cv:
-                u, inv = torch.unique(inp.quarters, dim=0, return_inverse=True)
-                jobs.append((i, inp.n // 2, u.contiguous(), inv))
+            for n, words in ((inp.n, inp.parent), (inp.n // 2, inp.quarters)):
+                if words is None:
+                    continue
+                u, inv = torch.unique(words, dim=0, return_inverse=True)
+                a, b, cuts = (0, u.shape[0], None) if self.mode == "replicas" else self._split(n, u)
+                jobs.append((i, n, u[a:b].contiguous(), inv, cuts))
         start = torch.cuda.Event()
         start.record(main)
         outs = [None] * len(jobs)
+        self.statuses = []
         # largest tier first (lane 0 = high priority)
         order = sorted(range(len(jobs)), key=lambda j: -self.cell(jobs[j][1]).dim)
         for lane, j in enumerate(order):
-            i, n, uniq, inv = jobs[j]
-            ctx, stream = self._lane(lane)
+            _, n, uniq, _, _ = jobs[j]
+            ctx, stream = self._lane(lane) if concurrent else (self.ctx, main)
             stream.wait_event(start)
             curves, status = self._solve(n, uniq, ctx, stream)
             done = torch.cuda.Event()
             done.record(stream)
-            outs[j] = (curves, done, status)
+            outs[j] = (curves, done)
+            self.statuses.append(status)
+        for _, done in outs:  # every lane joins the main stream before its outputs are used or released
+            main.wait_event(done)
+        allreduce = self._allreduce()
         res = []
         k = 0
         for inp in inputs:
-            sums = torch.zeros(2 * self.npts, dtype=torch.float64, device=self.dev)
             if inp.M == 0:
-                res.append(sums)
+                z = torch.zeros(self.npts, dtype=torch.float64, device=self.dev)
+                res.append((z, torch.full_like(z, float("nan"))))
                 continue
-            curves, done, _ = outs[k]
-            main.wait_event(done)
-            full = curves[jobs[k][3]]
-            k += 1
-            quarters = None
-            if inp.with_cv:
-                curves, done, _ = outs[k]
-                main.wait_event(done)
-                quarters = curves[jobs[k][3]].reshape(inp.M, 4, self.npts)
+            parts = []
+            for _ in range(2 if inp.with_cv else 1):
+                curves = outs[k][0]
+                if jobs[k][4] is not None:
+                    curves = self._gather(curves, jobs[k][4])
+                parts.append(curves[jobs[k][3]])
                 k += 1
-            _lib.check(self.lib.hx_level_moments_device(full.data_ptr(),
-                                                        0 if quarters is None else quarters.data_ptr(), inp.M,
-                                                        self.npts, 0, 0, 0, sums.data_ptr(), main.cuda_stream),
-                       "hx_level_moments_device")
-            res.append(sums)
-        for _, done, _ in outs:  # every lane joins the main stream before its outputs can be released
-            main.wait_event(done)
+            full = parts[0]
+            quarters = parts[1].reshape(inp.M, 4, self.npts) if inp.with_cv else None
+            _, world = self._world()
+            m_total = inp.M * world if self.mode == "replicas" else inp.M
+            res.append(exact_level_moments(full, quarters, m_total, allreduce))
         return res
+
+    def check_status(self):
+        """Raise if any (mask, k) solve of the last run reported a failure (HX_ST_NOT_PD / NONFINITE); the
+        all-vacant HX_ST_EMPTY is a valid zero curve (runner.py:122-125)."""
+        for st in self.statuses:
+            bad = ((st != _lib.HX_ST_OK) & (st != _lib.HX_ST_EMPTY)).sum().item()
+            if bad:
+                raise RuntimeError(f"{bad} (mask, k) solves failed in the device pipeline")
+
+
+def kept_dims_device(cell, uniq_words: torch.Tensor) -> torch.Tensor:
+    """Kept dimension d of each mask row, on the device (int64 [rows])."""
+    nunits = cell.supercell.nunits
+    w = uniq_words.shape[1]
+    shifts = torch.arange(64, dtype=torch.int64, device=uniq_words.device)
+    bits = ((uniq_words.unsqueeze(-1) >> shifts) & 1).reshape(uniq_words.shape[0], 64 * w)[:, :nunits]
+    per_unit = torch.tensor([len(d) for d in cell.unit_dofs], dtype=torch.int64, device=uniq_words.device)
+    return cell.dim - (bits * per_unit).sum(1)
 
 
 def kept_dims(cell, uniq_words: torch.Tensor) -> np.ndarray:

@@ -10,7 +10,21 @@ IDOS accumulation), so curves are identical for any grouping of requests.
 BZ mode "full" is evaluated on its q^2 base points with weights 1/q^2: the two rotated rhombi are
 periodic images of the base grid point for point (spectrum.py:8-14), so the quadrature is the same and
 curves agree with the reference's full mode to rounding (SURVEY finding 3; pinned by
-tests/test_engine_gpu.py against the reference's full-mode fixtures).
+tests/test_fx_gpu.py against the reference's full-mode fixtures).
+
+Several GPUs, results bitwise identical to one GPU (the reference's "identical for any worker
+count", /root/reference/pkg/tests/test_runner.py:39-43):
+  Engine(devices=G)          one process, the new unique masks of every (n, q) group split over G devices in
+                             contiguous slices balanced by sum d^3 (d = kept dimension); cache semantics and
+                             cache_hits are the single-device ones (the dedup is unchanged).
+  Engine(shard=(rank, world)) one process per GPU under torch.distributed: rank r draws the replicates
+                             [r*M, (r+1)*M) of each level stream and the level moments are combined exactly
+                             (fixed-point limbs, int64 all-reduce): the mean / variance bits of one process
+                             drawing world*M replicates.  cache_hits are per rank.
+  Engine(shard=(rank, world), shard_mode="split")  one process per GPU, strong scaling: every rank draws the
+                             whole level, dedups it identically and solves its d^3-balanced slice of each
+                             group's new masks; the slices' curves are all-gathered, so every rank holds the
+                             single-process results (curves, moments and cache_hits bit for bit).
 """
 
 from __future__ import annotations
@@ -18,6 +32,7 @@ from __future__ import annotations
 import functools
 import math
 import os
+import threading
 import time
 from concurrent.futures import FIRST_COMPLETED, ThreadPoolExecutor, wait
 from dataclasses import dataclass, field
@@ -25,7 +40,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .estimators import LevelPlan, LevelStats, MlmcEstimate, combine_levels, level_moments
+from .estimators import LevelPlan, LevelStats, MlmcEstimate, combine_levels, exact_level_moments, level_moments
 from .geometry import build_supercell, partition_quarters
 from .idos import EnergyGrid
 from .models import compile_cell
@@ -114,7 +129,7 @@ class Engine:
 
     def __init__(self, model, nq: int, delta: float, master_seed: int, workers: int = 1, bz_mode: str = "full",
                  energy_points: int = 4096, energy_range=None, dedup: bool = True, device: int = 0,
-                 shard=(0, 1)):
+                 shard=(0, 1), devices=1, shard_mode: str = "replicas"):
         self.model = model
         self.nq = nq
         self.delta = delta
@@ -124,8 +139,19 @@ class Engine:
         self.dedup = dedup
         self.device = device
         self.shard = shard  # (rank, world): rank r draws replicates [r*M, (r+1)*M) (weak-scaling replicas)
+        if isinstance(devices, int):
+            if devices < 1:
+                raise ValueError("devices must be >= 1")
+            devices = [device + g for g in range(devices)]
+        if shard_mode not in ("replicas", "split"):
+            raise ValueError(f"unknown shard mode {shard_mode!r}")
+        self.shard_mode = shard_mode
+        self.devices = list(devices)  # GPUs the new masks of a group are split over (int G: device .. device+G-1)
         self.io_bytes = [0, 0]  # host->device, device->host bytes moved by the batch calls
         self._cache: dict = {}
+        self._coll = threading.Condition()  # split mode: all-gathers in submission order on every rank
+        self._coll_turn = 0
+        self._coll_tickets = 0
         self._supercells: dict = {}
         self._cells: dict = {}
         self._kgrids: dict = {}
@@ -143,20 +169,21 @@ class Engine:
             self._supercells[n] = build_supercell(self.model.lattice_spec(), n)
         return self._supercells[n]
 
-    def cell(self, n: int):
-        if n not in self._cells:
+    def cell(self, n: int, device: int | None = None):
+        device = self.device if device is None else device
+        if (n, device) not in self._cells:
             try:
-                key = (self.model, n, self.device)
+                key = (self.model, n, device)
                 hash(key)
             except TypeError:
                 key = None
             if key is not None and key in _CELL_CACHE:
-                self._cells[n] = _CELL_CACHE[key]
+                self._cells[(n, device)] = _CELL_CACHE[key]
             else:
-                self._cells[n] = compile_cell(self.model, self.supercell(n), self.device)
+                self._cells[(n, device)] = compile_cell(self.model, self.supercell(n), device)
                 if key is not None:
-                    _CELL_CACHE[key] = self._cells[n]
-        return self._cells[n]
+                    _CELL_CACHE[key] = self._cells[(n, device)]
+        return self._cells[(n, device)]
 
     def kpoints(self, n: int, q: int) -> np.ndarray:
         """k-points solved for (n, q): the base q x q rhombus (full mode's rotated copies are images)."""
@@ -189,9 +216,73 @@ class Engine:
         return float(bands.energies.min()), float(bands.energies.max())
 
     # -- the batch seam --
-    def _solve_group(self, n: int, q: int, words, task_ids, ctx=None):
+    def _solve_split(self, n: int, q: int, words, task_ids, lane: int, high, ticket: int = 0):
+        """The new masks of one (n, q) group over self.devices: contiguous slices balanced by sum d^3 (d = kept
+        dimension), one thread + context per device; curves in row order (each curve is independent of the
+        batch it was solved in, so the split does not change a bit)."""
+        rank, world = self.shard
+        if world > 1 and self.shard_mode == "split":
+            return self._solve_ranks(n, q, words, task_ids, lane, high, ticket)
+        G = len(self.devices)
+        if G == 1 or len(words) < G:
+            ctx = _lib.Device.lane(self.device, lane, high) if lane is not None else None
+            return self._solve_group(n, q, words, task_ids, ctx)
+        cuts = self._cuts(n, words, G)
+        with ThreadPoolExecutor(max_workers=G) as ex:
+            # one context per slice (a context serves one host thread at a time; the same GPU may be listed
+            # more than once)
+            futs = [ex.submit(self._solve_group, n, q, words[a:b], task_ids[a:b],
+                              _lib.Device.lane(dev, (lane or 0) * G + g, high), dev)
+                    for g, (dev, a, b) in enumerate(zip(self.devices, cuts[:-1], cuts[1:])) if b > a]
+            parts = [f.result() for f in futs]
+        curves = np.concatenate([cu for cu, _ in parts])
+        per_job = sum(pj * len(cu) for cu, pj in parts) / max(1, len(curves))
+        return curves, per_job
+
+    def _cuts(self, n, words, parts):
+        """Contiguous slices of the rows with equal shares of sum d^3 (the eigensolve cost)."""
+        d = self.cell(n).kept_dims(words).astype(np.float64)
+        c = np.cumsum(d * d * d)
+        cuts = np.concatenate([[0], np.searchsorted(c, c[-1] * np.arange(1, parts) / parts) + 1, [len(words)]])
+        return np.maximum.accumulate(np.minimum(cuts, len(words)))
+
+    def _solve_ranks(self, n, q, words, task_ids, lane, high, ticket):
+        """shard_mode="split": this rank's d^3-balanced slice of the group's new masks, then an all-gather of
+        the slices' curves (NCCL on the device), so every rank returns the whole group in row order."""
+        import torch
+        import torch.distributed as dist
+
+        rank, world = self.shard
+        cuts = self._cuts(n, words, world)
+        a, b = int(cuts[rank]), int(cuts[rank + 1])
+        ctx = _lib.Device.lane(self.device, lane, high) if lane is not None else None
+        npts = self.grid.npoints
+        if b > a:
+            curves, per_job = self._solve_group(n, q, words[a:b], task_ids[a:b], ctx)
+        else:
+            curves, per_job = np.zeros((0, npts)), 0.0
+        width = int(max(cuts[1:] - cuts[:-1]))
+        # the gather runs where the backend lives: device memory for NCCL, host memory for gloo
+        dev = torch.device("cuda", self.device) if dist.get_backend() == "nccl" else torch.device("cpu")
+        pad = torch.zeros((width, npts + 1), dtype=torch.float64, device=dev)
+        pad[: b - a, :npts] = torch.from_numpy(curves).to(dev)
+        pad[:, npts] = per_job
+        out = torch.empty((world * width, npts + 1), dtype=torch.float64, device=dev)
+        with self._coll:  # the collectives of the process group in submission order (the same on every rank)
+            self._coll.wait_for(lambda: self._coll_turn == ticket)
+            try:
+                dist.all_gather_into_tensor(out, pad)
+            finally:
+                self._coll_turn += 1
+                self._coll.notify_all()
+        out = out.cpu().numpy()
+        rows = np.concatenate([out[r * width: r * width + int(cuts[r + 1] - cuts[r])] for r in range(world)])
+        self.io_bytes[0] += (world - 1) * pad.numel() * 8
+        return rows[:, :npts].copy(), float(rows[:, npts].mean()) if len(rows) else 0.0
+
+    def _solve_group(self, n: int, q: int, words, task_ids, ctx=None, device=None):
         """One GPU batch for the (n, q) group: words uint64 [R, w] (task_ids: R ids for error reports)."""
-        cell = self.cell(n)
+        cell = self.cell(n, device)
         kp, kmult = self.kpoints_tr(n, q)
         t0 = time.perf_counter()
         curves, _, status = eval_batch(cell, kp, words, self.grid.lo, self.grid.step, self.grid.npoints,
@@ -258,7 +349,8 @@ class Engine:
             return out
 
         for n, q in tiers:
-            self.cell(n)  # compile cells and k-sets up front (not thread-safe)
+            for dev in self.devices:
+                self.cell(n, dev)  # compile cells and k-sets up front (not thread-safe)
             self.kpoints_tr(n, q)
         order = sorted(tiers, key=lambda g: -self.cell(g[0]).dim)
         if _E2E_ORDER == "big-then-small" and len(order) > 2:
@@ -304,11 +396,13 @@ class Engine:
                             high = -100 if small else (-1 if lane == 0 else 0)
                         else:
                             high = lane == 0 or (_E2E_PRIO == "big+small" and small)
-                        ctx = (_lib.Device.lane(self.device, lane, high)
-                               if len(tiers) > 1 or len(tiers[tier]) > 1 else None)
+                        ln = lane if len(tiers) > 1 or len(tiers[tier]) > 1 else None
                         lane += 1
+                        ticket = self._coll_tickets
+                        self._coll_tickets += 1
                         pieces.setdefault(tier, []).append(
-                            (start, ex.submit(self._solve_group, tier[0], tier[1], uniq[new], ids, ctx), bi))
+                            (start, ex.submit(self._solve_split, tier[0], tier[1], uniq[new], ids, ln, high, ticket),
+                             bi))
                     plans[(bi, gi)] = (tier, uniq, inv, keys, src, start)
             # batch bi can be placed once every piece of its tiers submitted by batches <= bi is done;
             # batches are finished (placement, cache, on_batch) as soon as that holds, so their host work
@@ -396,9 +490,10 @@ class Engine:
         q = self.q_of(n)
         sc = self.supercell(n)
         stream = level if stream_level is None else stream_level
-        # weak-scaling replica: rank r of `world` draws the replicates [r*M, (r+1)*M) of the stream
+        # weak-scaling replica: rank r of `world` draws the replicates [r*M, (r+1)*M) of the stream (split
+        # mode: every rank draws the whole level)
         rank, _ = self.shard
-        m0 = rank * nsamples
+        m0 = rank * nsamples if self.shard_mode == "replicas" else 0
         words = sample_masks(sc.nunits, p_vac, self.master_seed, stream, m0, nsamples)
         groups = [(n, q, words)]
         if with_cv:
@@ -428,6 +523,20 @@ class Engine:
             quarters = qc.reshape(nsamples, 4, npts)
             nominal += float(qpj.sum())
         terms, mean, var = level_moments(full, quarters, self.device)
+        rank, world = self.shard
+        if world > 1 and self.shard_mode == "replicas":
+            # exact cross-rank combination (fixed-point limbs, int64 all-reduce): the bits of one process
+            # drawing all world * M replicates
+            import torch
+            import torch.distributed as dist
+
+            dev = torch.device("cuda", self.device)
+            mean, var = exact_level_moments(torch.as_tensor(full).to(dev),
+                                            None if quarters is None else torch.as_tensor(quarters).to(dev),
+                                            nsamples * world, allreduce=dist.all_reduce)
+            nsamples_all = nsamples * world
+        else:
+            nsamples_all = nsamples
         terms = terms.cpu().numpy()
         self.io_bytes[0] += full.nbytes + (0 if quarters is None else quarters.nbytes)
         self.io_bytes[1] += terms.nbytes + 2 * mean.numel() * 8
@@ -438,8 +547,8 @@ class Engine:
             for r in range(4):
                 cv += quarters[:, r, :]
             cv *= 0.25
-        stats = LevelStats(level=level, n=n, q=q, nsamples=nsamples, mean=mean.cpu().numpy(),
-                           sample_variance=var.cpu().numpy() if nsamples > 1 else None,
+        stats = LevelStats(level=level, n=n, q=q, nsamples=nsamples_all, mean=mean.cpu().numpy(),
+                           sample_variance=var.cpu().numpy() if nsamples_all > 1 else None,
                            work_per_sample=nominal / nsamples, wall_seconds=spent, cache_hits=hits)
         return LevelSampleSet(stats=stats, terms=terms, full=full, cv=cv)
 

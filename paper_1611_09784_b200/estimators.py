@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _lib
 
-__all__ = ["LevelPlan", "LevelStats", "MlmcEstimate", "mean_and_variance", "level_moments", "combine_levels",
+__all__ = ["LevelPlan", "LevelStats", "MlmcEstimate", "mean_and_variance", "level_moments", "exact_level_moments", "combine_levels",
            "control_variate_sample", "window_mask"]
 
 
@@ -125,7 +125,7 @@ def level_moments(full, quarters=None, device: int = 0):
         var = torch.empty(npts, dtype=torch.float64, device=dev)
         _lib.Device.ctx(device)
         _lib.check(_lib.load().hx_level_moments_device(f.data_ptr(), 0 if q is None else q.data_ptr(), M, npts,
-                                                       terms.data_ptr(), mean.data_ptr(), var.data_ptr(), 0,
+                                                       terms.data_ptr(), mean.data_ptr(), var.data_ptr(),
                                                        st.cuda_stream),
                    "hx_level_moments_device")
     torch.cuda.current_stream(dev).wait_stream(st)
@@ -144,16 +144,54 @@ def _moments_stream(device: int):
     return st
 
 
-def moments_from_sums(s1, s2, M: int):
-    """Level mean / unbiased variance from all-reduced sums (sum term, sum term^2) over M samples.
+def exact_level_moments(full, quarters, m_total: int, allreduce=None):
+    """Level (mean, var) over samples spread across ranks or devices, bitwise independent of the split.
 
-    Used after the cross-rank all-reduce of per-rank `hx_level_moments_device` sums (one-pass form;
-    single-rank runs use the kernel's two-pass variance, mlmc.py:143-154)."""
-    s1 = np.asarray(s1, dtype=np.float64)
-    s2 = np.asarray(s2, dtype=np.float64)
-    mean = s1 / M
-    var = None if M < 2 else np.maximum(s2 - M * mean * mean, 0.0) / (M - 1)
-    return mean, var
+    `full` [M, npts] and `quarters` [M, 4, npts] (or None) are this rank's samples - CUDA tensors (device
+    kernels) or numpy arrays (host twins); `m_total` is the level's sample count over all ranks;
+    `allreduce(int64 limbs)` sums the fixed-point limbs over the ranks in place (e.g. torch.distributed
+    all_reduce with NCCL / gloo; None = single rank).  Two passes as np.var (mlmc.py:143-154): the exact sum
+    of the terms gives the mean, then the exact sum of squared deviations from that mean gives the unbiased
+    variance (NaN for m_total < 2).  With one rank the result equals hx_level_moments_device's bit for bit."""
+    import torch
+
+    if isinstance(full, torch.Tensor) and full.is_cuda:
+        dev = full.device
+        st = torch.cuda.current_stream(dev).cuda_stream
+        lib = _lib.load()
+        M, npts = full.shape
+        f = full.contiguous()
+        q = None if quarters is None else quarters.contiguous()
+        limbs = torch.empty((npts, _lib.HX_FX_LIMBS), dtype=torch.int64, device=dev)
+        mean = torch.empty(npts, dtype=torch.float64, device=dev)
+        var = torch.empty(npts, dtype=torch.float64, device=dev)
+
+        def sums(center):
+            _lib.check(lib.hx_level_sums_fixed_device(f.data_ptr(), 0 if q is None else q.data_ptr(), M, npts,
+                                                      0 if center is None else center.data_ptr(),
+                                                      limbs.data_ptr(), st), "hx_level_sums_fixed_device")
+            if allreduce is not None:
+                allreduce(limbs)
+
+        sums(None)
+        _lib.check(lib.hx_fixed_finalize_device(limbs.data_ptr(), npts, float(m_total), mean.data_ptr(), st),
+                   "hx_fixed_finalize_device")
+        sums(mean)
+        _lib.check(lib.hx_fixed_finalize_device(limbs.data_ptr(), npts, float(m_total - 1), var.data_ptr(), st),
+                   "hx_fixed_finalize_device")
+        return mean, var
+
+    def host_reduce(x):
+        if allreduce is None:
+            return x
+        t = torch.from_numpy(x)
+        allreduce(t)
+        return t.numpy()
+
+    s1 = host_reduce(_lib.fixed_sums(full, quarters))
+    mean = _lib.fixed_finalize(s1, m_total)
+    s2 = host_reduce(_lib.fixed_sums(full, quarters, mean))
+    return mean, _lib.fixed_finalize(s2, m_total - 1)
 
 
 def mean_and_variance(curves):

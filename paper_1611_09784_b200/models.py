@@ -263,6 +263,13 @@ class CompiledCell:
             raise ValueError("empty system: all orbitals removed by vacancies")
         return keep
 
+    def kept_dims(self, words: np.ndarray) -> np.ndarray:
+        """Kept dimension d of each uint64 mask row [R, w] (N minus the dofs of the vacant units)."""
+        words = np.ascontiguousarray(words, dtype=np.uint64)
+        bits = np.unpackbits(words.view(np.uint8), axis=1, bitorder="little")[:, : self.supercell.nunits]
+        per_unit = np.array([len(d) for d in self.unit_dofs], dtype=np.int64)
+        return self.dim - bits.astype(np.int64) @ per_unit
+
     def mask_words(self, vacant_units) -> np.ndarray:
         words = max(1, (self.supercell.nunits + 63) // 64)
         out = np.zeros(words, dtype=np.uint64)

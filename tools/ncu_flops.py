@@ -12,7 +12,7 @@ W = {"sm__sass_thread_inst_executed_op_dfma_pred_on.sum": 2.0, "sm__sass_thread_
      "sm__sass_thread_inst_executed_op_dadd_pred_on.sum": 1.0, "sm__inst_executed_pipe_tensor_subpipe_dmma.sum": 512.0}
 
 
-def main(path, top=20):
+def main(path, top=20, json_out=None, passes=1, label=""):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     h = rows[hi]
@@ -41,8 +41,25 @@ def main(path, top=20):
     out.append(f"total {tot_ms:.2f} ms, {tot_fl / 1e9:.1f} GFLOP executed FP64, {tot_fl / (tot_ms * 1e-3) / 1e12:.2f} TFLOP/s "
                "averaged over the serialised kernel time")
     print("\n".join(out))
-    return {"ms": tot_ms, "gflop": tot_fl / 1e9}
+    res = {"label": label, "source_csv": path, "passes": passes, "serialised_ms_per_pass": tot_ms / passes,
+           "executed_gflop_per_pass": tot_fl / 1e9 / passes,
+           "dmma_gflop_per_pass": sum(a["dmma_flops"] for a in agg.values()) / 1e9 / passes,
+           "kernels": {k: {"ms": a["ms"] / passes, "gflop": a["flops"] / 1e9 / passes, "launches": len(a["ids"])}
+                       for k, a in agg.items()}}
+    if json_out:
+        with open(json_out, "w") as f:
+            json.dump(res, f, indent=1)
+    return res
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 20)
+    import argparse
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("csv")
+    ap.add_argument("top", nargs="?", type=int, default=20)
+    ap.add_argument("--json", default=None)
+    ap.add_argument("--passes", type=int, default=1)
+    ap.add_argument("--label", default="")
+    a = ap.parse_args()
+    main(a.csv, a.top, a.json, a.passes, a.label)
