@@ -43,8 +43,10 @@ CONFIGS = {
     # BASELINE config 4: 64 samples sharded over 8 GPUs -> 8 per GPU (weak: each rank its own replicates)
     "c4": ("graphene", [(64, 8)], 128, 0.02, None, "graphene MC nu=64 (N=8192) Gamma+2x2 grid (4 reduced k) p=0.02 M=8/GPU"),
     # BASELINE config 5: batched eigensolve + IDOS sweep, one matrix per (mask, k) (run_c5)
-    "c5": ("graphene", [(4, 0), (8, 0), (16, 0), (32, 0)], 0, 0.05, None,
-           "batched eigensolve+IDOS sweep n=32/128/512/2048 (graphene-vacancy Bloch matrices, ~50% HBM batches)"),
+    # (nu1, nu2) supercells: n = 2 nu1 nu2 = 32 ... 2048; the rectangular ones (n = 64, 256, 1024) are this
+    # package's n x n2 extension of the reference's square supercells (geometry.build_supercell(n, n2))
+    "c5": ("graphene", [(4, 4), (4, 8), (8, 8), (8, 16), (16, 16), (16, 32), (32, 32)], 0, 0.05, None,
+           "batched eigensolve+IDOS sweep n=32/64/128/256/512/1024/2048 (graphene-vacancy Bloch matrices, ~50% HBM batches)"),
 }
 FRAC_NOTE = ("frac = EXECUTED FP64 flops / device time / FP64 peak.  Executed flops are ncu instruction counts of the "
              "same workload and build (DFMA x2 + DMUL + DADD per thread instruction, DMMA m8n8k4 x512 per warp "
@@ -67,7 +69,7 @@ def executed_gflop(path):
 
 
 # c5 batches: floor(0.5 * 180 GB / (16 n^2)) matrices, one (mask, k) matrix each
-C5_BATCH = {4: 5_490_000, 8: 343_000, 16: 21_500, 32: 1_341}
+C5_BATCH = {32: 5_490_000, 64: 1_370_000, 128: 343_000, 256: 85_800, 512: 21_500, 1024: 5_360, 2048: 1_341}
 SEED = 2026
 DELTA = 0.01
 NPTS = 201
@@ -390,15 +392,18 @@ def run_c5(args):
     e2e_tot = [0, 0.0, 0, 0]  # matrices, seconds, h2d bytes, d2h bytes
     cpu_rows = []
     with ClockSampler(local) as clk:
-        for nu, _ in levels:
-            cell = hx.compile_cell(model, hx.build_supercell(model.lattice_spec(), nu), local)
+        for nu, nu2 in levels:
+            sc = hx.build_supercell(model.lattice_spec(), nu, nu2)
+            cell = hx.compile_cell(model, sc, local)
             nunits = cell.supercell.nunits
             w = max(1, (nunits + 63) // 64)
-            B = C5_BATCH[nu]
+            B = C5_BATCH[cell.dim]
             masks = torch.zeros((B, w), dtype=torch.int64, device=dev)
             _lib.check(lib.hx_sample_masks_device(SEED, 5, rank * B, B, p, nunits, masks.data_ptr(), st.cuda_stream),
                        "hx_sample_masks_device")
-            kp = np.ascontiguousarray(hx.make_bz_grid(model.lattice_spec(), nu, 3, "reduced").kpoints[4:5])
+            # one generic k: reduced point (1/3, 1/3) of the supercell zone (the q = 3 grid's point 4 when square)
+            b1, b2 = model.lattice_spec().reciprocal_vectors()
+            kp = np.ascontiguousarray((b1 / (3 * nu) + b2 / (3 * nu2)).reshape(1, 2))
             curves = torch.empty((B, NPTS), dtype=torch.float64, device=dev)
             status = torch.empty((B, 1), dtype=torch.int32, device=dev)
 
@@ -429,7 +434,7 @@ def run_c5(args):
             d = kept_dims(cell, masks)
             flops = float(np.sum(16.0 / 3.0 * d.astype(np.float64) ** 3))
             ach = flops / (ms * 1e-3) / 1e12
-            sweep.append({"n": cell.dim, "nu": nu, "batch": B, "ms": round(ms, 3),
+            sweep.append({"n": cell.dim, "nu": nu, "nu2": nu2, "batch": B, "ms": round(ms, 3),
                           "matrices_per_s": world * B / (ms * 1e-3), "algorithmic_tflops": round(ach, 3),
                           "roofline_frac": round(ach / peak, 4),
                           "status_ok": bool((status == 0).all().item())})
@@ -450,7 +455,7 @@ def run_c5(args):
                 e2e_tot[2] += hmask.nbytes + kp.nbytes
                 e2e_tot[3] += cv.nbytes + B * 4
                 del hmask, cv
-            if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            if rank == 0 and world == 1 and not args.no_cpu_baseline and nu == nu2:  # reference: square cells only
                 cpu_rows.append(c5_reference_sample(kind, nu, masks[:64].cpu().numpy().view(np.uint64), kp, lo, hi))
             del masks, curves, status
     launches = _lib.kernel_launches() - launches0

@@ -52,14 +52,17 @@ def reciprocal(a):
 class Cell:
     """n x n supercell; site s = (i*n + j)*2 + b (lattice.py:139-141, 173-177)."""
 
-    def __init__(self, n, orbitals=(1, 1), removable=(0, 1)):
+    def __init__(self, n, orbitals=(1, 1), removable=(0, 1), n2=None):
+        # n2: cells along a2 of a rectangular n x n2 supercell (the package's config-5 extension; the reference
+        # builds square cells only, lattice.py:160-195, so rectangular parity rests on this same restatement)
         self.n = n
+        self.m = n if n2 is None else n2
         self.orbitals = tuple(orbitals)
-        ii, jj, bb = np.meshgrid(np.arange(n), np.arange(n), np.arange(2), indexing="ij")
+        ii, jj, bb = np.meshgrid(np.arange(n), np.arange(self.m), np.arange(2), indexing="ij")
         self.ci = ii.reshape(-1)
         self.cj = jj.reshape(-1)
         self.basis = bb.reshape(-1)
-        self.nsites = 2 * n * n
+        self.nsites = 2 * n * self.m
         counts = np.array([orbitals[b] for b in self.basis])
         self.site_offset = np.concatenate(([0], np.cumsum(counts)))
         self.dim = int(self.site_offset[-1])
@@ -67,11 +70,10 @@ class Cell:
         self.nunits = len(self.unit_sites)
         # unit_dofs, tbmodel.py:191-196
         self.unit_dofs = [np.arange(self.site_offset[s], self.site_offset[s + 1]) for s in self.unit_sites]
-        self.area = float(n * n)  # normalized area (lattice.py:131-133, area_unit = cell area)
+        self.area = float(n * self.m)  # normalized area (lattice.py:131-133, area_unit = cell area)
 
     def site_index(self, i, j, b):
-        n = self.n
-        return ((i % n) * n + (j % n)) * 2 + b
+        return ((i % self.n) * self.m + (j % self.m)) * 2 + b
 
 
 # --- models (tbmodel.py:40-79, 321-385) ---------------------------------------------------------
@@ -126,8 +128,8 @@ def parse_table(path):
     }
 
 
-def make_cell(model, n):
-    return Cell(n, model["orbitals"], model["removable"])
+def make_cell(model, n, n2=None):
+    return Cell(n, model["orbitals"], model["removable"], n2)
 
 
 def expand(cell, entries):

@@ -40,7 +40,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .estimators import LevelPlan, LevelStats, MlmcEstimate, combine_levels, exact_level_moments, level_moments
+from .estimators import (LevelPlan, LevelStats, MlmcEstimate, RateEstimates, combine_levels, exact_level_moments,
+                         fit_rates, level_moments, mean_and_variance, window_mask)
 from .geometry import build_supercell, partition_quarters
 from .idos import EnergyGrid
 from .models import compile_cell
@@ -49,7 +50,7 @@ from .sampling import (DefectConfiguration, enumerate_configs, keys_from_words, 
 from .solver import (eval_batch, make_bz_grid, raise_status, solve_bands, time_reversal_reduce,
                      use_time_reversal)
 
-__all__ = ["Engine", "TaskError", "LevelSampleSet", "ExhaustiveResult", "SLMC_STREAM_OFFSET"]
+__all__ = ["Engine", "TaskError", "LevelSampleSet", "ExhaustiveResult", "RatesResult", "SLMC_STREAM_OFFSET"]
 
 SLMC_STREAM_OFFSET = 10_000
 
@@ -93,6 +94,34 @@ def first_rows(inv):
     return np.unique(inv, return_index=True)[1]
 
 
+class _TierCache:
+    """Run cache of one (n, q) tier: the (n, q, mask) keys of the reference's cache (runner.py:206-244) as a
+    sorted array of mask rows (void view of the uint64 words) with their curves and per-job costs, so lookups
+    and inserts are vectorised (searchsorted) instead of a dict probe per request."""
+
+    def __init__(self, npts):
+        self.keys = None
+        self.curves = np.zeros((0, npts))
+        self.pj = np.zeros(0)
+
+    def find(self, kv):
+        """Row of each key in the cache, -1 if absent."""
+        if self.keys is None or not len(self.keys) or not len(kv):
+            return np.full(len(kv), -1, dtype=np.int64)
+        pos = np.minimum(np.searchsorted(self.keys, kv), len(self.keys) - 1)
+        return np.where(self.keys[pos] == kv, pos, -1)
+
+    def add(self, kv, curves, pj):
+        keys = kv if self.keys is None else np.concatenate([self.keys, kv])
+        curves = np.concatenate([self.curves, curves])
+        pj = np.concatenate([self.pj, pj])
+        o = np.argsort(keys, kind="stable")
+        self.keys, self.curves, self.pj = keys[o], curves[o], pj[o]
+
+    def __len__(self):
+        return 0 if self.keys is None else len(self.keys)
+
+
 class TaskError(RuntimeError):
     """One or more tasks failed; message names the task ids (runner.py:56-72)."""
 
@@ -109,6 +138,13 @@ class LevelSampleSet:
     terms: np.ndarray = field(repr=False)
     full: np.ndarray = field(repr=False)
     cv: np.ndarray | None = field(repr=False, default=None)
+
+
+@dataclass(frozen=True, eq=False)
+class RatesResult:
+    records: list
+    rates: RateEstimates
+    bias_proxies: list
 
 
 @dataclass(frozen=True, eq=False)
@@ -148,7 +184,7 @@ class Engine:
         self.shard_mode = shard_mode
         self.devices = list(devices)  # GPUs the new masks of a group are split over (int G: device .. device+G-1)
         self.io_bytes = [0, 0]  # host->device, device->host bytes moved by the batch calls
-        self._cache: dict = {}
+        self._caches: dict = {}  # (n, q) -> _TierCache: the run-wide dedup cache (runner.py:206-244)
         self._coll = threading.Condition()  # split mode: all-gathers in submission order on every rank
         self._coll_turn = 0
         self._coll_tickets = 0
@@ -214,6 +250,12 @@ class Engine:
         grid = make_bz_grid(self.model.lattice_spec(), 1, self.nq, self.bz_mode)
         bands = solve_bands(self.model, self.supercell(1), None, grid, cell=self.cell(1))
         return float(bands.energies.min()), float(bands.energies.max())
+
+    def _tier_cache(self, tier, npts):
+        c = self._caches.get(tier)
+        if c is None:
+            c = self._caches[tier] = _TierCache(npts)
+        return c
 
     # -- the batch seam --
     def _solve_split(self, n: int, q: int, words, task_ids, lane: int, high, ticket: int = 0):
@@ -363,28 +405,33 @@ class Engine:
         lane = 0
         with ThreadPoolExecutor(max_workers=max(1, sum(len(v) for v in tiers.values()))) as ex:
             for tier in order:
-                pending = {}
+                cache = self._tier_cache(tier, npts)
+                pend = np.zeros(0, dtype=np.int64)  # sorted keys of this call's new masks so far, their rows
+                pend_keys = None
                 count = 0
                 for bi, gi, words in members(tier):
                     R = words.shape[0]
+                    start = count
                     if self.dedup and R:
                         uniq, inv = unique_rows(words)
-                        keys = [(tier[0], tier[1], row.tobytes()) for row in uniq]
+                        kv = uniq.view(f"V{8 * uniq.shape[1]}").ravel()
+                        src = np.where(cache.find(kv) >= 0, -1, -2)
+                        if pend_keys is not None and len(pend_keys):
+                            pos = np.minimum(np.searchsorted(pend_keys, kv), len(pend_keys) - 1)
+                            inp = (pend_keys[pos] == kv) & (src == -2)
+                            src[inp] = pend[pos[inp]]
+                        fresh = np.flatnonzero(src == -2)
+                        src[fresh] = count + np.arange(len(fresh))
+                        count += len(fresh)
+                        if len(fresh):  # fresh rows join the pending set (kept sorted)
+                            allk = kv[fresh] if pend_keys is None else np.concatenate([pend_keys, kv[fresh]])
+                            allr = src[fresh] if pend_keys is None else np.concatenate([pend, src[fresh]])
+                            o = np.argsort(allk, kind="stable")
+                            pend_keys, pend = allk[o], allr[o]
                     else:
-                        uniq, inv, keys = words, np.arange(R), None
-                    src = np.empty(len(uniq), dtype=np.int64)
-                    start = count
-                    for i in range(len(uniq)):
-                        k = keys[i] if keys is not None else None
-                        if k is not None and k in self._cache:
-                            src[i] = -1
-                        elif k is not None and k in pending:
-                            src[i] = pending[k]
-                        else:
-                            src[i] = count
-                            if k is not None:
-                                pending[k] = count
-                            count += 1
+                        uniq, inv, kv = words, np.arange(R), None
+                        src = count + np.arange(R)
+                        count += R
                     new = np.flatnonzero(src >= start)
                     hits[bi] += R - len(new)
                     if len(new):
@@ -403,7 +450,7 @@ class Engine:
                         pieces.setdefault(tier, []).append(
                             (start, ex.submit(self._solve_split, tier[0], tier[1], uniq[new], ids, ln, high, ticket),
                              bi))
-                    plans[(bi, gi)] = (tier, uniq, inv, keys, src, start)
+                    plans[(bi, gi)] = (tier, uniq, inv, kv, src, start)
             # batch bi can be placed once every piece of its tiers submitted by batches <= bi is done;
             # batches are finished (placement, cache, on_batch) as soon as that holds, so their host work
             # overlaps the device work still running for later batches
@@ -431,7 +478,7 @@ class Engine:
         """Per-request curves of batch bi from the run cache and the solved pieces (runner.py:234-243)."""
         res = []
         for gi in range(len(groups)):
-            tier, uniq, inv, keys, src, start = plans[(bi, gi)]
+            tier, uniq, inv, kv, src, start = plans[(bi, gi)]
             cu = np.empty((len(uniq), npts))
             pj = np.empty(len(uniq))
             got = np.flatnonzero(src >= 0)
@@ -444,14 +491,17 @@ class Engine:
                     sel = got[which == k]
                     cu[sel] = curves[src[sel] - lst[k][0]]
                     pj[sel] = per_job
-            for i in np.flatnonzero(src < 0):
-                cu[i], pj[i] = self._cache[keys[i]]
+            cached = np.flatnonzero(src < 0)
+            cache = self._tier_cache(tier, npts)
+            if len(cached):
+                at = cache.find(kv[cached])
+                cu[cached] = cache.curves[at]
+                pj[cached] = cache.pj[at]
             # masks this batch solved first: their cost is this batch's, and they enter the run cache
             own = np.flatnonzero(src >= start)
             spent[bi] += float(pj[own].sum())
-            if keys is not None:
-                for i in own:
-                    self._cache[keys[i]] = (cu[i], pj[i])
+            if kv is not None and len(own):
+                cache.add(kv[own], cu[own], pj[own])
             res.append((cu[inv], pj[inv]))
         return res, hits[bi], spent[bi]
 
@@ -585,6 +635,46 @@ class Engine:
         level = plan.num_levels
         return self.sample_level(level, plan.ns[-1], nsamples, plan.p_vac, with_cv=False,
                                  stream_level=SLMC_STREAM_OFFSET + level)
+
+    def run_rates(self, plan: LevelPlan, window=None) -> RatesResult:
+        """Standalone per-level statistics (every level with its quarter CV) and the fitted exponents
+        (runner.py:347-378): variance of Q_l, of the CV difference, the bias proxies |mean_l - mean_{l+1}| over
+        the energy window and the per-sample cost.  The levels go to the seam as one concurrent submission,
+        deduplicated in level order (the cache hits of sampling them one after another)."""
+        mask = window_mask(self.grid, window)
+        for n in plan.ns:
+            if n % 2:
+                raise ValueError("rate estimation needs even supercell factors for the CV")
+        levels = list(enumerate(zip(plan.ns, plan.samples), start=1))
+        batches = [functools.partial(self._level_batch, idx, n, m, plan.p_vac, True) for idx, (n, m) in levels]
+        tiers_of = [[(n, self.q_of(n)), (n // 2, self.q_of(n // 2))] for _, (n, _) in levels]
+        sets = [None] * len(levels)
+
+        def finish(bi, ev):
+            idx, (n, m) = levels[bi]
+            sets[bi] = self._level_finish(idx, n, m, True, ev)
+
+        self._evaluate_batches(batches, on_batch=finish, tiers_of=tiers_of)
+        records, means = [], []
+        for sset in sets:
+            _, var_q = mean_and_variance(sset.full)
+            mean_q = np.mean(sset.full, axis=0)
+            means.append(mean_q)
+            records.append({"set": sset, "n": sset.stats.n, "variance_q": float(np.mean(var_q[mask])),
+                            "variance_diff": float(np.mean(sset.stats.sample_variance[mask])),
+                            "seconds_per_sample": sset.stats.work_per_sample})
+        proxies = [float(np.mean(np.abs(means[i] - means[i + 1])[mask])) for i in range(len(means) - 1)]
+        rates = fit_rates(plan.ns, bias_proxies=proxies if len(proxies) >= 2 else None,
+                          variances=[r["variance_q"] for r in records],
+                          cv_diff_variances=[r["variance_diff"] for r in records],
+                          work=[r["seconds_per_sample"] for r in records])
+        return RatesResult(records=records, rates=rates, bias_proxies=proxies)
+
+    def band_structure(self, n: int, bz_mode: str | None = None):
+        """Unperturbed bands of the nu = n supercell on its (n, q) grid - the CLI's "bands" mode
+        (cli.py:132-152: solve_bands(model, supercell, None, make_bz_grid(..., bz_mode)))."""
+        grid = make_bz_grid(self.model.lattice_spec(), n, self.q_of(n), bz_mode or self.bz_mode)
+        return solve_bands(self.model, self.supercell(n), None, grid, cell=self.cell(n))
 
     def run_exhaustive(self, n: int, p_vac: float, symmetry_reduce: bool = False, cap: int = 24):
         """Exact expectation over all 2^N outcomes with binomial weights (runner.py:380-415)."""

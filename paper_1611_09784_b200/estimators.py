@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib
 
 __all__ = ["LevelPlan", "LevelStats", "MlmcEstimate", "mean_and_variance", "level_moments", "exact_level_moments", "combine_levels",
-           "control_variate_sample", "window_mask"]
+           "control_variate_sample", "window_mask", "RateFit", "RateEstimates", "fit_loglog_slope", "fit_rates"]
 
 
 @dataclass(frozen=True)
@@ -231,3 +231,70 @@ def combine_levels(grid, levels, total_wall_seconds: float = 0.0) -> MlmcEstimat
             var = var + ls.sample_variance / ls.nsamples
     return MlmcEstimate(grid=grid, mean=mean, estimator_variance=var if ok else None, levels=tuple(levels),
                         total_wall_seconds=total_wall_seconds)
+
+
+# ---- rate fits of the "rates" mode (mlmc.py:260-338): host arithmetic on a handful of level statistics --------
+@dataclass(frozen=True)
+class RateFit:
+    value: float
+    stderr: float
+
+    def __float__(self):
+        return self.value
+
+
+def fit_loglog_slope(sizes, observations) -> RateFit:
+    """Least-squares slope of log(observation) on log(size) with its standard error (NaN for two points)
+    (mlmc.py:268-285)."""
+    x = np.log(np.asarray(sizes, dtype=float))
+    y = np.asarray(observations, dtype=float)
+    if np.any(y <= 0):
+        raise ValueError("observations must be positive for a log-log fit")
+    if len(x) != len(y) or len(x) < 2:
+        raise ValueError("need at least two (size, observation) pairs")
+    y = np.log(y)
+    xc = x - x.mean()
+    sxx = float(np.dot(xc, xc))
+    slope = float(np.dot(xc, y) / sxx)
+    se = math.nan
+    if len(x) > 2:
+        r = y - (y.mean() + slope * xc)
+        se = math.sqrt(float(np.dot(r, r)) / (len(x) - 2) / sxx)
+    return RateFit(slope, se)
+
+
+@dataclass(frozen=True)
+class RateEstimates:
+    """Exponents: bias W, variance S, CV-difference variance D (decays, positive) and cost C (growth)
+    (mlmc.py:288-303)."""
+
+    w: RateFit | None = None
+    s: RateFit | None = None
+    d: RateFit | None = None
+    c: RateFit | None = None
+
+    @property
+    def mlmc_benefit(self) -> bool:
+        return self.d is not None and self.s is not None and self.d.value > self.s.value
+
+    @property
+    def mc_benefit(self) -> bool:
+        return self.c is not None and self.s is not None and self.c.value > self.s.value
+
+
+def fit_rates(sizes, bias_proxies=None, variances=None, cv_diff_variances=None, work=None) -> RateEstimates:
+    """Model exponents from per-level observations; bias proxies |mean_l - mean_{l+1}| pair with sizes[:-1]
+    (mlmc.py:306-338)."""
+    sizes = tuple(int(n) for n in sizes)
+    if len(sizes) < 2:
+        raise ValueError("need at least two levels to fit rates")
+
+    def decay(obs, xs):
+        f = fit_loglog_slope(xs, obs)
+        return RateFit(-f.value, f.stderr)
+
+    w = None if bias_proxies is None else decay(tuple(bias_proxies), sizes[: len(tuple(bias_proxies))])
+    s = None if variances is None else decay(variances, sizes)
+    d = None if cv_diff_variances is None else decay(cv_diff_variances, sizes)
+    c = None if work is None else fit_loglog_slope(sizes, work)
+    return RateEstimates(w=w, s=s, d=d, c=c)

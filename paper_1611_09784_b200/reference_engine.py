@@ -32,7 +32,7 @@ from .models import GrapheneNNModel, MultiOrbitalModel, compile_cell
 from .sampling import words_from_keys
 from .solver import eval_batch, make_bz_grid, raise_status
 
-__all__ = ["cuda_engine_class", "to_native_model"]
+__all__ = ["cuda_engine_class", "cuda_solve_bands", "install", "to_native_model"]
 
 
 def to_native_model(model):
@@ -130,3 +130,44 @@ def cuda_engine_class(base):
 
     CudaEngine.__name__ = CudaEngine.__qualname__ = "CudaEngine"
     return CudaEngine
+
+
+def cuda_solve_bands(spectrum):
+    """Drop-in for the reference's `spectrum.solve_bands(model, supercell, defects, grid, cell=None)`
+    (spectrum.py:120-134) on libhx: the ascending eigenvalues of every grid point of one sample in one GPU
+    batch, returned as the reference's own BandGrid (the CLI's "bands" mode calls it directly, cli.py:132-152,
+    bypassing the Engine seam).  Non-PD overlaps / failures raise the reference's SolverError text."""
+    from . import solver as native
+
+    def solve_bands(model, supercell, defects, grid, cell=None):
+        nmodel = to_native_model(model)
+        nsc = build_supercell(nmodel.lattice_spec(), supercell.n)
+        ncell = compile_cell(nmodel, nsc)
+        vacant = () if defects is None else tuple(sorted(defects.vacant))
+        keep = ncell.configure(vacant)
+        d = int(keep.sum())
+        words = ncell.mask_words(vacant).reshape(1, -1)
+        t0 = time.perf_counter()
+        _, eigs, status = eval_batch(ncell, grid.kpoints, words, 0.0, 1.0, 1, 1.0, want_eigs=True)
+        try:
+            raise_status(status, grid.kpoints)
+        except native.SolverError as exc:
+            raise spectrum.SolverError(str(exc)) from exc
+        return spectrum.BandGrid(grid=grid, energies=np.ascontiguousarray(eigs[0, :, :d]),
+                                 solve_seconds=time.perf_counter() - t0)
+
+    return solve_bands
+
+
+def install(hexmc):
+    """Point the reference CLI (hexmc.cli) at libhx: its Engine's batch seam and its bands-mode solve.
+    Returns the Engine class installed.  Everything else (config, drivers, artefact writers) stays the
+    reference's code."""
+    import hexmc.cli
+    import hexmc.runner
+    import hexmc.spectrum
+
+    engine_cls = cuda_engine_class(hexmc.runner.Engine)
+    hexmc.cli.Engine = engine_cls
+    hexmc.cli.solve_bands = cuda_solve_bands(hexmc.spectrum)
+    return engine_cls

@@ -136,3 +136,18 @@ def test_time_reversal_pairs_of_the_reference_grid(n, q):
         partners = [f for f in frac if np.allclose(np.mod(f + r + 1e-12, 1.0), 0.0, atol=1e-9)
                     or np.allclose(np.mod(f + r + 1e-12, 1.0), 1.0, atol=1e-9)]
         assert len(partners) == 1
+
+
+@pytest.mark.parametrize("n,n2", [(2, 3), (4, 8), (3, 1)])
+def test_rectangular_supercell_tables_match_oracle(n, n2):
+    """n x n2 supercells (config-5 sizes 64 / 256 / 1024): site order, instance tables, area."""
+    model = GrapheneNNModel()
+    sc = build_supercell(model.lattice_spec(), n, n2)
+    cell = compile_cell(model, sc)
+    ocell = O.make_cell(O.graphene_model(), n, n2)
+    assert cell.dim == ocell.dim == 2 * n * n2 and sc.area == pytest.approx(ocell.area, rel=1e-14)
+    src, dst, amp, disp = O.expand(ocell, O.graphene_model()["hops"])
+    np.testing.assert_array_equal(cell.h[0], src)
+    np.testing.assert_array_equal(cell.h[1], dst)
+    np.testing.assert_allclose(cell.h[3], disp, rtol=0, atol=1e-15)
+    assert build_supercell(model.lattice_spec(), n, n).n2 is None  # square stays the reference's cell

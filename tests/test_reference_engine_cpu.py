@@ -58,3 +58,28 @@ def test_model_conversion():
     assert (g.eps_2p, g.t, g.s) == (0.1, -2.8, 0.1)
     with pytest.raises(TypeError):
         to_native_model(object())
+
+
+def test_fit_rates_restatement_matches_reference():
+    """estimators.fit_rates / fit_loglog_slope (the rates mode's host arithmetic) against the reference's own
+    functions (mlmc.py:268-338) on random positive observations."""
+    hexmc = import_hexmc()
+    from paper_1611_09784_b200.estimators import fit_loglog_slope, fit_rates
+
+    rng = np.random.default_rng(4)
+    for nlev in (2, 3, 4):
+        sizes = [4 * 2**i for i in range(nlev)]
+        obs = {k: list(np.exp(rng.normal(size=nlev))) for k in ("v", "d", "w")}
+        prox = list(np.exp(rng.normal(size=nlev - 1))) if nlev > 2 else None
+        a = fit_rates(sizes, bias_proxies=prox, variances=obs["v"], cv_diff_variances=obs["d"], work=obs["w"])
+        b = hexmc.mlmc.fit_rates(sizes, bias_proxies=prox, variances=obs["v"], cv_diff_variances=obs["d"],
+                                 work=obs["w"])
+        for k in ("w", "s", "d", "c"):
+            x, y = getattr(a, k), getattr(b, k)
+            assert (x is None) == (y is None)
+            if x is not None:
+                assert x.value == y.value
+                assert (np.isnan(x.stderr) and np.isnan(y.stderr)) or x.stderr == y.stderr
+        assert a.mlmc_benefit == b.mlmc_benefit and a.mc_benefit == b.mc_benefit
+    with pytest.raises(ValueError):
+        fit_loglog_slope([4, 8], [1.0, -1.0])

@@ -143,3 +143,26 @@ def test_c3_table_nu16():
 # ---- c4 scale: a defected nu = 64 sample at Gamma against zhegv on the N = 8192 pencil -------------------------
 def test_c4_defected_nu64_gamma():
     check_batch("graphene", 64, 1, 0.02, 1, 2026, (0,))
+
+
+# ---- c5 sweep sizes on rectangular n x n2 supercells (n = 64, 256, 1024) --------------------------------------
+@pytest.mark.parametrize("nu,nu2,count", [(4, 8, 64), (8, 16, 24), (16, 32, 4)])
+def test_c5_rectangular_sizes(nu, nu2, count):
+    model = hx.GrapheneNNModel()
+    spec = model.lattice_spec()
+    sc = hx.build_supercell(spec, nu, nu2)
+    cell = hx.compile_cell(model, sc)
+    b1, b2 = spec.reciprocal_vectors()
+    kp = np.ascontiguousarray((b1 / (3 * nu) + b2 / (3 * nu2)).reshape(1, 2))
+    step = (HI_G - LO_G) / (NPTS - 1)
+    words = sample_masks(sc.nunits, 0.05, 2026, 5, 0, count)
+    curves, eigs, status = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01, want_eigs=True)
+    assert (status == 0).all()
+    om = O.graphene_model()
+    ocell = O.make_cell(om, nu, nu2)
+    for m in (0, count - 1):
+        ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
+        d = ref.shape[1]
+        assert np.max(np.abs(eigs[m, :, :d] - ref)) <= EIG_TOL * (ref.max() - ref.min())
+        rc = O.idos_from_bands(ref, np.ones(1), LO_G, HI_G, NPTS, 0.01, ocell.area)
+        np.testing.assert_allclose(curves[m], rc, rtol=0, atol=IDOS_TOL)
