@@ -45,8 +45,9 @@ const char* band_last_error() { return g_band_err.c_str(); }
 struct BandWs {
   // per-matrix layout inside one workspace slab (offsets in double2 units)
   size_t a_off, v_off, x_off, t_off, z_off, m_off, dg_off;  // dg: diag + e2 (2N doubles = N double2)
+  size_t b_off;                              // general pencil: S (then its Cholesky factor L), N x N
   size_t stride;                             // per matrix, double2 units
-  static BandWs make(int N) {
+  static BandWs make(int N, bool general = false) {
     BandWs w;
     w.a_off = 0;
     w.v_off = (size_t)N * N;
@@ -55,7 +56,8 @@ struct BandWs {
     w.z_off = w.t_off + (size_t)BW * BW;
     w.m_off = w.z_off + (size_t)16 * BW * BW;
     w.dg_off = w.m_off + (size_t)BW * BW;
-    w.stride = w.dg_off + (size_t)N + 16;
+    w.b_off = w.dg_off + (size_t)N + 16;
+    w.stride = w.b_off + (general ? (size_t)N * N : 0);
     w.stride = (w.stride + 15) & ~(size_t)15;
     return w;
   }
@@ -335,6 +337,217 @@ __global__ void __launch_bounds__(256) band_copy_kernel(const double2* __restric
 }
 
 // ------------------------------------------------------------------------------------------------
+// General pencil (overlap tables, zhegv in the reference: spectrum.py:106-108): S = L L^H (Cholesky), then the
+// standard problem L^-1 H L^-H goes through the same two-stage reduction.  Blocked with 32-wide blocks:
+//   chol_panel_kernel     L11 = chol(S11) in shared memory, L21 = S21 L11^-H (one row per thread)
+//   rank_update_kernel    S22 -= L21 L21^H                              (DMMA, hx_gemm.cuh)
+//   trsm_rows_kernel      A[k0:k0+32, :] = L11^-1 A[k0:k0+32, :], its conjugate transpose into X (N x 32)
+//   rank_update_kernel    A[k0+32:, :] -= L21 A[k0:k0+32, :]             (M -= U W^H, W = X)
+// run twice with an in-place conjugate transpose between (L^-1 H, then L^-1 (L^-1 H)^H = L^-1 H L^-H).
+// Vacancies: the kept d x d block is assembled in place and S's tail diagonal is 1, so L = diag(L11, I) and
+// the tail of L^-1 H L^-H stays exactly zero.  A non-positive (or non-finite) Cholesky pivot marks the matrix
+// HX_ST_NOT_PD (the reference's SolverError "overlap matrix not positive definite", spectrum.py:109-117) and is
+// replaced by 1 so the batch runs on.
+__global__ void __launch_bounds__(256) band_assemble_general_kernel(CellDev c, const double2* __restrict__ kpts,
+                                                                    int nk, const uint64_t* __restrict__ masks,
+                                                                    int64_t mat0, double2* ws, BandWs L, int* dims,
+                                                                    int* status) {
+  __shared__ int cnt[(HX_MAX_N + 31) / 32];
+  extern __shared__ int new_idx[];
+  const int N = c.N;
+  const int64_t mat = mat0 + blockIdx.x;
+  const int64_t mk = mat / nk;
+  const int kk = (int)(mat - mk * nk);
+  double2* A = ws + (size_t)blockIdx.x * L.stride + L.a_off;
+  double2* B = ws + (size_t)blockIdx.x * L.stride + L.b_off;
+  for (int64_t p = threadIdx.x; p < (int64_t)N * N; p += blockDim.x) {
+    A[p] = make_double2(0.0, 0.0);
+    B[p] = make_double2(0.0, 0.0);
+  }
+  const int d = block_compact(c, masks + mk * c.words, new_idx, cnt);
+  if (threadIdx.x == 0) {
+    dims[blockIdx.x] = d;
+    status[mat] = d == 0 ? 3 : 0;
+  }
+  for (int i = d + threadIdx.x; i < N; i += blockDim.x) B[i + (int64_t)i * N] = make_double2(1.0, 0.0);
+  if (d == 0) return;
+  assemble_full(c, new_idx, d, kpts[kk], A, N, false);
+  assemble_full(c, new_idx, d, kpts[kk], B, N, true);
+}
+
+// One CTA per matrix: Cholesky of the 32 x 32 diagonal block at k0 (lower), then L21 = S21 L11^-H.
+__global__ void __launch_bounds__(256) chol_panel_kernel(double2* ws, BandWs L, int N, int k0, int* status,
+                                                         int64_t mat0) {
+  __shared__ double2 Ls[BW][BW + 1];
+  __shared__ int bad;
+  double2* B = ws + (size_t)blockIdx.x * L.stride + L.b_off;
+  const int tid = threadIdx.x;
+  const int nb = min(BW, N - k0);
+  if (tid == 0) bad = 0;
+  for (int p = tid; p < BW * BW; p += blockDim.x) {
+    const int r = p % BW, cc = p / BW;
+    Ls[r][cc] = (r < nb && cc < nb && r >= cc) ? B[k0 + r + (size_t)(k0 + cc) * N] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int j = 0; j < nb; ++j) {
+    if (tid == 0) {
+      double pv = Ls[j][j].x;
+      if (!(pv > 0.0) || !isfinite(pv)) {
+        bad = 1;
+        pv = 1.0;
+      }
+      Ls[j][j] = make_double2(sqrt(pv), 0.0);
+    }
+    __syncthreads();
+    const double inv = 1.0 / Ls[j][j].x;
+    if (tid > j && tid < nb) Ls[tid][j] = make_double2(Ls[tid][j].x * inv, Ls[tid][j].y * inv);
+    __syncthreads();
+    // trailing: Ls[r][cc] -= Ls[r][j] conj(Ls[cc][j]), j < cc <= r
+    for (int p = tid; p < BW * BW; p += blockDim.x) {
+      const int r = p % BW, cc = p / BW;
+      if (cc > j && r >= cc && r < nb) {
+        const double2 a = Ls[r][j], b = Ls[cc][j];
+        Ls[r][cc].x -= a.x * b.x + a.y * b.y;
+        Ls[r][cc].y -= a.y * b.x - a.x * b.y;
+      }
+    }
+    __syncthreads();
+  }
+  if (bad && tid == 0) status[mat0 + blockIdx.x] = 1;  // HX_ST_NOT_PD
+  for (int p = tid; p < BW * BW; p += blockDim.x) {
+    const int r = p % BW, cc = p / BW;
+    if (r < nb && cc < nb) B[k0 + r + (size_t)(k0 + cc) * N] = r >= cc ? Ls[r][cc] : make_double2(0.0, 0.0);
+  }
+  // rows below: x L11^H = b  ->  x_j = (b_j - sum_{l<j} x_l conj(L_jl)) / L_jj
+  for (int r = k0 + nb + tid; r < N; r += blockDim.x) {
+    double2 x[BW];
+#pragma unroll
+    for (int j = 0; j < BW; ++j) x[j] = j < nb ? B[r + (size_t)(k0 + j) * N] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int j = 0; j < BW; ++j) {
+      if (j >= nb) break;
+      double2 t = x[j];
+      for (int l = 0; l < j; ++l) {
+        const double2 a = x[l], b = Ls[j][l];  // x_l conj(L_jl)
+        t.x -= a.x * b.x + a.y * b.y;
+        t.y -= a.y * b.x - a.x * b.y;
+      }
+      const double inv = 1.0 / Ls[j][j].x;
+      x[j] = make_double2(t.x * inv, t.y * inv);
+    }
+#pragma unroll
+    for (int j = 0; j < BW; ++j)
+      if (j < nb) B[r + (size_t)(k0 + j) * N] = x[j];
+  }
+}
+
+// Rows [k0, k0+32) of A <- L11^-1 (those rows), and X[c][i] = conj(new A[k0+i][c]) (N x 32, ld N).  CTA = 32
+// columns x 32 rows staged through shared memory; one thread per column runs the forward substitution.
+__global__ void __launch_bounds__(256) trsm_rows_kernel(double2* ws, BandWs L, int N, int k0) {
+  __shared__ double2 Ls[BW][BW + 1];
+  __shared__ double2 As[BW][BW + 1];  // As[i][c]
+  double2* base = ws + (size_t)blockIdx.y * L.stride;
+  const double2* B = base + L.b_off;
+  double2* A = base + L.a_off;
+  double2* X = base + L.x_off;
+  const int tid = threadIdx.x, c0 = blockIdx.x * BW;
+  const int nb = min(BW, N - k0), nc = min(BW, N - c0);
+  for (int p = tid; p < BW * BW; p += blockDim.x) {
+    const int i = p % BW, cc = p / BW;
+    Ls[i][cc] = (i < nb && cc < nb) ? B[k0 + i + (size_t)(k0 + cc) * N] : make_double2(0.0, 0.0);
+    As[i][cc] = (i < nb && cc < nc) ? A[k0 + i + (size_t)(c0 + cc) * N] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  if (tid < nc) {
+    for (int i = 0; i < nb; ++i) {
+      double2 t = As[i][tid];
+      for (int l = 0; l < i; ++l) {
+        const double2 a = Ls[i][l], b = As[l][tid];
+        t.x -= a.x * b.x - a.y * b.y;
+        t.y -= a.x * b.y + a.y * b.x;
+      }
+      const double inv = 1.0 / Ls[i][i].x;
+      As[i][tid] = make_double2(t.x * inv, t.y * inv);
+    }
+  }
+  __syncthreads();
+  for (int p = tid; p < BW * BW; p += blockDim.x) {
+    const int i = p % BW, cc = p / BW;
+    if (i < nb && cc < nc) A[k0 + i + (size_t)(c0 + cc) * N] = As[i][cc];
+  }
+  for (int p = tid; p < BW * BW; p += blockDim.x) {
+    const int cc = p % BW, i = p / BW;  // X[c0 + cc][i], coalesced over cc
+    if (cc < nc) X[c0 + cc + (size_t)i * N] = i < nb ? cconj(As[i][cc]) : make_double2(0.0, 0.0);
+  }
+}
+
+// In-place A <- A^H (N x N): one CTA per 32 x 32 tile pair (ti <= tj).
+__global__ void __launch_bounds__(256) conj_transpose_kernel(double2* ws, BandWs L, int N) {
+  __shared__ double2 P[BW][BW + 1], Q[BW][BW + 1];
+  double2* A = ws + (size_t)blockIdx.y * L.stride + L.a_off;
+  const int nt = (N + BW - 1) / BW;
+  int t = blockIdx.x, ti = 0;
+  while (t >= nt - ti) {
+    t -= nt - ti;
+    ++ti;
+  }
+  const int tj = ti + t;
+  const int tid = threadIdx.x;
+  for (int p = tid; p < BW * BW; p += blockDim.x) {
+    const int r = p % BW, cc = p / BW;
+    const int gr = ti * BW + r, gc = tj * BW + cc;
+    P[r][cc] = (gr < N && gc < N) ? A[gr + (size_t)gc * N] : make_double2(0.0, 0.0);
+    const int hr = tj * BW + r, hc = ti * BW + cc;
+    Q[r][cc] = (hr < N && hc < N) ? A[hr + (size_t)hc * N] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int p = tid; p < BW * BW; p += blockDim.x) {
+    const int r = p % BW, cc = p / BW;
+    const int gr = ti * BW + r, gc = tj * BW + cc;
+    if (gr < N && gc < N) A[gr + (size_t)gc * N] = cconj(Q[cc][r]);
+    const int hr = tj * BW + r, hc = ti * BW + cc;
+    if (hr < N && hc < N) A[hr + (size_t)hc * N] = cconj(P[cc][r]);
+  }
+}
+
+// A <- L^-1 A for the whole batch (the rows-then-update sweep of the file comment).
+static void band_trsm_left(double2* ws, const BandWs& L, int N, int64_t cnt, cudaStream_t st) {
+  const SlabGeom G{L.stride, N, L.a_off};
+  for (int k0 = 0; k0 < N; k0 += BW) {
+    trsm_rows_kernel<<<dim3((unsigned)((N + BW - 1) / BW), (unsigned)cnt), 256, 0, st>>>(ws, L, N, k0);
+    const int m = N - k0 - BW;
+    if (m > 0)
+      rank_update_kernel<64><<<dim3((unsigned)((m + RU_T - 1) / RU_T), (unsigned)((N + 63) / 64), (unsigned)cnt), 256,
+                               ru_smem<64>(), st>>>(ws, G, k0 + BW, 0, m, N, L.b_off + (size_t)k0 * N + k0 + BW,
+                                                    L.x_off);
+    count_launch(m > 0 ? 2 : 1);
+  }
+}
+
+// Standard form L^-1 H L^-H of the staged pencils (status of non-PD overlaps set by chol_panel_kernel).
+static int band_reduce_pencil(double2* ws, const BandWs& L, int N, int64_t cnt, int* status, int64_t mat0,
+                              cudaStream_t st) {
+  const SlabGeom GB{L.stride, N, L.b_off};
+  for (int k0 = 0; k0 < N; k0 += BW) {
+    chol_panel_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, L, N, k0, status, mat0);
+    const int m = N - k0 - BW;
+    if (m > 0)
+      rank_update_kernel<64><<<dim3((unsigned)((m + RU_T - 1) / RU_T), (unsigned)((m + 63) / 64), (unsigned)cnt), 256,
+                               ru_smem<64>(), st>>>(ws, GB, k0 + BW, k0 + BW, m, m,
+                                                    L.b_off + (size_t)k0 * N + k0 + BW,
+                                                    L.b_off + (size_t)k0 * N + k0 + BW);
+    count_launch(m > 0 ? 2 : 1);
+  }
+  band_trsm_left(ws, L, N, cnt, st);
+  const int nt = (N + BW - 1) / BW;
+  conj_transpose_kernel<<<dim3((unsigned)(nt * (nt + 1) / 2), (unsigned)cnt), 256, 0, st>>>(ws, L, N);
+  count_launch();
+  band_trsm_left(ws, L, N, cnt, st);
+  BAND_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// ------------------------------------------------------------------------------------------------
 
 constexpr size_t W_ROWS_SMEM = (size_t)(2 * BW * BW + 64 * (BW + 1)) * sizeof(double2);
 
@@ -342,6 +555,8 @@ void band_init_attributes() {
   set_smem_attr(w_rows_kernel, (int)W_ROWS_SMEM);
   cudaFuncSetAttribute(panel_qr_reg_kernel<16, 8, 32>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   set_smem_attr(band_assemble_kernel, 64 * 1024);
+  set_smem_attr(band_assemble_general_kernel, 64 * 1024);
+  set_smem_attr(rank_update_kernel<64>, (int)ru_smem<64>());
   set_smem_attr(her2k_kernel, (int)HK_SMEM);
   set_smem_attr(xv_kernel<0>, (int)XV_SMEM);
   set_smem_attr(xv_kernel<1>, (int)XV_SMEM);
@@ -427,7 +642,8 @@ int band_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks
               int* diff, unsigned long long* trans, double* eigs, int* status, int sharp, size_t ws_budget,
               const Alloc& alloc, cudaStream_t st, RefineItem* refine, unsigned long long* refine_count) {
   const int N = c.N;
-  const BandWs L = BandWs::make(N);
+  const bool general = c.pencil == 2;  // HX_PENCIL_GENERAL
+  const BandWs L = BandWs::make(N, general);
   const size_t per = L.stride * sizeof(double2) + sizeof(int) + (size_t)N * 8;
   const int64_t nmat = nmasks * nk;
   int64_t chunk = std::max<int64_t>(1, (int64_t)(ws_budget / per));
@@ -443,9 +659,16 @@ int band_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks
   const size_t smem = (size_t)N * sizeof(int);
   for (int64_t m0 = 0; m0 < nmat; m0 += chunk) {
     const int64_t cnt = std::min(chunk, nmat - m0);
-    band_assemble_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, masks, m0, ws, L, dims, status);
-    count_launch();
-    BAND_CUDA(cudaGetLastError());
+    if (general) {
+      band_assemble_general_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, masks, m0, ws, L, dims, status);
+      count_launch();
+      BAND_CUDA(cudaGetLastError());
+      if (band_reduce_pencil(ws, L, N, cnt, status, m0, st)) return -1;
+    } else {
+      band_assemble_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, masks, m0, ws, L, dims, status);
+      count_launch();
+      BAND_CUDA(cudaGetLastError());
+    }
     if (band_reduce(ws, L, N, cnt, dims, st)) return -1;
     launch_eig_idos(c, nk, g, m0, cnt, reinterpret_cast<const double*>(ws + L.dg_off), L.stride * 2, dims, diff,
                     trans, eigs, status, sharp, st, refine, refine_count);

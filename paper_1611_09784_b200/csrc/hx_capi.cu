@@ -45,6 +45,10 @@ long opt(const char* name, long dflt) {
 
 namespace {
 
+// general pencils above the shared-memory tier: Cholesky + the two-stage banded path (HX_GENERAL_BAND=0: the
+// single-CTA global-memory kernel)
+bool general_band() { return hx::opt("HX_GENERAL_BAND", 1) != 0; }
+
 thread_local std::string g_err;
 
 int fail(int code, const std::string& msg) {
@@ -556,7 +560,7 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
                          [&](size_t bytes) -> void* { return ctx->band.grow(bytes) ? nullptr : ctx->band.p; }, st,
                          refine, refine_count);
     if (rc) return fail(HX_E_CUDA, std::string("bipartite band path: ") + hx::bd_last_error());
-  } else if (c.pencil != HX_PENCIL_GENERAL && hx::band_path_supported(N)) {
+  } else if (hx::band_path_supported(N) && (c.pencil != HX_PENCIL_GENERAL || general_band())) {
     if (make_refine(nmat * N)) return fail(HX_E_CUDA, "alloc refinement list");
     int rc = hx::band_eval(c, kp, nk, d_masks, nmasks, g, diff, trans, d_eigs,
                            reinterpret_cast<int*>(d_status), sharp, ctx->ws_budget,

@@ -166,3 +166,69 @@ def test_c5_rectangular_sizes(nu, nu2, count):
         assert np.max(np.abs(eigs[m, :, :d] - ref)) <= EIG_TOL * (ref.max() - ref.min())
         rc = O.idos_from_bands(ref, np.ones(1), LO_G, HI_G, NPTS, 0.01, ocell.area)
         np.testing.assert_allclose(curves[m], rc, rtol=0, atol=IDOS_TOL)
+
+
+# ---- general pencils above the shared-memory tier (overlap tables: Cholesky + banded two-stage) ---------------
+def _general_models(kind):
+    """(native model, oracle dict) of a pencil with overlap couplings (zhegv in the reference)."""
+    if kind == "graphene":
+        hops, ovl = [], []
+        for di, dj in ((0, 0), (-1, 0), (0, -1)):
+            ovl += [(di, dj, 0, 0, 1, 0, 0.129 + 0j), (-di, -dj, 1, 0, 0, 0, 0.129 + 0j)]
+            hops += [(di, dj, 0, 0, 1, 0, -3.033 + 0j), (-di, -dj, 1, 0, 0, 0, -3.033 + 0j)]
+        onsite = [(0, 0, 0.0), (1, 0, 0.0)]
+        orbs, removable = (1, 1), ("A", "B")
+    else:  # two orbitals per site, complex hops and overlaps, B removable
+        rng = np.random.default_rng(12)
+        hops, ovl = [], []
+        for di, dj in ((0, 0), (-1, 0), (0, -1)):
+            for oa in range(2):
+                for ob in range(2):
+                    h = complex(rng.normal(-1.0, 0.3), rng.normal(0, 0.2))
+                    s = complex(rng.uniform(0.02, 0.06), rng.normal(0, 0.01))
+                    hops += [(di, dj, 0, oa, 1, ob, h), (-di, -dj, 1, ob, 0, oa, h.conjugate())]
+                    ovl += [(di, dj, 0, oa, 1, ob, s), (-di, -dj, 1, ob, 0, oa, s.conjugate())]
+        onsite = [(0, 0, 0.3), (0, 1, 0.7), (1, 0, -0.2), (1, 1, 0.1)]
+        orbs, removable = (2, 2), ("B",)
+    model = hx.MultiOrbitalModel(orbitals=(("A", orbs[0]), ("B", orbs[1])), onsite=tuple(onsite), hops=tuple(hops),
+                                 overlap=tuple(ovl), removable=removable)
+    om = {"orbitals": orbs, "removable": tuple({"A": 0, "B": 1}[r] for r in removable), "onsite": onsite,
+          "hops": hops, "overlap": ovl}
+    return model, om
+
+
+@pytest.mark.parametrize("kind,nu,q", [("graphene", 10, 1), ("graphene", 12, 2), ("twoorb", 6, 2), ("twoorb", 9, 1)])
+def test_general_pencil_banded_tier(kind, nu, q):
+    model, om = _general_models(kind)
+    spec = model.lattice_spec()
+    sc = hx.build_supercell(spec, nu)
+    cell = hx.compile_cell(model, sc)
+    assert cell.pencil == _lib.HX_PENCIL_GENERAL and cell.dim > 160
+    kp = np.ascontiguousarray(hx.make_bz_grid(spec, nu, q, "reduced").kpoints)
+    words = sample_masks(sc.nunits, 0.05, 2026, 3, 0, 3)
+    lo, hi = -12.0, 14.0
+    step = (hi - lo) / (NPTS - 1)
+    curves, eigs, status = eval_batch(cell, kp, words, lo, step, NPTS, 0.01, want_eigs=True)
+    assert (status == 0).all()
+    ocell = O.make_cell(om, nu)
+    for m in (0, 2):
+        ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
+        d = ref.shape[1]
+        assert np.max(np.abs(eigs[m, :, :d] - ref)) <= EIG_TOL * (ref.max() - ref.min())
+        rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), lo, hi, NPTS, 0.01, ocell.area)
+        np.testing.assert_allclose(curves[m], rc, rtol=0, atol=IDOS_TOL)
+    with _lib.options(HX_GENERAL_BAND=0):  # the single-CTA global kernel agrees
+        c2, _, _ = eval_batch(cell, kp, words, lo, step, NPTS, 0.01)
+    np.testing.assert_allclose(c2, curves, rtol=0, atol=1e-10)
+
+
+def test_general_pencil_banded_tier_non_pd_raises():
+    hops, ovl = [], []
+    for di, dj in ((0, 0), (-1, 0), (0, -1)):
+        ovl += [(di, dj, 0, 0, 1, 0, 0.5 + 0j), (-di, -dj, 1, 0, 0, 0, 0.5 + 0j)]
+        hops += [(di, dj, 0, 0, 1, 0, -1.0 + 0j), (-di, -dj, 1, 0, 0, 0, -1.0 + 0j)]
+    model = hx.MultiOrbitalModel(orbitals=(("A", 1), ("B", 1)), onsite=((0, 0, 0.0), (1, 0, 0.0)), hops=tuple(hops),
+                                 overlap=tuple(ovl), removable=("A", "B"))
+    sc = hx.build_supercell(model.lattice_spec(), 10)
+    with pytest.raises(hx.SolverError, match="not positive definite"):
+        hx.solve_bands(model, sc, None, hx.make_bz_grid(model.lattice_spec(), 10, 1, "reduced"))
