@@ -374,9 +374,21 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
   auto smem_of = [&](size_t need) {
     return cap > 0 && want < 6 && want >= 2 ? std::max(need, (size_t)(220 * 1024) / cap) : need;
   };
-#define BD_CHASE_REAL(NW)                                                                                 \
-  bd_chase_real_kernel<NW, BB><<<(unsigned)cnt, NW * 32, smem_of(bd_chase_real_smem<NW, BB>()), st>>>( \
-      ws2, a1, L.band_off, a3, S, dims)
+  // register-row chase for the many-matrix launches (HX_CHASE_REG=1 forces it everywhere, =0 off): measured
+  // 7.19 -> 6.69 ms on the 1024-matrix N = 512 launch; the one-CTA-per-matrix launches (16 warps) keep the
+  // shared-memory-tile kernel, whose 93 registers leave room on their SMs for the concurrent tiers' blocks
+  // (the 128-register variant fills the register file: c2 step 63.7 -> 64.7 ms)
+  const int reg_opt = (int)opt("HX_CHASE_REG", -1);
+  const bool regrow = reg_opt >= 0 ? reg_opt != 0 : want < 6;
+#define BD_CHASE_REAL(NW)                                                                                  \
+  do {                                                                                                     \
+    if (regrow)                                                                                            \
+      bd_chase_realr_kernel<NW><<<(unsigned)cnt, NW * 32, smem_of(bd_chase_realr_smem<NW>()), st>>>(       \
+          ws2, a1, L.band_off, a3, S, dims);                                                               \
+    else                                                                                                   \
+      bd_chase_real_kernel<NW, BB><<<(unsigned)cnt, NW * 32, smem_of(bd_chase_real_smem<NW, BB>()), st>>>( \
+          ws2, a1, L.band_off, a3, S, dims);                                                               \
+  } while (0)
   if (want >= 6 && rnw > 0) BD_CHASE_REAL(16);
   else if (rnw == 1) BD_CHASE_REAL(1);
   else if (rnw == 2) BD_CHASE_REAL(2);
@@ -385,9 +397,15 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
   else if (rnw == 16) BD_CHASE_REAL(16);
   else if (want >= 6 && rcl > 1) {
     // few matrices with long sweeps: CL CTAs (SMs) per matrix, CL x 16 sweeps in flight
-#define BD_CHASE_REAL_CL(CLN)                                                                                \
-  bd_chase_real_kernel<16, BB, CLN><<<(unsigned)(cnt * CLN), 16 * 32, bd_chase_real_smem<16, BB>(), st>>>( \
-      ws2, a1, L.band_off, a3, S, dims)
+#define BD_CHASE_REAL_CL(CLN)                                                                                 \
+  do {                                                                                                        \
+    if (regrow)                                                                                               \
+      bd_chase_realr_kernel<16, CLN><<<(unsigned)(cnt * CLN), 16 * 32, bd_chase_realr_smem<16>(), st>>>(      \
+          ws2, a1, L.band_off, a3, S, dims);                                                                  \
+    else                                                                                                      \
+      bd_chase_real_kernel<16, BB, CLN><<<(unsigned)(cnt * CLN), 16 * 32, bd_chase_real_smem<16, BB>(), st>>>( \
+          ws2, a1, L.band_off, a3, S, dims);                                                                  \
+  } while (0)
     if (rcl == 2) BD_CHASE_REAL_CL(2);
     else if (rcl == 4) BD_CHASE_REAL_CL(4);
     else BD_CHASE_REAL_CL(8);
@@ -438,6 +456,14 @@ void bd_init_attributes() {
   set_smem_attr(bd_chase_real_kernel<16, BB, 8>, bd_chase_real_smem<16, BB>());
   set_smem_attr(bd_chase_real_kernel<4, BB>, 220 * 1024);
   set_smem_attr(bd_chase_real_kernel<8, BB>, 220 * 1024);
+  set_smem_attr(bd_chase_realr_kernel<1>, 220 * 1024);
+  set_smem_attr(bd_chase_realr_kernel<2>, 220 * 1024);
+  set_smem_attr(bd_chase_realr_kernel<4>, 220 * 1024);
+  set_smem_attr(bd_chase_realr_kernel<8>, 220 * 1024);
+  set_smem_attr(bd_chase_realr_kernel<16>, 220 * 1024);
+  set_smem_attr(bd_chase_realr_kernel<16, 2>, bd_chase_realr_smem<16>());
+  set_smem_attr(bd_chase_realr_kernel<16, 4>, bd_chase_realr_smem<16>());
+  set_smem_attr(bd_chase_realr_kernel<16, 8>, bd_chase_realr_smem<16>());
   const char* sp = getenv("HX_CHASE_SPIN_NS");
   if (sp && sp[0]) {
     const unsigned v = (unsigned)atoi(sp);

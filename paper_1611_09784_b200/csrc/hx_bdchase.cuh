@@ -605,6 +605,232 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NW * 32, 1)
   if constexpr (CL > 1) cooperative_groups::this_cluster().sync();  // remote pollers may still read our counters
 }
 
+// ---------------------------------------------------------------------------------------------------
+// Register-row variant of the real chase (HX_CHASE_REG, default on): the lane's row of the X tile (then of the
+// Y tile) is loaded from the band straight into 32 registers (coalesced: a tile column is 32 consecutive
+// doubles of the compact band), the row passes and the rank-2 row updates run on those registers, and the tile
+// goes to shared memory once, TRANSPOSED (Xt[c][r], stride 33), only for the column pass (lane = column).
+// Against bd_chase_real_kernel (tile in shared memory, read by every pass): the shared-memory data pipe - the
+// measured limit of that kernel, 67-77 % of peak with 4-way conflicted 8-byte tile fills - carries about a
+// third of the wavefronts per task (fills conflict-free, row passes read only the broadcast vectors).
+struct __align__(16) BdChaseSmemRR {
+  double ug[32], vh[32], cb[32];
+  double Xt[32][33];  // X^T (then Y^T): Xt[c][r] = tile (r, c)
+};
+
+template <int CL>
+__device__ __forceinline__ double ld_band(const double* p) {
+  if constexpr (CL > 1) return __ldcg(p);  // written by other SMs of the cluster: through L2
+  else return *p;
+}
+
+// Row `lane` of a 32 x 32 tile of the compact band into registers: r[cc] = (s + lane, c0 + cc) at p[cc * (RB_LD - 1)];
+// columns >= ncols (and every column when ncols = 0: padded rows) read as zero.
+template <int CL>
+__device__ __forceinline__ void load_row(double (&r)[32], const double* p, bool full, int ncols) {
+  if (full) {
+#pragma unroll
+    for (int cc = 0; cc < 32; ++cc) r[cc] = ld_band<CL>(p + cc * (RB_LD - 1));
+  } else {
+#pragma unroll
+    for (int cc = 0; cc < 32; ++cc) r[cc] = cc < ncols ? ld_band<CL>(p + cc * (RB_LD - 1)) : 0.0;
+  }
+}
+
+// Register budget: 128 per thread (4 CTAs of 4 warps per SM for the many-matrix launches).
+template <int NW, int CL = 1>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NW * 32, NW == 4 ? 4 : (NW <= 2 ? 8 : 1))
+    bd_chase_realr_kernel(double2* ws, size_t stride, size_t band_off, size_t tgk_off, int S, const int* dims) {
+  constexpr int BWc = 32;
+  extern __shared__ __align__(16) unsigned char bd_smem[];
+  BdChaseSmemRR* all = reinterpret_cast<BdChaseSmemRR*>(bd_smem);
+  volatile int* prog = reinterpret_cast<volatile int*>(all + NW);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  BdChaseSmemRR& W = all[warp];
+  const int rank = CL > 1 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
+  const int gw = rank * NW + warp;
+  constexpr int TW = CL * NW;
+  const int64_t mat = blockIdx.x / CL;
+  double2* base = ws + (size_t)mat * stride;
+  double* B = reinterpret_cast<double*>(base + band_off);
+  double* diag = reinterpret_cast<double*>(base + tgk_off);
+  double* e2 = diag + 2 * S;
+  for (int q = threadIdx.x + rank * blockDim.x; q < 2 * S; q += blockDim.x * CL) {
+    diag[q] = 0.0;
+    e2[q] = 0.0;
+  }
+  if (lane == 0) prog[warp] = -1;
+  if constexpr (CL > 1) {
+    __threadfence();
+    cooperative_groups::this_cluster().sync();
+  } else {
+    __syncthreads();
+  }
+  if (rank == 0 && threadIdx.x == 0) {
+    const double a0 = B[RB_OFF];
+    e2[0] = a0 * a0;  // alpha_0: final after stage 1
+  }
+  const bool skip = dims && dims[mat] == 0;
+  const int nsweeps = skip ? 0 : S - 1;
+  for (int i = gw; i < nsweeps; i += TW) {
+    const int tasks = (S - 1 - i + BWc - 1) / BWc;
+    const int prev_tasks = i > 0 ? (S - i + BWc - 1) / BWc : 0;
+    volatile int* pflag;  // progress counter of the warp that owns sweep i - 1
+    {
+      const int gp = (i - 1 + TW) % TW;
+      if constexpr (CL > 1)
+        pflag = cooperative_groups::this_cluster().map_shared_rank(const_cast<int*>(prog), gp / NW) + gp % NW;
+      else pflag = prog + gp;
+    }
+    double taug = 0.0;
+    for (int t = 0; t < tasks; ++t) {
+      if (i > 0) {
+        const int need = (i - 1) * 65536 + min(t + 2, prev_tasks);
+        if (lane == 0)
+          while (*pflag < need) __nanosleep(g_spin_ns);
+        __syncwarp();
+        if constexpr (CL > 1) __threadfence();
+        else __threadfence_block();
+      }
+      const int s = i + 1 + t * BWc;
+      const int len = min(BWc, S - s);
+      const int lb = max(0, min(BWc, S - s - len));
+      // element (s + lane, s + cc) at blk[cc * (RB_LD - 1)]
+      double* const blk = B + ((size_t)s * RB_LD + lane + RB_OFF);
+      double xr[BWc];
+      load_row<CL>(xr, blk, len == BWc, lane < len ? len : 0);
+      if (t == 0) {
+        // right reflector from row i, columns [s, s+len): row i -> (beta, 0, ...)
+        double* const rowi = B + ((size_t)(s + lane) * RB_LD + i - (s + lane) + RB_OFF);  // (i, s + lane)
+        const double x = lane < len ? ld_band<CL>(rowi) : 0.0;
+        const double sig2 = warp_sum(x * x);
+        const QuickReflectorR h = quick_reflector_r(__shfl_sync(0xffffffffu, x, 0), sig2);
+        taug = h.tau;
+        W.ug[lane] = lane == 0 ? 1.0 : (lane < len ? x * h.scale : 0.0);
+        if (lane < len && taug != 0.0) *rowi = lane == 0 ? h.beta : 0.0;
+        if (lane == 0) e2[2 * i + 1] = sig2;
+      }
+#pragma unroll
+      for (int cc = 0; cc < BWc; ++cc) W.Xt[cc][lane] = xr[cc];
+      __syncwarp();
+      // ---- X row pass (registers): ty = tau_g (X u)_r; column 0 of X G -> left reflector H
+      double ty;
+      {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < BWc; c += 2) {
+          const double2 u = lds2(&W.ug[c]);
+          a0 = fma(xr[c], u.x, a0);
+          a1 = fma(xr[c + 1], u.y, a1);
+        }
+        ty = taug * (a0 + a1);
+      }
+      const double x0 = xr[0] - ty;
+      double sh2 = x0 * x0, xt = lane == 0 ? 0.0 : x0 * ty;
+      warp_sum2(sh2, xt);
+      const QuickReflectorR hh = quick_reflector_r(__shfl_sync(0xffffffffu, x0, 0), sh2);
+      const double tauh = hh.tau;
+      if (t == 0 && lane == 0) e2[2 * s] = sh2;
+      const double v = lane == 0 ? 1.0 : x0 * hh.scale;  // zero on padded rows
+      W.vh[lane] = v;
+      const double w = fma(hh.scale, xt, __shfl_sync(0xffffffffu, ty, 0));
+      __syncwarp();
+      // ---- X column pass (lane = column, X^T in shared memory): b_c = tau_h (v^T X_c - w u_c)
+      {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int r = 0; r < BWc; r += 2) {
+          const double2 vv = lds2(&W.vh[r]);
+          a0 = fma(vv.x, W.Xt[lane][r], a0);
+          a1 = fma(vv.y, W.Xt[lane][r + 1], a1);
+        }
+        W.cb[lane] = tauh * (a0 + a1 - w * W.ug[lane]);
+      }
+      __syncwarp();
+      // ---- X: fused rank-2 row update on the registers, straight to HBM: X' = X - ty u^T - v b^T
+      if (lane < len) {
+#pragma unroll
+        for (int c = 0; c < BWc; c += 2) {
+          const double2 u = lds2(&W.ug[c]), b = lds2(&W.cb[c]);
+          double z0 = fma(-v, b.x, fma(-ty, u.x, xr[c]));
+          const double z1 = fma(-v, b.y, fma(-ty, u.y, xr[c + 1]));
+          if (c == 0 && tauh != 0.0) z0 = lane == 0 ? hh.beta : 0.0;
+          if (c < len) blk[c * (RB_LD - 1)] = z0;
+          if (c + 1 < len) blk[(c + 1) * (RB_LD - 1)] = z1;
+          if ((c & 7) == 6) asm volatile("" ::: "memory");  // bound the broadcast loads in flight (registers)
+        }
+      }
+      double next_tau = 0.0;
+      if (lb > 0) {
+        // (s + lane, s + len + cc)
+        load_row<CL>(xr, blk + (size_t)len * (RB_LD - 1), len == BWc && lb == BWc, lane < len ? lb : 0);
+#pragma unroll
+        for (int cc = 0; cc < BWc; ++cc) W.Xt[cc][lane] = xr[cc];
+        __syncwarp();
+        // ---- Y column pass: q = v^T Y; row 0 of H Y -> next right reflector G'
+        double q;
+        {
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int r = 0; r < BWc; r += 2) {
+            const double2 vv = lds2(&W.vh[r]);
+            a0 = fma(vv.x, W.Xt[lane][r], a0);
+            a1 = fma(vv.y, W.Xt[lane][r + 1], a1);
+          }
+          q = a0 + a1;
+        }
+        const double xg = W.Xt[lane][0] - tauh * q;  // row 0 of H Y
+        double sg2 = xg * xg, qx = lane == 0 ? 0.0 : q * xg;
+        warp_sum2(sg2, qx);
+        const QuickReflectorR hg = quick_reflector_r(__shfl_sync(0xffffffffu, xg, 0), sg2);
+        next_tau = hg.tau;
+        const double u2 = lane == 0 ? 1.0 : xg * hg.scale;  // zero on padded columns
+        const double qu = fma(hg.scale, qx, __shfl_sync(0xffffffffu, q, 0));
+        __syncwarp();  // everyone is done with ug (X update) and cb
+        W.ug[lane] = u2;
+        W.cb[lane] = tauh * q;  // d_c
+        __syncwarp();
+        // ---- Y row pass (registers): f = tau_g' (Y u' - tau_h v (q . u')), Y' = Y - v d^T - f u'^T, to HBM
+        if (lane < len) {
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int c = 0; c < BWc; c += 2) {
+            const double2 u = lds2(&W.ug[c]);
+            a0 = fma(xr[c], u.x, a0);
+            a1 = fma(xr[c + 1], u.y, a1);
+          }
+          const double f = next_tau * (a0 + a1 - tauh * v * qu);
+          const bool row0 = lane == 0 && next_tau != 0.0;
+          double* const dst = blk + (size_t)len * (RB_LD - 1);
+#pragma unroll
+          for (int c = 0; c < BWc; c += 2) {
+            const double2 u = lds2(&W.ug[c]), b = lds2(&W.cb[c]);
+            double z0 = fma(-f, u.x, fma(-v, b.x, xr[c])), z1 = fma(-f, u.y, fma(-v, b.y, xr[c + 1]));
+            if (row0) {
+              z0 = c == 0 ? hg.beta : 0.0;
+              z1 = 0.0;
+            }
+            if (c < lb) dst[c * (RB_LD - 1)] = z0;
+            if (c + 1 < lb) dst[(c + 1) * (RB_LD - 1)] = z1;
+            if ((c & 7) == 6) asm volatile("" ::: "memory");
+          }
+        }
+      }
+      taug = next_tau;
+      if constexpr (CL > 1) __threadfence();
+      else __threadfence_block();
+      __syncwarp();
+      if (lane == 0) prog[warp] = i * 65536 + t + 1;
+    }
+  }
+  if constexpr (CL > 1) cooperative_groups::this_cluster().sync();  // remote pollers may still read our counters
+}
+
+template <int NW>
+constexpr size_t bd_chase_realr_smem() {
+  return NW * sizeof(BdChaseSmemRR) + 64;
+}
+
 // Real parts of the upper band (and the zero window around it) of the dense S x S slab C into the compact
 // band buffer of the real chase.  One CTA per matrix.
 static __global__ void __launch_bounds__(256) bd_band_extract_kernel(double2* ws, size_t stride, size_t c_off,

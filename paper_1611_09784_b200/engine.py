@@ -59,6 +59,8 @@ SLMC_STREAM_OFFSET = 10_000
 # cache in each worker (runner.py:98-111).  Rebuilding them per Engine costs a few ms of uploads, and
 # releasing them (cudaFree) synchronises the device.
 _CELL_CACHE: dict = {}
+# k-point sets (and their time-reversal reduction) per (lattice, n, q): process-wide like the cells
+_KGRID_CACHE: dict = {}
 # Concurrent tier schedule of the seam: the largest tier is planned and submitted first (it is the critical
 # path), then the others smallest first; the small tiers (dim <= 128) run on the greatest stream priority so
 # that their levels finish early and the host work of placing them overlaps the device work still running,
@@ -92,6 +94,26 @@ def first_rows(inv):
     if len(inv) == 0:
         return np.zeros(0, dtype=np.int64)
     return np.unique(inv, return_index=True)[1]
+
+
+class _InlineExecutor:
+    """Executor interface that runs the submitted call immediately (single-piece batches)."""
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+    def submit(self, fn, *args, **kw):
+        from concurrent.futures import Future
+
+        f = Future()
+        try:
+            f.set_result(fn(*args, **kw))
+        except BaseException as exc:  # noqa: BLE001 - delivered through the future like a pool would
+            f.set_exception(exc)
+        return f
 
 
 class _TierCache:
@@ -190,7 +212,6 @@ class Engine:
         self._coll_tickets = 0
         self._supercells: dict = {}
         self._cells: dict = {}
-        self._kgrids: dict = {}
         if energy_range is None:
             emin, emax = self.detect_energy_range()
         else:
@@ -202,7 +223,10 @@ class Engine:
     # -- geometry / caches --
     def supercell(self, n: int):
         if n not in self._supercells:
-            self._supercells[n] = build_supercell(self.model.lattice_spec(), n)
+            key = ("sc", self.model.lattice_spec(), n)
+            if key not in _KGRID_CACHE:
+                _KGRID_CACHE[key] = build_supercell(self.model.lattice_spec(), n)
+            self._supercells[n] = _KGRID_CACHE[key]
         return self._supercells[n]
 
     def cell(self, n: int, device: int | None = None):
@@ -223,22 +247,20 @@ class Engine:
 
     def kpoints(self, n: int, q: int) -> np.ndarray:
         """k-points solved for (n, q): the base q x q rhombus (full mode's rotated copies are images)."""
-        key = (n, q)
-        if key not in self._kgrids:
-            self._kgrids[key] = make_bz_grid(self.model.lattice_spec(), n, q, "reduced").kpoints
-        return self._kgrids[key]
+        key = (self.model.lattice_spec(), n, q)
+        if key not in _KGRID_CACHE:
+            _KGRID_CACHE[key] = make_bz_grid(self.model.lattice_spec(), n, q, "reduced").kpoints
+        return _KGRID_CACHE[key]
 
     def kpoints_tr(self, n: int, q: int):
         """(k-points, multiplicities) of the IDOS batches: time-reversal pairs merged for real-amplitude
         models (solver.time_reversal_reduce), otherwise the full base grid with multiplicity 1."""
-        key = ("tr", n, q)
-        if key not in self._kgrids:
+        tr = use_time_reversal() and self.cell(n).time_reversal_symmetric
+        key = ("tr", self.model.lattice_spec(), n, q, tr)
+        if key not in _KGRID_CACHE:
             kp = self.kpoints(n, q)
-            if use_time_reversal() and self.cell(n).time_reversal_symmetric:
-                self._kgrids[key] = time_reversal_reduce(self.model.lattice_spec(), n, kp)
-            else:
-                self._kgrids[key] = (kp, None)
-        return self._kgrids[key]
+            _KGRID_CACHE[key] = time_reversal_reduce(self.model.lattice_spec(), n, kp) if tr else (kp, None)
+        return _KGRID_CACHE[key]
 
     def q_of(self, n: int) -> int:
         if self.nq % n:
@@ -403,7 +425,9 @@ class Engine:
         plans = {}  # (bi, gi) -> (tier, uniq, inv, keys, src)
         pieces = {}  # tier -> [(first new row, future)] in row order
         lane = 0
-        with ThreadPoolExecutor(max_workers=max(1, sum(len(v) for v in tiers.values()))) as ex:
+        npieces = sum(len(v) for v in tiers.values())
+        # one piece (a single-level run): solve it inline, without a thread pool
+        with (_InlineExecutor() if npieces == 1 else ThreadPoolExecutor(max_workers=max(1, npieces))) as ex:
             for tier in order:
                 cache = self._tier_cache(tier, npts)
                 pend = np.zeros(0, dtype=np.int64)  # sorted keys of this call's new masks so far, their rows
@@ -572,7 +596,8 @@ class Engine:
             qc, qpj = res[1]
             quarters = qc.reshape(nsamples, 4, npts)
             nominal += float(qpj.sum())
-        terms, mean, var = level_moments(full, quarters, self.device)
+        # without the CV the level terms are the curves themselves: no device round trip for them
+        terms, mean, var = level_moments(full, quarters, self.device, want_terms=quarters is not None)
         rank, world = self.shard
         if world > 1 and self.shard_mode == "replicas":
             # exact cross-rank combination (fixed-point limbs, int64 all-reduce): the bits of one process
@@ -587,9 +612,9 @@ class Engine:
             nsamples_all = nsamples * world
         else:
             nsamples_all = nsamples
-        terms = terms.cpu().numpy()
         self.io_bytes[0] += full.nbytes + (0 if quarters is None else quarters.nbytes)
-        self.io_bytes[1] += terms.nbytes + 2 * mean.numel() * 8
+        self.io_bytes[1] += (0 if terms is None else full.nbytes) + 2 * mean.numel() * 8
+        terms = full.copy() if terms is None else terms.cpu().numpy()
         cv = None
         if quarters is not None:
             # cv exactly as the reference forms it: ((q1 + q2) + q3 + q4) * 0.25

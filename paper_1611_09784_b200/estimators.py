@@ -104,10 +104,11 @@ def window_mask(grid, window=None) -> np.ndarray:
     return mask
 
 
-def level_moments(full, quarters=None, device: int = 0):
+def level_moments(full, quarters=None, device: int = 0, want_terms: bool = True):
     """(terms, mean, var) on the GPU; `full` [M, npts], `quarters` [M, 4, npts] or None.
 
-    Accepts numpy arrays or CUDA torch tensors; returns torch tensors on the device.
+    Accepts numpy arrays or CUDA torch tensors; returns torch tensors on the device (terms None when
+    want_terms is False).  Host arrays go up through pinned staging (asynchronous DMA on the moments stream).
     """
     import torch
 
@@ -116,17 +117,24 @@ def level_moments(full, quarters=None, device: int = 0):
     # occupy the SMs - the priority puts their blocks ahead of the queued solve blocks
     st = _moments_stream(device)
     st.wait_stream(torch.cuda.current_stream(dev))
+
+    def up(a):
+        if isinstance(a, torch.Tensor):
+            return a.to(dev, dtype=torch.float64).contiguous()
+        h = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).pin_memory()
+        return h.to(dev, non_blocking=True)
+
     with torch.cuda.stream(st):
-        f = torch.as_tensor(full, dtype=torch.float64).to(dev, non_blocking=False).contiguous()
+        f = up(full)
         M, npts = f.shape
-        q = None if quarters is None else torch.as_tensor(quarters, dtype=torch.float64).to(dev).contiguous()
-        terms = torch.empty_like(f)
+        q = None if quarters is None else up(quarters)
+        terms = torch.empty_like(f) if want_terms else None
         mean = torch.empty(npts, dtype=torch.float64, device=dev)
         var = torch.empty(npts, dtype=torch.float64, device=dev)
         _lib.Device.ctx(device)
         _lib.check(_lib.load().hx_level_moments_device(f.data_ptr(), 0 if q is None else q.data_ptr(), M, npts,
-                                                       terms.data_ptr(), mean.data_ptr(), var.data_ptr(),
-                                                       st.cuda_stream),
+                                                       0 if terms is None else terms.data_ptr(), mean.data_ptr(),
+                                                       var.data_ptr(), st.cuda_stream),
                    "hx_level_moments_device")
     torch.cuda.current_stream(dev).wait_stream(st)
     return terms, mean, var

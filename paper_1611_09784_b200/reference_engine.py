@@ -160,14 +160,17 @@ def cuda_solve_bands(spectrum):
 
 
 def install(hexmc):
-    """Point the reference CLI (hexmc.cli) at libhx: its Engine's batch seam and its bands-mode solve.
-    Returns the Engine class installed.  Everything else (config, drivers, artefact writers) stays the
-    reference's code."""
+    """Point the reference CLI (hexmc.cli) at libhx: its Engine's batch seam, its bands-mode solve and the
+    Engine's energy-range detection (runner.py:189-202, which calls solve_bands on the nu = 1 cell).  Returns
+    the Engine class installed.  Everything else (config, drivers, artefact writers) stays the reference's
+    code."""
     import hexmc.cli
     import hexmc.runner
     import hexmc.spectrum
 
     engine_cls = cuda_engine_class(hexmc.runner.Engine)
+    gpu_solve = cuda_solve_bands(hexmc.spectrum)
     hexmc.cli.Engine = engine_cls
-    hexmc.cli.solve_bands = cuda_solve_bands(hexmc.spectrum)
+    hexmc.cli.solve_bands = gpu_solve
+    hexmc.runner.solve_bands = gpu_solve
     return engine_cls

@@ -77,7 +77,7 @@ def test_batches_match_sequential_reference(engine):
 
 
 def test_run_mlmc_equals_levels_in_order(engine, monkeypatch):
-    monkeypatch.setattr(E, "level_moments", lambda full, quarters, device: _np_moments(full, quarters))
+    monkeypatch.setattr(E, "level_moments", lambda full, quarters, device, want_terms=True: _np_moments(full, quarters))
     plan = hx.LevelPlan(ns=(2, 4, 8), samples=(64, 32, 8), nq=16, p_vac=0.2, delta=0.01)
     _, sets = engine.run_mlmc(plan)
     seq = FakeEngine(hx.GrapheneNNModel(), nq=16, delta=0.01, master_seed=7, bz_mode="reduced",

@@ -53,6 +53,7 @@ def test_reference_cli_bands_mode_on_libhx(tmp_path, monkeypatch):
     from paper_1611_09784_b200 import reference_engine
 
     monkeypatch.setattr(hexmc.cli, "solve_bands", hexmc.cli.solve_bands)  # restored after the test
+    monkeypatch.setattr(hexmc.runner, "solve_bands", hexmc.runner.solve_bands)
     monkeypatch.setattr(hexmc.cli, "Engine", hexmc.cli.Engine)
 
     def cfg(out):

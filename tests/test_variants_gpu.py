@@ -70,9 +70,11 @@ def check_batch(kind, nu, q, p, nmasks, seed, check, kp=None, opts=None, eigs_to
 
 
 # ---- real bulge chase: every warps-per-matrix variant, forced (nu = 16, q = 2: S = 256, real batch) ----------
+@pytest.mark.parametrize("reg", [1, 0])
 @pytest.mark.parametrize("rnw", [1, 2, 4, 8, 16])
-def test_real_chase_warp_variants_forced(rnw):
-    check_batch("graphene", 16, 2, 0.05, 6, 31, (0, 5), opts={"HX_CHASE_RNW": rnw})
+def test_real_chase_warp_variants_forced(rnw, reg):
+    """Register-row chase (HX_CHASE_REG=1, default) and shared-memory-tile chase, every warps-per-matrix count."""
+    check_batch("graphene", 16, 2, 0.05, 6, 31, (0, 5), opts={"HX_CHASE_RNW": rnw, "HX_CHASE_REG": reg})
 
 
 # ---- the variants the c2 batch sizes select by themselves ----------------------------------------------------
@@ -97,13 +99,14 @@ def test_clustered_real_chase_two_sms():
     check_batch("graphene", 32, 1, 0.05, 2, 5, (0, 1), opts={"HX_CHASE_RCL": 2})
 
 
+@pytest.mark.parametrize("reg", [1, 0])
 @pytest.mark.parametrize("rcl", [2, 4])
-def test_clustered_real_chase_nu46(rcl):
-    check_batch("graphene", 46, 1, 0.02, 1, 9, (0,), opts={"HX_CHASE_RCL": rcl})
+def test_clustered_real_chase_nu46(rcl, reg):
+    check_batch("graphene", 46, 1, 0.02, 1, 9, (0,), opts={"HX_CHASE_RCL": rcl, "HX_CHASE_REG": reg})
 
 
 # ---- real / complex storage and arithmetic switches -----------------------------------------------------------
-@pytest.mark.parametrize("opts", [{"HX_NO_REAL": 1}, {"HX_REAL_STAGE1": 0}, {"HX_CHASE_REAL": 0},
+@pytest.mark.parametrize("opts", [{"HX_NO_REAL": 1}, {"HX_REAL_STAGE1": 0}, {"HX_CHASE_REAL": 0}, {"HX_CHASE_REG": 0},
                                   {"HX_CHASE_PAIR": 0}, {"HX_REAL_FUSED": 1}, {"HX_FUSED_UPDATE": 1}])
 @pytest.mark.parametrize("nu,q", [(16, 2), (12, 1), (11, 1)])
 def test_real_path_switches(nu, q, opts):
@@ -197,7 +200,7 @@ def _general_models(kind):
     return model, om
 
 
-@pytest.mark.parametrize("kind,nu,q", [("graphene", 10, 1), ("graphene", 12, 2), ("twoorb", 6, 2), ("twoorb", 9, 1)])
+@pytest.mark.parametrize("kind,nu,q", [("graphene", 10, 1), ("graphene", 12, 2), ("twoorb", 7, 2), ("twoorb", 9, 1)])
 def test_general_pencil_banded_tier(kind, nu, q):
     model, om = _general_models(kind)
     spec = model.lattice_spec()
@@ -232,3 +235,38 @@ def test_general_pencil_banded_tier_non_pd_raises():
     sc = hx.build_supercell(model.lattice_spec(), 10)
     with pytest.raises(hx.SolverError, match="not positive definite"):
         hx.solve_bands(model, sc, None, hx.make_bz_grid(model.lattice_spec(), 10, 1, "reduced"))
+
+
+# ---- synchronisation safety of the flag-pipelined chases (compute-sanitizer is not available on this pool) -----
+@pytest.mark.parametrize("opts", [{"HX_CHASE_RNW": 16}, {"HX_CHASE_RNW": 4}, {"HX_CHASE_RNW": 1},
+                                  {"HX_CHASE_RNW": 16, "HX_CHASE_REG": 0}, {"HX_CHASE_RNW": 4, "HX_CHASE_REG": 0},
+                                  {"HX_CHASE_RCL": 2}, {"HX_CHASE_RCL": 2, "HX_CHASE_REG": 0},
+                                  {"HX_CHASE_REAL": 0}])
+def test_chase_results_bitwise_repeatable(opts):
+    """Every warp of a chase spins on its predecessor's progress counter before touching the band; a missing
+    acquire/release would let a task read a tile before the previous sweep wrote it, which shows up as
+    run-to-run differences.  The same batch is solved 12 times (with the GPU busy with a second batch on
+    another context in between) and must give identical bits every time."""
+    import threading
+
+    model = hx.GrapheneNNModel()
+    nu, q = (32, 1) if "HX_CHASE_RCL" in opts else (16, 2)
+    sc = hx.build_supercell(model.lattice_spec(), nu)
+    cell = hx.compile_cell(model, sc)
+    kp = np.ascontiguousarray(hx.make_bz_grid(model.lattice_spec(), nu, q, "reduced").kpoints)
+    words = sample_masks(sc.nunits, 0.05, 99, 1, 0, 8 if nu == 16 else 2)
+    step = (HI_G - LO_G) / (NPTS - 1)
+    other = _lib.Device.new_ctx(0, 0)
+    noise = sample_masks(sc.nunits, 0.05, 5, 1, 0, 16)
+    with _lib.options(**opts):
+        ref, eigs0, _ = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01, want_eigs=True)
+        for rep in range(12):
+            th = threading.Thread(target=eval_batch, args=(cell, kp, noise, LO_G, step, NPTS, 0.01),
+                                  kwargs={"ctx": other}) if rep % 3 == 0 else None
+            if th:
+                th.start()
+            cur, eigs, _ = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01, want_eigs=True)
+            if th:
+                th.join()
+            assert np.array_equal(cur, ref), rep
+            assert np.array_equal(eigs, eigs0, equal_nan=True), rep
