@@ -289,6 +289,16 @@ static bool launch_real_cluster_panel(double* ws, const RPanelArgs& a, int64_t c
   return true;
 }
 
+// bulk-copy persistent rank update (HX_RU_BULK=0: the load-compute-store kernel); one CTA per SM
+static void launch_rank_update_real_bulk(double* ws, const RSlab& G, int mr0, int mc0, int m, int n, size_t u_off,
+                                         size_t w_off, int64_t cnt, cudaStream_t st) {
+  const int ti = (m + RBU_T - 1) / RBU_T, tj = (n + RBU_T - 1) / RBU_T;
+  const int64_t ntiles = cnt * ti * tj;
+  if (ntiles <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, 148);
+  rank_update_real_bulk_kernel<<<grid, 256, rru_bulk_smem(), st>>>(ws, G, mr0, mc0, m, n, u_off, w_off, ti, tj, ntiles);
+}
+
 template <int RT>
 static void launch_rank_update_real(double* ws, const RSlab& G, int mr0, int mc0, int m, int n, size_t u_off,
                                     size_t w_off, int64_t cnt, cudaStream_t st) {
@@ -303,8 +313,13 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
                z = 2 * L.z_off, t1 = 2 * L.t1_off, t2 = 2 * L.t2_off;
   const RSlab G{sd, S, c0};
   const int ru_rt = opt("HX_RRU_RT", 64) == 128 ? 128 : 64;
+  // HX_RU_BULK=1: the persistent bulk-copy rank update (hx_real.cuh) - correct, but measured 3.2x slower
+  // (0.292 vs 0.090 ms per launch on the N = 2048 tier): one cp.async.bulk per 512-byte tile column is bound by
+  // the copy engine's per-request cost, not by HBM; kept as an option, off by default
+  const bool ru_bulk = opt("HX_RU_BULK", 0) != 0;
   auto rank_update = [&](int mr0, int mc0, int m, int n, size_t u, size_t w) {
-    if (ru_rt == 128) launch_rank_update_real<128>(ws, G, mr0, mc0, m, n, u, w, cnt, st);
+    if (ru_bulk) launch_rank_update_real_bulk(ws, G, mr0, mc0, m, n, u, w, cnt, st);
+    else if (ru_rt == 128) launch_rank_update_real<128>(ws, G, mr0, mc0, m, n, u, w, cnt, st);
     else launch_rank_update_real<64>(ws, G, mr0, mc0, m, n, u, w, cnt, st);
   };
   // Fused schedule (HX_REAL_FUSED=1 forces it on, =0 off; default on for S >= 2048): the trailing rank update
@@ -426,6 +441,7 @@ void bd_init_attributes() {
   set_smem_attr(xv_real_kernel<1, true>, (int)RXV_SMEM_UPD);
   set_smem_attr(rank_update_real_kernel<64>, (int)rru_smem<64>());
   set_smem_attr(rank_update_real_kernel<128>, (int)rru_smem<128>());
+  set_smem_attr(rank_update_real_bulk_kernel, (int)rru_bulk_smem());
   set_smem_attr(xv_kernel<0>, (int)XV_SMEM);
   set_smem_attr(xv_kernel<1>, (int)XV_SMEM);
   set_smem_attr(xv_kernel<0, true>, XV_SMEM_UPD);

@@ -203,7 +203,7 @@ static __device__ __forceinline__ void add_eigenvalue(const CellDev& c, const Gr
                                                       unsigned long long* trans, int* status, int64_t mat, int nk,
                                                       double lam) {
   const double E = pencil_map(c, lam);
-  if (!isfinite(E)) atomicMax(status + mat, 2);
+  if (!isfinite(E)) atomicCAS(status + mat, 0, 2);
   const int64_t mk = mat / nk;
   const int mult = kmul(g, mat, nk);
   if (sharp) sharp_state(g, E, diff + mk * (g.npts + 1), mult);
@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(128) eig_idos_kernel(CellDev c, int nk, GridDe
     if (!(done & 1)) add_eigenvalue(c, g, sharp, diff, trans, status, mat, nk, lam);
     if (!(done & 2)) add_eigenvalue(c, g, sharp, diff, trans, status, mat, nk, -lam);
   } else {
-    if (!isfinite(pencil_map(c, lam)) || (mirror && !isfinite(pencil_map(c, -lam)))) atomicMax(status + mat, 2);
+    if (!isfinite(pencil_map(c, lam)) || (mirror && !isfinite(pencil_map(c, -lam)))) atomicCAS(status + mat, 0, 2);
   }
   put(idx, pencil_map(c, lam));
   if (mirror) put(d - 1 - idx, pencil_map(c, -lam));

@@ -15,6 +15,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include "hx_bulk.cuh"
 #include "hx_dense.cuh"
 #include "hx_dmma.cuh"
 #include "hx_gemm.cuh"
@@ -501,6 +502,120 @@ __global__ void __launch_bounds__(256) rank_update_real_kernel(double* ws, RSlab
       if (r < m && cc < n) M[r + (size_t)cc * ld] = acc[rt][ct][0];
       if (r < m && cc + 1 < n) M[r + (size_t)(cc + 1) * ld] = acc[rt][ct][1];
     }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Persistent, double-buffered variant of rank_update_real_kernel<64> on the bulk-copy engine
+// (HX_RU_BULK=1; off by default - measured 3.2x slower, see bd_reduce_real): each CTA walks the 64 x 64 tiles (all matrices of the batch) with a stride of
+// gridDim.x; the C tile, the 64 x 32 U rows and the 64 x 32 W rows of the NEXT tile are in flight as bulk
+// copies (one per tile column, completing on the stage's mbarrier) while the current tile runs its DMMAs, and
+// the updated tile leaves through bulk stores.  The rank update is HBM-bound (C read and written once per
+// update, 3.7-4.0 TB/s with the load-compute-store kernel); this keeps ~2 tiles per SM in flight.
+constexpr int RBU_T = 64, RBU_LD = 68;  // tile, shared leading dimension (doubles; 2-way = minimal fragment reads)
+struct RBulkStage {
+  double M[RBU_T * RBU_LD];
+  double U[GBW * RBU_LD];
+  double W[GBW * RBU_LD];
+};
+constexpr size_t rru_bulk_smem() { return 2 * sizeof(RBulkStage) + 128; }
+
+__global__ void __launch_bounds__(256, 1) rank_update_real_bulk_kernel(double* ws, RSlab g, int mr0, int mc0, int m,
+                                                                        int n, size_t u_off, size_t w_off, int tiles_i,
+                                                                        int tiles_j, int64_t ntiles) {
+  extern __shared__ __align__(128) unsigned char rbu_raw[];
+  RBulkStage* stg = reinterpret_cast<RBulkStage*>(rbu_raw);
+  __shared__ __align__(8) uint64_t full[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wr = warp & 3, wc = warp >> 2;
+  const int ld = g.ld;
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  const int64_t per_mat = (int64_t)tiles_i * tiles_j;
+  auto tile_of = [&](int64_t t, double*& base, int& I0, int& J0) {
+    const int64_t b = t / per_mat;
+    const int r = (int)(t - b * per_mat);
+    I0 = (r % tiles_i) * RBU_T;
+    J0 = (r / tiles_i) * RBU_T;
+    base = ws + (size_t)b * g.stride;
+  };
+  // warp 0: arm stage s and issue the bulk loads of tile t (one copy per column)
+  auto issue = [&](int64_t t, int s) {
+    double* base;
+    int I0, J0;
+    tile_of(t, base, I0, J0);
+    const int rows = min(RBU_T, m - I0), cols = min(RBU_T, n - J0);
+    if (lane == 0) mbar_arrive_expect_tx(&full[s], (unsigned)(8 * rows * (cols + GBW) + 8 * cols * GBW));
+    __syncwarp();
+    const double* Mg = base + g.m_off + (size_t)(mc0 + J0) * ld + mr0 + I0;
+    for (int c = lane; c < cols; c += 32) bulk_g2s(stg[s].M + c * RBU_LD, Mg + (size_t)c * ld, 8u * rows, &full[s]);
+    bulk_g2s(stg[s].U + lane * RBU_LD, base + u_off + I0 + (size_t)lane * ld, 8u * rows, &full[s]);
+    bulk_g2s(stg[s].W + lane * RBU_LD, base + w_off + J0 + (size_t)lane * ld, 8u * cols, &full[s]);
+  };
+  const int64_t t0 = blockIdx.x, step = gridDim.x;
+  if (warp == 0) {
+    if (t0 < ntiles) issue(t0, 0);
+    if (t0 + step < ntiles) issue(t0 + step, 1);
+  }
+  unsigned phase0 = 0, phase1 = 0;
+  int s = 0;
+  for (int64_t t = t0; t < ntiles; t += step, s ^= 1) {
+    mbar_wait(&full[s], s ? phase1 : phase0);
+    if (s) phase1 ^= 1u;
+    else phase0 ^= 1u;
+    RBulkStage& S = stg[s];
+    double acc[2][4][2];
+#pragma unroll
+    for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+      for (int ct = 0; ct < 4; ++ct) {
+        const int r = 16 * wr + 8 * rt + (lane >> 2), cc = 32 * wc + 8 * ct + 2 * (lane & 3);
+        acc[rt][ct][0] = S.M[cc * RBU_LD + r];
+        acc[rt][ct][1] = S.M[(cc + 1) * RBU_LD + r];
+      }
+#pragma unroll
+    for (int k4 = 0; k4 < GBW / 4; ++k4) {
+      const int kc = 4 * k4 + (lane & 3);
+      double au[2], bw[4];
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt) au[rt] = -S.U[kc * RBU_LD + 16 * wr + 8 * rt + (lane >> 2)];
+#pragma unroll
+      for (int ct = 0; ct < 4; ++ct) bw[ct] = S.W[kc * RBU_LD + 32 * wc + 8 * ct + (lane >> 2)];
+#pragma unroll
+      for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+        for (int ct = 0; ct < 4; ++ct) dmma(acc[rt][ct][0], acc[rt][ct][1], au[rt], bw[ct]);
+    }
+#pragma unroll
+    for (int rt = 0; rt < 2; ++rt)
+#pragma unroll
+      for (int ct = 0; ct < 4; ++ct) {
+        const int r = 16 * wr + 8 * rt + (lane >> 2), cc = 32 * wc + 8 * ct + 2 * (lane & 3);
+        S.M[cc * RBU_LD + r] = acc[rt][ct][0];
+        S.M[(cc + 1) * RBU_LD + r] = acc[rt][ct][1];
+      }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (warp == 0) {
+      double* base;
+      int I0, J0;
+      tile_of(t, base, I0, J0);
+      const int rows = min(RBU_T, m - I0), cols = min(RBU_T, n - J0);
+      double* Mg = base + g.m_off + (size_t)(mc0 + J0) * ld + mr0 + I0;
+      for (int c = lane; c < cols; c += 32) bulk_s2g(Mg + (size_t)c * ld, S.M + c * RBU_LD, 8u * rows);
+      bulk_commit();
+      const int64_t tn = t + 2 * step;
+      if (tn < ntiles) {
+        bulk_wait_read0();  // this lane's stores have read the stage
+        __syncwarp();       // ... and every other lane's
+        issue(tn, s);
+      }
+    }
+  }
+  if (warp == 0) bulk_wait0();
 }
 
 }  // namespace hx

@@ -270,3 +270,9 @@ def test_chase_results_bitwise_repeatable(opts):
                 th.join()
             assert np.array_equal(cur, ref), rep
             assert np.array_equal(eigs, eigs0, equal_nan=True), rep
+
+
+@pytest.mark.parametrize("nu,q", [(16, 2), (12, 1)])
+def test_bulk_copy_rank_update_option(nu, q):
+    """HX_RU_BULK=1 (persistent cp.async.bulk rank update, off by default) against the oracle."""
+    check_batch("graphene", nu, q, 0.05, 4, 13, (0, 3), opts={"HX_RU_BULK": 1})

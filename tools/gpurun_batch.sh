@@ -1,10 +1,9 @@
 #!/bin/bash
 set -x
-timeout 900 python -m pytest tests/test_variants_gpu.py tests/test_modes_gpu.py -q > gpurun_out/gputest.log 2>&1; echo "pytest exit $?" >> gpurun_out/gputest.log
-for sp in 20 0 100; do
-  HX_CHASE_SPIN_NS=$sp timeout 300 python bench.py --no-e2e --no-cpu-baseline --steps 10 > gpurun_out/bench_spin$sp.json 2> /dev/null
+timeout 900 python -m pytest tests/test_variants_gpu.py tests/test_parity_gpu.py tests/test_large_gpu.py -q > gpurun_out/gputest.log 2>&1; echo "pytest exit $?" >> gpurun_out/gputest.log
+for b in 1 0; do
+  HX_RU_BULK=$b timeout 300 python bench.py --no-e2e --no-cpu-baseline --steps 10 > gpurun_out/bench_bulk$b.json 2> gpurun_out/bench_bulk$b.err
+  HX_RU_BULK=$b timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_bulk$b.csv python tools/profile_run.py --config c2 --levels 4 --parent-only > /dev/null 2>&1
 done
-for o in big-then-small big-first; do
-  HX_E2E_ORDER=$o timeout 300 python bench.py --no-cpu-baseline --steps 10 > gpurun_out/bench_order_$o.json 2> /dev/null
-done
-timeout 300 ncu --metrics gpu__time_duration.sum,launch__grid_size,launch__block_size --clock-control none --csv --log-file gpurun_out/launches_c2.csv python tools/profile_run.py --config c2 > /dev/null 2>&1
+HX_RU_BULK=1 timeout 600 python bench.py --config c4 --no-e2e --no-cpu-baseline --steps 3 > gpurun_out/bench_c4_bulk1.json 2>&1
+HX_RU_BULK=0 timeout 600 python bench.py --config c4 --no-e2e --no-cpu-baseline --steps 3 > gpurun_out/bench_c4_bulk0.json 2>&1
