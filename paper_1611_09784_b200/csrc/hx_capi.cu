@@ -841,67 +841,50 @@ __device__ __forceinline__ void fx_block_sum(int64_t (*sh)[FX_NL][MOM_P], const 
   __syncthreads();
 }
 
-// mode 0: terms, mean, var (single device).  mode 1: limbs of sum term.  mode 2: limbs of sum (term - center)^2.
-// bad[m] is raised for non-finite terms (they are left out of the sums).
-__global__ void __launch_bounds__(MOM_P * MOM_G) moments_kernel(const double* full, const double* quarters, int64_t M,
-                                                                int npts, double* terms, double* mean, double* var,
-                                                                int64_t* limbs, const double* center, int mode,
-                                                                int* bad) {
+// Exact level sums: block = 32 grid points x 8 row groups over one chunk of rows (blockIdx.y); the per-thread
+// limbs are combined in shared memory and added to the global accumulator with 64-bit integer atomics - integer
+// addition is associative, so the sums do not depend on the chunking or the order the blocks run in.
+//   center == NULL : acc += limbs of term_i (terms written when `terms` != NULL)
+//   center != NULL : acc += limbs of (term_i - center)^2
+constexpr int MOM_ROWS = 64;  // rows per block (8 per thread)
+__global__ void __launch_bounds__(MOM_P * MOM_G) level_sums_kernel(const double* full, const double* quarters, int64_t M,
+                                                                   int npts, double* terms, const double* center,
+                                                                   unsigned long long* acc, int* bad) {
   __shared__ int64_t sh[MOM_G][FX_NL][MOM_P];
-  __shared__ double smu[MOM_P];
-  __shared__ int sbad[MOM_P];
   const int pl = threadIdx.x % MOM_P, grp = threadIdx.x / MOM_P;
   const int m = blockIdx.x * MOM_P + pl;
   const bool on = m < npts;
-  int64_t L[FX_NL], T[FX_NL];
+  const int64_t r0 = (int64_t)blockIdx.y * MOM_ROWS, r1 = M < r0 + MOM_ROWS ? M : r0 + MOM_ROWS;
+  int64_t L[FX_NL];
 #pragma unroll
   for (int j = 0; j < FX_NL; ++j) L[j] = 0;
   bool ok = true;
-  if (grp == 0) sbad[pl] = 0;
-  __syncthreads();
-  if (on && mode != 2)
-    for (int64_t i = grp; i < M; i += MOM_G) {
+  if (on) {
+    const double mu = center ? center[m] : 0.0;
+    for (int64_t i = r0 + grp; i < r1; i += MOM_G) {
       const double t = cv_term(full, quarters, i, npts, m);
       if (terms) terms[i * npts + m] = t;
-      ok &= fx_add(L, t);
+      ok &= fx_add(L, center ? fx_sq_dev(t, mu) : t);
     }
-  if (mode == 1) {
-    fx_block_sum(sh, L, grp, pl, T);
-    if (grp == 0 && on)
-      for (int j = 0; j < FX_NL; ++j) limbs[(int64_t)m * FX_NL + j] = T[j];
-    if (!ok && bad) atomicOr(bad, 1);
-    return;
-  }
-  double mu = 0.0;
-  if (mode == 0) {
-    fx_block_sum(sh, L, grp, pl, T);
-    if (grp == 0) smu[pl] = fx_to_double(T) / (double)M;
-    __syncthreads();
-    mu = smu[pl];
-  } else if (on) {
-    mu = center[m];
   }
 #pragma unroll
-  for (int j = 0; j < FX_NL; ++j) L[j] = 0;
-  if (on)
-    for (int64_t i = grp; i < M; i += MOM_G) ok &= fx_add(L, fx_sq_dev(cv_term(full, quarters, i, npts, m), mu));
-  if (!ok) sbad[pl] = 1;
-  fx_block_sum(sh, L, grp, pl, T);
-  if (!ok && bad) atomicOr(bad, 1);
-  if (grp != 0 || !on) return;
-  ok = !sbad[pl];
-  if (mode == 2) {
-    for (int j = 0; j < FX_NL; ++j) limbs[(int64_t)m * FX_NL + j] = T[j];
-    return;
+  for (int j = 0; j < FX_NL; ++j) sh[grp][j][pl] = L[j];
+  __syncthreads();
+  if (grp == 0 && on) {
+#pragma unroll
+    for (int j = 0; j < FX_NL; ++j) {
+      int64_t a = 0;
+      for (int q = 0; q < MOM_G; ++q) a += sh[q][j][pl];
+      if (a) atomicAdd(acc + (int64_t)m * FX_NL + j, (unsigned long long)a);
+    }
   }
-  if (mean) mean[m] = ok ? mu : fx_nan();
-  if (var) var[m] = (M > 1 && ok) ? fx_to_double(T) / (double)(M - 1) : fx_nan();
+  if (!ok && bad) atomicOr(bad + (on ? m : 0), 1);
 }
 
-__global__ void fixed_finalize_kernel(const int64_t* limbs, int npts, double divisor, double* out) {
+__global__ void fixed_finalize_kernel(const int64_t* limbs, int npts, double divisor, double* out, const int* bad) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= npts) return;
-  out[m] = divisor > 0.0 ? fx_to_double(limbs + (int64_t)m * FX_NL) / divisor : fx_nan();
+  out[m] = (divisor > 0.0 && !(bad && bad[m])) ? fx_to_double(limbs + (int64_t)m * FX_NL) / divisor : fx_nan();
 }
 
 __global__ void sample_masks_kernel(uint64_t seed, uint64_t level, uint64_t rep0, int64_t count, double p, int nunits,
@@ -981,13 +964,50 @@ int hx_sharp_counts_device(const double* d_energies, const double* d_weights, in
   return 0;
 }
 
+// The stream-ordered scratch of hx_level_moments_device comes from the device's default memory pool; by
+// default that pool returns freed memory to the driver at every synchronisation, which makes the next
+// cudaMallocAsync a fresh mapping (milliseconds).  Keep the pool's memory instead (once per device).
+static void keep_pool_memory() {
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+
+// scratch for hx_level_moments_device: 2 x npts x limbs accumulators + npts bad flags (stream-ordered)
 int hx_level_moments_device(const double* d_full, const double* d_quarters, int64_t M, int32_t npts, double* d_terms,
                             double* d_mean, double* d_var, void* stream) {
   if (!d_full || M < 1 || npts < 1) return fail(HX_E_ARG, "level_moments: bad args");
-  hx::moments_kernel<<<(npts + hx::MOM_P - 1) / hx::MOM_P, hx::MOM_P * hx::MOM_G, 0, static_cast<cudaStream_t>(stream)>>>(
-      d_full, d_quarters, M, npts, d_terms, d_mean, d_var, nullptr, nullptr, 0, nullptr);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t lb = (size_t)npts * HX_FX_LIMBS * 8;
+  keep_pool_memory();
+  unsigned char* scratch = nullptr;
+  HX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), 2 * lb + (size_t)npts * (4 + 8) + 64, st));
+  auto* s1 = reinterpret_cast<unsigned long long*>(scratch);
+  auto* s2 = reinterpret_cast<unsigned long long*>(scratch + lb);
+  int* bad = reinterpret_cast<int*>(scratch + 2 * lb);
+  double* mean = d_mean ? d_mean : reinterpret_cast<double*>(scratch + 2 * lb + (((size_t)npts * 4 + 15) & ~(size_t)15));
+  HX_CUDA(cudaMemsetAsync(scratch, 0, 2 * lb + (size_t)npts * 4, st));
+  const dim3 grid((unsigned)((npts + hx::MOM_P - 1) / hx::MOM_P), (unsigned)((M + hx::MOM_ROWS - 1) / hx::MOM_ROWS));
+  hx::level_sums_kernel<<<grid, hx::MOM_P * hx::MOM_G, 0, st>>>(d_full, d_quarters, M, npts, d_terms, nullptr, s1, bad);
+  hx::fixed_finalize_kernel<<<(npts + 127) / 128, 128, 0, st>>>(reinterpret_cast<int64_t*>(s1), npts, (double)M, mean,
+                                                                bad);
+  if (d_var) {
+    hx::level_sums_kernel<<<grid, hx::MOM_P * hx::MOM_G, 0, st>>>(d_full, d_quarters, M, npts, nullptr, mean, s2, bad);
+    hx::fixed_finalize_kernel<<<(npts + 127) / 128, 128, 0, st>>>(reinterpret_cast<int64_t*>(s2), npts,
+                                                                  (double)(M - 1), d_var, bad);
+  }
   HX_CUDA(cudaGetLastError());
-  hx::count_launch();
+  hx::count_launch(d_var ? 4 : 2);
+  HX_CUDA(cudaFreeAsync(scratch, st));
   return 0;
 }
 
@@ -995,12 +1015,12 @@ int hx_level_sums_fixed_device(const double* d_full, const double* d_quarters, i
                                const double* d_center, int64_t* d_limbs, void* stream) {
   if (!d_full || M < 0 || npts < 1 || !d_limbs) return fail(HX_E_ARG, "level_sums_fixed_device: bad args");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (M == 0) {
-    HX_CUDA(cudaMemsetAsync(d_limbs, 0, (size_t)npts * HX_FX_LIMBS * 8, st));
-    return 0;
-  }
-  hx::moments_kernel<<<(npts + hx::MOM_P - 1) / hx::MOM_P, hx::MOM_P * hx::MOM_G, 0, st>>>(
-      d_full, d_quarters, M, npts, nullptr, nullptr, nullptr, d_limbs, d_center, d_center ? 2 : 1, nullptr);
+  HX_CUDA(cudaMemsetAsync(d_limbs, 0, (size_t)npts * HX_FX_LIMBS * 8, st));
+  if (M == 0) return 0;
+  const dim3 grid((unsigned)((npts + hx::MOM_P - 1) / hx::MOM_P), (unsigned)((M + hx::MOM_ROWS - 1) / hx::MOM_ROWS));
+  hx::level_sums_kernel<<<grid, hx::MOM_P * hx::MOM_G, 0, st>>>(d_full, d_quarters, M, npts, nullptr, d_center,
+                                                                  reinterpret_cast<unsigned long long*>(d_limbs),
+                                                                  nullptr);
   HX_CUDA(cudaGetLastError());
   hx::count_launch();
   return 0;
@@ -1009,7 +1029,7 @@ int hx_level_sums_fixed_device(const double* d_full, const double* d_quarters, i
 int hx_fixed_finalize_device(const int64_t* d_limbs, int32_t npts, double divisor, double* d_out, void* stream) {
   if (!d_limbs || !d_out || npts < 1) return fail(HX_E_ARG, "fixed_finalize_device: bad args");
   hx::fixed_finalize_kernel<<<(npts + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(d_limbs, npts, divisor,
-                                                                                            d_out);
+                                                                                            d_out, nullptr);
   HX_CUDA(cudaGetLastError());
   hx::count_launch();
   return 0;

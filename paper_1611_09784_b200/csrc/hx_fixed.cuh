@@ -10,6 +10,7 @@
 #pragma once
 #include <stdint.h>
 #include <math.h>
+#include <string.h>
 
 #include "../../include/hx.h"
 
@@ -21,25 +22,33 @@ constexpr int FX_FRAC = HX_FX_FRAC;
 // Adds v (exactly, truncated toward zero below 2^-FX_FRAC) to the limb accumulator L.  Returns false for
 // non-finite or out-of-range values (|v| >= 2^(32*FX_NL - FX_FRAC - 1)), which are not added.
 __host__ __device__ inline bool fx_add(int64_t* L, double v) {
-  if (v == 0.0) return true;
-  if (!(fabs(v) < 1e300)) return false;
-  int e;
-  const double m = frexp(fabs(v), &e);               // |v| = m 2^e, m in [0.5, 1)
-  uint64_t mant = (uint64_t)ldexp(m, 53);            // exact: |v| = mant 2^(e - 53)
-  int sh = e - 53 + FX_FRAC;                         // fixed-point bit position of mant's lowest bit
+  uint64_t bits;
+#ifdef __CUDA_ARCH__
+  bits = (uint64_t)__double_as_longlong(v);
+#else
+  memcpy(&bits, &v, 8);
+#endif
+  int e = (int)((bits >> 52) & 0x7ff);
+  if (e == 0x7ff) return false;                       // inf / nan
+  uint64_t mant = bits & 0xFFFFFFFFFFFFFull;
+  if (e) mant |= 1ull << 52;                          // normal: |v| = mant 2^(e - 1075)
+  else e = 1;                                         // subnormal: |v| = mant 2^(1 - 1075)
+  if (mant == 0) return true;
+  int sh = e - 1075 + FX_FRAC;                        // fixed-point bit position of mant's lowest bit
   if (sh + 53 > 32 * FX_NL - 1) return false;
   if (sh < 0) {
-    if (sh <= -53) return true;                      // below the resolution: contributes 0
+    if (sh <= -53) return true;                       // below the resolution: contributes 0
     mant >>= -sh;
     sh = 0;
   }
   const int li = sh >> 5, off = sh & 31;
-  const uint64_t lo = mant << off;                   // bits [off, off + 64) of mant << off
+  const uint64_t lo = mant << off;                    // bits [off, off + 64) of mant << off
   const uint64_t hi = off ? (mant >> (64 - off)) : 0;
-  const int64_t s = v < 0.0 ? -1 : 1;
-  L[li] += s * (int64_t)(lo & 0xffffffffull);
-  if (li + 1 < FX_NL) L[li + 1] += s * (int64_t)(lo >> 32);
-  if (li + 2 < FX_NL) L[li + 2] += s * (int64_t)hi;
+  const int64_t sgn = (bits >> 63) ? -1 : 1;
+  const int64_t p0 = sgn * (int64_t)(lo & 0xffffffffull), p1 = sgn * (int64_t)(lo >> 32), p2 = sgn * (int64_t)hi;
+  // static limb indices (the accumulator stays in registers)
+#pragma unroll
+  for (int j = 0; j < FX_NL; ++j) L[j] += (j == li ? p0 : 0) + (j == li + 1 ? p1 : 0) + (j == li + 2 ? p2 : 0);
   return true;
 }
 

@@ -96,6 +96,31 @@ def first_rows(inv):
     return np.unique(inv, return_index=True)[1]
 
 
+_RNG_STREAMS: dict = {}
+_QMAPS: dict = {}
+
+
+def _rng_stream(device):
+    import torch
+
+    st = _RNG_STREAMS.get(device)
+    if st is None:
+        st = _RNG_STREAMS[device] = torch.cuda.Stream(device=device, priority=-1)
+    return st
+
+
+def _quarter_maps(part, device):
+    """Device copies of a partition's quarter labels and unit map (cached per parent cell)."""
+    import torch
+
+    key = (part.parent.spec, part.parent.n, device)
+    if key not in _QMAPS:
+        dev = torch.device("cuda", device)
+        _QMAPS[key] = (torch.from_numpy(part.unit_assignment.astype(np.int32)).to(dev),
+                       torch.from_numpy(part.unit_map.astype(np.int32)).to(dev))
+    return _QMAPS[key]
+
+
 class _InlineExecutor:
     """Executor interface that runs the submitted call immediately (single-piece batches)."""
 
@@ -187,7 +212,7 @@ class Engine:
 
     def __init__(self, model, nq: int, delta: float, master_seed: int, workers: int = 1, bz_mode: str = "full",
                  energy_points: int = 4096, energy_range=None, dedup: bool = True, device: int = 0,
-                 shard=(0, 1), devices=1, shard_mode: str = "replicas"):
+                 shard=(0, 1), devices=1, shard_mode: str = "replicas", rng: str = "device"):
         self.model = model
         self.nq = nq
         self.delta = delta
@@ -204,6 +229,9 @@ class Engine:
         if shard_mode not in ("replicas", "split"):
             raise ValueError(f"unknown shard mode {shard_mode!r}")
         self.shard_mode = shard_mode
+        if rng not in ("device", "host"):
+            raise ValueError(f"unknown rng {rng!r}")
+        self.rng = rng  # where the level masks are drawn (bit-identical either way)
         self.devices = list(devices)  # GPUs the new masks of a group are split over (int G: device .. device+G-1)
         self.io_bytes = [0, 0]  # host->device, device->host bytes moved by the batch calls
         self._caches: dict = {}  # (n, q) -> _TierCache: the run-wide dedup cache (runner.py:206-244)
@@ -568,12 +596,14 @@ class Engine:
         # mode: every rank draws the whole level)
         rank, _ = self.shard
         m0 = rank * nsamples if self.shard_mode == "replicas" else 0
-        words = sample_masks(sc.nunits, p_vac, self.master_seed, stream, m0, nsamples)
+        if self.rng == "device":
+            words, sub = self._draw_device(sc, p_vac, stream, m0, nsamples, with_cv)
+        else:
+            words = sample_masks(sc.nunits, p_vac, self.master_seed, stream, m0, nsamples)
+            sub = restrict_words(words, partition_quarters(sc)) if with_cv else None  # [M, 4, w]
         groups = [(n, q, words)]
         if with_cv:
-            part = partition_quarters(sc)
             nsub = n // 2
-            sub = restrict_words(words, part)  # [M, 4, w]
             groups.append((nsub, self.q_of(nsub), sub.reshape(nsamples * 4, -1)))
 
         def ids(gi, new, inv):  # task ids (level, replicate, "Q" / "CVr") of the first row of each new mask
@@ -583,6 +613,36 @@ class Engine:
             return [(level, m0 + int(r) // 4, f"CV{int(r) % 4 + 1}") for r in rows]
 
         return groups, ids
+
+    def _draw_device(self, sc, p_vac, stream_level, m0, count, with_cv):
+        """Masks [count, w] (and quarter masks [count, 4, ws]) drawn on the GPU - the device port of the
+        reference sampler (hx_sample_masks_device: SeedSequence -> PCG64 -> random() < p, bit-identical to
+        disorder.py:66-81) and quarter restriction (hx_restrict_masks_device, disorder.py:84-94) - then copied
+        to the host, where the run cache keys them (runner.py:213-233)."""
+        import torch
+
+        dev = torch.device("cuda", self.device)
+        lib = _lib.load()
+        st = _rng_stream(self.device)
+        nunits = sc.nunits
+        w = max(1, (nunits + 63) // 64)
+        with torch.cuda.stream(st):
+            d = torch.empty((max(count, 1), w), dtype=torch.int64, device=dev)
+            _lib.check(lib.hx_sample_masks_device(self.master_seed, stream_level, m0, count, p_vac, nunits, d.data_ptr(),
+                                                  st.cuda_stream), "hx_sample_masks_device")
+            q = None
+            if with_cv:
+                part = partition_quarters(sc)
+                assign, umap = _quarter_maps(part, self.device)
+                sub_units = part.subcells[0].nunits
+                ws = max(1, (sub_units + 63) // 64)
+                q = torch.empty((max(count, 1) * 4, ws), dtype=torch.int64, device=dev)
+                _lib.check(lib.hx_restrict_masks_device(d.data_ptr(), count, nunits, assign.data_ptr(), umap.data_ptr(),
+                                                        sub_units, q.data_ptr(), st.cuda_stream),
+                           "hx_restrict_masks_device")
+            words = d[:count].cpu().numpy().view(np.uint64)
+            sub = None if q is None else q[:4 * count].cpu().numpy().view(np.uint64).reshape(count, 4, ws)
+        return words, sub
 
     def _level_finish(self, level, n, nsamples, with_cv, evaluated):
         """Level terms + moments from the seam's results for the level's batch (runner.py:281-311)."""

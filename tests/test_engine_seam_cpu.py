@@ -26,7 +26,7 @@ class FakeEngine(hx.Engine):
 @pytest.fixture
 def engine(monkeypatch):
     monkeypatch.setattr(_lib.Device, "lane", classmethod(lambda cls, d, i, high=None: None))
-    return FakeEngine(hx.GrapheneNNModel(), nq=16, delta=0.01, master_seed=7, bz_mode="reduced",
+    return FakeEngine(hx.GrapheneNNModel(), nq=16, delta=0.01, master_seed=7, bz_mode="reduced", rng="host",
                       energy_points=11, energy_range=(LO + 0.02, HI - 0.02))
 
 
@@ -80,7 +80,7 @@ def test_run_mlmc_equals_levels_in_order(engine, monkeypatch):
     monkeypatch.setattr(E, "level_moments", lambda full, quarters, device, want_terms=True: _np_moments(full, quarters))
     plan = hx.LevelPlan(ns=(2, 4, 8), samples=(64, 32, 8), nq=16, p_vac=0.2, delta=0.01)
     _, sets = engine.run_mlmc(plan)
-    seq = FakeEngine(hx.GrapheneNNModel(), nq=16, delta=0.01, master_seed=7, bz_mode="reduced",
+    seq = FakeEngine(hx.GrapheneNNModel(), nq=16, delta=0.01, master_seed=7, bz_mode="reduced", rng="host",
                      energy_points=11, energy_range=(LO + 0.02, HI - 0.02))
     for lvl, (n, m) in enumerate(zip(plan.ns, plan.samples), start=1):
         s = seq.sample_level(lvl, n, m, plan.p_vac, lvl > 1)

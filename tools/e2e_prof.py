@@ -22,6 +22,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--config", default="c2")
+    ap.add_argument("--rng", default="device", choices=["device", "host"])
     args = ap.parse_args()
     kind, levels, nq, p, erange, _ = bench.CONFIGS[args.config]
     lo, hi = bench.grid_range(kind, erange)
@@ -44,7 +45,7 @@ def main():
 
     def one(prof=None):
         eng = hx.Engine(model, nq=nq, delta=bench.DELTA, master_seed=bench.SEED, bz_mode="reduced",
-                        energy_points=bench.NPTS, energy_range=(lo + 2 * bench.DELTA, hi - 2 * bench.DELTA))
+                        energy_points=bench.NPTS, energy_range=(lo + 2 * bench.DELTA, hi - 2 * bench.DELTA), rng=args.rng)
         t0 = time.perf_counter()
         if prof:
             prof.enable()
@@ -55,13 +56,18 @@ def main():
         return time.perf_counter() - t0
 
     one()
+    all_dt = []
     for _ in range(args.reps):
         trace.clear()
         t0 = time.perf_counter()
         dt = one()
+        all_dt.append(dt)
         print(f"run_mlmc: {1e3 * dt:.1f} ms", flush=True)
         for n, q, m, a, b in sorted(trace, key=lambda x: x[3]):
             print(f"   tier n={n} q={q} masks={m}: {1e3 * (a - t0):7.1f} -> {1e3 * (b - t0):7.1f} ms", flush=True)
+    import statistics
+
+    print(f"run_mlmc median over {args.reps}: {1e3 * statistics.median(all_dt):.2f} ms, min {1e3 * min(all_dt):.2f} ms")
     # each tier alone (sequential, primary context), same masks as the concurrent run
     from paper_1611_09784_b200.solver import eval_batch
     eng = hx.Engine(model, nq=nq, delta=bench.DELTA, master_seed=bench.SEED, bz_mode="reduced",
