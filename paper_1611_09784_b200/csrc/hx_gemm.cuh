@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(128) xv_kernel(double2* ws, SlabGeom g, int ar
         rf[rt][k4] = r < rows ? Rg[r + (size_t)(4 * k4 + (lane & 3)) * ld] : make_double2(0.0, 0.0);
       }
   }
-  CTile acc[2][4];
+  CTile3 acc[2][4];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(128) xv_kernel(double2* ws, SlabGeom g, int ar
       // op(A)[rows of this warp][16 columns of the chunk] -= R S^H (K = 32), in place + back to M
       const double2* St = Ss + stg * XV_TK * XV_LDS;
       const int kk = ch * XV_TK;
-      CTile u[2][2];
+      CTile3 u[2][2];
 #pragma unroll
       for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(128) xv_kernel(double2* ws, SlabGeom g, int ar
           u[rt][ct].im0 = MODE == 1 ? -z0.y : z0.y;
           u[rt][ct].re1 = z1.x;
           u[rt][ct].im1 = MODE == 1 ? -z1.y : z1.y;
+          u[rt][ct].begin();
         }
 #pragma unroll
       for (int k4 = 0; k4 < GBW / 4; ++k4) {
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(128) xv_kernel(double2* ws, SlabGeom g, int ar
       for (int rt = 0; rt < 2; ++rt)
 #pragma unroll
         for (int ct = 0; ct < 2; ++ct) {
+          u[rt][ct].end();
           const int r = 16 * warp + 8 * rt + (lane >> 2), c = 8 * ct + 2 * (lane & 3);
           const double2 n0 = make_double2(u[rt][ct].re0, MODE == 1 ? -u[rt][ct].im0 : u[rt][ct].im0);
           const double2 n1 = make_double2(u[rt][ct].re1, MODE == 1 ? -u[rt][ct].im1 : u[rt][ct].im1);
@@ -235,6 +237,7 @@ __global__ void __launch_bounds__(128) xv_kernel(double2* ws, SlabGeom g, int ar
     for (int ct = 0; ct < 4; ++ct) {
       const int r = 16 * warp + 8 * rt + (lane >> 2);
       const int cc = 8 * ct + 2 * (lane & 3);
+      cend<RE>(acc[rt][ct]);
       Xs[r * XL + cc] = make_double2(acc[rt][ct].re0, acc[rt][ct].im0);
       Xs[r * XL + cc + 1] = make_double2(acc[rt][ct].re1, acc[rt][ct].im1);
       acc[rt][ct].zero();
@@ -259,6 +262,7 @@ __global__ void __launch_bounds__(128) xv_kernel(double2* ws, SlabGeom g, int ar
     for (int ct = 0; ct < 4; ++ct) {
       const int r = i0 + 16 * warp + 8 * rt + (lane >> 2);
       const int cc = 8 * ct + 2 * (lane & 3);
+      cend<RE>(acc[rt][ct]);
       if (r < rows) {
         X[r + (size_t)cc * ld] = make_double2(acc[rt][ct].re0, acc[rt][ct].im0);
         X[r + (size_t)(cc + 1) * ld] = make_double2(acc[rt][ct].re1, acc[rt][ct].im1);
@@ -316,6 +320,7 @@ __global__ void __launch_bounds__(2 * TN * 2, TN == 64 ? 2 : 4) rank_update_kern
       acc[rt][ct].im0 = z0.y;
       acc[rt][ct].re1 = z1.x;
       acc[rt][ct].im1 = z1.y;
+      cbegin<RE>(acc[rt][ct]);
     }
   cp_async_wait<0>();
   __syncthreads();
@@ -338,6 +343,7 @@ __global__ void __launch_bounds__(2 * TN * 2, TN == 64 ? 2 : 4) rank_update_kern
     for (int ct = 0; ct < 4; ++ct) {
       const int r = I0 + 16 * wr + 8 * rt + (lane >> 2);
       const int cc = J0 + 32 * wc + 8 * ct + 2 * (lane & 3);
+      cend<RE>(acc[rt][ct]);
       if (r < m && cc < n) M[r + (size_t)cc * ld] = make_double2(acc[rt][ct].re0, acc[rt][ct].im0);
       if (r < m && cc + 1 < n) M[r + (size_t)(cc + 1) * ld] = make_double2(acc[rt][ct].re1, acc[rt][ct].im1);
     }
@@ -399,6 +405,7 @@ static __global__ void __launch_bounds__(256, 2) her2k_kernel(double2* ws, SlabG
       acc[rt][ct].im0 = z0.y;
       acc[rt][ct].re1 = z1.x;
       acc[rt][ct].im1 = z1.y;
+      acc[rt][ct].begin();
     }
   auto mac_pass = [&]() {
 #pragma unroll
@@ -435,6 +442,7 @@ static __global__ void __launch_bounds__(256, 2) her2k_kernel(double2* ws, SlabG
       const int rl = 16 * wr + 8 * rt + (lane >> 2);
       const int cl = 32 * wc + 8 * ct + 2 * (lane & 3);
       const int r = I0 + rl, c = J0 + cl;
+      acc[rt][ct].end();
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int cc = c + e;

@@ -143,30 +143,52 @@ class _InlineExecutor:
 
 class _TierCache:
     """Run cache of one (n, q) tier: the (n, q, mask) keys of the reference's cache (runner.py:206-244) as a
-    sorted array of mask rows (void view of the uint64 words) with their curves and per-job costs, so lookups
-    and inserts are vectorised (searchsorted) instead of a dict probe per request."""
+    sorted array of mask rows (void view of the uint64 words) with the row of each key's curve in an append-only
+    buffer, so lookups and inserts are vectorised (searchsorted) and an insert copies only the new curves
+    (the buffer grows by doubling; only the small key / index arrays are re-sorted)."""
 
     def __init__(self, npts):
         self.keys = None
-        self.curves = np.zeros((0, npts))
-        self.pj = np.zeros(0)
+        self.rows = np.zeros(0, dtype=np.int64)
+        self.buf = np.zeros((0, npts))
+        self.pjb = np.zeros(0)
+        self.n = 0
 
     def find(self, kv):
-        """Row of each key in the cache, -1 if absent."""
+        """Buffer row of each key, -1 if absent."""
         if self.keys is None or not len(self.keys) or not len(kv):
             return np.full(len(kv), -1, dtype=np.int64)
         pos = np.minimum(np.searchsorted(self.keys, kv), len(self.keys) - 1)
-        return np.where(self.keys[pos] == kv, pos, -1)
+        return np.where(self.keys[pos] == kv, self.rows[pos], -1)
+
+    @property
+    def curves(self):
+        return self.buf
+
+    @property
+    def pj(self):
+        return self.pjb
 
     def add(self, kv, curves, pj):
+        k = len(kv)
+        if self.n + k > len(self.buf):
+            cap = max(2 * len(self.buf), self.n + k, 256)
+            nb = np.empty((cap, self.buf.shape[1]))
+            nb[: self.n] = self.buf[: self.n]
+            npj = np.empty(cap)
+            npj[: self.n] = self.pjb[: self.n]
+            self.buf, self.pjb = nb, npj
+        self.buf[self.n: self.n + k] = curves
+        self.pjb[self.n: self.n + k] = pj
+        rows = np.arange(self.n, self.n + k)
+        self.n += k
         keys = kv if self.keys is None else np.concatenate([self.keys, kv])
-        curves = np.concatenate([self.curves, curves])
-        pj = np.concatenate([self.pj, pj])
+        allrows = rows if self.keys is None else np.concatenate([self.rows, rows])
         o = np.argsort(keys, kind="stable")
-        self.keys, self.curves, self.pj = keys[o], curves[o], pj[o]
+        self.keys, self.rows = keys[o], allrows[o]
 
     def __len__(self):
-        return 0 if self.keys is None else len(self.keys)
+        return self.n
 
 
 class TaskError(RuntimeError):
@@ -527,34 +549,44 @@ class Engine:
         return out
 
     def _place_batch(self, bi, groups, plans, pieces, hits, spent, npts):
-        """Per-request curves of batch bi from the run cache and the solved pieces (runner.py:234-243)."""
+        """Per-request curves of batch bi from the run cache and the solved pieces (runner.py:234-243).  Every
+        request row is gathered once from its source (a solved piece or the cache) - no intermediate array of
+        the unique masks' curves."""
         res = []
         for gi in range(len(groups)):
             tier, uniq, inv, kv, src, start = plans[(bi, gi)]
-            cu = np.empty((len(uniq), npts))
-            pj = np.empty(len(uniq))
+            R = len(inv)
+            out = np.empty((R, npts))
+            opj = np.empty(R)
+            rsrc = src[inv]  # per request row: piece row (>= 0) or cached (< 0)
+            pj_u = np.empty(len(uniq))
             got = np.flatnonzero(src >= 0)
             if len(got):
                 lst = pieces[tier]
                 starts = np.array([st for st, _, _ in lst])
-                which = np.searchsorted(starts, src[got], side="right") - 1
-                for k in np.unique(which):
+                which_u = np.searchsorted(starts, src[got], side="right") - 1
+                which_r = np.searchsorted(starts, rsrc, side="right") - 1
+                for k in np.unique(which_u):
                     curves, per_job = lst[k][1].result()
-                    sel = got[which == k]
-                    cu[sel] = curves[src[sel] - lst[k][0]]
-                    pj[sel] = per_job
-            cached = np.flatnonzero(src < 0)
+                    rows = np.flatnonzero((rsrc >= 0) & (which_r == k))
+                    out[rows] = curves[rsrc[rows] - lst[k][0]]
+                    opj[rows] = per_job
+                    pj_u[got[which_u == k]] = per_job
+            cached_r = np.flatnonzero(rsrc < 0)
             cache = self._tier_cache(tier, npts)
-            if len(cached):
-                at = cache.find(kv[cached])
-                cu[cached] = cache.curves[at]
-                pj[cached] = cache.pj[at]
+            if len(cached_r):
+                at = cache.find(kv[inv[cached_r]])
+                out[cached_r] = cache.curves[at]
+                opj[cached_r] = cache.pj[at]
             # masks this batch solved first: their cost is this batch's, and they enter the run cache
             own = np.flatnonzero(src >= start)
-            spent[bi] += float(pj[own].sum())
+            spent[bi] += float(pj_u[own].sum())
             if kv is not None and len(own):
-                cache.add(kv[own], cu[own], pj[own])
-            res.append((cu[inv], pj[inv]))
+                # the first request row of each own mask carries its curve
+                first = np.empty(len(uniq), dtype=np.int64)
+                first[inv[::-1]] = np.arange(R - 1, -1, -1)
+                cache.add(kv[own], out[first[own]], pj_u[own])
+            res.append((out, opj))
         return res, hits[bi], spent[bi]
 
     def evaluate_masks(self, requests):

@@ -118,16 +118,25 @@ def level_moments(full, quarters=None, device: int = 0, want_terms: bool = True)
     st = _moments_stream(device)
     st.wait_stream(torch.cuda.current_stream(dev))
 
+    host = [a for a in (full, quarters) if a is not None and not isinstance(a, torch.Tensor)]
+    stage = _pinned_staging(device, sum(int(np.asarray(a).size) for a in host)) if host else None
+    off = [0]
+
     def up(a):
         if isinstance(a, torch.Tensor):
             return a.to(dev, dtype=torch.float64).contiguous()
-        h = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).pin_memory()
-        return h.to(dev, non_blocking=True)
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        h = stage[0][off[0]: off[0] + a.size]
+        off[0] += a.size
+        h.numpy()[:] = a.reshape(-1)
+        return h.to(dev, non_blocking=True).view(a.shape)
 
     with torch.cuda.stream(st):
         f = up(full)
         M, npts = f.shape
         q = None if quarters is None else up(quarters)
+        if stage is not None:
+            stage[1].record(st)  # the staging buffer is free again once these copies are done
         terms = torch.empty_like(f) if want_terms else None
         mean = torch.empty(npts, dtype=torch.float64, device=dev)
         var = torch.empty(npts, dtype=torch.float64, device=dev)
@@ -141,6 +150,25 @@ def level_moments(full, quarters=None, device: int = 0, want_terms: bool = True)
 
 
 _MOMENT_STREAMS: dict = {}
+_PINNED: dict = {}
+
+
+def _pinned_staging(device: int, count: int):
+    """(pinned float64 host buffer of >= count elements, event of its last copy) for `device`, reused across
+    calls (pin_memory() per call measured ~3 ms each in the Engine's level finish); waits for the previous
+    copy out of it before handing it out again."""
+    import torch
+
+    buf, ev = _PINNED.get(device, (None, None))
+    if buf is None or buf.numel() < count:
+        if ev is not None:
+            ev.synchronize()
+        buf = torch.empty(max(count, 1 << 20), dtype=torch.float64).pin_memory()
+        ev = torch.cuda.Event()
+        _PINNED[device] = (buf, ev)
+    else:
+        ev.synchronize()
+    return buf, ev
 
 
 def _moments_stream(device: int):

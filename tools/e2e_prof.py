@@ -42,6 +42,19 @@ def main():
         return out
 
     hx.Engine._solve_group = traced
+    phases = []
+
+    def timed(name, fn):
+        def wrap(self, *a, **k):
+            t = time.perf_counter()
+            out = fn(self, *a, **k)
+            phases.append((name, t, time.perf_counter()))
+            return out
+        return wrap
+
+    hx.Engine._place_batch = timed("place", hx.Engine._place_batch)
+    hx.Engine._level_finish = timed("finish", hx.Engine._level_finish)
+    hx.Engine._level_batch = timed("draw", hx.Engine._level_batch)
 
     def one(prof=None):
         eng = hx.Engine(model, nq=nq, delta=bench.DELTA, master_seed=bench.SEED, bz_mode="reduced",
@@ -59,10 +72,13 @@ def main():
     all_dt = []
     for _ in range(args.reps):
         trace.clear()
+        phases.clear()
         t0 = time.perf_counter()
         dt = one()
         all_dt.append(dt)
         print(f"run_mlmc: {1e3 * dt:.1f} ms", flush=True)
+        for name, a, b in sorted(phases, key=lambda x: x[1]):
+            print(f"   {name:7s} {1e3 * (a - t0):7.2f} -> {1e3 * (b - t0):7.2f} ms", flush=True)
         for n, q, m, a, b in sorted(trace, key=lambda x: x[3]):
             print(f"   tier n={n} q={q} masks={m}: {1e3 * (a - t0):7.1f} -> {1e3 * (b - t0):7.1f} ms", flush=True)
     import statistics
