@@ -56,9 +56,11 @@ FRAC_NOTE = ("frac = EXECUTED FP64 flops / device time / FP64 peak.  Executed fl
              "(a rate of the dense complex-Hermitian method, not a hardware fraction).")
 # executed-FP64 profiles (tools/profile_run.py under ncu + tools/ncu_flops.py --json): config -> path
 EXECUTED = {"c2": "profiles/r02_fp64_executed_c2.json", "c3": "profiles/r02_fp64_executed_c3.json",
-            "c4": "profiles/r02_fp64_executed_c4.json", "c1": "profiles/r02_fp64_executed_c1.json"}
+            "c4": "profiles/r02_fp64_executed_c4.json", "c1": "profiles/r02_fp64_executed_c1.json",
+            "c5": "profiles/r02_fp64_executed_c5.json"}
 # the dominant tier alone (--levels L --parent-only): (config, N) -> path
-EXECUTED_TIER = {("c2", 2048): "profiles/r02_fp64_executed_c2_L4_parent.json"}
+EXECUTED_TIER = {("c2", 2048): "profiles/r02_fp64_executed_c2_L4_parent.json",
+                 ("c4", 8192): "profiles/r02_fp64_executed_c4.json", ("c1", 32): "profiles/r02_fp64_executed_c1.json"}
 
 
 def executed_gflop(path):
@@ -95,7 +97,26 @@ def traffic_of(config, N):
 
 
 def env_rank():
-    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+    """(rank, world, local device).  HX_BENCH_ONE_DEVICE=1 puts every rank on device 0 - only for the functional
+    test of the multi-rank path on a one-GPU box (with HX_DIST_BACKEND=gloo: host-side collectives, the ranks'
+    kernels never wait on each other); never for a measurement."""
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    local = 0 if os.environ.get("HX_BENCH_ONE_DEVICE") == "1" else int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+from paper_1611_09784_b200 import _dist  # noqa: E402
+
+
+def init_dist(local):
+    import torch
+    import torch.distributed as dist
+
+    backend = os.environ.get("HX_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
 
 
 def make_model(kind):
@@ -372,7 +393,7 @@ def run_c5(args):
 
     rank, world, local = env_rank()
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     import paper_1611_09784_b200 as hx
@@ -388,6 +409,9 @@ def run_c5(args):
     g = _lib.EGrid()
     g.e0, g.step, g.npts, g.delta = lo, (hi - lo) / (NPTS - 1), NPTS, DELTA
     peak = fp64_peak_live(dev)
+    # executed FP64 per matrix of each size (ncu counts of tools/c5_sample.py batches, profiles/)
+    c5_path = ROOT / EXECUTED["c5"]
+    c5_exec = json.loads(c5_path.read_text())["per_matrix_gflop"] if c5_path.exists() else {}
     sweep, tot_mats, tot_ms, launches0 = [], 0, 0.0, _lib.kernel_launches()
     e2e_tot = [0, 0.0, 0, 0]  # matrices, seconds, h2d bytes, d2h bytes
     cpu_rows = []
@@ -429,15 +453,20 @@ def run_c5(args):
             ms = statistics.median(times)
             if world > 1:
                 t = torch.tensor([ms], dtype=torch.float64, device=dev)
-                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                _dist.all_reduce(t, op=dist.ReduceOp.MAX)
                 ms = float(t.item())
             d = kept_dims(cell, masks)
             flops = float(np.sum(16.0 / 3.0 * d.astype(np.float64) ** 3))
             ach = flops / (ms * 1e-3) / 1e12
+            per_mat = c5_exec.get(str(cell.dim))
+            exe = None if per_mat is None else per_mat * 1e9 * B / (ms * 1e-3) / 1e12
+            if not bool(((status == 0) | (status == 3)).all().item()):
+                raise SystemExit(f"c5 n={cell.dim}: failed solves in the timed batch")
             sweep.append({"n": cell.dim, "nu": nu, "nu2": nu2, "batch": B, "ms": round(ms, 3),
                           "matrices_per_s": world * B / (ms * 1e-3), "algorithmic_tflops": round(ach, 3),
-                          "roofline_frac": round(ach / peak, 4),
-                          "status_ok": bool((status == 0).all().item())})
+                          "executed_tflops": None if exe is None else round(exe, 3),
+                          "roofline_frac": None if exe is None else round(exe / peak, 4),
+                          "status_ok": True})
             tot_mats += world * B
             tot_ms += ms
             # e2e: the host-buffer API (masks H2D and curves D2H inside the timed region)
@@ -468,8 +497,11 @@ def run_c5(args):
             "data": "synthetic (seeded reference sampler, bit-exact masks, p=0.05)",
             "config": {"workload": desc, "sweep": sweep, "k": "one generic reduced-grid k-point per matrix",
                        "energy_points": NPTS, "delta": DELTA},
-            "roofline": {"bound": "fp64", "kernel": f"batched eigensolve n={dom['n']}", "achieved": dom["algorithmic_tflops"],
-                         "peak": peak, "unit": "TFLOP/s", "frac": dom["roofline_frac"], "traffic": None,
+            "roofline": {"bound": "fp64", "kernel": f"batched eigensolve n={dom['n']} (the sweep's longest batch)",
+                         "achieved": dom["executed_tflops"], "peak": peak, "unit": "TFLOP/s",
+                         "frac": dom["roofline_frac"], "traffic": None, "executed_source": EXECUTED["c5"],
+                         "algorithmic": {"count": "16/3 d^3 per matrix (SURVEY 8d)",
+                                         "rate_tflops": dom["algorithmic_tflops"]},
                          "peak_source": "live cuBLAS ZGEMM 4096^3 complex128 on this GPU (best of 5)",
                          "note": FRAC_NOTE},
             "gpu_launches": launches, "clocks": clk.summary(),
@@ -525,7 +557,7 @@ def main():
 
     rank, world, local = env_rank()
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
@@ -595,7 +627,7 @@ def main():
     total_ms = float(sum(times))
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        _dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     # weak: every rank runs a full level set of its own replicates; strong: one level set split over the ranks
@@ -721,7 +753,7 @@ def run_e2e(hx, model, levels, nq, p, erange, lo, hi, args, rank, world, dev):
     dt = statistics.median(dts)
     if world > 1:
         t = torch.tensor([dt], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        _dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
     total = (world if shard_mode == "replicas" else 1) * sum(M for _, M in levels)
     return {"value": total / dt, "unit": "samples/s", "h2d_bytes_per_step": int(io[0]), "d2h_bytes_per_step": int(io[1]),

@@ -557,7 +557,8 @@ void band_init_attributes() {
   set_smem_attr(band_assemble_kernel, 64 * 1024);
   set_smem_attr(band_assemble_general_kernel, 64 * 1024);
   set_smem_attr(rank_update_kernel<64>, (int)ru_smem<64>());
-  set_smem_attr(her2k_kernel, (int)HK_SMEM);
+  set_smem_attr(her2k_kernel<false>, (int)HK_SMEM);
+  set_smem_attr(her2k_kernel<true>, (int)HK_SMEM);
   set_smem_attr(xv_kernel<0>, (int)XV_SMEM);
   set_smem_attr(xv_kernel<1>, (int)XV_SMEM);
 #define HCHASE_ATTR(NW)                                                                           \
@@ -597,6 +598,7 @@ bool launch_cluster_panel(double2* ws, const PanelArgs& a, int64_t cnt, cudaStre
 
 // Stage 1 + 2 for `cnt` matrices already staged in the workspace.
 static int band_reduce(double2* ws, const BandWs& L, int N, int64_t cnt, const int* dims, cudaStream_t st) {
+  const bool herk_3m = opt("HX_HERK_3M", 0) != 0;
   for (int k0 = 0; N - k0 - BW > 0; k0 += BW) {
     const int m = N - k0 - BW;
     // register-resident panel QR; panels taller than 4096 rows use the L2-resident single-CTA kernel
@@ -613,7 +615,12 @@ static int band_reduce(double2* ws, const BandWs& L, int N, int64_t cnt, const i
     w_rows_kernel<<<dim3((unsigned)((m + 31) / 32), (unsigned)cnt), 256, W_ROWS_SMEM, st>>>(ws, L, N, k0);
     count_launch(2);
     const unsigned tt = (unsigned)((m + RU_T - 1) / RU_T);
-    her2k_kernel<<<dim3(tt * (tt + 1) / 2, (unsigned)cnt), 256, HK_SMEM, st>>>(ws, G, k0 + BW, m, L.x_off, L.v_off);
+    if (herk_3m)
+      her2k_kernel<true><<<dim3(tt * (tt + 1) / 2, (unsigned)cnt), 256, HK_SMEM, st>>>(ws, G, k0 + BW, m, L.x_off,
+                                                                                        L.v_off);
+    else
+      her2k_kernel<false><<<dim3(tt * (tt + 1) / 2, (unsigned)cnt), 256, HK_SMEM, st>>>(ws, G, k0 + BW, m, L.x_off,
+                                                                                         L.v_off);
     count_launch(4);
     BAND_CUDA(cudaGetLastError());
   }

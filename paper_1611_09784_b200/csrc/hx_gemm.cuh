@@ -7,6 +7,7 @@
 // same leading dimension.
 #pragma once
 #include <cuda_runtime.h>
+#include <type_traits>
 #include <stdint.h>
 
 #include "hx_dmma.cuh"
@@ -361,8 +362,12 @@ constexpr size_t ru_smem() {
 constexpr size_t HK_SMEM = RU_SMEM;
 static_assert((size_t)RU_T * (RU_T + 1) * sizeof(double2) <= HK_SMEM, "her2k mirror tile does not fit");
 
-static __global__ void __launch_bounds__(256, 2) her2k_kernel(double2* ws, SlabGeom g, int r0, int m, size_t w_off,
-                                                              size_t v_off) {
+// M3: the 3M complex product (CTile3, three DMMAs per fragment product) at 1 CTA per SM (its third
+// accumulator does not fit the 128-register budget of 2 CTAs/SM); HX_HERK_3M selects it.
+template <bool M3 = false>
+static __global__ void __launch_bounds__(256, M3 ? 1 : 2) her2k_kernel(double2* ws, SlabGeom g, int r0, int m,
+                                                                       size_t w_off, size_t v_off) {
+  using Tile = std::conditional_t<M3, CTile3, CTile>;
   extern __shared__ __align__(16) double2 hk_sm[];
   double2* Ai = hk_sm;                 // [RU_T][RU_LD]  rows I0..: first factor
   double2* Bj = hk_sm + RU_T * RU_LD;  // [RU_T][RU_LD]  rows J0..: second factor (conjugated at use)
@@ -391,7 +396,7 @@ static __global__ void __launch_bounds__(256, 2) her2k_kernel(double2* ws, SlabG
     cp_async_commit();
   };
   stage(W, V);
-  CTile acc[2][4];
+  Tile acc[2][4];
 #pragma unroll
   for (int rt = 0; rt < 2; ++rt)
 #pragma unroll

@@ -178,7 +178,9 @@ class DeviceMlmc:
             return None
         import torch.distributed as dist
 
-        return lambda t: dist.all_reduce(t, group=self.group)
+        from ._dist import all_reduce
+
+        return lambda t: all_reduce(t, group=self.group)
 
     def _split(self, n, uniq):
         """split mode: [start, stop) of this rank's contiguous slice of the unique masks, balanced by d^3, and
@@ -206,7 +208,9 @@ class DeviceMlmc:
         pad = torch.zeros((width, self.npts), dtype=torch.float64, device=self.dev)
         pad[: curves.shape[0]] = curves
         out = torch.empty((world * width, self.npts), dtype=torch.float64, device=self.dev)
-        dist.all_gather_into_tensor(out, pad, group=self.group)
+        from ._dist import all_gather_into_tensor
+
+        all_gather_into_tensor(out, pad, group=self.group)
         return torch.cat([out[r * width: r * width + (cuts[r + 1] - cuts[r])] for r in range(world)])
 
     def run_level(self, inp: LevelInputs):

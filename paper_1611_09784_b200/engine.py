@@ -695,12 +695,13 @@ class Engine:
             # exact cross-rank combination (fixed-point limbs, int64 all-reduce): the bits of one process
             # drawing all world * M replicates
             import torch
-            import torch.distributed as dist
+
+            from ._dist import all_reduce
 
             dev = torch.device("cuda", self.device)
             mean, var = exact_level_moments(torch.as_tensor(full).to(dev),
                                             None if quarters is None else torch.as_tensor(quarters).to(dev),
-                                            nsamples * world, allreduce=dist.all_reduce)
+                                            nsamples * world, allreduce=all_reduce)
             nsamples_all = nsamples * world
         else:
             nsamples_all = nsamples

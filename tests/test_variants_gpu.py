@@ -276,3 +276,8 @@ def test_chase_results_bitwise_repeatable(opts):
 def test_bulk_copy_rank_update_option(nu, q):
     """HX_RU_BULK=1 (persistent cp.async.bulk rank update, off by default) against the oracle."""
     check_batch("graphene", nu, q, 0.05, 4, 13, (0, 3), opts={"HX_RU_BULK": 1})
+
+
+def test_c3_table_her2k_3m_option():
+    """HX_HERK_3M=1: the 3M complex product in the Hermitian tier's her2k (1 CTA / SM) against zheevd."""
+    check_batch("table", 8, 2, 0.05, 3, 2026, (0, 2), opts={"HX_HERK_3M": 1})
