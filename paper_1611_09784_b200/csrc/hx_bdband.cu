@@ -228,9 +228,11 @@ static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, c
   }
 #undef BD_CHASE_REAL
   const bool pair = chase_mode >= 4 || (chase_mode == 0 && bd_chase_pair());
-  // warp-pair tasks for the throughput-bound launches (many matrices); the latency-bound one-CTA-per-matrix
-  // launch keeps one warp per task (its shared-memory pipe is the limit, measured 24.3 vs 25.1 ms)
-  if (pair && (want < 6 || chase_mode >= 4)) {
+  // warp-pair tasks for every launch size: the pair kernel's task arithmetic (two half sums per reduction)
+  // differs in rounding from the one-warp kernel's, so one family for all batch sizes keeps a mask's curve
+  // bitwise independent of the batch it is solved in (the one-warp kernel was 3 % faster on the latency-bound
+  // one-CTA-per-matrix launch: 24.3 vs 25.1 ms; HX_CHASE_PAIR=0 selects it everywhere)
+  if (pair) {
     if (want >= 6) BD_CHASE_PAIR(10)
     else if (want >= 2) BD_CHASE_PAIR(2)
     else BD_CHASE_PAIR(1)

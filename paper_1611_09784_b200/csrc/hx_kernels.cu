@@ -377,6 +377,11 @@ __device__ void refine_multisection(const CellDev& c, int nk, const GridDev& g, 
 
 // Phase 2: bisection of the eigenvalues left unsettled by eig_idos_kernel, densely
 // packed (every lane of a warp has real work), then the IDOS contribution (+ the TGK mirror).
+// Lanes per refinement item (1: per-thread Newton / bisection, 2-8: multisection), a function of the
+// matrix dimension alone (never the batch size).
+constexpr int g_refine_min_n = 1024;  // N >= this: multisection with 4 lanes per item
+__device__ __forceinline__ int refine_lanes(int N) { return N >= g_refine_min_n ? 4 : 1; }
+
 template <bool TGK>
 __global__ void __launch_bounds__(128) eig_refine_kernel(CellDev c, int nk, GridDev g, const double* __restrict__ tri,
                                                          size_t tri_stride, const int* __restrict__ dims, int* diff,
@@ -385,10 +390,10 @@ __global__ void __launch_bounds__(128) eig_refine_kernel(CellDev c, int nk, Grid
                                                          const unsigned long long* __restrict__ count) {
   const unsigned long long n = *count;
   const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
-  // G lanes per item: G-point multisection (log2(G+1) bits per Sturm round).  Few items (large matrices)
-  // are latency-bound and get up to 8 lanes each; many items are throughput-bound and keep one thread.
-  int G = 1;
-  while (G < 8 && n * (unsigned long long)(2 * G) * 2 <= nthreads) G *= 2;
+  // G lanes per item: G-point multisection (log2(G+1) bits per Sturm round).  The method is a function of
+  // the matrix size only (refine_lanes), never of the batch: the refined eigenvalues - and so the curves - are
+  // then bitwise independent of how the masks are split into batches, devices or ranks.
+  const int G = refine_lanes(c.N);
   if (G > 1) {
     refine_multisection<TGK>(c, nk, g, tri, tri_stride, dims, diff, trans, status, sharp, items, n, G);
     return;
@@ -643,13 +648,12 @@ __global__ void __launch_bounds__(128) zone_refine_kernel(CellDev c, int nk, Gri
                                                           const unsigned long long* __restrict__ count) {
   const unsigned long long n = *count;
   const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
-  // few items (large matrices): the slowest item bounds the launch, so use G-lane multisection with its
-  // fixed round count; many items: one thread per item, Newton (about 11 Sturm counts on average)
-  int G = 1;
-  while (G < 8 && n * (unsigned long long)(2 * G) * 2 <= nthreads) G *= 2;
-  // very large matrices hold ~10 eigenvalues per zone, often in near-degenerate clusters that Newton
-  // cannot isolate: the fixed round count of multisection wins there already at G = 2
-  if (G >= 4 || (G >= 2 && c.N >= 4096)) {
+  // large matrices (few per batch: the slowest item bounds the launch; ~10 eigenvalues per zone, often in
+  // near-degenerate clusters that Newton cannot isolate): G-lane multisection with its fixed round count;
+  // otherwise one thread per item, Newton (about 11 Sturm counts on average).  Chosen by the matrix size only
+  // (refine_lanes), so that results do not depend on the batch composition.
+  const int G = refine_lanes(c.N);
+  if (G > 1) {
     refine_multisection<ZD>(c, nk, g, tri, tri_stride, dims, diff, trans, status, sharp, items, n, G);
     return;
   }
