@@ -423,7 +423,16 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
       bd_chase_real_kernel<16, BB, CLN><<<(unsigned)(cnt * CLN), 16 * 32, bd_chase_real_smem<16, BB>(), st>>>( \
           ws2, a1, L.band_off, a3, S, dims);                                                                  \
   } while (0)
-    if (rcl == 2) BD_CHASE_REAL_CL(2);
+    // HX_CHASE_CLNW=8: 8 warps per CTA in the pairs of CTAs (the same 16 sweeps in flight per matrix as one
+    // 16-warp CTA, spread over two SMs: half the warps competing for each SM's issue slots)
+    if (rcl == 2 && opt("HX_CHASE_CLNW", 16) == 8) {
+      if (regrow)
+        bd_chase_realr_kernel<8, 2><<<(unsigned)(cnt * 2), 8 * 32, bd_chase_realr_smem<8>(), st>>>(
+            ws2, a1, L.band_off, a3, S, dims);
+      else
+        bd_chase_real_kernel<8, BB, 2><<<(unsigned)(cnt * 2), 8 * 32, bd_chase_real_smem<8, BB>(), st>>>(
+            ws2, a1, L.band_off, a3, S, dims);
+    } else if (rcl == 2) BD_CHASE_REAL_CL(2);
     else if (rcl == 4) BD_CHASE_REAL_CL(4);
     else BD_CHASE_REAL_CL(8);
 #undef BD_CHASE_REAL_CL
@@ -480,6 +489,8 @@ void bd_init_attributes() {
   set_smem_attr(bd_chase_realr_kernel<8>, 220 * 1024);
   set_smem_attr(bd_chase_realr_kernel<16>, 220 * 1024);
   set_smem_attr(bd_chase_realr_kernel<16, 2>, bd_chase_realr_smem<16>());
+  set_smem_attr(bd_chase_realr_kernel<8, 2>, bd_chase_realr_smem<8>());
+  set_smem_attr(bd_chase_real_kernel<8, BB, 2>, bd_chase_real_smem<8, BB>());
   set_smem_attr(bd_chase_realr_kernel<16, 4>, bd_chase_realr_smem<16>());
   set_smem_attr(bd_chase_realr_kernel<16, 8>, bd_chase_realr_smem<16>());
   const char* sp = getenv("HX_CHASE_SPIN_NS");
