@@ -30,6 +30,8 @@ from .models import compile_cell
 from .estimators import exact_level_moments
 from .solver import make_bz_grid, time_reversal_reduce, use_time_reversal
 
+_MERGE_TIERS = __import__("os").environ.get("HX_MERGE_TIERS", "0") == "1"
+
 
 @dataclass
 class LevelInputs:
@@ -237,16 +239,27 @@ class DeviceMlmc:
         start.record(main)
         outs = [None] * len(jobs)
         self.statuses = []
+        # HX_MERGE_TIERS=1: the jobs of one tier (the same n) from different levels go to ONE batch call
+        # (curves are batch independent, so only the packing of the GPU changes)
+        groups = {}
+        for j, (_, n, _, _, _) in enumerate(jobs):
+            groups.setdefault(n if _MERGE_TIERS else (n, j), []).append(j)
         # largest tier first (lane 0 = high priority)
-        order = sorted(range(len(jobs)), key=lambda j: -self.cell(jobs[j][1]).dim)
-        for lane, j in enumerate(order):
-            _, n, uniq, _, _ = jobs[j]
+        order = sorted(groups, key=lambda key: -self.cell(jobs[groups[key][0]][1]).dim)
+        for lane, key in enumerate(order):
+            js = groups[key]
+            n = jobs[js[0]][1]
+            uniq = jobs[js[0]][2] if len(js) == 1 else torch.cat([jobs[j][2] for j in js]).contiguous()
             ctx, stream = self._lane(lane) if concurrent else (self.ctx, main)
             stream.wait_event(start)
             curves, status = self._solve(n, uniq, ctx, stream)
             done = torch.cuda.Event()
             done.record(stream)
-            outs[j] = (curves, done)
+            off = 0
+            for j in js:
+                cnt = jobs[j][2].shape[0]
+                outs[j] = (curves[off: off + cnt], done)
+                off += cnt
             self.statuses.append(status)
         for _, done in outs:  # every lane joins the main stream before its outputs are used or released
             main.wait_event(done)

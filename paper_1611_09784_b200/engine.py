@@ -525,69 +525,68 @@ class Engine:
                             (start, ex.submit(self._solve_split, tier[0], tier[1], uniq[new], ids, ln, high, ticket),
                              bi))
                     plans[(bi, gi)] = (tier, uniq, inv, kv, src, start)
-            # batch bi can be placed once every piece of its tiers submitted by batches <= bi is done;
-            # batches are finished (placement, cache, on_batch) as soon as that holds, so their host work
-            # overlaps the device work still running for later batches
+            # group gi of batch bi can be placed once every piece of its tier submitted by batches <= bi is
+            # done; groups are placed (curves gathered, run cache filled) as soon as that holds and a batch is
+            # finished (on_batch) when its last group is in, so the host work overlaps the device work still
+            # running - at the end only the groups of the last tier to finish remain
             needs = {}
             for bi, tl in enumerate(tiers_of):
-                fs = []
-                for n, q in tl:
-                    fs += [f for (start, f, pbi) in pieces.get((n, q), []) if pbi <= bi]
-                needs[bi] = fs
+                for gi, (n, q) in enumerate(tl):
+                    needs[(bi, gi)] = [f for (start, f, pbi) in pieces.get((n, q), []) if pbi <= bi]
             out = [None] * len(batches)
-            left = list(range(len(batches)))
+            placed = {bi: [None] * len(tl) for bi, tl in enumerate(tiers_of)}
+            left = list(needs)
             while left:
-                ready = [bi for bi in left if all(f.done() for f in needs[bi])]
+                ready = [key for key in left if all(f.done() for f in needs[key])]
                 if not ready:
-                    wait([f for bi in left for f in needs[bi] if not f.done()], return_when=FIRST_COMPLETED)
+                    wait([f for key in left for f in needs[key] if not f.done()], return_when=FIRST_COMPLETED)
                     continue
-                for bi in ready:
-                    out[bi] = self._place_batch(bi, get(bi)[0], plans, pieces, hits, spent, npts)
-                    left.remove(bi)
-                    if on_batch is not None:
-                        on_batch(bi, out[bi])
+                for bi, gi in ready:
+                    placed[bi][gi] = self._place_group(bi, gi, plans, pieces, spent, npts)
+                    left.remove((bi, gi))
+                    if all(r is not None for r in placed[bi]):
+                        out[bi] = (placed[bi], hits[bi], spent[bi])
+                        if on_batch is not None:
+                            on_batch(bi, out[bi])
         return out
 
-    def _place_batch(self, bi, groups, plans, pieces, hits, spent, npts):
-        """Per-request curves of batch bi from the run cache and the solved pieces (runner.py:234-243).  Every
-        request row is gathered once from its source (a solved piece or the cache) - no intermediate array of
-        the unique masks' curves."""
-        res = []
-        for gi in range(len(groups)):
-            tier, uniq, inv, kv, src, start = plans[(bi, gi)]
-            R = len(inv)
-            out = np.empty((R, npts))
-            opj = np.empty(R)
-            rsrc = src[inv]  # per request row: piece row (>= 0) or cached (< 0)
-            pj_u = np.empty(len(uniq))
-            got = np.flatnonzero(src >= 0)
-            if len(got):
-                lst = pieces[tier]
-                starts = np.array([st for st, _, _ in lst])
-                which_u = np.searchsorted(starts, src[got], side="right") - 1
-                which_r = np.searchsorted(starts, rsrc, side="right") - 1
-                for k in np.unique(which_u):
-                    curves, per_job = lst[k][1].result()
-                    rows = np.flatnonzero((rsrc >= 0) & (which_r == k))
-                    out[rows] = curves[rsrc[rows] - lst[k][0]]
-                    opj[rows] = per_job
-                    pj_u[got[which_u == k]] = per_job
-            cached_r = np.flatnonzero(rsrc < 0)
-            cache = self._tier_cache(tier, npts)
-            if len(cached_r):
-                at = cache.find(kv[inv[cached_r]])
-                out[cached_r] = cache.curves[at]
-                opj[cached_r] = cache.pj[at]
-            # masks this batch solved first: their cost is this batch's, and they enter the run cache
-            own = np.flatnonzero(src >= start)
-            spent[bi] += float(pj_u[own].sum())
-            if kv is not None and len(own):
-                # the first request row of each own mask carries its curve
-                first = np.empty(len(uniq), dtype=np.int64)
-                first[inv[::-1]] = np.arange(R - 1, -1, -1)
-                cache.add(kv[own], out[first[own]], pj_u[own])
-            res.append((out, opj))
-        return res, hits[bi], spent[bi]
+    def _place_group(self, bi, gi, plans, pieces, spent, npts):
+        """Per-request curves of group gi of batch bi from the run cache and the solved pieces
+        (runner.py:234-243).  Every request row is gathered once from its source (a solved piece or the cache) -
+        no intermediate array of the unique masks' curves."""
+        tier, uniq, inv, kv, src, start = plans[(bi, gi)]
+        R = len(inv)
+        out = np.empty((R, npts))
+        opj = np.empty(R)
+        rsrc = src[inv]  # per request row: piece row (>= 0) or cached (< 0)
+        pj_u = np.empty(len(uniq))
+        got = np.flatnonzero(src >= 0)
+        if len(got):
+            lst = pieces[tier]
+            starts = np.array([st for st, _, _ in lst])
+            which_u = np.searchsorted(starts, src[got], side="right") - 1
+            which_r = np.searchsorted(starts, rsrc, side="right") - 1
+            for k in np.unique(which_u):
+                curves, per_job = lst[k][1].result()
+                rows = np.flatnonzero((rsrc >= 0) & (which_r == k))
+                out[rows] = curves[rsrc[rows] - lst[k][0]]
+                opj[rows] = per_job
+                pj_u[got[which_u == k]] = per_job
+        cached_r = np.flatnonzero(rsrc < 0)
+        cache = self._tier_cache(tier, npts)
+        if len(cached_r):
+            at = cache.find(kv[inv[cached_r]])
+            out[cached_r] = cache.curves[at]
+            opj[cached_r] = cache.pj[at]
+        # masks this batch solved first: their cost is this batch's, and they enter the run cache
+        own = np.flatnonzero(src >= start)
+        spent[bi] += float(pj_u[own].sum())
+        if kv is not None and len(own):
+            # the first request row of each own mask carries its curve
+            first = np.empty(len(uniq), dtype=np.int64)
+            first[inv[::-1]] = np.arange(R - 1, -1, -1)
+            cache.add(kv[own], out[first[own]], pj_u[own])
+        return out, opj
 
     def evaluate_masks(self, requests):
         """Dedup on (n, q, mask) against the run cache and within the batch; solve the new jobs of each

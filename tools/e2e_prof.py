@@ -52,7 +52,7 @@ def main():
             return out
         return wrap
 
-    hx.Engine._place_batch = timed("place", hx.Engine._place_batch)
+    hx.Engine._place_group = timed("place", hx.Engine._place_group)
     hx.Engine._level_finish = timed("finish", hx.Engine._level_finish)
     hx.Engine._level_batch = timed("draw", hx.Engine._level_batch)
 
