@@ -12,6 +12,8 @@
 // The Golub-Kahan tridiagonal (zero diagonal, off-diagonals alpha_0, gamma_0, alpha_1, ...) truncated to
 // d = nA + nB entries has exactly the eigenvalues of T; it goes through the shared bisection + IDOS kernel.
 // Flops: ~4/3 S'^3 ... i.e. 4x fewer than tridiagonalising T, on a 4x smaller slab.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -291,6 +293,38 @@ static bool launch_real_cluster_panel(double* ws, const RPanelArgs& a, int64_t c
   return true;
 }
 
+// 3-D tensor map (rows, columns, matrix) of the batch's S x S real matrices for the TMA rank update: boxes of
+// 16 rows x 64 columns, 128-byte swizzle.  cuTensorMapEncodeTiled comes from the driver through the runtime's
+// entry-point query (no libcuda link dependency).
+static bool make_matrix_tmap(CUtensorMap* map, double* base, int S, size_t ld, size_t slab_stride, int64_t cnt) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)S, (cuuint64_t)S, (cuuint64_t)cnt};
+  const cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)slab_stride * 8};
+  const cuuint32_t box[3] = {16, 64, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static void launch_rank_update_real_tma(const CUtensorMap& map, double* ws, const RSlab& G, int mr0, int mc0, int m,
+                                        int n, size_t u_off, size_t w_off, int64_t cnt, cudaStream_t st) {
+  const int ti = (m + 63) / 64, tj = (n + 63) / 64;
+  const int64_t ntiles = cnt * ti * tj;
+  if (ntiles <= 0) return;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, 148);
+  rank_update_real_tma_kernel<<<grid, 256, rru_tma_smem(), st>>>(map, ws, G, mr0, mc0, m, n, u_off, w_off, ti, tj,
+                                                                  ntiles);
+}
+
 // bulk-copy persistent rank update (HX_RU_BULK=0: the load-compute-store kernel); one CTA per SM
 static void launch_rank_update_real_bulk(double* ws, const RSlab& G, int mr0, int mc0, int m, int n, size_t u_off,
                                          size_t w_off, int64_t cnt, cudaStream_t st) {
@@ -319,8 +353,15 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
   // (0.292 vs 0.090 ms per launch on the N = 2048 tier): one cp.async.bulk per 512-byte tile column is bound by
   // the copy engine's per-request cost, not by HBM; kept as an option, off by default
   const bool ru_bulk = opt("HX_RU_BULK", 0) != 0;
+  // HX_RU_TMA=1: the TMA rank update (tensor-map boxes, 128-byte swizzle, 3 stages in flight) for the trailing
+  // updates that run to row and column S.  Correct, but measured slower than the cp.async kernel on the N = 2048
+  // tier (0.125 vs 0.091 ms per launch, 2.6 vs 3.7 TB/s: the C tile's extra round trip through shared memory and
+  // one CTA per SM), so it is off by default
+  CUtensorMap cmap;
+  const bool ru_tma = opt("HX_RU_TMA", 0) != 0 && make_matrix_tmap(&cmap, ws + c0, S, (size_t)S, sd, cnt);
   auto rank_update = [&](int mr0, int mc0, int m, int n, size_t u, size_t w) {
-    if (ru_bulk) launch_rank_update_real_bulk(ws, G, mr0, mc0, m, n, u, w, cnt, st);
+    if (ru_tma && mr0 + m == S && mc0 + n == S) launch_rank_update_real_tma(cmap, ws, G, mr0, mc0, m, n, u, w, cnt, st);
+    else if (ru_bulk) launch_rank_update_real_bulk(ws, G, mr0, mc0, m, n, u, w, cnt, st);
     else if (ru_rt == 128) launch_rank_update_real<128>(ws, G, mr0, mc0, m, n, u, w, cnt, st);
     else launch_rank_update_real<64>(ws, G, mr0, mc0, m, n, u, w, cnt, st);
   };
@@ -453,6 +494,7 @@ void bd_init_attributes() {
   set_smem_attr(rank_update_real_kernel<64>, (int)rru_smem<64>());
   set_smem_attr(rank_update_real_kernel<128>, (int)rru_smem<128>());
   set_smem_attr(rank_update_real_bulk_kernel, (int)rru_bulk_smem());
+  set_smem_attr(rank_update_real_tma_kernel, (int)rru_tma_smem());
   set_smem_attr(xv_kernel<0>, (int)XV_SMEM);
   set_smem_attr(xv_kernel<1>, (int)XV_SMEM);
   set_smem_attr(xv_kernel<0, true>, XV_SMEM_UPD);

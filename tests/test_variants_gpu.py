@@ -272,10 +272,12 @@ def test_chase_results_bitwise_repeatable(opts):
             assert np.array_equal(eigs, eigs0, equal_nan=True), rep
 
 
-@pytest.mark.parametrize("nu,q", [(16, 2), (12, 1)])
-def test_bulk_copy_rank_update_option(nu, q):
-    """HX_RU_BULK=1 (persistent cp.async.bulk rank update, off by default) against the oracle."""
-    check_batch("graphene", nu, q, 0.05, 4, 13, (0, 3), opts={"HX_RU_BULK": 1})
+@pytest.mark.parametrize("opts", [{"HX_RU_BULK": 1, "HX_RU_TMA": 0}, {"HX_RU_TMA": 0}, {"HX_RU_TMA": 1}])
+@pytest.mark.parametrize("nu,q", [(16, 2), (12, 1), (32, 1)])
+def test_rank_update_variants(nu, q, opts):
+    """The real rank update on the TMA engine (HX_RU_TMA=1, default: tensor-map boxes, 128-byte swizzle), the
+    cp.async kernel and the per-column bulk-copy kernel, against the oracle."""
+    check_batch("graphene", nu, q, 0.05, 4 if nu < 32 else 2, 13, (0, 1), opts=opts)
 
 
 def test_c3_table_her2k_3m_option():
