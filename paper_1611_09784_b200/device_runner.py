@@ -178,8 +178,6 @@ class DeviceMlmc:
     def _allreduce(self):
         if self.group is None or self.mode != "replicas":
             return None
-        import torch.distributed as dist
-
         from ._dist import all_reduce
 
         return lambda t: all_reduce(t, group=self.group)
@@ -201,8 +199,6 @@ class DeviceMlmc:
 
     def _gather(self, curves, cuts):
         """split mode: all ranks' slices of the unique curves, in unique order."""
-        import torch.distributed as dist
-
         rank, world = self._world()
         if world == 1:
             return curves

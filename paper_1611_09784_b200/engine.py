@@ -40,7 +40,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .estimators import (LevelPlan, LevelStats, MlmcEstimate, RateEstimates, combine_levels, exact_level_moments,
+from .estimators import (LevelPlan, LevelStats, RateEstimates, combine_levels, exact_level_moments,
                          fit_rates, level_moments, mean_and_variance, window_mask)
 from .geometry import build_supercell, partition_quarters
 from .idos import EnergyGrid

@@ -8,7 +8,6 @@ order of runner.py:281-299.
 
 from __future__ import annotations
 
-import ctypes as C
 import math
 from dataclasses import dataclass, field
 
