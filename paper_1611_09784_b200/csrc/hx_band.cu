@@ -684,9 +684,17 @@ int band_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks
   return 0;
 }
 
-int band_eigvalsh(int n, int64_t batch, const double2* A, double* eigs, int* status, size_t ws_budget,
-                  const Alloc& alloc, cudaStream_t st) {
-  const BandWs L = BandWs::make(n);
+__global__ void __launch_bounds__(256) band_copy_b_kernel(const double2* __restrict__ src, int64_t mat0, int N,
+                                                          double2* ws, BandWs L) {
+  double2* B = ws + (size_t)blockIdx.x * L.stride + L.b_off;
+  const double2* b = src + (size_t)(mat0 + blockIdx.x) * N * N;
+  for (int64_t p = threadIdx.x; p < (int64_t)N * N; p += blockDim.x) B[p] = b[p];
+}
+
+int band_eigvalsh(int n, int64_t batch, const double2* A, const double2* Bm, double* eigs, int* status,
+                  size_t ws_budget, const Alloc& alloc, cudaStream_t st) {
+  const bool general = Bm != nullptr;
+  const BandWs L = BandWs::make(n, general);
   const size_t per = L.stride * sizeof(double2) + sizeof(int) + (size_t)n * 8;
   int64_t chunk = std::max<int64_t>(1, (int64_t)(ws_budget / per));
   chunk = std::min<int64_t>(std::min<int64_t>(chunk, batch), 65535);
@@ -706,6 +714,11 @@ int band_eigvalsh(int n, int64_t batch, const double2* A, double* eigs, int* sta
     band_copy_kernel<<<(unsigned)cnt, 256, 0, st>>>(A, m0, n, ws, L, dims, status);
     count_launch();
     BAND_CUDA(cudaGetLastError());
+    if (general) {  // S = L L^H, then the standard problem L^-1 A L^-H (zhegv, spectrum.py:106-108)
+      band_copy_b_kernel<<<(unsigned)cnt, 256, 0, st>>>(Bm, m0, n, ws, L);
+      count_launch();
+      if (band_reduce_pencil(ws, L, n, cnt, status, m0, st)) return -1;
+    }
     if (band_reduce(ws, L, n, cnt, dims, st)) return -1;
     launch_eig_idos(c, 1, g, m0, cnt, reinterpret_cast<const double*>(ws + L.dg_off), L.stride * 2, dims, nullptr,
                     nullptr, eigs, status, 0, st);

@@ -21,9 +21,10 @@ int band_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks
               int* diff, unsigned long long* trans, double* eigs, int* status, int sharp, size_t ws_budget,
               const Alloc& alloc, cudaStream_t st, RefineItem* refine, unsigned long long* refine_count);
 
-// Eigenvalues of caller-provided Hermitian matrices (column-major complex, n x n each).
-int band_eigvalsh(int n, int64_t batch, const double2* A, double* eigs, int* status, size_t ws_budget,
-                  const Alloc& alloc, cudaStream_t st);
+// Eigenvalues of caller-provided Hermitian matrices (column-major complex, n x n each); B != nullptr: the
+// generalized problem A x = lambda B x (Cholesky of B, as the general-pencil tier).
+int band_eigvalsh(int n, int64_t batch, const double2* A, const double2* B, double* eigs, int* status,
+                  size_t ws_budget, const Alloc& alloc, cudaStream_t st);
 
 // Bipartite (graphene) banded tier: singular values of the A-B block (hx_bdband.cu).
 void bd_init_attributes();

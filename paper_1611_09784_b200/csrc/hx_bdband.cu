@@ -30,6 +30,7 @@
 #include "hx_panel.cuh"
 #include "hx_bdchase.cuh"
 #include "hx_real.cuh"
+#include "hx_gram.cuh"
 
 namespace hx {
 
@@ -486,7 +487,47 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
   return 0;
 }
 
+// Gram path (hx_gram.cuh): G = C^T C of the real batch formed in the slab, symmetric two-stage reduction to its
+// tridiagonal (diag[S], e2[S] doubles at the TGK offset).
+static int bd_reduce_gram(double2* ws2, const BdWs& L, int64_t cnt, int* status, cudaStream_t st) {
+  const int S = L.S;
+  double* ws = reinterpret_cast<double*>(ws2);
+  const size_t sd = 2 * L.stride, c0 = 2 * L.c_off, v1 = 2 * L.v1_off, x = 2 * L.x_off, t1 = 2 * L.t1_off;
+  const RSlab G{sd, S, c0};
+  gram_build_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, sd, c0, v1, S, status);
+  count_launch();
+  for (int k0 = 0; S - k0 - BB > 0; k0 += BB) {
+    const int m = S - k0 - BB;
+    const RPanelArgs p{sd, c0, S, k0 + BB, k0, m, 0, v1, S, t1};
+    if (!launch_real_cluster_panel(ws, p, cnt, st)) {
+      g_bd_err = "panel does not fit the cluster shared memory";
+      return -1;
+    }
+    xv_real_kernel<0><<<dim3((unsigned)((m + RXV_TM - 1) / RXV_TM), (unsigned)cnt), 128, RXV_SMEM, st>>>(
+        ws, G, k0 + BB, k0 + BB, m, m, v1, x, t1);
+    w_fix_real_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, G, m, v1, x, t1);
+    launch_rank_update_real<64>(ws, G, k0 + BB, k0 + BB, m, m, x, v1, cnt, st);  // G22 -= W V^T
+    launch_rank_update_real<64>(ws, G, k0 + BB, k0 + BB, m, m, v1, x, cnt, st);  // G22 -= V W^T
+    count_launch(5);
+    BD_CUDA(cudaGetLastError());
+  }
+  const int64_t want = (148 * 11 + cnt - 1) / cnt;
+#define SYM_CHASE(NW)                                                                                      \
+  sym_chase_real_kernel<NW><<<(unsigned)cnt, NW * 32, sym_chase_real_smem<NW>(), st>>>(ws, sd, c0,          \
+                                                                                      2 * L.tgk_off, S)
+  if (want >= 6) SYM_CHASE(16);
+  else if (want >= 2) SYM_CHASE(4);
+  else SYM_CHASE(1);
+#undef SYM_CHASE
+  count_launch();
+  BD_CUDA(cudaGetLastError());
+  return 0;
+}
+
 void bd_init_attributes() {
+  set_smem_attr(sym_chase_real_kernel<16>, (int)sym_chase_real_smem<16>());
+  set_smem_attr(sym_chase_real_kernel<4>, (int)sym_chase_real_smem<4>());
+  set_smem_attr(sym_chase_real_kernel<1>, (int)sym_chase_real_smem<1>());
   set_smem_attr(xv_real_kernel<0>, (int)RXV_SMEM);
   set_smem_attr(xv_real_kernel<1>, (int)RXV_SMEM);
   set_smem_attr(xv_real_kernel<0, true>, (int)RXV_SMEM_UPD);
@@ -564,12 +605,27 @@ int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, 
   // TGK tridiagonal of dimension up to 2S: eigenvalue kernel over cells of width 2S
   CellDev ce = c;
   ce.N = 2 * S;
+  // Gram path (HX_GRAM=1): real IDOS-only batches whose transition zones stay clear of lambda = 0.  Correct
+  // (tests/test_variants_gpu.py::test_gram_path_*), but measured slower on c2 (86.8 vs 63.0 ms per step): the
+  // symmetric chase on the dense slab runs at half the speed of the tuned compact-band bidiagonal chase and the
+  // panel / product savings (panels 11 -> 5 ms, xv 7.9 -> 3.7 ms per pass) do not cover it; off by default
+  CellDev cg = c;
+  cg.N = S;
+  const bool gram = real_s1 && !eigs && refine && refine_count && opt("HX_GRAM", 0) != 0 &&
+                    gram_zones_ok(cg, g, sharp, 1e-3);
   for (int64_t m0 = 0; m0 < nmat; m0 += chunk) {
     const int64_t cnt = std::min(chunk, nmat - m0);
     bd_assemble_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, masks, m0, ws, L, dims, status,
                                                          real ? (real_s1 ? 2 : 1) : 0);
     count_launch();
     BD_CUDA(cudaGetLastError());
+    if (gram) {
+      if (bd_reduce_gram(ws, L, cnt, status + m0, st)) return -1;
+      launch_gram_idos(cg, nk, g, m0, cnt, reinterpret_cast<const double*>(ws + L.tgk_off), L.stride * 2, dims, diff,
+                       trans, status, sharp, st, refine, refine_count);
+      BD_CUDA(cudaGetLastError());
+      continue;
+    }
     const int rc = real_s1 ? bd_reduce_real(ws, L, cnt, dims, st)
                            : (real ? bd_reduce<true>(ws, L, cnt, dims, st) : bd_reduce<false>(ws, L, cnt, dims, st));
     if (rc) return -1;

@@ -718,8 +718,9 @@ int hx_eigvalsh_batch_device(hx_ctx* ctx, int32_t n, int64_t batch, const double
   hx::CellDev c{};
   c.N = n;
   hx::GridDev g{};
-  if (!d_B && hx::band_path_supported(n)) {
-    int rc = hx::band_eigvalsh(n, batch, reinterpret_cast<const double2*>(d_A), d_eigs, status, ctx->ws_budget,
+  if (hx::band_path_supported(n) && (!d_B || general_band())) {
+    int rc = hx::band_eigvalsh(n, batch, reinterpret_cast<const double2*>(d_A),
+                               reinterpret_cast<const double2*>(d_B), d_eigs, status, ctx->ws_budget,
                                [&](size_t bytes) -> void* { return ctx->band.grow(bytes) ? nullptr : ctx->band.p; }, st);
     if (rc) return fail(HX_E_CUDA, std::string("band path: ") + hx::band_last_error());
     return 0;

@@ -1,0 +1,304 @@
+// Gram path of the bipartite (graphene) banded tier for real (time-reversal-invariant) IDOS batches.
+//
+// The eigenvalues of T = [[0, C], [C^T, 0]] are +-sigma(C) (plus zeros), and sigma^2 are the eigenvalues of
+// G = C^T C.  G is symmetric with ~7 nonzeros per column (B sites sharing an A neighbour), formed in O(S) from
+// the sparsity of C; its tridiagonalisation is a one-sided-per-step symmetric two-stage reduction - ONE panel
+// QR and ONE product per step instead of the two of the bidiagonal reduction of C - followed by a symmetric
+// band chase, and its tridiagonal has dimension S instead of the 2S of the TGK form.  The eigenvalue stage
+// counts and refines in mu = sigma^2 (zone_count_gram_kernel); sigma^2 keeps full relative accuracy away from
+// sigma = 0, and the host uses the path only when no transition zone comes near lambda = 0 (gram_zones_ok).
+//
+//   gram_build_kernel       dense C (slab, ld S) -> sparse column / row lists -> dense G in place
+//   stage 1 (per k0)        panel_qr_real (column panel below the band) -> Y = G22 V T (xv_real) ->
+//                           w_fix_real_kernel: W = Y - 1/2 V (T^T (V^T Y)) -> G22 -= W V^T, G22 -= V W^T (DMMA)
+//   sym_chase_real_kernel   symmetric band (lower, width 32) -> tridiagonal (diag, e2)
+#pragma once
+#include "hx_dense.cuh"
+#include "hx_real.cuh"
+
+namespace hx {
+
+constexpr int GRAM_K = 8;  // nonzeros kept per row / column of C (graphene: 3)
+
+// One CTA per matrix.  C: S x S doubles (ld S) at base + c_off; scratch (>= S * GRAM_K * 6 + 2 S doubles) at
+// base + l_off; G overwrites C.  Every column of G is accumulated by one thread in a fixed order (the lists are
+// in row / column order), so the result is deterministic.  A row or column of C with more than GRAM_K nonzeros
+// (not graphene) marks the matrix failed (status, this chunk's rows).
+__global__ void __launch_bounds__(256) gram_build_kernel(double* ws, size_t stride, size_t c_off, size_t l_off, int S,
+                                                         int* status) {
+  double* base = ws + (size_t)blockIdx.x * stride;
+  double* C = base + c_off;
+  double* colVal = base + l_off;                                   // [S][GRAM_K]
+  double* rowVal = colVal + (size_t)S * GRAM_K;                    // [S][GRAM_K]
+  int* colIdx = reinterpret_cast<int*>(rowVal + (size_t)S * GRAM_K);  // [S][GRAM_K]
+  int* rowIdx = colIdx + (size_t)S * GRAM_K;                       // [S][GRAM_K]
+  int* colCnt = rowIdx + (size_t)S * GRAM_K;                       // [S]
+  int* rowCnt = colCnt + S;                                        // [S]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  __shared__ int over;
+  if (tid == 0) over = 0;
+  __syncthreads();
+  // columns: one warp per column, lanes over rows (coalesced), ballot-compacted in row order
+  for (int j = warp; j < S; j += nw) {
+    int cnt = 0;
+    for (int r0 = 0; r0 < S; r0 += 32) {
+      const int r = r0 + lane;
+      const double v = r < S ? C[r + (size_t)j * S] : 0.0;
+      const unsigned nzb = __ballot_sync(0xffffffffu, v != 0.0);
+      const int pos = cnt + __popc(nzb & ((1u << lane) - 1u));
+      if (v != 0.0) {
+        if (pos < GRAM_K) {
+          colIdx[(size_t)j * GRAM_K + pos] = r;
+          colVal[(size_t)j * GRAM_K + pos] = v;
+        } else {
+          over = 1;
+        }
+      }
+      cnt += __popc(nzb);
+    }
+    if (lane == 0) colCnt[j] = min(cnt, GRAM_K);
+  }
+  // rows: one thread per row, columns in order (consecutive threads read consecutive rows: coalesced)
+  for (int i = tid; i < S; i += blockDim.x) {
+    int cnt = 0;
+    for (int c = 0; c < S; ++c) {
+      const double v = C[i + (size_t)c * S];
+      if (v != 0.0) {
+        if (cnt < GRAM_K) {
+          rowIdx[(size_t)i * GRAM_K + cnt] = c;
+          rowVal[(size_t)i * GRAM_K + cnt] = v;
+        } else {
+          over = 1;
+        }
+        ++cnt;
+      }
+    }
+    rowCnt[i] = min(cnt, GRAM_K);
+  }
+  __syncthreads();
+  for (size_t p = tid; p < (size_t)S * S; p += blockDim.x) C[p] = 0.0;
+  __syncthreads();
+  // G[:, j] = sum_{i in col(j)} C_ij C[i, :]^T
+  for (int j = tid; j < S; j += blockDim.x) {
+    double* Gj = C + (size_t)j * S;
+    const int nc = colCnt[j];
+    for (int a = 0; a < nc; ++a) {
+      const int i = colIdx[(size_t)j * GRAM_K + a];
+      const double cij = colVal[(size_t)j * GRAM_K + a];
+      const int nr = rowCnt[i];
+      for (int b = 0; b < nr; ++b) {
+        const int k = rowIdx[(size_t)i * GRAM_K + b];
+        Gj[k] = fma(cij, rowVal[(size_t)i * GRAM_K + b], Gj[k]);
+      }
+    }
+  }
+  if (tid == 0 && over) status[blockIdx.x] = 2;  // HX_ST_NONFINITE: surfaces as an error, never silently
+}
+
+// W = Y - 1/2 V (T^T (V^T Y)) for the m rows of the step (Y = X at x_off, overwritten), V at v_off, T at t_off
+// (doubles, ld = ld), one CTA per matrix.
+__global__ void __launch_bounds__(256) w_fix_real_kernel(double* ws, RSlab g, int m, size_t v_off, size_t x_off,
+                                                         size_t t_off) {
+  __shared__ double Vs[32][33], Ys[32][33], Zs[32][33], Ms[32][33];
+  double* base = ws + (size_t)blockIdx.x * g.stride;
+  const double* V = base + v_off;
+  double* Y = base + x_off;
+  const double* T = base + t_off;
+  const int ld = g.ld, tid = threadIdx.x;
+  const int a0 = tid >> 5, b = tid & 31;  // this thread: Z[a0 + 8 q][b], q < 4
+  double z[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int r0 = 0; r0 < m; r0 += 32) {
+    for (int p = tid; p < 1024; p += 256) {
+      const int rr = p & 31, c = p >> 5;
+      const bool ok = r0 + rr < m;
+      Vs[rr][c] = ok ? V[r0 + rr + (size_t)c * ld] : 0.0;
+      Ys[rr][c] = ok ? Y[r0 + rr + (size_t)c * ld] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < 32; ++rr) {
+      const double y = Ys[rr][b];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) z[q] = fma(Vs[rr][a0 + 8 * q], y, z[q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) Zs[a0 + 8 * q][b] = z[q];
+  for (int p = tid; p < 1024; p += 256) Vs[p & 31][p >> 5] = T[p];  // Vs[l][a] = T[l][a] (column-major T)
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // Ms = 1/2 T^T Z: Ms[a][b] = 1/2 sum_l T[l][a] Z[l][b]
+    const int a = a0 + 8 * q;
+    double t = 0.0;
+    for (int l = 0; l < 32; ++l) t = fma(Vs[l][a], Zs[l][b], t);
+    Ms[a][b] = 0.5 * t;
+  }
+  __syncthreads();
+  for (int r0 = 0; r0 < m; r0 += 32) {
+    for (int p = tid; p < 1024; p += 256) {
+      const int rr = p & 31, c = p >> 5;
+      Vs[rr][c] = r0 + rr < m ? V[r0 + rr + (size_t)c * ld] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int rr = a0 + 8 * q;
+      if (r0 + rr < m) {
+        double w = Y[r0 + rr + (size_t)b * ld];
+        for (int a = 0; a < 32; ++a) w = fma(-Vs[rr][a], Ms[a][b], w);
+        Y[r0 + rr + (size_t)b * ld] = w;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Real symmetric band (lower, width BWc, dense slab A with ld S) -> tridiagonal (diag[S], e2[S] doubles at
+// out), pipelined over sweeps exactly as bulge_chase_pipe_kernel (hx_chase.cuh) on real data: task t of sweep
+// i updates the diagonal block D = A[s:s+len, s:s+len] two-sidedly (p = D v, w = tau p - tau^2/2 (v.p) v,
+// D -= v w^T + w v^T) and the block below it, B'' = B - q v^T - v' z^T (q = tau B v; H' from column 0 of B H).
+struct SymChaseSmem {
+  double D[32][33];
+  double v[32], w[32], vp[32], z[32];
+};
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) sym_chase_real_kernel(double* ws, size_t stride, size_t a_off,
+                                                                     size_t out_off, int S) {
+  constexpr int BWc = 32;
+  extern __shared__ __align__(16) unsigned char scs_raw[];
+  SymChaseSmem* all = reinterpret_cast<SymChaseSmem*>(scs_raw);
+  volatile int* prog = reinterpret_cast<volatile int*>(all + NW);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  SymChaseSmem& W = all[warp];
+  double* base = ws + (size_t)blockIdx.x * stride;
+  double* A = base + a_off;
+  double* diag = base + out_off;
+  double* e2 = diag + S;
+  const int lda = S, d = S;
+  if (lane == 0) prog[warp] = -1;
+  for (int q = threadIdx.x; q < 2 * S; q += blockDim.x) diag[q] = 0.0;
+  __syncthreads();
+  const int nsweeps = d - 1;
+  for (int i = warp; i < nsweeps; i += NW) {
+    const int tasks = (d - 1 - i + BWc - 1) / BWc;
+    const int prev_tasks = i > 0 ? (d - i + BWc - 1) / BWc : 0;
+    const int pw = (i - 1 + NW) % NW;
+    double tau = 0.0;
+    for (int t = 0; t < tasks; ++t) {
+      if (i > 0) {
+        const int need = (i - 1) * 65536 + min(t + 2, prev_tasks);
+        if (lane == 0)
+          while (prog[pw] < need) __nanosleep(20);
+        __syncwarp();
+        __threadfence_block();
+      }
+      const int s = i + 1 + t * BWc;
+      const int len = min(BWc, d - s);
+      const int lb = max(0, min(BWc, d - s - len));
+      double* const colp = A + ((size_t)s * lda + s + lane);  // (s + lane, s + c) at colp[c * lda]
+      // D: lower triangle, mirrored
+#pragma unroll 4
+      for (int c = 0; c < BWc; ++c) W.D[lane][c] = (c < len && lane >= c && lane < len) ? colp[(size_t)c * lda] : 0.0;
+      if (t == 0) {
+        const double x = lane < len ? A[s + lane + (size_t)i * lda] : 0.0;  // column i, rows s ..
+        const double sig2 = warp_sum(x * x);
+        const QuickReflectorR h = quick_reflector_r(__shfl_sync(0xffffffffu, x, 0), sig2);
+        tau = h.tau;
+        W.v[lane] = lane == 0 ? 1.0 : (lane < len ? x * h.scale : 0.0);
+        if (lane < len && tau != 0.0) A[s + lane + (size_t)i * lda] = lane == 0 ? h.beta : 0.0;
+        if (lane == 0) {
+          diag[i] = A[i + (size_t)i * lda];
+          e2[i] = sig2;
+        }
+      }
+      __syncwarp();
+#pragma unroll 4
+      for (int c = 0; c < BWc; ++c)
+        if (c > lane) W.D[lane][c] = W.D[c][lane];
+      __syncwarp();
+      // p = D v (lane = row), w = tau p - tau^2/2 (v.p) v
+      double p;
+      {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+        for (int c = 0; c < BWc; c += 2) {
+          a0 = fma(W.D[lane][c], W.v[c], a0);
+          a1 = fma(W.D[lane][c + 1], W.v[c + 1], a1);
+        }
+        p = a0 + a1;
+      }
+      const double vr = W.v[lane];
+      const double cval = warp_sum(vr * p);
+      const double wr = tau * p - 0.5 * tau * tau * cval * vr;
+      W.w[lane] = wr;
+      __syncwarp();
+      if (lane < len) {
+#pragma unroll 4
+        for (int c = 0; c < BWc; ++c) {
+          const double z = W.D[lane][c] - (vr * W.w[c] + wr * W.v[c]);
+          if (c <= lane && c < len) colp[(size_t)c * lda] = z;
+        }
+      }
+      if (lb > 0) {
+        __syncwarp();
+#pragma unroll 4
+        for (int c = 0; c < BWc; ++c) W.D[lane][c] = (c < len && lane < lb) ? colp[len + (size_t)c * lda] : 0.0;
+        __syncwarp();
+        // q = tau B v (lane = row); column 0 of B - q v^T -> H'
+        double q;
+        {
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+          for (int c = 0; c < BWc; c += 2) {
+            a0 = fma(W.D[lane][c], W.v[c], a0);
+            a1 = fma(W.D[lane][c + 1], W.v[c + 1], a1);
+          }
+          q = tau * (a0 + a1);
+        }
+        const double x0 = W.D[lane][0] - q;
+        const double sg2 = warp_sum(x0 * x0);
+        const QuickReflectorR hp = quick_reflector_r(__shfl_sync(0xffffffffu, x0, 0), sg2);
+        const double vpr = lane == 0 ? 1.0 : x0 * hp.scale;  // zero on padded rows
+        W.vp[lane] = vpr;
+        const double wq = warp_sum(vpr * q);
+        __syncwarp();
+        // column pass (lane = column): z_c = tau' (v'.B[:, c] - wq v_c)
+        {
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+          for (int r = 0; r < BWc; r += 2) {
+            a0 = fma(W.vp[r], W.D[r][lane], a0);
+            a1 = fma(W.vp[r + 1], W.D[r + 1][lane], a1);
+          }
+          W.z[lane] = hp.tau * (a0 + a1 - wq * W.v[lane]);
+        }
+        __syncwarp();
+        if (lane < lb) {
+#pragma unroll 4
+          for (int c = 0; c < BWc; ++c) {
+            double y = W.D[lane][c] - (q * W.v[c] + vpr * W.z[c]);
+            if (c == 0 && hp.tau != 0.0) y = lane == 0 ? hp.beta : 0.0;
+            if (c < len) colp[len + (size_t)c * lda] = y;
+          }
+        }
+        __syncwarp();
+        W.v[lane] = vpr;
+        tau = hp.tau;
+      }
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) prog[warp] = i * 65536 + t + 1;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) diag[d - 1] = A[d - 1 + (size_t)(d - 1) * lda];
+}
+
+template <int NW>
+constexpr size_t sym_chase_real_smem() {
+  return NW * sizeof(SymChaseSmem) + 64;
+}
+
+}  // namespace hx

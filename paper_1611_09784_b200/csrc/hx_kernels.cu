@@ -686,6 +686,168 @@ static bool zone_path_ok(const CellDev& c, const GridDev& g, int sharp, bool& re
   return (size_t)g.npts * 2 * sizeof(int) <= 96 * 1024;
 }
 
+// ------------------------------------------------------------------------------------------------
+// Gram mode of the zone path (graphene IDOS batches reduced through G = C^T C, hx_gram.cuh): the tridiagonal is
+// that of G (dimension S = the padded sublattice size: the m = min(nA, nB) values sigma^2 plus S - m zeros), not
+// the TGK of C.  The eigenvalues of T = [[0, C], [C^T, 0]] (dimension d = nA + nB) are +-sigma plus d - 2m
+// zeros, so for x away from 0
+//     count_T(x) = d - S + count_G(x^2)   (x > 0),      count_T(x) = S - count_G(x^2)   (x < 0),
+// and the zone eigenvalues are located in mu = sigma^2 (relative accuracy eps in mu = eps/2 in sigma) and mapped
+// to lambda = +-sqrt(mu).  The host uses this mode only when no transition zone comes near lambda = 0, where
+// sigma^2 loses its relative accuracy (gram_zones_ok).
+__global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk, GridDev g, int sharp, int rev,
+                                                              int64_t mat0, int64_t nmat, const double* __restrict__ tri,
+                                                              size_t tri_stride, const int* __restrict__ dims,
+                                                              int* diff, RefineItem* refine,
+                                                              unsigned long long* refine_count) {
+  extern __shared__ int zc[];  // [2 npts] T counts at the zone edges, then [2 npts] Gram counts
+  __shared__ double red[3][32];
+  const int64_t lm = blockIdx.x;
+  if (lm >= nmat) return;
+  const int d = dims[lm];
+  if (d <= 0) return;
+  const int S = c.N, npts = g.npts;
+  int* zg = zc + 2 * npts;
+  const int64_t mat = mat0 + lm;
+  const int64_t mk = mat / nk;
+  const double* diag = tri + lm * tri_stride;
+  const double* e2 = diag + S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  double gl = 1e308, gu = -1e308, em = 0.0;
+  for (int i = tid; i < S; i += blockDim.x) {
+    const double el = i > 0 ? sqrt(e2[i - 1]) : 0.0;
+    const double er2 = i + 1 < S ? e2[i] : 0.0;
+    const double er = sqrt(er2);
+    gl = fmin(gl, diag[i] - el - er);
+    gu = fmax(gu, diag[i] + el + er);
+    em = fmax(em, er2);
+  }
+  gl = warp_min(gl);
+  gu = warp_max(gu);
+  em = warp_max(em);
+  if (lane == 0) {
+    red[0][warp] = gl;
+    red[1][warp] = gu;
+    red[2][warp] = em;
+  }
+  __syncthreads();
+  gl = red[0][0];
+  gu = red[1][0];
+  em = red[2][0];
+  for (int w = 1; w < nw; ++w) {
+    gl = fmin(gl, red[0][w]);
+    gu = fmax(gu, red[1][w]);
+    em = fmax(em, red[2][w]);
+  }
+  const double pivmin = DBL_MIN * fmax(1.0, em);
+  const double tnorm = fmax(fabs(gl), fabs(gu));
+  gl = gl - 2.1 * tnorm * DBL_EPSILON * S - 4.2 * pivmin;
+  gu = gu + 2.1 * tnorm * DBL_EPSILON * S + 4.2 * pivmin;
+  for (int m = tid; m < npts; m += blockDim.x) {
+    double la, lb;
+    zone_bracket(c, g, sharp, m, la, lb);
+    const bool pos = la > 0.0;
+    const double xa = pos ? la * la : lb * lb, xb = pos ? lb * lb : la * la;  // mu bracket, xa < xb
+    const bool ra = xa > gl && xa < gu, rb = xb > gl && xb < gu;
+    int ca = xa <= gl ? 0 : S, cb = xb <= gl ? 0 : S;
+    if (ra || rb) {
+      double qa = diag[0] - xa, qb = diag[0] - xb;
+      if (fabs(qa) <= pivmin) qa = -pivmin;
+      if (fabs(qb) <= pivmin) qb = -pivmin;
+      int na = qa < 0.0, nb = qb < 0.0;
+      for (int i = 1; i < S; ++i) {
+        const double e = e2[i - 1], a = diag[i];
+        qa = fma(-e, sturm_rcp(qa), a - xa);
+        qb = fma(-e, sturm_rcp(qb), a - xb);
+        if (fabs(qa) <= pivmin) qa = -pivmin;
+        if (fabs(qb) <= pivmin) qb = -pivmin;
+        na += qa < 0.0;
+        nb += qb < 0.0;
+      }
+      if (ra) ca = na;
+      if (rb) cb = nb;
+    }
+    cb = max(ca, cb);
+    zg[2 * m] = ca;
+    zg[2 * m + 1] = cb;
+    zc[2 * m] = pos ? d - S + ca : S - cb;
+    zc[2 * m + 1] = pos ? d - S + cb : S - ca;
+  }
+  __syncthreads();
+  int* drow = diff + mk * (npts + 1);
+  for (int m = tid; m < npts; m += blockDim.x) {
+    int n;
+    if (!rev) n = zc[2 * m] - (m > 0 ? zc[2 * m - 1] : 0);
+    else n = (m > 0 ? zc[2 * m - 2] : d) - zc[2 * m + 1];
+    if (n > 0) atomicAdd(drow + m, n * kmul(g, mat, nk));
+    const int i0 = zg[2 * m], nz = zg[2 * m + 1] - i0;
+    if (nz > 0) {
+      double la, lb;
+      zone_bracket(c, g, sharp, m, la, lb);
+      const bool pos = la > 0.0;
+      const double xa = pos ? la * la : lb * lb, xb = pos ? lb * lb : la * la;
+      const unsigned long long p0 = atomicAdd(refine_count, (unsigned long long)nz);
+      for (int k = 0; k < nz; ++k)
+        refine[p0 + k] = RefineItem{mat, lm, i0 + k,
+                                    (int)(1u | (pos ? 0u : 2u) | ((unsigned)k << 2) | ((unsigned)nz << 17)),
+                                    fmax(xa, gl), fmin(xb, gu), pivmin};
+    }
+  }
+}
+
+// Gram zone eigenvalues: mu by the bracketed Newton search of zone_locate on G's tridiagonal, lambda = +-sqrt(mu).
+__global__ void __launch_bounds__(128) zone_refine_gram_kernel(CellDev c, int nk, GridDev g,
+                                                               const double* __restrict__ tri, size_t tri_stride,
+                                                               int* diff, unsigned long long* trans, int* status,
+                                                               int sharp, const RefineItem* __restrict__ items,
+                                                               const unsigned long long* __restrict__ count) {
+  const unsigned long long n = *count;
+  const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+  const int S = c.N;
+  for (unsigned long long q = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += nthreads) {
+    const RefineItem it = items[q];
+    const double* diag = tri + it.lm * tri_stride;
+    const unsigned f = (unsigned)it.flags;
+    const int k = (int)((f >> 2) & 0x7fffu), nz = (int)(f >> 17);
+    const int clo = it.idx - k;
+    const double mu = zone_locate<false>(diag, diag + S, S, it.idx, it.lo, it.hi, clo, clo + nz, it.pivmin);
+    const double sg = sqrt(fmax(mu, 0.0));
+    add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, (f & 2u) ? -sg : sg);
+  }
+}
+
+bool gram_zones_ok(const CellDev& c, const GridDev& g, int sharp, double lam_min) {
+  bool rev = false;
+  if (c.pencil != 1 || !zone_path_ok(c, g, sharp, rev)) return false;
+  for (int m = 0; m < g.npts; ++m) {
+    const double em = g.e0 + g.step * m;
+    const double w = sharp ? 0.0 : g.delta;
+    const double a = pencil_inv(c.pencil, c.eps0, c.t, c.s, em - w - 1e-9),
+                 b = pencil_inv(c.pencil, c.eps0, c.t, c.s, em + w + 1e-9);
+    if (!(a * b > 0.0) || std::fmin(std::fabs(a), std::fabs(b)) < lam_min) return false;
+  }
+  return true;
+}
+
+// Gram-mode eigenvalue stage (IDOS only): false if the zone path does not apply (the caller uses the TGK path).
+bool launch_gram_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, int64_t nmat, const double* tri,
+                      size_t tri_stride, const int* dims, int* diff, unsigned long long* trans, int* status, int sharp,
+                      cudaStream_t st, RefineItem* refine, unsigned long long* refine_count) {
+  bool rev = false;
+  if (!refine || !refine_count || !diff || !zone_path_ok(c, g, sharp, rev)) return false;
+  cudaMemsetAsync(refine_count, 0, sizeof(unsigned long long), st);
+  const size_t zsm = (size_t)g.npts * 4 * sizeof(int);
+  const int zt = g.npts >= 256 ? 256 : ((g.npts + 31) / 32) * 32;
+  set_smem_attr(zone_count_gram_kernel, zsm);
+  zone_count_gram_kernel<<<(unsigned)nmat, zt, zsm, st>>>(c, nk, g, sharp, rev, mat0, nmat, tri, tri_stride, dims,
+                                                           diff, refine, refine_count);
+  zone_refine_gram_kernel<<<148 * 16, 128, 0, st>>>(c, nk, g, tri, tri_stride, diff, trans, status, sharp, refine,
+                                                    refine_count);
+  count_launch(2);
+  return true;
+}
+
+
 
 
 void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, int64_t nmat, const double* tri,

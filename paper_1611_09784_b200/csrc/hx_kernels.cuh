@@ -53,6 +53,11 @@ __global__ void finalize_kernel(const int* diff, const unsigned long long* trans
 // tridiagonals are Golub-Kahan (zero diagonal, spectrum symmetric about 0): one thread per +-pair.
 // smallest N that takes the zone path of the eigenvalue stage (HX_ZONE_MIN_N; 0 = always)
 
+// Gram mode (hx_kernels.cu): zone path on the tridiagonal of G = C^T C; false if it does not apply.
+bool gram_zones_ok(const CellDev& c, const GridDev& g, int sharp, double lam_min);
+bool launch_gram_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, int64_t nmat, const double* tri,
+                      size_t tri_stride, const int* dims, int* diff, unsigned long long* trans, int* status, int sharp,
+                      cudaStream_t st, RefineItem* refine, unsigned long long* refine_count);
 void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, int64_t nmat, const double* tri,
                      size_t tri_stride, const int* dims, int* diff, unsigned long long* trans, double* eigs,
                      int* status, int sharp, cudaStream_t st, RefineItem* refine = nullptr,

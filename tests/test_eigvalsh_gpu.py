@@ -23,18 +23,23 @@ def rand_herm(rng, n, batch, pad=0):
     return a
 
 
-def gpu_eigvalsh(a):
+def gpu_eigvalsh(a, b=None):
     import torch
 
     batch, n, _ = a.shape
     dev = torch.device("cuda", 0)
-    # column-major complex: store A^T row-major == A column-major
-    at = np.ascontiguousarray(np.swapaxes(a, 1, 2))
-    A = torch.from_numpy(at.view(np.float64).reshape(batch, n, n, 2)).to(dev)
+
+    def up(m):  # column-major complex: store M^T row-major == M column-major
+        mt = np.ascontiguousarray(np.swapaxes(m, 1, 2))
+        return torch.from_numpy(mt.view(np.float64).reshape(batch, n, n, 2)).to(dev)
+
+    A = up(a)
+    B = None if b is None else up(b)
     eig = torch.empty((batch, n), dtype=torch.float64, device=dev)
     st = torch.empty(batch, dtype=torch.int32, device=dev)
     ctx = _lib.Device.ctx(0)
-    _lib.check(_lib.load().hx_eigvalsh_batch_device(ctx, n, batch, A.data_ptr(), 0, eig.data_ptr(), st.data_ptr(),
+    _lib.check(_lib.load().hx_eigvalsh_batch_device(ctx, n, batch, A.data_ptr(), 0 if B is None else B.data_ptr(),
+                                                    eig.data_ptr(), st.data_ptr(),
                                                     torch.cuda.current_stream(dev).cuda_stream), "eigvalsh")
     torch.cuda.synchronize()
     return eig.cpu().numpy(), st.cpu().numpy()
@@ -79,3 +84,20 @@ def test_block_diagonal_already_tridiagonal():
     got, _ = gpu_eigvalsh(a[None])
     ref = np.linalg.eigvalsh(a)
     assert np.max(np.abs(got[0] - ref)) <= 1e-10 * (ref.max() - ref.min())
+
+
+@pytest.mark.parametrize("n,batch", [(40, 3), (200, 3), (320, 2)])
+def test_random_generalized(n, batch):
+    """A x = lambda B x with B Hermitian positive definite (zhegv, spectrum.py:106-108): the shared / global
+    kernels below n = 160, the Cholesky + banded two-stage path above."""
+    import scipy.linalg as sl
+
+    rng = np.random.default_rng(7 * n)
+    a = rand_herm(rng, n, batch)
+    g = rng.standard_normal((batch, n, n)) + 1j * rng.standard_normal((batch, n, n))
+    b = np.einsum("bij,bkj->bik", g, g.conj()) / n + np.eye(n)
+    got, st = gpu_eigvalsh(a, b)
+    assert (st == 0).all()
+    for m in range(batch):
+        ref = sl.eigh(a[m], b[m], eigvals_only=True)
+        assert np.max(np.abs(got[m] - ref)) <= 1e-10 * (ref.max() - ref.min())

@@ -283,3 +283,41 @@ def test_rank_update_variants(nu, q, opts):
 def test_c3_table_her2k_3m_option():
     """HX_HERK_3M=1: the 3M complex product in the Hermitian tier's her2k (1 CTA / SM) against zheevd."""
     check_batch("table", 8, 2, 0.05, 3, 2026, (0, 2), opts={"HX_HERK_3M": 1})
+
+
+# ---- Gram path (G = C^T C, symmetric two-stage reduction) of the real IDOS-only batches ---------------------
+@pytest.mark.parametrize("nu,q,count", [(16, 2, 8), (32, 1, 2), (12, 1, 6), (10, 2, 6), (20, 1, 3), (8, 2, 12)])
+def test_gram_path_vs_svd_path_and_oracle(nu, q, count):
+    """The IDOS of the Gram path (HX_GRAM=1: real batches whose zones avoid lambda = 0; off by default) equals the
+    SVD path's (HX_GRAM=0) to rounding and the oracle (zhegv) within the north-star tolerance."""
+    _, om, sc, cell, kp = _setup("graphene", nu, q)
+    step = (HI_G - LO_G) / (NPTS - 1)
+    words = sample_masks(sc.nunits, 0.05, 77, 2, 0, count)
+    with _lib.options(HX_GRAM=1):
+        gram, _, st1 = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
+    with _lib.options(HX_GRAM=0):
+        svd, _, st0 = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
+    assert (st1 == 0).all() and (st0 == 0).all()
+    np.testing.assert_allclose(gram, svd, rtol=0, atol=1e-11)
+    ocell = O.make_cell(om, nu)
+    for m in (0, count - 1):
+        ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
+        rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), LO_G, HI_G, NPTS, 0.01, ocell.area)
+        np.testing.assert_allclose(gram[m], rc, rtol=0, atol=IDOS_TOL)
+
+
+def test_gram_path_high_vacancy_and_empty():
+    """Many vacancies (zero modes, nA != nB) and an all-vacant mask through the Gram path."""
+    _, om, sc, cell, kp = _setup("graphene", 16, 2)
+    words = sample_masks(sc.nunits, 0.35, 5, 1, 0, 4)
+    words[3] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    step = (HI_G - LO_G) / (NPTS - 1)
+    with _lib.options(HX_GRAM=1):
+        gram, _, st = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
+    assert (st[:3] == 0).all() and (st[3] == _lib.HX_ST_EMPTY).all()
+    assert np.all(gram[3] == 0.0)
+    ocell = O.make_cell(om, 16)
+    for m in range(3):
+        ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
+        rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), LO_G, HI_G, NPTS, 0.01, ocell.area)
+        np.testing.assert_allclose(gram[m], rc, rtol=0, atol=IDOS_TOL)
