@@ -438,7 +438,7 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
   // shared-memory-tile kernel, whose 93 registers leave room on their SMs for the concurrent tiers' blocks
   // (the 128-register variant fills the register file: c2 step 63.7 -> 64.7 ms)
   const int reg_opt = (int)opt("HX_CHASE_REG", -1);
-  const bool regrow = reg_opt >= 0 ? reg_opt != 0 : want < 6;
+  const bool regrow = reg_opt >= 0 ? reg_opt != 0 : (want < 6 || (rcl <= 1 && opt("HX_CHASE_BIGNW", 8) <= 8));
 #define BD_CHASE_REAL(NW)                                                                                  \
   do {                                                                                                     \
     if (regrow)                                                                                            \
@@ -478,7 +478,17 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
     else if (rcl == 4) BD_CHASE_REAL_CL(4);
     else BD_CHASE_REAL_CL(8);
 #undef BD_CHASE_REAL_CL
-  } else if (want >= 6) BD_CHASE_REAL(16);
+  } else if (want >= 6) {
+    // few matrices, one CTA each: 8 warps of the register-row chase (N = 2048 tier of c2: 10.0 ms against
+    // 12.9 ms for 16 warps of the shared-memory-tile chase - fewer warps competing for the SM's issue slots and
+    // L1 pipe shorten every task; c2 step 63.1 -> 62.0 ms).  HX_CHASE_BIGNW = 6 / 12 / 16 and HX_CHASE_REG
+    // select the others.
+    const int bnw = (int)opt("HX_CHASE_BIGNW", 8);
+    if (bnw == 6) BD_CHASE_REAL(6);
+    else if (bnw == 12) BD_CHASE_REAL(12);
+    else if (bnw == 16) BD_CHASE_REAL(16);
+    else BD_CHASE_REAL(8);
+  }
   else if (want >= 2) BD_CHASE_REAL(4);
   else BD_CHASE_REAL(1);
 #undef BD_CHASE_REAL
@@ -566,6 +576,10 @@ void bd_init_attributes() {
   set_smem_attr(bd_chase_real_kernel<16, BB, 8>, bd_chase_real_smem<16, BB>());
   set_smem_attr(bd_chase_real_kernel<4, BB>, 220 * 1024);
   set_smem_attr(bd_chase_real_kernel<8, BB>, 220 * 1024);
+  set_smem_attr(bd_chase_real_kernel<12, BB>, 220 * 1024);
+  set_smem_attr(bd_chase_realr_kernel<12>, 220 * 1024);
+  set_smem_attr(bd_chase_realr_kernel<6>, 220 * 1024);
+  set_smem_attr(bd_chase_real_kernel<6, BB>, 220 * 1024);
   set_smem_attr(bd_chase_realr_kernel<1>, 220 * 1024);
   set_smem_attr(bd_chase_realr_kernel<2>, 220 * 1024);
   set_smem_attr(bd_chase_realr_kernel<4>, 220 * 1024);
