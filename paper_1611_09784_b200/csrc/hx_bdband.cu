@@ -114,10 +114,14 @@ static void launch_rank_update(double2* ws, const SlabGeom& G, int mr0, int mc0,
                                size_t w_off, int64_t cnt, cudaStream_t st) {
   const int tn = opt("HX_RU_TN", 64) == 32 ? 32 : 64;
   const unsigned gx = (unsigned)((m + RU_T - 1) / RU_T);
-  if (tn == 64)
-    rank_update_kernel<64, RE><<<dim3(gx, (unsigned)((n + 63) / 64), (unsigned)cnt), 256, ru_smem<64>(), st>>>(
-        ws, G, mr0, mc0, m, n, u_off, w_off);
-  else
+  if (tn == 64) {
+    if (!RE && opt("HX_RU_3M", 0) != 0)
+      rank_update_kernel<64, false, true><<<dim3(gx, (unsigned)((n + 63) / 64), (unsigned)cnt), 256, ru_smem<64>(), st>>>(
+          ws, G, mr0, mc0, m, n, u_off, w_off);
+    else
+      rank_update_kernel<64, RE><<<dim3(gx, (unsigned)((n + 63) / 64), (unsigned)cnt), 256, ru_smem<64>(), st>>>(
+          ws, G, mr0, mc0, m, n, u_off, w_off);
+  } else
     rank_update_kernel<32, RE><<<dim3(gx, (unsigned)((n + 31) / 32), (unsigned)cnt), 128, ru_smem<32>(), st>>>(
         ws, G, mr0, mc0, m, n, u_off, w_off);
 }
@@ -553,6 +557,7 @@ void bd_init_attributes() {
   set_smem_attr(rank_update_kernel<64>, (int)ru_smem<64>());
   set_smem_attr(rank_update_kernel<32>, (int)ru_smem<32>());
   set_smem_attr(rank_update_kernel<64, true>, (int)ru_smem<64>());
+  set_smem_attr(rank_update_kernel<64, false, true>, (int)ru_smem<64>());
   set_smem_attr(rank_update_kernel<32, true>, (int)ru_smem<32>());
   set_smem_attr(xv_kernel<0, false, true>, (int)XV_SMEM);
   set_smem_attr(xv_kernel<1, false, true>, (int)XV_SMEM);

@@ -278,10 +278,14 @@ constexpr int RU_T = 64, RU_LD = GBW + 4;
 constexpr size_t RU_SMEM = (size_t)2 * RU_T * RU_LD * sizeof(double2);
 
 // TN = 64: 8 warps (4 x 2) per 64 x 64 tile, 2 CTAs/SM; TN = 32: 4 warps per 64 x 32 tile, 4 CTAs/SM.
-template <int TN, bool RE = false>
-__global__ void __launch_bounds__(2 * TN * 2, TN == 64 ? 2 : 4) rank_update_kernel(double2* ws, SlabGeom g, int mr0,
-                                                                                  int mc0, int m, int n, size_t u_off,
-                                                                                  size_t w_off) {
+// M3: the 3M complex product (CTile3) at one CTA per SM (its third accumulator does not fit the 128 registers of
+// two CTAs per SM); HX_RU_3M selects it.
+template <int TN, bool RE = false, bool M3 = false>
+__global__ void __launch_bounds__(2 * TN * 2, M3 ? 1 : (TN == 64 ? 2 : 4)) rank_update_kernel(double2* ws, SlabGeom g,
+                                                                                            int mr0, int mc0, int m,
+                                                                                            int n, size_t u_off,
+                                                                                            size_t w_off) {
+  using Tile = std::conditional_t<M3 && !RE, CTile3, CTile>;
   constexpr int NT = 4 * TN;  // threads: 4 row warps x TN/32 column warps
   extern __shared__ __align__(16) double2 ru_sm[];
   double2* Us = ru_sm;                // [RU_T][RU_LD]
@@ -307,7 +311,7 @@ __global__ void __launch_bounds__(2 * TN * 2, TN == 64 ? 2 : 4) rank_update_kern
     cp_async16_zfill(Ws + r * RU_LD + k, W + (okw ? J0 + r + (size_t)k * ld : 0), okw);
   }
   cp_async_commit();
-  CTile acc[2][4];
+  Tile acc[2][4];
 #pragma unroll
   for (int rt = 0; rt < 2; ++rt)
 #pragma unroll

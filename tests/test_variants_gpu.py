@@ -122,9 +122,10 @@ def test_shared_memory_tiers_switches(nu, q, opts):
 
 
 # ---- complex bipartite banded tier (non-TRIM k, N > 160) ------------------------------------------------------
+@pytest.mark.parametrize("opts", [{}, {"HX_RU_3M": 1}])
 @pytest.mark.parametrize("nu,q", [(10, 3), (11, 4), (12, 3)])
-def test_complex_bipartite_banded_tier(nu, q):
-    check_batch("graphene", nu, q, 0.05, 3, 21, (0, 2))
+def test_complex_bipartite_banded_tier(nu, q, opts):
+    check_batch("graphene", nu, q, 0.05, 3, 21, (0, 2), opts=opts)
 
 
 @pytest.mark.parametrize("nu", [16, 32])
