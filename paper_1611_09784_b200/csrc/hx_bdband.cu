@@ -452,8 +452,8 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
       bd_chase_real_kernel<NW, BB><<<(unsigned)cnt, NW * 32, smem_of(bd_chase_real_smem<NW, BB>()), st>>>( \
           ws2, a1, L.band_off, a3, S, dims);                                                               \
   } while (0)
-  if (want >= 6 && rnw > 0) BD_CHASE_REAL(16);
-  else if (rnw == 1) BD_CHASE_REAL(1);
+  // HX_CHASE_RNW forces the warps per matrix for every batch size (tests run each variant on a few matrices)
+  if (rnw == 1) BD_CHASE_REAL(1);
   else if (rnw == 2) BD_CHASE_REAL(2);
   else if (rnw == 4) BD_CHASE_REAL(4);
   else if (rnw == 8) BD_CHASE_REAL(8);
