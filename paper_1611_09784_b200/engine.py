@@ -569,7 +569,10 @@ class Engine:
             for k in np.unique(which_u):
                 curves, per_job = lst[k][1].result()
                 rows = np.flatnonzero((rsrc >= 0) & (which_r == k))
-                out[rows] = curves[rsrc[rows] - lst[k][0]]
+                if len(rows) == R:  # every row from this piece: one gather straight into the output
+                    np.take(curves, rsrc - lst[k][0], axis=0, out=out)
+                else:
+                    out[rows] = curves[rsrc[rows] - lst[k][0]]
                 opj[rows] = per_job
                 pj_u[got[which_u == k]] = per_job
         cached_r = np.flatnonzero(rsrc < 0)
@@ -706,7 +709,7 @@ class Engine:
             nsamples_all = nsamples
         self.io_bytes[0] += full.nbytes + (0 if quarters is None else quarters.nbytes)
         self.io_bytes[1] += (0 if terms is None else full.nbytes) + 2 * mean.numel() * 8
-        terms = full.copy() if terms is None else terms.cpu().numpy()
+        terms = full if terms is None else terms.cpu().numpy()  # no CV: terms is full itself (runner.py:297)
         cv = None
         if quarters is not None:
             # cv exactly as the reference forms it: ((q1 + q2) + q3 + q4) * 0.25
