@@ -355,6 +355,233 @@ static __device__ void bidiag_tgk_warp(double2* M, int lm, int rows, int cols, d
 }
 
 // ------------------------------------------------------------------------------------------------
+// Register-resident Golub-Kahan for complex S <= 64 on 256 threads (hx_kernels.cuh BIDIAG_REG_THREADS).  The shared-memory
+// CTA variant above reads every active element of M twice and writes it once per reflector from shared
+// memory - ~50 bytes per complex FMA pair, which makes it shared-memory-bandwidth bound at ~4 TF/s.  Here
+// the matrix lives in registers: thread (a, b) = (lane & 15, 2 warp + (lane >> 4)) owns the 4 x 4 complex
+// elements M[a + 16 i][b + 16 k] (cyclic, so the active trailing block stays spread over every thread) and
+// shared memory only carries the reflectors and the reductions:
+//   left  (column j): the 16 owners of column j (one half-warp) build u, one barrier; the column dots
+//         reduce over the 16 lanes a of a half-warp (reduce-scatter by shuffles + a shared-memory
+//         all-gather inside the half-warp), no barrier;
+//   right (row j): the owners of row j publish it with their norm partials, one barrier; every thread
+//         builds the same reflector; the row dots reduce over b (xor-16 shuffle, then 8 warps through
+//         shared memory: two barriers).
+// Scratch (doubles): BIDIAG_REG_SCRATCH.  Same TGK output as bidiag_tgk.
+constexpr int BIDIAG_REG_SCRATCH = 128 + 2 + 128 + 128 + 8 + 1024 + 128;
+
+struct GkRegScratch {
+  double2* ubuf;    // 64: left reflector u
+  double* stau;     // left tau
+  double* sv;       // 16 x 8: tau u^H M per column class
+  double2* rowbuf;  // 64: row j after the left update
+  double* nred;     // 8: row-norm partials per warp
+  double* wred;     // 8 warps x 8 x 16: row-dot partials
+  double* wv;       // 4 x 16 double2: tau M u per row
+};
+
+// Steps j in [16 T, min(16 T + 16, cols)): rows and columns below 16 T are finished, so the register blocks
+// i < T and k < T are skipped statically; the partial block T is masked through u / s / w.
+template <int T>
+static __device__ __forceinline__ void gk_reg_phase(double2 (&m)[4][4], int rows, int cols, double* e2,
+                                                    const GkRegScratch& sc) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int a = lane & 15, hb = lane >> 4, b = 2 * warp + hb;
+  const unsigned FULL = 0xffffffffu;
+  const int jend = min(16 * T + 16, cols);
+  for (int j = 16 * T; j < jend; ++j) {
+    const int jl = j & 15;
+    // ---------------- left reflector: column j (owners: b == jl, one half-warp of warp jl >> 1)
+    if (warp == (jl >> 1)) {
+      double part = 0.0;
+#pragma unroll
+      for (int i = T; i < 4; ++i)
+        if (i > T || a >= jl) part = fma(m[i][T].x, m[i][T].x, fma(m[i][T].y, m[i][T].y, part));
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) part += __shfl_xor_sync(FULL, part, o);
+      const int src = 16 * (j & 1) + jl;
+      const double2 alpha = make_double2(__shfl_sync(FULL, m[T][T].x, src), __shfl_sync(FULL, m[T][T].y, src));
+      const QuickReflector h = quick_reflector(alpha, part);
+      if (hb == (j & 1)) {
+#pragma unroll
+        for (int i = T; i < 4; ++i) {
+          const int r = a + 16 * i;
+          sc.ubuf[r] = r < j ? make_double2(0.0, 0.0) : (r == j ? make_double2(1.0, 0.0) : cmul(m[i][T], h.scale));
+        }
+        if (lane == src) {
+          *sc.stau = h.tau;
+          e2[2 * j] = part;
+        }
+      }
+    }
+    __syncthreads();  // A: u, tau
+    {
+      const double tau = *sc.stau;
+      double2 uu[4];
+#pragma unroll
+      for (int i = T; i < 4; ++i) uu[i] = sc.ubuf[a + 16 * i];
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double2 acc = make_double2(0.0, 0.0);
+        if (k >= T)
+#pragma unroll
+          for (int i = T; i < 4; ++i) {
+            const double2 x = m[i][k];
+            acc.x = fma(uu[i].x, x.x, fma(uu[i].y, x.y, acc.x));
+            acc.y = fma(uu[i].x, x.y, fma(-uu[i].y, x.x, acc.y));
+          }
+        v[2 * k] = acc.x;
+        v[2 * k + 1] = acc.y;
+      }
+      // reduce-scatter over the 16 lanes a: the lane ends with the sum of value p = (a >> 1) & 7
+      double w4[4], w2[2];
+      const bool b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        w4[t] = t + 4 < 2 * T ? 0.0  // values of skipped blocks: zero on both sides
+                              : (b3 ? v[t + 4] : v[t]) + __shfl_xor_sync(FULL, b3 ? v[t] : v[t + 4], 8);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) w2[t] = (b2 ? w4[t + 2] : w4[t]) + __shfl_xor_sync(FULL, b2 ? w4[t] : w4[t + 2], 4);
+      double w1 = (b1 ? w2[1] : w2[0]) + __shfl_xor_sync(FULL, b1 ? w2[0] : w2[1], 2);
+      w1 += __shfl_xor_sync(FULL, w1, 1);
+      if (!(a & 1)) {
+        const int p = a >> 1, c = b + 16 * (p >> 1);
+        sc.sv[b * 8 + p] = c > j ? tau * w1 : 0.0;
+      }
+      __syncwarp();
+      const double2* s2 = reinterpret_cast<const double2*>(sc.sv + b * 8);
+#pragma unroll
+      for (int k = T; k < 4; ++k) {
+        const double2 s = s2[k];
+#pragma unroll
+        for (int i = T; i < 4; ++i) {
+          double2 x = m[i][k];
+          x.x = fma(-uu[i].x, s.x, fma(uu[i].y, s.y, x.x));
+          x.y = fma(-uu[i].x, s.y, fma(-uu[i].y, s.x, x.y));
+          m[i][k] = x;
+        }
+      }
+    }
+    if (j + 1 >= cols) break;
+    // owners of row j (a == jl) publish its columns > j and their squared norm
+    {
+      double np = 0.0;
+      if (a == jl) {
+#pragma unroll
+        for (int k = T; k < 4; ++k) {
+          const int c = b + 16 * k;
+          const double2 x = c > j ? m[T][k] : make_double2(0.0, 0.0);
+          sc.rowbuf[c] = x;
+          np = fma(x.x, x.x, fma(x.y, x.y, np));
+        }
+      }
+      np += __shfl_xor_sync(FULL, np, 16);
+      if (lane == jl) sc.nred[warp] = np;
+    }
+    __syncthreads();  // B: row j, norm partials
+    // ---------------- right reflector: row j, columns j+1.. (every thread builds the same one)
+    {
+      const double2* nr2 = reinterpret_cast<const double2*>(sc.nred);
+      double sig2 = 0.0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const double2 x = nr2[w];
+        sig2 += x.x;
+        sig2 += x.y;
+      }
+      const double2 a0 = sc.rowbuf[j + 1];
+      const QuickReflector h = quick_reflector(make_double2(a0.x, -a0.y), sig2);
+      if (tid == 0) e2[2 * j + 1] = sig2;
+      double2 uc[4];
+#pragma unroll
+      for (int k = T; k < 4; ++k) {
+        const int c = b + 16 * k;
+        const double2 x = sc.rowbuf[c];
+        uc[k] = c == j + 1 ? make_double2(1.0, 0.0) : cmul(make_double2(x.x, -x.y), h.scale);
+      }
+      double v[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double2 acc = make_double2(0.0, 0.0);
+        if (i >= T)
+#pragma unroll
+          for (int k = T; k < 4; ++k) {
+            const double2 x = m[i][k];
+            acc.x = fma(x.x, uc[k].x, fma(-x.y, uc[k].y, acc.x));
+            acc.y = fma(x.x, uc[k].y, fma(x.y, uc[k].x, acc.y));
+          }
+        v[2 * i] = acc.x;
+        v[2 * i + 1] = acc.y;
+      }
+      // the two column classes of the warp (xor 16), then the 8 warps through shared memory
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const double r = (hb ? v[t + 4] : v[t]) + __shfl_xor_sync(FULL, hb ? v[t] : v[t + 4], 16);
+        sc.wred[(warp * 8 + hb * 4 + t) * 16 + a] = r;
+      }
+      __syncthreads();  // C: row-dot partials
+      if (tid < 128) {
+        const int ar = tid & 15, p = tid >> 4;
+        double sum = 0.0;
+        if ((p >> 1) >= T) {
+#pragma unroll
+          for (int w = 0; w < 8; ++w) sum += sc.wred[(w * 8 + p) * 16 + ar];
+        }
+        const int r = ar + 16 * (p >> 1);
+        sc.wv[((p >> 1) * 16 + ar) * 2 + (p & 1)] = r > j ? h.tau * sum : 0.0;
+      }
+      __syncthreads();  // D: tau M u
+      const double2* wv2 = reinterpret_cast<const double2*>(sc.wv);
+#pragma unroll
+      for (int i = T; i < 4; ++i) {
+        const double2 w = wv2[i * 16 + a];
+#pragma unroll
+        for (int k = T; k < 4; ++k) {
+          double2 x = m[i][k];
+          // x -= w conj(u_c)
+          x.x = fma(-w.x, uc[k].x, fma(-w.y, uc[k].y, x.x));
+          x.y = fma(-w.y, uc[k].x, fma(w.x, uc[k].y, x.y));
+          m[i][k] = x;
+        }
+      }
+    }
+  }
+}
+
+static __device__ void bidiag_tgk_reg(const double2* Ms, int lm, int rows, int cols, double* diag, double* e2,
+                                      double* scratch) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int a = lane & 15, b = 2 * warp + (lane >> 4);
+  GkRegScratch sc;
+  sc.ubuf = reinterpret_cast<double2*>(scratch);
+  sc.stau = scratch + 128;
+  sc.sv = scratch + 130;
+  sc.rowbuf = reinterpret_cast<double2*>(scratch + 258);
+  sc.nred = scratch + 386;
+  sc.wred = scratch + 394;
+  sc.wv = scratch + 1418;
+  const int d = rows + cols;
+  for (int i = tid; i < d; i += blockDim.x) {
+    diag[i] = 0.0;
+    e2[i] = 0.0;
+  }
+  double2 m[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = a + 16 * i, c = b + 16 * k;
+      m[i][k] = (r < rows && c < cols) ? Ms[r + (size_t)c * lm] : make_double2(0.0, 0.0);
+    }
+  gk_reg_phase<0>(m, rows, cols, e2, sc);
+  if (cols > 16) gk_reg_phase<1>(m, rows, cols, e2, sc);
+  if (cols > 32) gk_reg_phase<2>(m, rows, cols, e2, sc);
+  if (cols > 48) gk_reg_phase<3>(m, rows, cols, e2, sc);
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------------------------------------
 // Real variants (periodic gauge at a time-reversal-invariant k: C is exactly real, hx_capi k_is_real):
 // the same schedules on doubles - a quarter of the FMAs and half the shared-memory traffic.
 // Leading dimensions: CTA variant 8 (mod 16) doubles (the half-warp's two columns x 8 rows hit distinct

@@ -122,6 +122,7 @@ struct hx_ctx {
   int bidiag_warp_max_s = 32;            // shared-memory bidiagonalisation: one warp per matrix up to this S
   int bidiag_threads = 256;              // ... and a CTA of this size above it
   int bidiag_real_warp_max_s = 64;       // real (time-reversal-invariant) k-points: one warp per matrix up to this S
+  bool bidiag_reg = true;                // register-resident reduction for complex S in (warp max, 64]
   bool bidiag_real = true;               // real Golub-Kahan for those k-points (HX_BIDIAG_REAL=0 disables)
   bool use_bipartite = true;            // graphene: singular values of the A-B block (HX_NO_BIPARTITE=1 disables)
   size_t ws_budget_default = ws_budget;
@@ -135,6 +136,7 @@ void refresh_opts(hx_ctx* ctx) {
   ctx->bidiag_warp_max_s = (int)hx::opt("HX_BIDIAG_WARP_MAX_S", 32);
   ctx->bidiag_threads = (int)hx::opt("HX_BIDIAG_THREADS", 256);
   ctx->bidiag_real = hx::opt("HX_BIDIAG_REAL", 1) != 0;
+  ctx->bidiag_reg = hx::opt("HX_BIDIAG_REG", 1) != 0;
   ctx->bidiag_real_warp_max_s = (int)hx::opt("HX_BIDIAG_REAL_WARP_MAX_S", 64);
   // experiments: workspace chunk budget in MB (L2-resident chunks)
   const long wb = hx::opt("HX_WS_BUDGET_MB", 0);
@@ -297,6 +299,7 @@ int hx_ctx_create_priority(int32_t device, int32_t priority, hx_ctx** out) {
   size_t freeb = 0, total = 0;
   cudaMemGetInfo(&freeb, &total);
   hx::set_smem_attr(hx::small_bidiag_kernel, 200 * 1024);
+  hx::set_smem_attr(hx::small_bidiag_reg_kernel, (int)hx::small_bidiag_reg_smem(128, 64));
   ctx->ws_budget = std::min(ctx->ws_budget, freeb / 3);
   ctx->ws_budget_default = ctx->ws_budget;
   refresh_opts(ctx);
@@ -527,15 +530,21 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
         // matrices per SM), a CTA beyond
         const int nkc = (int)klist_c.size(), nkr = (int)klist_r.size();
         const int64_t nm = cnt / nk;  // whole masks in this chunk
-        if (nkr == 0) {
-          hx::small_bidiag_kernel<<<(unsigned)cnt, c.nsub <= ctx->bidiag_warp_max_s ? 32 : ctx->bidiag_threads,
-                                    hx::small_bidiag_smem(N, c.nsub), st>>>(c, kp, nk, mk0, tri, dims, status + m0,
-                                                                            nullptr, nk, 0);
-        } else {
-          if (nkc > 0)
-            hx::small_bidiag_kernel<<<(unsigned)(nm * nkc), c.nsub <= ctx->bidiag_warp_max_s ? 32 : ctx->bidiag_threads,
+        // complex k-points: one warp per matrix up to S = 32, the register-resident 256-thread reduction up
+        // to S = 64 (HX_BIDIAG_REG=0: the shared-memory CTA), the shared-memory CTA beyond
+        auto launch_complex = [&](unsigned grid, const int* kl, int nks) {
+          if (c.nsub > ctx->bidiag_warp_max_s && c.nsub <= 64 && ctx->bidiag_reg)
+            hx::small_bidiag_reg_kernel<<<grid, hx::BIDIAG_REG_THREADS, hx::small_bidiag_reg_smem(N, c.nsub), st>>>(
+                c, kp, nk, mk0, tri, dims, status + m0, kl, nks);
+          else
+            hx::small_bidiag_kernel<<<grid, c.nsub <= ctx->bidiag_warp_max_s ? 32 : ctx->bidiag_threads,
                                       hx::small_bidiag_smem(N, c.nsub), st>>>(c, kp, nk, mk0, tri, dims, status + m0,
-                                                                              d_klist_c, nkc, 0);
+                                                                              kl, nks, 0);
+        };
+        if (nkr == 0) {
+          launch_complex((unsigned)cnt, nullptr, nk);
+        } else {
+          if (nkc > 0) launch_complex((unsigned)(nm * nkc), d_klist_c, nkc);
           // real k-points: one warp per matrix up to S = 64 (two columns / rows per lane)
           const bool rw = c.nsub <= ctx->bidiag_real_warp_max_s;
           hx::small_bidiag_kernel<<<(unsigned)(nm * nkr), rw ? 32 : ctx->bidiag_threads,

@@ -105,6 +105,49 @@ __global__ void __launch_bounds__(256) small_bidiag_kernel(CellDev c, const doub
   else bidiag_tgk(M, lm, rows, cols, diag, e2, u, s, red);
 }
 
+// Complex k-points with S <= 64: the matrix in registers of 256 threads (bidiag_tgk_reg); the assembly
+// still goes through shared memory.
+__global__ void __launch_bounds__(BIDIAG_REG_THREADS, 2)
+    small_bidiag_reg_kernel(CellDev c, const double2* __restrict__ kpts, int nk, const uint64_t* __restrict__ masks,
+                            double* tri, int* dims, int* status, const int* __restrict__ klist, int nks) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int N = c.N, S = c.nsub;
+  int64_t mk, mat;
+  int kk;
+  if (klist) {
+    mk = blockIdx.x / nks;
+    kk = klist[blockIdx.x - mk * nks];
+    mat = mk * nk + kk;
+  } else {
+    mat = blockIdx.x;
+    mk = mat / nk;
+    kk = (int)(mat - mk * nk);
+  }
+  const int lm = bidiag_ld(S);
+  double2* M = reinterpret_cast<double2*>(smem_raw);
+  double* scratch = reinterpret_cast<double*>(M + (size_t)lm * S);
+  int* idx_a = reinterpret_cast<int*>(scratch + BIDIAG_REG_SCRATCH);
+  int* idx_b = idx_a + N;
+  int* cnt = idx_b + N;
+  double* diag = tri + mat * 2 * N;
+  double* e2 = diag + N;
+  const int2 nn = block_compact_bipartite(c, masks + mk * c.words, idx_a, idx_b, cnt);
+  const int d = nn.x + nn.y;
+  if (threadIdx.x == 0) {
+    dims[mat] = d;
+    status[mat] = d == 0 ? 3 : 0;
+  }
+  if (d == 0) return;
+  const bool transpose = nn.x < nn.y;
+  const int rows = transpose ? nn.y : nn.x, cols = transpose ? nn.x : nn.y;
+  assemble_bipartite(c, idx_a, idx_b, kpts[kk], M, lm, rows, cols, transpose);
+  bidiag_tgk_reg(M, lm, rows, cols, diag, e2, scratch);
+}
+
+size_t small_bidiag_reg_smem(int N, int S) {
+  return ((size_t)bidiag_ld(S) * S) * 16 + BIDIAG_REG_SCRATCH * 8 + (size_t)N * 8 + 2 * ((N + 31) / 32) * 4 + 16;
+}
+
 size_t small_bidiag_smem(int N, int S) {
   return ((size_t)bidiag_ld(S) * S + 2 * (S + 1)) * 16 + 128 * 8 + (size_t)N * 8 + 2 * ((N + 31) / 32) * 4 + 16;
 }

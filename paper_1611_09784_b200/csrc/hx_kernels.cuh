@@ -31,6 +31,11 @@ __global__ void small_bidiag_kernel(CellDev c, const double2* kpts, int nk, cons
                                     int* dims, int* status, const int* klist, int nks, int real);
 size_t small_bidiag_smem(int N, int S);
 size_t small_bidiag_smem_real(int N, int S, bool warp);
+// complex k-points, S <= 64: matrix in registers of 256 threads (hx_bidiag.cuh bidiag_tgk_reg)
+constexpr int BIDIAG_REG_THREADS = 256;
+__global__ void small_bidiag_reg_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, double* tri,
+                                        int* dims, int* status, const int* klist, int nks);
+size_t small_bidiag_reg_smem(int N, int S);
 
 __global__ void global_tridiag_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, int64_t mat0,
                                       unsigned char* ws, size_t ws_stride, double* tri, int* dims, int* status);

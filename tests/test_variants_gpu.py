@@ -113,12 +113,21 @@ def test_real_path_switches(nu, q, opts):
     check_batch("graphene", nu, q, 0.1, 4, 13, (0, 3), opts=opts)
 
 
-@pytest.mark.parametrize("opts", [{}, {"HX_BIDIAG_REAL": 0}, {"HX_NO_REAL": 1}, {"HX_NO_BIPARTITE": 1}])
+@pytest.mark.parametrize("opts", [{}, {"HX_BIDIAG_REAL": 0}, {"HX_NO_REAL": 1}, {"HX_NO_BIPARTITE": 1},
+                                  {"HX_BIDIAG_REG": 0}])
 @pytest.mark.parametrize("nu,q", [(4, 8), (8, 4), (8, 2)])
 def test_shared_memory_tiers_switches(nu, q, opts):
     """The shared-memory tiers of c1/c2 (N = 32, 128): complex warp / CTA Golub-Kahan, real Golub-Kahan at the
     TRIM k-points, and the Hermitian (non-bipartite) tier with HX_NO_BIPARTITE."""
     check_batch("graphene", nu, q, 0.05, 40, 17, (0, 19, 39), opts=opts)
+
+
+@pytest.mark.parametrize("reg", [1, 0])
+@pytest.mark.parametrize("nu,q,conc", [(5, 3, 0.05), (6, 3, 0.2), (7, 5, 0.1), (8, 3, 0.3)])
+def test_register_golub_kahan(nu, q, conc, reg):
+    """Complex k-points with 32 < S <= 64 (N = 50..128): the register-resident 256-thread Golub-Kahan
+    (HX_BIDIAG_REG=1, default) and the shared-memory CTA, padded / rectangular blocks at high vacancy counts."""
+    check_batch("graphene", nu, q, conc, 24, 23, (0, 11, 23), opts={"HX_BIDIAG_REG": reg})
 
 
 # ---- complex bipartite banded tier (non-TRIM k, N > 160) ------------------------------------------------------
