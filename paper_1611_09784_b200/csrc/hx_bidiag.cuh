@@ -581,6 +581,188 @@ static __device__ void bidiag_tgk_reg(const double2* Ms, int lm, int rows, int c
   __syncthreads();
 }
 
+// Real register-resident variant (TRIM k-points, S <= 64): the same schedule on doubles, 4 x 4 per thread.
+// Scratch (doubles): BIDIAG_REG_SCRATCH_REAL.
+constexpr int BIDIAG_REG_SCRATCH_REAL = 64 + 2 + 64 + 64 + 8 + 512 + 64;
+
+struct GkRegScratchReal {
+  double* ubuf;    // 64
+  double* stau;
+  double* sv;      // 16 x 4
+  double* rowbuf;  // 64
+  double* nred;    // 8
+  double* wred;    // 8 warps x 4 x 16
+  double* wv;      // 4 x 16
+};
+
+template <int T>
+static __device__ __forceinline__ void gk_reg_phase_real(double (&m)[4][4], int rows, int cols, double* e2,
+                                                         const GkRegScratchReal& sc) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int a = lane & 15, hb = lane >> 4, b = 2 * warp + hb;
+  const unsigned FULL = 0xffffffffu;
+  const int jend = min(16 * T + 16, cols);
+  for (int j = 16 * T; j < jend; ++j) {
+    const int jl = j & 15;
+    if (warp == (jl >> 1)) {
+      double part = 0.0;
+#pragma unroll
+      for (int i = T; i < 4; ++i)
+        if (i > T || a >= jl) part = fma(m[i][T], m[i][T], part);
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) part += __shfl_xor_sync(FULL, part, o);
+      const int src = 16 * (j & 1) + jl;
+      const double alpha = __shfl_sync(FULL, m[T][T], src);
+      const QuickReflector h = quick_reflector(make_double2(alpha, 0.0), part);
+      if (hb == (j & 1)) {
+#pragma unroll
+        for (int i = T; i < 4; ++i) {
+          const int r = a + 16 * i;
+          sc.ubuf[r] = r < j ? 0.0 : (r == j ? 1.0 : m[i][T] * h.scale.x);
+        }
+        if (lane == src) {
+          *sc.stau = h.tau;
+          e2[2 * j] = part;
+        }
+      }
+    }
+    __syncthreads();  // A
+    {
+      const double tau = *sc.stau;
+      double uu[4];
+#pragma unroll
+      for (int i = T; i < 4; ++i) uu[i] = sc.ubuf[a + 16 * i];
+      double v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double acc = 0.0;
+        if (k >= T)
+#pragma unroll
+          for (int i = T; i < 4; ++i) acc = fma(uu[i], m[i][k], acc);
+        v[k] = acc;
+      }
+      // reduce-scatter over the 16 lanes a: the lane ends with the sum of value k = (a >> 2) & 3
+      const bool b3 = lane & 8, b2 = lane & 4;
+      double w2[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+        w2[t] = t + 2 < T ? 0.0 : (b3 ? v[t + 2] : v[t]) + __shfl_xor_sync(FULL, b3 ? v[t] : v[t + 2], 8);
+      double w1 = (b2 ? w2[1] : w2[0]) + __shfl_xor_sync(FULL, b2 ? w2[0] : w2[1], 4);
+      w1 += __shfl_xor_sync(FULL, w1, 2);
+      w1 += __shfl_xor_sync(FULL, w1, 1);
+      if (!(a & 3)) {
+        const int p = a >> 2, c = b + 16 * p;
+        sc.sv[b * 4 + p] = c > j ? tau * w1 : 0.0;
+      }
+      __syncwarp();
+      const double2* s2 = reinterpret_cast<const double2*>(sc.sv + b * 4);
+      const double2 s01 = s2[0], s23 = s2[1];
+      const double s[4] = {s01.x, s01.y, s23.x, s23.y};
+#pragma unroll
+      for (int k = T; k < 4; ++k)
+#pragma unroll
+        for (int i = T; i < 4; ++i) m[i][k] = fma(-uu[i], s[k], m[i][k]);
+    }
+    if (j + 1 >= cols) break;
+    {
+      double np = 0.0;
+      if (a == jl) {
+#pragma unroll
+        for (int k = T; k < 4; ++k) {
+          const int c = b + 16 * k;
+          const double x = c > j ? m[T][k] : 0.0;
+          sc.rowbuf[c] = x;
+          np = fma(x, x, np);
+        }
+      }
+      np += __shfl_xor_sync(FULL, np, 16);
+      if (lane == jl) sc.nred[warp] = np;
+    }
+    __syncthreads();  // B
+    {
+      const double2* nr2 = reinterpret_cast<const double2*>(sc.nred);
+      double sig2 = 0.0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const double2 x = nr2[w];
+        sig2 += x.x;
+        sig2 += x.y;
+      }
+      const QuickReflector h = quick_reflector(make_double2(sc.rowbuf[j + 1], 0.0), sig2);
+      if (tid == 0) e2[2 * j + 1] = sig2;
+      double uc[4];
+#pragma unroll
+      for (int k = T; k < 4; ++k) {
+        const int c = b + 16 * k;
+        uc[k] = c == j + 1 ? 1.0 : sc.rowbuf[c] * h.scale.x;
+      }
+      double v[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        double acc = 0.0;
+        if (i >= T)
+#pragma unroll
+          for (int k = T; k < 4; ++k) acc = fma(m[i][k], uc[k], acc);
+        v[i] = acc;
+      }
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const double r = (hb ? v[t + 2] : v[t]) + __shfl_xor_sync(FULL, hb ? v[t] : v[t + 2], 16);
+        sc.wred[(warp * 4 + hb * 2 + t) * 16 + a] = r;
+      }
+      __syncthreads();  // C
+      if (tid < 64) {
+        const int ar = tid & 15, i = tid >> 4;
+        double sum = 0.0;
+        if (i >= T) {
+#pragma unroll
+          for (int w = 0; w < 8; ++w) sum += sc.wred[(w * 4 + i) * 16 + ar];
+        }
+        sc.wv[i * 16 + ar] = ar + 16 * i > j ? h.tau * sum : 0.0;
+      }
+      __syncthreads();  // D
+#pragma unroll
+      for (int i = T; i < 4; ++i) {
+        const double w = sc.wv[i * 16 + a];
+#pragma unroll
+        for (int k = T; k < 4; ++k) m[i][k] = fma(-w, uc[k], m[i][k]);
+      }
+    }
+  }
+}
+
+static __device__ void bidiag_tgk_reg_real(const double* Ms, int lm, int rows, int cols, double* diag, double* e2,
+                                           double* scratch) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int a = lane & 15, b = 2 * warp + (lane >> 4);
+  GkRegScratchReal sc;
+  sc.ubuf = scratch;
+  sc.stau = scratch + 64;
+  sc.sv = scratch + 66;
+  sc.rowbuf = scratch + 130;
+  sc.nred = scratch + 194;
+  sc.wred = scratch + 202;
+  sc.wv = scratch + 714;
+  const int d = rows + cols;
+  for (int i = tid; i < d; i += blockDim.x) {
+    diag[i] = 0.0;
+    e2[i] = 0.0;
+  }
+  double m[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int r = a + 16 * i, c = b + 16 * k;
+      m[i][k] = (r < rows && c < cols) ? Ms[r + (size_t)c * lm] : 0.0;
+    }
+  gk_reg_phase_real<0>(m, rows, cols, e2, sc);
+  if (cols > 16) gk_reg_phase_real<1>(m, rows, cols, e2, sc);
+  if (cols > 32) gk_reg_phase_real<2>(m, rows, cols, e2, sc);
+  if (cols > 48) gk_reg_phase_real<3>(m, rows, cols, e2, sc);
+  __syncthreads();
+}
+
 // ------------------------------------------------------------------------------------------------
 // Real variants (periodic gauge at a time-reversal-invariant k: C is exactly real, hx_capi k_is_real):
 // the same schedules on doubles - a quarter of the FMAs and half the shared-memory traffic.

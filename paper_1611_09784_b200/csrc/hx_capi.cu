@@ -300,6 +300,7 @@ int hx_ctx_create_priority(int32_t device, int32_t priority, hx_ctx** out) {
   cudaMemGetInfo(&freeb, &total);
   hx::set_smem_attr(hx::small_bidiag_kernel, 200 * 1024);
   hx::set_smem_attr(hx::small_bidiag_reg_kernel, (int)hx::small_bidiag_reg_smem(128, 64));
+  hx::set_smem_attr(hx::small_bidiag_reg_real_kernel, (int)hx::small_bidiag_reg_real_smem(128, 64));
   ctx->ws_budget = std::min(ctx->ws_budget, freeb / 3);
   ctx->ws_budget_default = ctx->ws_budget;
   refresh_opts(ctx);
@@ -545,11 +546,19 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
           launch_complex((unsigned)cnt, nullptr, nk);
         } else {
           if (nkc > 0) launch_complex((unsigned)(nm * nkc), d_klist_c, nkc);
-          // real k-points: one warp per matrix up to S = 64 (two columns / rows per lane)
-          const bool rw = c.nsub <= ctx->bidiag_real_warp_max_s;
-          hx::small_bidiag_kernel<<<(unsigned)(nm * nkr), rw ? 32 : ctx->bidiag_threads,
-                                    hx::small_bidiag_smem_real(N, c.nsub, rw), st>>>(c, kp, nk, mk0, tri, dims,
-                                                                                     status + m0, d_klist_r, nkr, 1);
+          // real k-points: one warp per matrix up to S = 32 (two columns / rows per lane), the
+          // register-resident 256-thread reduction up to S = 64 (HX_BIDIAG_REG=0: warps up to
+          // HX_BIDIAG_REAL_WARP_MAX_S)
+          if (c.nsub > 32 && c.nsub <= 64 && ctx->bidiag_reg) {
+            hx::small_bidiag_reg_real_kernel<<<(unsigned)(nm * nkr), hx::BIDIAG_REG_THREADS,
+                                               hx::small_bidiag_reg_real_smem(N, c.nsub), st>>>(
+                c, kp, nk, mk0, tri, dims, status + m0, d_klist_r, nkr);
+          } else {
+            const bool rw = c.nsub <= ctx->bidiag_real_warp_max_s;
+            hx::small_bidiag_kernel<<<(unsigned)(nm * nkr), rw ? 32 : ctx->bidiag_threads,
+                                      hx::small_bidiag_smem_real(N, c.nsub, rw), st>>>(c, kp, nk, mk0, tri, dims,
+                                                                                       status + m0, d_klist_r, nkr, 1);
+          }
           hx::count_launch();
         }
       } else {

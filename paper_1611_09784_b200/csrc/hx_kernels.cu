@@ -144,6 +144,42 @@ __global__ void __launch_bounds__(BIDIAG_REG_THREADS, 2)
   bidiag_tgk_reg(M, lm, rows, cols, diag, e2, scratch);
 }
 
+// Real k-points (periodic gauge at TRIM k) with S <= 64: bidiag_tgk_reg_real.
+__global__ void __launch_bounds__(BIDIAG_REG_THREADS, 3)
+    small_bidiag_reg_real_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
+                                 const uint64_t* __restrict__ masks, double* tri, int* dims, int* status,
+                                 const int* __restrict__ klist, int nks) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int N = c.N, S = c.nsub;
+  const int64_t mk = blockIdx.x / nks;
+  const int kk = klist[blockIdx.x - mk * nks];
+  const int64_t mat = mk * nk + kk;
+  const int lm = bidiag_ld_real(S);
+  double* Mr = reinterpret_cast<double*>(smem_raw);
+  double* scratch = Mr + (size_t)lm * S;
+  int* idx_a = reinterpret_cast<int*>(scratch + BIDIAG_REG_SCRATCH_REAL);
+  int* idx_b = idx_a + N;
+  int* cnt = idx_b + N;
+  double* diag = tri + mat * 2 * N;
+  double* e2 = diag + N;
+  const int2 nn = block_compact_bipartite(c, masks + mk * c.words, idx_a, idx_b, cnt);
+  const int d = nn.x + nn.y;
+  if (threadIdx.x == 0) {
+    dims[mat] = d;
+    status[mat] = d == 0 ? 3 : 0;
+  }
+  if (d == 0) return;
+  const bool transpose = nn.x < nn.y;
+  const int rows = transpose ? nn.y : nn.x, cols = transpose ? nn.x : nn.y;
+  assemble_bipartite(c, idx_a, idx_b, kpts[kk], nullptr, lm, rows, cols, transpose, true, Mr);
+  bidiag_tgk_reg_real(Mr, lm, rows, cols, diag, e2, scratch);
+}
+
+size_t small_bidiag_reg_real_smem(int N, int S) {
+  return ((size_t)bidiag_ld_real(S) * S) * 8 + BIDIAG_REG_SCRATCH_REAL * 8 + (size_t)N * 8 +
+         2 * ((N + 31) / 32) * 4 + 16;
+}
+
 size_t small_bidiag_reg_smem(int N, int S) {
   return ((size_t)bidiag_ld(S) * S) * 16 + BIDIAG_REG_SCRATCH * 8 + (size_t)N * 8 + 2 * ((N + 31) / 32) * 4 + 16;
 }

@@ -36,6 +36,10 @@ constexpr int BIDIAG_REG_THREADS = 256;
 __global__ void small_bidiag_reg_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, double* tri,
                                         int* dims, int* status, const int* klist, int nks);
 size_t small_bidiag_reg_smem(int N, int S);
+// real (TRIM) k-points from klist, S <= 64: matrix in registers of 256 threads (bidiag_tgk_reg_real)
+__global__ void small_bidiag_reg_real_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks,
+                                             double* tri, int* dims, int* status, const int* klist, int nks);
+size_t small_bidiag_reg_real_smem(int N, int S);
 
 __global__ void global_tridiag_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, int64_t mat0,
                                       unsigned char* ws, size_t ws_stride, double* tri, int* dims, int* status);

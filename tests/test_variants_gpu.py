@@ -123,10 +123,12 @@ def test_shared_memory_tiers_switches(nu, q, opts):
 
 
 @pytest.mark.parametrize("reg", [1, 0])
-@pytest.mark.parametrize("nu,q,conc", [(5, 3, 0.05), (6, 3, 0.2), (7, 5, 0.1), (8, 3, 0.3)])
+@pytest.mark.parametrize("nu,q,conc", [(5, 3, 0.05), (6, 3, 0.2), (7, 5, 0.1), (8, 3, 0.3), (6, 4, 0.2), (7, 2, 0.1),
+                                       (8, 2, 0.3)])
 def test_register_golub_kahan(nu, q, conc, reg):
-    """Complex k-points with 32 < S <= 64 (N = 50..128): the register-resident 256-thread Golub-Kahan
-    (HX_BIDIAG_REG=1, default) and the shared-memory CTA, padded / rectangular blocks at high vacancy counts."""
+    """k-points with 32 < S <= 64 (N = 50..128): the register-resident 256-thread Golub-Kahan, complex and
+    real (TRIM k, q = 2 / 4) (HX_BIDIAG_REG=1, default), and the shared-memory CTA / warp kernels, padded /
+    rectangular blocks at high vacancy counts."""
     check_batch("graphene", nu, q, conc, 24, 23, (0, 11, 23), opts={"HX_BIDIAG_REG": reg})
 
 
