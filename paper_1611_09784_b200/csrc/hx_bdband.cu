@@ -106,6 +106,123 @@ __global__ void __launch_bounds__(256) bd_assemble_kernel(CellDev c, const doubl
 }
 
 // ------------------------------------------------------------------------------------------------
+// Gram-path assembly: G = C^T C of the real (periodic-gauge) block C straight from the hop tables - the sparse
+// rows of C (A dof -> its kept B partners) and columns (B dof -> its kept A partners) go to scratch lists, and one
+// thread per column j accumulates G[:, j] = sum_{i in col(j)} C_ij C[i, :]^T in list order (fixed: deterministic).
+// Replaces bd_assemble_kernel + gram_build_kernel (dense C, then an O(S^2) scan per matrix for its nonzeros).
+template <class F>
+static __device__ __forceinline__ void for_each_partner(const CellDev& c, int r, F&& f) {
+  for (int e = c.h_ptr[r]; e < c.h_ptr[r + 1]; ++e) {
+    const int cb = c.h_col[e];
+    bool dup = false;
+    for (int e2 = c.h_ptr[r]; e2 < e; ++e2) dup |= (c.h_col[e2] == cb);
+    if (!dup) f(cb);
+  }
+  for (int t = c.ht_ptr[r]; t < c.ht_ptr[r + 1]; ++t) {
+    const int cb = c.h_src[c.ht_inst[t]];
+    bool dup = false;
+    for (int e2 = c.h_ptr[r]; e2 < c.h_ptr[r + 1]; ++e2) dup |= (c.h_col[e2] == cb);
+    for (int t2 = c.ht_ptr[r]; t2 < t; ++t2) dup |= (c.h_src[c.ht_inst[t2]] == cb);
+    if (!dup) f(cb);
+  }
+}
+
+// Real periodic-gauge element C[a][b] (the arithmetic of assemble_bipartite's real branch).
+static __device__ __forceinline__ double gram_celem(const CellDev& c, int ra, int cb, double2 k) {
+  const double2 h = herm_element(c.h_ptr, c.h_col, c.h_amp, c.h_disp, ra, cb, k);
+  const double2 pa = c.pos[ra], pb = c.pos[cb];
+  double sn, cs;
+  sincos(k.x * (pa.x - pb.x) + k.y * (pa.y - pb.y), &sn, &cs);
+  return h.x * cs - h.y * sn;
+}
+
+__global__ void __launch_bounds__(256) gram_assemble_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
+                                                            const uint64_t* __restrict__ masks, int64_t mat0,
+                                                            double2* ws, BdWs L, int* dims, int* status) {
+  extern __shared__ int bsm[];
+  int* idx_a = bsm;
+  int* idx_b = idx_a + c.N;
+  int* cnt = idx_b + c.N;
+  __shared__ int over;
+  const int64_t mat = mat0 + blockIdx.x;
+  const int64_t mk = mat / nk;
+  const double2 k = kpts[(int)(mat - mk * nk)];
+  const int S = L.S, tid = threadIdx.x;
+  double* base = reinterpret_cast<double*>(ws + (size_t)blockIdx.x * L.stride);
+  double* G = base + 2 * L.c_off;
+  double* colVal = base + 2 * L.v1_off;                                // [S][GRAM_K]
+  double* rowVal = colVal + (size_t)S * GRAM_K;                        // [S][GRAM_K]
+  int* colIdx = reinterpret_cast<int*>(rowVal + (size_t)S * GRAM_K);   // [S][GRAM_K]
+  int* rowIdx = colIdx + (size_t)S * GRAM_K;                           // [S][GRAM_K]
+  int* colCnt = rowIdx + (size_t)S * GRAM_K;                           // [S]
+  int* rowCnt = colCnt + S;                                            // [S]
+  if (tid == 0) over = 0;
+  const int2 nn = block_compact_bipartite(c, masks + mk * c.words, idx_a, idx_b, cnt);
+  const int d = nn.x + nn.y;
+  if (tid == 0) {
+    dims[blockIdx.x] = d;
+    status[mat] = d == 0 ? 3 : 0;
+  }
+  {
+    double2* G2 = reinterpret_cast<double2*>(G);
+    const size_t n2 = (size_t)S * S / 2;  // S % 4 == 0
+    for (size_t p = tid; p < n2; p += blockDim.x) G2[p] = make_double2(0.0, 0.0);
+  }
+  for (int i = tid; i < S; i += blockDim.x) {
+    colCnt[i] = 0;
+    rowCnt[i] = 0;
+  }
+  __syncthreads();
+  for (int r = tid; r < c.N; r += blockDim.x) {
+    const int ia = idx_a[r], jb = idx_b[r];
+    if (ia >= 0) {
+      int n = 0;
+      for_each_partner(c, r, [&](int cb) {
+        const int j = idx_b[cb];
+        if (j < 0) return;
+        if (n < GRAM_K) {
+          rowIdx[(size_t)ia * GRAM_K + n] = j;
+          rowVal[(size_t)ia * GRAM_K + n] = gram_celem(c, r, cb, k);
+        } else {
+          over = 1;
+        }
+        ++n;
+      });
+      rowCnt[ia] = min(n, GRAM_K);
+    } else if (jb >= 0) {
+      int n = 0;
+      for_each_partner(c, r, [&](int ca) {
+        const int i = idx_a[ca];
+        if (i < 0) return;
+        if (n < GRAM_K) {
+          colIdx[(size_t)jb * GRAM_K + n] = i;
+          colVal[(size_t)jb * GRAM_K + n] = gram_celem(c, ca, r, k);
+        } else {
+          over = 1;
+        }
+        ++n;
+      });
+      colCnt[jb] = min(n, GRAM_K);
+    }
+  }
+  __syncthreads();
+  for (int j = tid; j < S; j += blockDim.x) {
+    double* Gj = G + (size_t)j * S;
+    const int nc = colCnt[j];
+    for (int a = 0; a < nc; ++a) {
+      const int i = colIdx[(size_t)j * GRAM_K + a];
+      const double cij = colVal[(size_t)j * GRAM_K + a];
+      const int nr = rowCnt[i];
+      for (int b = 0; b < nr; ++b) {
+        const int kk = rowIdx[(size_t)i * GRAM_K + b];
+        Gj[kk] = fma(cij, rowVal[(size_t)i * GRAM_K + b], Gj[kk]);
+      }
+    }
+  }
+  if (tid == 0 && over) status[mat] = 2;  // HX_ST_NONFINITE: surfaces as an error, never silently
+}
+
+// ------------------------------------------------------------------------------------------------
 bool launch_cluster_panel(double2* ws, const PanelArgs& a, int64_t cnt, cudaStream_t st);
 
 // M[mr0.., mc0..] -= U W^H (m x n, K = 32): 64 x 64 tiles at 2 CTAs/SM (HX_RU_TN=32: 64 x 32 at 4/SM, same speed)
@@ -503,13 +620,18 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
 
 // Gram path (hx_gram.cuh): G = C^T C of the real batch formed in the slab, symmetric two-stage reduction to its
 // tridiagonal (diag[S], e2[S] doubles at the TGK offset).
-static int bd_reduce_gram(double2* ws2, const BdWs& L, int64_t cnt, int* status, cudaStream_t st) {
+static int bd_reduce_gram(double2* ws2, const BdWs& L, int64_t cnt, const int* dims, int* status, bool direct,
+                          cudaStream_t st) {
   const int S = L.S;
   double* ws = reinterpret_cast<double*>(ws2);
   const size_t sd = 2 * L.stride, c0 = 2 * L.c_off, v1 = 2 * L.v1_off, x = 2 * L.x_off, t1 = 2 * L.t1_off;
   const RSlab G{sd, S, c0};
-  gram_build_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, sd, c0, v1, S, status);
-  count_launch();
+  if (!direct) {
+    gram_build_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, sd, c0, v1, S, status);
+    count_launch();
+  }
+  const bool wsplit = opt("HX_GRAM_WSPLIT", 1) != 0, sym2 = opt("HX_GRAM_SYM2", 1) != 0;
+  const size_t pz = 2 * L.z_off;  // partial V^T Y blocks (z is unused by the Gram path)
   for (int k0 = 0; S - k0 - BB > 0; k0 += BB) {
     const int m = S - k0 - BB;
     const RPanelArgs p{sd, c0, S, k0 + BB, k0, m, 0, v1, S, t1};
@@ -519,21 +641,72 @@ static int bd_reduce_gram(double2* ws2, const BdWs& L, int64_t cnt, int* status,
     }
     xv_real_kernel<0><<<dim3((unsigned)((m + RXV_TM - 1) / RXV_TM), (unsigned)cnt), 128, RXV_SMEM, st>>>(
         ws, G, k0 + BB, k0 + BB, m, m, v1, x, t1);
-    w_fix_real_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, G, m, v1, x, t1);
-    launch_rank_update_real<64>(ws, G, k0 + BB, k0 + BB, m, m, x, v1, cnt, st);  // G22 -= W V^T
-    launch_rank_update_real<64>(ws, G, k0 + BB, k0 + BB, m, m, v1, x, cnt, st);  // G22 -= V W^T
-    count_launch(5);
+    if (wsplit) {
+      const int nch = (m + GRAM_WR - 1) / GRAM_WR;
+      gram_vty_kernel<<<dim3((unsigned)nch, (unsigned)cnt), 256, 0, st>>>(ws, G, m, v1, x, pz);
+      gram_wfix_kernel<<<dim3((unsigned)nch, (unsigned)cnt), 256, 0, st>>>(ws, G, m, nch, v1, x, t1, pz);
+      count_launch();
+    } else {
+      w_fix_real_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, G, m, v1, x, t1);
+    }
+    if (sym2) {  // G22 -= W V^T + V W^T in one pass
+      rank_update_real_kernel<64, true>
+          <<<dim3((unsigned)((m + 63) / 64), (unsigned)((m + RRU_TN - 1) / RRU_TN), (unsigned)cnt), 256,
+             rru_smem<64, true>(), st>>>(ws, G, k0 + BB, k0 + BB, m, m, x, v1);
+      count_launch(4);
+    } else {
+      launch_rank_update_real<64>(ws, G, k0 + BB, k0 + BB, m, m, x, v1, cnt, st);  // G22 -= W V^T
+      launch_rank_update_real<64>(ws, G, k0 + BB, k0 + BB, m, m, v1, x, cnt, st);  // G22 -= V W^T
+      count_launch(5);
+    }
     BD_CUDA(cudaGetLastError());
   }
   const int64_t want = (148 * 11 + cnt - 1) / cnt;
+  if (opt("HX_GRAM_CHASE", 1) == 0) {
+    // dense-slab symmetric chase (shared-memory tiles): the first version, kept for comparison
 #define SYM_CHASE(NW)                                                                                      \
   sym_chase_real_kernel<NW><<<(unsigned)cnt, NW * 32, sym_chase_real_smem<NW>(), st>>>(ws, sd, c0,          \
                                                                                       2 * L.tgk_off, S)
-  if (want >= 6) SYM_CHASE(16);
-  else if (want >= 2) SYM_CHASE(4);
-  else SYM_CHASE(1);
+    if (want >= 6) SYM_CHASE(16);
+    else if (want >= 2) SYM_CHASE(4);
+    else SYM_CHASE(1);
 #undef SYM_CHASE
-  count_launch();
+    count_launch();
+    BD_CUDA(cudaGetLastError());
+    return 0;
+  }
+  // compact lower band (64 doubles per column) + register-row chase; launch shapes as the bidiagonal chase
+  const size_t bo = 2 * L.band_off, to = 2 * L.tgk_off;
+  sym_band_extract_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, sd, c0, bo, S);
+  const int cap = (int)opt("HX_CHASE_CAP", 5);
+  const int rnw = (int)opt("HX_CHASE_RNW", -1);
+  const int rcl_env = (int)opt("HX_CHASE_RCL", -1);
+  int rcl = rcl_env >= 0 ? rcl_env : (S >= 2048 ? 8 : 1);
+  rcl = rcl >= 8 ? 8 : rcl >= 4 ? 4 : rcl >= 2 ? 2 : 1;
+  while (rcl > 1 && (cnt * rcl > 148 || rcl * 16 > S / BB)) rcl /= 2;
+  auto smem_of = [&](size_t need) {
+    return cap > 0 && want < 6 && want >= 2 ? std::max(need, (size_t)(220 * 1024) / cap) : need;
+  };
+#define SYM_CHASE_R(NW)                                                                                          \
+  sym_chase_realr_kernel<NW><<<(unsigned)cnt, NW * 32, smem_of(sym_chase_realr_smem<NW>()), st>>>(ws, sd, bo, to, \
+                                                                                                  S, dims)
+#define SYM_CHASE_CL(CLN)                                                                                       \
+  sym_chase_realr_kernel<16, CLN><<<(unsigned)(cnt * CLN), 16 * 32, sym_chase_realr_smem<16>(), st>>>(ws, sd, bo, \
+                                                                                                      to, S, dims)
+  if (rnw == 1) SYM_CHASE_R(1);
+  else if (rnw == 2) SYM_CHASE_R(2);
+  else if (rnw == 4) SYM_CHASE_R(4);
+  else if (rnw == 8) SYM_CHASE_R(8);
+  else if (rnw == 16) SYM_CHASE_R(16);
+  else if (want >= 6 && rcl == 2) SYM_CHASE_CL(2);
+  else if (want >= 6 && rcl == 4) SYM_CHASE_CL(4);
+  else if (want >= 6 && rcl == 8) SYM_CHASE_CL(8);
+  else if (want >= 6) SYM_CHASE_R(8);
+  else if (want >= 2) SYM_CHASE_R(4);
+  else SYM_CHASE_R(1);
+#undef SYM_CHASE_R
+#undef SYM_CHASE_CL
+  count_launch(2);
   BD_CUDA(cudaGetLastError());
   return 0;
 }
@@ -542,6 +715,14 @@ void bd_init_attributes() {
   set_smem_attr(sym_chase_real_kernel<16>, (int)sym_chase_real_smem<16>());
   set_smem_attr(sym_chase_real_kernel<4>, (int)sym_chase_real_smem<4>());
   set_smem_attr(sym_chase_real_kernel<1>, (int)sym_chase_real_smem<1>());
+  set_smem_attr(sym_chase_realr_kernel<1>, 220 * 1024);
+  set_smem_attr(sym_chase_realr_kernel<2>, 220 * 1024);
+  set_smem_attr(sym_chase_realr_kernel<4>, 220 * 1024);
+  set_smem_attr(sym_chase_realr_kernel<8>, 220 * 1024);
+  set_smem_attr(sym_chase_realr_kernel<16>, 220 * 1024);
+  set_smem_attr(sym_chase_realr_kernel<16, 2>, (int)sym_chase_realr_smem<16>());
+  set_smem_attr(sym_chase_realr_kernel<16, 4>, (int)sym_chase_realr_smem<16>());
+  set_smem_attr(sym_chase_realr_kernel<16, 8>, (int)sym_chase_realr_smem<16>());
   set_smem_attr(xv_real_kernel<0>, (int)RXV_SMEM);
   set_smem_attr(xv_real_kernel<1>, (int)RXV_SMEM);
   set_smem_attr(xv_real_kernel<0, true>, (int)RXV_SMEM_UPD);
@@ -562,6 +743,8 @@ void bd_init_attributes() {
   set_smem_attr(xv_kernel<0, false, true>, (int)XV_SMEM);
   set_smem_attr(xv_kernel<1, false, true>, (int)XV_SMEM);
   set_smem_attr(bd_assemble_kernel, 140 * 1024);
+  set_smem_attr(gram_assemble_kernel, 140 * 1024);
+  set_smem_attr(rank_update_real_kernel<64, true>, (int)rru_smem<64, true>());
 #define BD_CHASE_ATTR(NW, DUAL, CL)                                                                        \
   set_smem_attr(bd_chase_kernel<NW, BB, DUAL, CL>, bd_chase_smem<NW, BB, DUAL>())
   BD_CHASE_ATTR(1, false, 1);
@@ -632,14 +815,18 @@ int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, 
   cg.N = S;
   const bool gram = real_s1 && !eigs && refine && refine_count && opt("HX_GRAM", 0) != 0 &&
                     gram_zones_ok(cg, g, sharp, 1e-3);
+  const bool gram_direct = gram && opt("HX_GRAM_ASSEMBLE", 1) != 0;
   for (int64_t m0 = 0; m0 < nmat; m0 += chunk) {
     const int64_t cnt = std::min(chunk, nmat - m0);
-    bd_assemble_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, masks, m0, ws, L, dims, status,
-                                                         real ? (real_s1 ? 2 : 1) : 0);
+    if (gram_direct)
+      gram_assemble_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, masks, m0, ws, L, dims, status);
+    else
+      bd_assemble_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, masks, m0, ws, L, dims, status,
+                                                           real ? (real_s1 ? 2 : 1) : 0);
     count_launch();
     BD_CUDA(cudaGetLastError());
     if (gram) {
-      if (bd_reduce_gram(ws, L, cnt, status + m0, st)) return -1;
+      if (bd_reduce_gram(ws, L, cnt, dims, status + m0, gram_direct, st)) return -1;
       launch_gram_idos(cg, nk, g, m0, cnt, reinterpret_cast<const double*>(ws + L.tgk_off), L.stride * 2, dims, diff,
                        trans, status, sharp, st, refine, refine_count);
       BD_CUDA(cudaGetLastError());

@@ -154,6 +154,92 @@ __global__ void __launch_bounds__(256) w_fix_real_kernel(double* ws, RSlab g, in
   }
 }
 
+// W = Y - 1/2 V (T^T (V^T Y)) in two launches with row-chunk parallelism (w_fix_real_kernel runs one CTA per
+// matrix: 0.53 ms per step on the 64-matrix N = 2048 tier).  gram_vty_kernel: partial Z = V^T Y of each chunk of
+// GRAM_WR rows (grid: chunks x matrices) to P[chunk][32 x 32]; gram_wfix_kernel: every CTA sums the partials in
+// chunk order (fixed order: deterministic), forms M = 1/2 T^T Z and updates its own rows, W = Y - V M.
+constexpr int GRAM_WR = 128;
+
+__global__ void __launch_bounds__(256) gram_vty_kernel(double* ws, RSlab g, int m, size_t v_off, size_t x_off,
+                                                       size_t p_off) {
+  __shared__ double Vs[32][33], Ys[32][33];
+  double* base = ws + (size_t)blockIdx.y * g.stride;
+  const double* V = base + v_off;
+  const double* Y = base + x_off;
+  double* P = base + p_off + (size_t)blockIdx.x * 1024;
+  const int ld = g.ld, tid = threadIdx.x;
+  const int rb = blockIdx.x * GRAM_WR, re = min(m, rb + GRAM_WR);
+  const int a0 = tid >> 5, b = tid & 31;  // this thread: Z[a0 + 8 q][b], q < 4
+  double z[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int r0 = rb; r0 < re; r0 += 32) {
+    for (int p = tid; p < 1024; p += 256) {
+      const int rr = p & 31, c = p >> 5;
+      const bool ok = r0 + rr < re;
+      Vs[rr][c] = ok ? V[r0 + rr + (size_t)c * ld] : 0.0;
+      Ys[rr][c] = ok ? Y[r0 + rr + (size_t)c * ld] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < 32; ++rr) {
+      const double y = Ys[rr][b];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) z[q] = fma(Vs[rr][a0 + 8 * q], y, z[q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) P[(a0 + 8 * q) * 32 + b] = z[q];
+}
+
+__global__ void __launch_bounds__(256) gram_wfix_kernel(double* ws, RSlab g, int m, int nchunks, size_t v_off,
+                                                        size_t x_off, size_t t_off, size_t p_off) {
+  __shared__ double Vs[32][33], Zs[32][33], Ms[32][33];
+  double* base = ws + (size_t)blockIdx.y * g.stride;
+  const double* V = base + v_off;
+  double* Y = base + x_off;
+  const double* T = base + t_off;
+  const double* P = base + p_off;
+  const int ld = g.ld, tid = threadIdx.x;
+  const int rb = blockIdx.x * GRAM_WR, re = min(m, rb + GRAM_WR);
+  const int a0 = tid >> 5, b = tid & 31;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int a = a0 + 8 * q;
+    double z = 0.0;
+    for (int ch = 0; ch < nchunks; ++ch) z += P[(size_t)ch * 1024 + a * 32 + b];
+    Zs[a][b] = z;
+  }
+  for (int p = tid; p < 1024; p += 256) Vs[p & 31][p >> 5] = T[p];  // Vs[l][a] = T[l][a] (column-major T)
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // Ms[a][b] = 1/2 sum_l T[l][a] Z[l][b]
+    const int a = a0 + 8 * q;
+    double t = 0.0;
+    for (int l = 0; l < 32; ++l) t = fma(Vs[l][a], Zs[l][b], t);
+    Ms[a][b] = 0.5 * t;
+  }
+  __syncthreads();
+  // rows: lane = row (coalesced Y loads and stores), warp + 8 q = column
+  for (int r0 = rb; r0 < re; r0 += 32) {
+    for (int p = tid; p < 1024; p += 256) {
+      const int rr = p & 31, c = p >> 5;
+      Vs[rr][c] = r0 + rr < re ? V[r0 + rr + (size_t)c * ld] : 0.0;
+    }
+    __syncthreads();
+    if (r0 + b < re) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = a0 + 8 * q;
+        double w = Y[r0 + b + (size_t)c * ld];
+#pragma unroll 8
+        for (int a = 0; a < 32; ++a) w = fma(-Vs[b][a], Ms[a][c], w);
+        Y[r0 + b + (size_t)c * ld] = w;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // Real symmetric band (lower, width BWc, dense slab A with ld S) -> tridiagonal (diag[S], e2[S] doubles at
 // out), pipelined over sweeps exactly as bulge_chase_pipe_kernel (hx_chase.cuh) on real data: task t of sweep
 // i updates the diagonal block D = A[s:s+len, s:s+len] two-sidedly (p = D v, w = tau p - tau^2/2 (v.p) v,
@@ -299,6 +385,225 @@ __global__ void __launch_bounds__(NW * 32, 1) sym_chase_real_kernel(double* ws, 
 template <int NW>
 constexpr size_t sym_chase_real_smem() {
   return NW * sizeof(SymChaseSmem) + 64;
+}
+
+// ---------------------------------------------------------------------------------------------------
+// Register-row symmetric chase on a compact lower band (the layout and task pipeline of bd_chase_realr_kernel,
+// hx_bdchase.cuh, for the symmetric band of the Gram path).  Element (r, c), c <= r <= c + 63 (the band of width
+// 32 plus the bulge of the tile below the diagonal tile) at Bs[c * SB_LD + r - c]: 64 doubles per column instead
+// of the 96 of the bidiagonal chase's band (and of the S of the dense slab), so the bands of a many-matrix launch
+// stay in L2.  The lane's row of the diagonal tile D (lower triangle from the band, coalesced; the mirrored part
+// through the transposed shared-memory copy) and then of the tile B below it live in 32 registers: p = D v, the
+// rank-2 updates D -= v w^T + w v^T and B -= q v^T + v' z^T run on registers, shared memory carries only the
+// broadcast vectors and the transposed tile of the column pass.  One reflector and two reduction rounds per task
+// (the bidiagonal task has two reflectors and two paired rounds).
+constexpr int SB_LD = 64;
+
+struct __align__(16) SymChaseSmemRR {
+  double v[32], w[32], vp[32], z[32];
+  double Xt[32][33];  // Xt[c][r] = tile (r, c)
+};
+
+// Lower band (width 32) of the dense S x S slab A into the compact band; the bulge window starts as zero.
+static __global__ void __launch_bounds__(256) sym_band_extract_kernel(double* ws, size_t stride, size_t a_off,
+                                                                       size_t band_off, int S) {
+  double* base = ws + (size_t)blockIdx.x * stride;
+  const double* A = base + a_off;
+  double* B = base + band_off;
+  const size_t n = (size_t)S * SB_LD;
+  for (size_t p = threadIdx.x; p < n; p += blockDim.x) {
+    const int c = (int)(p / SB_LD), j = (int)(p % SB_LD), r = c + j;
+    B[p] = (j <= 32 && r < S) ? A[r + (size_t)c * S] : 0.0;
+  }
+}
+
+template <int NW, int CL = 1>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NW * 32, NW == 4 ? 4 : (NW <= 2 ? 8 : 1))
+    sym_chase_realr_kernel(double* ws, size_t stride, size_t band_off, size_t out_off, int S, const int* dims) {
+  constexpr int BWc = 32, RS = SB_LD - 1;  // RS: one column to the right along a row
+  extern __shared__ __align__(16) unsigned char scr_raw[];
+  SymChaseSmemRR* all = reinterpret_cast<SymChaseSmemRR*>(scr_raw);
+  volatile int* prog = reinterpret_cast<volatile int*>(all + NW);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  SymChaseSmemRR& W = all[warp];
+  const int rank = CL > 1 ? (int)cooperative_groups::this_cluster().block_rank() : 0;
+  const int gw = rank * NW + warp;
+  constexpr int TW = CL * NW;
+  const int64_t mat = blockIdx.x / CL;
+  double* base = ws + (size_t)mat * stride;
+  double* B = base + band_off;
+  double* diag = base + out_off;
+  double* e2 = diag + S;
+  for (int q = threadIdx.x + rank * blockDim.x; q < 2 * S; q += blockDim.x * CL) diag[q] = 0.0;
+  if (lane == 0) prog[warp] = -1;
+  if constexpr (CL > 1) {
+    __threadfence();
+    cooperative_groups::this_cluster().sync();
+  } else {
+    __syncthreads();
+  }
+  const bool skip = dims && dims[mat] == 0;
+  const int nsweeps = skip ? 0 : S - 1;
+  for (int i = gw; i < nsweeps; i += TW) {
+    const int tasks = (S - 1 - i + BWc - 1) / BWc;
+    const int prev_tasks = i > 0 ? (S - i + BWc - 1) / BWc : 0;
+    volatile int* pflag;  // progress counter of the warp that owns sweep i - 1
+    {
+      const int gp = (i - 1 + TW) % TW;
+      if constexpr (CL > 1)
+        pflag = cooperative_groups::this_cluster().map_shared_rank(const_cast<int*>(prog), gp / NW) + gp % NW;
+      else pflag = prog + gp;
+    }
+    double tau = 0.0, vr = 0.0;
+    for (int t = 0; t < tasks; ++t) {
+      if (i > 0) {
+        const int need = (i - 1) * 65536 + min(t + 2, prev_tasks);
+        if (lane == 0)
+          while (*pflag < need) __nanosleep(g_spin_ns);
+        __syncwarp();
+        if constexpr (CL > 1) __threadfence();
+        else __threadfence_block();
+      }
+      const int s = i + 1 + t * BWc;
+      const int len = min(BWc, S - s);
+      const int lb = max(0, min(BWc, S - s - len));
+      double* const blk = B + ((size_t)s * SB_LD + lane);  // (s + lane, s + c), c <= lane, at blk[c * RS]
+      double xr[BWc];
+      {
+        const int nc = lane < len ? lane + 1 : 0;  // lower triangle of the diagonal tile
+#pragma unroll
+        for (int cc = 0; cc < BWc; ++cc) xr[cc] = cc < nc ? ld_band<CL>(blk + cc * RS) : 0.0;
+      }
+      if (t == 0) {
+        // reflector from column i, rows [s, s + len): column i -> (beta, 0, ...)
+        double* const coli = B + ((size_t)i * SB_LD + 1 + lane);  // (s + lane, i)
+        const double x = lane < len ? ld_band<CL>(coli) : 0.0;
+        const double sig2 = warp_sum(x * x);
+        const QuickReflectorR h = quick_reflector_r(__shfl_sync(0xffffffffu, x, 0), sig2);
+        tau = h.tau;
+        vr = lane == 0 ? 1.0 : (lane < len ? x * h.scale : 0.0);
+        W.v[lane] = vr;
+        if (lane < len && tau != 0.0) *coli = lane == 0 ? h.beta : 0.0;
+        if (lane == 0) {
+          diag[i] = ld_band<CL>(B + (size_t)i * SB_LD);
+          e2[i] = sig2;
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < BWc; ++cc) W.Xt[cc][lane] = xr[cc];
+      __syncwarp();
+      // mirrored part of the lane's row: D[lane][c] = D[c][lane] for c > lane
+#pragma unroll
+      for (int cc = 1; cc < BWc; ++cc)
+        if (cc > lane) xr[cc] = W.Xt[lane][cc];
+      // ---- p = D v (registers), w = tau p - tau^2/2 (v.p) v
+      double p;
+      {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < BWc; c += 2) {
+          const double2 u = lds2(&W.v[c]);
+          a0 = fma(xr[c], u.x, a0);
+          a1 = fma(xr[c + 1], u.y, a1);
+        }
+        p = a0 + a1;
+      }
+      const double cval = warp_sum(vr * p);
+      const double wr = tau * p - 0.5 * tau * tau * cval * vr;
+      W.w[lane] = wr;
+      __syncwarp();
+      // ---- D' = D - v w^T - w v^T on the lower triangle, straight to the band
+      if (lane < len) {
+#pragma unroll
+        for (int c = 0; c < BWc; c += 2) {
+          const double2 u = lds2(&W.v[c]), b = lds2(&W.w[c]);
+          const double z0 = fma(-wr, u.x, fma(-vr, b.x, xr[c]));
+          const double z1 = fma(-wr, u.y, fma(-vr, b.y, xr[c + 1]));
+          if (c <= lane) blk[c * RS] = z0;
+          if (c + 1 <= lane) blk[(c + 1) * RS] = z1;
+          if ((c & 7) == 6) asm volatile("" ::: "memory");  // bound the broadcast loads in flight (registers)
+        }
+      }
+      if (lb > 0) {
+        // tile below: (s + 32 + lane, s + c) at blk[32 + c * RS] (len == 32 here)
+        double* const blk2 = blk + BWc;
+        {
+          const bool rowok = lane < lb;
+#pragma unroll
+          for (int cc = 0; cc < BWc; ++cc) xr[cc] = rowok ? ld_band<CL>(blk2 + cc * RS) : 0.0;
+        }
+#pragma unroll
+        for (int cc = 0; cc < BWc; ++cc) W.Xt[cc][lane] = xr[cc];
+        // ---- q = tau B v (registers); column 0 of B - q v^T -> H'
+        double q;
+        {
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int c = 0; c < BWc; c += 2) {
+            const double2 u = lds2(&W.v[c]);
+            a0 = fma(xr[c], u.x, a0);
+            a1 = fma(xr[c + 1], u.y, a1);
+          }
+          q = tau * (a0 + a1);
+        }
+        const double x0 = xr[0] - q;
+        // one reduction round for |x0|^2 and sum_{r>=1} x0_r q_r: v'.q = q_0 + scale * that
+        double sg2 = x0 * x0, qx = lane == 0 ? 0.0 : x0 * q;
+        warp_sum2(sg2, qx);
+        const QuickReflectorR hp = quick_reflector_r(__shfl_sync(0xffffffffu, x0, 0), sg2);
+        const double vpr = lane == 0 ? 1.0 : x0 * hp.scale;  // zero on padded rows
+        const double wq = fma(hp.scale, qx, __shfl_sync(0xffffffffu, q, 0));
+        W.vp[lane] = vpr;
+        __syncwarp();
+        // ---- column pass (lane = column): z_c = tau' (v'.B[:, c] - (v'.q) v_c)
+        {
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int r = 0; r < BWc; r += 2) {
+            const double2 vv = lds2(&W.vp[r]);
+            a0 = fma(vv.x, W.Xt[lane][r], a0);
+            a1 = fma(vv.y, W.Xt[lane][r + 1], a1);
+          }
+          W.z[lane] = hp.tau * (a0 + a1 - wq * W.v[lane]);
+        }
+        __syncwarp();
+        // ---- B'' = B - q v^T - v' z^T, to the band
+        if (lane < lb) {
+          const bool row0 = hp.tau != 0.0;
+#pragma unroll
+          for (int c = 0; c < BWc; c += 2) {
+            const double2 u = lds2(&W.v[c]), zz = lds2(&W.z[c]);
+            double y0 = fma(-vpr, zz.x, fma(-q, u.x, xr[c]));
+            const double y1 = fma(-vpr, zz.y, fma(-q, u.y, xr[c + 1]));
+            if (c == 0 && row0) y0 = lane == 0 ? hp.beta : 0.0;
+            blk2[c * RS] = y0;
+            blk2[(c + 1) * RS] = y1;
+            if ((c & 7) == 6) asm volatile("" ::: "memory");
+          }
+        }
+        __syncwarp();  // every lane is done with v
+        W.v[lane] = vpr;
+        vr = vpr;
+        tau = hp.tau;
+      }
+      if constexpr (CL > 1) __threadfence();
+      else __threadfence_block();
+      __syncwarp();
+      if (lane == 0) prog[warp] = i * 65536 + t + 1;
+    }
+  }
+  if constexpr (CL > 1) {
+    __threadfence();
+    cooperative_groups::this_cluster().sync();
+  } else {
+    __syncthreads();
+  }
+  if (rank == 0 && threadIdx.x == 0 && !skip) diag[S - 1] = ld_band<CL>(B + (size_t)(S - 1) * SB_LD);
+}
+
+template <int NW>
+constexpr size_t sym_chase_realr_smem() {
+  return NW * sizeof(SymChaseSmemRR) + 64;
 }
 
 }  // namespace hx

@@ -435,18 +435,21 @@ __global__ void __launch_bounds__(128) xv_real_kernel(double* ws, RSlab g, int a
 // (4 x 2) of (RT/4) x 32, U and W staged once by cp.async as Us[k][r] / Ws[k][c] (ld = 4 mod 16 doubles),
 // the C tile read straight into the DMMA accumulators.
 constexpr int RRU_TN = 64;
-template <int RT>
+template <int RT, bool SYM2 = false>
 constexpr size_t rru_smem() {
-  return (size_t)GBW * ((RT + 4) + (RRU_TN + 4)) * sizeof(double);
+  return (size_t)(SYM2 ? 2 : 1) * GBW * ((RT + 4) + (RRU_TN + 4)) * sizeof(double);
 }
 
-template <int RT>
+// SYM2: the symmetric rank-2k update M -= U W^T + W U^T in ONE pass over M (the Gram path's G22 -= W V^T + V W^T):
+// the k index runs over 64, [U | W] against [W | U].
+template <int RT, bool SYM2 = false>
 __global__ void __launch_bounds__(256) rank_update_real_kernel(double* ws, RSlab g, int mr0, int mc0, int m, int n,
                                                                size_t u_off, size_t w_off) {
   constexpr int LU = RT + 4, LW = RRU_TN + 4, RF = RT / 32;  // row fragments per warp
+  constexpr int KK = SYM2 ? 2 * GBW : GBW;
   extern __shared__ __align__(16) double rru_sm[];
-  double* Us = rru_sm;             // [32][LU]
-  double* Ws = rru_sm + GBW * LU;  // [32][LW]
+  double* Us = rru_sm;            // [KK][LU]
+  double* Ws = rru_sm + KK * LU;  // [KK][LW]
   double* base = ws + (size_t)blockIdx.z * g.stride;
   const int ld = g.ld;
   double* M = base + g.m_off + (size_t)mc0 * ld + mr0;
@@ -460,12 +463,14 @@ __global__ void __launch_bounds__(256) rank_update_real_kernel(double* ws, RSlab
     const int p = tid + 256 * q, r = 2 * (p % (RT / 2)), k = p / (RT / 2);
     const bool ok = I0 + r < m;
     cp_async16_zfill(Us + k * LU + r, U + (ok ? I0 + r + (size_t)k * ld : 0), ok);
+    if constexpr (SYM2) cp_async16_zfill(Us + (GBW + k) * LU + r, W + (ok ? I0 + r + (size_t)k * ld : 0), ok);
   }
 #pragma unroll
   for (int q = 0; q < RRU_TN * GBW / 512; ++q) {
     const int p = tid + 256 * q, r = 2 * (p & 31), k = p >> 5;
     const bool ok = J0 + r < n;
     cp_async16_zfill(Ws + k * LW + r, W + (ok ? J0 + r + (size_t)k * ld : 0), ok);
+    if constexpr (SYM2) cp_async16_zfill(Ws + (GBW + k) * LW + r, U + (ok ? J0 + r + (size_t)k * ld : 0), ok);
   }
   cp_async_commit();
   double acc[RF][4][2];
@@ -482,7 +487,7 @@ __global__ void __launch_bounds__(256) rank_update_real_kernel(double* ws, RSlab
   cp_async_wait<0>();
   __syncthreads();
 #pragma unroll
-  for (int k4 = 0; k4 < GBW / 4; ++k4) {
+  for (int k4 = 0; k4 < KK / 4; ++k4) {
     const int kc = 4 * k4 + (lane & 3);
     double au[RF], bw[4];
 #pragma unroll

@@ -333,3 +333,25 @@ def test_gram_path_high_vacancy_and_empty():
         ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
         rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), LO_G, HI_G, NPTS, 0.01, ocell.area)
         np.testing.assert_allclose(gram[m], rc, rtol=0, atol=IDOS_TOL)
+
+
+@pytest.mark.parametrize("opts", [{"HX_CHASE_RNW": 1}, {"HX_CHASE_RNW": 2}, {"HX_CHASE_RNW": 4}, {"HX_CHASE_RNW": 8},
+                                  {"HX_CHASE_RNW": 16}, {"HX_CHASE_RCL": 2}, {"HX_CHASE_RCL": 4},
+                                  {"HX_GRAM_CHASE": 0}, {"HX_GRAM_ASSEMBLE": 0}, {"HX_GRAM_WSPLIT": 0},
+                                  {"HX_GRAM_SYM2": 0}])
+@pytest.mark.parametrize("nu,q,count", [(16, 2, 6), (32, 1, 2), (14, 1, 4)])
+def test_gram_chase_variants(nu, q, count, opts):
+    """Every launch shape of the compact-band register-row symmetric chase (warps per matrix, cluster sizes), the
+    dense-slab chase (HX_GRAM_CHASE=0), the dense-C Gram build (HX_GRAM_ASSEMBLE=0), the one-CTA W correction
+    (HX_GRAM_WSPLIT=0) and the two-pass rank update (HX_GRAM_SYM2=0) against the oracle."""
+    _, om, sc, cell, kp = _setup("graphene", nu, q)
+    step = (HI_G - LO_G) / (NPTS - 1)
+    words = sample_masks(sc.nunits, 0.07, 31, 1, 0, count)
+    with _lib.options(HX_GRAM=1, **opts):
+        gram, _, st = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
+    assert (st == 0).all()
+    ocell = O.make_cell(om, nu)
+    for m in (0, count - 1):
+        ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
+        rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), LO_G, HI_G, NPTS, 0.01, ocell.area)
+        np.testing.assert_allclose(gram[m], rc, rtol=0, atol=IDOS_TOL)
