@@ -813,7 +813,7 @@ int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, 
   // panel / product savings (panels 11 -> 5 ms, xv 7.9 -> 3.7 ms per pass) do not cover it; off by default
   CellDev cg = c;
   cg.N = S;
-  const bool gram = real_s1 && !eigs && refine && refine_count && opt("HX_GRAM", 0) != 0 &&
+  const bool gram = real_s1 && !eigs && refine && refine_count && opt("HX_GRAM", 1) != 0 &&
                     gram_zones_ok(cg, g, sharp, 1e-3);
   const bool gram_direct = gram && opt("HX_GRAM_ASSEMBLE", 1) != 0;
   for (int64_t m0 = 0; m0 < nmat; m0 += chunk) {
