@@ -701,6 +701,7 @@ static int bd_reduce_gram(double2* ws2, const BdWs& L, int64_t cnt, const int* d
   else if (want >= 6 && rcl == 2) SYM_CHASE_CL(2);
   else if (want >= 6 && rcl == 4) SYM_CHASE_CL(4);
   else if (want >= 6 && rcl == 8) SYM_CHASE_CL(8);
+  else if (want >= 6 && opt("HX_SYM_BIGNW", 8) == 16) SYM_CHASE_R(16);
   else if (want >= 6) SYM_CHASE_R(8);
   else if (want >= 2) SYM_CHASE_R(4);
   else SYM_CHASE_R(1);

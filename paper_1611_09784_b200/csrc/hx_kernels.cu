@@ -406,7 +406,7 @@ __device__ __forceinline__ double refine_tol(double lo, double hi, double pivmin
 
 // G lanes per item: G-point multisection (log2(G+1) bits per Sturm round) for the latency-bound case of
 // few items (large matrices); shared by the bisection and the zone refinement passes.
-template <bool TGK>
+template <bool TGK, bool GRAM = false>
 __device__ void refine_multisection(const CellDev& c, int nk, const GridDev& g, const double* __restrict__ tri,
                                     size_t tri_stride, const int* __restrict__ dims, int* diff,
                                     unsigned long long* trans, int* status, int sharp,
@@ -425,7 +425,7 @@ __device__ void refine_multisection(const CellDev& c, int nk, const GridDev& g, 
       RefineItem it = items[valid ? q : qw];
       const double* diag = tri + it.lm * tri_stride;
       const double* e2 = diag + c.N;
-      const int d = dims[it.lm];
+      const int d = GRAM ? c.N : dims[it.lm];  // Gram mode: the S x S tridiagonal of G, items in mu = sigma^2
       double lo = it.lo, hi = it.hi;
       bool done = false;
       for (int k = 0; k < 200; ++k) {
@@ -448,8 +448,13 @@ __device__ void refine_multisection(const CellDev& c, int nk, const GridDev& g, 
       }
       if (valid && sub == 0) {
         const double lam = 0.5 * (lo + hi);
-        if (it.flags & 1) add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, lam);
-        if (it.flags & 2) add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, -lam);
+        if constexpr (GRAM) {  // lambda = +-sqrt(mu), sign in flag bit 1
+          const double sg = sqrt(fmax(lam, 0.0));
+          add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, (it.flags & 2) ? -sg : sg);
+        } else {
+          if (it.flags & 1) add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, lam);
+          if (it.flags & 2) add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, -lam);
+        }
       }
     }
 }
@@ -531,6 +536,58 @@ __device__ __forceinline__ void zone_bracket(const CellDev& c, const GridDev& g,
   lb = fmax(a, b);
 }
 
+// Two interleaved Sturm counts (the two edges of a zone).
+template <bool ZD>
+__device__ __forceinline__ void sturm_count_pair(const double* __restrict__ diag, const double* __restrict__ e2, int d,
+                                                 double xa, double xb, double pivmin, int& na, int& nb) {
+#if HX_STURM_POLY
+  (void)pivmin;
+  const double a0 = ZD ? 0.0 : diag[0];
+  double pa1 = 1.0, pa0 = a0 - xa, pb1 = 1.0, pb0 = a0 - xb;
+  if (pa0 == 0.0) pa0 = -0x1p-200;
+  if (pb0 == 0.0) pb0 = -0x1p-200;
+  int ca = pa0 < 0.0, cb = pb0 < 0.0;
+  for (int i = 1; i < d; ++i) {
+    const double e = e2[i - 1], a = ZD ? 0.0 : diag[i];
+    double pan = fma(a - xa, pa0, -(e * pa1));
+    double pbn = fma(a - xb, pb0, -(e * pb1));
+    if (pan == 0.0) pan = -0x1p-200 * pa0;
+    if (pbn == 0.0) pbn = -0x1p-200 * pb0;
+    ca += sturm_sign_change(pan, pa0);
+    cb += sturm_sign_change(pbn, pb0);
+    pa1 = pa0;
+    pa0 = pan;
+    pb1 = pb0;
+    pb0 = pbn;
+    if ((i & 3) == 0) {
+      const double sa = sturm_scale_of(pa0, pa1), sb = sturm_scale_of(pb0, pb1);
+      pa0 *= sa;
+      pa1 *= sa;
+      pb0 *= sb;
+      pb1 *= sb;
+    }
+  }
+  na = ca;
+  nb = cb;
+#else
+  double qa = (ZD ? 0.0 : diag[0]) - xa, qb = (ZD ? 0.0 : diag[0]) - xb;
+  if (fabs(qa) <= pivmin) qa = -pivmin;
+  if (fabs(qb) <= pivmin) qb = -pivmin;
+  int ca = qa < 0.0, cb = qb < 0.0;
+  for (int i = 1; i < d; ++i) {
+    const double e = e2[i - 1], a = ZD ? 0.0 : diag[i];
+    qa = fma(-e, sturm_rcp(qa), a - xa);
+    qb = fma(-e, sturm_rcp(qb), a - xb);
+    if (fabs(qa) <= pivmin) qa = -pivmin;
+    if (fabs(qb) <= pivmin) qb = -pivmin;
+    ca += qa < 0.0;
+    cb += qb < 0.0;
+  }
+  na = ca;
+  nb = cb;
+#endif
+}
+
 // One CTA per matrix.  counts[2m] / counts[2m+1]: eigenvalues below the lower / upper lambda edge of zone m
 // (dynamic shared memory, 2 npts ints).  rev: E decreases with lambda.
 template <bool ZD>
@@ -589,19 +646,8 @@ __global__ void __launch_bounds__(256) zone_count_kernel(CellDev c, int nk, Grid
     const bool ra = xa > gl && xa < gu, rb = xb > gl && xb < gu;
     int ca = xa <= gl ? 0 : d, cb = xb <= gl ? 0 : d;
     if (ra || rb) {
-      double qa = (ZD ? 0.0 : diag[0]) - xa, qb = (ZD ? 0.0 : diag[0]) - xb;
-      if (fabs(qa) <= pivmin) qa = -pivmin;
-      if (fabs(qb) <= pivmin) qb = -pivmin;
-      int na = qa < 0.0, nb = qb < 0.0;
-      for (int i = 1; i < d; ++i) {
-        const double e = e2[i - 1], a = ZD ? 0.0 : diag[i];
-        qa = fma(-e, sturm_rcp(qa), a - xa);
-        qb = fma(-e, sturm_rcp(qb), a - xb);
-        if (fabs(qa) <= pivmin) qa = -pivmin;
-        if (fabs(qb) <= pivmin) qb = -pivmin;
-        na += qa < 0.0;
-        nb += qb < 0.0;
-      }
+      int na, nb;
+      sturm_count_pair<ZD>(diag, e2, d, xa, xb, pivmin, na, nb);
       if (ra) ca = na;
       if (rb) cb = nb;
     }
@@ -629,10 +675,39 @@ __global__ void __launch_bounds__(256) zone_count_kernel(CellDev c, int nk, Grid
   }
 }
 
-// Sturm count below x and, with it, s = d/dx log|det(T - x)| = sum_i q_i'/q_i (q_i' = -1 + e q_{i-1}'/q_{i-1}^2).
+// Sturm count below x and, with it, s = d/dx log|det(T - x)| = P'(x) / P(x): the determinant recurrence of
+// sturm_count_fast and its derivative P_i' = (a_i - x) P_{i-1}' - P_{i-1} - e2_{i-1} P_{i-2}' (P_{-1}' = 0,
+// P_0' = -1) under the same power-of-two scaling; one division at the end.  (HX_STURM_POLY=0: the dstebz quotients
+// with s = sum_i q_i'/q_i, q_i' = -1 + e q_{i-1}'/q_{i-1}^2.)
 template <bool ZD>
 __device__ __forceinline__ int sturm_count_deriv(const double* __restrict__ diag, const double* __restrict__ e2, int d,
                                                  double x, double pivmin, double& s) {
+#if HX_STURM_POLY
+  (void)pivmin;
+  double p1 = 1.0, p0 = (ZD ? 0.0 : diag[0]) - x, d1 = 0.0, d0 = -1.0;
+  if (p0 == 0.0) p0 = -0x1p-200;
+  int cnt = p0 < 0.0;
+  for (int i = 1; i < d; ++i) {
+    const double e = e2[i - 1], ax = (ZD ? 0.0 : diag[i]) - x;
+    double pn = fma(ax, p0, -(e * p1));
+    const double dn = fma(ax, d0, fma(-e, d1, -p0));
+    if (pn == 0.0) pn = -0x1p-200 * p0;
+    cnt += sturm_sign_change(pn, p0);
+    p1 = p0;
+    p0 = pn;
+    d1 = d0;
+    d0 = dn;
+    if ((i & 3) == 0) {
+      const double sc = sturm_scale_of(p0, p1);
+      p0 *= sc;
+      p1 *= sc;
+      d0 *= sc;
+      d1 *= sc;
+    }
+  }
+  s = d0 / p0;
+  return cnt;
+#else
   double q = (ZD ? 0.0 : diag[0]) - x;
   if (fabs(q) <= pivmin) q = -pivmin;
   int cnt = q < 0.0;
@@ -650,6 +725,7 @@ __device__ __forceinline__ int sturm_count_deriv(const double* __restrict__ diag
   }
   s = acc;
   return cnt;
+#endif
 }
 
 // Eigenvalue idx of the tridiagonal inside [lo, hi] (clo / chi: Sturm counts at lo / hi) to the
@@ -830,19 +906,8 @@ __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk,
     const bool ra = xa > gl && xa < gu, rb = xb > gl && xb < gu;
     int ca = xa <= gl ? 0 : S, cb = xb <= gl ? 0 : S;
     if (ra || rb) {
-      double qa = diag[0] - xa, qb = diag[0] - xb;
-      if (fabs(qa) <= pivmin) qa = -pivmin;
-      if (fabs(qb) <= pivmin) qb = -pivmin;
-      int na = qa < 0.0, nb = qb < 0.0;
-      for (int i = 1; i < S; ++i) {
-        const double e = e2[i - 1], a = diag[i];
-        qa = fma(-e, sturm_rcp(qa), a - xa);
-        qb = fma(-e, sturm_rcp(qb), a - xb);
-        if (fabs(qa) <= pivmin) qa = -pivmin;
-        if (fabs(qb) <= pivmin) qb = -pivmin;
-        na += qa < 0.0;
-        nb += qb < 0.0;
-      }
+      int na, nb;
+      sturm_count_pair<false>(diag, e2, S, xa, xb, pivmin, na, nb);
       if (ra) ca = na;
       if (rb) cb = nb;
     }
@@ -874,13 +939,22 @@ __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk,
   }
 }
 
-// Gram zone eigenvalues: mu by the bracketed Newton search of zone_locate on G's tridiagonal, lambda = +-sqrt(mu).
+// Gram zone eigenvalues in mu = sigma^2 on G's tridiagonal, lambda = +-sqrt(mu).  G = 1: the bracketed Newton
+// search of zone_locate, one thread per item; G > 1: G-lane multisection (uniform control flow: every lane runs one
+// Sturm count per round).  Chosen by the matrix size only (batch-independent results): the few-matrix launches of
+// S >= 1024 are bound by the slowest item of the diverging Newton search (near-degenerate clusters fall back to
+// bisection: 5.0 ms on the 64-matrix S = 1024 launch, 2.8 ms with 8 lanes); the many-matrix launches keep Newton
+// (S = 256: 1.3 ms, 4 lanes 3.1 ms).  HX_GRAM_REFINE_LANES overrides.
 __global__ void __launch_bounds__(128) zone_refine_gram_kernel(CellDev c, int nk, GridDev g,
                                                                const double* __restrict__ tri, size_t tri_stride,
                                                                int* diff, unsigned long long* trans, int* status,
                                                                int sharp, const RefineItem* __restrict__ items,
-                                                               const unsigned long long* __restrict__ count) {
+                                                               const unsigned long long* __restrict__ count, int G) {
   const unsigned long long n = *count;
+  if (G > 1) {
+    refine_multisection<false, true>(c, nk, g, tri, tri_stride, nullptr, diff, trans, status, sharp, items, n, G);
+    return;
+  }
   const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
   const int S = c.N;
   for (unsigned long long q = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += nthreads) {
@@ -920,8 +994,10 @@ bool launch_gram_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, 
   set_smem_attr(zone_count_gram_kernel, zsm);
   zone_count_gram_kernel<<<(unsigned)nmat, zt, zsm, st>>>(c, nk, g, sharp, rev, mat0, nmat, tri, tri_stride, dims,
                                                            diff, refine, refine_count);
+  const int lanes_opt = (int)opt("HX_GRAM_REFINE_LANES", 0);
+  const int G = lanes_opt > 0 ? lanes_opt : (c.N >= 1024 ? 8 : 1);
   zone_refine_gram_kernel<<<148 * 16, 128, 0, st>>>(c, nk, g, tri, tri_stride, diff, trans, status, sharp, refine,
-                                                    refine_count);
+                                                    refine_count, G);
   count_launch(2);
   return true;
 }
