@@ -569,6 +569,10 @@ void band_init_attributes() {
   HCHASE_ATTR(6);
   HCHASE_ATTR(11);
 #undef HCHASE_ATTR
+  set_smem_attr(herm_chase_r_kernel<1>, (int)herm_chase_r_smem<1>());
+  set_smem_attr(herm_chase_r_kernel<2>, (int)herm_chase_r_smem<2>());
+  set_smem_attr(herm_chase_r_kernel<4>, (int)herm_chase_r_smem<4>());
+  set_smem_attr(herm_chase_r_kernel<8>, (int)herm_chase_r_smem<8>());
 }
 
 bool band_path_supported(int N) { return N > HX_SMEM_MAX_N && N <= HX_MAX_N; }
@@ -631,6 +635,27 @@ static int band_reduce(double2* ws, const BandWs& L, int N, int64_t cnt, const i
   // HX_HCHASE_MIN_NW overrides
   const int min_nw = (int)opt("HX_HCHASE_MIN_NW", 3);
   const int64_t want = std::max<int64_t>(min_nw, (148 * 12 + cnt - 1) / cnt);
+  if (opt("HX_HCHASE_REG", 1) != 0) {
+    // compact band (in the V / X panels' space: N x 64 double2) + register-row chase
+    herm_band_extract_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, L.stride, L.a_off, L.v_off, N, dims);
+    const int rnw = (int)opt("HX_HCHASE_RNW", 0);
+    // warps (sweeps in flight) per matrix by the launch size: 242 registers per thread keep 8 warps per SM
+    // resident, so the launch is split 8 x 1 / 4 x 2 / 2 x 4 (warps x CTAs per SM); measured on c3: 128 x N = 2816:
+    // 8 warps 119 ms (shared-memory-tile kernel 177 ms); 1844 x N = 704: 8 / 4 / 2 warps 109 / 99 / 114 ms
+    // (151 ms); 3072 x N = 352: 23 / 13 / 9.7 ms
+    const int nw = rnw > 0 ? rnw : (cnt <= 300 ? 8 : (cnt <= 2400 ? 4 : 2));
+#define HCHASE_R(NW)                                                                                       \
+  herm_chase_r_kernel<NW><<<(unsigned)cnt, NW * 32, herm_chase_r_smem<NW>(), st>>>(ws, L.stride, L.v_off,   \
+                                                                                   L.dg_off, N, dims)
+    if (nw >= 8) HCHASE_R(8);
+    else if (nw >= 4) HCHASE_R(4);
+    else if (nw >= 2) HCHASE_R(2);
+    else HCHASE_R(1);
+#undef HCHASE_R
+    count_launch(2);
+    BAND_CUDA(cudaGetLastError());
+    return 0;
+  }
 #define HCHASE(NW)                                                                                \
   bulge_chase_pipe_kernel<NW, BW, false><<<(unsigned)cnt, NW * 32, chase_smem_bytes<NW, BW, false>(), st>>>( \
       ws, L.stride, L.a_off, L.dg_off, N, dims)

@@ -355,3 +355,26 @@ def test_gram_chase_variants(nu, q, count, opts):
         ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
         rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), LO_G, HI_G, NPTS, 0.01, ocell.area)
         np.testing.assert_allclose(gram[m], rc, rtol=0, atol=IDOS_TOL)
+
+
+# ---- Hermitian banded tier (tables): register-row chase on the compact complex band ---------------------------
+@pytest.mark.parametrize("opts", [{"HX_HCHASE_RNW": 1}, {"HX_HCHASE_RNW": 2}, {"HX_HCHASE_RNW": 4},
+                                  {"HX_HCHASE_RNW": 8}, {"HX_HCHASE_REG": 0}])
+def test_hermitian_chase_variants(opts):
+    """Every warps-per-matrix count of the register-row Hermitian chase (hx_chase.cuh: herm_chase_r_kernel) and the
+    shared-memory-tile chase on the dense slab (HX_HCHASE_REG=0), 11-band table at nu = 6 (N = 396, defected so
+    that d < N), eigenvalues and IDOS against zheevd."""
+    check_batch("table", 6, 2, 0.08, 3, 7, (0, 2), opts=opts)
+
+
+def test_hermitian_chase_bitwise_repeatable():
+    """The flag-pipelined register-row Hermitian chase gives identical bits run after run (4 and 8 warps)."""
+    _, om, sc, cell, kp = _setup("table", 6, 1)
+    words = sample_masks(sc.nunits, 0.05, 3, 1, 0, 4)
+    step = (HI_T - LO_T) / (NPTS - 1)
+    for nw in (4, 8):
+        with _lib.options(HX_HCHASE_RNW=nw):
+            ref, eigs0, _ = eval_batch(cell, kp, words, LO_T, step, NPTS, 0.01, want_eigs=True)
+            for _ in range(6):
+                cur, eigs, _ = eval_batch(cell, kp, words, LO_T, step, NPTS, 0.01, want_eigs=True)
+                assert np.array_equal(cur, ref) and np.array_equal(eigs, eigs0, equal_nan=True)

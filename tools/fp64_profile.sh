@@ -11,3 +11,4 @@ run() {  # name label args...
 run c2 "c2 one pass (tools/profile_run.py --config c2), serialised under ncu" --config c2
 run c2_L4_parent "c2 level 4 parent tier (N = 2048, 64 matrices at Gamma), tools/profile_run.py --config c2 --levels 4 --parent-only" --config c2 --levels 4 --parent-only
 run c4 "c4 one pass (tools/profile_run.py --config c4), serialised under ncu" --config c4
+run c3 "c3 one pass (tools/profile_run.py --config c3), serialised under ncu" --config c3
