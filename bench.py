@@ -79,7 +79,7 @@ NPTS = 201
 
 # ncu DRAM bytes (read + write) of one hx_eval_idos_batch_device call of the dominant tier, the same masks
 # as the bench's tier (seeded), from a committed capture: (config, N) -> (profile, line prefix)
-TRAFFIC = {("c2", 2048): ("profiles/r01_traffic_L4_parent.txt", "total (hx kernels)")}
+TRAFFIC = {("c2", 2048): ("profiles/r02_traffic_L4_parent.txt", "total (hx kernels)")}
 
 
 def traffic_of(config, N):

@@ -211,15 +211,20 @@ __global__ void __launch_bounds__(256) gram_wfix_kernel(double* ws, RSlab g, int
   }
   for (int p = tid; p < 1024; p += 256) Vs[p & 31][p >> 5] = T[p];  // Vs[l][a] = T[l][a] (column-major T)
   __syncthreads();
+  {  // Ms[a][b] = 1/2 sum_l T[l][a] Z[l][b], a = a0 + 8 q: one Z load per four products
+    double t[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+    for (int l = 0; l < 32; ++l) {
+      const double zl = Zs[l][b];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {  // Ms[a][b] = 1/2 sum_l T[l][a] Z[l][b]
-    const int a = a0 + 8 * q;
-    double t = 0.0;
-    for (int l = 0; l < 32; ++l) t = fma(Vs[l][a], Zs[l][b], t);
-    Ms[a][b] = 0.5 * t;
+      for (int q = 0; q < 4; ++q) t[q] = fma(Vs[l][a0 + 8 * q], zl, t[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) Ms[a0 + 8 * q][b] = 0.5 * t[q];
   }
   __syncthreads();
-  // rows: lane = row (coalesced Y loads and stores), warp + 8 q = column
+  // rows: lane = row (coalesced Y loads and stores), warp + 8 q = column; one V load per four products (the
+  // kernel was bound by its shared-memory loads: two per FMA, 144 us on the 1024-matrix launches)
   for (int r0 = rb; r0 < re; r0 += 32) {
     for (int p = tid; p < 1024; p += 256) {
       const int rr = p & 31, c = p >> 5;
@@ -227,14 +232,17 @@ __global__ void __launch_bounds__(256) gram_wfix_kernel(double* ws, RSlab g, int
     }
     __syncthreads();
     if (r0 + b < re) {
+      double w[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = a0 + 8 * q;
-        double w = Y[r0 + b + (size_t)c * ld];
+      for (int q = 0; q < 4; ++q) w[q] = Y[r0 + b + (size_t)(a0 + 8 * q) * ld];
 #pragma unroll 8
-        for (int a = 0; a < 32; ++a) w = fma(-Vs[b][a], Ms[a][c], w);
-        Y[r0 + b + (size_t)c * ld] = w;
+      for (int a = 0; a < 32; ++a) {
+        const double va = Vs[b][a];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) w[q] = fma(-va, Ms[a][a0 + 8 * q], w[q]);
       }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) Y[r0 + b + (size_t)(a0 + 8 * q) * ld] = w[q];
     }
     __syncthreads();
   }
