@@ -631,6 +631,7 @@ static int bd_reduce_gram(double2* ws2, const BdWs& L, int64_t cnt, const int* d
     count_launch();
   }
   const bool wsplit = opt("HX_GRAM_WSPLIT", 1) != 0, sym2 = opt("HX_GRAM_SYM2", 1) != 0;
+  const int tri = opt("HX_GRAM_TRI", 1) != 0;  // lower tiles only + mirror (hx_real.cuh)
   const size_t pz = 2 * L.z_off;  // partial V^T Y blocks (z is unused by the Gram path)
   for (int k0 = 0; S - k0 - BB > 0; k0 += BB) {
     const int m = S - k0 - BB;
@@ -652,7 +653,7 @@ static int bd_reduce_gram(double2* ws2, const BdWs& L, int64_t cnt, const int* d
     if (sym2) {  // G22 -= W V^T + V W^T in one pass
       rank_update_real_kernel<64, true>
           <<<dim3((unsigned)((m + 63) / 64), (unsigned)((m + RRU_TN - 1) / RRU_TN), (unsigned)cnt), 256,
-             rru_smem<64, true>(), st>>>(ws, G, k0 + BB, k0 + BB, m, m, x, v1);
+             rru_smem<64, true>(), st>>>(ws, G, k0 + BB, k0 + BB, m, m, x, v1, tri);
       count_launch(4);
     } else {
       launch_rank_update_real<64>(ws, G, k0 + BB, k0 + BB, m, m, x, v1, cnt, st);  // G22 -= W V^T

@@ -444,7 +444,7 @@ constexpr size_t rru_smem() {
 // the k index runs over 64, [U | W] against [W | U].
 template <int RT, bool SYM2 = false>
 __global__ void __launch_bounds__(256) rank_update_real_kernel(double* ws, RSlab g, int mr0, int mc0, int m, int n,
-                                                               size_t u_off, size_t w_off) {
+                                                               size_t u_off, size_t w_off, int tri = 0) {
   constexpr int LU = RT + 4, LW = RRU_TN + 4, RF = RT / 32;  // row fragments per warp
   constexpr int KK = SYM2 ? 2 * GBW : GBW;
   extern __shared__ __align__(16) double rru_sm[];
@@ -456,6 +456,11 @@ __global__ void __launch_bounds__(256) rank_update_real_kernel(double* ws, RSlab
   const double* U = base + u_off;
   const double* W = base + w_off;
   const int I0 = blockIdx.x * RT, J0 = blockIdx.y * RRU_TN;
+  // SYM2 with tri (square symmetric block, mr0 == mc0, RT == RRU_TN): only the tiles on and below the diagonal are
+  // computed; every element (r, c), r >= c, is stored at (r, c) AND mirrored to (c, r) - half the DMMA work of the
+  // two-triangle update and an exactly symmetric matrix
+  const bool mirror = SYM2 && tri;
+  if (mirror && blockIdx.y > blockIdx.x) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wr = warp & 3, wc = warp >> 2;
 #pragma unroll
@@ -505,6 +510,17 @@ __global__ void __launch_bounds__(256) rank_update_real_kernel(double* ws, RSlab
     for (int ct = 0; ct < 4; ++ct) {
       const int r = I0 + (RT / 4) * wr + 8 * rt + (lane >> 2);
       const int cc = J0 + 32 * wc + 8 * ct + 2 * (lane & 3);
+      if (mirror) {
+        if (r < m && cc < n && r >= cc) {
+          M[r + (size_t)cc * ld] = acc[rt][ct][0];
+          if (r > cc) M[cc + (size_t)r * ld] = acc[rt][ct][0];
+        }
+        if (r < m && cc + 1 < n && r >= cc + 1) {
+          M[r + (size_t)(cc + 1) * ld] = acc[rt][ct][1];
+          if (r > cc + 1) M[cc + 1 + (size_t)r * ld] = acc[rt][ct][1];
+        }
+        continue;
+      }
       if (r < m && cc < n) M[r + (size_t)cc * ld] = acc[rt][ct][0];
       if (r < m && cc + 1 < n) M[r + (size_t)(cc + 1) * ld] = acc[rt][ct][1];
     }

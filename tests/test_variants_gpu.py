@@ -338,7 +338,7 @@ def test_gram_path_high_vacancy_and_empty():
 @pytest.mark.parametrize("opts", [{"HX_CHASE_RNW": 1}, {"HX_CHASE_RNW": 2}, {"HX_CHASE_RNW": 4}, {"HX_CHASE_RNW": 8},
                                   {"HX_CHASE_RNW": 16}, {"HX_CHASE_RCL": 2}, {"HX_CHASE_RCL": 4},
                                   {"HX_GRAM_CHASE": 0}, {"HX_GRAM_ASSEMBLE": 0}, {"HX_GRAM_WSPLIT": 0},
-                                  {"HX_GRAM_SYM2": 0}])
+                                  {"HX_GRAM_SYM2": 0}, {"HX_GRAM_TRI": 0}])
 @pytest.mark.parametrize("nu,q,count", [(16, 2, 6), (32, 1, 2), (14, 1, 4)])
 def test_gram_chase_variants(nu, q, count, opts):
     """Every launch shape of the compact-band register-row symmetric chase (warps per matrix, cluster sizes), the
