@@ -429,6 +429,11 @@ template <int NW, int CL = 1>
 __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NW * 32, NW == 4 ? 4 : (NW <= 2 ? 8 : 1))
     sym_chase_realr_kernel(double* ws, size_t stride, size_t band_off, size_t out_off, int S, const int* dims) {
   constexpr int BWc = 32, RS = SB_LD - 1;  // RS: one column to the right along a row
+  // Progress counters count HALF tasks (D part, B part).  HALF (few matrices, critical-path-bound launches): the D
+  // part of task t waits only for the D part of task t + 1 of the previous sweep (its last overlap is the element
+  // (s + 31, s + 31)), the B part for that task's B part - sweep i + 1 trails sweep i by 1.5 tasks instead of 2.
+  // Many-matrix launches keep one wait and one publish per task.
+  constexpr bool HALF = CL > 1 || NW >= 8;
   extern __shared__ __align__(16) unsigned char scr_raw[];
   SymChaseSmemRR* all = reinterpret_cast<SymChaseSmemRR*>(scr_raw);
   volatile int* prog = reinterpret_cast<volatile int*>(all + NW);
@@ -465,7 +470,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NW * 32, NW == 4 ? 
     double tau = 0.0, vr = 0.0;
     for (int t = 0; t < tasks; ++t) {
       if (i > 0) {
-        const int need = (i - 1) * 65536 + min(t + 2, prev_tasks);
+        const int need = (i - 1) * 65536 + (HALF ? min(2 * t + 3, 2 * prev_tasks) : 2 * min(t + 2, prev_tasks));
         if (lane == 0)
           while (*pflag < need) __nanosleep(g_spin_ns);
         __syncwarp();
@@ -530,6 +535,21 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NW * 32, NW == 4 ? 
           if (c <= lane) blk[c * RS] = z0;
           if (c + 1 <= lane) blk[(c + 1) * RS] = z1;
           if ((c & 7) == 6) asm volatile("" ::: "memory");  // bound the broadcast loads in flight (registers)
+        }
+      }
+      if constexpr (HALF) {
+        // D part done: publish, then wait for the B part of task t + 1 of the previous sweep
+        if constexpr (CL > 1) __threadfence();
+        else __threadfence_block();
+        __syncwarp();
+        if (lane == 0) prog[warp] = i * 65536 + 2 * t + 1;
+        if (i > 0 && lb > 0) {
+          const int need = (i - 1) * 65536 + min(2 * t + 4, 2 * prev_tasks);
+          if (lane == 0)
+            while (*pflag < need) __nanosleep(g_spin_ns);
+          __syncwarp();
+          if constexpr (CL > 1) __threadfence();
+          else __threadfence_block();
         }
       }
       if (lb > 0) {
@@ -597,7 +617,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NW * 32, NW == 4 ? 
       if constexpr (CL > 1) __threadfence();
       else __threadfence_block();
       __syncwarp();
-      if (lane == 0) prog[warp] = i * 65536 + t + 1;
+      if (lane == 0) prog[warp] = i * 65536 + 2 * t + 2;
     }
   }
   if constexpr (CL > 1) {

@@ -378,3 +378,32 @@ def test_hermitian_chase_bitwise_repeatable():
             for _ in range(6):
                 cur, eigs, _ = eval_batch(cell, kp, words, LO_T, step, NPTS, 0.01, want_eigs=True)
                 assert np.array_equal(cur, ref) and np.array_equal(eigs, eigs0, equal_nan=True)
+
+
+@pytest.mark.parametrize("opts", [{"HX_CHASE_RNW": 8}, {"HX_CHASE_RNW": 4}, {"HX_CHASE_RNW": 16}, {"HX_CHASE_RCL": 2},
+                                  {"HX_CHASE_RCL": 4}])
+def test_gram_chase_bitwise_repeatable(opts):
+    """The flag-pipelined symmetric chase (half-task progress counters for the 8-warp and cluster launches) gives
+    identical curves run after run, with a second batch running on another context in between."""
+    import threading
+
+    model = hx.GrapheneNNModel()
+    nu, q = (32, 1) if "HX_CHASE_RCL" in opts else (16, 2)
+    sc = hx.build_supercell(model.lattice_spec(), nu)
+    cell = hx.compile_cell(model, sc)
+    kp = np.ascontiguousarray(hx.make_bz_grid(model.lattice_spec(), nu, q, "reduced").kpoints)
+    words = sample_masks(sc.nunits, 0.05, 99, 1, 0, 8 if nu == 16 else 2)
+    step = (HI_G - LO_G) / (NPTS - 1)
+    other = _lib.Device.new_ctx(0, 0)
+    noise = sample_masks(sc.nunits, 0.05, 5, 1, 0, 16)
+    with _lib.options(HX_GRAM=1, **opts):
+        ref, _, _ = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
+        for rep in range(12):
+            th = threading.Thread(target=eval_batch, args=(cell, kp, noise, LO_G, step, NPTS, 0.01),
+                                  kwargs={"ctx": other}) if rep % 3 == 0 else None
+            if th:
+                th.start()
+            cur, _, _ = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
+            if th:
+                th.join()
+            assert np.array_equal(cur, ref), rep
