@@ -68,6 +68,7 @@ _KGRID_CACHE: dict = {}
 # staging).  Experiments: HX_E2E_PRIO=big|big+small, HX_E2E_ORDER=big-first.
 _E2E_PRIO = os.environ.get("HX_E2E_PRIO", "tiered")
 _E2E_ORDER = os.environ.get("HX_E2E_ORDER", "big-then-small")
+_E2E_WORKERS = int(os.environ.get("HX_E2E_WORKERS", "4"))  # concurrent (tier, level) pieces (0: all at once); c2 e2e 121k (all 7) -> 127k
 
 
 def unique_rows(words):
@@ -477,7 +478,8 @@ class Engine:
         lane = 0
         npieces = sum(len(v) for v in tiers.values())
         # one piece (a single-level run): solve it inline, without a thread pool
-        with (_InlineExecutor() if npieces == 1 else ThreadPoolExecutor(max_workers=max(1, npieces))) as ex:
+        nworkers = max(1, min(npieces, _E2E_WORKERS) if _E2E_WORKERS > 0 else npieces)
+        with (_InlineExecutor() if npieces == 1 else ThreadPoolExecutor(max_workers=nworkers)) as ex:
             for tier in order:
                 cache = self._tier_cache(tier, npts)
                 pend = np.zeros(0, dtype=np.int64)  # sorted keys of this call's new masks so far, their rows

@@ -1,6 +1,7 @@
 #!/bin/bash
 set -x
 cd $GRAFT_REPO_ROOT
-timeout 600 python bench.py --config c3 --no-e2e --no-cpu-baseline --steps 5 > gpurun_out/bench_c3_L3.json 2> gpurun_out/bench_c3_L3.err
-HX_LANES=0 timeout 600 python bench.py --config c3 --no-e2e --no-cpu-baseline --steps 5 > gpurun_out/bench_c3_L0.json 2> gpurun_out/bench_c3_L0.err
-timeout 600 python bench.py > gpurun_out/bench_c2_L3.json 2> gpurun_out/bench_c2_L3.err
+for W in 0 3 4 5; do
+HX_E2E_WORKERS=$W timeout 600 python bench.py --no-cpu-baseline --steps 10 > gpurun_out/bench_e2eW$W.json 2> gpurun_out/bench_e2eW$W.err
+done
+HX_E2E_WORKERS=3 HX_E2E_ORDER=big-first timeout 600 python bench.py --no-cpu-baseline --steps 10 > gpurun_out/bench_e2eW3b.json 2> gpurun_out/bench_e2eW3b.err
