@@ -407,6 +407,19 @@ constexpr size_t sym_chase_real_smem() {
 // (the bidiagonal task has two reflectors and two paired rounds).
 constexpr int SB_LD = 64;
 
+// Progress counters of the cluster launches: release / acquire at cluster scope on the (distributed) shared-memory
+// word instead of device-scope fences around a volatile access.  The tile stores of the 32 lanes are ordered
+// before lane 0's release by the __syncwarp() in front of it (cumulativity); the consumer's tile loads
+// (ld.global.cg) follow lane 0's acquire through the __syncwarp() behind the poll.
+__device__ __forceinline__ void st_release_cluster(volatile int* p, int v) {
+  asm volatile("st.release.cluster.s32 [%0], %1;" ::"l"(const_cast<int*>(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cluster(const volatile int* p) {
+  int v;
+  asm volatile("ld.acquire.cluster.s32 %0, [%1];" : "=r"(v) : "l"(const_cast<int*>(p)) : "memory");
+  return v;
+}
+
 struct __align__(16) SymChaseSmemRR {
   double v[32], w[32], vp[32], z[32];
   double Xt[32][33];  // Xt[c][r] = tile (r, c)
@@ -471,11 +484,16 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NW * 32, NW == 4 ? 
     for (int t = 0; t < tasks; ++t) {
       if (i > 0) {
         const int need = (i - 1) * 65536 + (HALF ? min(2 * t + 3, 2 * prev_tasks) : 2 * min(t + 2, prev_tasks));
-        if (lane == 0)
-          while (*pflag < need) __nanosleep(g_spin_ns);
-        __syncwarp();
-        if constexpr (CL > 1) __threadfence();
-        else __threadfence_block();
+        if constexpr (CL > 1) {
+          if (lane == 0)
+            while (ld_acquire_cluster(pflag) < need) __nanosleep(g_spin_ns);
+          __syncwarp();
+        } else {
+          if (lane == 0)
+            while (*pflag < need) __nanosleep(g_spin_ns);
+          __syncwarp();
+          __threadfence_block();
+        }
       }
       const int s = i + 1 + t * BWc;
       const int len = min(BWc, S - s);
@@ -539,17 +557,26 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NW * 32, NW == 4 ? 
       }
       if constexpr (HALF) {
         // D part done: publish, then wait for the B part of task t + 1 of the previous sweep
-        if constexpr (CL > 1) __threadfence();
-        else __threadfence_block();
-        __syncwarp();
-        if (lane == 0) prog[warp] = i * 65536 + 2 * t + 1;
+        if constexpr (CL > 1) {
+          __syncwarp();
+          if (lane == 0) st_release_cluster(&prog[warp], i * 65536 + 2 * t + 1);
+        } else {
+          __threadfence_block();
+          __syncwarp();
+          if (lane == 0) prog[warp] = i * 65536 + 2 * t + 1;
+        }
         if (i > 0 && lb > 0) {
           const int need = (i - 1) * 65536 + min(2 * t + 4, 2 * prev_tasks);
-          if (lane == 0)
-            while (*pflag < need) __nanosleep(g_spin_ns);
-          __syncwarp();
-          if constexpr (CL > 1) __threadfence();
-          else __threadfence_block();
+          if constexpr (CL > 1) {
+            if (lane == 0)
+              while (ld_acquire_cluster(pflag) < need) __nanosleep(g_spin_ns);
+            __syncwarp();
+          } else {
+            if (lane == 0)
+              while (*pflag < need) __nanosleep(g_spin_ns);
+            __syncwarp();
+            __threadfence_block();
+          }
         }
       }
       if (lb > 0) {
@@ -614,10 +641,14 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(NW * 32, NW == 4 ? 
         vr = vpr;
         tau = hp.tau;
       }
-      if constexpr (CL > 1) __threadfence();
-      else __threadfence_block();
-      __syncwarp();
-      if (lane == 0) prog[warp] = i * 65536 + 2 * t + 2;
+      if constexpr (CL > 1) {
+        __syncwarp();
+        if (lane == 0) st_release_cluster(&prog[warp], i * 65536 + 2 * t + 2);
+      } else {
+        __threadfence_block();
+        __syncwarp();
+        if (lane == 0) prog[warp] = i * 65536 + 2 * t + 2;
+      }
     }
   }
   if constexpr (CL > 1) {
