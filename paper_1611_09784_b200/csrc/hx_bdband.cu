@@ -679,7 +679,9 @@ static int bd_reduce_gram(double2* ws2, const BdWs& L, int64_t cnt, const int* d
   // compact lower band (64 doubles per column) + register-row chase; launch shapes as the bidiagonal chase
   const size_t bo = 2 * L.band_off, to = 2 * L.tgk_off;
   sym_band_extract_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, sd, c0, bo, S);
-  const int cap = (int)opt("HX_CHASE_CAP", 5);
+  // no shared-memory padding (occupancy cap) here: 4 CTAs / SM by registers, and the smaller carve-out leaves more
+  // L1 (c2 step 40.4 -> 39.8 ms); HX_SYM_CAP = n pads to n CTAs / SM
+  const int cap = (int)opt("HX_SYM_CAP", 0);
   const int rnw = (int)opt("HX_CHASE_RNW", -1);
   const int rcl_env = (int)opt("HX_CHASE_RCL", -1);
   int rcl = rcl_env >= 0 ? rcl_env : (S >= 2048 ? 8 : 1);
@@ -704,6 +706,8 @@ static int bd_reduce_gram(double2* ws2, const BdWs& L, int64_t cnt, const int* d
   else if (want >= 6 && rcl == 8) SYM_CHASE_CL(8);
   else if (want >= 6 && opt("HX_SYM_BIGNW", 8) == 16) SYM_CHASE_R(16);
   else if (want >= 6) SYM_CHASE_R(8);
+  else if (want >= 2 && opt("HX_SYM_SMALLNW", 4) == 2) SYM_CHASE_R(2);
+  else if (want >= 2 && opt("HX_SYM_SMALLNW", 4) == 8) SYM_CHASE_R(8);
   else if (want >= 2) SYM_CHASE_R(4);
   else SYM_CHASE_R(1);
 #undef SYM_CHASE_R
