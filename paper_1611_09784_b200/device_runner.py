@@ -223,50 +223,76 @@ class DeviceMlmc:
         others.  Each solve is deterministic, so the results do not depend on the schedule.  Returns the
         per-level (mean, var) on the current stream (exact fixed-point moments, combined over the ranks)."""
         main = self.stream
-        jobs = []  # (input index, n, uniq slice of this rank, inv, cuts)
+        # (input index, n, words) of every (level, tier) solve
+        specs = []
         for i, inp in enumerate(inputs):
             if inp.M == 0:
                 continue
             for n, words in ((inp.n, inp.parent), (inp.n // 2, inp.quarters)):
-                if words is None:
-                    continue
-                u, inv = torch.unique(words, dim=0, return_inverse=True)
-                a, b, cuts = (0, u.shape[0], None) if self.mode == "replicas" else self._split(n, u)
-                jobs.append((i, n, u[a:b].contiguous(), inv, cuts))
-        start = torch.cuda.Event()
-        start.record(main)
-        outs = [None] * len(jobs)
+                if words is not None:
+                    specs.append((i, n, words))
+
+        def dedup(n, words):
+            u, inv = torch.unique(words, dim=0, return_inverse=True)
+            a, b, cuts = (0, u.shape[0], None) if self.mode == "replicas" else self._split(n, u)
+            return u[a:b].contiguous(), inv, cuts
+
+        jobs = [None] * len(specs)  # (input index, n, uniq slice of this rank, inv, cuts)
+        outs = [None] * len(specs)
         self.statuses = []
-        # HX_MERGE_TIERS=1: the jobs of one tier (the same n) from different levels go to ONE batch call
-        # (curves are batch independent, so only the packing of the GPU changes)
-        groups = {}
-        for j, (_, n, _, _, _) in enumerate(jobs):
-            groups.setdefault(n if _MERGE_TIERS else (n, j), []).append(j)
         # largest tier first (lane 0 = high priority)
-        order = sorted(groups, key=lambda key: -self.cell(jobs[groups[key][0]][1]).dim)
-        for lane, key in enumerate(order):
-            js = groups[key]
-            n = jobs[js[0]][1]
-            uniq = jobs[js[0]][2] if len(js) == 1 else torch.cat([jobs[j][2] for j in js]).contiguous()
-            # HX_LANES = L > 1 (default 3): the largest tier keeps lane 0, the others share lanes 1 .. L-1 round-robin
-            # (tiers on one lane run one after another); 0: one lane per tier.  Measured on c2 (7 tiers): 7 lanes
-            # 41.5 ms, 3 lanes 40.5 ms, 2 lanes 43.0 ms - the throughput-bound small tiers gain nothing from
-            # running beside each other, and fewer co-resident kernels leave more L2 / issue slots per kernel
-            if _LANE_MAP:
-                lane = _LANE_MAP[min(lane, len(_LANE_MAP) - 1)]
-            elif _LANES > 1 and lane > 0:
-                lane = 1 + (lane - 1) % (_LANES - 1)
-            ctx, stream = self._lane(lane) if concurrent else (self.ctx, main)
-            stream.wait_event(start)
-            curves, status = self._solve(n, uniq, ctx, stream)
-            done = torch.cuda.Event()
-            done.record(stream)
-            off = 0
-            for j in js:
-                cnt = jobs[j][2].shape[0]
-                outs[j] = (curves[off: off + cnt], done)
-                off += cnt
-            self.statuses.append(status)
+        by_size = sorted(range(len(specs)), key=lambda j: -self.cell(specs[j][1]).dim)
+        if not _MERGE_TIERS:
+            # every tier is deduplicated (main stream) and submitted (its lane) in turn, largest first: the largest
+            # tier is on the GPU after its own torch.unique instead of after all of them (~1 ms of a c2 step)
+            for lane, j in enumerate(by_size):
+                i, n, words = specs[j]
+                uniq, inv, cuts = dedup(n, words)
+                jobs[j] = (i, n, uniq, inv, cuts)
+                ready = torch.cuda.Event()
+                ready.record(main)
+                # HX_LANES = L > 1 (default 3): the largest tier keeps lane 0, the others share lanes 1 .. L-1
+                # round-robin (tiers on one lane run one after another); 0: one lane per tier.  Measured on c2
+                # (7 tiers): 7 lanes 41.5 ms, 3 lanes 40.5 ms, 2 lanes 43.0 ms - the throughput-bound small tiers
+                # gain nothing from running beside each other, and fewer co-resident kernels leave more L2 /
+                # issue slots per kernel
+                if _LANE_MAP:
+                    lane = _LANE_MAP[min(lane, len(_LANE_MAP) - 1)]
+                elif _LANES > 1 and lane > 0:
+                    lane = 1 + (lane - 1) % (_LANES - 1)
+                ctx, stream = self._lane(lane) if concurrent else (self.ctx, main)
+                stream.wait_event(ready)
+                curves, status = self._solve(n, uniq, ctx, stream)
+                done = torch.cuda.Event()
+                done.record(stream)
+                outs[j] = (curves, done)
+                self.statuses.append(status)
+        else:
+            # HX_MERGE_TIERS=1: the jobs of one tier (the same n) from different levels go to ONE batch call
+            # (curves are batch independent, so only the packing of the GPU changes)
+            for j, (i, n, words) in enumerate(specs):
+                jobs[j] = (i, n) + dedup(n, words)
+            start = torch.cuda.Event()
+            start.record(main)
+            groups = {}
+            for j, (_, n, _, _, _) in enumerate(jobs):
+                groups.setdefault(n, []).append(j)
+            order = sorted(groups, key=lambda key: -self.cell(key).dim)
+            for lane, key in enumerate(order):
+                js = groups[key]
+                n = jobs[js[0]][1]
+                uniq = jobs[js[0]][2] if len(js) == 1 else torch.cat([jobs[j][2] for j in js]).contiguous()
+                ctx, stream = self._lane(lane) if concurrent else (self.ctx, main)
+                stream.wait_event(start)
+                curves, status = self._solve(n, uniq, ctx, stream)
+                done = torch.cuda.Event()
+                done.record(stream)
+                off = 0
+                for j in js:
+                    cnt = jobs[j][2].shape[0]
+                    outs[j] = (curves[off: off + cnt], done)
+                    off += cnt
+                self.statuses.append(status)
         for _, done in outs:  # every lane joins the main stream before its outputs are used or released
             main.wait_event(done)
         allreduce = self._allreduce()

@@ -1,7 +1,6 @@
 #!/bin/bash
 set -x
 cd $GRAFT_REPO_ROOT
-for r in 1 2; do
-timeout 300 python bench.py --no-e2e --no-cpu-baseline --steps 10 > gpurun_out/bench_capd$r.json 2> gpurun_out/bench_capd$r.err
-HX_SYM_CAP=5 timeout 300 python bench.py --no-e2e --no-cpu-baseline --steps 10 > gpurun_out/bench_cap5$r.json 2> gpurun_out/bench_cap5$r.err
-done
+timeout 900 python -m pytest tests/test_device_pipeline_gpu.py tests/test_multirank_gpu.py -q -x > gpurun_out/gputest_dp.log 2>&1; echo "pytest exit $?" >> gpurun_out/gputest_dp.log
+python tools/timeline.py --config c2 > gpurun_out/timeline_c2_il.txt 2>&1
+timeout 300 python bench.py --no-cpu-baseline --steps 10 > gpurun_out/bench_il.json 2> gpurun_out/bench_il.err
