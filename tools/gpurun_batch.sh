@@ -1,6 +1,9 @@
 #!/bin/bash
 set -x
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_device_pipeline_gpu.py tests/test_multirank_gpu.py -q -x > gpurun_out/gputest_dp.log 2>&1; echo "pytest exit $?" >> gpurun_out/gputest_dp.log
-python tools/timeline.py --config c2 > gpurun_out/timeline_c2_il.txt 2>&1
-timeout 300 python bench.py --no-cpu-baseline --steps 10 > gpurun_out/bench_il.json 2> gpurun_out/bench_il.err
+i=0
+for M in 0,1,2,1,2,0,0 0,1,2,0,1,2,0 0,1,2,0,1,2,1 0,1,2,1,2,0,1 0,1,2,3,3,0,1 0,1,2,0,1,0,1; do
+i=$((i+1))
+HX_LANE_MAP=$M python tools/timeline.py --config c2 > gpurun_out/timeline_c2_M$i.txt 2>&1
+echo $M >> gpurun_out/timeline_c2_M$i.txt
+done
