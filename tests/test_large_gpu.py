@@ -83,3 +83,8 @@ def test_nu46_defected_matches_oracle_on_the_large_real_path():
     assert np.max(np.abs(eigs[0, :, :d] - ref)) <= 1e-10 * (ref.max() - ref.min())
     rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), LO, HI, NPTS, 0.01, ocell.area)
     np.testing.assert_allclose(curves[0], rc, rtol=0, atol=1e-9)
+    # the IDOS-only call takes the Gram path (G = C^T C, lower-tile rank-2k update, 4-SM clustered symmetric chase
+    # with release / acquire half-task counters, 8-lane multisection in mu = sigma^2): same oracle, same tolerance
+    fast, _, st = eval_batch(cell, kp, words, LO, (HI - LO) / (NPTS - 1), NPTS, 0.01)
+    assert (st == 0).all()
+    np.testing.assert_allclose(fast[0], rc, rtol=0, atol=1e-9)

@@ -78,20 +78,26 @@ def test_real_chase_warp_variants_forced(rnw, reg):
 
 
 # ---- the variants the c2 batch sizes select by themselves ----------------------------------------------------
-def test_real_chase_padded_nw4_at_bench_batch():
-    """c2 level 3 / level-4 quarters: 256 masks x 4 k = 1024 N = 512 matrices -> want = 2: the 4-warp chase with
-    padded shared memory (5 CTAs / SM).  8 masks spread over the batch are checked."""
-    check_batch("graphene", 16, 2, 0.05, 256, 2026, (0, 37, 101, 128, 170, 201, 240, 255), eigs_too=False)
+@pytest.mark.parametrize("gram", [1, 0])
+def test_real_chase_padded_nw4_at_bench_batch(gram):
+    """c2 level 3 / level-4 quarters: 256 masks x 4 k = 1024 N = 512 matrices -> want = 2: the 4-warp chase at
+    4-5 CTAs / SM - the symmetric chase of the Gram path (default for IDOS-only batches) and the bidiagonal chase of
+    the SVD path (HX_GRAM=0).  8 masks spread over the batch are checked against the oracle."""
+    check_batch("graphene", 16, 2, 0.05, 256, 2026, (0, 37, 101, 128, 170, 201, 240, 255), eigs_too=False,
+                opts={"HX_GRAM": gram})
 
 
-def test_real_chase_nw1_at_large_batch():
+@pytest.mark.parametrize("gram", [1, 0])
+def test_real_chase_nw1_at_large_batch(gram):
     """>= 1628 matrices -> want = 1: one warp per matrix (c5 n = 512 batches)."""
-    check_batch("graphene", 16, 2, 0.05, 420, 7, (0, 211, 419), eigs_too=False)
+    check_batch("graphene", 16, 2, 0.05, 420, 7, (0, 211, 419), eigs_too=False, opts={"HX_GRAM": gram})
 
 
-def test_c2_level4_parent_batch():
-    """c2 level 4: 64 nu = 32 masks at Gamma (N = 2048, S = 1024) in one batch - the 16-warp real chase."""
-    check_batch("graphene", 32, 1, 0.05, 64, 2026, (0, 33, 63), eigs_too=False)
+@pytest.mark.parametrize("gram", [1, 0])
+def test_c2_level4_parent_batch(gram):
+    """c2 level 4: 64 nu = 32 masks at Gamma (N = 2048, S = 1024) in one batch - the 8-warp chase (Gram path:
+    half-task progress counters; SVD path: register-row bidiagonal chase)."""
+    check_batch("graphene", 32, 1, 0.05, 64, 2026, (0, 33, 63), eigs_too=False, opts={"HX_GRAM": gram})
 
 
 def test_clustered_real_chase_two_sms():
