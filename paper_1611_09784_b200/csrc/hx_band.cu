@@ -670,6 +670,16 @@ static int band_reduce(double2* ws, const BandWs& L, int N, int64_t cnt, const i
   return 0;
 }
 
+HermSlab herm_slab(int n) {
+  const BandWs L = BandWs::make(n);
+  // scratch: the V and X panels (adjacent, n x 64 double2), free until the first panel QR
+  return HermSlab{L.a_off, L.v_off, (size_t)2 * n * BW, L.dg_off, L.stride};
+}
+
+int herm_reduce(double2* ws, int n, int64_t cnt, const int* dims, cudaStream_t st) {
+  return band_reduce(ws, BandWs::make(n), n, cnt, dims, st);
+}
+
 int band_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, int64_t nmasks, const GridDev& g,
               int* diff, unsigned long long* trans, double* eigs, int* status, int sharp, size_t ws_budget,
               const Alloc& alloc, cudaStream_t st, RefineItem* refine, unsigned long long* refine_count) {

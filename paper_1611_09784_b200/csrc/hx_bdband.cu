@@ -222,6 +222,105 @@ __global__ void __launch_bounds__(256) gram_assemble_kernel(CellDev c, const dou
   if (tid == 0 && over) status[mat] = 2;  // HX_ST_NONFINITE: surfaces as an error, never silently
 }
 
+// Complex Gram assembly (non-time-reversal-invariant k): G = C^H C (Hermitian, S x S double2, both triangles) in
+// the Hermitian tier's slab, from the sparse rows and columns of the complex block C.  dims_t = nA + nB (the
+// dimension of T for the counts), dims_g = nB (the leading nonzero block of G); the tridiagonal output region is
+// zeroed (the chase writes its first dims_g entries only).
+__global__ void __launch_bounds__(256) gram_assemble_c_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
+                                                              const uint64_t* __restrict__ masks, int64_t mat0,
+                                                              double2* ws, HermSlab H, int S, int* dims_t, int* dims_g,
+                                                              int* status) {
+  extern __shared__ int bsm[];
+  int* idx_a = bsm;
+  int* idx_b = idx_a + c.N;
+  int* cnt = idx_b + c.N;
+  __shared__ int over;
+  const int64_t mat = mat0 + blockIdx.x;
+  const int64_t mk = mat / nk;
+  const double2 k = kpts[(int)(mat - mk * nk)];
+  const int tid = threadIdx.x;
+  double2* base = ws + (size_t)blockIdx.x * H.stride;
+  double2* G = base + H.a_off;
+  double2* colVal = base + H.scratch_off;                             // [S][GRAM_K]
+  double2* rowVal = colVal + (size_t)S * GRAM_K;                      // [S][GRAM_K]
+  int* colIdx = reinterpret_cast<int*>(rowVal + (size_t)S * GRAM_K);  // [S][GRAM_K]
+  int* rowIdx = colIdx + (size_t)S * GRAM_K;                          // [S][GRAM_K]
+  int* colCnt = rowIdx + (size_t)S * GRAM_K;                          // [S]
+  int* rowCnt = colCnt + S;                                           // [S]
+  if (tid == 0) over = 0;
+  const int2 nn = block_compact_bipartite(c, masks + mk * c.words, idx_a, idx_b, cnt);
+  const int d = nn.x + nn.y;
+  if (tid == 0) {
+    dims_t[blockIdx.x] = d;
+    dims_g[blockIdx.x] = nn.y;
+    status[mat] = d == 0 ? 3 : 0;
+  }
+  const double2 zero = make_double2(0.0, 0.0);
+  for (size_t p = tid; p < (size_t)S * S; p += blockDim.x) G[p] = zero;
+  {
+    double* dg = reinterpret_cast<double*>(base + H.dg_off);
+    for (int i = tid; i < 2 * S; i += blockDim.x) dg[i] = 0.0;
+  }
+  for (int i = tid; i < S; i += blockDim.x) {
+    colCnt[i] = 0;
+    rowCnt[i] = 0;
+  }
+  __syncthreads();
+  for (int r = tid; r < c.N; r += blockDim.x) {
+    const int ia = idx_a[r], jb = idx_b[r];
+    if (ia >= 0) {
+      int n = 0;
+      for_each_partner(c, r, [&](int cb) {
+        const int j = idx_b[cb];
+        if (j < 0) return;
+        if (n < GRAM_K) {
+          rowIdx[(size_t)ia * GRAM_K + n] = j;
+          rowVal[(size_t)ia * GRAM_K + n] = herm_element(c.h_ptr, c.h_col, c.h_amp, c.h_disp, r, cb, k);
+        } else {
+          over = 1;
+        }
+        ++n;
+      });
+      rowCnt[ia] = min(n, GRAM_K);
+    } else if (jb >= 0) {
+      int n = 0;
+      for_each_partner(c, r, [&](int ca) {
+        const int i = idx_a[ca];
+        if (i < 0) return;
+        if (n < GRAM_K) {
+          colIdx[(size_t)jb * GRAM_K + n] = i;
+          colVal[(size_t)jb * GRAM_K + n] = herm_element(c.h_ptr, c.h_col, c.h_amp, c.h_disp, ca, r, k);
+        } else {
+          over = 1;
+        }
+        ++n;
+      });
+      colCnt[jb] = min(n, GRAM_K);
+    }
+  }
+  __syncthreads();
+  // G[kk][j] = sum_i conj(C_i,kk) C_ij, one thread per column j (fixed order: deterministic)
+  for (int j = tid; j < S; j += blockDim.x) {
+    double2* Gj = G + (size_t)j * S;
+    const int nc = colCnt[j];
+    for (int a = 0; a < nc; ++a) {
+      const int i = colIdx[(size_t)j * GRAM_K + a];
+      const double2 cij = colVal[(size_t)j * GRAM_K + a];
+      const int nr = rowCnt[i];
+      for (int b = 0; b < nr; ++b) {
+        const int kk = rowIdx[(size_t)i * GRAM_K + b];
+        const double2 cik = rowVal[(size_t)i * GRAM_K + b];
+        double2 acc = Gj[kk];
+        acc.x = fma(cik.x, cij.x, fma(cik.y, cij.y, acc.x));
+        acc.y = fma(cik.x, cij.y, fma(-cik.y, cij.x, acc.y));
+        if (kk == j) acc.y = 0.0;
+        Gj[kk] = acc;
+      }
+    }
+  }
+  if (tid == 0 && over) status[mat] = 2;  // HX_ST_NONFINITE: surfaces as an error, never silently
+}
+
 // ------------------------------------------------------------------------------------------------
 bool launch_cluster_panel(double2* ws, const PanelArgs& a, int64_t cnt, cudaStream_t st);
 
@@ -750,6 +849,7 @@ void bd_init_attributes() {
   set_smem_attr(xv_kernel<1, false, true>, (int)XV_SMEM);
   set_smem_attr(bd_assemble_kernel, 140 * 1024);
   set_smem_attr(gram_assemble_kernel, 140 * 1024);
+  set_smem_attr(gram_assemble_c_kernel, 140 * 1024);
   set_smem_attr(rank_update_real_kernel<64, true>, (int)rru_smem<64, true>());
 #define BD_CHASE_ATTR(NW, DUAL, CL)                                                                        \
   set_smem_attr(bd_chase_kernel<NW, BB, DUAL, CL>, bd_chase_smem<NW, BB, DUAL>())
@@ -796,9 +896,47 @@ int bd_eval(const CellDev& c, const double2* kp, int nk, const uint64_t* masks, 
             size_t ws_budget, const Alloc& alloc, cudaStream_t st, RefineItem* refine,
             unsigned long long* refine_count) {
   const int S = c.nsub;
+  const int64_t nmat = nmasks * nk;
+  // Complex Gram path (HX_GRAM_C, default on): IDOS-only batches at k-points that are not time-reversal invariant,
+  // zones clear of lambda = 0: G = C^H C (Hermitian) through the Hermitian banded tier (panel QR, 3M xv, her2k,
+  // register-row chase) - half the flops of bidiagonalising C - and the mu = sigma^2 eigenvalue stage
+  {
+    CellDev cgc = c;
+    cgc.N = S;
+    if (!real && !eigs && refine && refine_count && opt("HX_GRAM_C", 1) != 0 && S > 80 &&
+        gram_zones_ok(cgc, g, sharp, 1e-3)) {
+      const HermSlab H = herm_slab(S);
+      const size_t perg = H.stride * sizeof(double2) + 2 * sizeof(int);
+      int64_t chunk = std::max<int64_t>(1, (int64_t)(ws_budget / perg));
+      chunk = std::min<int64_t>(std::min<int64_t>(chunk, nmat), 65535);
+      unsigned char* buf = static_cast<unsigned char*>(alloc(perg * (size_t)chunk + 256));
+      if (!buf) {
+        g_bd_err = "workspace allocation failed";
+        return -1;
+      }
+      double2* ws = reinterpret_cast<double2*>(buf);
+      int* dims_t = reinterpret_cast<int*>(buf + H.stride * sizeof(double2) * chunk);
+      int* dims_g = dims_t + chunk;
+      const size_t smem = (size_t)c.N * 8 + 2 * ((c.N + 31) / 32) * 4 + 64;
+      for (int64_t m0 = 0; m0 < nmat; m0 += chunk) {
+        const int64_t cnt = std::min(chunk, nmat - m0);
+        gram_assemble_c_kernel<<<(unsigned)cnt, 256, smem, st>>>(c, kp, nk, masks, m0, ws, H, S, dims_t, dims_g,
+                                                                 status);
+        count_launch();
+        BD_CUDA(cudaGetLastError());
+        if (herm_reduce(ws, S, cnt, dims_g, st)) {
+          g_bd_err = std::string("Hermitian reduction of the Gram matrix: ") + band_last_error();
+          return -1;
+        }
+        launch_gram_idos(cgc, nk, g, m0, cnt, reinterpret_cast<const double*>(ws + H.dg_off), H.stride * 2, dims_t,
+                         diff, trans, status, sharp, st, refine, refine_count);
+        BD_CUDA(cudaGetLastError());
+      }
+      return 0;
+    }
+  }
   const BdWs L = BdWs::make(S);
   const size_t per = L.stride * sizeof(double2) + sizeof(int);
-  const int64_t nmat = nmasks * nk;
   const bool real_s1 = real && bd_real_stage1() && bd_chase_real() && S % 4 == 0;
   int64_t chunk = std::max<int64_t>(1, (int64_t)(ws_budget / per));
   chunk = std::min<int64_t>(std::min<int64_t>(chunk, nmat), 65535);

@@ -413,3 +413,38 @@ def test_gram_chase_bitwise_repeatable(opts):
             if th:
                 th.join()
             assert np.array_equal(cur, ref), rep
+
+
+# ---- complex Gram path: G = C^H C through the Hermitian banded tier (non-time-reversal-invariant k-points) ------
+@pytest.mark.parametrize("nu,q,count,p", [(12, 3, 4, 0.05), (16, 4, 3, 0.05), (10, 3, 6, 0.08), (24, 3, 2, 0.05),
+                                          (14, 5, 3, 0.3)])
+def test_complex_gram_path_vs_svd_path_and_oracle(nu, q, count, p):
+    """IDOS-only batches with complex k-points (q >= 3) and N > 160: the default (HX_GRAM_C=1) forms G = C^H C and
+    runs the Hermitian two-stage reduction; it equals the complex bidiagonal path (HX_GRAM_C=0) to rounding and the
+    oracle (zhegv) within the north-star tolerance, also with many vacancies (nA != nB, zero modes)."""
+    _, om, sc, cell, kp = _setup("graphene", nu, q)
+    step = (HI_G - LO_G) / (NPTS - 1)
+    words = sample_masks(sc.nunits, p, 41, 2, 0, count)
+    with _lib.options(HX_GRAM_C=1):
+        gram, _, st1 = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
+    with _lib.options(HX_GRAM_C=0):
+        svd, _, st0 = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
+    assert (st1 == 0).all() and (st0 == 0).all()
+    np.testing.assert_allclose(gram, svd, rtol=0, atol=1e-11)
+    ocell = O.make_cell(om, nu)
+    for m in (0, count - 1):
+        ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
+        rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), LO_G, HI_G, NPTS, 0.01, ocell.area)
+        np.testing.assert_allclose(gram[m], rc, rtol=0, atol=IDOS_TOL)
+
+
+def test_complex_gram_path_all_vacant_and_repeatable():
+    _, om, sc, cell, kp = _setup("graphene", 12, 3)
+    step = (HI_G - LO_G) / (NPTS - 1)
+    words = sample_masks(sc.nunits, 0.05, 8, 1, 0, 3)
+    words[2] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    with _lib.options(HX_GRAM_C=1):
+        a, _, st = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
+        b, _, _ = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
+    assert (st[:2] == 0).all() and (st[2] == _lib.HX_ST_EMPTY).all()
+    assert np.all(a[2] == 0.0) and np.array_equal(a, b)
