@@ -301,6 +301,8 @@ int hx_ctx_create_priority(int32_t device, int32_t priority, hx_ctx** out) {
   hx::set_smem_attr(hx::small_bidiag_kernel, 200 * 1024);
   hx::set_smem_attr(hx::small_bidiag_reg_kernel, (int)hx::small_bidiag_reg_smem(128, 64));
   hx::set_smem_attr(hx::small_bidiag_reg_real_kernel, (int)hx::small_bidiag_reg_real_smem(128, 64));
+  hx::set_smem_attr(hx::small_gram_reg_kernel, (int)hx::small_gram_reg_smem(128, 64, false));
+  hx::set_smem_attr(hx::small_gram_reg_real_kernel, (int)hx::small_gram_reg_smem(128, 64, true));
   ctx->ws_budget = std::min(ctx->ws_budget, freeb / 3);
   ctx->ws_budget_default = ctx->ws_budget;
   refresh_opts(ctx);
@@ -526,6 +528,38 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
       if (m0 % nk) return fail(HX_E_ARG, "internal: chunk not aligned to k-point groups");
       const uint64_t* mk0 = d_masks + (m0 / nk) * c.words;
       const bool tgk = c.bipartite && ctx->use_bipartite && hx::small_bidiag_smem(N, c.nsub) <= 200 * 1024;
+      // Gram path of the S in (32, 64] tiers (hx_smallgram.cuh; HX_SMALL_GRAM=0: Golub-Kahan): IDOS only, graphene
+      // pencil, zone path of the eigenvalue stage applicable and every transition zone clear of lambda = 0
+      hx::CellDev cs = c;
+      cs.N = c.nsub;
+      const bool small_gram = tgk && !d_eigs && refine && refine_count && c.pencil == 1 && c.nsub > 32 &&
+                              c.nsub <= 64 && c.nsub > ctx->bidiag_warp_max_s && ctx->bidiag_reg &&
+                              hx::opt("HX_SMALL_GRAM", 1) != 0 && N >= hx::opt("HX_ZONE_MIN_N", 96) &&
+                              hx::gram_zones_ok(cs, g, sharp, 1e-3);
+      if (small_gram) {
+        const int nkc = (int)klist_c.size(), nkr = (int)klist_r.size();
+        const int64_t nm = cnt / nk;
+        const size_t sm_c = hx::small_gram_reg_smem(N, c.nsub, false), sm_r = hx::small_gram_reg_smem(N, c.nsub, true);
+        if (nkr == 0) {
+          hx::small_gram_reg_kernel<<<(unsigned)cnt, hx::BIDIAG_REG_THREADS, sm_c, st>>>(c, kp, nk, mk0, tri, dims,
+                                                                                        status + m0, nullptr, nk);
+        } else {
+          if (nkc > 0) {
+            hx::small_gram_reg_kernel<<<(unsigned)(nm * nkc), hx::BIDIAG_REG_THREADS, sm_c, st>>>(
+                c, kp, nk, mk0, tri, dims, status + m0, d_klist_c, nkc);
+            hx::count_launch();
+          }
+          hx::small_gram_reg_real_kernel<<<(unsigned)(nm * nkr), hx::BIDIAG_REG_THREADS, sm_r, st>>>(
+              c, kp, nk, mk0, tri, dims, status + m0, d_klist_r, nkr);
+        }
+        HX_CUDA(cudaGetLastError());
+        hx::count_launch();
+        if (!hx::launch_gram_idos(cs, nk, g, m0, cnt, tri, (size_t)2 * N, dims, diff, trans, status, sharp, st, refine,
+                                  refine_count))
+          return fail(HX_E_CUDA, "internal: Gram eigenvalue stage refused a batch gram_zones_ok accepted");
+        HX_CUDA(cudaGetLastError());
+        continue;
+      }
       if (tgk) {
         // one warp per matrix up to S = 32 (latency of the serial reflector chain is hidden by many
         // matrices per SM), a CTA beyond

@@ -18,6 +18,7 @@
 #include "hx_bidiag.cuh"
 #include "hx_dense.cuh"
 #include "hx_kernels.cuh"
+#include "hx_smallgram.cuh"
 
 namespace hx {
 
@@ -173,6 +174,77 @@ __global__ void __launch_bounds__(BIDIAG_REG_THREADS, 3)
   const int rows = transpose ? nn.y : nn.x, cols = transpose ? nn.x : nn.y;
   assemble_bipartite(c, idx_a, idx_b, kpts[kk], nullptr, lm, rows, cols, transpose, true, Mr);
   bidiag_tgk_reg_real(Mr, lm, rows, cols, diag, e2, scratch);
+}
+
+// Gram path of the S in (32, 64] tiers (hx_smallgram.cuh): compaction -> dense C in shared memory -> G = C^H C in
+// registers -> Hermitian tridiagonalisation; output (diag[S], e2[S]) of G padded to S at tri + mat * 2N, read by
+// launch_gram_idos with a cell of N = S.  dims = kept dimension nA + nB as in the TGK kernels.
+template <bool REAL>
+static __device__ __forceinline__ void small_gram_body(const CellDev& c, const double2* __restrict__ kpts, int nk,
+                                                       const uint64_t* __restrict__ masks, double* tri, int* dims,
+                                                       int* status, const int* __restrict__ klist, int nks) {
+  using E = typename SgElem<REAL>::E;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int N = c.N, S = c.nsub;
+  int64_t mk, mat;
+  int kk;
+  if (klist) {
+    mk = blockIdx.x / nks;
+    kk = klist[blockIdx.x - mk * nks];
+    mat = mk * nk + kk;
+  } else {
+    mat = blockIdx.x;
+    mk = mat / nk;
+    kk = (int)(mat - mk * nk);
+  }
+  const int lm = REAL ? bidiag_ld_real(S) : bidiag_ld(S);
+  E* M = reinterpret_cast<E*>(smem_raw);
+  double* scratch = reinterpret_cast<double*>(M + (size_t)lm * S);
+  E* lval = reinterpret_cast<E*>(scratch + sg_scratch_doubles<REAL>());
+  int* lrow = reinterpret_cast<int*>(lval + 64 * SG_NZ);
+  int* flag = lrow + 64 * SG_NZ;
+  int* idx_a = flag + 2;
+  int* idx_b = idx_a + N;
+  int* cnt = idx_b + N;
+  double* diag = tri + mat * 2 * N;
+  double* e2 = diag + S;
+  const int2 nn = block_compact_bipartite(c, masks + mk * c.words, idx_a, idx_b, cnt);
+  const int d = nn.x + nn.y;
+  if (threadIdx.x == 0) {
+    dims[mat] = d;
+    status[mat] = d == 0 ? 3 : 0;
+  }
+  if (d == 0) return;
+  const bool transpose = nn.x < nn.y;
+  const int rows = transpose ? nn.y : nn.x, cols = transpose ? nn.x : nn.y;
+  if constexpr (REAL)
+    assemble_bipartite(c, idx_a, idx_b, kpts[kk], nullptr, lm, rows, cols, transpose, true, M);
+  else
+    assemble_bipartite(c, idx_a, idx_b, kpts[kk], M, lm, rows, cols, transpose);
+  if (!small_gram_tridiag<REAL>(M, lm, rows, cols, S, diag, e2, scratch, lrow, lval, flag) && threadIdx.x == 0) {
+    dims[mat] = 0;
+    status[mat] = 2;  // not a nearest-neighbour block: the host never routes such a model here
+  }
+}
+
+__global__ void __launch_bounds__(BIDIAG_REG_THREADS, 2)
+    small_gram_reg_kernel(CellDev c, const double2* __restrict__ kpts, int nk, const uint64_t* __restrict__ masks,
+                          double* tri, int* dims, int* status, const int* __restrict__ klist, int nks) {
+  small_gram_body<false>(c, kpts, nk, masks, tri, dims, status, klist, nks);
+}
+
+__global__ void __launch_bounds__(BIDIAG_REG_THREADS, 3)
+    small_gram_reg_real_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
+                               const uint64_t* __restrict__ masks, double* tri, int* dims, int* status,
+                               const int* __restrict__ klist, int nks) {
+  small_gram_body<true>(c, kpts, nk, masks, tri, dims, status, klist, nks);
+}
+
+size_t small_gram_reg_smem(int N, int S, bool real) {
+  const size_t es = real ? 8 : 16;
+  const size_t lm = real ? bidiag_ld_real(S) : bidiag_ld(S);
+  return lm * S * es + (size_t)(real ? sg_scratch_doubles<true>() : sg_scratch_doubles<false>()) * 8 +
+         64 * SG_NZ * (es + 4) + 8 + (size_t)N * 8 + 2 * ((N + 31) / 32) * 4 + 16;
 }
 
 size_t small_bidiag_reg_real_smem(int N, int S) {

@@ -41,6 +41,14 @@ __global__ void small_bidiag_reg_real_kernel(CellDev c, const double2* kpts, int
                                              double* tri, int* dims, int* status, const int* klist, int nks);
 size_t small_bidiag_reg_real_smem(int N, int S);
 
+// Gram path of the S in (32, 64] tiers (hx_smallgram.cuh): tridiagonal (diag[S], e2[S]) of G = C^H C per matrix at
+// tri + mat * 2N, for launch_gram_idos with a cell of N = S; klist == NULL: every k-point
+__global__ void small_gram_reg_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, double* tri,
+                                      int* dims, int* status, const int* klist, int nks);
+__global__ void small_gram_reg_real_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks,
+                                           double* tri, int* dims, int* status, const int* klist, int nks);
+size_t small_gram_reg_smem(int N, int S, bool real);
+
 __global__ void global_tridiag_kernel(CellDev c, const double2* kpts, int nk, const uint64_t* masks, int64_t mat0,
                                       unsigned char* ws, size_t ws_stride, double* tri, int* dims, int* status);
 size_t global_ws_stride(int N, bool general);

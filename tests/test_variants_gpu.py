@@ -448,3 +448,50 @@ def test_complex_gram_path_all_vacant_and_repeatable():
         b, _, _ = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
     assert (st[:2] == 0).all() and (st[2] == _lib.HX_ST_EMPTY).all()
     assert np.all(a[2] == 0.0) and np.array_equal(a, b)
+
+
+# ---- Gram path of the shared-memory tier (S in (32, 64]: G = C^H C in registers, hx_smallgram.cuh) ----------
+@pytest.mark.parametrize("nu,q,conc,count", [(8, 4, 0.05, 40), (8, 3, 0.05, 24), (8, 2, 0.05, 24), (7, 5, 0.1, 16),
+                                             (6, 3, 0.1, 16), (5, 4, 0.05, 16), (8, 4, 0.3, 24), (7, 2, 0.25, 16)])
+def test_small_gram_path_vs_golub_kahan_and_oracle(nu, q, conc, count):
+    """N = 50..128 tiers (c2's N = 128 tier is nu = 8, q = 4): the register-resident Hermitian tridiagonalisation of
+    G = C^H C (complex k-points) / C^T C (TRIM k-points) with the mu = sigma^2 zone path (HX_SMALL_GRAM=1, default
+    for IDOS-only calls) equals the Golub-Kahan path (HX_SMALL_GRAM=0) to rounding and the oracle within the
+    north-star tolerance; rectangular / padded blocks at high vacancy counts."""
+    _, om, sc, cell, kp = _setup("graphene", nu, q)
+    step = (HI_G - LO_G) / (NPTS - 1)
+    words = sample_masks(sc.nunits, conc, 91, 2, 0, count)
+    with _lib.options(HX_SMALL_GRAM=1):
+        gram, _, st1 = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
+        again, _, _ = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
+    with _lib.options(HX_SMALL_GRAM=0):
+        gk, _, st0 = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
+    assert (st1 == 0).all() and (st0 == 0).all()
+    assert np.array_equal(gram, again)
+    np.testing.assert_allclose(gram, gk, rtol=0, atol=1e-11)
+    ocell = O.make_cell(om, nu)
+    for m in (0, count // 2, count - 1):
+        ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
+        rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), LO_G, HI_G, NPTS, 0.01, ocell.area)
+        np.testing.assert_allclose(gram[m], rc, rtol=0, atol=IDOS_TOL)
+
+
+def test_small_gram_path_all_vacant_and_single_site():
+    """All-vacant mask (zero curve, HX_ST_EMPTY), a mask that keeps one unit only, and a pristine cell through the
+    small-tier Gram path."""
+    _, om, sc, cell, kp = _setup("graphene", 8, 4)
+    words = sample_masks(sc.nunits, 0.05, 3, 1, 0, 4)
+    words[1] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    words[2] = np.uint64(0xFFFFFFFFFFFFFFFF)
+    words[2, 0] = np.uint64(0xFFFFFFFFFFFFFFFE)
+    words[3] = np.uint64(0)
+    step = (HI_G - LO_G) / (NPTS - 1)
+    with _lib.options(HX_SMALL_GRAM=1):
+        gram, _, st = eval_batch(cell, kp, words, LO_G, step, NPTS, 0.01)
+    assert (st[1] == _lib.HX_ST_EMPTY).all() and np.all(gram[1] == 0.0)
+    assert (st[[0, 2, 3]] == 0).all()
+    ocell = O.make_cell(om, 8)
+    for m in (0, 2, 3):
+        ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
+        rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), LO_G, HI_G, NPTS, 0.01, ocell.area)
+        np.testing.assert_allclose(gram[m], rc, rtol=0, atol=IDOS_TOL)
