@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(BIDIAG_REG_THREADS, 2)
   small_gram_body<false>(c, kpts, nk, masks, tri, dims, status, klist, nks);
 }
 
-__global__ void __launch_bounds__(BIDIAG_REG_THREADS, 3)
+__global__ void __launch_bounds__(BIDIAG_REG_THREADS, 4)
     small_gram_reg_real_kernel(CellDev c, const double2* __restrict__ kpts, int nk,
                                const uint64_t* __restrict__ masks, double* tri, int* dims, int* status,
                                const int* __restrict__ klist, int nks) {

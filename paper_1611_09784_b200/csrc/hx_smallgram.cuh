@@ -22,7 +22,7 @@
 
 namespace hx {
 
-constexpr int SG_NZ = 4;  // nonzeros kept per column of C (graphene: <= 3 neighbours)
+constexpr int SG_NZ = 3;  // nonzeros kept per column of C (honeycomb: <= 3 distinct neighbours)
 
 template <bool REAL>
 struct SgElem {
@@ -211,13 +211,13 @@ static __device__ __forceinline__ void sg_phase(typename SgElem<REAL>::E (&m)[4]
     __syncthreads();  // B: p, dot partials
     {
       const double2* d2 = reinterpret_cast<const double2*>(sc.dbuf);
-      double cdot = 0.0;
+      double cd[4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const double2 x = d2[q];
-        cdot += x.x;
-        cdot += x.y;
+      for (int q = 0; q < 4; ++q) {
+        const double2 x = d2[2 * q], y = d2[2 * q + 1];
+        cd[q] = (x.x + x.y) + (y.x + y.y);
       }
+      const double cdot = (cd[0] + cd[1]) + (cd[2] + cd[3]);
       const double hc = 0.5 * tau * cdot;
       E wr[4], wc[4];
 #pragma unroll
@@ -255,25 +255,47 @@ static __device__ bool small_gram_tridiag(const typename SgElem<REAL>::E* Ms, in
   for (int i = tid; i < 2 * S; i += blockDim.x) diag[i] = 0.0;  // diag and e2 (e2 = diag + S)
   if (tid == 0) *flag = 0;
   __syncthreads();
-  // sparse columns of C
-  if (tid < 64) {
-    int cnt = 0;
-    if (tid < cols)
-      for (int x = 0; x < rows; ++x) {
-        const E val = Ms[x + (size_t)tid * lm];
+  // sparse columns of C: four threads per column (16 rows each), merged in row order (deterministic lists)
+  {
+    const int col = tid & 63, qd = tid >> 6;
+    int cnt = 0, xr[SG_NZ];
+    E xv[SG_NZ];
+#pragma unroll
+    for (int q = 0; q < SG_NZ; ++q) {
+      xr[q] = 0;
+      xv[q] = sg_zero(E{});
+    }
+    if (col < cols) {
+      const int x1 = min(rows, 16 * qd + 16);
+      for (int x = 16 * qd; x < x1; ++x) {
+        const E val = Ms[x + (size_t)col * lm];
         if (sg_nonzero(val)) {
-          if (cnt < SG_NZ) {
-            lrow[tid * SG_NZ + cnt] = x;
-            lval[tid * SG_NZ + cnt] = val;
-          }
+#pragma unroll
+          for (int q = 0; q < SG_NZ; ++q)
+            if (q == cnt) {
+              xr[q] = x;
+              xv[q] = val;
+            }
           ++cnt;
         }
       }
-    if (cnt > SG_NZ) *flag = 1;
-    for (int q = min(cnt, SG_NZ); q < SG_NZ; ++q) {
-      lrow[tid * SG_NZ + q] = 0;
-      lval[tid * SG_NZ + q] = sg_zero(E{});
     }
+    int* qcnt = reinterpret_cast<int*>(scratch);  // [4][64], before the reflector buffers are in use
+    qcnt[qd * 64 + col] = cnt;
+    for (int q = tid; q < 64 * SG_NZ; q += blockDim.x) {
+      lrow[q] = 0;
+      lval[q] = sg_zero(E{});
+    }
+    __syncthreads();
+    int off = 0;
+    for (int q = 0; q < qd; ++q) off += qcnt[q * 64 + col];
+    if (off + cnt > SG_NZ) *flag = 1;
+#pragma unroll
+    for (int q = 0; q < SG_NZ; ++q)
+      if (q < cnt && off + q < SG_NZ) {
+        lrow[col * SG_NZ + off + q] = xr[q];
+        lval[col * SG_NZ + off + q] = xv[q];
+      }
   }
   __syncthreads();
   if (*flag) return false;
