@@ -922,19 +922,32 @@ static bool zone_path_ok(const CellDev& c, const GridDev& g, int sharp, bool& re
 // and the zone eigenvalues are located in mu = sigma^2 (relative accuracy eps in mu = eps/2 in sigma) and mapped
 // to lambda = +-sqrt(mu).  The host uses this mode only when no transition zone comes near lambda = 0, where
 // sigma^2 loses its relative accuracy (gram_zones_ok).
+// fuse != 0 (many-matrix launches, S < 1024): the block also locates its own zone eigenvalues, on a copy of the
+// tridiagonal in shared memory (zone_locate with the arguments zone_refine_gram_kernel would pass: the same bits),
+// instead of handing them to the global refinement list - the list's items of one warp belong to different
+// matrices, so every Sturm row step of zone_refine_gram_kernel was 32 scattered loads (ncu: 10 of 14 stall cycles
+// per issue on the long scoreboard, 9 of 32 lanes active).
+// Dynamic shared memory: fuse: [2 S] doubles (diag, e2), then ints: [2 npts] T counts at the zone edges,
+// [2 npts] Gram counts, fuse: [npts + 1] item offsets, [2 S] items.
 __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk, GridDev g, int sharp, int rev,
                                                               int64_t mat0, int64_t nmat, const double* __restrict__ tri,
                                                               size_t tri_stride, const int* __restrict__ dims,
                                                               int* diff, RefineItem* refine,
-                                                              unsigned long long* refine_count) {
-  extern __shared__ int zc[];  // [2 npts] T counts at the zone edges, then [2 npts] Gram counts
+                                                              unsigned long long* refine_count, int fuse,
+                                                              unsigned long long* trans, int* status) {
+  extern __shared__ __align__(16) unsigned char zraw[];
   __shared__ double red[3][32];
+  __shared__ int wsum[8];
   const int64_t lm = blockIdx.x;
   if (lm >= nmat) return;
   const int d = dims[lm];
   if (d <= 0) return;
   const int S = c.N, npts = g.npts;
+  double* sd = reinterpret_cast<double*>(zraw);
+  int* zc = reinterpret_cast<int*>(zraw + (fuse ? (size_t)2 * S * sizeof(double) : 0));
   int* zg = zc + 2 * npts;
+  int* zoff = zg + 2 * npts;     // fuse only
+  int* ilist = zoff + npts + 1;  // fuse only
   const int64_t mat = mat0 + lm;
   const int64_t mk = mat / nk;
   const double* diag = tri + lm * tri_stride;
@@ -948,6 +961,10 @@ __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk,
     gl = fmin(gl, diag[i] - el - er);
     gu = fmax(gu, diag[i] + el + er);
     em = fmax(em, er2);
+    if (fuse) {
+      sd[i] = diag[i];
+      sd[S + i] = e2[i];
+    }
   }
   gl = warp_min(gl);
   gu = warp_max(gu);
@@ -970,6 +987,8 @@ __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk,
   const double tnorm = fmax(fabs(gl), fabs(gu));
   gl = gl - 2.1 * tnorm * DBL_EPSILON * S - 4.2 * pivmin;
   gu = gu + 2.1 * tnorm * DBL_EPSILON * S + 4.2 * pivmin;
+  const double* cd = fuse ? sd : diag;
+  const double* ce2 = fuse ? sd + S : e2;
   for (int m = tid; m < npts; m += blockDim.x) {
     double la, lb;
     zone_bracket(c, g, sharp, m, la, lb);
@@ -979,7 +998,7 @@ __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk,
     int ca = xa <= gl ? 0 : S, cb = xb <= gl ? 0 : S;
     if (ra || rb) {
       int na, nb;
-      sturm_count_pair<false>(diag, e2, S, xa, xb, pivmin, na, nb);
+      sturm_count_pair<false>(cd, ce2, S, xa, xb, pivmin, na, nb);
       if (ra) ca = na;
       if (rb) cb = nb;
     }
@@ -991,6 +1010,28 @@ __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk,
   }
   __syncthreads();
   int* drow = diff + mk * (npts + 1);
+  if (fuse) {
+    // item offsets: block-wide exclusive scan of the zone item counts (one zone per thread and round)
+    int carry = 0;
+    for (int m0 = 0; m0 < npts; m0 += blockDim.x) {
+      const int m = m0 + tid;
+      const int nz = m < npts ? zg[2 * m + 1] - zg[2 * m] : 0;
+      int incl = nz;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) wsum[warp] = incl;
+      __syncthreads();
+      int before = carry;
+      for (int w = 0; w < warp; ++w) before += wsum[w];
+      if (m < npts) zoff[m] = before + incl - nz;
+      for (int w = 0; w < nw; ++w) carry += wsum[w];
+      __syncthreads();
+    }
+    if (tid == 0) zoff[npts] = carry;
+  }
   for (int m = tid; m < npts; m += blockDim.x) {
     int n;
     if (!rev) n = zc[2 * m] - (m > 0 ? zc[2 * m - 1] : 0);
@@ -998,6 +1039,11 @@ __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk,
     if (n > 0) atomicAdd(drow + m, n * kmul(g, mat, nk));
     const int i0 = zg[2 * m], nz = zg[2 * m + 1] - i0;
     if (nz > 0) {
+      if (fuse) {
+        const int o = zoff[m];
+        for (int k = 0; k < nz; ++k) ilist[o + k] = m | (k << 16);
+        continue;
+      }
       double la, lb;
       zone_bracket(c, g, sharp, m, la, lb);
       const bool pos = la > 0.0;
@@ -1008,6 +1054,20 @@ __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk,
                                     (int)(1u | (pos ? 0u : 2u) | ((unsigned)k << 2) | ((unsigned)nz << 17)),
                                     fmax(xa, gl), fmin(xb, gu), pivmin};
     }
+  }
+  if (!fuse) return;
+  __syncthreads();
+  const int total = zoff[npts];
+  for (int q = tid; q < total; q += blockDim.x) {
+    const int il = ilist[q], m = il & 0xffff, k = il >> 16;
+    double la, lb;
+    zone_bracket(c, g, sharp, m, la, lb);
+    const bool pos = la > 0.0;
+    const double xa = pos ? la * la : lb * lb, xb = pos ? lb * lb : la * la;
+    const int i0 = zg[2 * m], nz = zg[2 * m + 1] - i0;
+    const double mu = zone_locate<false>(sd, sd + S, S, i0 + k, fmax(xa, gl), fmin(xb, gu), i0, i0 + nz, pivmin);
+    const double sg = sqrt(fmax(mu, 0.0));
+    add_eigenvalue(c, g, sharp, diff, trans, status, mat, nk, pos ? sg : -sg);
   }
 }
 
@@ -1060,17 +1120,24 @@ bool launch_gram_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, 
                       cudaStream_t st, RefineItem* refine, unsigned long long* refine_count) {
   bool rev = false;
   if (!refine || !refine_count || !diff || !zone_path_ok(c, g, sharp, rev)) return false;
-  cudaMemsetAsync(refine_count, 0, sizeof(unsigned long long), st);
-  const size_t zsm = (size_t)g.npts * 4 * sizeof(int);
-  const int zt = g.npts >= 256 ? 256 : ((g.npts + 31) / 32) * 32;
-  set_smem_attr(zone_count_gram_kernel, zsm);
-  zone_count_gram_kernel<<<(unsigned)nmat, zt, zsm, st>>>(c, nk, g, sharp, rev, mat0, nmat, tri, tri_stride, dims,
-                                                           diff, refine, refine_count);
   const int lanes_opt = (int)opt("HX_GRAM_REFINE_LANES", 0);
   const int G = lanes_opt > 0 ? lanes_opt : (c.N >= 1024 ? 8 : 1);
-  zone_refine_gram_kernel<<<148 * 16, 128, 0, st>>>(c, nk, g, tri, tri_stride, diff, trans, status, sharp, refine,
-                                                    refine_count, G);
-  count_launch(2);
+  // per-thread refinement (G == 1): fused into the count kernel (HX_ZONE_FUSE=0: the global item list)
+  const int fuse = G == 1 && opt("HX_ZONE_FUSE", 1) != 0 && g.npts < 65536 && c.N < 32768;
+  const size_t zsm = (size_t)g.npts * 4 * sizeof(int) +
+                     (fuse ? (size_t)2 * c.N * (sizeof(double) + sizeof(int)) + (size_t)(g.npts + 1) * sizeof(int) : 0);
+  const int zt = g.npts >= 256 ? 256 : ((g.npts + 31) / 32) * 32;
+  if (zsm > 200 * 1024) return false;
+  set_smem_attr(zone_count_gram_kernel, zsm);
+  if (!fuse) cudaMemsetAsync(refine_count, 0, sizeof(unsigned long long), st);
+  zone_count_gram_kernel<<<(unsigned)nmat, zt, zsm, st>>>(c, nk, g, sharp, rev, mat0, nmat, tri, tri_stride, dims,
+                                                           diff, refine, refine_count, fuse, trans, status);
+  count_launch();
+  if (!fuse) {
+    zone_refine_gram_kernel<<<148 * 16, 128, 0, st>>>(c, nk, g, tri, tri_stride, diff, trans, status, sharp, refine,
+                                                      refine_count, G);
+    count_launch();
+  }
   return true;
 }
 

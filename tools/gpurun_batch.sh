@@ -1,5 +1,4 @@
 #!/bin/bash
 cd $GRAFT_REPO_ROOT
-timeout 1200 python -m pytest tests/test_variants_gpu.py -q -x -k "small_gram" > gpurun_out/gputest_sg.log 2>&1; echo "pytest exit $?" >> gpurun_out/gputest_sg.log
-tail -4 gpurun_out/gputest_sg.log
-python scratch_sg.py
+timeout 600 ncu --metrics gpu__time_duration.sum,smsp__thread_inst_executed_per_inst_executed.ratio,sm__warps_active.avg.per_cycle_active --clock-control none --kernel-name regex:"zone_" -c 40 --csv --log-file gpurun_out/zone_l.csv python tools/profile_run.py --config c2 --levels 2,3 > /dev/null 2>&1
+HX_ZONE_FUSE=0 timeout 600 ncu --metrics gpu__time_duration.sum,smsp__thread_inst_executed_per_inst_executed.ratio,sm__warps_active.avg.per_cycle_active --clock-control none --kernel-name regex:"zone_" -c 40 --csv --log-file gpurun_out/zone_l0.csv python tools/profile_run.py --config c2 --levels 2,3 > /dev/null 2>&1
