@@ -677,6 +677,7 @@ HermSlab herm_slab(int n) {
 }
 
 int herm_reduce(double2* ws, int n, int64_t cnt, const int* dims, cudaStream_t st) {
+  NvtxRange nvtx_red("Hermitian two-stage reduce n=%d cnt=%lld", n, (long long)cnt);
   return band_reduce(ws, BandWs::make(n), n, cnt, dims, st);
 }
 

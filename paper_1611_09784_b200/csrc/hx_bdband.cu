@@ -358,6 +358,7 @@ static void launch_rank_update(double2* ws, const SlabGeom& G, int mr0, int mc0,
 template <bool RE>
 static int bd_reduce(double2* ws, const BdWs& L, int64_t cnt, const int* dims, cudaStream_t st) {
   const int S = L.S;
+  NvtxRange nvtx_red("bipartite SVD reduce S=%d cnt=%lld", S, (long long)cnt);
   const SlabGeom G{L.stride, S, L.c_off};
   // HX_FUSED_UPDATE=1: fold the trailing rank updates into the next product (one pass over the trailing
   // matrix per side).  Correct, but measured ~10% slower than separate rank updates on sm_100a (the fused
@@ -565,6 +566,7 @@ static void launch_rank_update_real(double* ws, const RSlab& G, int mr0, int mc0
 
 static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* dims, cudaStream_t st) {
   const int S = L.S;
+  NvtxRange nvtx_red("bipartite SVD reduce (real) S=%d cnt=%lld", S, (long long)cnt);
   double* ws = reinterpret_cast<double*>(ws2);
   const size_t sd = 2 * L.stride, c0 = 2 * L.c_off, v1 = 2 * L.v1_off, v2 = 2 * L.v2_off, x = 2 * L.x_off,
                z = 2 * L.z_off, t1 = 2 * L.t1_off, t2 = 2 * L.t2_off;
@@ -722,6 +724,7 @@ static int bd_reduce_real(double2* ws2, const BdWs& L, int64_t cnt, const int* d
 static int bd_reduce_gram(double2* ws2, const BdWs& L, int64_t cnt, const int* dims, int* status, bool direct,
                           cudaStream_t st) {
   const int S = L.S;
+  NvtxRange nvtx_red("gram reduce S=%d cnt=%lld: stage 1 (panel, xv, W, rank-2k) + symmetric chase", S, (long long)cnt);
   double* ws = reinterpret_cast<double*>(ws2);
   const size_t sd = 2 * L.stride, c0 = 2 * L.c_off, v1 = 2 * L.v1_off, x = 2 * L.x_off, t1 = 2 * L.t1_off;
   const RSlab G{sd, S, c0};
@@ -776,6 +779,7 @@ static int bd_reduce_gram(double2* ws2, const BdWs& L, int64_t cnt, const int* d
     return 0;
   }
   // compact lower band (64 doubles per column) + register-row chase; launch shapes as the bidiagonal chase
+  NvtxRange nvtx_chase("gram symmetric chase S=%d cnt=%lld", S, (long long)cnt);
   const size_t bo = 2 * L.band_off, to = 2 * L.tgk_off;
   sym_band_extract_kernel<<<(unsigned)cnt, 256, 0, st>>>(ws, sd, c0, bo, S);
   // no shared-memory padding (occupancy cap) here: 4 CTAs / SM by registers, and the smaller carve-out leaves more

@@ -451,6 +451,7 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
   refresh_opts(ctx);
   const hx::CellDev& c = cell->dev;
   const int N = c.N;
+  hx::NvtxRange nvtx_batch("hx_eval_idos_batch N=%d nk=%d masks=%lld", N, (int)nk, (long long)nmasks);
   int64_t nk_total = nk;
   if (kmult) {
     if (d_eigs) return fail(HX_E_ARG, "k-point multiplicities need the IDOS-only call (no eigenvalue output)");

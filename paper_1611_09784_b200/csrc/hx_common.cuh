@@ -1,9 +1,25 @@
 // Shared device helpers for libhx (sm_100a).
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
+#include <stdio.h>
 
 namespace hx {
+
+// NVTX range over a host-side submission phase (tier / stage of a batch): shows the (tier, stage) structure of
+// a step in Nsight Systems / ncu --nvtx; a no-op without an attached tool.
+struct NvtxRange {
+  template <class... A>
+  explicit NvtxRange(const char* fmt, A... a) {
+    char buf[96];
+    snprintf(buf, sizeof buf, fmt, a...);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Number of libhx kernel launches issued by this process (reported by bench.py as gpu_launches).
 void count_launch(unsigned long long n = 1);

@@ -1120,6 +1120,7 @@ bool launch_gram_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, 
                       cudaStream_t st, RefineItem* refine, unsigned long long* refine_count) {
   bool rev = false;
   if (!refine || !refine_count || !diff || !zone_path_ok(c, g, sharp, rev)) return false;
+  NvtxRange nvtx_eig("eigenvalue stage (Gram zone path) S=%d nmat=%lld", c.N, (long long)nmat);
   const int lanes_opt = (int)opt("HX_GRAM_REFINE_LANES", 0);
   const int G = lanes_opt > 0 ? lanes_opt : (c.N >= 1024 ? 8 : 1);
   // per-thread refinement (G == 1): fused into the count kernel (HX_ZONE_FUSE=0: the global item list)
@@ -1148,6 +1149,7 @@ void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, i
                      size_t tri_stride, const int* dims, int* diff, unsigned long long* trans, double* eigs,
                      int* status, int sharp, cudaStream_t st, RefineItem* refine, unsigned long long* refine_count,
                      bool tgk) {
+  NvtxRange nvtx_eig("eigenvalue stage N=%d nmat=%lld tgk=%d", c.N, (long long)nmat, (int)tgk);
   const int64_t per = tgk ? (c.N + 1) / 2 : c.N;
   const int64_t slots = nmat * per;
   const bool two_pass = refine && refine_count && diff && !eigs;
