@@ -508,7 +508,8 @@ static int eval_impl(hx_ctx* ctx, hx_cell* cell, const double* kpoints, int32_t 
   unsigned long long* refine_count = nullptr;
   auto make_refine = [&](int64_t items) -> int {
     if (d_eigs) return 0;  // eigenvalue output requested: single full-precision pass
-    if (ctx->refine.grow(256 + (size_t)items * sizeof(hx::RefineItem))) return -1;
+    // + 64 per matrix: the grouped list of the staged multisection pads every matrix's range (hx_kernels.cu)
+    if (ctx->refine.grow(256 + (size_t)(items + 64 * nmat) * sizeof(hx::RefineItem))) return -1;
     refine_count = static_cast<unsigned long long*>(ctx->refine.p);
     refine = reinterpret_cast<hx::RefineItem*>(static_cast<unsigned char*>(ctx->refine.p) + 256);
     return 0;

@@ -531,6 +531,64 @@ __device__ void refine_multisection(const CellDev& c, int nk, const GridDev& g, 
     }
 }
 
+// Staged G-lane multisection of the zone items (grouped list: zone_count(_gram)_kernel with group =
+// blockDim.x / G): every block iteration works on blockDim.x / G consecutive items of ONE matrix, whose tridiagonal
+// (2 S doubles) it first copies to shared memory - the Sturm row steps then read shared memory with at most a few
+// distinct addresses per warp instead of L2 (ncu on the unstaged kernel: long-scoreboard stalls dominate).  Same
+// search as refine_multisection (same points, same counts: the same bits).
+template <bool ZD, bool GRAM>
+__device__ void refine_multisection_staged(const CellDev& c, int nk, const GridDev& g,
+                                           const double* __restrict__ tri, size_t tri_stride,
+                                           const int* __restrict__ dims, int* diff, unsigned long long* trans,
+                                           int* status, int sharp, const RefineItem* __restrict__ items,
+                                           unsigned long long n, int G, double* sm) {
+  const int S = c.N;
+  const int per_block = blockDim.x / G;
+  const unsigned long long stride = (unsigned long long)gridDim.x * per_block;
+  const int lane = threadIdx.x & 31, sub = lane % G, base = lane - sub;
+  const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << base;
+  const double inv = 1.0 / (double)(G + 1);
+  for (unsigned long long qb = (unsigned long long)blockIdx.x * per_block; qb < n; qb += stride) {
+    const RefineItem it = items[qb + threadIdx.x / G];  // n is a multiple of per_block
+    const int64_t lm0 = items[qb].lm;
+    const double* src = tri + lm0 * tri_stride;
+    const int d = GRAM ? S : dims[lm0];  // Gram mode: the S x S tridiagonal of G, items in mu = sigma^2
+    __syncthreads();  // the previous iteration's readers are done
+    for (int i = threadIdx.x; i < 2 * S; i += blockDim.x) sm[i] = src[i];
+    __syncthreads();
+    const bool valid = it.idx >= 0;
+    double lo = it.lo, hi = it.hi;
+    bool done = !valid;
+    for (int k = 0; k < 200; ++k) {
+      const double tol = refine_tol(lo, hi, it.pivmin);
+      const double mid = 0.5 * (lo + hi);
+      done = done || hi - lo <= tol || mid <= lo || mid >= hi;
+      if (__all_sync(0xffffffffu, done)) break;
+      const double x = fma((double)(sub + 1) * inv, hi - lo, lo);
+      bool above = true;
+      if (!done) above = (x > lo && x < hi) ? sturm_count_fast<ZD>(sm, sm + S, d, x, it.pivmin) > it.idx : x >= hi;
+      const unsigned b = (__ballot_sync(0xffffffffu, above) & gmask) >> base;
+      const int m = b ? __ffs(b) - 1 : G;
+      const double nlo = __shfl_sync(0xffffffffu, x, base + (m == 0 ? 0 : m - 1));
+      const double nhi = __shfl_sync(0xffffffffu, x, base + (m == G ? G - 1 : m));
+      if (!done) {
+        lo = m == 0 ? lo : nlo;
+        hi = m == G ? hi : nhi;
+      }
+    }
+    if (valid && sub == 0) {
+      const double lam = 0.5 * (lo + hi);
+      if constexpr (GRAM) {  // lambda = +-sqrt(mu), sign in flag bit 1
+        const double sg = sqrt(fmax(lam, 0.0));
+        add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, (it.flags & 2) ? -sg : sg);
+      } else {
+        if (it.flags & 1) add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, lam);
+        if (it.flags & 2) add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, -lam);
+      }
+    }
+  }
+}
+
 // Phase 2: bisection of the eigenvalues left unsettled by eig_idos_kernel, densely
 // packed (every lane of a warp has real work), then the IDOS contribution (+ the TGK mirror).
 // Lanes per refinement item (1: per-thread Newton / bisection, 2-8: multisection), a function of the
@@ -660,20 +718,61 @@ __device__ __forceinline__ void sturm_count_pair(const double* __restrict__ diag
 #endif
 }
 
+template <bool ZD>
+__device__ double zone_locate(const double* diag, const double* e2, int d, int idx, double lo, double hi, int clo,
+                              int chi, double pivmin);
+
+// Block-wide exclusive scan of the zone item counts nz(m), m < npts, into zoff[0 .. npts] (zoff[npts] = total);
+// wsum: 8 ints of shared memory.  Every thread of the block calls it; ends with a barrier.
+template <class F>
+__device__ __forceinline__ void zone_item_offsets(int npts, int* zoff, int* wsum, F nz_of) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  int carry = 0;
+  for (int m0 = 0; m0 < npts; m0 += blockDim.x) {
+    const int m = m0 + tid;
+    const int nz = m < npts ? nz_of(m) : 0;
+    int incl = nz;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int before = carry;
+    for (int w = 0; w < warp; ++w) before += wsum[w];
+    if (m < npts) zoff[m] = before + incl - nz;
+    for (int w = 0; w < nw; ++w) carry += wsum[w];
+    __syncthreads();
+  }
+  if (tid == 0) zoff[npts] = carry;
+  __syncthreads();
+}
+
 // One CTA per matrix.  counts[2m] / counts[2m+1]: eigenvalues below the lower / upper lambda edge of zone m
 // (dynamic shared memory, 2 npts ints).  rev: E decreases with lambda.
 template <bool ZD>
 __global__ void __launch_bounds__(256) zone_count_kernel(CellDev c, int nk, GridDev g, int sharp, int rev,
                                                          int64_t mat0, int64_t nmat, const double* __restrict__ tri,
                                                          size_t tri_stride, const int* __restrict__ dims, int* diff,
-                                                         RefineItem* refine, unsigned long long* refine_count) {
-  extern __shared__ int zc[];
+                                                         RefineItem* refine, unsigned long long* refine_count,
+                                                         int fuse, unsigned long long* trans, int* status, int group) {
+  // fuse != 0 (per-thread refinement, N < 1024): the block locates its own zone eigenvalues on a shared-memory copy
+  // of the tridiagonal (as zone_count_gram_kernel).  Dynamic shared memory: fuse: [2 N] doubles (diag, e2), then
+  // ints: [2 npts] counts, fuse: [npts + 1] item offsets, [N] items.
+  extern __shared__ __align__(16) unsigned char zraw[];
   __shared__ double red[3][32];
+  __shared__ int wsum[8];
+  __shared__ unsigned long long list_base;  // group > 0: the matrix's padded range of the item list
   const int64_t lm = blockIdx.x;
   if (lm >= nmat) return;
   const int d = dims[lm];
   if (d <= 0) return;
   const int N = c.N, npts = g.npts;
+  double* sd = reinterpret_cast<double*>(zraw);
+  int* zc = reinterpret_cast<int*>(zraw + (fuse ? (size_t)2 * N * sizeof(double) : 0));
+  int* zoff = zc + 2 * npts;     // fuse only
+  int* ilist = zoff + npts + 1;  // fuse only
   const int64_t mat = mat0 + lm;
   const int64_t mk = mat / nk;
   const double* diag = tri + lm * tri_stride;
@@ -689,6 +788,10 @@ __global__ void __launch_bounds__(256) zone_count_kernel(CellDev c, int nk, Grid
     gl = fmin(gl, di - el - er);
     gu = fmax(gu, di + el + er);
     em = fmax(em, er2);
+    if (fuse) {
+      sd[i] = di;
+      sd[N + i] = e2[i];
+    }
   }
   gl = warp_min(gl);
   gu = warp_max(gu);
@@ -719,7 +822,7 @@ __global__ void __launch_bounds__(256) zone_count_kernel(CellDev c, int nk, Grid
     int ca = xa <= gl ? 0 : d, cb = xb <= gl ? 0 : d;
     if (ra || rb) {
       int na, nb;
-      sturm_count_pair<ZD>(diag, e2, d, xa, xb, pivmin, na, nb);
+      sturm_count_pair<ZD>(fuse ? sd : diag, fuse ? sd + N : e2, d, xa, xb, pivmin, na, nb);
       if (ra) ca = na;
       if (rb) cb = nb;
     }
@@ -728,6 +831,16 @@ __global__ void __launch_bounds__(256) zone_count_kernel(CellDev c, int nk, Grid
   }
   __syncthreads();
   int* drow = diff + mk * (npts + 1);
+  if (fuse || group > 0) {
+    zone_item_offsets(npts, zoff, wsum, [&](int m) { return zc[2 * m + 1] - zc[2 * m]; });
+    if (!fuse) {
+      const int total = zoff[npts], padded = (total + group - 1) / group * group;
+      if (tid == 0) list_base = atomicAdd(refine_count, (unsigned long long)padded);
+      __syncthreads();
+      for (int q = total + tid; q < padded; q += blockDim.x)
+        refine[list_base + q] = RefineItem{mat, lm, -1, 0, 0.0, 0.0, 0.0};
+    }
+  }
   for (int m = tid; m < npts; m += blockDim.x) {
     // gap below zone m (in E): settles at index m
     int n;
@@ -737,13 +850,30 @@ __global__ void __launch_bounds__(256) zone_count_kernel(CellDev c, int nk, Grid
     // eigenvalues inside zone m: refinement items from the zone's own bracket
     const int i0 = zc[2 * m], nz = zc[2 * m + 1] - i0;
     if (nz > 0) {
+      if (fuse) {
+        const int o = zoff[m];
+        for (int k = 0; k < nz; ++k) ilist[o + k] = m | (k << 16);
+        continue;
+      }
       double xa, xb;
       zone_bracket(c, g, sharp, m, xa, xb);
-      const unsigned long long pos = atomicAdd(refine_count, (unsigned long long)nz);
+      const unsigned long long pos =
+          group > 0 ? list_base + (unsigned long long)zoff[m] : atomicAdd(refine_count, (unsigned long long)nz);
       for (int k = 0; k < nz; ++k)
         refine[pos + k] = RefineItem{mat, lm, i0 + k, (int)(1u | ((unsigned)k << 2) | ((unsigned)nz << 17)),
                                      fmax(xa, gl), fmin(xb, gu), pivmin};
     }
+  }
+  if (!fuse) return;
+  __syncthreads();
+  const int total = zoff[npts];
+  for (int q = tid; q < total; q += blockDim.x) {
+    const int il = ilist[q], m = il & 0xffff, k = il >> 16;
+    double xa, xb;
+    zone_bracket(c, g, sharp, m, xa, xb);
+    const int i0 = zc[2 * m], nz = zc[2 * m + 1] - i0;
+    const double lam = zone_locate<ZD>(sd, sd + N, d, i0 + k, fmax(xa, gl), fmin(xb, gu), i0, i0 + nz, pivmin);
+    add_eigenvalue(c, g, sharp, diff, trans, status, mat, nk, lam);
   }
 }
 
@@ -868,11 +998,12 @@ __device__ double zone_locate(const double* diag, const double* e2, int d, int i
 }
 
 template <bool ZD>
-__global__ void __launch_bounds__(128) zone_refine_kernel(CellDev c, int nk, GridDev g, const double* __restrict__ tri,
+__global__ void __launch_bounds__(512) zone_refine_kernel(CellDev c, int nk, GridDev g, const double* __restrict__ tri,
                                                           size_t tri_stride, const int* __restrict__ dims, int* diff,
                                                           unsigned long long* trans, int* status, int sharp,
                                                           const RefineItem* __restrict__ items,
-                                                          const unsigned long long* __restrict__ count) {
+                                                          const unsigned long long* __restrict__ count, int staged) {
+  extern __shared__ __align__(16) double zsm_stage[];
   const unsigned long long n = *count;
   const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
   // large matrices (few per batch: the slowest item bounds the launch; ~10 eigenvalues per zone, often in
@@ -881,7 +1012,11 @@ __global__ void __launch_bounds__(128) zone_refine_kernel(CellDev c, int nk, Gri
   // (refine_lanes), so that results do not depend on the batch composition.
   const int G = refine_lanes(c.N);
   if (G > 1) {
-    refine_multisection<ZD>(c, nk, g, tri, tri_stride, dims, diff, trans, status, sharp, items, n, G);
+    if (staged)
+      refine_multisection_staged<ZD, false>(c, nk, g, tri, tri_stride, dims, diff, trans, status, sharp, items, n, G,
+                                            zsm_stage);
+    else
+      refine_multisection<ZD>(c, nk, g, tri, tri_stride, dims, diff, trans, status, sharp, items, n, G);
     return;
   }
   for (unsigned long long q = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += nthreads) {
@@ -934,10 +1069,13 @@ __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk,
                                                               size_t tri_stride, const int* __restrict__ dims,
                                                               int* diff, RefineItem* refine,
                                                               unsigned long long* refine_count, int fuse,
-                                                              unsigned long long* trans, int* status) {
+                                                              unsigned long long* trans, int* status, int group) {
+  // group > 0 (list mode): the matrix's items go to ONE contiguous range of the list, padded with invalid items
+  // (idx < 0) to a multiple of `group` - every block of the staged multisection kernel then works on one matrix
   extern __shared__ __align__(16) unsigned char zraw[];
   __shared__ double red[3][32];
   __shared__ int wsum[8];
+  __shared__ unsigned long long list_base;
   const int64_t lm = blockIdx.x;
   if (lm >= nmat) return;
   const int d = dims[lm];
@@ -946,7 +1084,7 @@ __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk,
   double* sd = reinterpret_cast<double*>(zraw);
   int* zc = reinterpret_cast<int*>(zraw + (fuse ? (size_t)2 * S * sizeof(double) : 0));
   int* zg = zc + 2 * npts;
-  int* zoff = zg + 2 * npts;     // fuse only
+  int* zoff = zg + 2 * npts;     // fuse / grouped list
   int* ilist = zoff + npts + 1;  // fuse only
   const int64_t mat = mat0 + lm;
   const int64_t mk = mat / nk;
@@ -1010,27 +1148,15 @@ __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk,
   }
   __syncthreads();
   int* drow = diff + mk * (npts + 1);
-  if (fuse) {
-    // item offsets: block-wide exclusive scan of the zone item counts (one zone per thread and round)
-    int carry = 0;
-    for (int m0 = 0; m0 < npts; m0 += blockDim.x) {
-      const int m = m0 + tid;
-      const int nz = m < npts ? zg[2 * m + 1] - zg[2 * m] : 0;
-      int incl = nz;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      if (lane == 31) wsum[warp] = incl;
+  if (fuse || group > 0) {
+    zone_item_offsets(npts, zoff, wsum, [&](int m) { return zg[2 * m + 1] - zg[2 * m]; });
+    if (!fuse) {
+      const int total = zoff[npts], padded = (total + group - 1) / group * group;
+      if (tid == 0) list_base = atomicAdd(refine_count, (unsigned long long)padded);
       __syncthreads();
-      int before = carry;
-      for (int w = 0; w < warp; ++w) before += wsum[w];
-      if (m < npts) zoff[m] = before + incl - nz;
-      for (int w = 0; w < nw; ++w) carry += wsum[w];
-      __syncthreads();
+      for (int q = total + tid; q < padded; q += blockDim.x)
+        refine[list_base + q] = RefineItem{mat, lm, -1, 0, 0.0, 0.0, 0.0};
     }
-    if (tid == 0) zoff[npts] = carry;
   }
   for (int m = tid; m < npts; m += blockDim.x) {
     int n;
@@ -1048,7 +1174,8 @@ __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk,
       zone_bracket(c, g, sharp, m, la, lb);
       const bool pos = la > 0.0;
       const double xa = pos ? la * la : lb * lb, xb = pos ? lb * lb : la * la;
-      const unsigned long long p0 = atomicAdd(refine_count, (unsigned long long)nz);
+      const unsigned long long p0 =
+          group > 0 ? list_base + (unsigned long long)zoff[m] : atomicAdd(refine_count, (unsigned long long)nz);
       for (int k = 0; k < nz; ++k)
         refine[p0 + k] = RefineItem{mat, lm, i0 + k,
                                     (int)(1u | (pos ? 0u : 2u) | ((unsigned)k << 2) | ((unsigned)nz << 17)),
@@ -1077,14 +1204,20 @@ __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk,
 // S >= 1024 are bound by the slowest item of the diverging Newton search (near-degenerate clusters fall back to
 // bisection: 5.0 ms on the 64-matrix S = 1024 launch, 2.8 ms with 8 lanes); the many-matrix launches keep Newton
 // (S = 256: 1.3 ms, 4 lanes 3.1 ms).  HX_GRAM_REFINE_LANES overrides.
-__global__ void __launch_bounds__(128) zone_refine_gram_kernel(CellDev c, int nk, GridDev g,
+__global__ void __launch_bounds__(512) zone_refine_gram_kernel(CellDev c, int nk, GridDev g,
                                                                const double* __restrict__ tri, size_t tri_stride,
                                                                int* diff, unsigned long long* trans, int* status,
                                                                int sharp, const RefineItem* __restrict__ items,
-                                                               const unsigned long long* __restrict__ count, int G) {
+                                                               const unsigned long long* __restrict__ count, int G,
+                                                               int staged) {
+  extern __shared__ __align__(16) double zsm_refine[];
   const unsigned long long n = *count;
   if (G > 1) {
-    refine_multisection<false, true>(c, nk, g, tri, tri_stride, nullptr, diff, trans, status, sharp, items, n, G);
+    if (staged)
+      refine_multisection_staged<false, true>(c, nk, g, tri, tri_stride, nullptr, diff, trans, status, sharp, items, n, G,
+                                              zsm_refine);
+    else
+      refine_multisection<false, true>(c, nk, g, tri, tri_stride, nullptr, diff, trans, status, sharp, items, n, G);
     return;
   }
   const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
@@ -1125,18 +1258,31 @@ bool launch_gram_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, 
   const int G = lanes_opt > 0 ? lanes_opt : (c.N >= 1024 ? 8 : 1);
   // per-thread refinement (G == 1): fused into the count kernel (HX_ZONE_FUSE=0: the global item list)
   const int fuse = G == 1 && opt("HX_ZONE_FUSE", 1) != 0 && g.npts < 65536 && c.N < 32768;
-  const size_t zsm = (size_t)g.npts * 4 * sizeof(int) +
-                     (fuse ? (size_t)2 * c.N * (sizeof(double) + sizeof(int)) + (size_t)(g.npts + 1) * sizeof(int) : 0);
+  // multisection (G > 1): grouped item list + the tridiagonal staged in shared memory (HX_ZONE_STAGE=0: scattered
+  // list, loads from L2); block size so that >= 32 warps per SM stay resident beside the staged copies
+  const size_t stage_b = (size_t)2 * c.N * sizeof(double);
+  const int staged = G > 1 && 128 % G == 0 && opt("HX_ZONE_STAGE", 1) != 0 && stage_b <= 64 * 1024;
+  const int rthreads = !staged ? 128 : (stage_b <= 16 * 1024 ? 128 : (stage_b <= 32 * 1024 ? 256 : 512));
+  const int group = staged ? rthreads / G : 0;
+  const size_t zsm = (size_t)g.npts * 4 * sizeof(int) + (size_t)(g.npts + 1) * sizeof(int) +
+                     (fuse ? (size_t)2 * c.N * (sizeof(double) + sizeof(int)) : 0);
   const int zt = g.npts >= 256 ? 256 : ((g.npts + 31) / 32) * 32;
   if (zsm > 200 * 1024) return false;
   set_smem_attr(zone_count_gram_kernel, zsm);
   if (!fuse) cudaMemsetAsync(refine_count, 0, sizeof(unsigned long long), st);
   zone_count_gram_kernel<<<(unsigned)nmat, zt, zsm, st>>>(c, nk, g, sharp, rev, mat0, nmat, tri, tri_stride, dims,
-                                                           diff, refine, refine_count, fuse, trans, status);
+                                                           diff, refine, refine_count, fuse, trans, status, group);
   count_launch();
   if (!fuse) {
-    zone_refine_gram_kernel<<<148 * 16, 128, 0, st>>>(c, nk, g, tri, tri_stride, diff, trans, status, sharp, refine,
-                                                      refine_count, G);
+    if (staged) {
+      set_smem_attr(zone_refine_gram_kernel, stage_b);
+      const int per_sm = (int)std::min<size_t>(2048 / rthreads, (200 * 1024) / stage_b);
+      zone_refine_gram_kernel<<<148 * per_sm, rthreads, stage_b, st>>>(c, nk, g, tri, tri_stride, diff, trans, status,
+                                                                      sharp, refine, refine_count, G, 1);
+    } else {
+      zone_refine_gram_kernel<<<148 * 16, 128, 0, st>>>(c, nk, g, tri, tri_stride, diff, trans, status, sharp, refine,
+                                                        refine_count, G, 0);
+    }
     count_launch();
   }
   return true;
@@ -1157,25 +1303,40 @@ void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, i
   bool rev = false;
   // zone path: 2 npts Sturm counts per matrix beat ~d/2 x 10 bisection steps from d ~ 96 on
   if (two_pass && c.N >= opt("HX_ZONE_MIN_N", 96) && zone_path_ok(c, g, sharp, rev)) {
-    const size_t zsm = (size_t)g.npts * 2 * sizeof(int);
+    // per-thread refinement (N < 1024, refine_lanes): fused into the count kernel (HX_ZONE_FUSE=0: the item list)
+    const int fuse = c.N < g_refine_min_n && opt("HX_ZONE_FUSE", 1) != 0 && g.npts < 65536;
+    // multisection (N >= 1024): grouped item list + the tridiagonal staged in shared memory (HX_ZONE_STAGE=0: off)
+    const int G = c.N >= g_refine_min_n ? 4 : 1;  // refine_lanes
+    const size_t stage_b = (size_t)2 * c.N * sizeof(double);
+    const int staged = G > 1 && opt("HX_ZONE_STAGE", 1) != 0 && stage_b <= 64 * 1024;
+    const int rthreads = !staged ? 128 : (stage_b <= 16 * 1024 ? 128 : (stage_b <= 32 * 1024 ? 256 : 512));
+    const int group = staged ? rthreads / G : 0;
+    const size_t zsm = (size_t)g.npts * 2 * sizeof(int) + (size_t)(g.npts + 1) * sizeof(int) +
+                       (fuse ? (size_t)c.N * (2 * sizeof(double) + sizeof(int)) : 0);
     const int zt = g.npts >= 256 ? 256 : ((g.npts + 31) / 32) * 32;
     if (tgk) {
       set_smem_attr(zone_count_kernel<true>, zsm);
-      zone_count_kernel<true><<<(unsigned)nmat, zt, zsm, st>>>(c, nk, g, sharp, rev, mat0, nmat, tri, tri_stride,
-                                                              dims, diff, refine, refine_count);
+      zone_count_kernel<true><<<(unsigned)nmat, zt, zsm, st>>>(c, nk, g, sharp, rev, mat0, nmat, tri, tri_stride, dims,
+                                                              diff, refine, refine_count, fuse, trans, status, group);
     } else {
       set_smem_attr(zone_count_kernel<false>, zsm);
-      zone_count_kernel<false><<<(unsigned)nmat, zt, zsm, st>>>(c, nk, g, sharp, rev, mat0, nmat, tri, tri_stride,
-                                                               dims, diff, refine, refine_count);
+      zone_count_kernel<false><<<(unsigned)nmat, zt, zsm, st>>>(c, nk, g, sharp, rev, mat0, nmat, tri, tri_stride, dims,
+                                                               diff, refine, refine_count, fuse, trans, status, group);
     }
     count_launch();
-    const int64_t rblocks = 148 * 16;
-    if (tgk)
-      zone_refine_kernel<true><<<(unsigned)rblocks, 128, 0, st>>>(c, nk, g, tri, tri_stride, dims, diff, trans, status,
-                                                                  sharp, refine, refine_count);
-    else
-      zone_refine_kernel<false><<<(unsigned)rblocks, 128, 0, st>>>(c, nk, g, tri, tri_stride, dims, diff, trans,
-                                                                   status, sharp, refine, refine_count);
+    if (fuse) return;
+    const int per_sm = staged ? (int)std::min<size_t>(2048 / rthreads, (200 * 1024) / stage_b) : 16;
+    const int64_t rblocks = 148 * per_sm;
+    const size_t rsm = staged ? stage_b : 0;
+    if (tgk) {
+      if (staged) set_smem_attr(zone_refine_kernel<true>, rsm);
+      zone_refine_kernel<true><<<(unsigned)rblocks, rthreads, rsm, st>>>(c, nk, g, tri, tri_stride, dims, diff, trans,
+                                                                        status, sharp, refine, refine_count, staged);
+    } else {
+      if (staged) set_smem_attr(zone_refine_kernel<false>, rsm);
+      zone_refine_kernel<false><<<(unsigned)rblocks, rthreads, rsm, st>>>(c, nk, g, tri, tri_stride, dims, diff, trans,
+                                                                         status, sharp, refine, refine_count, staged);
+    }
     count_launch();
     return;
   }

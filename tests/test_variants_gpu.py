@@ -495,3 +495,30 @@ def test_small_gram_path_all_vacant_and_single_site():
         ref = O.solve_bands(ocell, om, words_to_int(words[m]), kp)
         rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), LO_G, HI_G, NPTS, 0.01, ocell.area)
         np.testing.assert_allclose(gram[m], rc, rtol=0, atol=IDOS_TOL)
+
+
+# ---- zone path of the eigenvalue stage: fused per-matrix refinement / staged multisection vs the item list ----
+@pytest.mark.parametrize("kind,nu,q,count", [("graphene", 16, 2, 12), ("graphene", 32, 1, 3), ("graphene", 8, 4, 24),
+                                             ("graphene", 11, 1, 6), ("graphene", 12, 3, 4), ("table", 4, 2, 6),
+                                             ("table", 6, 1, 3), ("graphene", 23, 1, 2), ("table", 10, 1, 2),
+                                             ("graphene", 24, 3, 2)])
+def test_zone_refinement_variants_same_bits(kind, nu, q, count):
+    """The refinement fused into the zone-count kernel (HX_ZONE_FUSE, matrices below 1024) and the staged
+    multisection on the grouped item list (HX_ZONE_STAGE, Gram tridiagonals from S = 1024) run the same searches
+    with the same arguments as the global item list: curves bitwise equal; Gram (S = 256, 1024, 64), TGK (odd S,
+    complex k) and Hermitian (table) tridiagonals, below and above the multisection threshold (N = 1024)."""
+    _, om, sc, cell, kp = _setup(kind, nu, q)
+    lo, hi = (LO_T, HI_T) if kind == "table" else (LO_G, HI_G)
+    step = (hi - lo) / (NPTS - 1)
+    words = sample_masks(sc.nunits, 0.06, 57, 1, 0, count)
+    base, _, st = eval_batch(cell, kp, words, lo, step, NPTS, 0.01)
+    assert (st == 0).all()
+    for opts in ({"HX_ZONE_FUSE": 0}, {"HX_ZONE_STAGE": 0}, {"HX_ZONE_FUSE": 0, "HX_ZONE_STAGE": 0}):
+        with _lib.options(**opts):
+            alt, _, st2 = eval_batch(cell, kp, words, lo, step, NPTS, 0.01)
+        assert (st2 == 0).all()
+        assert np.array_equal(base, alt), opts
+    ocell = O.make_cell(om, nu)
+    ref = O.solve_bands(ocell, om, words_to_int(words[0]), kp)
+    rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), lo, hi, NPTS, 0.01, ocell.area)
+    np.testing.assert_allclose(base[0], rc, rtol=0, atol=IDOS_TOL)
