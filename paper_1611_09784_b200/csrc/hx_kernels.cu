@@ -1002,7 +1002,8 @@ __global__ void __launch_bounds__(512) zone_refine_kernel(CellDev c, int nk, Gri
                                                           size_t tri_stride, const int* __restrict__ dims, int* diff,
                                                           unsigned long long* trans, int* status, int sharp,
                                                           const RefineItem* __restrict__ items,
-                                                          const unsigned long long* __restrict__ count, int staged) {
+                                                          const unsigned long long* __restrict__ count, int staged,
+                                                          int G) {
   extern __shared__ __align__(16) double zsm_stage[];
   const unsigned long long n = *count;
   const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
@@ -1010,13 +1011,32 @@ __global__ void __launch_bounds__(512) zone_refine_kernel(CellDev c, int nk, Gri
   // near-degenerate clusters that Newton cannot isolate): G-lane multisection with its fixed round count;
   // otherwise one thread per item, Newton (about 11 Sturm counts on average).  Chosen by the matrix size only
   // (refine_lanes), so that results do not depend on the batch composition.
-  const int G = refine_lanes(c.N);
   if (G > 1) {
     if (staged)
       refine_multisection_staged<ZD, false>(c, nk, g, tri, tri_stride, dims, diff, trans, status, sharp, items, n, G,
                                             zsm_stage);
     else
       refine_multisection<ZD>(c, nk, g, tri, tri_stride, dims, diff, trans, status, sharp, items, n, G);
+    return;
+  }
+  if (staged) {
+    // grouped list: blockDim.x items of one matrix per block iteration, its tridiagonal in shared memory
+    const int N = c.N;
+    for (unsigned long long qb = (unsigned long long)blockIdx.x * blockDim.x; qb < n; qb += nthreads) {
+      const RefineItem it = items[qb + threadIdx.x];
+      const int64_t lm0 = items[qb].lm;
+      const double* src = tri + lm0 * tri_stride;
+      __syncthreads();
+      for (int i = threadIdx.x; i < 2 * N; i += blockDim.x) zsm_stage[i] = src[i];
+      __syncthreads();
+      if (it.idx < 0) continue;
+      const unsigned f = (unsigned)it.flags;
+      const int k = (int)((f >> 2) & 0x7fffu), nz = (int)(f >> 17);
+      const int clo = it.idx - k;
+      const double lam =
+          zone_locate<ZD>(zsm_stage, zsm_stage + N, dims[lm0], it.idx, it.lo, it.hi, clo, clo + nz, it.pivmin);
+      add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, lam);
+    }
     return;
   }
   for (unsigned long long q = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += nthreads) {
@@ -1222,6 +1242,26 @@ __global__ void __launch_bounds__(512) zone_refine_gram_kernel(CellDev c, int nk
   }
   const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
   const int S = c.N;
+  if (staged) {
+    // grouped list (group = blockDim.x): a block iteration = blockDim.x items of one matrix, its tridiagonal staged
+    // in shared memory; one thread per item, the bracketed Newton search of zone_locate
+    for (unsigned long long qb = (unsigned long long)blockIdx.x * blockDim.x; qb < n; qb += nthreads) {
+      const RefineItem it = items[qb + threadIdx.x];
+      const double* src = tri + items[qb].lm * tri_stride;
+      __syncthreads();
+      for (int i = threadIdx.x; i < 2 * S; i += blockDim.x) zsm_refine[i] = src[i];
+      __syncthreads();
+      if (it.idx < 0) continue;
+      const unsigned f = (unsigned)it.flags;
+      const int k = (int)((f >> 2) & 0x7fffu), nz = (int)(f >> 17);
+      const int clo = it.idx - k;
+      const double mu =
+          zone_locate<false>(zsm_refine, zsm_refine + S, S, it.idx, it.lo, it.hi, clo, clo + nz, it.pivmin);
+      const double sg = sqrt(fmax(mu, 0.0));
+      add_eigenvalue(c, g, sharp, diff, trans, status, it.mat, nk, (f & 2u) ? -sg : sg);
+    }
+    return;
+  }
   for (unsigned long long q = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; q < n; q += nthreads) {
     const RefineItem it = items[q];
     const double* diag = tri + it.lm * tri_stride;
@@ -1254,14 +1294,20 @@ bool launch_gram_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, 
   bool rev = false;
   if (!refine || !refine_count || !diff || !zone_path_ok(c, g, sharp, rev)) return false;
   NvtxRange nvtx_eig("eigenvalue stage (Gram zone path) S=%d nmat=%lld", c.N, (long long)nmat);
-  const int lanes_opt = (int)opt("HX_GRAM_REFINE_LANES", 0);
-  const int G = lanes_opt > 0 ? lanes_opt : (c.N >= 1024 ? 8 : 1);
-  // per-thread refinement (G == 1): fused into the count kernel (HX_ZONE_FUSE=0: the global item list)
-  const int fuse = G == 1 && opt("HX_ZONE_FUSE", 1) != 0 && g.npts < 65536 && c.N < 32768;
-  // multisection (G > 1): grouped item list + the tridiagonal staged in shared memory (HX_ZONE_STAGE=0: scattered
-  // list, loads from L2); block size so that >= 32 warps per SM stay resident beside the staged copies
+  // Refinement of the zone eigenvalues, a function of the matrix size (and the options) only - never of the batch:
+  //   S < 1024: one thread per item (zone_locate: isolation + safeguarded Newton), fused into the count kernel on a
+  //             shared-memory copy of the tridiagonal (HX_ZONE_FUSE=0: global item list, same bits);
+  //   S >= 1024: the same per-thread search on the GROUPED item list, the block's matrix staged in shared memory
+  //             (HX_ZONE_STAGE=0: loads from L2, same bits).  Per item ~11 Sturm counts instead of the 8 lanes x 13
+  //             rounds of the multisection that the unstaged kernel needed to hide the L2 latency of its scattered
+  //             loads (S = 1024, 64 matrices: 2.1 ms; staged multisection 1.45 ms at 67 % issue utilisation);
+  //   HX_GRAM_REFINE_LANES = G > 1, or a tridiagonal too large to stage (S > 4096): G-lane multisection.
   const size_t stage_b = (size_t)2 * c.N * sizeof(double);
-  const int staged = G > 1 && 128 % G == 0 && opt("HX_ZONE_STAGE", 1) != 0 && stage_b <= 64 * 1024;
+  const bool can_stage = stage_b <= 64 * 1024;
+  const int lanes_opt = (int)opt("HX_GRAM_REFINE_LANES", 0);
+  const int G = lanes_opt > 0 ? lanes_opt : (c.N >= 1024 && !can_stage ? 8 : 1);
+  const int fuse = G == 1 && c.N < 1024 && opt("HX_ZONE_FUSE", 1) != 0 && g.npts < 65536;
+  const int staged = !fuse && c.N >= 1024 && can_stage && 128 % G == 0 && opt("HX_ZONE_STAGE", 1) != 0;
   const int rthreads = !staged ? 128 : (stage_b <= 16 * 1024 ? 128 : (stage_b <= 32 * 1024 ? 256 : 512));
   const int group = staged ? rthreads / G : 0;
   const size_t zsm = (size_t)g.npts * 4 * sizeof(int) + (size_t)(g.npts + 1) * sizeof(int) +
@@ -1304,11 +1350,15 @@ void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, i
   // zone path: 2 npts Sturm counts per matrix beat ~d/2 x 10 bisection steps from d ~ 96 on
   if (two_pass && c.N >= opt("HX_ZONE_MIN_N", 96) && zone_path_ok(c, g, sharp, rev)) {
     // per-thread refinement (N < 1024, refine_lanes): fused into the count kernel (HX_ZONE_FUSE=0: the item list)
-    const int fuse = c.N < g_refine_min_n && opt("HX_ZONE_FUSE", 1) != 0 && g.npts < 65536;
-    // multisection (N >= 1024): grouped item list + the tridiagonal staged in shared memory (HX_ZONE_STAGE=0: off)
-    const int G = c.N >= g_refine_min_n ? 4 : 1;  // refine_lanes
+    // refinement method by matrix size only, as launch_gram_idos: fused below N = 1024, the grouped list with the
+    // matrix staged in shared memory from there (per-thread Newton), 4-lane multisection when the tridiagonal does
+    // not fit (N > 4096) or with HX_REFINE_LANES = G > 1
     const size_t stage_b = (size_t)2 * c.N * sizeof(double);
-    const int staged = G > 1 && opt("HX_ZONE_STAGE", 1) != 0 && stage_b <= 64 * 1024;
+    const bool can_stage = stage_b <= 64 * 1024;
+    const int lanes_opt = (int)opt("HX_REFINE_LANES", 0);
+    const int G = lanes_opt > 0 ? lanes_opt : (c.N >= g_refine_min_n && !can_stage ? 4 : 1);
+    const int fuse = G == 1 && c.N < g_refine_min_n && opt("HX_ZONE_FUSE", 1) != 0 && g.npts < 65536;
+    const int staged = !fuse && c.N >= g_refine_min_n && can_stage && 128 % G == 0 && opt("HX_ZONE_STAGE", 1) != 0;
     const int rthreads = !staged ? 128 : (stage_b <= 16 * 1024 ? 128 : (stage_b <= 32 * 1024 ? 256 : 512));
     const int group = staged ? rthreads / G : 0;
     const size_t zsm = (size_t)g.npts * 2 * sizeof(int) + (size_t)(g.npts + 1) * sizeof(int) +
@@ -1331,11 +1381,11 @@ void launch_eig_idos(const CellDev& c, int nk, const GridDev& g, int64_t mat0, i
     if (tgk) {
       if (staged) set_smem_attr(zone_refine_kernel<true>, rsm);
       zone_refine_kernel<true><<<(unsigned)rblocks, rthreads, rsm, st>>>(c, nk, g, tri, tri_stride, dims, diff, trans,
-                                                                        status, sharp, refine, refine_count, staged);
+                                                                        status, sharp, refine, refine_count, staged, G);
     } else {
       if (staged) set_smem_attr(zone_refine_kernel<false>, rsm);
       zone_refine_kernel<false><<<(unsigned)rblocks, rthreads, rsm, st>>>(c, nk, g, tri, tri_stride, dims, diff, trans,
-                                                                         status, sharp, refine, refine_count, staged);
+                                                                         status, sharp, refine, refine_count, staged, G);
     }
     count_launch();
     return;

@@ -518,6 +518,16 @@ def test_zone_refinement_variants_same_bits(kind, nu, q, count):
             alt, _, st2 = eval_batch(cell, kp, words, lo, step, NPTS, 0.01)
         assert (st2 == 0).all()
         assert np.array_equal(base, alt), opts
+    # the G-lane multisection (the method of matrices too large to stage): staged and unstaged give the same bits,
+    # and the per-thread Newton search agrees with it to the refinement tolerance
+    lanes = {"HX_GRAM_REFINE_LANES": 8, "HX_REFINE_LANES": 4}
+    with _lib.options(**lanes):
+        ms, _, st3 = eval_batch(cell, kp, words, lo, step, NPTS, 0.01)
+    with _lib.options(HX_ZONE_STAGE=0, **lanes):
+        ms0, _, st4 = eval_batch(cell, kp, words, lo, step, NPTS, 0.01)
+    assert (st3 == 0).all() and (st4 == 0).all()
+    assert np.array_equal(ms, ms0)
+    np.testing.assert_allclose(ms, base, rtol=0, atol=1e-11)
     ocell = O.make_cell(om, nu)
     ref = O.solve_bands(ocell, om, words_to_int(words[0]), kp)
     rc = O.idos_from_bands(ref, np.full(len(kp), 1.0 / len(kp)), lo, hi, NPTS, 0.01, ocell.area)
