@@ -757,7 +757,7 @@ def run_e2e(hx, model, levels, nq, p, erange, lo, hi, args, rank, world, dev):
         dt = float(t.item())
     total = (world if shard_mode == "replicas" else 1) * sum(M for _, M in levels)
     return {"value": total / dt, "unit": "samples/s", "h2d_bytes_per_step": int(io[0]), "d2h_bytes_per_step": int(io[1]),
-            "api": f"paper_1611_09784_b200.Engine.run_mlmc (shard_mode={shard_mode}; host RNG + dedup per level, every (n, q) tier of every level through hx_eval_idos_batch concurrently)"}, means
+            "api": f"paper_1611_09784_b200.Engine.run_mlmc (shard_mode={shard_mode}; masks drawn on the GPU and read back (rng='device', bit-identical to the host sampler), host dedup / cache / placement per level, every (n, q) tier of every level through hx_eval_idos_batch with host buffers, concurrently)"}, means
 
 
 def cpu_baseline(kind, levels, nq, p, erange):
