@@ -1,7 +1,10 @@
 #!/bin/bash
+# Round-end check on the GPU box: smoke, the GPU test suite, the default bench line and the reference arm.
 cd $GRAFT_REPO_ROOT
-for m in "" "0,1,2,0,1,2,1" "0,1,2,0,0,1,2" "0,1,2,1,2,0,0" "0,1,1,2,2,2,2" "0,1,2,3,3,1,2" "0,1,2,2,1,1,2"; do
-  HX_LANE_MAP=$m timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 12 > gpurun_out/lm.json 2>/dev/null
-  python -c "
-import json; d=json.load(open('gpurun_out/lm.json')); print('map [$m]', round(d['value']), round(d['ms_per_step'],2))"
-done
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke.log
+tail -2 gpurun_out/smoke.log
+timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/gputest_all.log 2>&1; echo "pytest exit $?" >> gpurun_out/gputest_all.log
+tail -4 gpurun_out/gputest_all.log
+timeout 900 python bench.py > gpurun_out/bench_c2_final.json 2> gpurun_out/bench_c2_final.err
+python -c "
+import json; d=json.load(open('gpurun_out/bench_c2_final.json')); print(d['value'], d['ms_per_step'], d['e2e']['value'], d['roofline']['frac'], d['cpu_baseline']['value'], d['self_check'], d['gpu_launches'], d['clocks'])"
