@@ -1007,10 +1007,10 @@ __global__ void __launch_bounds__(512) zone_refine_kernel(CellDev c, int nk, Gri
   extern __shared__ __align__(16) double zsm_stage[];
   const unsigned long long n = *count;
   const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
-  // large matrices (few per batch: the slowest item bounds the launch; ~10 eigenvalues per zone, often in
-  // near-degenerate clusters that Newton cannot isolate): G-lane multisection with its fixed round count;
-  // otherwise one thread per item, Newton (about 11 Sturm counts on average).  Chosen by the matrix size only
-  // (refine_lanes), so that results do not depend on the batch composition.
+  // G (launch_eig_idos: a function of the matrix size and the options only, so that results do not depend on the
+  // batch composition): 1 = one thread per item, Newton (about 11 Sturm counts on average; staged: grouped list,
+  // the matrix in shared memory); > 1 = G-lane multisection with its fixed round count (tridiagonals too large to
+  // stage, HX_REFINE_LANES).
   if (G > 1) {
     if (staged)
       refine_multisection_staged<ZD, false>(c, nk, g, tri, tri_stride, dims, diff, trans, status, sharp, items, n, G,
@@ -1218,12 +1218,13 @@ __global__ void __launch_bounds__(256) zone_count_gram_kernel(CellDev c, int nk,
   }
 }
 
-// Gram zone eigenvalues in mu = sigma^2 on G's tridiagonal, lambda = +-sqrt(mu).  G = 1: the bracketed Newton
-// search of zone_locate, one thread per item; G > 1: G-lane multisection (uniform control flow: every lane runs one
-// Sturm count per round).  Chosen by the matrix size only (batch-independent results): the few-matrix launches of
-// S >= 1024 are bound by the slowest item of the diverging Newton search (near-degenerate clusters fall back to
-// bisection: 5.0 ms on the 64-matrix S = 1024 launch, 2.8 ms with 8 lanes); the many-matrix launches keep Newton
-// (S = 256: 1.3 ms, 4 lanes 3.1 ms).  HX_GRAM_REFINE_LANES overrides.
+// Gram zone eigenvalues in mu = sigma^2 on G's tridiagonal, lambda = +-sqrt(mu), for the launches that are not fused
+// into zone_count_gram_kernel (launch_gram_idos chooses by the matrix size and the options only: batch-independent
+// results).  G = 1: the bracketed Newton search of zone_locate, one thread per item - staged: on the grouped list,
+// the block's matrix in shared memory (S >= 1024 by default), else on the scattered list with loads from L2
+// (HX_ZONE_FUSE=0 / HX_ZONE_STAGE=0: same bits, 5.0 ms on the 64-matrix S = 1024 launch).  G > 1
+// (HX_GRAM_REFINE_LANES, or a tridiagonal too large to stage): G-lane multisection, uniform control flow, every
+// lane one Sturm count per round (2.1 ms unstaged / 1.45 ms staged with 8 lanes on that launch).
 __global__ void __launch_bounds__(512) zone_refine_gram_kernel(CellDev c, int nk, GridDev g,
                                                                const double* __restrict__ tri, size_t tri_stride,
                                                                int* diff, unsigned long long* trans, int* status,
