@@ -32,6 +32,7 @@ from .solver import make_bz_grid, time_reversal_reduce, use_time_reversal
 
 _MERGE_TIERS = __import__("os").environ.get("HX_MERGE_TIERS", "0") == "1"
 _LANES = int(__import__("os").environ.get("HX_LANES", "3"))
+_JOINT_DEDUP = __import__("os").environ.get("HX_JOINT_DEDUP", "1") != "0"
 _LANE_MAP = [int(x) for x in __import__("os").environ.get("HX_LANE_MAP", "").split(",") if x]
 
 
@@ -245,10 +246,29 @@ class DeviceMlmc:
         if not _MERGE_TIERS:
             # every tier is deduplicated (main stream) and submitted (its lane) in turn, largest first: the largest
             # tier is on the GPU after its own torch.unique instead of after all of them (~1 ms of a c2 step)
-            for lane, j in enumerate(by_size):
-                i, n, words = specs[j]
+            # Tiers of the same small cell (one-word masks: nu = 4 in c2, where a level's quarter masks repeat the
+            # parent masks of the level below) are deduplicated TOGETHER and solved once - the cross-level hits of
+            # the reference's run cache (runner.py:213-233; Engine.evaluate_masks does the same on the host).
+            # HX_JOINT_DEDUP=0: every tier on its own.
+            groups, seen = [], set()
+            for j in by_size:
+                if j in seen:
+                    continue
+                n = specs[j][1]
+                same = [j2 for j2 in by_size if j2 not in seen and specs[j2][1] == n] \
+                    if _JOINT_DEDUP and self.cell(n).supercell.nunits <= 64 else [j]
+                seen.update(same)
+                groups.append(same)
+            for lane, js in enumerate(groups):
+                j = js[0]
+                i, n, _ = specs[j]
+                words = specs[j][2] if len(js) == 1 else torch.cat([specs[j2][2] for j2 in js])
                 uniq, inv, cuts = dedup(n, words)
-                jobs[j] = (i, n, uniq, inv, cuts)
+                off = 0
+                for j2 in js:
+                    rows = specs[j2][2].shape[0]
+                    jobs[j2] = (specs[j2][0], n, uniq, inv[off: off + rows], cuts)
+                    off += rows
                 ready = torch.cuda.Event()
                 ready.record(main)
                 # HX_LANES = L > 1 (default 3): the largest tier keeps lane 0, the others share lanes 1 .. L-1
@@ -265,7 +285,8 @@ class DeviceMlmc:
                 curves, status = self._solve(n, uniq, ctx, stream)
                 done = torch.cuda.Event()
                 done.record(stream)
-                outs[j] = (curves, done)
+                for j2 in js:
+                    outs[j2] = (curves, done)
                 self.statuses.append(status)
         else:
             # HX_MERGE_TIERS=1: the jobs of one tier (the same n) from different levels go to ONE batch call

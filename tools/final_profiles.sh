@@ -10,7 +10,7 @@ run() {  # name label args...
   timeout 900 ncu --metrics $M --clock-control none --csv --log-file $OUT/fp64_$name.csv python tools/profile_run.py "$@" > /dev/null 2>&1
   python tools/ncu_flops.py $OUT/fp64_$name.csv --json $OUT/r02_fp64_executed_$name.json --label "$label" > $OUT/r02_fp64_executed_$name.txt
 }
-run c2 "c2 one pass (tools/profile_run.py --config c2), serialised under ncu" --config c2
+run c2 "c2 one level set as the bench step submits it (tools/profile_run.py --config c2 --concurrent: run_levels, same-cell small tiers deduplicated together), serialised under ncu" --config c2 --concurrent
 run c2_L4_parent "c2 level 4 parent tier (N = 2048, 64 matrices at Gamma), tools/profile_run.py --config c2 --levels 4 --parent-only" --config c2 --levels 4 --parent-only
 ARGS=""
 for nb in 32:20000 64:5000 128:2000 256:500 512:200 1024:50 2048:16; do
