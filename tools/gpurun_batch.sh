@@ -1,13 +1,10 @@
 #!/bin/bash
+# Round-end check on the GPU box: smoke, the GPU test suite, the default bench line.
 cd $GRAFT_REPO_ROOT
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 1200 python -m pytest tests/test_device_pipeline_gpu.py tests/test_multirank_gpu.py -q -x 2>&1 | tail -4
-timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench_c2_jd.json 2> gpurun_out/bench_c2_jd.err
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke.log
+tail -2 gpurun_out/smoke.log
+timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/gputest_all.log 2>&1; echo "pytest exit $?" >> gpurun_out/gputest_all.log
+tail -4 gpurun_out/gputest_all.log
+timeout 900 python bench.py > gpurun_out/bench_c2_final.json 2> gpurun_out/bench_c2_final.err
 python -c "
-import json; d=json.load(open('gpurun_out/bench_c2_jd.json')); print(d['value'], d['ms_per_step'], d['e2e']['value'], d['self_check'], d['gpu_launches']); print(d['roofline']['tiers'])"
-HX_JOINT_DEDUP=0 timeout 900 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_c2_jd0.json 2> gpurun_out/bench_c2_jd0.err
-python -c "
-import json; d=json.load(open('gpurun_out/bench_c2_jd0.json')); print(d['value'], d['ms_per_step'])"
-timeout 900 python bench.py --config c1 --no-cpu-baseline > gpurun_out/bench_c1_jd.json 2> gpurun_out/bench_c1_jd.err
-python -c "
-import json; d=json.load(open('gpurun_out/bench_c1_jd.json')); print('c1', d['value'], d['ms_per_step'], d['e2e']['value'])"
+import json; d=json.load(open('gpurun_out/bench_c2_final.json')); print(d['value'], d['ms_per_step'], d['e2e']['value'], d['roofline']['frac'], d['cpu_baseline']['value'], d['self_check'], d['gpu_launches'], d['clocks'])"
