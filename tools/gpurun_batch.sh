@@ -1,10 +1,7 @@
 #!/bin/bash
-# Round-end check on the GPU box: smoke, the GPU test suite, the default bench line.
 cd $GRAFT_REPO_ROOT
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke exit $?" >> gpurun_out/smoke.log
-tail -2 gpurun_out/smoke.log
-timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/gputest_all.log 2>&1; echo "pytest exit $?" >> gpurun_out/gputest_all.log
-tail -4 gpurun_out/gputest_all.log
-timeout 900 python bench.py > gpurun_out/bench_c2_final.json 2> gpurun_out/bench_c2_final.err
-python -c "
-import json; d=json.load(open('gpurun_out/bench_c2_final.json')); print(d['value'], d['ms_per_step'], d['e2e']['value'], d['roofline']['frac'], d['cpu_baseline']['value'], d['self_check'], d['gpu_launches'], d['clocks'])"
+timeout 1200 python -m pytest tests/test_variants_gpu.py -q -x -k "gram" 2>&1 | tail -3
+for i in 1 2; do timeout 600 python bench.py --no-cpu-baseline --no-e2e --steps 12 > gpurun_out/kn.json 2>/dev/null; python -c "
+import json; d=json.load(open('gpurun_out/kn.json')); print(round(d['value']), round(d['ms_per_step'],2))"; done
+timeout 600 python bench.py --config c4 --no-cpu-baseline --no-e2e > gpurun_out/kn.json 2>/dev/null; python -c "
+import json; d=json.load(open('gpurun_out/kn.json')); print('c4', d['value'], round(d['ms_per_step'],2))"
