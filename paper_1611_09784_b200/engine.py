@@ -280,6 +280,14 @@ class Engine:
             self._supercells[n] = _KGRID_CACHE[key]
         return self._supercells[n]
 
+    def quarters(self, sc):
+        """partition_quarters(sc), cached process-wide like the supercells (the nu = 32 partition costs ~1 ms of
+        host time, on the critical path of run_mlmc's first submission)."""
+        key = ("part", sc.spec, sc.n)
+        if key not in _KGRID_CACHE:
+            _KGRID_CACHE[key] = partition_quarters(sc)
+        return _KGRID_CACHE[key]
+
     def cell(self, n: int, device: int | None = None):
         device = self.device if device is None else device
         if (n, device) not in self._cells:
@@ -636,7 +644,7 @@ class Engine:
             words, sub = self._draw_device(sc, p_vac, stream, m0, nsamples, with_cv)
         else:
             words = sample_masks(sc.nunits, p_vac, self.master_seed, stream, m0, nsamples)
-            sub = restrict_words(words, partition_quarters(sc)) if with_cv else None  # [M, 4, w]
+            sub = restrict_words(words, self.quarters(sc)) if with_cv else None  # [M, 4, w]
         groups = [(n, q, words)]
         if with_cv:
             nsub = n // 2
@@ -668,7 +676,7 @@ class Engine:
                                                   st.cuda_stream), "hx_sample_masks_device")
             q = None
             if with_cv:
-                part = partition_quarters(sc)
+                part = self.quarters(sc)
                 assign, umap = _quarter_maps(part, self.device)
                 sub_units = part.subcells[0].nunits
                 ws = max(1, (sub_units + 63) // 64)
