@@ -479,6 +479,12 @@ class Engine:
         if _E2E_ORDER == "big-then-small" and len(order) > 2:
             # the largest tier first (critical path), then the rest smallest first
             order = order[:1] + order[1:][::-1]
+        elif _E2E_ORDER == "big2-then-small" and len(order) > 3:
+            # experiment: the two largest tiers first, then the rest smallest first.  The GPU phase of c2 ends 1.2 ms
+            # earlier, but the level-moment kernels of the small levels then queue behind the resident chase CTAs of
+            # the large tiers (they hold every register of their SMs for ~4 ms each): level 1's finish waits 24 ms
+            # and the host work of the small levels piles up after the GPU is done - e2e 109k vs 138k samples/s
+            order = order[:2] + order[2:][::-1]
         hits = [0] * len(batches)
         spent = [0.0] * len(batches)
         plans = {}  # (bi, gi) -> (tier, uniq, inv, keys, src)
