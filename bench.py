@@ -678,7 +678,7 @@ def main():
             "config": {"workload": desc, "bz_mode": "reduced (== full to <1e-10, SURVEY finding 3)",
                        "energy_points": NPTS, "delta": DELTA, "master_seed": SEED, "levels": level_info,
                        "l2": "flushed between timed steps (256 MB write)", "parallelism": (f"replicas x{world} (rank r draws replicates [r*M, (r+1)*M) of each level stream; exact fixed-point level sums, int64 all-reduce)" if mode == "replicas" else f"split x{world} (one level set; unique masks of each tier split over the ranks by sum d^3, curves all-gathered)"),
-                       "schedule": "all levels and both tiers of each level (parent nu, quarters nu/2) in flight at once on independent streams + contexts; largest tier on a high-priority stream",
+                       "schedule": "all levels and both tiers of each level (parent nu, quarters nu/2) in flight at once on independent streams + contexts; largest tier on a high-priority stream; unique masks per tier (torch.unique on the device), tiers of the same one-word cell deduplicated together (the reference run cache's cross-level hits, runner.py:213-233)",
                        "levels_note": "per-level ms from a separate sequential analysis pass (the timed step runs them concurrently)"},
             "roofline": roofline_block(args.config, world, mode, ms_per_step, peak, dom, tiers, apasses),
             "gpu_launches": launches,
