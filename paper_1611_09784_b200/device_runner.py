@@ -33,6 +33,18 @@ from .solver import make_bz_grid, time_reversal_reduce, use_time_reversal
 _MERGE_TIERS = __import__("os").environ.get("HX_MERGE_TIERS", "0") == "1"
 _LANES = int(__import__("os").environ.get("HX_LANES", "3"))
 _JOINT_DEDUP = __import__("os").environ.get("HX_JOINT_DEDUP", "1") != "0"
+# HX_SUBMIT_THREADS=1: every lane's tier solves are enqueued from the lane's own submission thread
+_SUBMIT_THREADS = __import__("os").environ.get("HX_SUBMIT_THREADS", "1") != "0"
+
+
+class _Done:
+    """Future-like wrapper of an already available result."""
+
+    def __init__(self, value):
+        self._value = value
+
+    def result(self):
+        return self._value
 _LANE_MAP = [int(x) for x in __import__("os").environ.get("HX_LANE_MAP", "").split(",") if x]
 
 
@@ -83,6 +95,15 @@ class DeviceMlmc:
             prio = -1 if not self._lanes else 0
             self._lanes.append((_lib.Device.new_ctx(self.device), torch.cuda.Stream(self.dev, priority=prio)))
         return self._lanes[i]
+
+    def _submitter(self, lane):
+        from concurrent.futures import ThreadPoolExecutor
+
+        if not hasattr(self, "_submitters"):
+            self._submitters = {}
+        if lane not in self._submitters:
+            self._submitters[lane] = ThreadPoolExecutor(max_workers=1, thread_name_prefix=f"hx-lane{lane}")
+        return self._submitters[lane]
 
     def cell(self, n):
         if n not in self._cells:
@@ -142,12 +163,27 @@ class DeviceMlmc:
         """Curves [U, npts] of the unique masks `uniq`, enqueued on `stream` with context `ctx`.  The
         outputs (curves, status) are allocated on the caller's current stream, which must wait on `stream`
         before using or releasing them."""
+        curves, status = self._solve_alloc(n, uniq)
+        self._solve_launch(n, uniq, curves, status, ctx, stream)
+        return curves, status
+
+    def _solve_alloc(self, n, uniq: torch.Tensor):
+        """Output buffers of one tier solve, allocated on the caller's current stream."""
+        kp, _ = self.kpoints(n, self.q_of(n))
+        U = uniq.shape[0]
+        return (torch.empty((U, self.npts), dtype=torch.float64, device=self.dev),
+                torch.empty((U, kp.shape[0]), dtype=torch.int32, device=self.dev))
+
+    def _solve_launch(self, n, uniq, curves, status, ctx, stream, after=None):
+        """Enqueue the solve on `stream` (after the event `after`); may run on a lane's submission thread: the C
+        call releases the GIL, so the caller goes on deduplicating the next tier while this one is enqueued."""
+        torch.cuda.set_device(self.dev)  # a submission thread starts on device 0
+        if after is not None:
+            stream.wait_event(after)
         cell = self.cell(n)
         q = self.q_of(n)
         kp, kmult = self.kpoints(n, q)
         U = uniq.shape[0]
-        curves = torch.empty((U, self.npts), dtype=torch.float64, device=self.dev)
-        status = torch.empty((U, kp.shape[0]), dtype=torch.int32, device=self.dev)
         g = _lib.EGrid()
         g.e0, g.step, g.npts, g.delta = self.lo, self.step, self.npts, self.delta
         ev = None
@@ -169,7 +205,9 @@ class DeviceMlmc:
             ev[1].record(stream)
             self.records.append({"n": n, "N": cell.dim, "unique": U, "nk": kp.shape[0], "events": ev,
                                  "uniq": uniq, "cell": cell})
-        return curves, status
+        done = torch.cuda.Event()
+        done.record(stream)
+        return done
 
     def _world(self):
         if self.group is None:
@@ -281,13 +319,16 @@ class DeviceMlmc:
                 elif _LANES > 1 and lane > 0:
                     lane = 1 + (lane - 1) % (_LANES - 1)
                 ctx, stream = self._lane(lane) if concurrent else (self.ctx, main)
-                stream.wait_event(ready)
-                curves, status = self._solve(n, uniq, ctx, stream)
-                done = torch.cuda.Event()
-                done.record(stream)
+                curves, status = self._solve_alloc(n, uniq)
+                if concurrent and _SUBMIT_THREADS:
+                    # one submission thread per lane (tiers of a lane stay in order; one host thread per context)
+                    fut = self._submitter(lane).submit(self._solve_launch, n, uniq, curves, status, ctx, stream, ready)
+                else:
+                    fut = _Done(self._solve_launch(n, uniq, curves, status, ctx, stream, ready))
                 for j2 in js:
-                    outs[j2] = (curves, done)
+                    outs[j2] = (curves, fut)
                 self.statuses.append(status)
+            outs = [None if o is None else (o[0], o[1].result()) for o in outs]  # enqueued: the `done` events
         else:
             # HX_MERGE_TIERS=1: the jobs of one tier (the same n) from different levels go to ONE batch call
             # (curves are batch independent, so only the packing of the GPU changes)
