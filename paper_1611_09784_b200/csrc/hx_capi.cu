@@ -27,6 +27,19 @@ namespace hx {
 static std::atomic<unsigned long long> g_launches{0};
 void count_launch(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+void raise_smem_attr(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> limit;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = limit[{dev, kernel}];
+  if (bytes > cur) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cur = bytes;
+  }
+}
+
 namespace {
 std::mutex g_opt_mu;
 std::map<std::string, long> g_opts;

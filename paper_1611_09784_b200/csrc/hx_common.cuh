@@ -99,9 +99,14 @@ __device__ __forceinline__ double warp_min(double v) {
 // Dynamic shared memory limit of a kernel.  (Forcing the maximum shared-memory carveout as well was
 // measured slower: the bulge chase and the rank update lose more to the smaller L1 than they gain from
 // extra resident CTAs.)
+// The limit is only ever RAISED, under a lock, per (device, kernel) (raise_smem_attr, hx_capi.cu): contexts on
+// several host threads launch the same kernels with different dynamic sizes (e.g. the zone kernels stage tridiagonals
+// of different S); setting the exact size per launch let one thread lower the limit between another thread's
+// set and launch ("invalid argument" on that launch).
+void raise_smem_attr(const void* kernel, size_t bytes);
 template <typename K>
 inline void set_smem_attr(K* kernel, size_t bytes) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  raise_smem_attr(reinterpret_cast<const void*>(kernel), bytes);
 }
 
 }  // namespace hx
